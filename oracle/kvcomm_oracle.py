@@ -1,0 +1,377 @@
+"""KVComm CPU oracle — plain, slow, float64 NumPy, written from PAPER.md.
+
+*** TEST INFRASTRUCTURE ONLY. ***  Only `tests/`, `__graft_entry__.smoke()` and
+`bench.py` (its `cpu_baseline` leg and `--impl reference`) may import this module.
+The product path (`paper_2510_12872_b200/`) never imports, links or executes it,
+and this module imports nothing from the product path: the two share no code.
+
+Every intermediate is float64.  bf16 inputs are widened exactly (callers pass
+float64 arrays holding bf16 values); results that the product stores in bf16 are
+rounded once, round-to-nearest-even, by `bf16_round` (reading A14).
+
+Citations: "P:n" = /root/reference/PAPER.md line n (with the section / equation),
+"S:n" = SPEC.md line n.  DESIGN.md lists every reading (A1..A21) taken where the
+paper is silent, ambiguous or garbled.
+
+Notation (§3.3-3.4):
+  φ        the new placeholder sample (query), length L_φ
+  ψ ∈ 𝒜    anchors of the placeholder's pool; 𝒜_φ ⊆ 𝒜 the candidates (Eq. 5)
+  h        token embeddings [L, D_e]                      (reading A1)
+  w        softmax(-‖h_φ - h_ψ‖) over anchors              (Eq. 5/6)
+  Δk/Δv    stored offsets in the base frame                (reading A10)
+  δ        target_start - base_start (RoPE position delta)
+
+Parity status per function: every function below is
+pinned by tests/test_oracle_pins.py except where "parity unpinned" is written.
+The scalar-distance reading A4 (`scalar_weights`) and the Eq. 7 weight reading A3
+are pinned only by closed forms of the chosen reading: no printed value in the
+paper separates the readings — "parity unpinned" with respect to the paper's
+intended (unstated) definition.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+# ---------------------------------------------------------------------------
+# bf16 rounding (reading A14: one RNE rounding at the output)
+# ---------------------------------------------------------------------------
+
+BF16_MANT_BITS = 7          # stored mantissa bits of bfloat16
+BF16_MIN_EXP = -126         # smallest normal exponent (same range as fp32)
+BF16_MAX = (2.0 - 2.0 ** -7) * 2.0 ** 127
+
+
+def bf16_round(x) -> np.ndarray:
+    """Round float64 values to the nearest bfloat16 value, ties to even.
+
+    Definition: with |x| in [2^e, 2^(e+1)), the bf16 spacing is 2^(e-7) (or 2^(-133)
+    in the subnormal range); x is rounded to the nearest multiple of the spacing,
+    ties to even (np.rint), scaling by powers of two being exact in float64.
+    Values beyond the largest finite bf16 after rounding become ±inf.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    nz = (x != 0) & np.isfinite(x)
+    m, e = np.frexp(x[nz])                       # x = m * 2^e, 0.5 <= |m| < 1
+    # |x| in [2^(e-1), 2^e): spacing = 2^(e-1-7); subnormal floor 2^(-126-7)
+    spacing_exp = np.maximum(e - 1 - BF16_MANT_BITS, BF16_MIN_EXP - BF16_MANT_BITS)
+    q = np.rint(np.ldexp(x[nz], -spacing_exp))
+    r = np.ldexp(q, spacing_exp)
+    r = np.where(np.abs(r) > BF16_MAX, np.sign(r) * np.inf, r)
+    out[nz] = r
+    out[~np.isfinite(x)] = x[~np.isfinite(x)]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# RoPE (§3.1 P:116-121 "k_n = R_n W_K h_n"; alignment P:145-148)
+# ---------------------------------------------------------------------------
+
+
+def rope_rotate(x: np.ndarray, delta: int, inv_freq: np.ndarray) -> np.ndarray:
+    """Apply R_δ to key vectors x[..., d] (HF `rotate_half` pairing, reading A12).
+
+    For f < d/2 with angle a_f = δ · inv_freq[f] (float64, reading A13):
+        y[f]       = x[f]       cos a_f - x[f + d/2] sin a_f
+        y[f + d/2] = x[f + d/2] cos a_f + x[f]       sin a_f
+    R_0 = I exactly; R_a R_b = R_{a+b}; R_δ is orthogonal ("orthogonal rotation").
+    """
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    assert d % 2 == 0 and inv_freq.shape == (d // 2,)
+    if delta == 0:
+        return x.copy()
+    a = float(delta) * np.asarray(inv_freq, dtype=np.float64)
+    c, s = np.cos(a), np.sin(a)
+    x1, x2 = x[..., : d // 2], x[..., d // 2:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+# ---------------------------------------------------------------------------
+# Offset measurement — insert path (Algorithm 1)
+# ---------------------------------------------------------------------------
+
+
+def measure_offset(k_real, v_real, s_real: int, k_base, v_base, s_base: int,
+                   inv_freq: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Δk = R_{-(s_real - s_base)} k_real - k_base ;  Δv = v_real - v_base.
+
+    Keys are de-rotated into the base frame before differencing ("always
+    de-rotates the stored key by R_{-Δ}", reading A10).  Returns float64; the
+    stored pool value is bf16_round of it.
+    """
+    dk = rope_rotate(k_real, -(s_real - s_base), inv_freq) - np.asarray(k_base, np.float64)
+    dv = np.asarray(v_real, np.float64) - np.asarray(v_base, np.float64)
+    return dk, dv
+
+
+# ---------------------------------------------------------------------------
+# Anchor prediction (Eq. 5)
+# ---------------------------------------------------------------------------
+
+
+def candidate_slots(anchor_len: Dict[int, int], offsets_present: Dict[int, bool],
+                    L_phi: int) -> List[int]:
+    """𝒜_φ: anchors at least as long as φ (reading A6: L_ψ >= L_φ) that hold the
+    consumer's offsets (reading A9), in ascending slot order."""
+    return sorted(s for s, L in anchor_len.items() if L >= L_phi and offsets_present.get(s, False))
+
+
+def distances(h_phi: np.ndarray, h_anchor: Sequence[np.ndarray]) -> np.ndarray:
+    """d[i, j] = ‖h_φ[i] - h_ψj[i]‖₂ for i < L_φ (Eq. 5/6 "‖h_φ - h_ψ‖").
+
+    Anchors longer than φ are truncated to their first L_φ rows (reading A8).
+    Returns float64 [L_φ, |𝒜_φ|].
+    """
+    h_phi = np.asarray(h_phi, dtype=np.float64)
+    L_phi = h_phi.shape[0]
+    cols = []
+    for h in h_anchor:
+        diff = h_phi - np.asarray(h, dtype=np.float64)[:L_phi]
+        cols.append(np.sqrt(np.sum(diff * diff, axis=1)))
+    if not cols:
+        return np.zeros((L_phi, 0))
+    return np.stack(cols, axis=1)
+
+
+def softmax_neg(dist: np.ndarray, axis: int = -1) -> np.ndarray:
+    """softmax(-dist) along `axis`, temperature 1, max-subtracted (reading A15)."""
+    z = -np.asarray(dist, dtype=np.float64)
+    z = z - np.max(z, axis=axis, keepdims=True)
+    e = np.exp(z)
+    return e / np.sum(e, axis=axis, keepdims=True)
+
+
+def position_weights(dist: np.ndarray, top_k: int = 0,
+                     slots: Optional[Sequence[int]] = None) -> Tuple[np.ndarray, Optional[np.ndarray]]:
+    """Per-position weights W[i, j] = softmax_j(-d[i, j]) (Eq. 6 "softmax mapping of
+    -‖h_φ - h_ψ‖ across the anchor dimension"; per position: reading A2).
+
+    top_k > 0 (reading A16, not in the paper): keep the k anchors with the smallest
+    distance per position (ties broken by the smaller slot id), softmax over those,
+    zero elsewhere.  Returns (W [L_φ, n], idx [L_φ, k] of slot ids or None).
+    """
+    n = dist.shape[1]
+    if top_k <= 0 or top_k >= n:
+        W = softmax_neg(dist, axis=1) if n else np.zeros_like(dist)
+        return W, None
+    slots = list(range(n)) if slots is None else list(slots)
+    W = np.zeros_like(dist, dtype=np.float64)
+    idx = np.zeros((dist.shape[0], top_k), dtype=np.int64)
+    for i in range(dist.shape[0]):
+        order = sorted(range(n), key=lambda j: (dist[i, j], slots[j]))[:top_k]
+        W[i, order] = softmax_neg(dist[i, order])
+        idx[i] = [slots[j] for j in order]
+    return W, idx
+
+
+def scalar_weights(dist: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Scalar (per-anchor) distance and weight: d̄_j = mean_i d[i, j] (reading A4),
+    w̄ = softmax(-d̄) (Eq. 5 "w_{φ→ψ} = softmax(-‖h_φ - h_ψ‖)")."""
+    dbar = np.mean(np.asarray(dist, np.float64), axis=0)
+    return dbar, softmax_neg(dbar)
+
+
+def entropy(w: np.ndarray) -> float:
+    """H = -Σ w log w with 0 log 0 = 0 (Eq. 5, sign per reading A5)."""
+    w = np.asarray(w, dtype=np.float64)
+    nz = w > 0
+    return float(-np.sum(w[nz] * np.log(w[nz])))
+
+
+SHAREABLE, NEW_ANCHOR = 0, 1
+R_OK, R_EMPTY_POOL, R_TOO_LONG, R_NO_CANDIDATES, R_HIGH_ENTROPY = 0, 1, 2, 3, 4
+
+
+@dataclass
+class MatchResult:
+    verdict: int
+    reason: int
+    candidates: List[int]
+    W: Optional[np.ndarray] = None         # [L_φ, |𝒜_φ|]
+    idx: Optional[np.ndarray] = None
+    dist: Optional[np.ndarray] = None
+    dbar: Optional[np.ndarray] = None
+    wbar: Optional[np.ndarray] = None
+    H: float = 0.0
+    threshold: float = 0.0
+
+
+def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int, np.ndarray],
+            offsets_present: Dict[int, bool], gamma: float, top_k: int = 0) -> MatchResult:
+    """Eq. 5:  NewAnchor ⇔ (L_φ > max_{ψ∈𝒜} L_ψ) ∪ (H_{φ|𝒜} > γ log|𝒜_φ|).
+
+    Readings: the max runs over the whole pool (A7); an empty pool or an empty 𝒜_φ
+    is NewAnchor (A19); |𝒜_φ| = 1 gives H = 0 = threshold → Shareable.
+    Weights for Eq. 6/7 are returned alongside (Alg. 1).
+    """
+    if not (0.0 <= gamma <= 1.0):
+        raise ValueError("gamma must lie in [0, 1] (S:237)")
+    L_phi = int(np.asarray(h_phi).shape[0])
+    if not anchor_len:
+        return MatchResult(NEW_ANCHOR, R_EMPTY_POOL, [])
+    if L_phi > max(anchor_len.values()):
+        return MatchResult(NEW_ANCHOR, R_TOO_LONG, [])
+    cand = candidate_slots(anchor_len, offsets_present, L_phi)
+    if not cand:
+        return MatchResult(NEW_ANCHOR, R_NO_CANDIDATES, [])
+    dist = distances(h_phi, [anchor_emb[s] for s in cand])
+    W, idx = position_weights(dist, top_k, cand)
+    dbar, wbar = scalar_weights(dist)
+    H = entropy(wbar)
+    thr = gamma * math.log(len(cand))
+    verdict = NEW_ANCHOR if H > thr else SHAREABLE
+    return MatchResult(verdict, R_HIGH_ENTROPY if verdict == NEW_ANCHOR else R_OK, cand,
+                       W, idx, dist, dbar, wbar, H, thr)
+
+
+# ---------------------------------------------------------------------------
+# Offset approximation (Eq. 6, Eq. 7) and alignment
+# ---------------------------------------------------------------------------
+
+
+def blend_placeholder(W: np.ndarray, offsets: Sequence[np.ndarray]) -> np.ndarray:
+    """Eq. 6 offset term: Δ̂[..., i, :] = Σ_j W[i, j] · Δ_j[..., i, :].
+
+    offsets[j]: [L, H, ≥L_φ, d] (the anchor's stored placeholder offset, truncated
+    to the first L_φ tokens, reading A8).  W: [L_φ, n].
+    """
+    L_phi = W.shape[0]
+    acc = None
+    for j, off in enumerate(offsets):
+        term = W[:, j][:, None] * np.asarray(off, np.float64)[..., :L_phi, :]
+        acc = term if acc is None else acc + term
+    return acc
+
+
+def blend_prefix(wbar: np.ndarray, offsets: Sequence[np.ndarray]) -> np.ndarray:
+    """Eq. 7 offset term with one weight per anchor (reading A3):
+    Δ̂^p = Σ_j w̄_j · Δ^p_j."""
+    acc = None
+    for j, off in enumerate(offsets):
+        term = float(wbar[j]) * np.asarray(off, np.float64)
+        acc = term if acc is None else acc + term
+    return acc
+
+
+def apply_offset(k_base, v_base, dk_hat, dv_hat, delta: int,
+                 inv_freq: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """K̂ = R_δ(K_base + Δ̂K),  V̂ = V_base + Δ̂V   (reading A10).
+
+    Offsets live in the base frame, so the sum is re-rotated by δ = target_start -
+    base_start (workflow step 3, "aligning Key positions via RoPE
+    de-rotation/re-rotation, adding the estimated Key/Value offsets").
+    Returns float64 (caller rounds with bf16_round).
+    """
+    k = rope_rotate(np.asarray(k_base, np.float64) + dk_hat, delta, inv_freq)
+    v = np.asarray(v_base, np.float64) + dv_hat
+    return k, v
+
+
+def realign_segment(weights: np.ndarray, k_base, v_base, dk: Sequence[np.ndarray],
+                    dv: Sequence[np.ndarray], base_start: int, target_start: int,
+                    inv_freq: np.ndarray, kind: str = "placeholder"):
+    """One segment of Algorithm 1's reuse branch.
+
+    kind = "placeholder": weights is W [L_seg, n] and Eq. 6 applies;
+    kind = "prefix":      weights is w̄ [n] and Eq. 7 applies.
+    Returns dict with float64 blended offsets and bf16-rounded outputs.
+    """
+    if kind == "placeholder":
+        dk_hat = blend_placeholder(weights, dk)
+        dv_hat = blend_placeholder(weights, dv)
+    elif kind == "prefix":
+        dk_hat = blend_prefix(weights, dk)
+        dv_hat = blend_prefix(weights, dv)
+    else:
+        raise ValueError(kind)
+    k, v = apply_offset(k_base, v_base, dk_hat, dv_hat, target_start - base_start, inv_freq)
+    return {"dk_hat": dk_hat, "dv_hat": dv_hat, "k": bf16_round(k), "v": bf16_round(v),
+            "k64": k, "v64": v}
+
+
+# ---------------------------------------------------------------------------
+# Concatenation and ledger ("updated caches are concatenated")
+# ---------------------------------------------------------------------------
+
+
+class LedgerError(ValueError):
+    def __init__(self, kind: str, where: int):
+        super().__init__(f"{kind} at position {where}")
+        self.kind = kind
+        self.where = where
+
+
+def check_ledger(spans: Sequence[Tuple[int, int]], N: int) -> None:
+    """Segments (start, length) must tile [0, N) exactly, in order.
+    Raises LedgerError('gap'|'overlap'|'short'|'long', position)."""
+    pos = 0
+    for start, length in spans:
+        if start > pos:
+            raise LedgerError("gap", pos)
+        if start < pos:
+            raise LedgerError("overlap", start)
+        pos = start + length
+    if pos < N:
+        raise LedgerError("gap", pos)
+    if pos > N:
+        raise LedgerError("long", N)
+
+
+def concat(parts: Sequence[Tuple[int, np.ndarray]], N: int, axis: int = -2) -> np.ndarray:
+    """Concatenate (start, tensor) parts along the token axis after the ledger check."""
+    check_ledger([(s, p.shape[axis]) for s, p in parts], N)
+    return np.concatenate([p for _, p in parts], axis=axis)
+
+
+# ---------------------------------------------------------------------------
+# Anchor pool metadata: insertion and pruning (§3.3 "Anchor Update", P:273-274;
+# Alg. 1)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class PoolModel:
+    """Host metadata of one anchor pool of capacity 𝒱.
+
+    Pruning reading A17: when an insert finds the pool full, the existing anchor
+    with the smallest access count is discarded, ties going to the earliest
+    inserted ("least frequently accessed anchor among the earliest-added
+    entries").  The incoming anchor is never its own victim.
+    Slots are reused lowest-free-first.
+    """
+    capacity: int
+    slot_len: Dict[int, int] = field(default_factory=dict)
+    access: Dict[int, int] = field(default_factory=dict)
+    inserted: Dict[int, int] = field(default_factory=dict)
+    next_index: int = 0
+
+    def victim(self) -> int:
+        return min(self.slot_len, key=lambda s: (self.access[s], self.inserted[s]))
+
+    def insert(self, L_psi: int) -> Tuple[int, int]:
+        evicted = -1
+        if len(self.slot_len) >= self.capacity:
+            evicted = self.victim()
+            self.evict(evicted)
+        slot = min(set(range(self.capacity)) - set(self.slot_len))
+        self.slot_len[slot] = L_psi
+        self.access[slot] = 0
+        self.inserted[slot] = self.next_index
+        self.next_index += 1
+        return slot, evicted
+
+    def evict(self, slot: int) -> None:
+        if slot not in self.slot_len:
+            raise KeyError(slot)
+        del self.slot_len[slot], self.access[slot], self.inserted[slot]
+
+    def record_access(self, slots: Sequence[int]) -> None:
+        for s in slots:
+            if s not in self.slot_len:
+                raise KeyError(s)
+            self.access[s] += 1
