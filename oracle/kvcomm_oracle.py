@@ -23,10 +23,11 @@ Notation (§3.3-3.4):
 
 Parity status per function: every function below is
 pinned by tests/test_oracle_pins.py except where "parity unpinned" is written.
-The scalar-distance reading A4 (`scalar_weights`) and the Eq. 7 weight reading A3
-are pinned only by closed forms of the chosen reading: no printed value in the
-paper separates the readings — "parity unpinned" with respect to the paper's
-intended (unstated) definition.
+The sample-level distance of reading A4 (`scalar_weights`: Frobenius by default,
+SPEC's mean-of-ℓ2 as a switch) and the Eq. 7 weight reading A3 are pinned only by
+closed forms / library routines of the chosen reading: no printed value in the
+paper separates the readings, so with respect to the paper's intended (unstated)
+definition they are "parity unpinned".
 """
 from __future__ import annotations
 
@@ -169,10 +170,23 @@ def position_weights(dist: np.ndarray, top_k: int = 0,
     return W, idx
 
 
-def scalar_weights(dist: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
-    """Scalar (per-anchor) distance and weight: d̄_j = mean_i d[i, j] (reading A4),
-    w̄ = softmax(-d̄) (Eq. 5 "w_{φ→ψ} = softmax(-‖h_φ - h_ψ‖)", P:271)."""
-    dbar = np.mean(np.asarray(dist, np.float64), axis=0)
+FROBENIUS, MEAN_L2 = "frobenius", "mean_l2"
+
+
+def scalar_weights(dist: np.ndarray, mode: str = FROBENIUS) -> Tuple[np.ndarray, np.ndarray]:
+    """Sample-level distance and weight of Eq. 5 / Eq. 7:
+    w̄ = softmax(-d̄) with d̄_j = ‖h_φ - h_ψj‖ over the whole sample (reading A4):
+
+      FROBENIUS (default): d̄_j = ‖h_φ - h_ψj[:L_φ]‖_F = sqrt(Σ_i d[i, j]²)
+      MEAN_L2: d̄_j = mean_i d[i, j]
+    """
+    dist = np.asarray(dist, np.float64)
+    if mode == FROBENIUS:
+        dbar = np.sqrt(np.sum(dist * dist, axis=0))
+    elif mode == MEAN_L2:
+        dbar = np.mean(dist, axis=0)
+    else:
+        raise ValueError(mode)
     return dbar, softmax_neg(dbar)
 
 
@@ -202,7 +216,8 @@ class MatchResult:
 
 
 def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int, np.ndarray],
-            offsets_present: Dict[int, bool], gamma: float, top_k: int = 0) -> MatchResult:
+            offsets_present: Dict[int, bool], gamma: float, top_k: int = 0,
+            scalar: str = FROBENIUS) -> MatchResult:
     """Eq. 5:  NewAnchor ⇔ (L_φ > max_{ψ∈𝒜} L_ψ) ∪ (H_{φ|𝒜} > γ log|𝒜_φ|).
 
     Readings: the max runs over the whole pool (A7); an empty pool or an empty 𝒜_φ
@@ -221,7 +236,7 @@ def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int,
         return MatchResult(NEW_ANCHOR, R_NO_CANDIDATES, [])
     dist = distances(h_phi, [anchor_emb[s] for s in cand])
     W, idx = position_weights(dist, top_k, cand)
-    dbar, wbar = scalar_weights(dist)
+    dbar, wbar = scalar_weights(dist, scalar)
     H = entropy(wbar)
     thr = gamma * math.log(len(cand))
     verdict = NEW_ANCHOR if H > thr else SHAREABLE

@@ -195,9 +195,23 @@ def test_topk_selection_and_tiebreak():
     assert idx1[:, 0].tolist() == [5, 9] and W1[0, 2] == 1.0 and W1[1, 3] == 1.0
 
 
+def test_scalar_distance_is_frobenius_norm_of_sample_difference():
+    # Eq. 5: ‖h_φ - h_ψ‖ of whole samples; default reading A4 = Frobenius
+    # norm of the [L_φ, D_e] difference (library matrix norm), anchors truncated (A8)
+    h = bf16_values((30, 16))
+    anchors = [bf16_values((30 + e, 16)) for e in (0, 5, 9)]
+    dbar, wbar = O.scalar_weights(O.distances(h, anchors))
+    ref = np.array([np.linalg.norm(h - a[:30], "fro") for a in anchors])
+    np.testing.assert_allclose(dbar, ref, rtol=1e-14)
+    np.testing.assert_allclose(wbar, scipy.special.softmax(-ref), rtol=1e-13)
+    r = O.predict(h, {j: a.shape[0] for j, a in enumerate(anchors)}, dict(enumerate(anchors)),
+                  {0: True, 1: True, 2: True}, 0.5)
+    np.testing.assert_allclose(r.dbar, ref, rtol=1e-14)
+
+
 def test_scalar_weights_and_entropy_library():
     dist = np.abs(rng.standard_normal((40, 6)))
-    dbar, wbar = O.scalar_weights(dist)
+    dbar, wbar = O.scalar_weights(dist, O.MEAN_L2)
     np.testing.assert_allclose(dbar, dist.mean(axis=0), rtol=1e-15)
     np.testing.assert_allclose(wbar, scipy.special.softmax(-dist.mean(axis=0)), rtol=1e-14)
     assert O.entropy(wbar) == pytest.approx(scipy.stats.entropy(wbar), rel=1e-13)
