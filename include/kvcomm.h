@@ -1,0 +1,271 @@
+/*
+ * kvcomm.h — C ABI of the B200-native KVComm anchor-realignment hot path.
+ *
+ * KVComm (arXiv 2510.12872) reuses the KV-cache of a text segment that an agent
+ * shares with other agents: the segment's *base* cache (computed standalone) is
+ * moved under a new prefix by adding an *offset* interpolated from anchors.
+ * "P:n" below is a line of the paper text, with the
+ * equation or section it falls in.  The library implements:
+ *
+ *   a0  anchor-pool store + insert (Alg. 1 fallback branch P:786-796; §3.3)
+ *   a1  candidate filter / length clause of Eq. 5
+ *   a2  embedding distances ‖h_φ - h_ψ‖₂                   (Eq. 5/6)
+ *   a3  softmax weights, entropy, NewAnchor verdict         (Eq. 5, Eq. 6)
+ *   a4  offset blend                                        (Eq. 6, Eq. 7)
+ *   a5  RoPE position delta + add into the base cache
+ *   a6  concatenation of the updated segments + ledger      (Alg. 1)
+ *
+ * Conventions for every call
+ *   - Pointers named "device" must be CUDA device pointers on the pool's device,
+ *     16-byte aligned.  "host" pointers are ordinary host memory, only read during
+ *     the call.  The caller owns every buffer it passes; the pool owns its slabs.
+ *   - Tensors of one model shard use the layout [Ls][Hs][ld][d] bf16 (token rows
+ *     of d elements, d fastest; `ld` = row stride between consecutive (layer,
+ *     head) blocks, >= the number of rows used).  Ls/Hs are the pool's shard sizes.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *     stream-ordered and asynchronous except kvcomm_match_anchors, which
+ *     synchronises `stream` to fill its host `info` (Algorithm 1's reuse/fallback
+ *     branch is a host decision).
+ *   - Errors never throw across the ABI: each call returns a kvcomm_status and sets
+ *     a thread-local message (kvcomm_last_error_message).  Contract violations are
+ *     errors, never silent fallbacks.
+ *   - Thread safety: a pool admits many concurrent readers (match, realign) or one
+ *     writer (insert, set_offsets, evict, record_access, destroy).
+ */
+#ifndef KVCOMM_H
+#define KVCOMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVCOMM_API __attribute__((visibility("default")))
+
+#define KVCOMM_VERSION 1
+#define KVCOMM_MAX_CAPACITY 1024  /* anchors per pool (𝒱) */
+#define KVCOMM_MAX_CONSUMERS 64   /* (agent, slot) consumers per pool */
+#define KVCOMM_MAX_TOPK 32
+#define KVCOMM_ALL_CONSUMERS (-1)
+
+typedef enum {
+  KVCOMM_OK = 0,
+  KVCOMM_ERR_INVALID_ARGUMENT = 1, /* null pointer, odd d, gamma outside [0,1], misaligned */
+  KVCOMM_ERR_SHAPE_MISMATCH = 2,   /* length / layer / head mismatch          */
+  KVCOMM_ERR_NO_CANDIDATES = 3,    /* realign with an empty candidate set                    */
+  KVCOMM_ERR_MISSING_OFFSET = 4,   /* reuse needs an offset the anchor lacks          */
+  KVCOMM_ERR_POSITION_GAP = 5,     /* concat ledger: segments leave a hole                   */
+  KVCOMM_ERR_POSITION_OVERLAP = 6, /* concat ledger: segments overlap                        */
+  KVCOMM_ERR_NOT_FOUND = 7,        /* empty slot / unknown consumer                                  */
+  KVCOMM_ERR_OUT_OF_MEMORY = 8,
+  KVCOMM_ERR_CUDA = 9,
+  KVCOMM_ERR_NCCL = 10
+} kvcomm_status;
+
+typedef enum { KVCOMM_SHAREABLE = 0, KVCOMM_NEW_ANCHOR = 1 } kvcomm_verdict;
+
+typedef enum {
+  KVCOMM_REASON_OK = 0,
+  KVCOMM_REASON_EMPTY_POOL = 1,     /* pool holds no anchor                                   */
+  KVCOMM_REASON_TOO_LONG = 2,       /* L_φ > max_{ψ∈𝒜} L_ψ  (Eq. 5 first clause)             */
+  KVCOMM_REASON_NO_CANDIDATES = 3,  /* no anchor with L_ψ >= L_φ and the consumer's offsets  */
+  KVCOMM_REASON_HIGH_ENTROPY = 4    /* H_{φ|𝒜} > γ log|𝒜_φ|  (Eq. 5 second clause)           */
+} kvcomm_reason;
+
+typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_scalar_distance;
+typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1 } kvcomm_segment_kind;
+typedef enum { KVCOMM_OFFSET_GIVEN = 0, KVCOMM_OFFSET_MEASURE = 1 } kvcomm_offset_mode;
+
+typedef struct kvcomm_pool_s* kvcomm_pool_t;
+
+/* Pool geometry.  One pool per placeholder name ("Each placeholder initializes
+ * an individual anchor pool"); consumer c = one (agent m, slot i) that reads the pool.
+ * The pool holds layers [layer_begin, layer_end) and KV heads [head_begin, head_end)
+ * of the model (Ls = layer_end-layer_begin, Hs = head_end-head_begin). */
+typedef struct {
+  int32_t device;          /* CUDA device ordinal                                        */
+  int32_t num_layers;      /* L of the model                                             */
+  int32_t layer_begin, layer_end;
+  int32_t num_kv_heads;    /* H of the model                                             */
+  int32_t head_begin, head_end;
+  int32_t head_dim;        /* d: multiple of 16, <= 256                                   */
+  int32_t emb_dim;         /* D_e of the token embeddings h (reading A1): multiple of 8  */
+  int32_t capacity;        /* 𝒱, 1..KVCOMM_MAX_CAPACITY (paper default 20)        */
+  int32_t max_anchor_len;  /* longest anchor sample L_ψ the pool will store             */
+  int32_t num_consumers;   /* 1..KVCOMM_MAX_CONSUMERS                                     */
+  int32_t scalar_distance; /* sample-level distance d̄ of Eq. 5/7 (reading A4):
+                              KVCOMM_SCALAR_FROBENIUS (0, default) d̄_j = sqrt(Σ_i d[i,j]²),
+                              KVCOMM_SCALAR_MEAN_L2  (1)           d̄_j = mean_i d[i,j]     */
+  const int32_t* prefix_len; /* host [num_consumers]: |p_(m,i)| following this placeholder */
+  const double* inv_freq;  /* host [head_dim/2]: RoPE inverse frequencies (copied)        */
+} kvcomm_pool_config;
+
+/* A strided view of K and V rows of one shard: element (l, h, i, e) lives at
+ * ptr + ((l*Hs + h)*ld + i)*d + e.  `start` = absolute position of row 0. */
+typedef struct {
+  const void* k;   /* device bf16 */
+  const void* v;   /* device bf16 */
+  int64_t ld;      /* rows between (l,h) blocks; 0 means "= the segment length"   */
+  int32_t start;   /* absolute token position of row 0 (MEASURE mode only)         */
+  int32_t _pad;
+} kvcomm_kv_view;
+
+/* Offsets of one anchor for one consumer (Table A.1: agent_id_ph / agent_id_pf).
+ * GIVEN:   ph_delta / pf_delta hold ΔK,ΔV already in the base frame (reading A10).
+ * MEASURE: the device measures them (Alg. 1; step a0):
+ *          ΔK = R_{-(s_real - s_base)} K_real - K_base,  ΔV = V_real - V_base,
+ *          fp32 arithmetic, one RNE rounding to bf16.
+ * Either part may be omitted by passing k == NULL (it stays absent/unchanged). */
+typedef struct {
+  int32_t consumer;
+  int32_t mode;            /* kvcomm_offset_mode */
+  kvcomm_kv_view ph_delta; /* [Ls,Hs,L_ψ,d]  (GIVEN)      */
+  kvcomm_kv_view pf_delta; /* [Ls,Hs,P_c,d]  (GIVEN)      */
+  kvcomm_kv_view ph_real, ph_base; /* [Ls,Hs,L_ψ,d] (MEASURE) */
+  kvcomm_kv_view pf_real, pf_base; /* [Ls,Hs,P_c,d] (MEASURE) */
+} kvcomm_offset_desc;
+
+typedef struct {
+  int32_t occupied;
+  int32_t length;          /* L_ψ */
+  int64_t access_count;
+  int64_t insertion_index;
+  uint64_t ph_present_mask; /* bit c: placeholder offsets of consumer c present */
+  uint64_t pf_present_mask; /* bit c: prefix offsets of consumer c present      */
+} kvcomm_slot_info;
+
+typedef struct {
+  int32_t verdict;         /* kvcomm_verdict                                             */
+  int32_t reason;          /* kvcomm_reason                                              */
+  int32_t n_candidates;    /* |𝒜_φ|                                                       */
+  int32_t top_k;           /* effective k (n_candidates when top_k = 0)                  */
+  int32_t candidates[KVCOMM_MAX_CAPACITY]; /* slot ids of 𝒜_φ, ascending               */
+  double entropy;          /* H = -Σ w̄ log w̄ (reading A5)                                */
+  double threshold;        /* γ log|𝒜_φ|                                                  */
+  int32_t verdict_in_tie_band; /* |H - threshold| <= 1e-6 * threshold                   */
+  int32_t tie_band_count;  /* positions whose top-k boundary/order has a relative
+                              distance gap <= 1e-6 (0 when top_k = 0)                   */
+} kvcomm_match_info;
+
+/* One segment to realign (step a4+a5).  PLACEHOLDER (Eq. 6): token i of the
+ * segment uses weights W[slot][i].  PREFIX (Eq. 7, reading A3): every token uses
+ * the scalar w̄[slot].  Output rows target_start .. target_start+L_seg-1 of dst:
+ *   K̂ = R_δ(K_base + Σ_j w_j ΔK_j),  V̂ = V_base + Σ_j w_j ΔV_j,  δ = target_start - base_start,
+ * accumulated in fp32, rounded once (RNE) to bf16. */
+typedef struct {
+  kvcomm_pool_t pool;
+  int32_t consumer;        /* 0..num_consumers-1                                          */
+  int32_t kind;            /* kvcomm_segment_kind                                         */
+  const float* weights;    /* device. PLACEHOLDER: W [capacity][ld_w] (slot-major, as
+                              written by kvcomm_match_anchors).  PREFIX: w̄ [capacity]  */
+  int64_t ld_w;            /* PLACEHOLDER: row stride of W, multiple of 4, >= L_seg        */
+  const int32_t* candidates; /* host [n_candidates]: slot ids to blend (info.candidates) */
+  int32_t n_candidates;
+  int32_t L_seg;           /* tokens; PREFIX requires L_seg == prefix_len[consumer]; 0 = no-op */
+  kvcomm_kv_view base;     /* device [Ls,Hs,ld,d] base K/V rows 0..L_seg-1               */
+  int32_t base_start;      /* placeholder base: 0; prefix base: |p_(m,0)| (reading A11)   */
+  int32_t target_start;    /* first destination row (absolute position in the prompt)     */
+  void* dst_k;             /* device bf16 [Ls,Hs,dst_ld,d]                                 */
+  void* dst_v;
+  int64_t dst_ld;          /* prompt length N of the consumer                             */
+  float* debug_delta_k;    /* optional device fp32 [Ls,Hs,L_seg,d]: Σ_j w_j ΔK_j (parity) */
+  float* debug_delta_v;
+} kvcomm_realign_desc;
+
+/* A segment of the consumer's prompt for the concatenation ledger (step a6).
+ * src.k != NULL: rows are copied verbatim from src (e.g. p_(m,0), reading A20);
+ * src.k == NULL: rows were already written in place (by realign). */
+typedef struct {
+  int32_t start;
+  int32_t length;
+  kvcomm_kv_view src;
+} kvcomm_segment_ref;
+
+/* ---- status / diagnostics ------------------------------------------------- */
+KVCOMM_API const char* kvcomm_status_string(kvcomm_status s);
+KVCOMM_API const char* kvcomm_last_error_message(void);      /* thread-local */
+KVCOMM_API int32_t kvcomm_version(void);
+/* Number of CUDA kernels this library has launched in this process. */
+KVCOMM_API int64_t kvcomm_kernel_launch_count(void);
+
+/* ---- a0: anchor-pool store ------------------------------------------------- */
+/* Allocates the pool's device slabs (embeddings [𝒱][max_len][D_e], placeholder
+ * offsets [C][𝒱][2][Ls][Hs][max_len][d], prefix offsets [C][𝒱][2][Ls][Hs][P_c][d],
+ * bf16) on config->device.  OUT_OF_MEMORY if they do not fit. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* config,
+                                                   kvcomm_pool_t* out);
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_destroy(kvcomm_pool_t pool);
+/* Bytes of device memory the pool owns. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_bytes(kvcomm_pool_t pool, int64_t* bytes);
+
+/* Insert a new anchor ψ ("the newly-generated cache becomes a new anchor"):
+ * copies its embeddings emb (device bf16 [L_psi][D_e]) and the given/measured offsets
+ * into a free slot.  If the pool is full, first evicts the anchor with the smallest
+ * access count, ties to the earliest inserted (reading A17); the incoming
+ * anchor is never its own victim.  *slot_out = slot used; *evicted_out = evicted
+ * slot or -1.  L_psi in [1, max_anchor_len]. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t pool, int32_t L_psi,
+                                                   const void* emb,
+                                                   const kvcomm_offset_desc* offs, int32_t n_offs,
+                                                   void* stream, int32_t* slot_out,
+                                                   int32_t* evicted_out);
+/* Fill in (or replace) offsets of an existing anchor ("dependent agents fill in
+ * deviations under their respective contexts"). */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_set_offsets(kvcomm_pool_t pool, int32_t slot,
+                                                        const kvcomm_offset_desc* offs,
+                                                        int32_t n_offs, void* stream);
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_evict(kvcomm_pool_t pool, int32_t slot);
+/* +1 access for each listed slot (reading A18: once per Shareable turn). */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_record_access(kvcomm_pool_t pool,
+                                                          const int32_t* slots, int32_t n);
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t pool, int32_t slot,
+                                                      kvcomm_slot_info* info);
+/* Device view of a stored offset (which: 0 placeholder, 1 prefix) for inspection:
+ * *k, *v point at [Ls][Hs][*ld][d] bf16 rows of the slot. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t pool, int32_t slot,
+                                                        int32_t consumer, int32_t which,
+                                                        const void** k, const void** v,
+                                                        int64_t* ld);
+
+/* ---- a1-a3: anchor matching (Eq. 5, Eq. 6 weights) -------------------------- */
+/* query_emb: device bf16 [L_phi][D_e] (the sample's token embeddings h_φ).
+ * consumer: candidates must hold that consumer's placeholder+prefix offsets;
+ *   KVCOMM_ALL_CONSUMERS requires every consumer's (weights are then shared by all
+ *   consumers of the sample, reading A21).
+ * Computes, on the device, d[i,j] = ‖h_φ[i] - h_ψj[i]‖₂ (fp32 differences, fp64
+ * accumulation), W[j][i] = softmax_j(-d[i,j]) (fp64, stored fp32), optional top-k
+ * (distance asc, slot asc; KVCOMM_MAX_TOPK), d̄_j per config.scalar_distance, w̄ = softmax(-d̄),
+ * H = -Σ w̄ log w̄ and the verdict.
+ * Outputs (device): W [capacity][ld_w] fp32 (rows of non-candidate slots = 0),
+ * idx [L_phi][top_k] int32 slot ids (may be NULL; ignored if top_k = 0),
+ * wbar [capacity] fp32 (0 for non-candidates), dist (optional fp64 [capacity][ld_w]).
+ * When the verdict is decided by the length clause / empty pool, no kernel runs and
+ * the device outputs are left untouched. */
+KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t pool, const void* query_emb,
+                                              int32_t L_phi, int32_t consumer, float gamma,
+                                              int32_t top_k, float* W, int64_t ld_w,
+                                              int32_t* idx, float* wbar, double* dist,
+                                              kvcomm_match_info* info, void* stream);
+
+/* ---- a4-a5: fused blend + RoPE-δ + add ------------------------------------ */
+KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, void* stream);
+/* All segments of one request in ONE persistent kernel launch.  Segments may come
+ * from different pools but must share (Ls, Hs, d) and device. */
+KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs, int32_t n,
+                                                 void* stream);
+
+/* ---- a6: concatenation + ledger ------------------------------------------- */
+/* Checks that segs tile [0, N_total) in order (POSITION_GAP / POSITION_OVERLAP
+ * otherwise, nothing launched) and copies the rows of segments with src.k != NULL
+ * into dst [Ls][Hs][dst_ld][d] (dst_ld >= N_total). */
+KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n,
+                                                     int32_t N_total, int32_t Ls, int32_t Hs,
+                                                     int32_t d, void* dst_k, void* dst_v,
+                                                     int64_t dst_ld, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVCOMM_H */

@@ -1,0 +1,138 @@
+"""ctypes mirror of include/kvcomm.h and the loader of lib/libkvcomm.so.
+
+There is no fallback: if the shared library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libkvcomm.so")
+HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "kvcomm.h")
+
+MAX_CAPACITY = 1024
+MAX_CONSUMERS = 64
+MAX_TOPK = 32
+ALL_CONSUMERS = -1
+
+OK = 0
+STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE_MISMATCH", "NO_CANDIDATES", "MISSING_OFFSET",
+                "POSITION_GAP", "POSITION_OVERLAP", "NOT_FOUND", "OUT_OF_MEMORY", "CUDA", "NCCL"]
+SHAREABLE, NEW_ANCHOR = 0, 1
+REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY"]
+PLACEHOLDER, PREFIX = 0, 1
+OFFSET_GIVEN, OFFSET_MEASURE = 0, 1
+SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1
+
+
+class PoolConfig(C.Structure):
+    _fields_ = [("device", C.c_int32), ("num_layers", C.c_int32), ("layer_begin", C.c_int32),
+                ("layer_end", C.c_int32), ("num_kv_heads", C.c_int32), ("head_begin", C.c_int32),
+                ("head_end", C.c_int32), ("head_dim", C.c_int32), ("emb_dim", C.c_int32),
+                ("capacity", C.c_int32), ("max_anchor_len", C.c_int32), ("num_consumers", C.c_int32),
+                ("scalar_distance", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
+
+
+class KVView(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("ld", C.c_int64), ("start", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class OffsetDesc(C.Structure):
+    _fields_ = [("consumer", C.c_int32), ("mode", C.c_int32), ("ph_delta", KVView), ("pf_delta", KVView),
+                ("ph_real", KVView), ("ph_base", KVView), ("pf_real", KVView), ("pf_base", KVView)]
+
+
+class SlotInfo(C.Structure):
+    _fields_ = [("occupied", C.c_int32), ("length", C.c_int32), ("access_count", C.c_int64),
+                ("insertion_index", C.c_int64), ("ph_present_mask", C.c_uint64),
+                ("pf_present_mask", C.c_uint64)]
+
+
+class MatchInfo(C.Structure):
+    _fields_ = [("verdict", C.c_int32), ("reason", C.c_int32), ("n_candidates", C.c_int32),
+                ("top_k", C.c_int32), ("candidates", C.c_int32 * MAX_CAPACITY), ("entropy", C.c_double),
+                ("threshold", C.c_double), ("verdict_in_tie_band", C.c_int32), ("tie_band_count", C.c_int32)]
+
+
+class RealignDesc(C.Structure):
+    _fields_ = [("pool", C.c_void_p), ("consumer", C.c_int32), ("kind", C.c_int32), ("weights", C.c_void_p),
+                ("ld_w", C.c_int64), ("candidates", C.POINTER(C.c_int32)), ("n_candidates", C.c_int32),
+                ("L_seg", C.c_int32), ("base", KVView), ("base_start", C.c_int32), ("target_start", C.c_int32),
+                ("dst_k", C.c_void_p), ("dst_v", C.c_void_p), ("dst_ld", C.c_int64),
+                ("debug_delta_k", C.c_void_p), ("debug_delta_v", C.c_void_p)]
+
+
+class SegmentRef(C.Structure):
+    _fields_ = [("start", C.c_int32), ("length", C.c_int32), ("src", KVView)]
+
+
+_SIGS = {
+    "kvcomm_status_string": (C.c_char_p, [C.c_int]),
+    "kvcomm_last_error_message": (C.c_char_p, []),
+    "kvcomm_version": (C.c_int32, []),
+    "kvcomm_kernel_launch_count": (C.c_int64, []),
+    "kvcomm_anchor_pool_create": (C.c_int, [C.POINTER(PoolConfig), C.POINTER(C.c_void_p)]),
+    "kvcomm_anchor_pool_destroy": (C.c_int, [C.c_void_p]),
+    "kvcomm_anchor_pool_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "kvcomm_anchor_pool_insert": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(OffsetDesc), C.c_int32,
+                                            C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "kvcomm_anchor_pool_set_offsets": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(OffsetDesc), C.c_int32,
+                                                 C.c_void_p]),
+    "kvcomm_anchor_pool_evict": (C.c_int, [C.c_void_p, C.c_int32]),
+    "kvcomm_anchor_pool_record_access": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32]),
+    "kvcomm_anchor_pool_slot_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(SlotInfo)]),
+    "kvcomm_anchor_pool_offset_view": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                 C.POINTER(C.c_int64)]),
+    "kvcomm_match_anchors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_int32,
+                                       C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.POINTER(MatchInfo), C.c_void_p]),
+    "kvcomm_realign_segment": (C.c_int, [C.POINTER(RealignDesc), C.c_void_p]),
+    "kvcomm_realign_segments": (C.c_int, [C.POINTER(RealignDesc), C.c_int32, C.c_void_p]),
+    "kvcomm_concat_prefill_cache": (C.c_int, [C.POINTER(SegmentRef), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+}
+
+
+def header_symbols(path: str = HEADER_PATH):
+    """Names of every KVCOMM_API function declared in include/kvcomm.h."""
+    text = open(path).read()
+    return re.findall(r"KVCOMM_API\s+[\w\s\*]+?\b(kvcomm_\w+)\s*\(", text)
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise RuntimeError(f"libkvcomm.so not found at {path}: build it with "
+                           "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+class KVCommError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{name}: {message}")
+        self.status = status
+        self.status_name = name
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        _LIB = load()
+    return _LIB
+
+
+def check(status: int) -> None:
+    if status != OK:
+        raise KVCommError(status, lib().kvcomm_last_error_message().decode())

@@ -1,0 +1,797 @@
+// C ABI of libkvcomm (include/kvcomm.h): anchor-pool store (host metadata + device
+// slabs), argument validation, work-table construction and kernel launches.
+// No exception crosses the ABI; every entry point returns a kvcomm_status.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <shared_mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/kvcomm.h"
+#include "kvcomm_internal.h"
+
+using namespace kvc;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+kvcomm_status fail(kvcomm_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+kvcomm_status ok() {
+  g_err.clear();
+  return KVCOMM_OK;
+}
+
+#define KV_CUDA(expr)                                                                          \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) return fail(KVCOMM_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define KV_TRY(expr)                  \
+  do {                                \
+    kvcomm_status _s = (expr);        \
+    if (_s != KVCOMM_OK) return _s;   \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Makes `dev` current for the scope of a call and restores the caller's device.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// pool
+// ---------------------------------------------------------------------------
+struct SlotMeta {
+  bool occupied = false;
+  int32_t length = 0;
+  int64_t access = 0;
+  int64_t inserted = 0;
+  uint64_t ph_mask = 0, pf_mask = 0;
+};
+
+struct kvcomm_pool_s {
+  kvcomm_pool_config cfg{};
+  int Ls = 0, Hs = 0, d = 0, De = 0, cap = 0, maxlen = 0, C = 0;
+  std::vector<int32_t> prefix_len;
+  std::vector<double> inv_freq;
+  // device slabs
+  bf16* emb = nullptr;                 // [cap][maxlen][De]
+  bf16* ph = nullptr;                  // [C][cap][2][Ls][Hs][maxlen][d]
+  std::vector<bf16*> pf;               // per consumer: [cap][2][Ls][Hs][P_c][d]
+  double* inv_freq_dev = nullptr;
+  // match scratch
+  int32_t* d_cand = nullptr;           // [cap]
+  int32_t* d_slot2cand = nullptr;      // [cap]
+  double* d_dist = nullptr;            // [cap][maxlen]
+  double* d_partial = nullptr;         // [n_blocks_max][cap]
+  int32_t* d_tie = nullptr;
+  MatchResultDev* d_res = nullptr;
+  MatchResultDev* h_res = nullptr;     // pinned
+  int32_t* h_cand = nullptr;           // pinned staging for candidate lists [2*cap]
+  int64_t bytes = 0;
+  std::vector<SlotMeta> slots;
+  int64_t next_index = 0;
+  mutable std::shared_mutex mu;        // metadata: many readers / one writer
+  std::mutex match_mu;                 // match scratch buffers
+  void* prev_tab_event = nullptr;
+
+  int64_t ph_slot_stride() const { return int64_t(2) * Ls * Hs * maxlen * d; }
+  int64_t ph_plane_stride() const { return int64_t(Ls) * Hs * maxlen * d; }
+  bf16* ph_base(int c) const { return ph + int64_t(c) * cap * ph_slot_stride(); }
+  int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * prefix_len[c] * d; }
+  int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * prefix_len[c] * d; }
+};
+
+static constexpr int kMatchP = 4;  // positions per match block
+
+static void pool_free(kvcomm_pool_s* p) {
+  if (!p) return;
+  DeviceGuard g(p->cfg.device);
+  cudaFree(p->emb);
+  cudaFree(p->ph);
+  for (auto* x : p->pf) cudaFree(x);
+  cudaFree(p->inv_freq_dev);
+  cudaFree(p->d_cand);
+  cudaFree(p->d_slot2cand);
+  cudaFree(p->d_dist);
+  cudaFree(p->d_partial);
+  cudaFree(p->d_tie);
+  cudaFree(p->d_res);
+  if (p->h_res) cudaFreeHost(p->h_res);
+  if (p->h_cand) cudaFreeHost(p->h_cand);
+  delete p;
+}
+
+template <typename T>
+static kvcomm_status dev_alloc(kvcomm_pool_s* p, T** out, int64_t count, const char* what) {
+  const size_t bytes = size_t(std::max<int64_t>(count, 1)) * sizeof(T);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(out), bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? KVCOMM_ERR_OUT_OF_MEMORY : KVCOMM_ERR_CUDA,
+                "allocating %s (%zu bytes): %s", what, bytes, cudaGetErrorString(e));
+  }
+  p->bytes += int64_t(bytes);
+  return KVCOMM_OK;
+}
+
+extern "C" {
+
+KVCOMM_API const char* kvcomm_status_string(kvcomm_status s) {
+  switch (s) {
+    case KVCOMM_OK: return "OK";
+    case KVCOMM_ERR_INVALID_ARGUMENT: return "INVALID_ARGUMENT";
+    case KVCOMM_ERR_SHAPE_MISMATCH: return "SHAPE_MISMATCH";
+    case KVCOMM_ERR_NO_CANDIDATES: return "NO_CANDIDATES";
+    case KVCOMM_ERR_MISSING_OFFSET: return "MISSING_OFFSET";
+    case KVCOMM_ERR_POSITION_GAP: return "POSITION_GAP";
+    case KVCOMM_ERR_POSITION_OVERLAP: return "POSITION_OVERLAP";
+    case KVCOMM_ERR_NOT_FOUND: return "NOT_FOUND";
+    case KVCOMM_ERR_OUT_OF_MEMORY: return "OUT_OF_MEMORY";
+    case KVCOMM_ERR_CUDA: return "CUDA";
+    case KVCOMM_ERR_NCCL: return "NCCL";
+  }
+  return "UNKNOWN";
+}
+
+KVCOMM_API const char* kvcomm_last_error_message(void) { return g_err.c_str(); }
+KVCOMM_API int32_t kvcomm_version(void) { return KVCOMM_VERSION; }
+KVCOMM_API int64_t kvcomm_kernel_launch_count(void) { return g_launches.load(); }
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, kvcomm_pool_t* out) {
+  if (!c || !out) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null config/out");
+  *out = nullptr;
+  const int Ls = c->layer_end - c->layer_begin, Hs = c->head_end - c->head_begin;
+  if (c->num_layers <= 0 || c->layer_begin < 0 || c->layer_end > c->num_layers || Ls <= 0)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad layer shard [%d,%d) of %d", c->layer_begin, c->layer_end,
+                c->num_layers);
+  if (c->num_kv_heads <= 0 || c->head_begin < 0 || c->head_end > c->num_kv_heads || Hs <= 0)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad head shard [%d,%d) of %d", c->head_begin, c->head_end,
+                c->num_kv_heads);
+  if (c->head_dim <= 0 || c->head_dim % 16 != 0 || c->head_dim > 256)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "head_dim %d must be a multiple of 16 in [16,256]", c->head_dim);
+  if (c->emb_dim <= 0 || c->emb_dim % 8 != 0)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "emb_dim %d must be a positive multiple of 8", c->emb_dim);
+  if (c->capacity < 1 || c->capacity > KVCOMM_MAX_CAPACITY)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "capacity %d outside [1,%d]", c->capacity, KVCOMM_MAX_CAPACITY);
+  if (c->max_anchor_len < 1) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "max_anchor_len %d", c->max_anchor_len);
+  if (c->num_consumers < 1 || c->num_consumers > KVCOMM_MAX_CONSUMERS)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "num_consumers %d outside [1,%d]", c->num_consumers,
+                KVCOMM_MAX_CONSUMERS);
+  if (!c->prefix_len || !c->inv_freq) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null prefix_len/inv_freq");
+  if (c->scalar_distance != KVCOMM_SCALAR_FROBENIUS && c->scalar_distance != KVCOMM_SCALAR_MEAN_L2)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "scalar_distance %d", c->scalar_distance);
+  for (int i = 0; i < c->num_consumers; ++i)
+    if (c->prefix_len[i] < 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "prefix_len[%d] < 0", i);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device < 0 || c->device >= ndev) {
+    cudaGetLastError();
+    return fail(KVCOMM_ERR_CUDA, "device %d not available (%d devices)", c->device, ndev);
+  }
+  DeviceGuard guard(c->device);
+  if (!guard.ok) return fail(KVCOMM_ERR_CUDA, "cudaSetDevice(%d) failed", c->device);
+
+  auto* p = new kvcomm_pool_s();
+  p->cfg = *c;
+  p->Ls = Ls; p->Hs = Hs; p->d = c->head_dim; p->De = c->emb_dim; p->cap = c->capacity;
+  p->maxlen = c->max_anchor_len; p->C = c->num_consumers;
+  p->prefix_len.assign(c->prefix_len, c->prefix_len + c->num_consumers);
+  p->inv_freq.assign(c->inv_freq, c->inv_freq + c->head_dim / 2);
+  p->cfg.prefix_len = nullptr;
+  p->cfg.inv_freq = nullptr;
+  p->slots.resize(p->cap);
+  kvcomm_status st;
+#define ALLOC(ptr, n, what)                          \
+  if ((st = dev_alloc(p, &(ptr), (n), what)) != KVCOMM_OK) { pool_free(p); return st; }
+  ALLOC(p->emb, int64_t(p->cap) * p->maxlen * p->De, "embedding slab");
+  ALLOC(p->ph, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab");
+  p->pf.assign(p->C, nullptr);
+  for (int i = 0; i < p->C; ++i) ALLOC(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
+  ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
+  ALLOC(p->d_cand, p->cap, "candidate list");
+  ALLOC(p->d_slot2cand, p->cap, "slot map");
+  ALLOC(p->d_dist, int64_t(p->cap) * p->maxlen, "distance scratch");
+  ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * p->cap, "partial sums");
+  ALLOC(p->d_tie, 1, "tie counter");
+  ALLOC(p->d_res, 1, "match result");
+#undef ALLOC
+  if (cudaMallocHost(reinterpret_cast<void**>(&p->h_res), sizeof(MatchResultDev)) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&p->h_cand), sizeof(int32_t) * 2 * p->cap) != cudaSuccess) {
+    cudaGetLastError();
+    pool_free(p);
+    return fail(KVCOMM_ERR_OUT_OF_MEMORY, "pinned host staging");
+  }
+  cudaError_t e = cudaMemcpy(p->inv_freq_dev, p->inv_freq.data(), sizeof(double) * (p->d / 2),
+                             cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    pool_free(p);
+    return fail(KVCOMM_ERR_CUDA, "inv_freq upload: %s", cudaGetErrorString(e));
+  }
+  *out = p;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_destroy(kvcomm_pool_t p) {
+  if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool");
+  {
+    DeviceGuard g(p->cfg.device);
+    cudaDeviceSynchronize();
+  }
+  pool_free(p);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_bytes(kvcomm_pool_t p, int64_t* bytes) {
+  if (!p || !bytes) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  *bytes = p->bytes;
+  return ok();
+}
+
+// ---- offsets -----------------------------------------------------------------
+static kvcomm_status check_view(const kvcomm_kv_view& v, int rows, const char* what) {
+  if (!v.k || !v.v) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "%s: null k/v", what);
+  if (!aligned16(v.k) || !aligned16(v.v)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "%s: not 16-byte aligned", what);
+  if (v.ld != 0 && v.ld < rows)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "%s: ld %lld < rows %d", what, (long long)v.ld, rows);
+  return KVCOMM_OK;
+}
+
+static int64_t ld_of(const kvcomm_kv_view& v, int rows) { return v.ld ? v.ld : rows; }
+
+// Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
+static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const kvcomm_offset_desc& o,
+                                   cudaStream_t s, uint64_t* ph_set, uint64_t* pf_set) {
+  const int c = o.consumer;
+  if (c < 0 || c >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d outside [0,%d)", c, p->C);
+  const int P = p->prefix_len[c];
+  bf16* phk = p->ph_base(c) + int64_t(slot) * p->ph_slot_stride();
+  bf16* phv = phk + p->ph_plane_stride();
+  bf16* pfk = p->pf[c] + int64_t(slot) * p->pf_slot_stride(c);
+  bf16* pfv = pfk + p->pf_plane_stride(c);
+  if (P == 0) *pf_set |= 1ull << c;  // an empty prefix segment needs no offsets
+  if (o.mode == KVCOMM_OFFSET_GIVEN) {
+    if (o.ph_delta.k) {
+      KV_TRY(check_view(o.ph_delta, L_psi, "ph_delta"));
+      const int64_t ld = ld_of(o.ph_delta, L_psi);
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.k), ld, phk, p->maxlen, p->Ls, p->Hs, L_psi,
+                               p->d, s));
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.v), ld, phv, p->maxlen, p->Ls, p->Hs, L_psi,
+                               p->d, s));
+      g_launches += 2;
+      *ph_set |= 1ull << c;
+    }
+    if (o.pf_delta.k) {
+      KV_TRY(check_view(o.pf_delta, P, "pf_delta"));
+      const int64_t ld = ld_of(o.pf_delta, P);
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.pf_delta.k), ld, pfk, P, p->Ls, p->Hs, P, p->d, s));
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.pf_delta.v), ld, pfv, P, p->Ls, p->Hs, P, p->d, s));
+      g_launches += 2;
+      *pf_set |= 1ull << c;
+    }
+  } else if (o.mode == KVCOMM_OFFSET_MEASURE) {
+    if (o.ph_real.k) {
+      KV_TRY(check_view(o.ph_real, L_psi, "ph_real"));
+      KV_TRY(check_view(o.ph_base, L_psi, "ph_base"));
+      KV_CUDA(launch_measure(static_cast<const bf16*>(o.ph_real.k), static_cast<const bf16*>(o.ph_real.v),
+                             ld_of(o.ph_real, L_psi), static_cast<const bf16*>(o.ph_base.k),
+                             static_cast<const bf16*>(o.ph_base.v), ld_of(o.ph_base, L_psi), L_psi, p->Ls, p->Hs,
+                             p->d, -(o.ph_real.start - o.ph_base.start), p->inv_freq_dev, phk, phv, p->maxlen, s));
+      g_launches += 1;
+      *ph_set |= 1ull << c;
+    }
+    if (o.pf_real.k) {
+      KV_TRY(check_view(o.pf_real, P, "pf_real"));
+      KV_TRY(check_view(o.pf_base, P, "pf_base"));
+      KV_CUDA(launch_measure(static_cast<const bf16*>(o.pf_real.k), static_cast<const bf16*>(o.pf_real.v),
+                             ld_of(o.pf_real, P), static_cast<const bf16*>(o.pf_base.k),
+                             static_cast<const bf16*>(o.pf_base.v), ld_of(o.pf_base, P), P, p->Ls, p->Hs, p->d,
+                             -(o.pf_real.start - o.pf_base.start), p->inv_freq_dev, pfk, pfv, P, s));
+      g_launches += 1;
+      *pf_set |= 1ull << c;
+    }
+  } else {
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "offset mode %d", o.mode);
+  }
+  return KVCOMM_OK;
+}
+
+static int lfu_victim(const kvcomm_pool_s* p) {
+  int best = -1;
+  for (int s = 0; s < p->cap; ++s) {
+    const SlotMeta& m = p->slots[s];
+    if (!m.occupied) continue;
+    if (best < 0 || m.access < p->slots[best].access ||
+        (m.access == p->slots[best].access && m.inserted < p->slots[best].inserted))
+      best = s;
+  }
+  return best;
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_psi, const void* emb,
+                                                   const kvcomm_offset_desc* offs, int32_t n_offs, void* stream,
+                                                   int32_t* slot_out, int32_t* evicted_out) {
+  if (!p || !emb || (n_offs > 0 && !offs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (L_psi < 1 || L_psi > p->maxlen)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "L_psi %d outside [1,%d]", L_psi, p->maxlen);
+  if (!aligned16(emb)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "emb not 16-byte aligned");
+  DeviceGuard guard(p->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::unique_lock<std::shared_mutex> lk(p->mu);
+  int evicted = -1;
+  int slot = -1;
+  for (int i = 0; i < p->cap; ++i)
+    if (!p->slots[i].occupied) { slot = i; break; }
+  if (slot < 0) {
+    evicted = lfu_victim(p);
+    p->slots[evicted] = SlotMeta();
+    slot = evicted;
+  }
+  KV_CUDA(launch_copy_flat(static_cast<const bf16*>(emb), p->emb + int64_t(slot) * p->maxlen * p->De,
+                           int64_t(L_psi) * p->De, s));
+  g_launches += 1;
+  uint64_t phm = 0, pfm = 0;
+  for (int i = 0; i < n_offs; ++i) {
+    kvcomm_status st = write_offsets(p, slot, L_psi, offs[i], s, &phm, &pfm);
+    if (st != KVCOMM_OK) {
+      if (evicted < 0) p->slots[slot] = SlotMeta();  // leave the pool as it was (minus the victim)
+      return st;
+    }
+  }
+  SlotMeta& m = p->slots[slot];
+  m.occupied = true;
+  m.length = L_psi;
+  m.access = 0;
+  m.inserted = p->next_index++;
+  m.ph_mask = phm;
+  m.pf_mask = pfm;
+  if (slot_out) *slot_out = slot;
+  if (evicted_out) *evicted_out = evicted;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_set_offsets(kvcomm_pool_t p, int32_t slot,
+                                                        const kvcomm_offset_desc* offs, int32_t n_offs,
+                                                        void* stream) {
+  if (!p || (n_offs > 0 && !offs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  std::unique_lock<std::shared_mutex> lk(p->mu);
+  if (slot < 0 || slot >= p->cap || !p->slots[slot].occupied)
+    return fail(KVCOMM_ERR_NOT_FOUND, "slot %d is empty", slot);
+  DeviceGuard guard(p->cfg.device);
+  SlotMeta& m = p->slots[slot];
+  for (int i = 0; i < n_offs; ++i)
+    KV_TRY(write_offsets(p, slot, m.length, offs[i], static_cast<cudaStream_t>(stream), &m.ph_mask, &m.pf_mask));
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_evict(kvcomm_pool_t p, int32_t slot) {
+  if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool");
+  std::unique_lock<std::shared_mutex> lk(p->mu);
+  if (slot < 0 || slot >= p->cap || !p->slots[slot].occupied)
+    return fail(KVCOMM_ERR_NOT_FOUND, "slot %d is empty", slot);
+  p->slots[slot] = SlotMeta();
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_record_access(kvcomm_pool_t p, const int32_t* slots, int32_t n) {
+  if (!p || (n > 0 && !slots)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  std::unique_lock<std::shared_mutex> lk(p->mu);
+  for (int i = 0; i < n; ++i)
+    if (slots[i] < 0 || slots[i] >= p->cap || !p->slots[slots[i]].occupied)
+      return fail(KVCOMM_ERR_NOT_FOUND, "slot %d is empty", slots[i]);
+  for (int i = 0; i < n; ++i) p->slots[slots[i]].access += 1;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t p, int32_t slot, kvcomm_slot_info* info) {
+  if (!p || !info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d outside [0,%d)", slot, p->cap);
+  std::shared_lock<std::shared_mutex> lk(p->mu);
+  const SlotMeta& m = p->slots[slot];
+  info->occupied = m.occupied;
+  info->length = m.length;
+  info->access_count = m.access;
+  info->insertion_index = m.inserted;
+  info->ph_present_mask = m.ph_mask;
+  info->pf_present_mask = m.pf_mask;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t p, int32_t slot, int32_t consumer,
+                                                        int32_t which, const void** k, const void** v,
+                                                        int64_t* ld) {
+  if (!p || !k || !v || !ld) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d", slot);
+  if (consumer < 0 || consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
+  if (which == 0) {
+    const bf16* b = p->ph_base(consumer) + int64_t(slot) * p->ph_slot_stride();
+    *k = b;
+    *v = b + p->ph_plane_stride();
+    *ld = p->maxlen;
+  } else {
+    const bf16* b = p->pf[consumer] + int64_t(slot) * p->pf_slot_stride(consumer);
+    *k = b;
+    *v = b + p->pf_plane_stride(consumer);
+    *ld = p->prefix_len[consumer];
+  }
+  return ok();
+}
+
+// ---- match -------------------------------------------------------------------
+KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t p, const void* query_emb, int32_t L_phi,
+                                              int32_t consumer, float gamma, int32_t top_k, float* W,
+                                              int64_t ld_w, int32_t* idx, float* wbar, double* dist,
+                                              kvcomm_match_info* info, void* stream) {
+  if (!p || !info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool/info");
+  if (!(gamma >= 0.f && gamma <= 1.f)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "gamma %g outside [0,1]", gamma);
+  if (L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "L_phi %d < 1", L_phi);
+  if (top_k < 0 || top_k > KVCOMM_MAX_TOPK)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "top_k %d outside [0,%d]", top_k, KVCOMM_MAX_TOPK);
+  if (consumer != KVCOMM_ALL_CONSUMERS && (consumer < 0 || consumer >= p->C))
+    return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
+  std::memset(info, 0, sizeof(*info));
+  std::shared_lock<std::shared_mutex> lk(p->mu);
+  // a1: candidate filter and length clause (host, integer metadata)
+  int32_t maxL = 0, n_occ = 0;
+  const uint64_t need = consumer == KVCOMM_ALL_CONSUMERS
+                            ? (p->C >= 64 ? ~0ull : ((1ull << p->C) - 1))
+                            : (1ull << consumer);
+  int n_cand = 0;
+  for (int s = 0; s < p->cap; ++s) {
+    const SlotMeta& m = p->slots[s];
+    if (!m.occupied) continue;
+    ++n_occ;
+    maxL = std::max(maxL, m.length);
+    if (m.length >= L_phi && (m.ph_mask & need) == need && (m.pf_mask & need) == need)
+      info->candidates[n_cand++] = s;
+  }
+  info->n_candidates = n_cand;
+  info->verdict = KVCOMM_NEW_ANCHOR;
+  if (n_occ == 0) { info->reason = KVCOMM_REASON_EMPTY_POOL; return ok(); }
+  if (L_phi > maxL) { info->reason = KVCOMM_REASON_TOO_LONG; return ok(); }
+  if (n_cand == 0) { info->reason = KVCOMM_REASON_NO_CANDIDATES; return ok(); }
+  if (!query_emb || !W || !wbar) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null query/W/wbar");
+  if (!aligned16(query_emb)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "query_emb not 16-byte aligned");
+  if (ld_w < L_phi) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "ld_w %lld < L_phi %d", (long long)ld_w, L_phi);
+  const int k_eff = top_k > 0 ? std::min(top_k, n_cand) : 0;
+  info->top_k = k_eff > 0 ? k_eff : n_cand;
+
+  DeviceGuard guard(p->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> mlk(p->match_mu);
+  // upload candidate list and slot->candidate map (pinned staging; the previous
+  // match on this pool synchronised its stream, so the staging is free)
+  std::vector<int32_t> s2c(p->cap, -1);
+  for (int j = 0; j < n_cand; ++j) s2c[info->candidates[j]] = j;
+  std::memcpy(p->h_cand, info->candidates, sizeof(int32_t) * n_cand);
+  std::memcpy(p->h_cand + p->cap, s2c.data(), sizeof(int32_t) * p->cap);
+  KV_CUDA(cudaMemcpyAsync(p->d_cand, p->h_cand, sizeof(int32_t) * n_cand, cudaMemcpyHostToDevice, s));
+  KV_CUDA(cudaMemcpyAsync(p->d_slot2cand, p->h_cand + p->cap, sizeof(int32_t) * p->cap, cudaMemcpyHostToDevice, s));
+  KV_CUDA(cudaMemsetAsync(p->d_tie, 0, sizeof(int32_t), s));
+
+  MatchArgs a{};
+  a.query = static_cast<const bf16*>(query_emb);
+  a.emb = p->emb;
+  a.slot_stride = int64_t(p->maxlen) * p->De;
+  a.cand = p->d_cand;
+  a.slot2cand = p->d_slot2cand;
+  a.n_cand = n_cand;
+  a.cap = p->cap;
+  a.L_phi = L_phi;
+  a.De = p->De;
+  a.top_k = k_eff;
+  a.scalar_mode = p->cfg.scalar_distance;
+  a.W = W;
+  a.ld_w = ld_w;
+  a.idx = k_eff > 0 ? idx : nullptr;
+  a.dist = p->d_dist;
+  a.ld_d = p->maxlen;
+  a.dist_user = dist;
+  a.partial = p->d_partial;
+  a.tie_count = p->d_tie;
+  const int n_blocks = (L_phi + kMatchP - 1) / kMatchP;
+  KV_CUDA(launch_match(a, kMatchP, s));
+  KV_CUDA(launch_match_finalize(a, n_blocks, double(gamma), wbar, p->d_res, s));
+  g_launches += 2;
+  KV_CUDA(cudaMemcpyAsync(p->h_res, p->d_res, sizeof(MatchResultDev), cudaMemcpyDeviceToHost, s));
+  KV_CUDA(cudaStreamSynchronize(s));
+  info->entropy = p->h_res->entropy;
+  info->threshold = p->h_res->threshold;
+  info->verdict = p->h_res->verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
+  info->reason = p->h_res->verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
+  info->verdict_in_tie_band = p->h_res->tie_flag;
+  info->tie_band_count = p->h_res->tie_count;
+  return ok();
+}
+
+// ---- realign -----------------------------------------------------------------
+namespace {
+
+// A small ring of (pinned host, device) buffers for realign work tables.  Slot
+// reuse waits on the event recorded after the kernel that consumed it.
+struct TableRing {
+  static constexpr int kN = 8;
+  struct Entry {
+    void* host = nullptr;
+    void* dev = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+    bool used = false;
+  } e[kN];
+  int next = 0;
+  std::mutex mu;
+};
+TableRing g_rings[64];
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx, int* out_rows_len) {
+  kvcomm_pool_s* p = g.pool;
+  if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", idx);
+  if (g.consumer < 0 || g.consumer >= p->C)
+    return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: consumer %d outside [0,%d)", idx, g.consumer, p->C);
+  if (g.kind != KVCOMM_PLACEHOLDER && g.kind != KVCOMM_PREFIX)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: kind %d", idx, g.kind);
+  if (g.L_seg < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: L_seg %d", idx, g.L_seg);
+  if (g.L_seg == 0) return KVCOMM_OK;
+  if (g.n_candidates < 1 || !g.candidates)
+    return fail(KVCOMM_ERR_NO_CANDIDATES, "segment %d: empty candidate set", idx);
+  if (g.n_candidates > p->cap) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: n_candidates", idx);
+  if (!g.weights) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null weights", idx);
+  if (g.kind == KVCOMM_PREFIX) {
+    if (g.L_seg != p->prefix_len[g.consumer])
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: prefix L_seg %d != prefix_len %d", idx, g.L_seg,
+                  p->prefix_len[g.consumer]);
+  } else {
+    if (g.L_seg > p->maxlen)
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: L_seg %d > max_anchor_len %d", idx, g.L_seg, p->maxlen);
+    if (g.ld_w % 4 != 0 || g.ld_w < ((g.L_seg + 3) & ~3))
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: ld_w %lld must be a multiple of 4 >= L_seg", idx,
+                  (long long)g.ld_w);
+    if (!aligned16(g.weights)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: W not 16-byte aligned", idx);
+  }
+  KV_TRY(check_view(g.base, g.L_seg, "base"));
+  if (!g.dst_k || !g.dst_v || !aligned16(g.dst_k) || !aligned16(g.dst_v))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: dst null or misaligned", idx);
+  if (g.target_start < 0 || int64_t(g.target_start) + g.L_seg > g.dst_ld)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: rows [%d,%d) outside dst_ld %lld", idx, g.target_start,
+                g.target_start + g.L_seg, (long long)g.dst_ld);
+  if ((g.debug_delta_k && !aligned16(g.debug_delta_k)) || (g.debug_delta_v && !aligned16(g.debug_delta_v)))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: debug buffers misaligned", idx);
+  const uint64_t bit = 1ull << g.consumer;
+  for (int j = 0; j < g.n_candidates; ++j) {
+    const int s = g.candidates[j];
+    if (s < 0 || s >= p->cap || !p->slots[s].occupied)
+      return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: candidate slot %d is empty", idx, s);
+    const SlotMeta& m = p->slots[s];
+    if (g.kind == KVCOMM_PLACEHOLDER) {
+      if (m.length < g.L_seg)
+        return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: anchor slot %d has L=%d < L_seg %d", idx, s, m.length,
+                    g.L_seg);
+      if (!(m.ph_mask & bit))
+        return fail(KVCOMM_ERR_MISSING_OFFSET, "segment %d: slot %d lacks placeholder offsets of consumer %d", idx,
+                    s, g.consumer);
+    } else if (!(m.pf_mask & bit)) {
+      return fail(KVCOMM_ERR_MISSING_OFFSET, "segment %d: slot %d lacks prefix offsets of consumer %d", idx, s,
+                  g.consumer);
+    }
+  }
+  *out_rows_len = g.L_seg;
+  return KVCOMM_OK;
+}
+
+KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
+  // shared geometry
+  kvcomm_pool_s* p0 = nullptr;
+  std::vector<std::shared_lock<std::shared_mutex>> locks;
+  std::vector<kvcomm_pool_s*> locked;
+  for (int i = 0; i < n; ++i) {
+    kvcomm_pool_s* p = segs[i].pool;
+    if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", i);
+    if (!p0) p0 = p;
+    if (p->Ls != p0->Ls || p->Hs != p0->Hs || p->d != p0->d || p->cfg.device != p0->cfg.device)
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: pool geometry differs from segment 0", i);
+    if (std::find(locked.begin(), locked.end(), p) == locked.end()) {
+      locked.push_back(p);
+      locks.emplace_back(p->mu);
+    }
+  }
+  if (!p0) return ok();
+  const int d = p0->d, Ls = p0->Ls, Hs = p0->Hs;
+  const int rpt = kStageBytes / (2 * d);
+
+  // validate, and size the work table
+  std::vector<int> live;
+  size_t n_cand_total = 0, n_wexp = 0;
+  for (int i = 0; i < n; ++i) {
+    int rows = 0;
+    KV_TRY(validate_segment(segs[i], i, &rows));
+    if (rows == 0) continue;
+    live.push_back(i);
+    n_cand_total += segs[i].n_candidates;
+    if (segs[i].kind == KVCOMM_PREFIX) n_wexp += size_t(segs[i].n_candidates) * ((segs[i].L_seg + 3) & ~3);
+  }
+  if (live.empty()) return ok();
+  const int n_seg = int(live.size());
+  TableHdr hdr{};
+  hdr.n_seg = n_seg;
+  hdr.d = d;
+  hdr.Ls = Ls;
+  hdr.Hs = Hs;
+  hdr.rows_per_tile = rpt;
+  size_t off = align_up(sizeof(TableHdr), 64);
+  hdr.seg_off = int64_t(off);
+  off = align_up(off + sizeof(SegDev) * n_seg, 64);
+  hdr.cand_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * n_cand_total, 64);
+  hdr.cs_off = int64_t(off);
+  off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
+  hdr.wexp_off = int64_t(off);
+  off = align_up(off + sizeof(float) * n_wexp, 64);
+  const size_t table_bytes = off;
+
+  const int dev = p0->cfg.device;
+  DeviceGuard guard(dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TableRing& ring = g_rings[dev & 63];
+  std::lock_guard<std::mutex> rlk(ring.mu);
+  TableRing::Entry& E = ring.e[ring.next];
+  ring.next = (ring.next + 1) % TableRing::kN;
+  if (E.used) KV_CUDA(cudaEventSynchronize(E.done));
+  if (!E.done) KV_CUDA(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming));
+  if (E.cap < table_bytes) {
+    if (E.host) cudaFreeHost(E.host);
+    if (E.dev) cudaFree(E.dev);
+    E.host = E.dev = nullptr;
+    E.cap = 0;
+    const size_t cap = std::max<size_t>(align_up(table_bytes, 1 << 16), 1 << 16);
+    if (cudaMallocHost(&E.host, cap) != cudaSuccess || cudaMalloc(&E.dev, cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KVCOMM_ERR_OUT_OF_MEMORY, "realign work table (%zu bytes)", cap);
+    }
+    E.cap = cap;
+  }
+  uint8_t* h = static_cast<uint8_t*>(E.host);
+  uint8_t* dv = static_cast<uint8_t*>(E.dev);
+  SegDev* hs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
+  int32_t* hc = reinterpret_cast<int32_t*>(h + hdr.cand_off);
+  float* dwexp = reinterpret_cast<float*>(dv + hdr.wexp_off);
+  int64_t units = 0;
+  int cand_pos = 0, wexp_pos = 0;
+  for (int t = 0; t < n_seg; ++t) {
+    const kvcomm_realign_desc& g = segs[live[t]];
+    kvcomm_pool_s* p = g.pool;
+    SegDev& x = hs[t];
+    std::memset(&x, 0, sizeof(x));
+    x.base[0] = static_cast<const bf16*>(g.base.k);
+    x.base[1] = static_cast<const bf16*>(g.base.v);
+    x.base_ld = ld_of(g.base, g.L_seg);
+    x.dst[0] = static_cast<bf16*>(g.dst_k);
+    x.dst[1] = static_cast<bf16*>(g.dst_v);
+    x.dst_ld = g.dst_ld;
+    x.dbg[0] = g.debug_delta_k;
+    x.dbg[1] = g.debug_delta_v;
+    x.inv_freq = p->inv_freq_dev;
+    x.L_seg = g.L_seg;
+    x.target_start = g.target_start;
+    x.delta = g.target_start - g.base_start;
+    x.n_cand = g.n_candidates;
+    x.cand_off = cand_pos;
+    x.cs_off = t * (d / 2);
+    x.tiles = (g.L_seg + rpt - 1) / rpt;
+    x.unit_begin = units;
+    units += int64_t(Ls) * Hs * 2 * x.tiles;
+    std::memcpy(hc + cand_pos, g.candidates, sizeof(int32_t) * g.n_candidates);
+    cand_pos += g.n_candidates;
+    if (g.kind == KVCOMM_PLACEHOLDER) {
+      x.w = g.weights;
+      x.ld_w = g.ld_w;
+      x.w_by_slot = 1;
+      x.off = p->ph_base(g.consumer);
+      x.slot_stride = p->ph_slot_stride();
+      x.plane_stride = p->ph_plane_stride();
+      x.off_ld = p->maxlen;
+    } else {
+      x.ld_w = (g.L_seg + 3) & ~3;
+      x.w = dwexp + wexp_pos;
+      x.wexp_off = wexp_pos;
+      x.wbar = g.weights;
+      x.w_by_slot = 0;
+      wexp_pos += int(x.ld_w) * g.n_candidates;
+      x.off = p->pf[g.consumer];
+      x.slot_stride = p->pf_slot_stride(g.consumer);
+      x.plane_stride = p->pf_plane_stride(g.consumer);
+      x.off_ld = p->prefix_len[g.consumer];
+    }
+  }
+  hdr.total_units = units;
+  std::memcpy(h, &hdr, sizeof(hdr));
+  KV_CUDA(cudaMemcpyAsync(E.dev, E.host, size_t(hdr.cs_off), cudaMemcpyHostToDevice, s));
+  static int grid_cache[64] = {0};
+  if (!grid_cache[dev & 63]) grid_cache[dev & 63] = realign_grid_size(dev);
+  KV_CUDA(launch_realign(E.dev, hdr, 0, grid_cache[dev & 63], s));
+  g_launches += units > 0 ? 2 : 1;
+  KV_CUDA(cudaEventRecord(E.done, s));
+  E.used = true;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, void* stream) {
+  if (!seg) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null segment");
+  return kvcomm_realign_segments(seg, 1, stream);
+}
+
+// ---- concat ------------------------------------------------------------------
+KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n, int32_t N_total,
+                                                     int32_t Ls, int32_t Hs, int32_t d, void* dst_k, void* dst_v,
+                                                     int64_t dst_ld, void* stream) {
+  if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
+  if (Ls < 1 || Hs < 1 || d < 16 || d % 16 != 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad geometry");
+  if (N_total < 0 || dst_ld < N_total) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "dst_ld %lld < N_total %d",
+                                                   (long long)dst_ld, N_total);
+  // ledger: segments tile [0, N_total) in order
+  int64_t pos = 0;
+  for (int i = 0; i < n; ++i) {
+    if (segs[i].length < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: negative length", i);
+    if (segs[i].start > pos) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (segment %d)", (long long)pos, i);
+    if (segs[i].start < pos)
+      return fail(KVCOMM_ERR_POSITION_OVERLAP, "overlap at position %d (segment %d)", segs[i].start, i);
+    pos = int64_t(segs[i].start) + segs[i].length;
+  }
+  if (pos < N_total) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (end)", (long long)pos);
+  if (pos > N_total) return fail(KVCOMM_ERR_POSITION_OVERLAP, "segments run past N_total %d", N_total);
+  if (!dst_k || !dst_v || !aligned16(dst_k) || !aligned16(dst_v))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "dst null or misaligned");
+  for (int i = 0; i < n; ++i)
+    if (segs[i].src.k && segs[i].length > 0) KV_TRY(check_view(segs[i].src, segs[i].length, "concat src"));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n; ++i) {
+    if (!segs[i].src.k || segs[i].length == 0) continue;
+    const int64_t ld = ld_of(segs[i].src, segs[i].length);
+    bf16* dk = static_cast<bf16*>(dst_k) + int64_t(segs[i].start) * d;
+    bf16* dvp = static_cast<bf16*>(dst_v) + int64_t(segs[i].start) * d;
+    KV_CUDA(launch_copy_rows(static_cast<const bf16*>(segs[i].src.k), ld, dk, dst_ld, Ls, Hs, segs[i].length, d, s));
+    KV_CUDA(launch_copy_rows(static_cast<const bf16*>(segs[i].src.v), ld, dvp, dst_ld, Ls, Hs, segs[i].length, d, s));
+    g_launches += 2;
+  }
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Internal structures shared between the C-ABI layer (kvcomm_api.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace kvc {
+
+using bf16 = __nv_bfloat16;
+
+// Bytes of data one realign pipeline stage carries (a tile of rows_per_tile token
+// rows of one (layer, head, K|V) plane): 16 KiB = 64 rows of d=128 bf16.
+constexpr int kStageBytes = 16384;
+constexpr int kStageWBytes = 2048;  // weight slice: up to kStageBytes/(2*16) floats
+constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
+constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
+
+// One segment of a realign batch, as the kernels see it (device resident).
+struct SegDev {
+  const bf16* base[2];  // K, V base rows, [Ls][Hs][base_ld][d]
+  bf16* dst[2];         // destination [Ls][Hs][dst_ld][d]
+  float* dbg[2];        // optional fp32 blended offsets [Ls][Hs][L_seg][d]
+  const float* w;       // weight rows: row r at w + r*ld_w (r = slot or j, see w_by_slot)
+  const bf16* off;      // offsets of (consumer, kind): element (slot, plane, l, h, row, e)
+  const double* inv_freq;  // [d/2] of the owning pool
+  const float* wbar;    // PREFIX: scalar weights [capacity] (expanded by the prep kernel)
+  int64_t base_ld, dst_ld, ld_w;
+  int64_t slot_stride, plane_stride, off_ld;  // elements
+  int64_t unit_begin;   // first work unit of this segment
+  int32_t L_seg, target_start, delta, n_cand;
+  int32_t cand_off;     // index of this segment's first candidate in Table::cand
+  int32_t cs_off;       // index (in float2) of its cos/sin table in Table::cs
+  int32_t w_by_slot;    // 1: weight row = slot (PLACEHOLDER W); 0: row = j (expanded w̄)
+  int32_t tiles;        // ceil(L_seg / rows_per_tile)
+  int32_t wexp_off;     // PREFIX: float offset of the expanded weights in Table::wexp
+  int32_t _pad;
+};
+
+// Device-side work table for one realign launch (lives in one contiguous buffer).
+struct TableHdr {
+  int32_t n_seg, d, Ls, Hs;
+  int32_t rows_per_tile, _pad0;
+  int64_t total_units;
+  // byte offsets from the table base
+  int64_t seg_off, cand_off, cs_off, wexp_off;
+};
+
+// Launchers (stream-ordered).  Return cudaGetLastError().
+cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int n_prefix_segments,
+                           int grid, cudaStream_t s);
+int realign_grid_size(int device);
+
+struct MatchArgs {
+  const bf16* query;    // [L_phi][De]
+  const bf16* emb;      // pool slab [cap][maxlen][De]
+  int64_t slot_stride;  // elements between slots of emb
+  const int32_t* cand;  // device [n_cand]
+  const int32_t* slot2cand;  // device [cap]: candidate index or -1
+  int32_t n_cand, cap, L_phi, De;
+  int32_t top_k;
+  int32_t scalar_mode;  // 0 Frobenius: partial = Σ d², 1 mean-ℓ2: partial = Σ d
+  float* W;             // [cap][ld_w]
+  int64_t ld_w;
+  int32_t* idx;         // [L_phi][top_k] or null
+  double* dist;         // scratch/out [n_cand][ld_d] (candidate-major)
+  int64_t ld_d;
+  double* dist_user;    // optional [cap][ld_w] user copy
+  double* partial;      // [n_blocks][n_cand]
+  int32_t* tie_count;   // device counter
+};
+
+struct MatchResultDev {
+  double entropy, threshold;
+  int32_t verdict, tie_flag, tie_count, _pad;
+};
+
+cudaError_t launch_match(const MatchArgs& a, int positions_per_block, cudaStream_t s);
+cudaError_t launch_match_finalize(const MatchArgs& a, int n_blocks, double gamma, float* wbar,
+                                  MatchResultDev* res, cudaStream_t s);
+
+// Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
+cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,
+                             int rows, int d, cudaStream_t s);
+// Contiguous copy of n bf16 elements (multiple of 8).
+cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
+// Offset measurement (insert path, step a0).
+cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
+                           const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
+                           const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld, cudaStream_t s);
+
+}  // namespace kvc

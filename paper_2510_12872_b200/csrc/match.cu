@@ -1,0 +1,259 @@
+// Anchor matching (SURVEY §8(a) a2+a3; Eq. 5, Eq. 6):
+//
+//   d[i,j]  = ‖h_φ[i] - h_ψj[i]‖₂                   i < L_φ, ψ_j ∈ 𝒜_φ (first L_φ rows, reading A8)
+//   W[j][i] = softmax_j(-d[i,j])                     (per position, reading A2; optional top-k A16)
+//   d̄_j     = sqrt(Σ_i d[i,j]²) (Frobenius, reading A4; or mean_i d[i,j]),  w̄ = softmax(-d̄),  H = -Σ w̄ log w̄,  NewAnchor ⇔ H > γ log|𝒜_φ|
+//
+// Numerics: each lane forms 8 differences of bf16 values in fp32 (exact unless the
+// exponents are >16 binades apart), squares/accumulates those 8 with fp32 FMA
+// (relative error <= 8·2^-24 on a sum of positive terms), and adds the partials in
+// fp64.  The resulting distance has a relative error below 3e-7, inside the 1e-6
+// tie band of the parity contract.  Softmax, means and entropy run in fp64 with
+// fixed-order reductions, so the verdict is deterministic run to run.
+//
+// Why not tensor cores: the distance compares row i of φ only with row i of each
+// anchor (a batched GEMV, ~0.5 FLOP/byte) — it is HBM-bound, not a dense GEMM, and
+// the ‖a‖²+‖b‖²-2a·b expansion would cancel catastrophically near ties.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cfloat>
+#include "kvcomm_internal.h"
+#include "ptx.cuh"
+
+namespace kvc {
+
+constexpr int kMatchThreads = 256;
+constexpr int kMatchWarps = kMatchThreads / 32;
+constexpr double kTieRel = 1e-6;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// (d, slot) lexicographic "less than"
+__device__ __forceinline__ bool key_less(double da, int sa, double db, int sb) {
+  return da < db || (da == db && sa < sb);
+}
+
+__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, int P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int De = a.De;
+  const int n_cand = a.n_cand;
+  bf16* q = reinterpret_cast<bf16*>(smem);
+  double* sd = reinterpret_cast<double*>(smem + ((size_t(P) * De * 2 + 15) & ~size_t(15)));
+  const int i0 = blockIdx.x * P;
+  const int np = min(P, a.L_phi - i0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // stage the query rows of this block's positions
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.query + size_t(i0) * De);
+    uint4* dst = reinterpret_cast<uint4*>(q);
+    const int nvec = np * De / 8;
+    for (int x = threadIdx.x; x < nvec; x += kMatchThreads) dst[x] = src[x];
+  }
+  __syncthreads();
+
+  // distances: one warp per (position, candidate) task
+  const int ntask = np * n_cand;
+  for (int task = warp; task < ntask; task += kMatchWarps) {
+    const int p = task / n_cand;
+    const int j = task - p * n_cand;
+    const bf16* arow = a.emb + int64_t(a.cand[j]) * a.slot_stride + int64_t(i0 + p) * De;
+    const bf16* qrow = q + size_t(p) * De;
+    double s = 0.0;
+    int e = lane * 8;
+    // 4 independent 16-byte loads in flight per lane
+    for (; e + 3 * 256 < De; e += 4 * 256) {
+      uint4 av[4], qv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = ldg128_nc(arow + e + r * 256);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) qv[r] = lds128(qrow + e + r * 256);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t aw[4] = {av[r].x, av[r].y, av[r].z, av[r].w};
+        const uint32_t qw[4] = {qv[r].x, qv[r].y, qv[r].z, qv[r].w};
+        float part = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
+          const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
+          part = fmaf(d0, d0, part);
+          part = fmaf(d1, d1, part);
+        }
+        s += double(part);
+      }
+    }
+    for (; e < De; e += 256) {
+      const uint4 av = ldg128_nc(arow + e);
+      const uint4 qv = lds128(qrow + e);
+      const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+      const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+      float part = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
+        const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
+        part = fmaf(d0, d0, part);
+        part = fmaf(d1, d1, part);
+      }
+      s += double(part);
+    }
+    s = warp_sum_d(s);
+    if (lane == 0) sd[p * n_cand + j] = sqrt(s);
+  }
+  __syncthreads();
+
+  // per-position weights (one warp per position)
+  for (int p = warp; p < np; p += kMatchWarps) {
+    const int i = i0 + p;
+    const double* dr = sd + p * n_cand;
+    for (int j = lane; j < n_cand; j += 32) {
+      a.dist[int64_t(j) * a.ld_d + i] = dr[j];
+      if (a.dist_user) a.dist_user[int64_t(a.cand[j]) * a.ld_w + i] = dr[j];
+    }
+    const bool dense = a.top_k <= 0;  // host passes the effective k = min(top_k, n_cand)
+    if (dense) {
+      double mn = DBL_MAX;
+      for (int j = lane; j < n_cand; j += 32) mn = fmin(mn, dr[j]);
+      mn = warp_min_d(mn);
+      double sum = 0.0;
+      for (int j = lane; j < n_cand; j += 32) sum += exp(-(dr[j] - mn));
+      sum = warp_sum_d(sum);
+      for (int sl = lane; sl < a.cap; sl += 32) {
+        const int j = a.slot2cand[sl];
+        a.W[int64_t(sl) * a.ld_w + i] = j >= 0 ? float(exp(-(dr[j] - mn)) / sum) : 0.f;
+      }
+    } else {
+      // top-k: k rounds of lexicographic (distance, slot) argmin over the unselected
+      const int k = a.top_k;
+      double sel_d = 0.0;   // lane r < k keeps the r-th selected distance / slot
+      int sel_s = -1;
+      double prev_d = -1.0;
+      int prev_s = -1;
+      bool tie = false;
+      double last_d = 0.0;
+      for (int r = 0; r <= k && r < n_cand; ++r) {
+        double bd = DBL_MAX;
+        int bs = INT32_MAX;
+        for (int j = lane; j < n_cand; j += 32) {
+          const double dj = dr[j];
+          const int sj = a.cand[j];
+          // unselected == strictly after (prev_d, prev_s) in the lexicographic order
+          const bool after = (prev_s < 0) || key_less(prev_d, prev_s, dj, sj);
+          if (after && key_less(dj, sj, bd, bs)) { bd = dj; bs = sj; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+          if (key_less(od, os, bd, bs)) { bd = od; bs = os; }
+        }
+        if (r > 0 && (bd - last_d) <= kTieRel * fmax(bd, 1e-300)) tie = true;
+        last_d = bd;
+        if (r == k) break;  // the (k+1)-th only serves the boundary tie test
+        if (lane == r) { sel_d = bd; sel_s = bs; }
+        prev_d = bd;
+        prev_s = bs;
+      }
+      const double mn = __shfl_sync(0xffffffffu, sel_d, 0);
+      double ev = (lane < k) ? exp(-(sel_d - mn)) : 0.0;
+      const double sum = warp_sum_d(ev);
+      for (int sl = lane; sl < a.cap; sl += 32) a.W[int64_t(sl) * a.ld_w + i] = 0.f;
+      __syncwarp();
+      if (lane < k) {
+        a.W[int64_t(sel_s) * a.ld_w + i] = float(ev / sum);
+        if (a.idx) a.idx[int64_t(i) * k + lane] = sel_s;
+      }
+      if (lane == 0 && tie) atomicAdd(a.tie_count, 1);
+    }
+  }
+
+  // deterministic per-block partial sums of distances for d̄
+  for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
+    double s = 0.0;
+    for (int p = 0; p < np; ++p) {
+      const double dv = sd[p * n_cand + j];
+      s += a.scalar_mode == 0 ? dv * dv : dv;
+    }
+    a.partial[int64_t(blockIdx.x) * n_cand + j] = s;
+  }
+}
+
+// Fixed-order tree reduction over 1024 entries in shared memory.
+template <bool kMin>
+__device__ double block_reduce_1024(double* buf, double v) {
+  const int t = threadIdx.x;
+  buf[t] = v;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (t < o) buf[t] = kMin ? fmin(buf[t], buf[t + o]) : buf[t] + buf[t + o];
+    __syncthreads();
+  }
+  const double r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) match_finalize_kernel(MatchArgs a, int n_blocks, double gamma,
+                                                              float* wbar, MatchResultDev* res) {
+  __shared__ double buf[1024];
+  __shared__ double wsh[kMaxCapDev];
+  const int j = threadIdx.x;
+  const bool valid = j < a.n_cand;
+  double dbar = 0.0;
+  if (valid) {
+    double s = 0.0;
+    for (int b = 0; b < n_blocks; ++b) s += a.partial[int64_t(b) * a.n_cand + j];
+    dbar = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
+  }
+  const double mn = block_reduce_1024<true>(buf, valid ? dbar : DBL_MAX);
+  const double e = valid ? exp(-(dbar - mn)) : 0.0;
+  const double S = block_reduce_1024<false>(buf, e);
+  const double w = e / S;
+  const double t = (valid && w > 0.0) ? -w * log(w) : 0.0;
+  const double H = block_reduce_1024<false>(buf, t);
+  if (valid) wsh[j] = w;
+  __syncthreads();
+  for (int sl = threadIdx.x; sl < a.cap; sl += blockDim.x) {
+    const int jj = a.slot2cand[sl];
+    wbar[sl] = jj >= 0 ? float(wsh[jj]) : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    const double thr = gamma * log(double(a.n_cand));
+    res->entropy = H;
+    res->threshold = thr;
+    res->verdict = H > thr ? 1 : 0;
+    res->tie_flag = fabs(H - thr) <= kTieRel * thr ? 1 : 0;
+    res->tie_count = *a.tie_count;
+  }
+}
+
+cudaError_t launch_match(const MatchArgs& a, int P, cudaStream_t s) {
+  const int n_blocks = (a.L_phi + P - 1) / P;
+  const size_t smem = ((size_t(P) * a.De * 2 + 15) & ~size_t(15)) + size_t(P) * a.n_cand * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  match_dist_kernel<<<n_blocks, kMatchThreads, smem, s>>>(a, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_match_finalize(const MatchArgs& a, int n_blocks, double gamma, float* wbar,
+                                  MatchResultDev* res, cudaStream_t s) {
+  match_finalize_kernel<<<1, 1024, 0, s>>>(a, n_blocks, gamma, wbar, res);
+  return cudaGetLastError();
+}
+
+}  // namespace kvc

@@ -1,0 +1,286 @@
+// Fused anchor-offset blend + RoPE-δ + add (SURVEY §8(a) a4+a5):
+//
+//   K̂[l,h,i,:] = R_δ( K_base[l,h,i,:] + Σ_j w[i,j] ΔK_j[l,h,i,:] )     (Eq. 6 P:289 / Eq. 7 P:297,
+//   V̂[l,h,i,:] =      V_base[l,h,i,:] + Σ_j w[i,j] ΔV_j[l,h,i,:]        alignment P:141)
+//
+// The path is pure HBM streaming: per output row it reads k offset rows + 1 base
+// row and writes 1 row, ≈ k FMAs per 2(k+2) bytes.  Design:
+//   * one persistent CTA per SM walks a static round-robin list of work units
+//     (segment, layer, head, K|V plane, 16 KiB tile of token rows);
+//   * warp 8 (one elected lane) is the TMA producer: for every unit it streams the
+//     k anchor tiles (and, for placeholders, the matching 256-byte weight slice)
+//     and finally the base tile into an NSTAGE-deep shared-memory ring with
+//     cp.async.bulk (UBLKCP) + mbarrier complete_tx, L2 evict-first;
+//   * warps 0-7 consume: each thread owns two 32-byte "items" (8 elements of the
+//     first half of a row and the matching 8 of the second half, so the
+//     rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
+//     registers, and on the base tile adds, rotates (K only) and stores bf16 (RNE)
+//     straight to the destination prompt cache.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include "kvcomm_internal.h"
+#include "ptx.cuh"
+
+namespace kvc {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kNStage = 11;
+constexpr int kItems = kStageBytes / 32;                  // 512 items of 32 B per stage
+constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);  // 2
+
+static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
+
+constexpr size_t realign_smem_bytes() {
+  return size_t(kNStage) * (kStageBytes + kStageWBytes) + 2 * kNStage * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ int find_segment(const SegDev* segs, int n_seg, int64_t u) {
+  int lo = 0, hi = n_seg - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].unit_begin <= u) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct Unit {
+  int s, l, h, p, t;
+};
+
+__device__ __forceinline__ Unit decode_unit(const SegDev* segs, int n_seg, int Hs, int64_t u) {
+  Unit r;
+  r.s = find_segment(segs, n_seg, u);
+  int64_t rem = u - segs[r.s].unit_begin;
+  const int tiles = segs[r.s].tiles;
+  r.t = int(rem % tiles);
+  rem /= tiles;
+  r.p = int(rem & 1);
+  rem >>= 1;
+  r.h = int(rem % Hs);
+  r.l = int(rem / Hs);
+  return r;
+}
+
+// Per-segment preparation: cos/sin of δ·inv_freq (fp64 angle, reading A13) and,
+// for PREFIX segments, the scalar weights w̄[cand[j]] expanded into rows of the
+// same shape as a placeholder W slice so the main kernel treats both kinds alike.
+__global__ void realign_prep_kernel(uint8_t* tab) {
+  const TableHdr* hdr = reinterpret_cast<const TableHdr*>(tab);
+  SegDev* segs = reinterpret_cast<SegDev*>(tab + hdr->seg_off);
+  const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr->cand_off);
+  float2* cs = reinterpret_cast<float2*>(tab + hdr->cs_off);
+  float* wexp = reinterpret_cast<float*>(tab + hdr->wexp_off);
+  const int s = blockIdx.x;
+  const SegDev& g = segs[s];
+  const int half = hdr->d / 2;
+  for (int f = threadIdx.x; f < half; f += blockDim.x) {
+    double sn, cn;
+    sincos(double(g.delta) * g.inv_freq[f], &sn, &cn);
+    cs[g.cs_off + f] = make_float2(float(cn), float(sn));
+  }
+  if (!g.w_by_slot) {
+    const int ld = int(g.ld_w);
+    for (int x = threadIdx.x; x < g.n_cand * ld; x += blockDim.x) {
+      const int j = x / ld;
+      wexp[g.wexp_off + x] = g.wbar[cand[g.cand_off + j]];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __restrict__ tab) {
+  const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
+  const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
+  const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr.cand_off);
+  const float2* cs = reinterpret_cast<const float2*>(tab + hdr.cs_off);
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* sdata = smem;
+  float* sw = reinterpret_cast<float*>(smem + size_t(kNStage) * kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(kNStage) * (kStageBytes + kStageWBytes));
+  uint64_t* empty = full + kNStage;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNStage; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int d = hdr.d;
+  const int Hs = hdr.Hs;
+  const int rpt = hdr.rows_per_tile;
+  const int64_t total = hdr.total_units;
+  const int row_bytes = 2 * d;
+
+  if (warp == kConsumerWarps) {
+    // ---------------- TMA producer (one lane) ----------------
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
+        const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
+        const SegDev& g = segs[un.s];
+        const int i0 = un.t * rpt;
+        const int nrows = min(rpt, g.L_seg - i0);
+        const uint32_t bytes = uint32_t(nrows) * row_bytes;
+        const uint32_t wbytes = (uint32_t(nrows) * 4u + 15u) & ~15u;
+        const int64_t lh = int64_t(un.l) * Hs + un.h;
+        for (int c = 0; c <= g.n_cand; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          uint8_t* dst = sdata + size_t(stage) * kStageBytes;
+          if (c < g.n_cand) {
+            const int slot = cand[g.cand_off + c];
+            const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
+                              (lh * g.off_ld + i0) * d;
+            const float* wsrc = g.w + int64_t(g.w_by_slot ? slot : c) * g.ld_w + i0;
+            mbar_arrive_expect_tx(&full[stage], bytes + wbytes);
+            bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
+            bulk_g2s(sw + size_t(stage) * (kStageWBytes / 4), wsrc, wbytes, &full[stage], pol_stream);
+          } else {
+            const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
+          }
+          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int vpr = d >> 4;  // items per row
+  const int ct = threadIdx.x;
+  int irow[kItemsPerThread], ivec[kItemsPerThread];
+#pragma unroll
+  for (int q = 0; q < kItemsPerThread; ++q) {
+    const int it = ct + q * kConsumerWarps * 32;
+    irow[q] = it / vpr;
+    ivec[q] = it - irow[q] * vpr;
+  }
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
+    const SegDev& g = segs[un.s];
+    const int i0 = un.t * rpt;
+    const int nrows = min(rpt, g.L_seg - i0);
+    float acc[kItemsPerThread][16];
+#pragma unroll
+    for (int q = 0; q < kItemsPerThread; ++q)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[q][e] = 0.f;
+
+    const int n_cand = g.n_cand;
+    for (int c = 0; c < n_cand; ++c) {
+      mbar_wait(&full[stage], phase);
+      const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
+      const float* wv = sw + size_t(stage) * (kStageWBytes / 4);
+#pragma unroll
+      for (int q = 0; q < kItemsPerThread; ++q) {
+        const float w = wv[irow[q]];
+        const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
+        const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+        const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[q][2 * e] = fmaf(w, bf_lo(av[e]), acc[q][2 * e]);
+          acc[q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[q][2 * e + 1]);
+          acc[q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[q][8 + 2 * e]);
+          acc[q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[q][8 + 2 * e + 1]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+    }
+
+    // base tile: add, rotate (K), round, store
+    mbar_wait(&full[stage], phase);
+    {
+      const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
+      const int64_t lh = int64_t(un.l) * Hs + un.h;
+      bf16* dst = g.dst[un.p];
+      float* dbg = g.dbg[un.p];
+#pragma unroll
+      for (int q = 0; q < kItemsPerThread; ++q) {
+        if (irow[q] >= nrows) continue;
+        const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
+        const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+        const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+        float y0[8], y1[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          y0[2 * e] = bf_lo(av[e]) + acc[q][2 * e];
+          y0[2 * e + 1] = bf_hi(av[e]) + acc[q][2 * e + 1];
+          y1[2 * e] = bf_lo(bv[e]) + acc[q][8 + 2 * e];
+          y1[2 * e + 1] = bf_hi(bv[e]) + acc[q][8 + 2 * e + 1];
+        }
+        if (un.p == 0) {
+          const float2* csr = cs + g.cs_off + ivec[q] * 8;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 r = csr[e];
+            const float x0 = y0[e], x1 = y1[e];
+            y0[e] = x0 * r.x - x1 * r.y;
+            y1[e] = x1 * r.x + x0 * r.y;
+          }
+        }
+        const int64_t orow = lh * g.dst_ld + g.target_start + i0 + irow[q];
+        bf16* o = dst + orow * d + ivec[q] * 8;
+        stg128_cs(o, make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),
+                                pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7])));
+        stg128_cs(o + d / 2, make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
+                                        pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7])));
+        if (dbg != nullptr) {
+          float* od = dbg + (lh * g.L_seg + i0 + irow[q]) * d + ivec[q] * 8;
+          float4* o0 = reinterpret_cast<float4*>(od);
+          float4* o1 = reinterpret_cast<float4*>(od + d / 2);
+          o0[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+          o0[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
+          o1[0] = make_float4(acc[q][8], acc[q][9], acc[q][10], acc[q][11]);
+          o1[1] = make_float4(acc[q][12], acc[q][13], acc[q][14], acc[q][15]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+  }
+}
+
+int realign_grid_size(int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms > 0 ? sms : 148;
+}
+
+cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int n_prefix_segments, int grid,
+                           cudaStream_t s) {
+  (void)n_prefix_segments;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(realign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(realign_smem_bytes()));
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63] = true;
+  }
+  realign_prep_kernel<<<hdr.n_seg, 128, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
+  if (hdr.total_units <= 0) return cudaGetLastError();
+  const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
+  realign_kernel<<<int(g), kThreads, realign_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(table_dev));
+  return cudaGetLastError();
+}
+
+}  // namespace kvc

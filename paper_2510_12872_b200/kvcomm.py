@@ -1,0 +1,321 @@
+"""Thin Python binding of libkvcomm (include/kvcomm.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module turns
+torch tensors into (pointer, shape, stride) arguments, allocates output buffers with
+torch (device-memory plumbing) and raises KVCommError on a non-OK status.  There is
+no CPU fallback.
+
+Tensor conventions: K/V of one model shard are bf16 CUDA tensors shaped
+[Ls, Hs, T, d] whose last two dims are dense (a token slice of a bigger cache is
+fine: the (layer, head) row stride is read from the tensor's strides).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import (ALL_CONSUMERS, NEW_ANCHOR, OFFSET_GIVEN, OFFSET_MEASURE, PLACEHOLDER, PREFIX, SHAREABLE,
+                   KVCommError)
+
+__all__ = ["AnchorPool", "OffsetGiven", "OffsetMeasure", "Match", "Segment", "realign_segments",
+           "realign_segment", "prepare_segments", "realign_prepared", "concat_prefill_cache", "kernel_launch_count", "KVCommError", "ALL_CONSUMERS",
+           "SHAREABLE", "NEW_ANCHOR", "PLACEHOLDER", "PREFIX"]
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def _rows_ld(t: torch.Tensor, what: str) -> int:
+    """Row stride (in rows) between (layer, head) blocks of a [Ls, Hs, T, d] tensor."""
+    if t.dim() != 4:
+        raise ValueError(f"{what}: expected [Ls, Hs, T, d], got {tuple(t.shape)}")
+    if not t.is_cuda or t.dtype != torch.bfloat16:
+        raise ValueError(f"{what}: expected a bf16 CUDA tensor")
+    Ls, Hs, T, d = t.shape
+    s0, s1, s2, s3 = t.stride()
+    if s3 != 1 or (T > 1 and s2 != d) or s1 % d != 0 or (Ls > 1 and s0 != Hs * s1):
+        raise ValueError(f"{what}: strides {t.stride()} are not [Ls,Hs,ld,d] row-major")
+    return s1 // d
+
+
+def _view(k: Optional[torch.Tensor], v: Optional[torch.Tensor], start: int = 0, what: str = "kv") -> L.KVView:
+    if k is None:
+        return L.KVView()
+    ld = _rows_ld(k, what + ".k")
+    if v.shape != k.shape or _rows_ld(v, what + ".v") != ld:
+        raise ValueError(f"{what}: k and v differ in shape/stride")
+    return L.KVView(k.data_ptr(), v.data_ptr(), ld, int(start), 0)
+
+
+def kernel_launch_count() -> int:
+    return int(L.lib().kvcomm_kernel_launch_count())
+
+
+@dataclass
+class OffsetGiven:
+    """Precomputed offsets of one consumer, base frame (reading A10)."""
+    consumer: int
+    dk_ph: Optional[torch.Tensor] = None   # [Ls, Hs, L_psi, d]
+    dv_ph: Optional[torch.Tensor] = None
+    dk_pf: Optional[torch.Tensor] = None   # [Ls, Hs, P_c, d]
+    dv_pf: Optional[torch.Tensor] = None
+
+    def desc(self) -> L.OffsetDesc:
+        return L.OffsetDesc(self.consumer, OFFSET_GIVEN, _view(self.dk_ph, self.dv_ph, what="dk_ph"),
+                            _view(self.dk_pf, self.dv_pf, what="dk_pf"))
+
+
+@dataclass
+class OffsetMeasure:
+    """Offsets measured on device from real (in-context) and base caches (Alg. 1).
+    Each cache is (K, V, absolute start position)."""
+    consumer: int
+    ph_real: Optional[Tuple[torch.Tensor, torch.Tensor, int]] = None
+    ph_base: Optional[Tuple[torch.Tensor, torch.Tensor, int]] = None
+    pf_real: Optional[Tuple[torch.Tensor, torch.Tensor, int]] = None
+    pf_base: Optional[Tuple[torch.Tensor, torch.Tensor, int]] = None
+
+    def desc(self) -> L.OffsetDesc:
+        d = L.OffsetDesc()
+        d.consumer = self.consumer
+        d.mode = OFFSET_MEASURE
+        if self.ph_real is not None:
+            d.ph_real = _view(*self.ph_real, what="ph_real")
+            d.ph_base = _view(*self.ph_base, what="ph_base")
+        if self.pf_real is not None:
+            d.pf_real = _view(*self.pf_real, what="pf_real")
+            d.pf_base = _view(*self.pf_base, what="pf_base")
+        return d
+
+
+@dataclass
+class Match:
+    verdict: int
+    reason: str
+    candidates: List[int]
+    top_k: int
+    entropy: float
+    threshold: float
+    verdict_in_tie_band: bool
+    tie_band_count: int
+    W: Optional[torch.Tensor] = None        # [capacity, ld_w] fp32, slot-major
+    wbar: Optional[torch.Tensor] = None     # [capacity] fp32
+    idx: Optional[torch.Tensor] = None      # [L_phi, top_k] int32
+    dist: Optional[torch.Tensor] = None     # [capacity, ld_w] fp64
+
+    @property
+    def shareable(self) -> bool:
+        return self.verdict == SHAREABLE
+
+
+class _DevView:
+    """__cuda_array_interface__ wrapper to view library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+class AnchorPool:
+    """Device-resident anchor pool of one placeholder (§3.3, Table A.1)."""
+
+    def __init__(self, *, num_layers: int, num_kv_heads: int, head_dim: int, emb_dim: int, capacity: int,
+                 max_anchor_len: int, prefix_len: Sequence[int], inv_freq, device: int = 0,
+                 layer_range: Optional[Tuple[int, int]] = None, head_range: Optional[Tuple[int, int]] = None,
+                 scalar_distance: str = "frobenius"):
+        lb, le = layer_range or (0, num_layers)
+        hb, he = head_range or (0, num_kv_heads)
+        self.Ls, self.Hs, self.d, self.De = le - lb, he - hb, head_dim, emb_dim
+        self.capacity, self.max_anchor_len = capacity, max_anchor_len
+        self.prefix_len = [int(x) for x in prefix_len]
+        self.device = torch.device("cuda", device)
+        pl = (C.c_int32 * len(self.prefix_len))(*self.prefix_len)
+        inv = np.ascontiguousarray(np.asarray(inv_freq, dtype=np.float64))
+        cfg = L.PoolConfig(device, num_layers, lb, le, num_kv_heads, hb, he, head_dim, emb_dim, capacity,
+                           max_anchor_len, len(self.prefix_len),
+                           {"frobenius": L.SCALAR_FROBENIUS, "mean_l2": L.SCALAR_MEAN_L2}[scalar_distance], pl,
+                           inv.ctypes.data_as(C.POINTER(C.c_double)))
+        h = C.c_void_p()
+        L.check(L.lib().kvcomm_anchor_pool_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self) -> int:
+        if self._h is None:
+            raise RuntimeError("pool destroyed")
+        return self._h.value
+
+    def destroy(self) -> None:
+        if self._h is not None:
+            L.check(L.lib().kvcomm_anchor_pool_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None:
+                L.lib().kvcomm_anchor_pool_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def nbytes(self) -> int:
+        b = C.c_int64()
+        L.check(L.lib().kvcomm_anchor_pool_bytes(self.handle, C.byref(b)))
+        return b.value
+
+    # -- a0 ------------------------------------------------------------------
+    def insert(self, emb: torch.Tensor, offsets: Sequence = (), stream=None) -> Tuple[int, int]:
+        if emb.dim() != 2 or emb.shape[1] != self.De or emb.dtype != torch.bfloat16 or not emb.is_contiguous():
+            raise ValueError("emb must be a contiguous bf16 [L_psi, D_e] tensor")
+        descs = (L.OffsetDesc * max(len(offsets), 1))(*[o.desc() for o in offsets])
+        slot, ev = C.c_int32(), C.c_int32()
+        L.check(L.lib().kvcomm_anchor_pool_insert(self.handle, emb.shape[0], emb.data_ptr(), descs, len(offsets),
+                                                  _stream_handle(stream), C.byref(slot), C.byref(ev)))
+        return slot.value, ev.value
+
+    def set_offsets(self, slot: int, offsets: Sequence, stream=None) -> None:
+        descs = (L.OffsetDesc * max(len(offsets), 1))(*[o.desc() for o in offsets])
+        L.check(L.lib().kvcomm_anchor_pool_set_offsets(self.handle, slot, descs, len(offsets),
+                                                       _stream_handle(stream)))
+
+    def evict(self, slot: int) -> None:
+        L.check(L.lib().kvcomm_anchor_pool_evict(self.handle, slot))
+
+    def record_access(self, slots: Sequence[int]) -> None:
+        arr = (C.c_int32 * max(len(slots), 1))(*slots)
+        L.check(L.lib().kvcomm_anchor_pool_record_access(self.handle, arr, len(slots)))
+
+    def slot_info(self, slot: int) -> dict:
+        s = L.SlotInfo()
+        L.check(L.lib().kvcomm_anchor_pool_slot_info(self.handle, slot, C.byref(s)))
+        return {"occupied": bool(s.occupied), "length": s.length, "access_count": s.access_count,
+                "insertion_index": s.insertion_index, "ph_present_mask": s.ph_present_mask,
+                "pf_present_mask": s.pf_present_mask}
+
+    def offset_view(self, slot: int, consumer: int, which: str = "ph", rows: Optional[int] = None):
+        """(ΔK, ΔV) stored for (slot, consumer) as [Ls, Hs, rows, d] bf16 views of pool memory."""
+        k, v, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
+        L.check(L.lib().kvcomm_anchor_pool_offset_view(self.handle, slot, consumer, 0 if which == "ph" else 1,
+                                                       C.byref(k), C.byref(v), C.byref(ld)))
+        rows = ld.value if rows is None else rows
+        out = []
+        for p in (k.value, v.value):
+            flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "<i2"),
+                                   device=self.device)
+            out.append(flat.view(torch.bfloat16).view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
+        return tuple(out)
+
+    # -- a1-a3 ---------------------------------------------------------------
+    def match(self, query_emb: torch.Tensor, consumer: int = ALL_CONSUMERS, gamma: float = 0.3, top_k: int = 0,
+              want_dist: bool = False, ld_w: Optional[int] = None, out: Optional[Match] = None,
+              stream=None) -> Match:
+        if query_emb.dim() != 2 or query_emb.shape[1] != self.De or query_emb.dtype != torch.bfloat16 \
+                or not query_emb.is_contiguous():
+            raise ValueError("query_emb must be a contiguous bf16 [L_phi, D_e] tensor")
+        L_phi = query_emb.shape[0]
+        if out is not None and out.W is not None:
+            W, wbar, idx, dist = out.W, out.wbar, out.idx, out.dist
+            ld_w = W.shape[1]
+        else:
+            ld_w = ld_w or ((L_phi + 3) // 4 * 4)
+            W = torch.zeros(self.capacity, ld_w, dtype=torch.float32, device=self.device)
+            wbar = torch.zeros(self.capacity, dtype=torch.float32, device=self.device)
+            idx = torch.zeros(L_phi, max(top_k, 1), dtype=torch.int32, device=self.device) if top_k else None
+            dist = torch.zeros(self.capacity, ld_w, dtype=torch.float64, device=self.device) if want_dist else None
+        info = L.MatchInfo()
+        L.check(L.lib().kvcomm_match_anchors(self.handle, query_emb.data_ptr(), L_phi, consumer, float(gamma),
+                                             int(top_k), W.data_ptr(), ld_w,
+                                             idx.data_ptr() if idx is not None else None, wbar.data_ptr(),
+                                             dist.data_ptr() if dist is not None else None, C.byref(info),
+                                             _stream_handle(stream)))
+        cands = list(info.candidates[: info.n_candidates])
+        if idx is not None and info.top_k < idx.shape[1] and info.n_candidates > 0:
+            idx = idx.view(-1)[: L_phi * info.top_k].view(L_phi, info.top_k)
+        return Match(info.verdict, L.REASONS[info.reason], cands, info.top_k, info.entropy, info.threshold,
+                     bool(info.verdict_in_tie_band), info.tie_band_count, W, wbar, idx, dist)
+
+
+@dataclass
+class Segment:
+    """One segment to realign (Eq. 6 placeholder / Eq. 7 prefix + RoPE δ)."""
+    pool: AnchorPool
+    consumer: int
+    kind: int                         # PLACEHOLDER | PREFIX
+    weights: torch.Tensor             # PLACEHOLDER: Match.W [capacity, ld_w]; PREFIX: Match.wbar [capacity]
+    candidates: Sequence[int]
+    base_k: torch.Tensor              # [Ls, Hs, >=L_seg, d]
+    base_v: torch.Tensor
+    base_start: int
+    target_start: int
+    dst_k: torch.Tensor               # [Ls, Hs, N, d]
+    dst_v: torch.Tensor
+    L_seg: Optional[int] = None
+    debug_k: Optional[torch.Tensor] = None   # fp32 [Ls, Hs, L_seg, d]
+    debug_v: Optional[torch.Tensor] = None
+
+    def desc(self, keep: list) -> L.RealignDesc:
+        L_seg = self.base_k.shape[2] if self.L_seg is None else self.L_seg
+        cand = (C.c_int32 * max(len(self.candidates), 1))(*self.candidates)
+        keep.append(cand)
+        if self.weights.dtype != torch.float32 or not self.weights.is_cuda:
+            raise ValueError("weights must be fp32 CUDA")
+        ld_w = self.weights.shape[1] if self.kind == PLACEHOLDER else 0
+        dst_ld = _rows_ld(self.dst_k, "dst_k")
+        if _rows_ld(self.dst_v, "dst_v") != dst_ld:
+            raise ValueError("dst_k/dst_v strides differ")
+        for t in (self.debug_k, self.debug_v):
+            if t is not None and (t.dtype != torch.float32 or not t.is_contiguous()):
+                raise ValueError("debug buffers must be contiguous fp32")
+        return L.RealignDesc(self.pool.handle, self.consumer, self.kind, self.weights.data_ptr(), ld_w, cand,
+                             len(self.candidates), L_seg, _view(self.base_k, self.base_v, what="base"),
+                             self.base_start, self.target_start, self.dst_k.data_ptr(), self.dst_v.data_ptr(),
+                             dst_ld, self.debug_k.data_ptr() if self.debug_k is not None else None,
+                             self.debug_v.data_ptr() if self.debug_v is not None else None)
+
+
+@dataclass
+class PreparedSegments:
+    """Marshalled descriptor array (host work done ahead of the launch)."""
+    arr: object
+    n: int
+    keep: list
+
+
+def prepare_segments(segs: Sequence[Segment]) -> PreparedSegments:
+    keep: list = []
+    arr = (L.RealignDesc * max(len(segs), 1))(*[s.desc(keep) for s in segs])
+    return PreparedSegments(arr, len(segs), keep)
+
+
+def realign_prepared(prep: PreparedSegments, stream=None) -> None:
+    L.check(L.lib().kvcomm_realign_segments(prep.arr, prep.n, _stream_handle(stream)))
+
+
+def realign_segments(segs: Sequence[Segment], stream=None) -> None:
+    """All segments in one persistent-kernel launch (kvcomm_realign_segments)."""
+    realign_prepared(prepare_segments(segs), stream)
+
+
+def realign_segment(seg: Segment, stream=None) -> None:
+    keep: list = []
+    d = seg.desc(keep)
+    L.check(L.lib().kvcomm_realign_segment(C.byref(d), _stream_handle(stream)))
+
+
+def concat_prefill_cache(parts: Sequence[Tuple[int, int, Optional[torch.Tensor], Optional[torch.Tensor]]],
+                         N_total: int, dst_k: torch.Tensor, dst_v: torch.Tensor, stream=None) -> None:
+    """parts: (start, length, src_k, src_v); src None = rows already in place (realigned)."""
+    Ls, Hs, _, d = dst_k.shape
+    dst_ld = _rows_ld(dst_k, "dst_k")
+    refs = (L.SegmentRef * max(len(parts), 1))()
+    for i, (start, length, sk, sv) in enumerate(parts):
+        refs[i] = L.SegmentRef(int(start), int(length), _view(sk, sv, what="concat src"))
+    L.check(L.lib().kvcomm_concat_prefill_cache(refs, len(parts), N_total, Ls, Hs, d, dst_k.data_ptr(),
+                                                dst_v.data_ptr(), dst_ld, _stream_handle(stream)))

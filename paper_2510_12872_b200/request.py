@@ -1,0 +1,108 @@
+"""Algorithm 1's reuse branch for all agents of one request.
+
+For every placeholder pool the sample is matched once (weights depend only on the
+sample and the pool, reading A21); every agent whose placeholders are all
+Shareable gets all its placeholder and prefix segments realigned in ONE persistent
+kernel launch (kvcomm_realign_segments), then its p_(m,0) rows are copied and the
+position ledger is checked (kvcomm_concat_prefill_cache).  Agents with any
+NewAnchor verdict take the dense fallback, which needs the model and is
+outside this library: they are reported, not processed.
+
+Host bookkeeping only; all arithmetic runs in libkvcomm's kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import torch
+
+from . import kvcomm as K
+
+
+@dataclass
+class SegmentLayout:
+    kind: int                    # K.PLACEHOLDER | K.PREFIX
+    pool: str                    # placeholder (pool) name this segment belongs to
+    consumer: int                # consumer index of this (agent, slot) in the pool
+    base_k: torch.Tensor         # [Ls, Hs, L_seg, d]
+    base_v: torch.Tensor
+    base_start: int
+    target_start: int
+
+
+@dataclass
+class AgentLayout:
+    agent: int
+    N: int                       # prompt length
+    p0_k: torch.Tensor           # [Ls, Hs, |p_(m,0)|, d]  system prompt cache (copied verbatim)
+    p0_v: torch.Tensor
+    segments: List[SegmentLayout]
+    dst_k: torch.Tensor          # [Ls, Hs, N, d]
+    dst_v: torch.Tensor
+
+
+@dataclass
+class RequestResult:
+    matches: Dict[str, K.Match]
+    reused_agents: List[int]
+    fallback_agents: List[int]
+    realigned_tokens: int
+    blended_rows: int            # Σ_segments n_candidates * L_seg (for the byte model)
+
+
+class ReuseRequest:
+    def __init__(self, pools: Dict[str, K.AnchorPool], agents: List[AgentLayout], gamma: float = 0.3,
+                 top_k: int = 0):
+        self.pools, self.agents, self.gamma, self.top_k = pools, agents, gamma, top_k
+        self._match_out: Dict[str, Optional[K.Match]] = {n: None for n in pools}
+
+    def match(self, queries: Dict[str, torch.Tensor], stream=None) -> Dict[str, K.Match]:
+        out = {}
+        for name, q in queries.items():
+            m = self.pools[name].match(q, consumer=K.ALL_CONSUMERS, gamma=self.gamma, top_k=self.top_k,
+                                       out=self._match_out[name], stream=stream)
+            self._match_out[name] = m
+            out[name] = m
+        return out
+
+    def segments(self, matches: Dict[str, K.Match]):
+        segs, reused, fallback, toks, rows = [], [], [], 0, 0
+        for a in self.agents:
+            names = {s.pool for s in a.segments}
+            if not all(matches[n].shareable for n in names):
+                fallback.append(a.agent)
+                continue
+            reused.append(a.agent)
+            for s in a.segments:
+                m = matches[s.pool]
+                w = m.W if s.kind == K.PLACEHOLDER else m.wbar
+                segs.append(K.Segment(self.pools[s.pool], s.consumer, s.kind, w, m.candidates, s.base_k, s.base_v,
+                                      s.base_start, s.target_start, a.dst_k, a.dst_v))
+                toks += s.base_k.shape[2]
+                rows += s.base_k.shape[2] * len(m.candidates)
+        return segs, reused, fallback, toks, rows
+
+    def realign(self, segs, stream=None) -> None:
+        K.realign_segments(segs, stream=stream)
+
+    def concat(self, reused: List[int], stream=None) -> None:
+        for a in self.agents:
+            if a.agent not in reused:
+                continue
+            p0 = a.p0_k.shape[2]
+            parts = [(0, p0, a.p0_k, a.p0_v)]
+            for s in sorted(a.segments, key=lambda s: s.target_start):
+                parts.append((s.target_start, s.base_k.shape[2], None, None))
+            K.concat_prefill_cache(parts, a.N, a.dst_k, a.dst_v, stream=stream)
+
+    def run(self, queries: Dict[str, torch.Tensor], stream=None) -> RequestResult:
+        matches = self.match(queries, stream)
+        segs, reused, fallback, toks, rows = self.segments(matches)
+        if segs:
+            self.realign(segs, stream)
+        self.concat(reused, stream)
+        for name, m in matches.items():            # reading A18: +1 per Shareable turn
+            if m.shareable:
+                self.pools[name].record_access(m.candidates)
+        return RequestResult(matches, reused, fallback, toks, rows)

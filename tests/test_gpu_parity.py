@@ -1,0 +1,225 @@
+"""CUDA path vs CPU oracle, element by element, through the C ABI (-m gpu).
+
+Sizes are small enough for the oracle to finish in seconds yet span several
+16 KiB tiles and a ragged tail; edge cases cover the degenerate inputs of the
+method.  Full-size (BASELINE configs[1]) sampled parity lives in
+test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import kvcomm_oracle as O
+from tests import harness
+
+pytestmark = pytest.mark.gpu
+
+K = None
+
+
+def setup_module(module):
+    global K
+    assert torch.cuda.is_available(), "gpu tests need CUDA"
+    from paper_2510_12872_b200 import kvcomm as _K
+    module.K = _K
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("gamma", [0.3, 0.9])
+@pytest.mark.parametrize("scalar", ["frobenius", "mean_l2"])
+def test_tiny_config_full_parity(seed, gamma, scalar):
+    p = synth.tiny_problem(seed)
+    gpu = harness.run_gpu(p, gamma=gamma, scalar=scalar)
+    ora = harness.run_oracle(p, gamma=gamma, scalar=scalar)
+    harness.compare(gpu, ora, p)
+
+
+@pytest.mark.parametrize("d,De,L_phi,P", [(128, 256, 150, 37), (64, 64, 300, 5), (256, 128, 70, 64),
+                                          (16, 32, 600, 3), (128, 4096, 64, 32)])
+def test_medium_multi_tile_ragged(d, De, L_phi, P):
+    g = np.random.default_rng(d + L_phi)
+    lens = [L_phi + int(x) for x in g.integers(0, 65, size=6)]
+    p = synth.make_problem(11, L=3, H=2, d=d, D_e=De, L_phi=L_phi, anchor_lens=lens, prefix_lens=[P],
+                           target_start=77, pf_base_start=200, pf_target_start=[77 + L_phi],
+                           inv_freq=synth.llama3_inv_freq(d))
+    gpu = harness.run_gpu(p, gamma=1.0)
+    ora = harness.run_oracle(p, gamma=1.0)
+    harness.compare(gpu, ora, p)
+
+
+def test_negative_delta_and_large_positions():
+    p = synth.make_problem(5, L=2, H=2, d=128, D_e=64, L_phi=65, anchor_lens=[65, 80, 90], prefix_lens=[32],
+                           target_start=8100, pf_base_start=9000, pf_target_start=[8165],
+                           inv_freq=synth.llama3_inv_freq(128))
+    gpu = harness.run_gpu(p, gamma=1.0)
+    ora = harness.run_oracle(p, gamma=1.0)
+    harness.compare(gpu, ora, p)
+
+
+@pytest.mark.parametrize("top_k", [1, 3, 8])
+def test_topk_indices_outside_tie_band(top_k):
+    # query = anchor 0 with swaps: exact zero distances and ties between identical rows
+    p = synth.make_problem(7, L=2, H=2, d=64, D_e=64, L_phi=100, anchor_lens=[100] * 10, prefix_lens=[16],
+                           target_start=12, pf_base_start=12, inv_freq=synth.llama3_inv_freq(64), n_vocab=32)
+    gpu = harness.run_gpu(p, gamma=1.0, top_k=top_k)
+    ora = harness.run_oracle(p, gamma=1.0, top_k=top_k)
+    stats = harness.compare(gpu, ora, p)
+    # the small vocabulary makes many rows identical across anchors -> exact ties,
+    # which the (distance, slot) order resolves identically on both sides
+    assert "idx_tie_positions" in stats
+
+
+def test_exact_single_anchor_returns_its_offset():
+    p = synth.make_problem(3, L=2, H=2, d=128, D_e=64, L_phi=70, anchor_lens=[70], prefix_lens=[8],
+                           target_start=30, pf_base_start=30, p_swap=0.0)
+    gpu = harness.run_gpu(p, gamma=0.3)
+    m = gpu["match"]
+    assert m.shareable and m.candidates == [0] and m.entropy == 0.0
+    assert torch.all(m.W[0, :70] == 1.0)
+    # blended offset equals the stored offset exactly (weight exactly 1)
+    assert torch.equal(gpu["dbg_k"], p.dk_ph[0][0].float())
+    assert torch.equal(gpu["dbg_v"], p.dv_ph[0][0].float())
+    ora = harness.run_oracle(p, gamma=0.3)
+    harness.compare(gpu, ora, p)
+
+
+def test_unchanged_prefix_reproduces_identical_cache():
+    dev = torch.device("cuda", 0)
+    L_, H, d, De, T = 2, 2, 128, 64, 100
+    g = synth.make_gen(9)
+    pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=De, capacity=3, max_anchor_len=T,
+                        prefix_len=[0], inv_freq=synth.llama3_inv_freq(d))
+    z = torch.zeros(L_, H, T, d, dtype=torch.bfloat16, device=dev)
+    emb = [synth.randn_bf16((T, De), g).to(dev) for _ in range(3)]
+    for e in emb:
+        pool.insert(e, [K.OffsetGiven(0, z, z, z[:, :, :0], z[:, :, :0])])
+    m = pool.match(emb[1], consumer=0, gamma=1.0)
+    base_k = synth.randn_bf16((L_, H, T, d), g).to(dev)
+    base_v = synth.randn_bf16((L_, H, T, d), g).to(dev)
+    dk = torch.empty_like(base_k)
+    dv = torch.empty_like(base_v)
+    K.realign_segment(K.Segment(pool, 0, K.PLACEHOLDER, m.W, m.candidates, base_k, base_v, 0, 0, dk, dv))
+    torch.cuda.synchronize()
+    assert torch.equal(dk, base_k) and torch.equal(dv, base_v)
+
+
+def test_measure_insert_matches_oracle():
+    dev = torch.device("cuda", 0)
+    L_, H, d, De, T, P = 2, 3, 128, 64, 90, 20
+    inv = synth.llama3_inv_freq(d)
+    g = synth.make_gen(21)
+    t = lambda n: synth.randn_bf16((L_, H, n, d), g)
+    kr, vr, kb, vb = t(T), t(T), t(T), t(T)
+    pkr, pvr, pkb, pvb = t(P), t(P), t(P), t(P)
+    pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=De, capacity=2, max_anchor_len=T + 5,
+                        prefix_len=[P], inv_freq=inv)
+    off = K.OffsetMeasure(0, ph_real=(kr.to(dev), vr.to(dev), 731), ph_base=(kb.to(dev), vb.to(dev), 0),
+                          pf_real=(pkr.to(dev), pvr.to(dev), 731 + T), pf_base=(pkb.to(dev), pvb.to(dev), 40))
+    slot, ev = pool.insert(synth.randn_bf16((T, De), g).to(dev), [off])
+    torch.cuda.synchronize()
+    for which, (a, b, c_, d_, sr, sb, n) in {"ph": (kr, vr, kb, vb, 731, 0, T),
+                                             "pf": (pkr, pvr, pkb, pvb, 731 + T, 40, P)}.items():
+        gk, gv = pool.offset_view(slot, 0, which, rows=n)
+        odk, odv = O.measure_offset(harness.f64(a), harness.f64(b), sr, harness.f64(c_), harness.f64(d_), sb, inv)
+        harness.check_kv(harness.f64(gk), O.bf16_round(odk), np.zeros_like(odk),
+                         np.abs(harness.f64(a)) + np.abs(harness.f64(c_)), f"measured ΔK {which}")
+        # ΔV: a difference of two bf16 values, rounded once -> bit-exact
+        assert np.array_equal(harness.f64(gv), O.bf16_round(odv)), which
+
+
+def test_error_contracts():
+    dev = torch.device("cuda", 0)
+    p = synth.tiny_problem(1)
+    pool = K.AnchorPool(num_layers=p.L, num_kv_heads=p.H, head_dim=p.d, emb_dim=p.D_e, capacity=4,
+                        max_anchor_len=48, prefix_len=[4, 4], inv_freq=p.inv_freq)
+    q = p.emb_query.to(dev)
+    assert pool.match(q, gamma=0.3).reason == "EMPTY_POOL"
+    # anchor 0 has offsets for consumer 0 only
+    s0, _ = pool.insert(p.emb_anchor[0].to(dev), [K.OffsetGiven(0, p.dk_ph[0][0].to(dev), p.dv_ph[0][0].to(dev),
+                                                                p.dk_pf[0][0].to(dev), p.dv_pf[0][0].to(dev))])
+    assert pool.match(q, consumer=1, gamma=0.3).reason == "NO_CANDIDATES"
+    assert pool.match(q, consumer=K.ALL_CONSUMERS, gamma=0.3).reason == "NO_CANDIDATES"
+    m = pool.match(q, consumer=0, gamma=0.3)
+    assert m.candidates == [s0] and m.shareable
+    long_q = torch.cat([q, q], 0)
+    assert pool.match(long_q, consumer=0, gamma=0.3).reason == "TOO_LONG"
+    with pytest.raises(K.KVCommError, match="INVALID_ARGUMENT"):
+        pool.match(q, consumer=0, gamma=1.5)
+    dst = torch.zeros(p.L, p.H, 64, p.d, dtype=torch.bfloat16, device=dev)
+    bk, bv = p.base_k.to(dev), p.base_v.to(dev)
+    with pytest.raises(K.KVCommError, match="MISSING_OFFSET"):
+        K.realign_segment(K.Segment(pool, 1, K.PLACEHOLDER, m.W, [s0], bk, bv, 0, 8, dst, dst.clone()))
+    with pytest.raises(K.KVCommError, match="NO_CANDIDATES"):
+        K.realign_segment(K.Segment(pool, 0, K.PLACEHOLDER, m.W, [], bk, bv, 0, 8, dst, dst.clone()))
+    with pytest.raises(K.KVCommError, match="SHAPE_MISMATCH"):   # prefix length must equal prefix_len
+        K.realign_segment(K.Segment(pool, 0, K.PREFIX, m.wbar, [s0], bk, bv, 8, 40, dst, dst.clone()))
+    with pytest.raises(K.KVCommError, match="SHAPE_MISMATCH"):   # rows past the destination
+        K.realign_segment(K.Segment(pool, 0, K.PLACEHOLDER, m.W, [s0], bk, bv, 0, 40, dst, dst.clone()))
+    with pytest.raises(K.KVCommError, match="NOT_FOUND"):
+        pool.evict(3)
+    # a zero-length segment is a no-op
+    before = dst.clone()
+    K.realign_segment(K.Segment(pool, 0, K.PLACEHOLDER, m.W, [s0], bk, bv, 0, 8, dst, dst.clone(), L_seg=0))
+    torch.cuda.synchronize()
+    assert torch.equal(dst, before)
+
+
+def test_lfu_eviction_matches_oracle_model():
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(0)
+    pool = K.AnchorPool(num_layers=1, num_kv_heads=1, head_dim=16, emb_dim=8, capacity=5, max_anchor_len=8,
+                        prefix_len=[1], inv_freq=synth.plain_inv_freq(16))
+    model = O.PoolModel(5)
+    emb = torch.zeros(4, 8, dtype=torch.bfloat16, device=dev)
+    for step in range(60):
+        s_gpu, ev_gpu = pool.insert(emb, [])
+        s_ora, ev_ora = model.insert(4)
+        assert (s_gpu, ev_gpu) == (s_ora, ev_ora), step
+        acc = [int(x) for x in rng.choice(sorted(model.slot_len), size=int(rng.integers(0, 4)))]
+        pool.record_access(acc)
+        model.record_access(acc)
+        if step % 17 == 16:
+            victim = sorted(model.slot_len)[0]
+            pool.evict(victim)
+            model.evict(victim)
+    for s in range(5):
+        info = pool.slot_info(s)
+        assert info["occupied"] == (s in model.slot_len)
+        if info["occupied"]:
+            assert info["access_count"] == model.access[s]
+
+
+def test_determinism_and_batch_equals_single_and_layer_sharding():
+    """T2: realigning layer shards separately gives the unsharded result bitwise;
+    one batched launch equals per-segment launches; repeated runs are identical."""
+    dev = torch.device("cuda", 0)
+    p = synth.make_problem(13, L=4, H=2, d=128, D_e=128, L_phi=130, anchor_lens=[130, 140, 150, 190],
+                           prefix_lens=[32], target_start=50, pf_base_start=50, inv_freq=synth.llama3_inv_freq(128))
+    full1 = harness.run_gpu(p, gamma=1.0)
+    full2 = harness.run_gpu(p, gamma=1.0)
+    assert torch.equal(full1["dst_k"], full2["dst_k"]) and torch.equal(full1["dst_v"], full2["dst_v"])
+    assert full1["match"].entropy == full2["match"].entropy
+    # layer shards [0,2) and [2,4) as separate pools
+    for lb, le in [(0, 2), (2, 4)]:
+        pool = K.AnchorPool(num_layers=4, num_kv_heads=2, head_dim=128, emb_dim=128, capacity=4,
+                            max_anchor_len=190, prefix_len=[32], inv_freq=p.inv_freq, layer_range=(lb, le))
+        for j in range(4):
+            pool.insert(p.emb_anchor[j].to(dev), [K.OffsetGiven(0, p.dk_ph[0][j][lb:le].to(dev),
+                                                                p.dv_ph[0][j][lb:le].to(dev),
+                                                                p.dk_pf[0][j][lb:le].to(dev),
+                                                                p.dv_pf[0][j][lb:le].to(dev))])
+        m = pool.match(p.emb_query.to(dev), consumer=0, gamma=1.0)
+        assert torch.equal(m.W.cpu(), full1["match"].W.cpu())
+        N = full1["N"]
+        dk = torch.zeros(le - lb, 2, N, 128, dtype=torch.bfloat16, device=dev)
+        dv = torch.zeros_like(dk)
+        segs = [K.Segment(pool, 0, K.PLACEHOLDER, m.W, m.candidates, p.base_k[lb:le].to(dev),
+                          p.base_v[lb:le].to(dev), 0, 50, dk, dv),
+                K.Segment(pool, 0, K.PREFIX, m.wbar, m.candidates, p.pf_base_k[0][lb:le].to(dev),
+                          p.pf_base_v[0][lb:le].to(dev), 50, 180, dk, dv)]
+        for s in segs:   # one launch per segment
+            K.realign_segment(s)
+        torch.cuda.synchronize()
+        assert torch.equal(dk[:, :, 50:].cpu(), full1["dst_k"][lb:le, :, 50:])
+        assert torch.equal(dv[:, :, 50:].cpu(), full1["dst_v"][lb:le, :, 50:])
