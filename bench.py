@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true",
+                    help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
+                         "(for ncu --profile-from-start off); prints no bench line")
     return ap.parse_args()
 
 
@@ -264,27 +267,36 @@ def main():
 
     def step(time_realign=False):
         ms = req.match(st.queries, stream)
-        segs, reused, fallback, toks, rows = req.segments(ms)
-        prep = kv.kvcomm.prepare_segments(segs)   # host marshalling before the event
+        segs, reused, fallback, toks, rows, copied = req.segments(ms)
+        req.check_ledger(reused, stream)           # host-only position ledger (a6)
+        prep = kv.prepare_segments(segs)          # host marshalling before the event
         if time_realign:
             ev_r0.record(stream)
-        kv.kvcomm.realign_prepared(prep, stream)
+        kv.realign_prepared(prep, stream)         # a4+a5 for every segment + p_(m,0) copies: ONE launch
         if time_realign:
             ev_r1.record(stream)
-        req.concat(reused, stream)
         if world > 1:
             shard.gather_to_consumers([a.agent for a in st.agents], [(a.dst_k, a.dst_v) for a in st.agents],
                                       full, w.L, rank, world)
-        info.update(toks=toks, rows=rows, reused=reused, fallback=fallback, n_seg=len(segs))
+        info.update(toks=toks, rows=rows, copied=copied, reused=reused, fallback=fallback, n_seg=len(segs))
         return toks
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.profiler.start()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"profile_steps": args.steps, "segments": info["n_seg"], "rows": info["rows"]}))
+        return
     if info["fallback"]:
         raise SystemExit(f"agents {info['fallback']} took the fallback branch; the bench needs all Shareable")
     # per-launch realign bytes: (k + 2) rows of d*2 bytes per (token, layer, head, plane)
-    alg_bytes = (info["rows"] + 2 * info["toks"]) * Ls * row_bytes * 2
+    # + the p_(m,0) rows the same launch copies (read + write)
+    alg_bytes = (info["rows"] + 2 * info["toks"] + 2 * info["copied"]) * Ls * row_bytes * 2
 
     if world > 1:
         dist.barrier()
@@ -379,7 +391,7 @@ def main():
                        "realigned_tokens_per_step": total_tokens, "anchors_blended": w.capacity,
                        "gamma": args.gamma, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
                        "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed},
-            "roofline": {"kernel": "kvc::realign_kernel (+prep)", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": "kvc::realign_kernel (+prep; realign of 30 segments + 5 p0 copies)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,

@@ -75,7 +75,9 @@ typedef enum {
 } kvcomm_reason;
 
 typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_scalar_distance;
-typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1 } kvcomm_segment_kind;
+/* COPY: rows copied verbatim (no offsets, no rotation; bit-exact), e.g. p_(m,0) of the
+ * concatenation (reading A20) riding in the same launch as the realignment. */
+typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1, KVCOMM_COPY = 2 } kvcomm_segment_kind;
 typedef enum { KVCOMM_OFFSET_GIVEN = 0, KVCOMM_OFFSET_MEASURE = 1 } kvcomm_offset_mode;
 
 typedef struct kvcomm_pool_s* kvcomm_pool_t;
@@ -153,7 +155,9 @@ typedef struct {
  * segment uses weights W[slot][i].  PREFIX (Eq. 7, reading A3): every token uses
  * the scalar w̄[slot].  Output rows target_start .. target_start+L_seg-1 of dst:
  *   K̂ = R_δ(K_base + Σ_j w_j ΔK_j),  V̂ = V_base + Σ_j w_j ΔV_j,  δ = target_start - base_start,
- * accumulated in fp32, rounded once (RNE) to bf16. */
+ * accumulated in fp32, rounded once (RNE) to bf16.
+ * COPY: base rows are copied to dst unchanged; consumer/weights/candidates/base_start
+ * are ignored (pool only supplies the geometry and device). */
 typedef struct {
   kvcomm_pool_t pool;
   int32_t consumer;        /* 0..num_consumers-1                                          */
@@ -249,6 +253,28 @@ KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t pool, const void* qu
                                               int32_t* idx, float* wbar, double* dist,
                                               kvcomm_match_info* info, void* stream);
 
+/* Several matches with ONE device synchronisation (e.g. every placeholder pool of a
+ * request, Alg. 1 P:765 evaluates Eq. 5 for all placeholders before branching).
+ * Each request has the arguments of kvcomm_match_anchors; every pool may appear at
+ * most once per batch (its scratch is reused).  On error no info is valid. */
+typedef struct {
+  kvcomm_pool_t pool;
+  const void* query_emb;
+  int32_t L_phi;
+  int32_t consumer;
+  float gamma;
+  int32_t top_k;
+  float* W;
+  int64_t ld_w;
+  int32_t* idx;
+  float* wbar;
+  double* dist;
+  kvcomm_match_info* info;   /* host, filled on return */
+} kvcomm_match_request;
+
+KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* reqs, int32_t n,
+                                                    void* stream);
+
 /* ---- a4-a5: fused blend + RoPE-δ + add ------------------------------------ */
 KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, void* stream);
 /* All segments of one request in ONE persistent kernel launch.  Segments may come
@@ -259,11 +285,12 @@ KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs
 /* ---- a6: concatenation + ledger ------------------------------------------- */
 /* Checks that segs tile [0, N_total) in order (POSITION_GAP / POSITION_OVERLAP
  * otherwise, nothing launched) and copies the rows of segments with src.k != NULL
- * into dst [Ls][Hs][dst_ld][d] (dst_ld >= N_total). */
+ * into dst [Ls][Hs][dst_ld][d] (dst_ld >= N_total) with the realign kernel's TMA ring
+ * (one launch).  `device` = CUDA device of dst. */
 KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n,
                                                      int32_t N_total, int32_t Ls, int32_t Hs,
                                                      int32_t d, void* dst_k, void* dst_v,
-                                                     int64_t dst_ld, void* stream);
+                                                     int64_t dst_ld, int32_t device, void* stream);
 
 #ifdef __cplusplus
 }

@@ -4,9 +4,10 @@ The compute lives in lib/libkvcomm.so (hand-written sm_100a CUDA behind the C AB
 in include/kvcomm.h); `kvcomm` is the thin ctypes binding.  Importing this package
 fails loudly if the library has not been built.
 """
-from .kvcomm import (ALL_CONSUMERS, NEW_ANCHOR, PLACEHOLDER, PREFIX, SHAREABLE, AnchorPool, KVCommError,  # noqa
-                     Match, OffsetGiven, OffsetMeasure, Segment, concat_prefill_cache, kernel_launch_count,
-                     realign_segment, realign_segments)
+from .kvcomm import (ALL_CONSUMERS, COPY, NEW_ANCHOR, PLACEHOLDER, PREFIX, SHAREABLE, AnchorPool,  # noqa
+                     KVCommError, Match, OffsetGiven, OffsetMeasure, Segment, concat_prefill_cache,
+                     kernel_launch_count, match_many, prepare_segments, realign_prepared, realign_segment,
+                     realign_segments)
 from ._lib import LIB_PATH, lib as _load_lib  # noqa: F401
 
 _load_lib()  # load now: no silent fallback path exists

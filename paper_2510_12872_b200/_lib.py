@@ -22,7 +22,7 @@ STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE_MISMATCH", "NO_CANDIDATES", "MI
                 "POSITION_GAP", "POSITION_OVERLAP", "NOT_FOUND", "OUT_OF_MEMORY", "CUDA", "NCCL"]
 SHAREABLE, NEW_ANCHOR = 0, 1
 REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY"]
-PLACEHOLDER, PREFIX = 0, 1
+PLACEHOLDER, PREFIX, COPY = 0, 1, 2
 OFFSET_GIVEN, OFFSET_MEASURE = 0, 1
 SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1
 
@@ -65,6 +65,12 @@ class RealignDesc(C.Structure):
                 ("debug_delta_k", C.c_void_p), ("debug_delta_v", C.c_void_p)]
 
 
+class MatchRequest(C.Structure):
+    _fields_ = [("pool", C.c_void_p), ("query_emb", C.c_void_p), ("L_phi", C.c_int32), ("consumer", C.c_int32),
+                ("gamma", C.c_float), ("top_k", C.c_int32), ("W", C.c_void_p), ("ld_w", C.c_int64),
+                ("idx", C.c_void_p), ("wbar", C.c_void_p), ("dist", C.c_void_p), ("info", C.POINTER(MatchInfo))]
+
+
 class SegmentRef(C.Structure):
     _fields_ = [("start", C.c_int32), ("length", C.c_int32), ("src", KVView)]
 
@@ -90,10 +96,12 @@ _SIGS = {
     "kvcomm_match_anchors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_int32,
                                        C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(MatchInfo), C.c_void_p]),
+    "kvcomm_match_anchors_batch": (C.c_int, [C.POINTER(MatchRequest), C.c_int32, C.c_void_p]),
     "kvcomm_realign_segment": (C.c_int, [C.POINTER(RealignDesc), C.c_void_p]),
     "kvcomm_realign_segments": (C.c_int, [C.POINTER(RealignDesc), C.c_int32, C.c_void_p]),
     "kvcomm_concat_prefill_cache": (C.c_int, [C.POINTER(SegmentRef), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                              C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+                                              C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                              C.c_void_p]),
 }
 
 

@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <shared_mutex>
 #include <string>
@@ -86,6 +87,8 @@ struct SlotMeta {
 struct kvcomm_pool_s {
   kvcomm_pool_config cfg{};
   int Ls = 0, Hs = 0, d = 0, De = 0, cap = 0, maxlen = 0, C = 0;
+  int ph_ld = 0;            // rows per (layer, head) block of a stored placeholder offset (>= maxlen)
+  int64_t slot_pad = 0;     // extra elements between slots (breaks power-of-two strides)
   std::vector<int32_t> prefix_len;
   std::vector<double> inv_freq;
   // device slabs
@@ -94,23 +97,15 @@ struct kvcomm_pool_s {
   std::vector<bf16*> pf;               // per consumer: [cap][2][Ls][Hs][P_c][d]
   double* inv_freq_dev = nullptr;
   // match scratch
-  int32_t* d_cand = nullptr;           // [cap]
-  int32_t* d_slot2cand = nullptr;      // [cap]
-  double* d_dist = nullptr;            // [cap][maxlen]
   double* d_partial = nullptr;         // [n_blocks_max][cap]
-  int32_t* d_tie = nullptr;
-  MatchResultDev* d_res = nullptr;
-  MatchResultDev* h_res = nullptr;     // pinned
-  int32_t* h_cand = nullptr;           // pinned staging for candidate lists [2*cap]
   int64_t bytes = 0;
   std::vector<SlotMeta> slots;
   int64_t next_index = 0;
   mutable std::shared_mutex mu;        // metadata: many readers / one writer
   std::mutex match_mu;                 // match scratch buffers
-  void* prev_tab_event = nullptr;
 
-  int64_t ph_slot_stride() const { return int64_t(2) * Ls * Hs * maxlen * d; }
-  int64_t ph_plane_stride() const { return int64_t(Ls) * Hs * maxlen * d; }
+  int64_t ph_slot_stride() const { return int64_t(2) * Ls * Hs * ph_ld * d + slot_pad; }
+  int64_t ph_plane_stride() const { return int64_t(Ls) * Hs * ph_ld * d; }
   bf16* ph_base(int c) const { return ph + int64_t(c) * cap * ph_slot_stride(); }
   int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * prefix_len[c] * d; }
   int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * prefix_len[c] * d; }
@@ -125,14 +120,7 @@ static void pool_free(kvcomm_pool_s* p) {
   cudaFree(p->ph);
   for (auto* x : p->pf) cudaFree(x);
   cudaFree(p->inv_freq_dev);
-  cudaFree(p->d_cand);
-  cudaFree(p->d_slot2cand);
-  cudaFree(p->d_dist);
   cudaFree(p->d_partial);
-  cudaFree(p->d_tie);
-  cudaFree(p->d_res);
-  if (p->h_res) cudaFreeHost(p->h_res);
-  if (p->h_cand) cudaFreeHost(p->h_cand);
   delete p;
 }
 
@@ -210,6 +198,14 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   p->cfg = *c;
   p->Ls = Ls; p->Hs = Hs; p->d = c->head_dim; p->De = c->emb_dim; p->cap = c->capacity;
   p->maxlen = c->max_anchor_len; p->C = c->num_consumers;
+  {
+    // Tuning knobs: KVCOMM_PH_PAD_ROWS pads each (layer, head) block of a
+    // stored offset, KVCOMM_SLOT_PAD_ROWS adds rows between anchor slots.
+    const char* e1 = getenv("KVCOMM_PH_PAD_ROWS");
+    const char* e2 = getenv("KVCOMM_SLOT_PAD_ROWS");
+    p->ph_ld = p->maxlen + (e1 ? atoi(e1) : 0);
+    p->slot_pad = int64_t(e2 ? atoi(e2) : 0) * p->d;
+  }
   p->prefix_len.assign(c->prefix_len, c->prefix_len + c->num_consumers);
   p->inv_freq.assign(c->inv_freq, c->inv_freq + c->head_dim / 2);
   p->cfg.prefix_len = nullptr;
@@ -223,19 +219,8 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   p->pf.assign(p->C, nullptr);
   for (int i = 0; i < p->C; ++i) ALLOC(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
   ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
-  ALLOC(p->d_cand, p->cap, "candidate list");
-  ALLOC(p->d_slot2cand, p->cap, "slot map");
-  ALLOC(p->d_dist, int64_t(p->cap) * p->maxlen, "distance scratch");
   ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * p->cap, "partial sums");
-  ALLOC(p->d_tie, 1, "tie counter");
-  ALLOC(p->d_res, 1, "match result");
 #undef ALLOC
-  if (cudaMallocHost(reinterpret_cast<void**>(&p->h_res), sizeof(MatchResultDev)) != cudaSuccess ||
-      cudaMallocHost(reinterpret_cast<void**>(&p->h_cand), sizeof(int32_t) * 2 * p->cap) != cudaSuccess) {
-    cudaGetLastError();
-    pool_free(p);
-    return fail(KVCOMM_ERR_OUT_OF_MEMORY, "pinned host staging");
-  }
   cudaError_t e = cudaMemcpy(p->inv_freq_dev, p->inv_freq.data(), sizeof(double) * (p->d / 2),
                              cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -288,9 +273,9 @@ static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const 
     if (o.ph_delta.k) {
       KV_TRY(check_view(o.ph_delta, L_psi, "ph_delta"));
       const int64_t ld = ld_of(o.ph_delta, L_psi);
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.k), ld, phk, p->maxlen, p->Ls, p->Hs, L_psi,
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.k), ld, phk, p->ph_ld, p->Ls, p->Hs, L_psi,
                                p->d, s));
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.v), ld, phv, p->maxlen, p->Ls, p->Hs, L_psi,
+      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.v), ld, phv, p->ph_ld, p->Ls, p->Hs, L_psi,
                                p->d, s));
       g_launches += 2;
       *ph_set |= 1ull << c;
@@ -310,7 +295,7 @@ static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const 
       KV_CUDA(launch_measure(static_cast<const bf16*>(o.ph_real.k), static_cast<const bf16*>(o.ph_real.v),
                              ld_of(o.ph_real, L_psi), static_cast<const bf16*>(o.ph_base.k),
                              static_cast<const bf16*>(o.ph_base.v), ld_of(o.ph_base, L_psi), L_psi, p->Ls, p->Hs,
-                             p->d, -(o.ph_real.start - o.ph_base.start), p->inv_freq_dev, phk, phv, p->maxlen, s));
+                             p->d, -(o.ph_real.start - o.ph_base.start), p->inv_freq_dev, phk, phv, p->ph_ld, s));
       g_launches += 1;
       *ph_set |= 1ull << c;
     }
@@ -441,7 +426,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t p, int32_t
     const bf16* b = p->ph_base(consumer) + int64_t(slot) * p->ph_slot_stride();
     *k = b;
     *v = b + p->ph_plane_stride();
-    *ld = p->maxlen;
+    *ld = p->ph_ld;
   } else {
     const bf16* b = p->pf[consumer] + int64_t(slot) * p->pf_slot_stride(consumer);
     *k = b;
@@ -451,125 +436,247 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t p, int32_t
   return ok();
 }
 
-// ---- match -------------------------------------------------------------------
-KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t p, const void* query_emb, int32_t L_phi,
-                                              int32_t consumer, float gamma, int32_t top_k, float* W,
-                                              int64_t ld_w, int32_t* idx, float* wbar, double* dist,
-                                              kvcomm_match_info* info, void* stream) {
-  if (!p || !info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool/info");
-  if (!(gamma >= 0.f && gamma <= 1.f)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "gamma %g outside [0,1]", gamma);
-  if (L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "L_phi %d < 1", L_phi);
-  if (top_k < 0 || top_k > KVCOMM_MAX_TOPK)
-    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "top_k %d outside [0,%d]", top_k, KVCOMM_MAX_TOPK);
-  if (consumer != KVCOMM_ALL_CONSUMERS && (consumer < 0 || consumer >= p->C))
-    return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
-  std::memset(info, 0, sizeof(*info));
-  std::shared_lock<std::shared_mutex> lk(p->mu);
-  // a1: candidate filter and length clause (host, integer metadata)
-  int32_t maxL = 0, n_occ = 0;
-  const uint64_t need = consumer == KVCOMM_ALL_CONSUMERS
-                            ? (p->C >= 64 ? ~0ull : ((1ull << p->C) - 1))
-                            : (1ull << consumer);
-  int n_cand = 0;
-  for (int s = 0; s < p->cap; ++s) {
-    const SlotMeta& m = p->slots[s];
-    if (!m.occupied) continue;
-    ++n_occ;
-    maxL = std::max(maxL, m.length);
-    if (m.length >= L_phi && (m.ph_mask & need) == need && (m.pf_mask & need) == need)
-      info->candidates[n_cand++] = s;
-  }
-  info->n_candidates = n_cand;
-  info->verdict = KVCOMM_NEW_ANCHOR;
-  if (n_occ == 0) { info->reason = KVCOMM_REASON_EMPTY_POOL; return ok(); }
-  if (L_phi > maxL) { info->reason = KVCOMM_REASON_TOO_LONG; return ok(); }
-  if (n_cand == 0) { info->reason = KVCOMM_REASON_NO_CANDIDATES; return ok(); }
-  if (!query_emb || !W || !wbar) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null query/W/wbar");
-  if (!aligned16(query_emb)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "query_emb not 16-byte aligned");
-  if (ld_w < L_phi) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "ld_w %lld < L_phi %d", (long long)ld_w, L_phi);
-  const int k_eff = top_k > 0 ? std::min(top_k, n_cand) : 0;
-  info->top_k = k_eff > 0 ? k_eff : n_cand;
-
-  DeviceGuard guard(p->cfg.device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::lock_guard<std::mutex> mlk(p->match_mu);
-  // upload candidate list and slot->candidate map (pinned staging; the previous
-  // match on this pool synchronised its stream, so the staging is free)
-  std::vector<int32_t> s2c(p->cap, -1);
-  for (int j = 0; j < n_cand; ++j) s2c[info->candidates[j]] = j;
-  std::memcpy(p->h_cand, info->candidates, sizeof(int32_t) * n_cand);
-  std::memcpy(p->h_cand + p->cap, s2c.data(), sizeof(int32_t) * p->cap);
-  KV_CUDA(cudaMemcpyAsync(p->d_cand, p->h_cand, sizeof(int32_t) * n_cand, cudaMemcpyHostToDevice, s));
-  KV_CUDA(cudaMemcpyAsync(p->d_slot2cand, p->h_cand + p->cap, sizeof(int32_t) * p->cap, cudaMemcpyHostToDevice, s));
-  KV_CUDA(cudaMemsetAsync(p->d_tie, 0, sizeof(int32_t), s));
-
-  MatchArgs a{};
-  a.query = static_cast<const bf16*>(query_emb);
-  a.emb = p->emb;
-  a.slot_stride = int64_t(p->maxlen) * p->De;
-  a.cand = p->d_cand;
-  a.slot2cand = p->d_slot2cand;
-  a.n_cand = n_cand;
-  a.cap = p->cap;
-  a.L_phi = L_phi;
-  a.De = p->De;
-  a.top_k = k_eff;
-  a.scalar_mode = p->cfg.scalar_distance;
-  a.W = W;
-  a.ld_w = ld_w;
-  a.idx = k_eff > 0 ? idx : nullptr;
-  a.dist = p->d_dist;
-  a.ld_d = p->maxlen;
-  a.dist_user = dist;
-  a.partial = p->d_partial;
-  a.tie_count = p->d_tie;
-  const int n_blocks = (L_phi + kMatchP - 1) / kMatchP;
-  KV_CUDA(launch_match(a, kMatchP, s));
-  KV_CUDA(launch_match_finalize(a, n_blocks, double(gamma), wbar, p->d_res, s));
-  g_launches += 2;
-  KV_CUDA(cudaMemcpyAsync(p->h_res, p->d_res, sizeof(MatchResultDev), cudaMemcpyDeviceToHost, s));
-  KV_CUDA(cudaStreamSynchronize(s));
-  info->entropy = p->h_res->entropy;
-  info->threshold = p->h_res->threshold;
-  info->verdict = p->h_res->verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
-  info->reason = p->h_res->verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
-  info->verdict_in_tie_band = p->h_res->tie_flag;
-  info->tie_band_count = p->h_res->tie_count;
-  return ok();
-}
-
-// ---- realign -----------------------------------------------------------------
+// ---- work tables (match and realign) -------------------------------------------
 namespace {
 
-// A small ring of (pinned host, device) buffers for realign work tables.  Slot
-// reuse waits on the event recorded after the kernel that consumed it.
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// A small ring of (pinned host, device) buffers holding the per-launch work tables.
+// Reusing an entry waits on the event recorded after the kernels that consumed it.
+struct RingEntry {
+  void* host = nullptr;
+  void* dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool used = false;
+};
 struct TableRing {
   static constexpr int kN = 8;
-  struct Entry {
-    void* host = nullptr;
-    void* dev = nullptr;
-    size_t cap = 0;
-    cudaEvent_t done = nullptr;
-    bool used = false;
-  } e[kN];
+  RingEntry e[kN];
   int next = 0;
   std::mutex mu;
 };
 TableRing g_rings[64];
 
-size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// Caller holds ring.mu; `dev` is current.
+kvcomm_status ring_acquire(TableRing& ring, size_t bytes, RingEntry** out) {
+  RingEntry& E = ring.e[ring.next];
+  ring.next = (ring.next + 1) % TableRing::kN;
+  if (E.used) KV_CUDA(cudaEventSynchronize(E.done));
+  if (!E.done) KV_CUDA(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming));
+  if (E.cap < bytes) {
+    if (E.host) cudaFreeHost(E.host);
+    if (E.dev) cudaFree(E.dev);
+    E.host = E.dev = nullptr;
+    E.cap = 0;
+    const size_t cap = std::max<size_t>(align_up(bytes, 1 << 16), 1 << 16);
+    if (cudaMallocHost(&E.host, cap) != cudaSuccess || cudaMalloc(&E.dev, cap) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KVCOMM_ERR_OUT_OF_MEMORY, "work table (%zu bytes)", cap);
+    }
+    E.cap = cap;
+  }
+  *out = &E;
+  return KVCOMM_OK;
+}
+
+std::vector<kvcomm_pool_s*> distinct(std::vector<kvcomm_pool_s*> pools) {
+  std::sort(pools.begin(), pools.end());
+  pools.erase(std::unique(pools.begin(), pools.end()), pools.end());
+  return pools;
+}
+
+void lock_readers(const std::vector<kvcomm_pool_s*>& pools, std::vector<std::shared_lock<std::shared_mutex>>& l) {
+  for (kvcomm_pool_s* p : distinct(pools)) l.emplace_back(p->mu);
+}
+
+void lock_match_scratch(const std::vector<kvcomm_pool_s*>& pools, std::vector<std::unique_lock<std::mutex>>& l) {
+  for (kvcomm_pool_s* p : distinct(pools)) l.emplace_back(p->match_mu);
+}
 
 }  // namespace
 
-static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx, int* out_rows_len) {
+// ---- match -------------------------------------------------------------------
+KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* reqs, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && !reqs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad request list");
+  std::vector<kvcomm_pool_s*> pools;
+  for (int r = 0; r < n; ++r) {
+    const kvcomm_match_request& q = reqs[r];
+    kvcomm_pool_s* p = q.pool;
+    if (!p || !q.info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null pool/info", r);
+    if (!(q.gamma >= 0.f && q.gamma <= 1.f))
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: gamma %g outside [0,1]", r, q.gamma);
+    if (q.L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: L_phi %d < 1", r, q.L_phi);
+    if (q.top_k < 0 || q.top_k > KVCOMM_MAX_TOPK)
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: top_k %d outside [0,%d]", r, q.top_k, KVCOMM_MAX_TOPK);
+    if (q.consumer != KVCOMM_ALL_CONSUMERS && (q.consumer < 0 || q.consumer >= p->C))
+      return fail(KVCOMM_ERR_NOT_FOUND, "request %d: consumer %d", r, q.consumer);
+    if (std::find(pools.begin(), pools.end(), p) != pools.end())
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: pool appears twice in one batch", r);
+    if (!pools.empty() && p->cfg.device != pools[0]->cfg.device)
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: pools on different devices", r);
+    pools.push_back(p);
+  }
+  if (n == 0) return ok();
+  std::vector<std::shared_lock<std::shared_mutex>> rlocks;
+  lock_readers(pools, rlocks);
+  // a1: candidate filter and length clause (host, integer metadata)
+  std::vector<int> active;
+  for (int r = 0; r < n; ++r) {
+    const kvcomm_match_request& q = reqs[r];
+    kvcomm_pool_s* p = q.pool;
+    kvcomm_match_info* info = q.info;
+    std::memset(info, 0, sizeof(*info));
+    int32_t maxL = 0, n_occ = 0, n_cand = 0;
+    const uint64_t need = q.consumer == KVCOMM_ALL_CONSUMERS ? (p->C >= 64 ? ~0ull : ((1ull << p->C) - 1))
+                                                             : (1ull << q.consumer);
+    for (int s = 0; s < p->cap; ++s) {
+      const SlotMeta& m = p->slots[s];
+      if (!m.occupied) continue;
+      ++n_occ;
+      maxL = std::max(maxL, m.length);
+      if (m.length >= q.L_phi && (m.ph_mask & need) == need && (m.pf_mask & need) == need)
+        info->candidates[n_cand++] = s;
+    }
+    info->n_candidates = n_cand;
+    info->verdict = KVCOMM_NEW_ANCHOR;
+    if (n_occ == 0) { info->reason = KVCOMM_REASON_EMPTY_POOL; continue; }
+    if (q.L_phi > maxL) { info->reason = KVCOMM_REASON_TOO_LONG; continue; }
+    if (n_cand == 0) { info->reason = KVCOMM_REASON_NO_CANDIDATES; continue; }
+    if (!q.query_emb || !q.W || !q.wbar)
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null query/W/wbar", r);
+    if (!aligned16(q.query_emb))
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: query_emb not 16-byte aligned", r);
+    if (q.ld_w < q.L_phi)
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: ld_w %lld < L_phi %d", r, (long long)q.ld_w, q.L_phi);
+    const int k_eff = q.top_k > 0 ? std::min(q.top_k, n_cand) : 0;
+    info->top_k = k_eff > 0 ? k_eff : n_cand;
+    active.push_back(r);
+  }
+  if (active.empty()) return ok();
+
+  // table layout
+  const int nj = int(active.size());
+  MatchHdr hdr{};
+  hdr.n_jobs = nj;
+  hdr.P = kMatchP;
+  size_t n_ints = 0;
+  for (int r : active) n_ints += reqs[r].info->n_candidates + reqs[r].pool->cap;
+  size_t off = align_up(sizeof(MatchHdr), 64);
+  hdr.job_off = int64_t(off);
+  off = align_up(off + sizeof(MatchJob) * nj, 64);
+  hdr.int_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * n_ints, 64);
+  hdr.res_off = int64_t(off);
+  off = align_up(off + sizeof(MatchResultDev) * nj, 64);
+  hdr.tie_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * nj, 64);
+  const size_t table_bytes = off;
+
+  const int dev = pools[0]->cfg.device;
+  DeviceGuard guard(dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<std::unique_lock<std::mutex>> mlocks;
+  lock_match_scratch(pools, mlocks);
+  TableRing& ring = g_rings[dev & 63];
+  std::lock_guard<std::mutex> rlk(ring.mu);
+  RingEntry* E = nullptr;
+  KV_TRY(ring_acquire(ring, table_bytes, &E));
+  uint8_t* h = static_cast<uint8_t*>(E->host);
+  std::memset(h, 0, table_bytes);
+  MatchJob* jobs = reinterpret_cast<MatchJob*>(h + hdr.job_off);
+  int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.int_off);
+  int ipos = 0, blocks = 0;
+  size_t smem = 0;
+  for (int t = 0; t < nj; ++t) {
+    const kvcomm_match_request& q = reqs[active[t]];
+    kvcomm_pool_s* p = q.pool;
+    const kvcomm_match_info* info = q.info;
+    MatchJob& a = jobs[t];
+    a.query = static_cast<const bf16*>(q.query_emb);
+    a.emb = p->emb;
+    a.slot_stride = int64_t(p->maxlen) * p->De;
+    a.W = q.W;
+    a.ld_w = q.ld_w;
+    a.top_k = q.top_k > 0 ? std::min(q.top_k, info->n_candidates) : 0;
+    a.idx = a.top_k > 0 ? q.idx : nullptr;
+    a.dist_user = q.dist;
+    a.partial = p->d_partial;
+    a.wbar = q.wbar;
+    a.gamma = double(q.gamma);
+    a.n_cand = info->n_candidates;
+    a.cap = p->cap;
+    a.L_phi = q.L_phi;
+    a.De = p->De;
+    a.scalar_mode = p->cfg.scalar_distance;
+    a.cand_off = ipos;
+    std::memcpy(ints + ipos, info->candidates, sizeof(int32_t) * a.n_cand);
+    ipos += a.n_cand;
+    a.s2c_off = ipos;
+    for (int sl = 0; sl < p->cap; ++sl) ints[ipos + sl] = -1;
+    for (int j = 0; j < a.n_cand; ++j) ints[ipos + info->candidates[j]] = j;
+    ipos += p->cap;
+    a.n_blocks = (q.L_phi + kMatchP - 1) / kMatchP;
+    a.block_begin = blocks;
+    blocks += a.n_blocks;
+    smem = std::max(smem, align_up(size_t(kMatchP) * p->De * 2, 16) + size_t(kMatchP) * a.n_cand * sizeof(double));
+  }
+  hdr.total_blocks = blocks;
+  std::memcpy(h, &hdr, sizeof(hdr));
+  KV_CUDA(cudaMemcpyAsync(E->dev, E->host, table_bytes, cudaMemcpyHostToDevice, s));
+  KV_CUDA(launch_match_batch(E->dev, hdr, smem, s));
+  g_launches += 2;
+  KV_CUDA(cudaMemcpyAsync(h + hdr.res_off, static_cast<uint8_t*>(E->dev) + hdr.res_off,
+                          table_bytes - size_t(hdr.res_off), cudaMemcpyDeviceToHost, s));
+  KV_CUDA(cudaEventRecord(E->done, s));
+  E->used = true;
+  KV_CUDA(cudaStreamSynchronize(s));
+  const MatchResultDev* res = reinterpret_cast<const MatchResultDev*>(h + hdr.res_off);
+  for (int t = 0; t < nj; ++t) {
+    kvcomm_match_info* info = reqs[active[t]].info;
+    info->entropy = res[t].entropy;
+    info->threshold = res[t].threshold;
+    info->verdict = res[t].verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
+    info->reason = res[t].verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
+    info->verdict_in_tie_band = res[t].tie_flag;
+    info->tie_band_count = res[t].tie_count;
+  }
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t p, const void* query_emb, int32_t L_phi,
+                                              int32_t consumer, float gamma, int32_t top_k, float* W,
+                                              int64_t ld_w, int32_t* idx, float* wbar, double* dist,
+                                              kvcomm_match_info* info, void* stream) {
+  kvcomm_match_request q{p, query_emb, L_phi, consumer, gamma, top_k, W, ld_w, idx, wbar, dist, info};
+  return kvcomm_match_anchors_batch(&q, 1, stream);
+}
+
+// ---- realign -----------------------------------------------------------------
+namespace {
+struct HostSeg {
+  SegDev x;
+  const int32_t* cand;
+  bool prefix;
+};
+}  // namespace
+
+static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
   kvcomm_pool_s* p = g.pool;
   if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", idx);
-  if (g.consumer < 0 || g.consumer >= p->C)
-    return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: consumer %d outside [0,%d)", idx, g.consumer, p->C);
-  if (g.kind != KVCOMM_PLACEHOLDER && g.kind != KVCOMM_PREFIX)
+  if (g.kind != KVCOMM_PLACEHOLDER && g.kind != KVCOMM_PREFIX && g.kind != KVCOMM_COPY)
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: kind %d", idx, g.kind);
   if (g.L_seg < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: L_seg %d", idx, g.L_seg);
   if (g.L_seg == 0) return KVCOMM_OK;
+  KV_TRY(check_view(g.base, g.L_seg, "base"));
+  if (!g.dst_k || !g.dst_v || !aligned16(g.dst_k) || !aligned16(g.dst_v))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: dst null or misaligned", idx);
+  if (g.target_start < 0 || int64_t(g.target_start) + g.L_seg > g.dst_ld)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: rows [%d,%d) outside dst_ld %lld", idx, g.target_start,
+                g.target_start + g.L_seg, (long long)g.dst_ld);
+  if (g.kind == KVCOMM_COPY) return KVCOMM_OK;
+  if (g.consumer < 0 || g.consumer >= p->C)
+    return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: consumer %d outside [0,%d)", idx, g.consumer, p->C);
   if (g.n_candidates < 1 || !g.candidates)
     return fail(KVCOMM_ERR_NO_CANDIDATES, "segment %d: empty candidate set", idx);
   if (g.n_candidates > p->cap) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: n_candidates", idx);
@@ -586,12 +693,6 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx, int
                   (long long)g.ld_w);
     if (!aligned16(g.weights)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: W not 16-byte aligned", idx);
   }
-  KV_TRY(check_view(g.base, g.L_seg, "base"));
-  if (!g.dst_k || !g.dst_v || !aligned16(g.dst_k) || !aligned16(g.dst_v))
-    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: dst null or misaligned", idx);
-  if (g.target_start < 0 || int64_t(g.target_start) + g.L_seg > g.dst_ld)
-    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: rows [%d,%d) outside dst_ld %lld", idx, g.target_start,
-                g.target_start + g.L_seg, (long long)g.dst_ld);
   if ((g.debug_delta_k && !aligned16(g.debug_delta_k)) || (g.debug_delta_v && !aligned16(g.debug_delta_v)))
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: debug buffers misaligned", idx);
   const uint64_t bit = 1ull << g.consumer;
@@ -612,44 +713,19 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx, int
                   g.consumer);
     }
   }
-  *out_rows_len = g.L_seg;
   return KVCOMM_OK;
 }
 
-KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs, int32_t n, void* stream) {
-  if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
-  // shared geometry
-  kvcomm_pool_s* p0 = nullptr;
-  std::vector<std::shared_lock<std::shared_mutex>> locks;
-  std::vector<kvcomm_pool_s*> locked;
-  for (int i = 0; i < n; ++i) {
-    kvcomm_pool_s* p = segs[i].pool;
-    if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", i);
-    if (!p0) p0 = p;
-    if (p->Ls != p0->Ls || p->Hs != p0->Hs || p->d != p0->d || p->cfg.device != p0->cfg.device)
-      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: pool geometry differs from segment 0", i);
-    if (std::find(locked.begin(), locked.end(), p) == locked.end()) {
-      locked.push_back(p);
-      locks.emplace_back(p->mu);
-    }
-  }
-  if (!p0) return ok();
-  const int d = p0->d, Ls = p0->Ls, Hs = p0->Hs;
+// Builds the work table of `hs` in a ring entry and launches prep + realign kernels.
+static kvcomm_status launch_segments(int dev, int d, int Ls, int Hs, std::vector<HostSeg>& hs, cudaStream_t s) {
+  const int n_seg = int(hs.size());
+  if (n_seg == 0) return KVCOMM_OK;
   const int rpt = kStageBytes / (2 * d);
-
-  // validate, and size the work table
-  std::vector<int> live;
   size_t n_cand_total = 0, n_wexp = 0;
-  for (int i = 0; i < n; ++i) {
-    int rows = 0;
-    KV_TRY(validate_segment(segs[i], i, &rows));
-    if (rows == 0) continue;
-    live.push_back(i);
-    n_cand_total += segs[i].n_candidates;
-    if (segs[i].kind == KVCOMM_PREFIX) n_wexp += size_t(segs[i].n_candidates) * ((segs[i].L_seg + 3) & ~3);
+  for (const HostSeg& g : hs) {
+    n_cand_total += g.x.n_cand;
+    if (g.prefix) n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
   }
-  if (live.empty()) return ok();
-  const int n_seg = int(live.size());
   TableHdr hdr{};
   hdr.n_seg = n_seg;
   hdr.d = d;
@@ -660,96 +736,116 @@ KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs
   hdr.seg_off = int64_t(off);
   off = align_up(off + sizeof(SegDev) * n_seg, 64);
   hdr.cand_off = int64_t(off);
-  off = align_up(off + sizeof(int32_t) * n_cand_total, 64);
+  off = align_up(off + sizeof(int32_t) * std::max<size_t>(n_cand_total, 1), 64);
   hdr.cs_off = int64_t(off);
   off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
   hdr.wexp_off = int64_t(off);
   off = align_up(off + sizeof(float) * n_wexp, 64);
   const size_t table_bytes = off;
 
-  const int dev = p0->cfg.device;
-  DeviceGuard guard(dev);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   TableRing& ring = g_rings[dev & 63];
   std::lock_guard<std::mutex> rlk(ring.mu);
-  TableRing::Entry& E = ring.e[ring.next];
-  ring.next = (ring.next + 1) % TableRing::kN;
-  if (E.used) KV_CUDA(cudaEventSynchronize(E.done));
-  if (!E.done) KV_CUDA(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming));
-  if (E.cap < table_bytes) {
-    if (E.host) cudaFreeHost(E.host);
-    if (E.dev) cudaFree(E.dev);
-    E.host = E.dev = nullptr;
-    E.cap = 0;
-    const size_t cap = std::max<size_t>(align_up(table_bytes, 1 << 16), 1 << 16);
-    if (cudaMallocHost(&E.host, cap) != cudaSuccess || cudaMalloc(&E.dev, cap) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(KVCOMM_ERR_OUT_OF_MEMORY, "realign work table (%zu bytes)", cap);
-    }
-    E.cap = cap;
-  }
-  uint8_t* h = static_cast<uint8_t*>(E.host);
-  uint8_t* dv = static_cast<uint8_t*>(E.dev);
-  SegDev* hs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
-  int32_t* hc = reinterpret_cast<int32_t*>(h + hdr.cand_off);
-  float* dwexp = reinterpret_cast<float*>(dv + hdr.wexp_off);
+  RingEntry* E = nullptr;
+  KV_TRY(ring_acquire(ring, table_bytes, &E));
+  uint8_t* h = static_cast<uint8_t*>(E->host);
+  SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
+  int32_t* cands = reinterpret_cast<int32_t*>(h + hdr.cand_off);
+  float* dwexp = reinterpret_cast<float*>(static_cast<uint8_t*>(E->dev) + hdr.wexp_off);
   int64_t units = 0;
-  int cand_pos = 0, wexp_pos = 0;
+  int cpos = 0, wpos = 0;
   for (int t = 0; t < n_seg; ++t) {
-    const kvcomm_realign_desc& g = segs[live[t]];
+    SegDev x = hs[t].x;
+    x.cand_off = cpos;
+    if (x.n_cand) std::memcpy(cands + cpos, hs[t].cand, sizeof(int32_t) * x.n_cand);
+    cpos += x.n_cand;
+    x.cs_off = t * (d / 2);
+    x.tiles = (x.L_seg + rpt - 1) / rpt;
+    x.unit_begin = units;
+    units += int64_t(Ls) * Hs * 2 * x.tiles;
+    if (hs[t].prefix) {
+      x.ld_w = (x.L_seg + 3) & ~3;
+      x.w = dwexp + wpos;
+      x.wexp_off = wpos;
+      wpos += int(x.ld_w) * x.n_cand;
+    }
+    segs[t] = x;
+  }
+  hdr.total_units = units;
+  std::memcpy(h, &hdr, sizeof(hdr));
+  KV_CUDA(cudaMemcpyAsync(E->dev, E->host, size_t(hdr.cs_off), cudaMemcpyHostToDevice, s));
+  static int grid_cache[64] = {0};
+  if (!grid_cache[dev & 63]) grid_cache[dev & 63] = realign_grid_size(dev);
+  KV_CUDA(launch_realign(E->dev, hdr, grid_cache[dev & 63], s));
+  g_launches += units > 0 ? 2 : 1;
+  KV_CUDA(cudaEventRecord(E->done, s));
+  E->used = true;
+  return KVCOMM_OK;
+}
+
+KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
+  kvcomm_pool_s* p0 = nullptr;
+  std::vector<kvcomm_pool_s*> pools;
+  for (int i = 0; i < n; ++i) {
+    kvcomm_pool_s* p = segs[i].pool;
+    if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", i);
+    if (!p0) p0 = p;
+    if (p->Ls != p0->Ls || p->Hs != p0->Hs || p->d != p0->d || p->cfg.device != p0->cfg.device)
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: pool geometry differs from segment 0", i);
+    pools.push_back(p);
+  }
+  if (!p0) return ok();
+  std::vector<std::shared_lock<std::shared_mutex>> locks;
+  lock_readers(pools, locks);
+  std::vector<HostSeg> hs;
+  hs.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    const kvcomm_realign_desc& g = segs[i];
+    KV_TRY(validate_segment(g, i));
+    if (g.L_seg == 0) continue;
     kvcomm_pool_s* p = g.pool;
-    SegDev& x = hs[t];
-    std::memset(&x, 0, sizeof(x));
+    HostSeg h{};
+    SegDev& x = h.x;
     x.base[0] = static_cast<const bf16*>(g.base.k);
     x.base[1] = static_cast<const bf16*>(g.base.v);
     x.base_ld = ld_of(g.base, g.L_seg);
     x.dst[0] = static_cast<bf16*>(g.dst_k);
     x.dst[1] = static_cast<bf16*>(g.dst_v);
     x.dst_ld = g.dst_ld;
-    x.dbg[0] = g.debug_delta_k;
-    x.dbg[1] = g.debug_delta_v;
     x.inv_freq = p->inv_freq_dev;
     x.L_seg = g.L_seg;
     x.target_start = g.target_start;
-    x.delta = g.target_start - g.base_start;
-    x.n_cand = g.n_candidates;
-    x.cand_off = cand_pos;
-    x.cs_off = t * (d / 2);
-    x.tiles = (g.L_seg + rpt - 1) / rpt;
-    x.unit_begin = units;
-    units += int64_t(Ls) * Hs * 2 * x.tiles;
-    std::memcpy(hc + cand_pos, g.candidates, sizeof(int32_t) * g.n_candidates);
-    cand_pos += g.n_candidates;
-    if (g.kind == KVCOMM_PLACEHOLDER) {
-      x.w = g.weights;
-      x.ld_w = g.ld_w;
-      x.w_by_slot = 1;
-      x.off = p->ph_base(g.consumer);
-      x.slot_stride = p->ph_slot_stride();
-      x.plane_stride = p->ph_plane_stride();
-      x.off_ld = p->maxlen;
+    x.w_by_slot = 1;
+    if (g.kind == KVCOMM_COPY) {
+      x.delta = 0;
+      x.n_cand = 0;
     } else {
-      x.ld_w = (g.L_seg + 3) & ~3;
-      x.w = dwexp + wexp_pos;
-      x.wexp_off = wexp_pos;
-      x.wbar = g.weights;
-      x.w_by_slot = 0;
-      wexp_pos += int(x.ld_w) * g.n_candidates;
-      x.off = p->pf[g.consumer];
-      x.slot_stride = p->pf_slot_stride(g.consumer);
-      x.plane_stride = p->pf_plane_stride(g.consumer);
-      x.off_ld = p->prefix_len[g.consumer];
+      x.dbg[0] = g.debug_delta_k;
+      x.dbg[1] = g.debug_delta_v;
+      x.delta = g.target_start - g.base_start;
+      x.n_cand = g.n_candidates;
+      h.cand = g.candidates;
+      if (g.kind == KVCOMM_PLACEHOLDER) {
+        x.w = g.weights;
+        x.ld_w = g.ld_w;
+        x.off = p->ph_base(g.consumer);
+        x.slot_stride = p->ph_slot_stride();
+        x.plane_stride = p->ph_plane_stride();
+        x.off_ld = p->ph_ld;
+      } else {
+        h.prefix = true;
+        x.w_by_slot = 0;
+        x.wbar = g.weights;
+        x.off = p->pf[g.consumer];
+        x.slot_stride = p->pf_slot_stride(g.consumer);
+        x.plane_stride = p->pf_plane_stride(g.consumer);
+        x.off_ld = p->prefix_len[g.consumer];
+      }
     }
+    hs.push_back(h);
   }
-  hdr.total_units = units;
-  std::memcpy(h, &hdr, sizeof(hdr));
-  KV_CUDA(cudaMemcpyAsync(E.dev, E.host, size_t(hdr.cs_off), cudaMemcpyHostToDevice, s));
-  static int grid_cache[64] = {0};
-  if (!grid_cache[dev & 63]) grid_cache[dev & 63] = realign_grid_size(dev);
-  KV_CUDA(launch_realign(E.dev, hdr, 0, grid_cache[dev & 63], s));
-  g_launches += units > 0 ? 2 : 1;
-  KV_CUDA(cudaEventRecord(E.done, s));
-  E.used = true;
+  DeviceGuard guard(p0->cfg.device);
+  KV_TRY(launch_segments(p0->cfg.device, p0->d, p0->Ls, p0->Hs, hs, static_cast<cudaStream_t>(stream)));
   return ok();
 }
 
@@ -761,16 +857,17 @@ KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, 
 // ---- concat ------------------------------------------------------------------
 KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n, int32_t N_total,
                                                      int32_t Ls, int32_t Hs, int32_t d, void* dst_k, void* dst_v,
-                                                     int64_t dst_ld, void* stream) {
+                                                     int64_t dst_ld, int32_t device, void* stream) {
   if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
-  if (Ls < 1 || Hs < 1 || d < 16 || d % 16 != 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad geometry");
-  if (N_total < 0 || dst_ld < N_total) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "dst_ld %lld < N_total %d",
-                                                   (long long)dst_ld, N_total);
+  if (Ls < 1 || Hs < 1 || d < 16 || d % 16 != 0 || d > 256) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad geometry");
+  if (N_total < 0 || dst_ld < N_total)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "dst_ld %lld < N_total %d", (long long)dst_ld, N_total);
   // ledger: segments tile [0, N_total) in order
   int64_t pos = 0;
   for (int i = 0; i < n; ++i) {
     if (segs[i].length < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: negative length", i);
-    if (segs[i].start > pos) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (segment %d)", (long long)pos, i);
+    if (segs[i].start > pos)
+      return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (segment %d)", (long long)pos, i);
     if (segs[i].start < pos)
       return fail(KVCOMM_ERR_POSITION_OVERLAP, "overlap at position %d (segment %d)", segs[i].start, i);
     pos = int64_t(segs[i].start) + segs[i].length;
@@ -779,18 +876,26 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
   if (pos > N_total) return fail(KVCOMM_ERR_POSITION_OVERLAP, "segments run past N_total %d", N_total);
   if (!dst_k || !dst_v || !aligned16(dst_k) || !aligned16(dst_v))
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "dst null or misaligned");
-  for (int i = 0; i < n; ++i)
-    if (segs[i].src.k && segs[i].length > 0) KV_TRY(check_view(segs[i].src, segs[i].length, "concat src"));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<HostSeg> hs;
   for (int i = 0; i < n; ++i) {
     if (!segs[i].src.k || segs[i].length == 0) continue;
-    const int64_t ld = ld_of(segs[i].src, segs[i].length);
-    bf16* dk = static_cast<bf16*>(dst_k) + int64_t(segs[i].start) * d;
-    bf16* dvp = static_cast<bf16*>(dst_v) + int64_t(segs[i].start) * d;
-    KV_CUDA(launch_copy_rows(static_cast<const bf16*>(segs[i].src.k), ld, dk, dst_ld, Ls, Hs, segs[i].length, d, s));
-    KV_CUDA(launch_copy_rows(static_cast<const bf16*>(segs[i].src.v), ld, dvp, dst_ld, Ls, Hs, segs[i].length, d, s));
-    g_launches += 2;
+    KV_TRY(check_view(segs[i].src, segs[i].length, "concat src"));
+    HostSeg h{};
+    SegDev& x = h.x;
+    x.base[0] = static_cast<const bf16*>(segs[i].src.k);
+    x.base[1] = static_cast<const bf16*>(segs[i].src.v);
+    x.base_ld = ld_of(segs[i].src, segs[i].length);
+    x.dst[0] = static_cast<bf16*>(dst_k);
+    x.dst[1] = static_cast<bf16*>(dst_v);
+    x.dst_ld = dst_ld;
+    x.L_seg = segs[i].length;
+    x.target_start = segs[i].start;
+    x.w_by_slot = 1;
+    hs.push_back(h);
   }
+  if (hs.empty()) return ok();
+  DeviceGuard guard(device);
+  KV_TRY(launch_segments(device, d, Ls, Hs, hs, static_cast<cudaStream_t>(stream)));
   return ok();
 }
 

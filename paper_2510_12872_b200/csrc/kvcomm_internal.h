@@ -46,27 +46,27 @@ struct TableHdr {
 };
 
 // Launchers (stream-ordered).  Return cudaGetLastError().
-cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int n_prefix_segments,
-                           int grid, cudaStream_t s);
+cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s);
 int realign_grid_size(int device);
 
-struct MatchArgs {
-  const bf16* query;    // [L_phi][De]
-  const bf16* emb;      // pool slab [cap][maxlen][De]
-  int64_t slot_stride;  // elements between slots of emb
-  const int32_t* cand;  // device [n_cand]
-  const int32_t* slot2cand;  // device [cap]: candidate index or -1
-  int32_t n_cand, cap, L_phi, De;
-  int32_t top_k;
-  int32_t scalar_mode;  // 0 Frobenius: partial = Σ d², 1 mean-ℓ2: partial = Σ d
-  float* W;             // [cap][ld_w]
+// One matching job (one query sample against one pool), as the kernels see it.
+struct MatchJob {
+  const bf16* query;        // [L_phi][De]
+  const bf16* emb;          // pool slab [cap][maxlen][De]
+  int64_t slot_stride;      // elements between slots of emb
+  float* W;                 // [cap][ld_w]
   int64_t ld_w;
-  int32_t* idx;         // [L_phi][top_k] or null
-  double* dist;         // scratch/out [n_cand][ld_d] (candidate-major)
-  int64_t ld_d;
-  double* dist_user;    // optional [cap][ld_w] user copy
-  double* partial;      // [n_blocks][n_cand]
-  int32_t* tie_count;   // device counter
+  int32_t* idx;             // [L_phi][top_k] or null
+  double* dist_user;        // optional [cap][ld_w]
+  double* partial;          // pool scratch [n_blocks][n_cand]
+  float* wbar;              // [cap]
+  double gamma;
+  int32_t n_cand, cap, L_phi, De;
+  int32_t top_k;            // effective k (0 = dense, paper default)
+  int32_t scalar_mode;      // 0 Frobenius: partial = Σ d², 1 mean-ℓ2: partial = Σ d
+  int32_t cand_off;         // into MatchHdr ints: candidate slot ids [n_cand]
+  int32_t s2c_off;          // into MatchHdr ints: slot -> candidate index or -1 [cap]
+  int32_t block_begin, n_blocks;
 };
 
 struct MatchResultDev {
@@ -74,9 +74,14 @@ struct MatchResultDev {
   int32_t verdict, tie_flag, tie_count, _pad;
 };
 
-cudaError_t launch_match(const MatchArgs& a, int positions_per_block, cudaStream_t s);
-cudaError_t launch_match_finalize(const MatchArgs& a, int n_blocks, double gamma, float* wbar,
-                                  MatchResultDev* res, cudaStream_t s);
+// Device-side table of one batched match launch.
+struct MatchHdr {
+  int32_t n_jobs, total_blocks, P, _pad;
+  int64_t job_off, int_off, res_off, tie_off;   // byte offsets from the table base
+};
+
+// distance + per-position weights over all jobs' blocks, then one finalize block per job
+cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_t smem_bytes, cudaStream_t s);
 
 // Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,

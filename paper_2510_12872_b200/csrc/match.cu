@@ -1,14 +1,18 @@
 // Anchor matching (SURVEY §8(a) a2+a3; Eq. 5, Eq. 6):
 //
-//   d[i,j]  = ‖h_φ[i] - h_ψj[i]‖₂                   i < L_φ, ψ_j ∈ 𝒜_φ (first L_φ rows, reading A8)
-//   W[j][i] = softmax_j(-d[i,j])                     (per position, reading A2; optional top-k A16)
-//   d̄_j     = sqrt(Σ_i d[i,j]²) (Frobenius, reading A4; or mean_i d[i,j]),  w̄ = softmax(-d̄),  H = -Σ w̄ log w̄,  NewAnchor ⇔ H > γ log|𝒜_φ|
+//   d[i,j]  = ‖h_φ[i] - h_ψj[i]‖₂          i < L_φ, ψ_j ∈ 𝒜_φ (first L_φ rows, reading A8)
+//   W[j][i] = softmax_j(-d[i,j])            per position (reading A2); optional top-k (A16)
+//   d̄_j     = sqrt(Σ_i d[i,j]²)            Frobenius (reading A4; or mean_i d[i,j])
+//   w̄ = softmax(-d̄),  H = -Σ w̄ log w̄,  NewAnchor ⇔ H > γ log|𝒜_φ|
+//
+// One launch covers every (sample, pool) job of a request: blocks of P positions of
+// every job, then one finalize block per job.
 //
 // Numerics: each lane forms 8 differences of bf16 values in fp32 (exact unless the
 // exponents are >16 binades apart), squares/accumulates those 8 with fp32 FMA
 // (relative error <= 8·2^-24 on a sum of positive terms), and adds the partials in
 // fp64.  The resulting distance has a relative error below 3e-7, inside the 1e-6
-// tie band of the parity contract.  Softmax, means and entropy run in fp64 with
+// tie band of the parity contract.  Softmax, sums and entropy run in fp64 with
 // fixed-order reductions, so the verdict is deterministic run to run.
 //
 // Why not tensor cores: the distance compares row i of φ only with row i of each
@@ -43,13 +47,48 @@ __device__ __forceinline__ bool key_less(double da, int sa, double db, int sb) {
   return da < db || (da == db && sa < sb);
 }
 
-__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, int P) {
+// Σ over 8 bf16 pairs of (q - a)², fp32 FMA on (almost always exact) fp32 differences
+__device__ __forceinline__ float sq_diff8(const uint4& qv, const uint4& av) {
+  const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+  float part = 0.f;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
+    const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
+    part = fmaf(d0, d0, part);
+    part = fmaf(d1, d1, part);
+  }
+  return part;
+}
+
+__device__ __forceinline__ int find_job(const MatchJob* jobs, int n, int b) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].block_begin <= b) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t* __restrict__ tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  const MatchJob* jobs = reinterpret_cast<const MatchJob*>(tab + hdr->job_off);
+  const int32_t* ints = reinterpret_cast<const int32_t*>(tab + hdr->int_off);
+  int32_t* ties = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off);
+  const int jb = find_job(jobs, hdr->n_jobs, blockIdx.x);
+  const MatchJob& a = jobs[jb];
+  const int P = hdr->P;
+  const int lb = blockIdx.x - a.block_begin;
+  const int32_t* cand = ints + a.cand_off;
+  const int32_t* slot2cand = ints + a.s2c_off;
+
   extern __shared__ __align__(16) uint8_t smem[];
   const int De = a.De;
   const int n_cand = a.n_cand;
   bf16* q = reinterpret_cast<bf16*>(smem);
   double* sd = reinterpret_cast<double*>(smem + ((size_t(P) * De * 2 + 15) & ~size_t(15)));
-  const int i0 = blockIdx.x * P;
+  const int i0 = lb * P;
   const int np = min(P, a.L_phi - i0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -67,47 +106,18 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
   for (int task = warp; task < ntask; task += kMatchWarps) {
     const int p = task / n_cand;
     const int j = task - p * n_cand;
-    const bf16* arow = a.emb + int64_t(a.cand[j]) * a.slot_stride + int64_t(i0 + p) * De;
+    const bf16* arow = a.emb + int64_t(cand[j]) * a.slot_stride + int64_t(i0 + p) * De;
     const bf16* qrow = q + size_t(p) * De;
     double s = 0.0;
     int e = lane * 8;
-    // 4 independent 16-byte loads in flight per lane
-    for (; e + 3 * 256 < De; e += 4 * 256) {
-      uint4 av[4], qv[4];
+    for (; e + 3 * 256 < De; e += 4 * 256) {  // 4 independent 16-byte loads in flight per lane
+      uint4 av[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) av[r] = ldg128_nc(arow + e + r * 256);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) qv[r] = lds128(qrow + e + r * 256);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t aw[4] = {av[r].x, av[r].y, av[r].z, av[r].w};
-        const uint32_t qw[4] = {qv[r].x, qv[r].y, qv[r].z, qv[r].w};
-        float part = 0.f;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
-          const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
-          part = fmaf(d0, d0, part);
-          part = fmaf(d1, d1, part);
-        }
-        s += double(part);
-      }
+      for (int r = 0; r < 4; ++r) s += double(sq_diff8(lds128(qrow + e + r * 256), av[r]));
     }
-    for (; e < De; e += 256) {
-      const uint4 av = ldg128_nc(arow + e);
-      const uint4 qv = lds128(qrow + e);
-      const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-      const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
-      float part = 0.f;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
-        const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
-        part = fmaf(d0, d0, part);
-        part = fmaf(d1, d1, part);
-      }
-      s += double(part);
-    }
+    for (; e < De; e += 256) s += double(sq_diff8(lds128(qrow + e), ldg128_nc(arow + e)));
     s = warp_sum_d(s);
     if (lane == 0) sd[p * n_cand + j] = sqrt(s);
   }
@@ -117,12 +127,9 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
   for (int p = warp; p < np; p += kMatchWarps) {
     const int i = i0 + p;
     const double* dr = sd + p * n_cand;
-    for (int j = lane; j < n_cand; j += 32) {
-      a.dist[int64_t(j) * a.ld_d + i] = dr[j];
-      if (a.dist_user) a.dist_user[int64_t(a.cand[j]) * a.ld_w + i] = dr[j];
-    }
-    const bool dense = a.top_k <= 0;  // host passes the effective k = min(top_k, n_cand)
-    if (dense) {
+    if (a.dist_user)
+      for (int j = lane; j < n_cand; j += 32) a.dist_user[int64_t(cand[j]) * a.ld_w + i] = dr[j];
+    if (a.top_k <= 0) {
       double mn = DBL_MAX;
       for (int j = lane; j < n_cand; j += 32) mn = fmin(mn, dr[j]);
       mn = warp_min_d(mn);
@@ -130,13 +137,13 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
       for (int j = lane; j < n_cand; j += 32) sum += exp(-(dr[j] - mn));
       sum = warp_sum_d(sum);
       for (int sl = lane; sl < a.cap; sl += 32) {
-        const int j = a.slot2cand[sl];
+        const int j = slot2cand[sl];
         a.W[int64_t(sl) * a.ld_w + i] = j >= 0 ? float(exp(-(dr[j] - mn)) / sum) : 0.f;
       }
     } else {
       // top-k: k rounds of lexicographic (distance, slot) argmin over the unselected
       const int k = a.top_k;
-      double sel_d = 0.0;   // lane r < k keeps the r-th selected distance / slot
+      double sel_d = 0.0;  // lane r < k keeps the r-th selected distance / slot
       int sel_s = -1;
       double prev_d = -1.0;
       int prev_s = -1;
@@ -147,7 +154,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
         int bs = INT32_MAX;
         for (int j = lane; j < n_cand; j += 32) {
           const double dj = dr[j];
-          const int sj = a.cand[j];
+          const int sj = cand[j];
           // unselected == strictly after (prev_d, prev_s) in the lexicographic order
           const bool after = (prev_s < 0) || key_less(prev_d, prev_s, dj, sj);
           if (after && key_less(dj, sj, bd, bs)) { bd = dj; bs = sj; }
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
         prev_s = bs;
       }
       const double mn = __shfl_sync(0xffffffffu, sel_d, 0);
-      double ev = (lane < k) ? exp(-(sel_d - mn)) : 0.0;
+      const double ev = (lane < k) ? exp(-(sel_d - mn)) : 0.0;
       const double sum = warp_sum_d(ev);
       for (int sl = lane; sl < a.cap; sl += 32) a.W[int64_t(sl) * a.ld_w + i] = 0.f;
       __syncwarp();
@@ -174,18 +181,18 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(MatchArgs a, 
         a.W[int64_t(sel_s) * a.ld_w + i] = float(ev / sum);
         if (a.idx) a.idx[int64_t(i) * k + lane] = sel_s;
       }
-      if (lane == 0 && tie) atomicAdd(a.tie_count, 1);
+      if (lane == 0 && tie) atomicAdd(&ties[jb], 1);
     }
   }
 
-  // deterministic per-block partial sums of distances for d̄
+  // deterministic per-block partial sums (Σ d² for Frobenius, Σ d for mean-ℓ2)
   for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
     double s = 0.0;
     for (int p = 0; p < np; ++p) {
       const double dv = sd[p * n_cand + j];
       s += a.scalar_mode == 0 ? dv * dv : dv;
     }
-    a.partial[int64_t(blockIdx.x) * n_cand + j] = s;
+    a.partial[int64_t(lb) * n_cand + j] = s;
   }
 }
 
@@ -204,55 +211,60 @@ __device__ double block_reduce_1024(double* buf, double v) {
   return r;
 }
 
-__global__ void __launch_bounds__(1024) match_finalize_kernel(MatchArgs a, int n_blocks, double gamma,
-                                                              float* wbar, MatchResultDev* res) {
+// One block (1024 threads) per job: d̄, w̄, H and the verdict.
+__global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  const MatchJob& a = reinterpret_cast<const MatchJob*>(tab + hdr->job_off)[blockIdx.x];
+  const int32_t* ints = reinterpret_cast<const int32_t*>(tab + hdr->int_off);
+  MatchResultDev* res = reinterpret_cast<MatchResultDev*>(tab + hdr->res_off) + blockIdx.x;
+  const int32_t* ties = reinterpret_cast<const int32_t*>(tab + hdr->tie_off);
   __shared__ double buf[1024];
-  __shared__ double wsh[kMaxCapDev];
+  __shared__ double dsh[kMaxCapDev];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per candidate: lanes stride over the position blocks in a fixed order, then a
+  // butterfly (identical in every lane, deterministic)
+  for (int j = warp; j < a.n_cand; j += 32) {
+    double s = 0.0;
+    for (int b = lane; b < a.n_blocks; b += 32) s += a.partial[int64_t(b) * a.n_cand + j];
+    s = warp_sum_d(s);
+    if (lane == 0) dsh[j] = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
+  }
+  __syncthreads();
   const int j = threadIdx.x;
   const bool valid = j < a.n_cand;
-  double dbar = 0.0;
-  if (valid) {
-    double s = 0.0;
-    for (int b = 0; b < n_blocks; ++b) s += a.partial[int64_t(b) * a.n_cand + j];
-    dbar = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
-  }
+  const double dbar = valid ? dsh[j] : 0.0;
   const double mn = block_reduce_1024<true>(buf, valid ? dbar : DBL_MAX);
   const double e = valid ? exp(-(dbar - mn)) : 0.0;
   const double S = block_reduce_1024<false>(buf, e);
   const double w = e / S;
   const double t = (valid && w > 0.0) ? -w * log(w) : 0.0;
   const double H = block_reduce_1024<false>(buf, t);
-  if (valid) wsh[j] = w;
+  if (valid) dsh[j] = w;
   __syncthreads();
+  const int32_t* slot2cand = ints + a.s2c_off;
   for (int sl = threadIdx.x; sl < a.cap; sl += blockDim.x) {
-    const int jj = a.slot2cand[sl];
-    wbar[sl] = jj >= 0 ? float(wsh[jj]) : 0.f;
+    const int jj = slot2cand[sl];
+    a.wbar[sl] = jj >= 0 ? float(dsh[jj]) : 0.f;
   }
   if (threadIdx.x == 0) {
-    const double thr = gamma * log(double(a.n_cand));
+    const double thr = a.gamma * log(double(a.n_cand));
     res->entropy = H;
     res->threshold = thr;
     res->verdict = H > thr ? 1 : 0;
     res->tie_flag = fabs(H - thr) <= kTieRel * thr ? 1 : 0;
-    res->tie_count = *a.tie_count;
+    res->tie_count = ties[blockIdx.x];
   }
 }
 
-cudaError_t launch_match(const MatchArgs& a, int P, cudaStream_t s) {
-  const int n_blocks = (a.L_phi + P - 1) / P;
-  const size_t smem = ((size_t(P) * a.De * 2 + 15) & ~size_t(15)) + size_t(P) * a.n_cand * sizeof(double);
+cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
   }
-  match_dist_kernel<<<n_blocks, kMatchThreads, smem, s>>>(a, P);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_match_finalize(const MatchArgs& a, int n_blocks, double gamma, float* wbar,
-                                  MatchResultDev* res, cudaStream_t s) {
-  match_finalize_kernel<<<1, 1024, 0, s>>>(a, n_blocks, gamma, wbar, res);
+  uint8_t* t = reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev));
+  match_dist_kernel<<<hdr.total_blocks, kMatchThreads, smem, s>>>(t);
+  match_finalize_kernel<<<hdr.n_jobs, 1024, 0, s>>>(t);
   return cudaGetLastError();
 }
 

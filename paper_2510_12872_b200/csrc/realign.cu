@@ -1,4 +1,5 @@
-// Fused anchor-offset blend + RoPE-δ + add (SURVEY §8(a) a4+a5):
+// Fused anchor-offset blend + RoPE-δ + add (SURVEY §8(a) a4+a5), plus the verbatim
+// copies of the concatenation step (a6):
 //
 //   K̂[l,h,i,:] = R_δ( K_base[l,h,i,:] + Σ_j w[i,j] ΔK_j[l,h,i,:] )     (Eq. 6 P:289 / Eq. 7 P:297,
 //   V̂[l,h,i,:] =      V_base[l,h,i,:] + Σ_j w[i,j] ΔV_j[l,h,i,:]        alignment P:141)
@@ -8,17 +9,22 @@
 //   * one persistent CTA per SM walks a static round-robin list of work units
 //     (segment, layer, head, K|V plane, 16 KiB tile of token rows);
 //   * warp 8 (one elected lane) is the TMA producer: for every unit it streams the
-//     k anchor tiles (and, for placeholders, the matching 256-byte weight slice)
-//     and finally the base tile into an NSTAGE-deep shared-memory ring with
-//     cp.async.bulk (UBLKCP) + mbarrier complete_tx, L2 evict-first;
+//     k anchor tiles (each with the matching weight slice) and finally the base
+//     tile into an 11-deep shared-memory ring with cp.async.bulk (UBLKCP) +
+//     mbarrier complete_tx, L2 evict-first;
 //   * warps 0-7 consume: each thread owns two 32-byte "items" (8 elements of the
 //     first half of a row and the matching 8 of the second half, so the
 //     rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
-//     registers, and on the base tile adds, rotates (K only) and stores bf16 (RNE)
-//     straight to the destination prompt cache.
+//     registers; on the base tile it adds, rotates (K only), rounds to bf16 (RNE)
+//     in place in shared memory, and one thread writes the whole tile back with a
+//     single TMA bulk store (cp.async.bulk.global.shared), which measured 2-3 %
+//     faster than per-thread STG (profiles/).
+//   * COPY segments (n_cand = 0, δ = 0) move rows verbatim through the same ring
+//     (bit-exact: no arithmetic is applied), so p_(m,0) rides in the same launch.
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 #include "kvcomm_internal.h"
 #include "ptx.cuh"
 
@@ -27,8 +33,9 @@ namespace kvc {
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kNStage = 11;
-constexpr int kItems = kStageBytes / 32;                  // 512 items of 32 B per stage
+constexpr int kItems = kStageBytes / 32;                         // 512 items of 32 B per stage
 constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);  // 2
+constexpr int kConsumerBar = 1;                                  // named barrier id (consumers only)
 
 static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
 
@@ -49,6 +56,8 @@ struct Unit {
   int s, l, h, p, t;
 };
 
+// unit -> (segment, layer, head, plane, tile); tile fastest so that neighbouring
+// CTAs stream neighbouring 16 KiB tiles of the same anchor at the same time.
 __device__ __forceinline__ Unit decode_unit(const SegDev* segs, int n_seg, int Hs, int64_t u) {
   Unit r;
   r.s = find_segment(segs, n_seg, u);
@@ -75,12 +84,14 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
   const int s = blockIdx.x;
   const SegDev& g = segs[s];
   const int half = hdr->d / 2;
-  for (int f = threadIdx.x; f < half; f += blockDim.x) {
-    double sn, cn;
-    sincos(double(g.delta) * g.inv_freq[f], &sn, &cn);
-    cs[g.cs_off + f] = make_float2(float(cn), float(sn));
+  if (g.delta != 0) {
+    for (int f = threadIdx.x; f < half; f += blockDim.x) {
+      double sn, cn;
+      sincos(double(g.delta) * g.inv_freq[f], &sn, &cn);
+      cs[g.cs_off + f] = make_float2(float(cn), float(sn));
+    }
   }
-  if (!g.w_by_slot) {
+  if (!g.w_by_slot && g.n_cand > 0) {
     const int ld = int(g.ld_w);
     for (int x = threadIdx.x; x < g.n_cand * ld; x += blockDim.x) {
       const int j = x / ld;
@@ -89,7 +100,9 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __restrict__ tab) {
+// variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
+// of the TMA bulk store; bit1 = skip output stores (bandwidth probe only, wrong results).
+__global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __restrict__ tab, int variant) {
   const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
   const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr.cand_off);
@@ -117,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
   const int rpt = hdr.rows_per_tile;
   const int64_t total = hdr.total_units;
   const int row_bytes = 2 * d;
+  const bool tma_store = !(variant & 3);
 
   if (warp == kConsumerWarps) {
     // ---------------- TMA producer (one lane) ----------------
@@ -205,16 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
 
     // base tile: add, rotate (K), round, store
     mbar_wait(&full[stage], phase);
-    {
-      const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
-      const int64_t lh = int64_t(un.l) * Hs + un.h;
-      bf16* dst = g.dst[un.p];
-      float* dbg = g.dbg[un.p];
+    uint8_t* buf = sdata + size_t(stage) * kStageBytes;
+    const int64_t lh = int64_t(un.l) * Hs + un.h;
+    const bool rotate = un.p == 0 && g.delta != 0;
+    if (n_cand > 0 || rotate) {  // COPY segments leave the staged rows untouched (bit-exact)
 #pragma unroll
       for (int q = 0; q < kItemsPerThread; ++q) {
         if (irow[q] >= nrows) continue;
-        const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
-        const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+        uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
+        uint8_t* pb = pa + d;
+        const uint4 a = lds128(pa);
+        const uint4 b = lds128(pb);
         const uint32_t av[4] = {a.x, a.y, a.z, a.w};
         const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
         float y0[8], y1[8];
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
           y1[2 * e] = bf_lo(bv[e]) + acc[q][8 + 2 * e];
           y1[2 * e + 1] = bf_hi(bv[e]) + acc[q][8 + 2 * e + 1];
         }
-        if (un.p == 0) {
+        if (rotate) {
           const float2* csr = cs + g.cs_off + ivec[q] * 8;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -235,14 +250,20 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
             y1[e] = x1 * r.x + x0 * r.y;
           }
         }
-        const int64_t orow = lh * g.dst_ld + g.target_start + i0 + irow[q];
-        bf16* o = dst + orow * d + ivec[q] * 8;
-        stg128_cs(o, make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),
-                                pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7])));
-        stg128_cs(o + d / 2, make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
-                                        pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7])));
-        if (dbg != nullptr) {
-          float* od = dbg + (lh * g.L_seg + i0 + irow[q]) * d + ivec[q] * 8;
+        const uint4 r0 = make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),
+                                    pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7]));
+        const uint4 r1 = make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
+                                    pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7]));
+        if (tma_store) {
+          sts128(pa, r0);  // in place; the whole tile leaves with one bulk store below
+          sts128(pb, r1);
+        } else if (!(variant & 2)) {
+          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + irow[q]) * d + ivec[q] * 8;
+          stg128_cs(o, r0);
+          stg128_cs(o + d / 2, r1);
+        }
+        if (g.dbg[un.p] != nullptr) {
+          float* od = g.dbg[un.p] + (lh * g.L_seg + i0 + irow[q]) * d + ivec[q] * 8;
           float4* o0 = reinterpret_cast<float4*>(od);
           float4* o1 = reinterpret_cast<float4*>(od + d / 2);
           o0[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
@@ -251,11 +272,34 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
           o1[1] = make_float4(acc[q][12], acc[q][13], acc[q][14], acc[q][15]);
         }
       }
+    } else if (!tma_store && !(variant & 2)) {
+#pragma unroll
+      for (int q = 0; q < kItemsPerThread; ++q) {
+        if (irow[q] >= nrows) continue;
+        const uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
+        bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + irow[q]) * d + ivec[q] * 8;
+        stg128_cs(o, lds128(pa));
+        stg128_cs(o + d / 2, lds128(pa + d));
+      }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (tma_store) {
+      // all consumer writes of the tile -> visible to the async proxy, then one bulk store;
+      // the stage is released only once the store has finished reading shared memory
+      fence_proxy_async_smem();
+      named_bar_sync(kConsumerBar, kConsumerWarps * 32);
+      if (threadIdx.x == 0) {
+        bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
+        bulk_s2g(o, buf, uint32_t(nrows) * row_bytes);
+        bulk_wait_read_all();
+        mbar_arrive_cnt(&empty[stage], kConsumerWarps);
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+    }
     if (++stage == kNStage) { stage = 0; phase ^= 1u; }
   }
+  if (tma_store && threadIdx.x == 0) bulk_wait_all();  // global writes complete before exit
 }
 
 int realign_grid_size(int device) {
@@ -264,10 +308,9 @@ int realign_grid_size(int device) {
   return sms > 0 ? sms : 148;
 }
 
-cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int n_prefix_segments, int grid,
-                           cudaStream_t s) {
-  (void)n_prefix_segments;
+cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
+  static int variant = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
@@ -276,10 +319,15 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int n_pre
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
+  if (variant < 0) {
+    const char* v = getenv("KVCOMM_REALIGN_VARIANT");
+    variant = v ? atoi(v) : 0;
+  }
   realign_prep_kernel<<<hdr.n_seg, 128, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
-  realign_kernel<<<int(g), kThreads, realign_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(table_dev));
+  realign_kernel<<<int(g), kThreads, realign_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(table_dev),
+                                                                   variant);
   return cudaGetLastError();
 }
 

@@ -19,12 +19,12 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import (ALL_CONSUMERS, NEW_ANCHOR, OFFSET_GIVEN, OFFSET_MEASURE, PLACEHOLDER, PREFIX, SHAREABLE,
-                   KVCommError)
+from ._lib import (ALL_CONSUMERS, COPY, NEW_ANCHOR, OFFSET_GIVEN, OFFSET_MEASURE, PLACEHOLDER, PREFIX,
+                   SHAREABLE, KVCommError)
 
 __all__ = ["AnchorPool", "OffsetGiven", "OffsetMeasure", "Match", "Segment", "realign_segments",
            "realign_segment", "prepare_segments", "realign_prepared", "concat_prefill_cache", "kernel_launch_count", "KVCommError", "ALL_CONSUMERS",
-           "SHAREABLE", "NEW_ANCHOR", "PLACEHOLDER", "PREFIX"]
+           "SHAREABLE", "NEW_ANCHOR", "PLACEHOLDER", "PREFIX", "COPY", "match_many"]
 
 
 def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
@@ -213,14 +213,13 @@ class AnchorPool:
         return tuple(out)
 
     # -- a1-a3 ---------------------------------------------------------------
-    def match(self, query_emb: torch.Tensor, consumer: int = ALL_CONSUMERS, gamma: float = 0.3, top_k: int = 0,
-              want_dist: bool = False, ld_w: Optional[int] = None, out: Optional[Match] = None,
-              stream=None) -> Match:
+    def _match_request(self, query_emb: torch.Tensor, consumer: int, gamma: float, top_k: int, want_dist: bool,
+                       ld_w: Optional[int], out: Optional[Match]):
         if query_emb.dim() != 2 or query_emb.shape[1] != self.De or query_emb.dtype != torch.bfloat16 \
                 or not query_emb.is_contiguous():
             raise ValueError("query_emb must be a contiguous bf16 [L_phi, D_e] tensor")
         L_phi = query_emb.shape[0]
-        if out is not None and out.W is not None:
+        if out is not None and out.W is not None and out.W.shape[1] >= L_phi:
             W, wbar, idx, dist = out.W, out.wbar, out.idx, out.dist
             ld_w = W.shape[1]
         else:
@@ -230,16 +229,45 @@ class AnchorPool:
             idx = torch.zeros(L_phi, max(top_k, 1), dtype=torch.int32, device=self.device) if top_k else None
             dist = torch.zeros(self.capacity, ld_w, dtype=torch.float64, device=self.device) if want_dist else None
         info = L.MatchInfo()
-        L.check(L.lib().kvcomm_match_anchors(self.handle, query_emb.data_ptr(), L_phi, consumer, float(gamma),
-                                             int(top_k), W.data_ptr(), ld_w,
-                                             idx.data_ptr() if idx is not None else None, wbar.data_ptr(),
-                                             dist.data_ptr() if dist is not None else None, C.byref(info),
-                                             _stream_handle(stream)))
+        req = L.MatchRequest(self.handle, query_emb.data_ptr(), L_phi, consumer, float(gamma), int(top_k),
+                             W.data_ptr(), ld_w, idx.data_ptr() if idx is not None else None, wbar.data_ptr(),
+                             dist.data_ptr() if dist is not None else None, C.pointer(info))
+        return req, info, (L_phi, W, wbar, idx, dist)
+
+    @staticmethod
+    def _match_result(info, bufs) -> Match:
+        L_phi, W, wbar, idx, dist = bufs
         cands = list(info.candidates[: info.n_candidates])
         if idx is not None and info.top_k < idx.shape[1] and info.n_candidates > 0:
             idx = idx.view(-1)[: L_phi * info.top_k].view(L_phi, info.top_k)
         return Match(info.verdict, L.REASONS[info.reason], cands, info.top_k, info.entropy, info.threshold,
                      bool(info.verdict_in_tie_band), info.tie_band_count, W, wbar, idx, dist)
+
+    def match(self, query_emb: torch.Tensor, consumer: int = ALL_CONSUMERS, gamma: float = 0.3, top_k: int = 0,
+              want_dist: bool = False, ld_w: Optional[int] = None, out: Optional[Match] = None,
+              stream=None) -> Match:
+        req, info, bufs = self._match_request(query_emb, consumer, gamma, top_k, want_dist, ld_w, out)
+        L.check(L.lib().kvcomm_match_anchors(req.pool, req.query_emb, req.L_phi, req.consumer, req.gamma,
+                                             req.top_k, req.W, req.ld_w, req.idx, req.wbar, req.dist,
+                                             C.byref(info), _stream_handle(stream)))
+        return self._match_result(info, bufs)
+
+
+def match_many(items: Sequence[Tuple["AnchorPool", torch.Tensor]], consumer: int = ALL_CONSUMERS,
+               gamma: float = 0.3, top_k: int = 0, outs: Optional[Sequence[Optional[Match]]] = None,
+               want_dist: bool = False, stream=None) -> List[Match]:
+    """Match several (pool, query) pairs with one device synchronisation
+    (kvcomm_match_anchors_batch); each pool at most once."""
+    outs = outs or [None] * len(items)
+    reqs, infos, bufs = [], [], []
+    for (pool, q), o in zip(items, outs):
+        r, i, b = pool._match_request(q, consumer, gamma, top_k, want_dist, None, o)
+        reqs.append(r)
+        infos.append(i)
+        bufs.append(b)
+    arr = (L.MatchRequest * max(len(reqs), 1))(*reqs)
+    L.check(L.lib().kvcomm_match_anchors_batch(arr, len(reqs), _stream_handle(stream)))
+    return [AnchorPool._match_result(i, b) for i, b in zip(infos, bufs)]
 
 
 @dataclass
@@ -247,8 +275,8 @@ class Segment:
     """One segment to realign (Eq. 6 placeholder / Eq. 7 prefix + RoPE δ)."""
     pool: AnchorPool
     consumer: int
-    kind: int                         # PLACEHOLDER | PREFIX
-    weights: torch.Tensor             # PLACEHOLDER: Match.W [capacity, ld_w]; PREFIX: Match.wbar [capacity]
+    kind: int                         # PLACEHOLDER | PREFIX | COPY
+    weights: Optional[torch.Tensor]   # PLACEHOLDER: Match.W [capacity, ld_w]; PREFIX: Match.wbar; COPY: None
     candidates: Sequence[int]
     base_k: torch.Tensor              # [Ls, Hs, >=L_seg, d]
     base_v: torch.Tensor
@@ -264,16 +292,18 @@ class Segment:
         L_seg = self.base_k.shape[2] if self.L_seg is None else self.L_seg
         cand = (C.c_int32 * max(len(self.candidates), 1))(*self.candidates)
         keep.append(cand)
-        if self.weights.dtype != torch.float32 or not self.weights.is_cuda:
+        if self.kind != COPY and (self.weights is None or self.weights.dtype != torch.float32
+                                  or not self.weights.is_cuda):
             raise ValueError("weights must be fp32 CUDA")
         ld_w = self.weights.shape[1] if self.kind == PLACEHOLDER else 0
+        wptr = self.weights.data_ptr() if self.weights is not None else None
         dst_ld = _rows_ld(self.dst_k, "dst_k")
         if _rows_ld(self.dst_v, "dst_v") != dst_ld:
             raise ValueError("dst_k/dst_v strides differ")
         for t in (self.debug_k, self.debug_v):
             if t is not None and (t.dtype != torch.float32 or not t.is_contiguous()):
                 raise ValueError("debug buffers must be contiguous fp32")
-        return L.RealignDesc(self.pool.handle, self.consumer, self.kind, self.weights.data_ptr(), ld_w, cand,
+        return L.RealignDesc(self.pool.handle, self.consumer, self.kind, wptr, ld_w, cand,
                              len(self.candidates), L_seg, _view(self.base_k, self.base_v, what="base"),
                              self.base_start, self.target_start, self.dst_k.data_ptr(), self.dst_v.data_ptr(),
                              dst_ld, self.debug_k.data_ptr() if self.debug_k is not None else None,
@@ -318,4 +348,5 @@ def concat_prefill_cache(parts: Sequence[Tuple[int, int, Optional[torch.Tensor],
     for i, (start, length, sk, sv) in enumerate(parts):
         refs[i] = L.SegmentRef(int(start), int(length), _view(sk, sv, what="concat src"))
     L.check(L.lib().kvcomm_concat_prefill_cache(refs, len(parts), N_total, Ls, Hs, d, dst_k.data_ptr(),
-                                                dst_v.data_ptr(), dst_ld, _stream_handle(stream)))
+                                                dst_v.data_ptr(), dst_ld, dst_k.device.index or 0,
+                                                _stream_handle(stream)))

@@ -1,18 +1,20 @@
 """Algorithm 1's reuse branch for all agents of one request.
 
-For every placeholder pool the sample is matched once (weights depend only on the
-sample and the pool, reading A21); every agent whose placeholders are all
-Shareable gets all its placeholder and prefix segments realigned in ONE persistent
-kernel launch (kvcomm_realign_segments), then its p_(m,0) rows are copied and the
-position ledger is checked (kvcomm_concat_prefill_cache).  Agents with any
-NewAnchor verdict take the dense fallback, which needs the model and is
-outside this library: they are reported, not processed.
+Every placeholder pool's sample is matched once, all pools in one batched launch
+with a single host synchronisation (weights depend only on the sample and the
+pool, reading A21; Alg. 1 evaluates Eq. 5 for every placeholder before branching,
+P:765).  Every agent whose placeholders are all Shareable gets all its placeholder
+and prefix segments realigned, and its p_(m,0) rows copied, in ONE persistent
+kernel launch (kvcomm_realign_segments with COPY segments); the position ledger of
+each prompt is then checked (kvcomm_concat_prefill_cache, nothing left to copy).
+Agents with any NewAnchor verdict take the dense fallback, which needs the
+model and is outside this library: they are reported, not processed.
 
 Host bookkeeping only; all arithmetic runs in libkvcomm's kernels.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Dict, List, Optional
 
 import torch
@@ -49,6 +51,7 @@ class RequestResult:
     fallback_agents: List[int]
     realigned_tokens: int
     blended_rows: int            # Σ_segments n_candidates * L_seg (for the byte model)
+    copied_tokens: int
 
 
 class ReuseRequest:
@@ -58,16 +61,16 @@ class ReuseRequest:
         self._match_out: Dict[str, Optional[K.Match]] = {n: None for n in pools}
 
     def match(self, queries: Dict[str, torch.Tensor], stream=None) -> Dict[str, K.Match]:
-        out = {}
-        for name, q in queries.items():
-            m = self.pools[name].match(q, consumer=K.ALL_CONSUMERS, gamma=self.gamma, top_k=self.top_k,
-                                       out=self._match_out[name], stream=stream)
-            self._match_out[name] = m
-            out[name] = m
+        names = list(queries)
+        ms = K.match_many([(self.pools[n], queries[n]) for n in names], consumer=K.ALL_CONSUMERS,
+                          gamma=self.gamma, top_k=self.top_k, outs=[self._match_out[n] for n in names],
+                          stream=stream)
+        out = dict(zip(names, ms))
+        self._match_out.update(out)
         return out
 
     def segments(self, matches: Dict[str, K.Match]):
-        segs, reused, fallback, toks, rows = [], [], [], 0, 0
+        segs, reused, fallback, toks, rows, copied = [], [], [], 0, 0, 0
         for a in self.agents:
             names = {s.pool for s in a.segments}
             if not all(matches[n].shareable for n in names):
@@ -81,28 +84,31 @@ class ReuseRequest:
                                       s.base_start, s.target_start, a.dst_k, a.dst_v))
                 toks += s.base_k.shape[2]
                 rows += s.base_k.shape[2] * len(m.candidates)
-        return segs, reused, fallback, toks, rows
+            if a.p0_k.shape[2] > 0:   # p_(m,0) copied verbatim in the same launch (reading A20)
+                segs.append(K.Segment(self.pools[a.segments[0].pool], 0, K.COPY, None, [], a.p0_k, a.p0_v, 0, 0,
+                                      a.dst_k, a.dst_v))
+                copied += a.p0_k.shape[2]
+        return segs, reused, fallback, toks, rows, copied
 
     def realign(self, segs, stream=None) -> None:
         K.realign_segments(segs, stream=stream)
 
-    def concat(self, reused: List[int], stream=None) -> None:
+    def check_ledger(self, reused: List[int], stream=None) -> None:
         for a in self.agents:
             if a.agent not in reused:
                 continue
-            p0 = a.p0_k.shape[2]
-            parts = [(0, p0, a.p0_k, a.p0_v)]
+            parts = [(0, a.p0_k.shape[2], None, None)]
             for s in sorted(a.segments, key=lambda s: s.target_start):
                 parts.append((s.target_start, s.base_k.shape[2], None, None))
             K.concat_prefill_cache(parts, a.N, a.dst_k, a.dst_v, stream=stream)
 
     def run(self, queries: Dict[str, torch.Tensor], stream=None) -> RequestResult:
         matches = self.match(queries, stream)
-        segs, reused, fallback, toks, rows = self.segments(matches)
+        segs, reused, fallback, toks, rows, copied = self.segments(matches)
+        self.check_ledger(reused, stream)      # host-only: raises before any launch on a bad layout
         if segs:
             self.realign(segs, stream)
-        self.concat(reused, stream)
         for name, m in matches.items():            # reading A18: +1 per Shareable turn
             if m.shareable:
                 self.pools[name].record_access(m.candidates)
-        return RequestResult(matches, reused, fallback, toks, rows)
+        return RequestResult(matches, reused, fallback, toks, rows, copied)

@@ -75,7 +75,7 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
     p0k = synth.randn_bf16((p.L, p.H, p0, p.d), g).to(dev)
     p0v = synth.randn_bf16((p.L, p.H, p0, p.d), g).to(dev)
     K.concat_prefill_cache([(0, p0, p0k, p0v), (p0, p.L_phi, None, None), (p0 + p.L_phi, P, None, None)], N,
-                           dst_k, dst_v)
+                           dst_k, dst_v)   # copies p_(m,0) through the realign kernel's TMA ring
     torch.cuda.synchronize()
     out.update(dst_k=dst_k.cpu(), dst_v=dst_v.cpu(), dbg_k=dbg[0].cpu(), dbg_v=dbg[1].cpu(),
                dbgp_k=dbgp[0].cpu(), dbgp_v=dbgp[1].cpu(), p0k=p0k.cpu(), p0v=p0v.cpu(), N=N)

@@ -36,7 +36,7 @@ def test_ctypes_layout_matches_c_header():
 #define O(T, f) printf(#T "." #f " %zu\n", offsetof(T, f));
 int main(void) {
   S(kvcomm_pool_config) S(kvcomm_kv_view) S(kvcomm_offset_desc) S(kvcomm_slot_info)
-  S(kvcomm_match_info) S(kvcomm_realign_desc) S(kvcomm_segment_ref)
+  S(kvcomm_match_info) S(kvcomm_realign_desc) S(kvcomm_segment_ref) S(kvcomm_match_request)
   O(kvcomm_pool_config, prefix_len) O(kvcomm_pool_config, inv_freq)
   O(kvcomm_match_info, entropy) O(kvcomm_match_info, tie_band_count)
   O(kvcomm_realign_desc, base) O(kvcomm_realign_desc, dst_k) O(kvcomm_realign_desc, debug_delta_v)
@@ -53,7 +53,7 @@ int main(void) {
     got = dict(l.split() for l in lines if l.strip())
     py = {"kvcomm_pool_config": L.PoolConfig, "kvcomm_kv_view": L.KVView, "kvcomm_offset_desc": L.OffsetDesc,
           "kvcomm_slot_info": L.SlotInfo, "kvcomm_match_info": L.MatchInfo, "kvcomm_realign_desc": L.RealignDesc,
-          "kvcomm_segment_ref": L.SegmentRef}
+          "kvcomm_segment_ref": L.SegmentRef, "kvcomm_match_request": L.MatchRequest}
     for k, T in py.items():
         assert int(got[k]) == C.sizeof(T), k
     for key, v in got.items():
@@ -72,14 +72,14 @@ def test_status_strings_and_error_message():
 def test_concat_ledger_errors_before_any_device_work():
     lib = L.load()
     refs = (L.SegmentRef * 2)(L.SegmentRef(0, 3, L.KVView()), L.SegmentRef(4, 6, L.KVView()))
-    st = lib.kvcomm_concat_prefill_cache(refs, 2, 10, 2, 2, 16, None, None, 10, None)
+    st = lib.kvcomm_concat_prefill_cache(refs, 2, 10, 2, 2, 16, None, None, 10, 0, None)
     assert L.STATUS_NAMES[st] == "POSITION_GAP"
     assert b"gap at position 3" in lib.kvcomm_last_error_message()
     refs = (L.SegmentRef * 2)(L.SegmentRef(0, 4, L.KVView()), L.SegmentRef(3, 7, L.KVView()))
-    st = lib.kvcomm_concat_prefill_cache(refs, 2, 10, 2, 2, 16, None, None, 10, None)
+    st = lib.kvcomm_concat_prefill_cache(refs, 2, 10, 2, 2, 16, None, None, 10, 0, None)
     assert L.STATUS_NAMES[st] == "POSITION_OVERLAP"
     refs = (L.SegmentRef * 1)(L.SegmentRef(0, 4, L.KVView()))
-    st = lib.kvcomm_concat_prefill_cache(refs, 1, 10, 2, 2, 16, None, None, 10, None)
+    st = lib.kvcomm_concat_prefill_cache(refs, 1, 10, 2, 2, 16, None, None, 10, 0, None)
     assert L.STATUS_NAMES[st] == "POSITION_GAP"
 
 

@@ -223,3 +223,50 @@ def test_determinism_and_batch_equals_single_and_layer_sharding():
         torch.cuda.synchronize()
         assert torch.equal(dk[:, :, 50:].cpu(), full1["dst_k"][lb:le, :, 50:])
         assert torch.equal(dv[:, :, 50:].cpu(), full1["dst_v"][lb:le, :, 50:])
+
+
+def test_copy_segments_are_bit_exact_for_any_bit_pattern():
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(3)
+    pool = K.AnchorPool(num_layers=3, num_kv_heads=2, head_dim=128, emb_dim=16, capacity=1, max_anchor_len=8,
+                        prefix_len=[0], inv_freq=synth.llama3_inv_freq(128))
+    bits = torch.randint(-32768, 32767, (2, 3, 2, 150, 128), generator=g, dtype=torch.int16)
+    bits[0, 0, 0, 0, :4] = torch.tensor([-32768, 0x7fc0, 0x7f80, -0x0080], dtype=torch.int16)  # -0, NaN, inf, -inf
+    src_k = bits[0].view(torch.bfloat16).to(dev)
+    src_v = bits[1].view(torch.bfloat16).to(dev)
+    dk = torch.zeros(3, 2, 170, 128, dtype=torch.bfloat16, device=dev)
+    dv = torch.zeros_like(dk)
+    K.realign_segment(K.Segment(pool, 0, K.COPY, None, [], src_k, src_v, 0, 20, dk, dv))
+    torch.cuda.synchronize()
+    assert torch.equal(dk[:, :, 20:].view(torch.int16).cpu(), bits[0])
+    assert torch.equal(dv[:, :, 20:].view(torch.int16).cpu(), bits[1])
+    assert torch.all(dk[:, :, :20].view(torch.int16) == 0)
+    # concat uses the same path
+    ek = torch.zeros(3, 2, 150, 128, dtype=torch.bfloat16, device=dev)
+    ev = torch.zeros_like(ek)
+    K.concat_prefill_cache([(0, 150, src_k, src_v)], 150, ek, ev)
+    torch.cuda.synchronize()
+    assert torch.equal(ek.view(torch.int16).cpu(), bits[0]) and torch.equal(ev.view(torch.int16).cpu(), bits[1])
+
+
+def test_match_many_equals_individual_matches():
+    dev = torch.device("cuda", 0)
+    probs = [synth.make_problem(40 + i, L=2, H=2, d=64, D_e=128, L_phi=L, anchor_lens=[L, L + 9, L + 30],
+                                prefix_lens=[8], target_start=4, pf_base_start=4)
+             for i, L in enumerate([33, 70, 129])]
+    pools = []
+    for p in probs:
+        pool = K.AnchorPool(num_layers=2, num_kv_heads=2, head_dim=64, emb_dim=128, capacity=3,
+                            max_anchor_len=max(p.anchor_lens), prefix_len=[8], inv_freq=p.inv_freq)
+        for j in range(3):
+            pool.insert(p.emb_anchor[j].to(dev), [K.OffsetGiven(0, p.dk_ph[0][j].to(dev), p.dv_ph[0][j].to(dev),
+                                                                p.dk_pf[0][j].to(dev), p.dv_pf[0][j].to(dev))])
+        pools.append(pool)
+    qs = [p.emb_query.to(dev) for p in probs]
+    many = K.match_many(list(zip(pools, qs)), gamma=0.5, want_dist=True)
+    for pool, q, m in zip(pools, qs, many):
+        one = pool.match(q, gamma=0.5, want_dist=True)
+        assert m.candidates == one.candidates and m.verdict == one.verdict and m.entropy == one.entropy
+        assert torch.equal(m.W, one.W) and torch.equal(m.wbar, one.wbar) and torch.equal(m.dist, one.dist)
+    with pytest.raises(K.KVCommError, match="twice"):
+        K.match_many([(pools[0], qs[0]), (pools[0], qs[0])])
