@@ -260,58 +260,53 @@ def main():
             else:
                 full.append((None, None))
 
-    ev_r0 = torch.cuda.Event(enable_timing=True)
-    ev_r1 = torch.cuda.Event(enable_timing=True)
-    realign_ms = []
-    info = {}
+    plan = req.plan                      # native executor: 1 match launch + 1 gated realign launch per step
+    qlist = [st.queries[n] for n in req.names]
+    agents_all = [a.agent for a in st.agents]
 
-    def step(time_realign=False):
-        ms = req.match(st.queries, stream)
-        segs, reused, fallback, toks, rows, copied = req.segments(ms)
-        req.check_ledger(reused, stream)           # host-only position ledger (a6)
-        prep = kv.prepare_segments(segs)          # host marshalling before the event
-        if time_realign:
-            ev_r0.record(stream)
-        kv.realign_prepared(prep, stream)         # a4+a5 for every segment + p_(m,0) copies: ONE launch
-        if time_realign:
-            ev_r1.record(stream)
+    def step(events=None):
+        if events is not None:
+            plan.set_events(*events)     # recorded right before / after the realign launch
+        plan.run(qlist, sync=False, stream=stream)   # no host synchronisation inside a step
         if world > 1:
-            shard.gather_to_consumers([a.agent for a in st.agents], [(a.dst_k, a.dst_v) for a in st.agents],
-                                      full, w.L, rank, world)
-        info.update(toks=toks, rows=rows, copied=copied, reused=reused, fallback=fallback, n_seg=len(segs))
-        return toks
+            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    res = req.results()
     if args.profile:
         torch.cuda.profiler.start()
         for _ in range(args.steps):
             step()
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
-        print(json.dumps({"profile_steps": args.steps, "segments": info["n_seg"], "rows": info["rows"]}))
+        print(json.dumps({"profile_steps": args.steps, "rows": res.blended_rows}))
         return
-    if info["fallback"]:
-        raise SystemExit(f"agents {info['fallback']} took the fallback branch; the bench needs all Shareable")
+    if res.fallback_agents:
+        raise SystemExit(f"agents {res.fallback_agents} took the fallback branch; the bench needs all Shareable")
     # per-launch realign bytes: (k + 2) rows of d*2 bytes per (token, layer, head, plane)
     # + the p_(m,0) rows the same launch copies (read + write)
-    alg_bytes = (info["rows"] + 2 * info["toks"] + 2 * info["copied"]) * Ls * row_bytes * 2
+    alg_bytes = (res.blended_rows + 2 * res.realigned_tokens + 2 * res.copied_tokens) * Ls * row_bytes * 2
 
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     n_launch0 = kv.kernel_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            step(time_realign=True)
-            e1.record(stream)
-            e1.synchronize()
-            realign_ms.append(ev_r0.elapsed_time(ev_r1))
+        for i in range(args.steps):
+            step(evs[i])
+        e1.record(stream)
         torch.cuda.synchronize()
+    plan.set_events(None, None)
     n_launch = kv.kernel_launch_count() - n_launch0
+    res = req.results()
+    if res.fallback_agents:
+        raise SystemExit(f"agents {res.fallback_agents} took the fallback branch during the timed steps")
+    realign_ms = [a.elapsed_time(b) for a, b in evs]
     elapsed = e0.elapsed_time(e1)  # ms
     if world > 1:
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
@@ -391,7 +386,8 @@ def main():
                        "realigned_tokens_per_step": total_tokens, "anchors_blended": w.capacity,
                        "gamma": args.gamma, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
                        "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed},
-            "roofline": {"kernel": "kvc::realign_kernel (+prep; realign of 30 segments + 5 p0 copies)", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": "kvc::realign_kernel (30 segments + 5 p0 copies, one launch)", "bound": "hbm",
+                         "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,

@@ -292,6 +292,71 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
                                                      int32_t d, void* dst_k, void* dst_v,
                                                      int64_t dst_ld, int32_t device, void* stream);
 
+/* ---- request plan: Algorithm 1's reuse branch as one native executor -------- */
+/* A plan fixes, for a multi-agent prompt layout, which placeholder pools are matched
+ * per request and which segments every agent realigns (Eq. 1: p_(m,0), φ_(m,1),
+ * p_(m,1), ...).  kvcomm_plan_run then issues, stream-ordered and without host
+ * synchronisation: the candidate filter (host), ONE batched match launch, and ONE
+ * realign launch covering every agent's placeholder, prefix and COPY (p_(m,0))
+ * segments.  The reuse/fallback branch of Alg. 1 is taken ON THE DEVICE:
+ * an agent's segments run only if every pool it depends on was matched Shareable
+ * (agents decided NewAnchor by the host-side length clause are skipped outright).
+ * Their prompt caches are left untouched and reported as fallback (dense prefill,
+ * P:784, is outside this library).  Every agent's segments must tile [0, N)
+ * exactly (checked at create).  The plan owns its W / w̄ buffers and two work
+ * tables, so one run may be in flight while the next is prepared. */
+typedef struct kvcomm_plan_s* kvcomm_plan_t;
+
+typedef struct {
+  kvcomm_pool_t pool;      /* each pool at most once per plan                           */
+  int32_t L_phi;           /* length of the sample matched against this pool per request */
+  int32_t consumer;        /* KVCOMM_ALL_CONSUMERS (weights shared by all consumers)    */
+  float gamma;             /* Eq. 5 threshold (paper default 0.3)                 */
+  int32_t top_k;           /* 0 = all candidates (paper)                                 */
+} kvcomm_plan_match;
+
+typedef struct {
+  int32_t agent;           /* index into the agents array                                */
+  int32_t match;           /* pool (index into matches) the segment belongs to; ignored
+                              for COPY                                                   */
+  int32_t kind;            /* PLACEHOLDER (L_seg == L_phi) | PREFIX | COPY               */
+  int32_t consumer;        /* consumer index of this (agent, slot) in the pool          */
+  kvcomm_kv_view base;     /* device [Ls,Hs,ld,d]: base cache (COPY: rows to copy)       */
+  int32_t L_seg;
+  int32_t base_start;
+  int32_t target_start;
+  int32_t _pad;
+} kvcomm_plan_segment;
+
+typedef struct {
+  int32_t N;               /* prompt length                                              */
+  int32_t _pad;
+  void* dst_k;             /* device bf16 [Ls,Hs,dst_ld,d]                               */
+  void* dst_v;
+  int64_t dst_ld;
+} kvcomm_plan_agent;
+
+KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, int32_t n_matches,
+                                            const kvcomm_plan_segment* segs, int32_t n_segs,
+                                            const kvcomm_plan_agent* agents, int32_t n_agents,
+                                            kvcomm_plan_t* out);
+KVCOMM_API kvcomm_status kvcomm_plan_destroy(kvcomm_plan_t plan);
+/* query_embs: host array of n_matches device pointers (bf16 [L_phi][D_e]).  sync != 0
+ * waits for the run to finish.  Pool metadata is read at call time. */
+KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t plan, const void* const* query_embs, int32_t sync,
+                                         void* stream);
+/* Waits for the last run and reports it: infos [n_matches], agent_reused [n_agents]
+ * (1 = realigned, 0 = fallback).  Either may be NULL. */
+KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t plan, kvcomm_match_info* infos,
+                                             int32_t* agent_reused);
+/* Optional CUDA events (cudaEvent_t, created by the caller) recorded on the run's
+ * stream immediately before and after the realign launch of every later run; NULL
+ * disables.  Lets a caller time the realign kernel alone inside a pipelined run. */
+KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before_realign, void* after_realign);
+/* Device pointers of the plan's weights for match `match` (W [capacity][ld_w], w̄). */
+KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, const float** W,
+                                             int64_t* ld_w, const float** wbar);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,7 +7,7 @@ fails loudly if the library has not been built.
 from .kvcomm import (ALL_CONSUMERS, COPY, NEW_ANCHOR, PLACEHOLDER, PREFIX, SHAREABLE, AnchorPool,  # noqa
                      KVCommError, Match, OffsetGiven, OffsetMeasure, Segment, concat_prefill_cache,
                      kernel_launch_count, match_many, prepare_segments, realign_prepared, realign_segment,
-                     realign_segments)
+                     realign_segments, Plan, PlanSegment)
 from ._lib import LIB_PATH, lib as _load_lib  # noqa: F401
 
 _load_lib()  # load now: no silent fallback path exists

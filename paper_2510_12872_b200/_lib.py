@@ -71,6 +71,22 @@ class MatchRequest(C.Structure):
                 ("idx", C.c_void_p), ("wbar", C.c_void_p), ("dist", C.c_void_p), ("info", C.POINTER(MatchInfo))]
 
 
+class PlanMatch(C.Structure):
+    _fields_ = [("pool", C.c_void_p), ("L_phi", C.c_int32), ("consumer", C.c_int32), ("gamma", C.c_float),
+                ("top_k", C.c_int32)]
+
+
+class PlanSegment(C.Structure):
+    _fields_ = [("agent", C.c_int32), ("match", C.c_int32), ("kind", C.c_int32), ("consumer", C.c_int32),
+                ("base", KVView), ("L_seg", C.c_int32), ("base_start", C.c_int32), ("target_start", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class PlanAgent(C.Structure):
+    _fields_ = [("N", C.c_int32), ("_pad", C.c_int32), ("dst_k", C.c_void_p), ("dst_v", C.c_void_p),
+                ("dst_ld", C.c_int64)]
+
+
 class SegmentRef(C.Structure):
     _fields_ = [("start", C.c_int32), ("length", C.c_int32), ("src", KVView)]
 
@@ -102,6 +118,14 @@ _SIGS = {
     "kvcomm_concat_prefill_cache": (C.c_int, [C.POINTER(SegmentRef), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                               C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                               C.c_void_p]),
+    "kvcomm_plan_create": (C.c_int, [C.POINTER(PlanMatch), C.c_int32, C.POINTER(PlanSegment), C.c_int32,
+                                     C.POINTER(PlanAgent), C.c_int32, C.POINTER(C.c_void_p)]),
+    "kvcomm_plan_destroy": (C.c_int, [C.c_void_p]),
+    "kvcomm_plan_run": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p]),
+    "kvcomm_plan_results": (C.c_int, [C.c_void_p, C.POINTER(MatchInfo), C.POINTER(C.c_int32)]),
+    "kvcomm_plan_set_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvcomm_plan_weights": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_void_p)]),
 }
 
 

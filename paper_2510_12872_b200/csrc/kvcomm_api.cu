@@ -441,8 +441,8 @@ namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// A small ring of (pinned host, device) buffers holding the per-launch work tables.
-// Reusing an entry waits on the event recorded after the kernels that consumed it.
+// A pair of (pinned host, device) buffers holding one launch's work table; reusing
+// it waits on the event recorded after the kernels that consumed it.
 struct RingEntry {
   void* host = nullptr;
   void* dev = nullptr;
@@ -450,19 +450,10 @@ struct RingEntry {
   cudaEvent_t done = nullptr;
   bool used = false;
 };
-struct TableRing {
-  static constexpr int kN = 8;
-  RingEntry e[kN];
-  int next = 0;
-  std::mutex mu;
-};
-TableRing g_rings[64];
 
-// Caller holds ring.mu; `dev` is current.
-kvcomm_status ring_acquire(TableRing& ring, size_t bytes, RingEntry** out) {
-  RingEntry& E = ring.e[ring.next];
-  ring.next = (ring.next + 1) % TableRing::kN;
+kvcomm_status entry_reserve(RingEntry& E, size_t bytes) {
   if (E.used) KV_CUDA(cudaEventSynchronize(E.done));
+  E.used = false;
   if (!E.done) KV_CUDA(cudaEventCreateWithFlags(&E.done, cudaEventDisableTiming));
   if (E.cap < bytes) {
     if (E.host) cudaFreeHost(E.host);
@@ -476,9 +467,24 @@ kvcomm_status ring_acquire(TableRing& ring, size_t bytes, RingEntry** out) {
     }
     E.cap = cap;
   }
-  *out = &E;
   return KVCOMM_OK;
 }
+
+void entry_free(RingEntry& E) {
+  if (E.used && E.done) cudaEventSynchronize(E.done);
+  if (E.host) cudaFreeHost(E.host);
+  if (E.dev) cudaFree(E.dev);
+  if (E.done) cudaEventDestroy(E.done);
+  E = RingEntry();
+}
+
+struct TableRing {
+  static constexpr int kN = 8;
+  RingEntry e[kN];
+  int next = 0;
+  std::mutex mu;
+};
+TableRing g_rings[64];
 
 std::vector<kvcomm_pool_s*> distinct(std::vector<kvcomm_pool_s*> pools) {
   std::sort(pools.begin(), pools.end());
@@ -494,23 +500,240 @@ void lock_match_scratch(const std::vector<kvcomm_pool_s*>& pools, std::vector<st
   for (kvcomm_pool_s* p : distinct(pools)) l.emplace_back(p->match_mu);
 }
 
+// ---- a1: candidate filter + length clause (host, integer metadata) ----------
+// Fills info->{candidates, n_candidates, verdict, reason}; returns true when the
+// verdict still needs the device (entropy clause).
+bool candidate_filter(const kvcomm_pool_s* p, int L_phi, int consumer, kvcomm_match_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  int32_t maxL = 0, n_occ = 0, n_cand = 0;
+  const uint64_t need = consumer == KVCOMM_ALL_CONSUMERS ? (p->C >= 64 ? ~0ull : ((1ull << p->C) - 1))
+                                                         : (1ull << consumer);
+  for (int s = 0; s < p->cap; ++s) {
+    const SlotMeta& m = p->slots[s];
+    if (!m.occupied) continue;
+    ++n_occ;
+    maxL = std::max(maxL, m.length);
+    if (m.length >= L_phi && (m.ph_mask & need) == need && (m.pf_mask & need) == need)
+      info->candidates[n_cand++] = s;
+  }
+  info->n_candidates = n_cand;
+  info->verdict = KVCOMM_NEW_ANCHOR;
+  if (n_occ == 0) { info->reason = KVCOMM_REASON_EMPTY_POOL; return false; }
+  if (L_phi > maxL) { info->reason = KVCOMM_REASON_TOO_LONG; return false; }
+  if (n_cand == 0) { info->reason = KVCOMM_REASON_NO_CANDIDATES; return false; }
+  info->reason = KVCOMM_REASON_OK;
+  return true;
+}
+
+void fill_info_from_result(kvcomm_match_info* info, const MatchResultDev& r) {
+  info->entropy = r.entropy;
+  info->threshold = r.threshold;
+  info->verdict = r.verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
+  info->reason = r.verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
+  info->verdict_in_tie_band = r.tie_flag;
+  info->tie_band_count = r.tie_count;
+}
+
+// ---- match work table ---------------------------------------------------------
+struct MatchItem {
+  kvcomm_pool_s* p;
+  const void* query;
+  int L_phi;
+  float gamma;
+  int top_k;  // effective k, 0 = dense
+  float* W;
+  int64_t ld_w;
+  int32_t* idx;
+  float* wbar;
+  double* dist;
+  const kvcomm_match_info* info;  // candidates
+};
+
+struct MatchLayout {
+  MatchHdr hdr{};
+  size_t bytes = 0;
+  size_t smem = 0;
+};
+
+MatchLayout layout_match(const std::vector<MatchItem>& items) {
+  MatchLayout L;
+  const int nj = int(items.size());
+  L.hdr.n_jobs = nj;
+  L.hdr.P = kMatchP;
+  size_t n_ints = 0;
+  int blocks = 0;
+  for (const MatchItem& it : items) {
+    n_ints += it.info->n_candidates + it.p->cap;
+    blocks += (it.L_phi + kMatchP - 1) / kMatchP;
+    L.smem = std::max(L.smem, align_up(size_t(kMatchP) * it.p->De * 2, 16) +
+                                  size_t(kMatchP) * it.info->n_candidates * sizeof(double));
+  }
+  L.hdr.total_blocks = blocks;
+  size_t off = align_up(sizeof(MatchHdr), 64);
+  L.hdr.job_off = int64_t(off);
+  off = align_up(off + sizeof(MatchJob) * nj, 64);
+  L.hdr.int_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * n_ints, 64);
+  L.hdr.res_off = int64_t(off);
+  off = align_up(off + sizeof(MatchResultDev) * nj, 64);
+  L.hdr.tie_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * nj, 64);
+  L.bytes = off;
+  return L;
+}
+
+void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>& items) {
+  std::memset(h, 0, L.bytes);
+  std::memcpy(h, &L.hdr, sizeof(L.hdr));
+  MatchJob* jobs = reinterpret_cast<MatchJob*>(h + L.hdr.job_off);
+  int32_t* ints = reinterpret_cast<int32_t*>(h + L.hdr.int_off);
+  int ipos = 0, blocks = 0;
+  for (size_t t = 0; t < items.size(); ++t) {
+    const MatchItem& it = items[t];
+    kvcomm_pool_s* p = it.p;
+    MatchJob& a = jobs[t];
+    a.query = static_cast<const bf16*>(it.query);
+    a.emb = p->emb;
+    a.slot_stride = int64_t(p->maxlen) * p->De;
+    a.W = it.W;
+    a.ld_w = it.ld_w;
+    a.top_k = it.top_k;
+    a.idx = it.top_k > 0 ? it.idx : nullptr;
+    a.dist_user = it.dist;
+    a.partial = p->d_partial;
+    a.wbar = it.wbar;
+    a.gamma = double(it.gamma);
+    a.n_cand = it.info->n_candidates;
+    a.cap = p->cap;
+    a.L_phi = it.L_phi;
+    a.De = p->De;
+    a.scalar_mode = p->cfg.scalar_distance;
+    a.cand_off = ipos;
+    std::memcpy(ints + ipos, it.info->candidates, sizeof(int32_t) * a.n_cand);
+    ipos += a.n_cand;
+    a.s2c_off = ipos;
+    for (int sl = 0; sl < p->cap; ++sl) ints[ipos + sl] = -1;
+    for (int j = 0; j < a.n_cand; ++j) ints[ipos + it.info->candidates[j]] = j;
+    ipos += p->cap;
+    a.n_blocks = (it.L_phi + kMatchP - 1) / kMatchP;
+    a.block_begin = blocks;
+    blocks += a.n_blocks;
+  }
+}
+
+// ---- realign work table -------------------------------------------------------
+struct HostSeg {
+  SegDev x;
+  const int32_t* cand = nullptr;
+  bool prefix = false;
+  std::vector<int32_t> gates;  // indices into the gate results (match jobs)
+};
+
+struct RealignLayout {
+  TableHdr hdr{};
+  size_t bytes = 0;
+};
+
+RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& hs) {
+  RealignLayout L;
+  const int n_seg = int(hs.size());
+  size_t n_ints = 0, n_wexp = 0;
+  for (const HostSeg& g : hs) {
+    n_ints += g.x.n_cand + g.gates.size();
+    if (g.prefix) n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
+  }
+  TableHdr& hdr = L.hdr;
+  hdr.n_seg = n_seg;
+  hdr.d = d;
+  hdr.Ls = Ls;
+  hdr.Hs = Hs;
+  hdr.rows_per_tile = kStageBytes / (2 * d);
+  size_t off = align_up(sizeof(TableHdr), 64);
+  hdr.seg_off = int64_t(off);
+  off = align_up(off + sizeof(SegDev) * n_seg, 64);
+  hdr.cand_off = int64_t(off);
+  off = align_up(off + sizeof(int32_t) * std::max<size_t>(n_ints, 1), 64);
+  hdr.cs_off = int64_t(off);
+  off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
+  hdr.wexp_off = int64_t(off);
+  off = align_up(off + sizeof(float) * n_wexp, 64);
+  L.bytes = off;
+  return L;
+}
+
+// h/dev: host image and device address of the realign part of a table.
+void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector<HostSeg>& hs,
+                   const MatchResultDev* gate_results) {
+  TableHdr& hdr = L.hdr;
+  const int d = hdr.d, rpt = hdr.rows_per_tile;
+  SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
+  int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.cand_off);
+  float* dwexp = reinterpret_cast<float*>(dev + hdr.wexp_off);
+  int64_t units = 0;
+  int ipos = 0, wpos = 0;
+  for (size_t t = 0; t < hs.size(); ++t) {
+    SegDev x = hs[t].x;
+    x.cand_off = ipos;
+    if (x.n_cand) std::memcpy(ints + ipos, hs[t].cand, sizeof(int32_t) * x.n_cand);
+    ipos += x.n_cand;
+    x.n_gate = int32_t(hs[t].gates.size());
+    x.gate_off = ipos;
+    for (int32_t gi : hs[t].gates) ints[ipos++] = gi;
+    x.cs_off = int32_t(t) * (d / 2);
+    x.tiles = (x.L_seg + rpt - 1) / rpt;
+    x.unit_begin = units;
+    units += int64_t(hdr.Ls) * hdr.Hs * 2 * x.tiles;
+    if (hs[t].prefix) {
+      x.ld_w = (x.L_seg + 3) & ~3;
+      x.w = dwexp + wpos;
+      x.wexp_off = wpos;
+      wpos += int(x.ld_w) * x.n_cand;
+    }
+    segs[t] = x;
+  }
+  hdr.total_units = units;
+  hdr.gate_results = gate_results;
+  std::memcpy(h, &hdr, sizeof(hdr));
+}
+
+int grid_for_device(int dev) {
+  static int grid_cache[64] = {0};
+  if (!grid_cache[dev & 63]) grid_cache[dev & 63] = realign_grid_size(dev);
+  return grid_cache[dev & 63];
+}
+
 }  // namespace
 
 // ---- match -------------------------------------------------------------------
+static kvcomm_status check_match_request(const kvcomm_match_request& q, int r) {
+  kvcomm_pool_s* p = q.pool;
+  if (!p || !q.info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null pool/info", r);
+  if (!(q.gamma >= 0.f && q.gamma <= 1.f))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: gamma %g outside [0,1]", r, q.gamma);
+  if (q.L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: L_phi %d < 1", r, q.L_phi);
+  if (q.top_k < 0 || q.top_k > KVCOMM_MAX_TOPK)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: top_k %d outside [0,%d]", r, q.top_k, KVCOMM_MAX_TOPK);
+  if (q.consumer != KVCOMM_ALL_CONSUMERS && (q.consumer < 0 || q.consumer >= p->C))
+    return fail(KVCOMM_ERR_NOT_FOUND, "request %d: consumer %d", r, q.consumer);
+  if (q.L_phi > p->maxlen && q.query_emb == nullptr) return KVCOMM_OK;
+  return KVCOMM_OK;
+}
+
+static kvcomm_status check_match_buffers(const kvcomm_match_request& q, int r) {
+  if (!q.query_emb || !q.W || !q.wbar) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null query/W/wbar", r);
+  if (!aligned16(q.query_emb))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: query_emb not 16-byte aligned", r);
+  if (q.ld_w < q.L_phi)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: ld_w %lld < L_phi %d", r, (long long)q.ld_w, q.L_phi);
+  return KVCOMM_OK;
+}
+
 KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* reqs, int32_t n, void* stream) {
   if (n < 0 || (n > 0 && !reqs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad request list");
   std::vector<kvcomm_pool_s*> pools;
   for (int r = 0; r < n; ++r) {
-    const kvcomm_match_request& q = reqs[r];
-    kvcomm_pool_s* p = q.pool;
-    if (!p || !q.info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null pool/info", r);
-    if (!(q.gamma >= 0.f && q.gamma <= 1.f))
-      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: gamma %g outside [0,1]", r, q.gamma);
-    if (q.L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: L_phi %d < 1", r, q.L_phi);
-    if (q.top_k < 0 || q.top_k > KVCOMM_MAX_TOPK)
-      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: top_k %d outside [0,%d]", r, q.top_k, KVCOMM_MAX_TOPK);
-    if (q.consumer != KVCOMM_ALL_CONSUMERS && (q.consumer < 0 || q.consumer >= p->C))
-      return fail(KVCOMM_ERR_NOT_FOUND, "request %d: consumer %d", r, q.consumer);
+    KV_TRY(check_match_request(reqs[r], r));
+    kvcomm_pool_s* p = reqs[r].pool;
     if (std::find(pools.begin(), pools.end(), p) != pools.end())
       return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: pool appears twice in one batch", r);
     if (!pools.empty() && p->cfg.device != pools[0]->cfg.device)
@@ -520,59 +743,19 @@ KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* 
   if (n == 0) return ok();
   std::vector<std::shared_lock<std::shared_mutex>> rlocks;
   lock_readers(pools, rlocks);
-  // a1: candidate filter and length clause (host, integer metadata)
+  std::vector<MatchItem> items;
   std::vector<int> active;
   for (int r = 0; r < n; ++r) {
     const kvcomm_match_request& q = reqs[r];
-    kvcomm_pool_s* p = q.pool;
-    kvcomm_match_info* info = q.info;
-    std::memset(info, 0, sizeof(*info));
-    int32_t maxL = 0, n_occ = 0, n_cand = 0;
-    const uint64_t need = q.consumer == KVCOMM_ALL_CONSUMERS ? (p->C >= 64 ? ~0ull : ((1ull << p->C) - 1))
-                                                             : (1ull << q.consumer);
-    for (int s = 0; s < p->cap; ++s) {
-      const SlotMeta& m = p->slots[s];
-      if (!m.occupied) continue;
-      ++n_occ;
-      maxL = std::max(maxL, m.length);
-      if (m.length >= q.L_phi && (m.ph_mask & need) == need && (m.pf_mask & need) == need)
-        info->candidates[n_cand++] = s;
-    }
-    info->n_candidates = n_cand;
-    info->verdict = KVCOMM_NEW_ANCHOR;
-    if (n_occ == 0) { info->reason = KVCOMM_REASON_EMPTY_POOL; continue; }
-    if (q.L_phi > maxL) { info->reason = KVCOMM_REASON_TOO_LONG; continue; }
-    if (n_cand == 0) { info->reason = KVCOMM_REASON_NO_CANDIDATES; continue; }
-    if (!q.query_emb || !q.W || !q.wbar)
-      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null query/W/wbar", r);
-    if (!aligned16(q.query_emb))
-      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: query_emb not 16-byte aligned", r);
-    if (q.ld_w < q.L_phi)
-      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: ld_w %lld < L_phi %d", r, (long long)q.ld_w, q.L_phi);
-    const int k_eff = q.top_k > 0 ? std::min(q.top_k, n_cand) : 0;
-    info->top_k = k_eff > 0 ? k_eff : n_cand;
+    if (!candidate_filter(q.pool, q.L_phi, q.consumer, q.info)) continue;
+    KV_TRY(check_match_buffers(q, r));
+    const int k_eff = q.top_k > 0 ? std::min(q.top_k, q.info->n_candidates) : 0;
+    q.info->top_k = k_eff > 0 ? k_eff : q.info->n_candidates;
+    items.push_back({q.pool, q.query_emb, q.L_phi, q.gamma, k_eff, q.W, q.ld_w, q.idx, q.wbar, q.dist, q.info});
     active.push_back(r);
   }
-  if (active.empty()) return ok();
-
-  // table layout
-  const int nj = int(active.size());
-  MatchHdr hdr{};
-  hdr.n_jobs = nj;
-  hdr.P = kMatchP;
-  size_t n_ints = 0;
-  for (int r : active) n_ints += reqs[r].info->n_candidates + reqs[r].pool->cap;
-  size_t off = align_up(sizeof(MatchHdr), 64);
-  hdr.job_off = int64_t(off);
-  off = align_up(off + sizeof(MatchJob) * nj, 64);
-  hdr.int_off = int64_t(off);
-  off = align_up(off + sizeof(int32_t) * n_ints, 64);
-  hdr.res_off = int64_t(off);
-  off = align_up(off + sizeof(MatchResultDev) * nj, 64);
-  hdr.tie_off = int64_t(off);
-  off = align_up(off + sizeof(int32_t) * nj, 64);
-  const size_t table_bytes = off;
-
+  if (items.empty()) return ok();
+  const MatchLayout L = layout_match(items);
   const int dev = pools[0]->cfg.device;
   DeviceGuard guard(dev);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -580,67 +763,21 @@ KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* 
   lock_match_scratch(pools, mlocks);
   TableRing& ring = g_rings[dev & 63];
   std::lock_guard<std::mutex> rlk(ring.mu);
-  RingEntry* E = nullptr;
-  KV_TRY(ring_acquire(ring, table_bytes, &E));
-  uint8_t* h = static_cast<uint8_t*>(E->host);
-  std::memset(h, 0, table_bytes);
-  MatchJob* jobs = reinterpret_cast<MatchJob*>(h + hdr.job_off);
-  int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.int_off);
-  int ipos = 0, blocks = 0;
-  size_t smem = 0;
-  for (int t = 0; t < nj; ++t) {
-    const kvcomm_match_request& q = reqs[active[t]];
-    kvcomm_pool_s* p = q.pool;
-    const kvcomm_match_info* info = q.info;
-    MatchJob& a = jobs[t];
-    a.query = static_cast<const bf16*>(q.query_emb);
-    a.emb = p->emb;
-    a.slot_stride = int64_t(p->maxlen) * p->De;
-    a.W = q.W;
-    a.ld_w = q.ld_w;
-    a.top_k = q.top_k > 0 ? std::min(q.top_k, info->n_candidates) : 0;
-    a.idx = a.top_k > 0 ? q.idx : nullptr;
-    a.dist_user = q.dist;
-    a.partial = p->d_partial;
-    a.wbar = q.wbar;
-    a.gamma = double(q.gamma);
-    a.n_cand = info->n_candidates;
-    a.cap = p->cap;
-    a.L_phi = q.L_phi;
-    a.De = p->De;
-    a.scalar_mode = p->cfg.scalar_distance;
-    a.cand_off = ipos;
-    std::memcpy(ints + ipos, info->candidates, sizeof(int32_t) * a.n_cand);
-    ipos += a.n_cand;
-    a.s2c_off = ipos;
-    for (int sl = 0; sl < p->cap; ++sl) ints[ipos + sl] = -1;
-    for (int j = 0; j < a.n_cand; ++j) ints[ipos + info->candidates[j]] = j;
-    ipos += p->cap;
-    a.n_blocks = (q.L_phi + kMatchP - 1) / kMatchP;
-    a.block_begin = blocks;
-    blocks += a.n_blocks;
-    smem = std::max(smem, align_up(size_t(kMatchP) * p->De * 2, 16) + size_t(kMatchP) * a.n_cand * sizeof(double));
-  }
-  hdr.total_blocks = blocks;
-  std::memcpy(h, &hdr, sizeof(hdr));
-  KV_CUDA(cudaMemcpyAsync(E->dev, E->host, table_bytes, cudaMemcpyHostToDevice, s));
-  KV_CUDA(launch_match_batch(E->dev, hdr, smem, s));
+  RingEntry& E = ring.e[ring.next];
+  ring.next = (ring.next + 1) % TableRing::kN;
+  KV_TRY(entry_reserve(E, L.bytes));
+  uint8_t* h = static_cast<uint8_t*>(E.host);
+  write_match(h, L, items);
+  KV_CUDA(cudaMemcpyAsync(E.dev, E.host, L.bytes, cudaMemcpyHostToDevice, s));
+  KV_CUDA(launch_match_batch(E.dev, L.hdr, L.smem, s));
   g_launches += 2;
-  KV_CUDA(cudaMemcpyAsync(h + hdr.res_off, static_cast<uint8_t*>(E->dev) + hdr.res_off,
-                          table_bytes - size_t(hdr.res_off), cudaMemcpyDeviceToHost, s));
-  KV_CUDA(cudaEventRecord(E->done, s));
-  E->used = true;
+  KV_CUDA(cudaMemcpyAsync(h + L.hdr.res_off, static_cast<uint8_t*>(E.dev) + L.hdr.res_off,
+                          L.bytes - size_t(L.hdr.res_off), cudaMemcpyDeviceToHost, s));
+  KV_CUDA(cudaEventRecord(E.done, s));
+  E.used = true;
   KV_CUDA(cudaStreamSynchronize(s));
-  const MatchResultDev* res = reinterpret_cast<const MatchResultDev*>(h + hdr.res_off);
-  for (int t = 0; t < nj; ++t) {
-    kvcomm_match_info* info = reqs[active[t]].info;
-    info->entropy = res[t].entropy;
-    info->threshold = res[t].threshold;
-    info->verdict = res[t].verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
-    info->reason = res[t].verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
-    info->verdict_in_tie_band = res[t].tie_flag;
-    info->tie_band_count = res[t].tie_count;
-  }
+  const MatchResultDev* res = reinterpret_cast<const MatchResultDev*>(h + L.hdr.res_off);
+  for (size_t t = 0; t < active.size(); ++t) fill_info_from_result(reqs[active[t]].info, res[t]);
   return ok();
 }
 
@@ -653,14 +790,6 @@ KVCOMM_API kvcomm_status kvcomm_match_anchors(kvcomm_pool_t p, const void* query
 }
 
 // ---- realign -----------------------------------------------------------------
-namespace {
-struct HostSeg {
-  SegDev x;
-  const int32_t* cand;
-  bool prefix;
-};
-}  // namespace
-
 static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
   kvcomm_pool_s* p = g.pool;
   if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null pool", idx);
@@ -716,69 +845,61 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
   return KVCOMM_OK;
 }
 
-// Builds the work table of `hs` in a ring entry and launches prep + realign kernels.
-static kvcomm_status launch_segments(int dev, int d, int Ls, int Hs, std::vector<HostSeg>& hs, cudaStream_t s) {
-  const int n_seg = int(hs.size());
-  if (n_seg == 0) return KVCOMM_OK;
-  const int rpt = kStageBytes / (2 * d);
-  size_t n_cand_total = 0, n_wexp = 0;
-  for (const HostSeg& g : hs) {
-    n_cand_total += g.x.n_cand;
-    if (g.prefix) n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
+static HostSeg host_segment(const kvcomm_realign_desc& g) {
+  kvcomm_pool_s* p = g.pool;
+  HostSeg h{};
+  SegDev& x = h.x;
+  x.base[0] = static_cast<const bf16*>(g.base.k);
+  x.base[1] = static_cast<const bf16*>(g.base.v);
+  x.base_ld = ld_of(g.base, g.L_seg);
+  x.dst[0] = static_cast<bf16*>(g.dst_k);
+  x.dst[1] = static_cast<bf16*>(g.dst_v);
+  x.dst_ld = g.dst_ld;
+  x.inv_freq = p->inv_freq_dev;
+  x.L_seg = g.L_seg;
+  x.target_start = g.target_start;
+  x.w_by_slot = 1;
+  if (g.kind == KVCOMM_COPY) return h;  // delta 0, no candidates: verbatim rows
+  x.dbg[0] = g.debug_delta_k;
+  x.dbg[1] = g.debug_delta_v;
+  x.delta = g.target_start - g.base_start;
+  x.n_cand = g.n_candidates;
+  h.cand = g.candidates;
+  if (g.kind == KVCOMM_PLACEHOLDER) {
+    x.w = g.weights;
+    x.ld_w = g.ld_w;
+    x.off = p->ph_base(g.consumer);
+    x.slot_stride = p->ph_slot_stride();
+    x.plane_stride = p->ph_plane_stride();
+    x.off_ld = p->ph_ld;
+  } else {
+    h.prefix = true;
+    x.w_by_slot = 0;
+    x.wbar = g.weights;
+    x.off = p->pf[g.consumer];
+    x.slot_stride = p->pf_slot_stride(g.consumer);
+    x.plane_stride = p->pf_plane_stride(g.consumer);
+    x.off_ld = p->prefix_len[g.consumer];
   }
-  TableHdr hdr{};
-  hdr.n_seg = n_seg;
-  hdr.d = d;
-  hdr.Ls = Ls;
-  hdr.Hs = Hs;
-  hdr.rows_per_tile = rpt;
-  size_t off = align_up(sizeof(TableHdr), 64);
-  hdr.seg_off = int64_t(off);
-  off = align_up(off + sizeof(SegDev) * n_seg, 64);
-  hdr.cand_off = int64_t(off);
-  off = align_up(off + sizeof(int32_t) * std::max<size_t>(n_cand_total, 1), 64);
-  hdr.cs_off = int64_t(off);
-  off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
-  hdr.wexp_off = int64_t(off);
-  off = align_up(off + sizeof(float) * n_wexp, 64);
-  const size_t table_bytes = off;
+  return h;
+}
 
+// Builds the work table of `hs` in a ring entry and launches prep + realign kernels.
+static kvcomm_status launch_segments(int dev, int d, int Ls, int Hs, const std::vector<HostSeg>& hs,
+                                     cudaStream_t s) {
+  if (hs.empty()) return KVCOMM_OK;
+  RealignLayout L = layout_realign(d, Ls, Hs, hs);
   TableRing& ring = g_rings[dev & 63];
   std::lock_guard<std::mutex> rlk(ring.mu);
-  RingEntry* E = nullptr;
-  KV_TRY(ring_acquire(ring, table_bytes, &E));
-  uint8_t* h = static_cast<uint8_t*>(E->host);
-  SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
-  int32_t* cands = reinterpret_cast<int32_t*>(h + hdr.cand_off);
-  float* dwexp = reinterpret_cast<float*>(static_cast<uint8_t*>(E->dev) + hdr.wexp_off);
-  int64_t units = 0;
-  int cpos = 0, wpos = 0;
-  for (int t = 0; t < n_seg; ++t) {
-    SegDev x = hs[t].x;
-    x.cand_off = cpos;
-    if (x.n_cand) std::memcpy(cands + cpos, hs[t].cand, sizeof(int32_t) * x.n_cand);
-    cpos += x.n_cand;
-    x.cs_off = t * (d / 2);
-    x.tiles = (x.L_seg + rpt - 1) / rpt;
-    x.unit_begin = units;
-    units += int64_t(Ls) * Hs * 2 * x.tiles;
-    if (hs[t].prefix) {
-      x.ld_w = (x.L_seg + 3) & ~3;
-      x.w = dwexp + wpos;
-      x.wexp_off = wpos;
-      wpos += int(x.ld_w) * x.n_cand;
-    }
-    segs[t] = x;
-  }
-  hdr.total_units = units;
-  std::memcpy(h, &hdr, sizeof(hdr));
-  KV_CUDA(cudaMemcpyAsync(E->dev, E->host, size_t(hdr.cs_off), cudaMemcpyHostToDevice, s));
-  static int grid_cache[64] = {0};
-  if (!grid_cache[dev & 63]) grid_cache[dev & 63] = realign_grid_size(dev);
-  KV_CUDA(launch_realign(E->dev, hdr, grid_cache[dev & 63], s));
-  g_launches += units > 0 ? 2 : 1;
-  KV_CUDA(cudaEventRecord(E->done, s));
-  E->used = true;
+  RingEntry& E = ring.e[ring.next];
+  ring.next = (ring.next + 1) % TableRing::kN;
+  KV_TRY(entry_reserve(E, L.bytes));
+  write_realign(static_cast<uint8_t*>(E.host), static_cast<uint8_t*>(E.dev), L, hs, nullptr);
+  KV_CUDA(cudaMemcpyAsync(E.dev, E.host, size_t(L.hdr.cs_off), cudaMemcpyHostToDevice, s));
+  KV_CUDA(launch_realign(E.dev, L.hdr, grid_for_device(dev), s));
+  g_launches += L.hdr.total_units > 0 ? 2 : 1;
+  KV_CUDA(cudaEventRecord(E.done, s));
+  E.used = true;
   return KVCOMM_OK;
 }
 
@@ -800,49 +921,8 @@ KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs
   std::vector<HostSeg> hs;
   hs.reserve(n);
   for (int i = 0; i < n; ++i) {
-    const kvcomm_realign_desc& g = segs[i];
-    KV_TRY(validate_segment(g, i));
-    if (g.L_seg == 0) continue;
-    kvcomm_pool_s* p = g.pool;
-    HostSeg h{};
-    SegDev& x = h.x;
-    x.base[0] = static_cast<const bf16*>(g.base.k);
-    x.base[1] = static_cast<const bf16*>(g.base.v);
-    x.base_ld = ld_of(g.base, g.L_seg);
-    x.dst[0] = static_cast<bf16*>(g.dst_k);
-    x.dst[1] = static_cast<bf16*>(g.dst_v);
-    x.dst_ld = g.dst_ld;
-    x.inv_freq = p->inv_freq_dev;
-    x.L_seg = g.L_seg;
-    x.target_start = g.target_start;
-    x.w_by_slot = 1;
-    if (g.kind == KVCOMM_COPY) {
-      x.delta = 0;
-      x.n_cand = 0;
-    } else {
-      x.dbg[0] = g.debug_delta_k;
-      x.dbg[1] = g.debug_delta_v;
-      x.delta = g.target_start - g.base_start;
-      x.n_cand = g.n_candidates;
-      h.cand = g.candidates;
-      if (g.kind == KVCOMM_PLACEHOLDER) {
-        x.w = g.weights;
-        x.ld_w = g.ld_w;
-        x.off = p->ph_base(g.consumer);
-        x.slot_stride = p->ph_slot_stride();
-        x.plane_stride = p->ph_plane_stride();
-        x.off_ld = p->ph_ld;
-      } else {
-        h.prefix = true;
-        x.w_by_slot = 0;
-        x.wbar = g.weights;
-        x.off = p->pf[g.consumer];
-        x.slot_stride = p->pf_slot_stride(g.consumer);
-        x.plane_stride = p->pf_plane_stride(g.consumer);
-        x.off_ld = p->prefix_len[g.consumer];
-      }
-    }
-    hs.push_back(h);
+    KV_TRY(validate_segment(segs[i], i));
+    if (segs[i].L_seg > 0) hs.push_back(host_segment(segs[i]));
   }
   DeviceGuard guard(p0->cfg.device);
   KV_TRY(launch_segments(p0->cfg.device, p0->d, p0->Ls, p0->Hs, hs, static_cast<cudaStream_t>(stream)));
@@ -855,6 +935,19 @@ KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, 
 }
 
 // ---- concat ------------------------------------------------------------------
+static kvcomm_status check_ledger(const int32_t* starts, const int32_t* lengths, int n, int32_t N_total) {
+  int64_t pos = 0;  // segments tile [0, N_total) in order
+  for (int i = 0; i < n; ++i) {
+    if (lengths[i] < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: negative length", i);
+    if (starts[i] > pos) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (segment %d)", (long long)pos, i);
+    if (starts[i] < pos) return fail(KVCOMM_ERR_POSITION_OVERLAP, "overlap at position %d (segment %d)", starts[i], i);
+    pos = int64_t(starts[i]) + lengths[i];
+  }
+  if (pos < N_total) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (end)", (long long)pos);
+  if (pos > N_total) return fail(KVCOMM_ERR_POSITION_OVERLAP, "segments run past N_total %d", N_total);
+  return KVCOMM_OK;
+}
+
 KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n, int32_t N_total,
                                                      int32_t Ls, int32_t Hs, int32_t d, void* dst_k, void* dst_v,
                                                      int64_t dst_ld, int32_t device, void* stream) {
@@ -862,18 +955,12 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
   if (Ls < 1 || Hs < 1 || d < 16 || d % 16 != 0 || d > 256) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad geometry");
   if (N_total < 0 || dst_ld < N_total)
     return fail(KVCOMM_ERR_SHAPE_MISMATCH, "dst_ld %lld < N_total %d", (long long)dst_ld, N_total);
-  // ledger: segments tile [0, N_total) in order
-  int64_t pos = 0;
+  std::vector<int32_t> st(n), ln(n);
   for (int i = 0; i < n; ++i) {
-    if (segs[i].length < 0) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: negative length", i);
-    if (segs[i].start > pos)
-      return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (segment %d)", (long long)pos, i);
-    if (segs[i].start < pos)
-      return fail(KVCOMM_ERR_POSITION_OVERLAP, "overlap at position %d (segment %d)", segs[i].start, i);
-    pos = int64_t(segs[i].start) + segs[i].length;
+    st[i] = segs[i].start;
+    ln[i] = segs[i].length;
   }
-  if (pos < N_total) return fail(KVCOMM_ERR_POSITION_GAP, "gap at position %lld (end)", (long long)pos);
-  if (pos > N_total) return fail(KVCOMM_ERR_POSITION_OVERLAP, "segments run past N_total %d", N_total);
+  KV_TRY(check_ledger(st.data(), ln.data(), n, N_total));
   if (!dst_k || !dst_v || !aligned16(dst_k) || !aligned16(dst_v))
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "dst null or misaligned");
   std::vector<HostSeg> hs;
@@ -896,6 +983,277 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
   if (hs.empty()) return ok();
   DeviceGuard guard(device);
   KV_TRY(launch_segments(device, d, Ls, Hs, hs, static_cast<cudaStream_t>(stream)));
+  return ok();
+}
+
+// ---- request plan (native executor of Algorithm 1's reuse branch) --------------
+struct kvcomm_plan_s {
+  int dev = 0, d = 0, Ls = 0, Hs = 0;
+  std::vector<kvcomm_plan_match> matches;
+  std::vector<kvcomm_plan_segment> segs;
+  std::vector<kvcomm_plan_agent> agents;
+  std::vector<std::vector<int>> agent_matches;  // distinct matches each agent depends on
+  std::vector<float*> W, wbar;
+  std::vector<int64_t> ld_w;
+  RingEntry tab[2];
+  int next = 0;
+  // last run
+  int last = -1;
+  std::vector<kvcomm_match_info> infos;
+  std::vector<int> job_of;        // match -> job index in the last run (-1: decided on host)
+  std::vector<int32_t> agent_state;  // 0 reuse pending/ok, 1 fallback (host-decided)
+  int64_t res_off = 0;
+  cudaEvent_t ev_before = nullptr, ev_after = nullptr;
+  std::mutex mu;
+};
+
+static void plan_free(kvcomm_plan_s* pl) {
+  if (!pl) return;
+  DeviceGuard g(pl->dev);
+  for (auto& e : pl->tab) entry_free(e);
+  for (float* x : pl->W) cudaFree(x);
+  for (float* x : pl->wbar) cudaFree(x);
+  delete pl;
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, int32_t n_matches,
+                                            const kvcomm_plan_segment* segs, int32_t n_segs,
+                                            const kvcomm_plan_agent* agents, int32_t n_agents, kvcomm_plan_t* out) {
+  if (!out || n_matches < 1 || !matches || n_segs < 0 || (n_segs > 0 && !segs) || n_agents < 1 || !agents)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad plan arguments");
+  *out = nullptr;
+  kvcomm_pool_s* p0 = matches[0].pool;
+  for (int i = 0; i < n_matches; ++i) {
+    const kvcomm_plan_match& m = matches[i];
+    kvcomm_pool_s* p = m.pool;
+    if (!p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "match %d: null pool", i);
+    if (p->Ls != p0->Ls || p->Hs != p0->Hs || p->d != p0->d || p->cfg.device != p0->cfg.device)
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "match %d: pool geometry differs from match 0", i);
+    for (int j = 0; j < i; ++j)
+      if (matches[j].pool == p) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "match %d: pool used twice", i);
+    if (!(m.gamma >= 0.f && m.gamma <= 1.f)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "match %d: gamma", i);
+    if (m.L_phi < 1 || m.L_phi > p->maxlen) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "match %d: L_phi %d", i, m.L_phi);
+    if (m.top_k < 0 || m.top_k > KVCOMM_MAX_TOPK) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "match %d: top_k", i);
+    if (m.consumer != KVCOMM_ALL_CONSUMERS && (m.consumer < 0 || m.consumer >= p->C))
+      return fail(KVCOMM_ERR_NOT_FOUND, "match %d: consumer %d", i, m.consumer);
+  }
+  std::vector<std::vector<int>> am(n_agents);
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> ledger(n_agents);
+  for (int i = 0; i < n_segs; ++i) {
+    const kvcomm_plan_segment& s = segs[i];
+    if (s.agent < 0 || s.agent >= n_agents) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: agent", i);
+    const kvcomm_plan_agent& a = agents[s.agent];
+    if (s.kind != KVCOMM_COPY) {
+      if (s.match < 0 || s.match >= n_matches) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: match", i);
+      kvcomm_pool_s* p = matches[s.match].pool;
+      if (s.kind == KVCOMM_PLACEHOLDER && s.L_seg != matches[s.match].L_phi)
+        return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: placeholder length %d != L_phi %d", i, s.L_seg,
+                    matches[s.match].L_phi);
+      if (s.consumer < 0 || s.consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: consumer", i);
+      if (s.kind == KVCOMM_PREFIX && s.L_seg != p->prefix_len[s.consumer])
+        return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: prefix length %d != %d", i, s.L_seg,
+                    p->prefix_len[s.consumer]);
+      if (std::find(am[s.agent].begin(), am[s.agent].end(), s.match) == am[s.agent].end())
+        am[s.agent].push_back(s.match);
+    } else if (s.kind != KVCOMM_COPY) {
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: kind", i);
+    }
+    if (s.L_seg > 0) KV_TRY(check_view(s.base, s.L_seg, "plan segment base"));
+    if (!a.dst_k || !a.dst_v || !aligned16(a.dst_k) || !aligned16(a.dst_v) || a.dst_ld < a.N)
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "agent %d: bad destination", s.agent);
+    ledger[s.agent].push_back({s.target_start, s.L_seg});
+  }
+  for (int a = 0; a < n_agents; ++a) {  // every prompt must be tiled exactly (reading A20 + P:304)
+    auto& l = ledger[a];
+    std::sort(l.begin(), l.end());
+    std::vector<int32_t> st, ln;
+    for (auto& x : l) {
+      st.push_back(x.first);
+      ln.push_back(x.second);
+    }
+    kvcomm_status s = check_ledger(st.data(), ln.data(), int(st.size()), agents[a].N);
+    if (s != KVCOMM_OK) {
+      g_err = "agent " + std::to_string(a) + ": " + g_err;
+      return s;
+    }
+  }
+  DeviceGuard guard(p0->cfg.device);
+  auto* pl = new kvcomm_plan_s();
+  pl->dev = p0->cfg.device;
+  pl->d = p0->d;
+  pl->Ls = p0->Ls;
+  pl->Hs = p0->Hs;
+  pl->matches.assign(matches, matches + n_matches);
+  pl->segs.assign(segs, segs + n_segs);
+  pl->agents.assign(agents, agents + n_agents);
+  pl->agent_matches = am;
+  pl->infos.resize(n_matches);
+  pl->job_of.assign(n_matches, -1);
+  pl->agent_state.assign(n_agents, 1);
+  for (int i = 0; i < n_matches; ++i) {
+    const int64_t ldw = (matches[i].L_phi + 3) & ~3;
+    float *w = nullptr, *wb = nullptr;
+    if (cudaMalloc(&w, sizeof(float) * ldw * matches[i].pool->cap) != cudaSuccess ||
+        cudaMalloc(&wb, sizeof(float) * matches[i].pool->cap) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(w);
+      cudaFree(wb);
+      plan_free(pl);
+      return fail(KVCOMM_ERR_OUT_OF_MEMORY, "plan weight buffers");
+    }
+    pl->W.push_back(w);
+    pl->wbar.push_back(wb);
+    pl->ld_w.push_back(ldw);
+  }
+  *out = pl;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_destroy(kvcomm_plan_t pl) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  plan_free(pl);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* query_embs, int32_t sync,
+                                         void* stream) {
+  if (!pl || !query_embs) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/queries");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  const int nm = int(pl->matches.size());
+  for (int i = 0; i < nm; ++i)
+    if (!query_embs[i] || !aligned16(query_embs[i]))
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT, "query %d null or misaligned", i);
+  std::vector<kvcomm_pool_s*> pools;
+  for (auto& m : pl->matches) pools.push_back(m.pool);
+  std::vector<std::shared_lock<std::shared_mutex>> rlocks;
+  lock_readers(pools, rlocks);
+  DeviceGuard guard(pl->dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RingEntry& E = pl->tab[pl->next];
+  KV_TRY(entry_reserve(E, 0));  // waits for the run that used this table two runs ago
+  // a1 on the host; jobs for the entropy clause
+  std::vector<MatchItem> items;
+  std::vector<bool> host_new(nm, false);
+  for (int i = 0; i < nm; ++i) {
+    const kvcomm_plan_match& m = pl->matches[i];
+    kvcomm_match_info* info = &pl->infos[i];
+    pl->job_of[i] = -1;
+    if (!candidate_filter(m.pool, m.L_phi, m.consumer, info)) {
+      host_new[i] = true;
+      continue;
+    }
+    const int k_eff = m.top_k > 0 ? std::min(m.top_k, info->n_candidates) : 0;
+    info->top_k = k_eff > 0 ? k_eff : info->n_candidates;
+    pl->job_of[i] = int(items.size());
+    items.push_back({m.pool, query_embs[i], m.L_phi, m.gamma, k_eff, pl->W[i], pl->ld_w[i], nullptr, pl->wbar[i],
+                     nullptr, info});
+  }
+  // segments of agents not already decided by the length clause, gated on device
+  std::vector<HostSeg> hs;
+  for (size_t a = 0; a < pl->agents.size(); ++a) {
+    bool closed = false;
+    for (int mi : pl->agent_matches[a]) closed |= host_new[mi];
+    pl->agent_state[a] = closed ? 1 : 0;
+  }
+  for (const kvcomm_plan_segment& g : pl->segs) {
+    if (g.L_seg == 0 || pl->agent_state[g.agent]) continue;
+    const kvcomm_plan_agent& a = pl->agents[g.agent];
+    kvcomm_realign_desc d{};
+    d.pool = g.kind == KVCOMM_COPY ? pl->matches[0].pool : pl->matches[g.match].pool;
+    d.consumer = g.consumer;
+    d.kind = g.kind;
+    d.L_seg = g.L_seg;
+    d.base = g.base;
+    d.base_start = g.base_start;
+    d.target_start = g.target_start;
+    d.dst_k = a.dst_k;
+    d.dst_v = a.dst_v;
+    d.dst_ld = a.dst_ld;
+    if (g.kind != KVCOMM_COPY) {
+      const kvcomm_match_info* info = &pl->infos[g.match];
+      d.weights = g.kind == KVCOMM_PLACEHOLDER ? pl->W[g.match] : pl->wbar[g.match];
+      d.ld_w = pl->ld_w[g.match];
+      d.candidates = info->candidates;
+      d.n_candidates = info->n_candidates;
+      KV_TRY(validate_segment(d, int(&g - pl->segs.data())));
+    }
+    HostSeg h = host_segment(d);
+    for (int mi : pl->agent_matches[g.agent]) h.gates.push_back(pl->job_of[mi]);
+    hs.push_back(std::move(h));
+  }
+  // one table: [match part][realign part]
+  const MatchLayout ML = items.empty() ? MatchLayout() : layout_match(items);
+  RealignLayout RL = layout_realign(pl->d, pl->Ls, pl->Hs, hs);
+  const size_t roff = align_up(ML.bytes, 256);
+  KV_TRY(entry_reserve(E, roff + RL.bytes));
+  uint8_t* h = static_cast<uint8_t*>(E.host);
+  uint8_t* dv = static_cast<uint8_t*>(E.dev);
+  std::vector<std::unique_lock<std::mutex>> mlocks;
+  lock_match_scratch(pools, mlocks);
+  if (!items.empty()) write_match(h, ML, items);
+  const MatchResultDev* gres = items.empty() ? nullptr
+                                             : reinterpret_cast<const MatchResultDev*>(dv + ML.hdr.res_off);
+  if (!hs.empty()) write_realign(h + roff, dv + roff, RL, hs, gres);
+  KV_CUDA(cudaMemcpyAsync(dv, h, hs.empty() ? ML.bytes : roff + size_t(RL.hdr.cs_off), cudaMemcpyHostToDevice, s));
+  if (!items.empty()) {
+    KV_CUDA(launch_match_batch(dv, ML.hdr, ML.smem, s));
+    g_launches += 2;
+  }
+  if (pl->ev_before) KV_CUDA(cudaEventRecord(pl->ev_before, s));
+  if (!hs.empty()) {
+    KV_CUDA(launch_realign(dv + roff, RL.hdr, grid_for_device(pl->dev), s));
+    g_launches += RL.hdr.total_units > 0 ? 2 : 1;
+  }
+  if (pl->ev_after) KV_CUDA(cudaEventRecord(pl->ev_after, s));
+  if (!items.empty())
+    KV_CUDA(cudaMemcpyAsync(h + ML.hdr.res_off, dv + ML.hdr.res_off, ML.bytes - size_t(ML.hdr.res_off),
+                            cudaMemcpyDeviceToHost, s));
+  KV_CUDA(cudaEventRecord(E.done, s));
+  E.used = true;
+  pl->res_off = items.empty() ? -1 : ML.hdr.res_off;
+  pl->last = pl->next;
+  pl->next ^= 1;
+  if (sync) KV_CUDA(cudaEventSynchronize(E.done));
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t pl, kvcomm_match_info* infos, int32_t* agent_reused) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  if (pl->last < 0) return fail(KVCOMM_ERR_NOT_FOUND, "plan has not run");
+  RingEntry& E = pl->tab[pl->last];
+  KV_CUDA(cudaEventSynchronize(E.done));
+  const int nm = int(pl->matches.size());
+  if (pl->res_off >= 0) {
+    const MatchResultDev* res = reinterpret_cast<const MatchResultDev*>(static_cast<uint8_t*>(E.host) + pl->res_off);
+    for (int i = 0; i < nm; ++i)
+      if (pl->job_of[i] >= 0) fill_info_from_result(&pl->infos[i], res[pl->job_of[i]]);
+  }
+  if (infos)
+    for (int i = 0; i < nm; ++i) infos[i] = pl->infos[i];
+  if (agent_reused)
+    for (size_t a = 0; a < pl->agents.size(); ++a) {
+      bool okk = pl->agent_state[a] == 0;
+      for (int mi : pl->agent_matches[a]) okk &= pl->infos[mi].verdict == KVCOMM_SHAREABLE;
+      agent_reused[a] = okk ? 1 : 0;
+    }
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t pl, void* before_realign, void* after_realign) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  pl->ev_before = static_cast<cudaEvent_t>(before_realign);
+  pl->ev_after = static_cast<cudaEvent_t>(after_realign);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t pl, int32_t match, const float** W, int64_t* ld_w,
+                                             const float** wbar) {
+  if (!pl || match < 0 || match >= int32_t(pl->matches.size())) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad match");
+  if (W) *W = pl->W[match];
+  if (ld_w) *ld_w = pl->ld_w[match];
+  if (wbar) *wbar = pl->wbar[match];
   return ok();
 }
 

@@ -33,7 +33,14 @@ struct SegDev {
   int32_t w_by_slot;    // 1: weight row = slot (PLACEHOLDER W); 0: row = j (expanded w̄)
   int32_t tiles;        // ceil(L_seg / rows_per_tile)
   int32_t wexp_off;     // PREFIX: float offset of the expanded weights in Table::wexp
+  int32_t n_gate;       // segment runs iff every listed match verdict is SHAREABLE (device-side
+  int32_t gate_off;     //   branch of Alg. 1); indices into Table::cand area, n_gate = 0: always
   int32_t _pad;
+};
+
+struct MatchResultDev {
+  double entropy, threshold;
+  int32_t verdict, tie_flag, tie_count, _pad;
 };
 
 // Device-side work table for one realign launch (lives in one contiguous buffer).
@@ -43,6 +50,7 @@ struct TableHdr {
   int64_t total_units;
   // byte offsets from the table base
   int64_t seg_off, cand_off, cs_off, wexp_off;
+  const MatchResultDev* gate_results;  // verdicts the segments' gates index (device), or null
 };
 
 // Launchers (stream-ordered).  Return cudaGetLastError().
@@ -67,11 +75,6 @@ struct MatchJob {
   int32_t cand_off;         // into MatchHdr ints: candidate slot ids [n_cand]
   int32_t s2c_off;          // into MatchHdr ints: slot -> candidate index or -1 [cap]
   int32_t block_begin, n_blocks;
-};
-
-struct MatchResultDev {
-  double entropy, threshold;
-  int32_t verdict, tie_flag, tie_count, _pad;
 };
 
 // Device-side table of one batched match launch.

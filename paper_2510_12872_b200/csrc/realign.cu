@@ -72,6 +72,14 @@ __device__ __forceinline__ Unit decode_unit(const SegDev* segs, int n_seg, int H
   return r;
 }
 
+// Device-side branch of Algorithm 1: a segment of an agent is realigned only
+// if every placeholder pool the agent depends on was matched Shareable.
+__device__ __forceinline__ bool seg_open(const TableHdr& hdr, const int32_t* ints, const SegDev& g) {
+  for (int i = 0; i < g.n_gate; ++i)
+    if (hdr.gate_results[ints[g.gate_off + i]].verdict != 0) return false;
+  return true;
+}
+
 // Per-segment preparation: cos/sin of δ·inv_freq (fp64 angle, reading A13) and,
 // for PREFIX segments, the scalar weights w̄[cand[j]] expanded into rows of the
 // same shape as a placeholder W slice so the main kernel treats both kinds alike.
@@ -141,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
       for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
         const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
         const SegDev& g = segs[un.s];
+        if (!seg_open(hdr, cand, g)) continue;
         const int i0 = un.t * rpt;
         const int nrows = min(rpt, g.L_seg - i0);
         const uint32_t bytes = uint32_t(nrows) * row_bytes;
@@ -184,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
   for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
     const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
     const SegDev& g = segs[un.s];
+    if (!seg_open(hdr, cand, g)) continue;
     const int i0 = un.t * rpt;
     const int nrows = min(rpt, g.L_seg - i0);
     float acc[kItemsPerThread][16];

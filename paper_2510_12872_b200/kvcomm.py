@@ -24,7 +24,7 @@ from ._lib import (ALL_CONSUMERS, COPY, NEW_ANCHOR, OFFSET_GIVEN, OFFSET_MEASURE
 
 __all__ = ["AnchorPool", "OffsetGiven", "OffsetMeasure", "Match", "Segment", "realign_segments",
            "realign_segment", "prepare_segments", "realign_prepared", "concat_prefill_cache", "kernel_launch_count", "KVCommError", "ALL_CONSUMERS",
-           "SHAREABLE", "NEW_ANCHOR", "PLACEHOLDER", "PREFIX", "COPY", "match_many"]
+           "SHAREABLE", "NEW_ANCHOR", "PLACEHOLDER", "PREFIX", "COPY", "match_many", "Plan", "PlanSegment"]
 
 
 def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
@@ -350,3 +350,96 @@ def concat_prefill_cache(parts: Sequence[Tuple[int, int, Optional[torch.Tensor],
     L.check(L.lib().kvcomm_concat_prefill_cache(refs, len(parts), N_total, Ls, Hs, d, dst_k.data_ptr(),
                                                 dst_v.data_ptr(), dst_ld, dst_k.device.index or 0,
                                                 _stream_handle(stream)))
+
+
+@dataclass
+class PlanSegment:
+    agent: int
+    match: int                        # index of the pool in the plan's match list (ignored for COPY)
+    kind: int                         # PLACEHOLDER | PREFIX | COPY
+    consumer: int
+    base_k: torch.Tensor              # [Ls, Hs, L_seg, d]
+    base_v: torch.Tensor
+    base_start: int
+    target_start: int
+
+
+class Plan:
+    """Native executor of Algorithm 1's reuse branch for a fixed multi-agent layout
+    (kvcomm_plan_*): per run, one batched match launch and one realign launch with
+    the Shareable/NewAnchor branch taken on the device; no host synchronisation
+    unless requested."""
+
+    def __init__(self, matches: Sequence[Tuple[AnchorPool, int, float, int]], segments: Sequence[PlanSegment],
+                 agents: Sequence[Tuple[int, torch.Tensor, torch.Tensor]], consumer: int = ALL_CONSUMERS):
+        """matches: (pool, L_phi, gamma, top_k); agents: (N, dst_k, dst_v)."""
+        self.pools = [m[0] for m in matches]
+        self._keep = [segments, agents]
+        ms = (L.PlanMatch * len(matches))(*[L.PlanMatch(p.handle, int(Lp), consumer, float(g), int(k))
+                                            for p, Lp, g, k in matches])
+        ss = (L.PlanSegment * max(len(segments), 1))()
+        for i, s in enumerate(segments):
+            ss[i] = L.PlanSegment(s.agent, s.match, s.kind, s.consumer, _view(s.base_k, s.base_v, what="base"),
+                                  s.base_k.shape[2], s.base_start, s.target_start, 0)
+        ags = (L.PlanAgent * len(agents))()
+        for i, (N, dk, dv) in enumerate(agents):
+            ld = _rows_ld(dk, "dst_k")
+            if _rows_ld(dv, "dst_v") != ld:
+                raise ValueError("dst_k/dst_v strides differ")
+            ags[i] = L.PlanAgent(int(N), 0, dk.data_ptr(), dv.data_ptr(), ld)
+        h = C.c_void_p()
+        L.check(L.lib().kvcomm_plan_create(ms, len(matches), ss, len(segments), ags, len(agents), C.byref(h)))
+        self._h = h
+        self.n_matches, self.n_agents = len(matches), len(agents)
+        self._events = None
+
+    def run(self, queries: Sequence[torch.Tensor], sync: bool = False, stream=None) -> None:
+        for q in queries:
+            if q.dtype != torch.bfloat16 or not q.is_cuda or not q.is_contiguous():
+                raise ValueError("queries must be contiguous bf16 CUDA tensors")
+        arr = (C.c_void_p * self.n_matches)(*[q.data_ptr() for q in queries])
+        L.check(L.lib().kvcomm_plan_run(self._h, arr, 1 if sync else 0, _stream_handle(stream)))
+
+    def set_events(self, before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]) -> None:
+        """Record `before`/`after` around the realign launch of later runs (kernel timing)."""
+        self._events = (before, after)
+        for e in (before, after):   # torch creates the CUDA event lazily at its first record
+            if e is not None and not e.cuda_event:
+                e.record()
+        L.check(L.lib().kvcomm_plan_set_events(self._h, before.cuda_event if before is not None else None,
+                                               after.cuda_event if after is not None else None))
+
+    def results(self):
+        """(list of Match without tensors, list of agent_reused flags) of the last run."""
+        infos = (L.MatchInfo * self.n_matches)()
+        reused = (C.c_int32 * self.n_agents)()
+        L.check(L.lib().kvcomm_plan_results(self._h, infos, reused))
+        out = []
+        for i in range(self.n_matches):
+            W, ldw, wb = self.weights(i)
+            inf = infos[i]
+            out.append(Match(inf.verdict, L.REASONS[inf.reason], list(inf.candidates[: inf.n_candidates]), inf.top_k,
+                             inf.entropy, inf.threshold, bool(inf.verdict_in_tie_band), inf.tie_band_count, W, wb))
+        return out, [bool(x) for x in reused]
+
+    def weights(self, match: int):
+        W, ld, wb = C.c_void_p(), C.c_int64(), C.c_void_p()
+        L.check(L.lib().kvcomm_plan_weights(self._h, match, C.byref(W), C.byref(ld), C.byref(wb)))
+        cap = self.pools[match].capacity
+        dev = self.pools[match].device
+        Wt = torch.as_tensor(_DevView(W.value, (cap * ld.value,), "<f4"), device=dev).view(cap, ld.value)
+        wbt = torch.as_tensor(_DevView(wb.value, (cap,), "<f4"), device=dev)
+        return Wt, ld.value, wbt
+
+    def destroy(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            L.check(L.lib().kvcomm_plan_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None:
+                L.lib().kvcomm_plan_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass

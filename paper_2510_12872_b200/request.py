@@ -1,14 +1,18 @@
 """Algorithm 1's reuse branch for all agents of one request.
 
-Every placeholder pool's sample is matched once, all pools in one batched launch
-with a single host synchronisation (weights depend only on the sample and the
-pool, reading A21; Alg. 1 evaluates Eq. 5 for every placeholder before branching,
-P:765).  Every agent whose placeholders are all Shareable gets all its placeholder
-and prefix segments realigned, and its p_(m,0) rows copied, in ONE persistent
-kernel launch (kvcomm_realign_segments with COPY segments); the position ledger of
-each prompt is then checked (kvcomm_concat_prefill_cache, nothing left to copy).
-Agents with any NewAnchor verdict take the dense fallback, which needs the
-model and is outside this library: they are reported, not processed.
+Every placeholder pool's sample is matched once (weights depend only on the sample
+and the pool, reading A21; Alg. 1 evaluates Eq. 5 for every placeholder before
+branching).  Every agent whose placeholders are all Shareable gets all its
+placeholder and prefix segments realigned and its p_(m,0) rows copied.  Agents
+with any NewAnchor verdict take the dense fallback, which needs the model
+and is outside this library: they are reported, not processed.
+
+Two equivalent executions:
+  run()          the native plan (kvcomm_plan_*): ONE batched match launch and ONE
+                 realign launch per request, the branch taken on the device, no
+                 host synchronisation needed (this is what bench.py times);
+  run_unfused()  the individual C-ABI calls (match_many with one host sync, host
+                 branch, realign_segments with COPY segments, ledger check).
 
 Host bookkeeping only; all arithmetic runs in libkvcomm's kernels.
 """
@@ -55,10 +59,58 @@ class RequestResult:
 
 
 class ReuseRequest:
+    """run() executes the request through the native plan (kvcomm_plan_*: one match
+    launch + one gated realign launch, device-side branch); run_unfused() does the
+    same through the individual calls (match_many, realign_segments, concat) with
+    the branch taken on the host — both produce identical caches."""
+
     def __init__(self, pools: Dict[str, K.AnchorPool], agents: List[AgentLayout], gamma: float = 0.3,
                  top_k: int = 0):
         self.pools, self.agents, self.gamma, self.top_k = pools, agents, gamma, top_k
         self._match_out: Dict[str, Optional[K.Match]] = {n: None for n in pools}
+        self.names = list(pools)
+        self._plan: Optional[K.Plan] = None
+
+    @property
+    def plan(self) -> K.Plan:
+        if self._plan is None:
+            idx = {n: i for i, n in enumerate(self.names)}
+            L_phi = {}
+            segs = []
+            for ai, a in enumerate(self.agents):
+                for s in a.segments:
+                    if s.kind == K.PLACEHOLDER:
+                        L_phi[s.pool] = s.base_k.shape[2]
+                    segs.append(K.PlanSegment(ai, idx[s.pool], s.kind, s.consumer, s.base_k, s.base_v, s.base_start,
+                                              s.target_start))
+                if a.p0_k.shape[2] > 0:
+                    segs.append(K.PlanSegment(ai, 0, K.COPY, 0, a.p0_k, a.p0_v, 0, 0))
+            matches = [(self.pools[n], L_phi[n], self.gamma, self.top_k) for n in self.names]
+            self._plan = K.Plan(matches, segs, [(a.N, a.dst_k, a.dst_v) for a in self.agents])
+        return self._plan
+
+    def run(self, queries: Dict[str, torch.Tensor], stream=None, sync: bool = True) -> Optional["RequestResult"]:
+        """Plan path.  sync=False only enqueues (collect with results())."""
+        self.plan.run([queries[n] for n in self.names], sync=sync, stream=stream)
+        return self.results() if sync else None
+
+    def results(self) -> "RequestResult":
+        ms, reused_flags = self.plan.results()
+        matches = dict(zip(self.names, ms))
+        reused = [a.agent for a, f in zip(self.agents, reused_flags) if f]
+        fallback = [a.agent for a, f in zip(self.agents, reused_flags) if not f]
+        toks = rows = copied = 0
+        for a in self.agents:
+            if a.agent not in reused:
+                continue
+            for s in a.segments:
+                toks += s.base_k.shape[2]
+                rows += s.base_k.shape[2] * len(matches[s.pool].candidates)
+            copied += a.p0_k.shape[2]
+        for name, m in matches.items():            # reading A18: +1 per Shareable turn
+            if m.shareable:
+                self.pools[name].record_access(m.candidates)
+        return RequestResult(matches, reused, fallback, toks, rows, copied)
 
     def match(self, queries: Dict[str, torch.Tensor], stream=None) -> Dict[str, K.Match]:
         names = list(queries)
@@ -102,7 +154,7 @@ class ReuseRequest:
                 parts.append((s.target_start, s.base_k.shape[2], None, None))
             K.concat_prefill_cache(parts, a.N, a.dst_k, a.dst_v, stream=stream)
 
-    def run(self, queries: Dict[str, torch.Tensor], stream=None) -> RequestResult:
+    def run_unfused(self, queries: Dict[str, torch.Tensor], stream=None) -> RequestResult:
         matches = self.match(queries, stream)
         segs, reused, fallback, toks, rows, copied = self.segments(matches)
         self.check_ledger(reused, stream)      # host-only: raises before any launch on a bad layout

@@ -37,6 +37,8 @@ def test_ctypes_layout_matches_c_header():
 int main(void) {
   S(kvcomm_pool_config) S(kvcomm_kv_view) S(kvcomm_offset_desc) S(kvcomm_slot_info)
   S(kvcomm_match_info) S(kvcomm_realign_desc) S(kvcomm_segment_ref) S(kvcomm_match_request)
+  S(kvcomm_plan_match) S(kvcomm_plan_segment) S(kvcomm_plan_agent)
+  O(kvcomm_plan_segment, base) O(kvcomm_plan_segment, target_start) O(kvcomm_plan_agent, dst_ld)
   O(kvcomm_pool_config, prefix_len) O(kvcomm_pool_config, inv_freq)
   O(kvcomm_match_info, entropy) O(kvcomm_match_info, tie_band_count)
   O(kvcomm_realign_desc, base) O(kvcomm_realign_desc, dst_k) O(kvcomm_realign_desc, debug_delta_v)
@@ -53,7 +55,8 @@ int main(void) {
     got = dict(l.split() for l in lines if l.strip())
     py = {"kvcomm_pool_config": L.PoolConfig, "kvcomm_kv_view": L.KVView, "kvcomm_offset_desc": L.OffsetDesc,
           "kvcomm_slot_info": L.SlotInfo, "kvcomm_match_info": L.MatchInfo, "kvcomm_realign_desc": L.RealignDesc,
-          "kvcomm_segment_ref": L.SegmentRef, "kvcomm_match_request": L.MatchRequest}
+          "kvcomm_segment_ref": L.SegmentRef, "kvcomm_match_request": L.MatchRequest,
+          "kvcomm_plan_match": L.PlanMatch, "kvcomm_plan_segment": L.PlanSegment, "kvcomm_plan_agent": L.PlanAgent}
     for k, T in py.items():
         assert int(got[k]) == C.sizeof(T), k
     for key, v in got.items():

@@ -1,0 +1,79 @@
+"""Native request plan (kvcomm_plan_*) vs the unfused C-ABI calls, and the
+device-side Shareable/NewAnchor branch of Algorithm 1 (-m gpu)."""
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _small_state(seed=0, gamma=0.3):
+    from synth.state import build_five_agent_state
+    w = synth.five_agent_workload(L=3, H=2, d=64, D_e=64, user_len=96, resp_len=40, prefix_total=48,
+                                  slot_prefix=4, capacity=4)
+    return build_five_agent_state(w, seed=seed, gamma=gamma, anchor_extra=8)
+
+
+def _snap(st):
+    return [(a.dst_k.clone(), a.dst_v.clone()) for a in st.agents]
+
+
+def test_plan_equals_unfused_bitwise_and_reports_all_reused():
+    st = _small_state()
+    for a in st.agents:
+        a.dst_k.fill_(7.0)
+        a.dst_v.fill_(7.0)
+    res_u = st.request.run_unfused(st.queries)
+    torch.cuda.synchronize()
+    ref = _snap(st)
+    for a in st.agents:
+        a.dst_k.fill_(-3.0)
+        a.dst_v.fill_(-3.0)
+    res_p = st.request.run(st.queries)           # plan, sync
+    assert res_p.reused_agents == res_u.reused_agents == [1, 2, 3, 4, 5]
+    assert res_p.realigned_tokens == res_u.realigned_tokens
+    for (k, v), a in zip(ref, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+    for n in st.request.names:
+        mu, mp = res_u.matches[n], res_p.matches[n]
+        assert mu.candidates == mp.candidates and mu.verdict == mp.verdict and mu.entropy == mp.entropy
+        assert torch.equal(mu.W, mp.W[:, : mu.W.shape[1]]) and torch.equal(mu.wbar, mp.wbar)
+
+
+def test_plan_pipelined_runs_match_single_run():
+    st = _small_state(seed=3)
+    st.request.run(st.queries)
+    ref = _snap(st)
+    for _ in range(5):                            # several runs in flight, no host sync in between
+        st.request.run(st.queries, sync=False)
+    res = st.request.results()
+    assert res.reused_agents == [1, 2, 3, 4, 5]
+    for (k, v), a in zip(ref, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+
+
+def test_device_side_branch_skips_agents_of_a_new_anchor_pool():
+    st = _small_state(seed=5)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q = dict(st.queries)
+    # agent_2_current's sample is far from every anchor -> high entropy -> NewAnchor
+    q["agent_2_current"] = (torch.randn(q["agent_2_current"].shape, generator=g, device="cuda") * 0.125
+                            ).to(torch.bfloat16)
+    for a in st.agents:
+        a.dst_k.fill_(5.0)
+        a.dst_v.fill_(5.0)
+    res_u = st.request.run_unfused(q)
+    torch.cuda.synchronize()
+    ref = _snap(st)
+    for a in st.agents:
+        a.dst_k.fill_(5.0)
+        a.dst_v.fill_(5.0)
+    res_p = st.request.run(q)
+    assert res_u.matches["agent_2_current"].verdict == 1 and res_u.matches["agent_2_current"].reason == "HIGH_ENTROPY"
+    assert res_p.fallback_agents == res_u.fallback_agents == [3, 4, 5]   # agents that consume agent_2_current
+    assert res_p.reused_agents == [1, 2]
+    for (k, v), a in zip(ref, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+    for a in st.agents[2:]:
+        assert torch.all(a.dst_k == 5.0)          # fallback agents untouched
