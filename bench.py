@@ -222,6 +222,147 @@ def run_reference(args):
     }))
 
 
+# --------------------------------------------------------------------------- e2e
+
+def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, shard):
+    """The same step through the public API with HOST buffers: every step copies the
+    request's inputs (query embeddings of the 5 samples + their base caches; the
+    prefix / p_(m,0) caches are per-template and stay resident) from pinned host
+    memory and reads the 5 realigned prompt caches back into pinned host memory.
+    N = 1: double-buffered over two plans and three streams (H2D of step t+1 and
+    D2H of step t-1 overlap the compute of step t).  N > 1: sequential per step."""
+    from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
+    pinned_q = {n: q.cpu().pin_memory() for n, q in st.queries.items()}
+    bases = {}
+    for a in st.agents:
+        for sg in a.segments:
+            if sg.kind == kv.PLACEHOLDER and sg.pool not in bases:
+                bases[sg.pool] = (sg.base_k.cpu().pin_memory(), sg.base_v.cpu().pin_memory())
+    h2d = sum(q.numel() * 2 for q in pinned_q.values()) + sum(b[0].numel() * 4 for b in bases.values())
+
+    if world > 1:
+        host_out = [(torch.empty(f[0].shape, dtype=torch.bfloat16, pin_memory=True),
+                     torch.empty(f[1].shape, dtype=torch.bfloat16, pin_memory=True)) if f[0] is not None else None
+                    for f in full]
+        d2h = sum(f[0].numel() * 4 for f in full if f[0] is not None)
+        dev_bases = {}
+        for a in st.agents:
+            for sg in a.segments:
+                if sg.kind == kv.PLACEHOLDER:
+                    dev_bases[sg.pool] = (sg.base_k, sg.base_v)
+        qlist = [st.queries[n] for n in req.names]
+        agents_all = [a.agent for a in st.agents]
+
+        def e2e_step():
+            for n, q in pinned_q.items():
+                st.queries[n].copy_(q, non_blocking=True)
+            for n, (hk, hv) in bases.items():
+                dev_bases[n][0].copy_(hk, non_blocking=True)
+                dev_bases[n][1].copy_(hv, non_blocking=True)
+            req.plan.run(qlist, sync=False, stream=stream)
+            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
+            for f, ho in zip(full, host_out):
+                if ho is not None:
+                    ho[0].copy_(f[0], non_blocking=True)
+                    ho[1].copy_(f[1], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        k2 = max(3, args.steps // 3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        el2 = e0.elapsed_time(e1)
+        t = torch.tensor([el2], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el2 = float(t.item())
+        return {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": False}
+
+    # two buffer sets: set 0 = the bench state, set 1 = clones of the per-request inputs/outputs
+    sets = []
+    for b in range(2):
+        if b == 0:
+            agents, queries = st.agents, st.queries
+        else:
+            queries = {n: torch.empty_like(q) for n, q in st.queries.items()}
+            dev_b = {}
+            for a in st.agents:
+                for sg in a.segments:
+                    if sg.kind == kv.PLACEHOLDER and sg.pool not in dev_b:
+                        dev_b[sg.pool] = (torch.empty_like(sg.base_k), torch.empty_like(sg.base_v))
+            agents = []
+            for a in st.agents:
+                segs = [SegmentLayout(sg.kind, sg.pool, sg.consumer,
+                                      dev_b[sg.pool][0] if sg.kind == kv.PLACEHOLDER else sg.base_k,
+                                      dev_b[sg.pool][1] if sg.kind == kv.PLACEHOLDER else sg.base_v,
+                                      sg.base_start, sg.target_start) for sg in a.segments]
+                agents.append(AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, segs, torch.empty_like(a.dst_k),
+                                          torch.empty_like(a.dst_v)))
+        r = req if b == 0 else ReuseRequest(st.pools, agents, gamma=req.gamma, top_k=req.top_k)
+        dev_bases = {}
+        for a in agents:
+            for sg in a.segments:
+                if sg.kind == kv.PLACEHOLDER:
+                    dev_bases[sg.pool] = (sg.base_k, sg.base_v)
+        host_out = [(torch.empty(a.dst_k.shape, dtype=torch.bfloat16, pin_memory=True),
+                     torch.empty(a.dst_v.shape, dtype=torch.bfloat16, pin_memory=True)) for a in agents]
+        sets.append(dict(req=r, agents=agents, queries=queries, bases=dev_bases, host_out=host_out,
+                         qlist=[queries[n] for n in r.names],
+                         ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(), ev_out=torch.cuda.Event()))
+    d2h = sum(a.dst_k.numel() * 4 for a in st.agents)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    for S in sets:                      # events start "complete"
+        for e in (S["ev_comp"], S["ev_out"]):
+            e.record(stream)
+
+    def e2e_step(t):
+        S = sets[t % 2]
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(S["ev_comp"])             # step t-2 finished reading this input set
+            for n, q in pinned_q.items():
+                S["queries"][n].copy_(q, non_blocking=True)
+            for n, (hk, hv) in bases.items():
+                S["bases"][n][0].copy_(hk, non_blocking=True)
+                S["bases"][n][1].copy_(hv, non_blocking=True)
+            S["ev_in"].record(s_in)
+        stream.wait_event(S["ev_in"])
+        stream.wait_event(S["ev_out"])                # step t-2's results have left this output set
+        S["req"].plan.run(S["qlist"], sync=False, stream=stream)
+        S["ev_comp"].record(stream)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(S["ev_comp"])
+            for a, (hk, hv) in zip(S["agents"], S["host_out"]):
+                hk.copy_(a.dst_k, non_blocking=True)
+                hv.copy_(a.dst_v, non_blocking=True)
+            S["ev_out"].record(s_out)
+
+    for t in range(2):
+        e2e_step(t)
+    torch.cuda.synchronize()
+    k2 = max(4, args.steps // 3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(k2):
+        e2e_step(t)
+    for S in sets:
+        stream.wait_event(S["ev_out"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    el2 = e0.elapsed_time(e1)
+    for S in sets:
+        res = S["req"].results()
+        if res.fallback_agents:
+            raise SystemExit(f"e2e: agents {res.fallback_agents} fell back")
+    return {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": True}
+
+
 # --------------------------------------------------------------------------- ours
 
 def main():
@@ -285,9 +426,16 @@ def main():
         return
     if res.fallback_agents:
         raise SystemExit(f"agents {res.fallback_agents} took the fallback branch; the bench needs all Shareable")
-    # per-launch realign bytes: (k + 2) rows of d*2 bytes per (token, layer, head, plane)
-    # + the p_(m,0) rows the same launch copies (read + write)
-    alg_bytes = (res.blended_rows + 2 * res.realigned_tokens + 2 * res.copied_tokens) * Ls * row_bytes * 2
+    # per-launch realign bytes (unique traffic the algorithm must move), in token rows of
+    # d*2 bytes per (layer, head, plane): k offset rows + 1 output row per realigned token,
+    # each distinct base cache once (a sample realigned for several consumers shares it),
+    # and read + write of the p_(m,0) rows the same launch copies
+    uniq_base = {}
+    for a in st.agents:
+        for sg in a.segments:
+            uniq_base[sg.base_k.data_ptr()] = sg.base_k.shape[2]
+    base_tokens = sum(uniq_base.values())
+    alg_bytes = (res.blended_rows + res.realigned_tokens + base_tokens + 2 * res.copied_tokens) * Ls * row_bytes * 2
 
     if world > 1:
         dist.barrier()
@@ -331,46 +479,7 @@ def main():
     # ------------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
-        pinned_q = {n: q.cpu().pin_memory() for n, q in st.queries.items()}
-        bases = {}
-        for a in st.agents:
-            for s in a.segments:
-                if s.kind == kv.PLACEHOLDER and s.pool not in bases:
-                    bases[s.pool] = (s.base_k, s.base_v, s.base_k.cpu().pin_memory(), s.base_v.cpu().pin_memory())
-        host_out = [(torch.empty(a.dst_k.shape, dtype=torch.bfloat16, pin_memory=True),
-                     torch.empty(a.dst_v.shape, dtype=torch.bfloat16, pin_memory=True)) for a in st.agents]
-        h2d = sum(q.numel() * 2 for q in pinned_q.values()) + sum(b[2].numel() * 4 for b in bases.values())
-        d2h = sum(a.dst_k.numel() * 4 for a in st.agents)
-
-        def e2e_step():
-            for n, q in pinned_q.items():
-                st.queries[n].copy_(q, non_blocking=True)
-            for dk, dv, hk, hv in bases.values():
-                dk.copy_(hk, non_blocking=True)
-                dv.copy_(hv, non_blocking=True)
-            step()
-            for a, (hk, hv) in zip(st.agents, host_out):
-                hk.copy_(a.dst_k, non_blocking=True)
-                hv.copy_(a.dst_v, non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        k2 = max(3, args.steps // 3)
-        e0.record(stream)
-        for _ in range(k2):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        el2 = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([el2], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el2 = float(t.item())
-        e2e = {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": k2}
+        e2e = run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, shard)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -391,7 +500,9 @@ def main():
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,
-                         "realign_share_of_step": realign_avg / ms_per_step},
+                         "realign_share_of_step": realign_avg / ms_per_step,
+                         "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "
+                                        "base once + 2 per copied p0 token, x 128 KiB"},
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": int(n_launch),

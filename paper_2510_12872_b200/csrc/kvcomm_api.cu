@@ -662,34 +662,55 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
 }
 
 // h/dev: host image and device address of the realign part of a table.
-void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector<HostSeg>& hs,
+void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector<HostSeg>& hs_in,
                    const MatchResultDev* gate_results) {
   TableHdr& hdr = L.hdr;
   const int d = hdr.d, rpt = hdr.rows_per_tile;
+  // group segments that share a base cache (and hence its tiles): consecutive in the table
+  std::vector<int> order(hs_in.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const SegDev &x = hs_in[a].x, &y = hs_in[b].x;
+    if (x.base[0] != y.base[0]) return x.base[0] < y.base[0];
+    return x.L_seg < y.L_seg;
+  });
   SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
   int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.cand_off);
   float* dwexp = reinterpret_cast<float*>(dev + hdr.wexp_off);
   int64_t units = 0;
   int ipos = 0, wpos = 0;
-  for (size_t t = 0; t < hs.size(); ++t) {
-    SegDev x = hs[t].x;
-    x.cand_off = ipos;
-    if (x.n_cand) std::memcpy(ints + ipos, hs[t].cand, sizeof(int32_t) * x.n_cand);
-    ipos += x.n_cand;
-    x.n_gate = int32_t(hs[t].gates.size());
-    x.gate_off = ipos;
-    for (int32_t gi : hs[t].gates) ints[ipos++] = gi;
-    x.cs_off = int32_t(t) * (d / 2);
-    x.tiles = (x.L_seg + rpt - 1) / rpt;
-    x.unit_begin = units;
-    units += int64_t(hdr.Ls) * hdr.Hs * 2 * x.tiles;
-    if (hs[t].prefix) {
-      x.ld_w = (x.L_seg + 3) & ~3;
-      x.w = dwexp + wpos;
-      x.wexp_off = wpos;
-      wpos += int(x.ld_w) * x.n_cand;
+  const int n = int(order.size());
+  for (int t0 = 0; t0 < n;) {
+    int t1 = t0 + 1;
+    const SegDev& lead = hs_in[order[t0]].x;
+    while (t1 < n && hs_in[order[t1]].x.base[0] == lead.base[0] && hs_in[order[t1]].x.base[1] == lead.base[1] &&
+           hs_in[order[t1]].x.base_ld == lead.base_ld && hs_in[order[t1]].x.L_seg == lead.L_seg)
+      ++t1;
+    const int G = t1 - t0;
+    const int tiles = (lead.L_seg + rpt - 1) / rpt;
+    for (int t = t0; t < t1; ++t) {
+      const HostSeg& src = hs_in[order[t]];
+      SegDev x = src.x;
+      x.cand_off = ipos;
+      if (x.n_cand) std::memcpy(ints + ipos, src.cand, sizeof(int32_t) * x.n_cand);
+      ipos += x.n_cand;
+      x.n_gate = int32_t(src.gates.size());
+      x.gate_off = ipos;
+      for (int32_t gi : src.gates) ints[ipos++] = gi;
+      x.cs_off = t * (d / 2);
+      x.tiles = tiles;
+      x.unit_begin = units;
+      x.group_size = G;
+      if (src.prefix) {
+        x.ld_w = (x.L_seg + 3) & ~3;
+        x.w = dwexp + wpos;
+        x.wexp_off = wpos;
+        wpos += int(x.ld_w) * x.n_cand;
+      }
+      segs[t] = x;
     }
-    segs[t] = x;
+    units += int64_t(hdr.Ls) * hdr.Hs * 2 * tiles * G;
+    t0 = t1;
   }
   hdr.total_units = units;
   hdr.gate_results = gate_results;

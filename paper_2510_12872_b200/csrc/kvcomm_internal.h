@@ -26,7 +26,7 @@ struct SegDev {
   const float* wbar;    // PREFIX: scalar weights [capacity] (expanded by the prep kernel)
   int64_t base_ld, dst_ld, ld_w;
   int64_t slot_stride, plane_stride, off_ld;  // elements
-  int64_t unit_begin;   // first work unit of this segment
+  int64_t unit_begin;   // first work unit of this segment's group (same for every member)
   int32_t L_seg, target_start, delta, n_cand;
   int32_t cand_off;     // index of this segment's first candidate in Table::cand
   int32_t cs_off;       // index (in float2) of its cos/sin table in Table::cs
@@ -35,7 +35,8 @@ struct SegDev {
   int32_t wexp_off;     // PREFIX: float offset of the expanded weights in Table::wexp
   int32_t n_gate;       // segment runs iff every listed match verdict is SHAREABLE (device-side
   int32_t gate_off;     //   branch of Alg. 1); indices into Table::cand area, n_gate = 0: always
-  int32_t _pad;
+  int32_t group_size;   // segments sharing this base tile (consecutive in the table; units interleave
+                        //   members so the shared base tile is read from HBM once and hit in L2 after)
 };
 
 struct MatchResultDev {

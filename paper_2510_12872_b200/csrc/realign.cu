@@ -56,15 +56,23 @@ struct Unit {
   int s, l, h, p, t;
 };
 
-// unit -> (segment, layer, head, plane, tile); tile fastest so that neighbouring
-// CTAs stream neighbouring 16 KiB tiles of the same anchor at the same time.
+// unit -> (segment, layer, head, plane, tile), tile fastest so that neighbouring CTAs
+// stream neighbouring 16 KiB tiles of the same anchor at the same time.  Segments that
+// share one base cache (one sample realigned for several consumers) form a group whose
+// members are interleaved just outside the tile index: all members' units of one
+// (layer, head, plane) fall in the same round of CTAs, so the shared base tile is
+// fetched from HBM once and hit in L2 by the other members.
 __device__ __forceinline__ Unit decode_unit(const SegDev* segs, int n_seg, int Hs, int64_t u) {
   Unit r;
-  r.s = find_segment(segs, n_seg, u);
-  int64_t rem = u - segs[r.s].unit_begin;
-  const int tiles = segs[r.s].tiles;
+  const int last = find_segment(segs, n_seg, u);   // last member of the unit's group
+  int64_t rem = u - segs[last].unit_begin;
+  const int G = segs[last].group_size;
+  const int tiles = segs[last].tiles;              // equal for every member
   r.t = int(rem % tiles);
   rem /= tiles;
+  const int member = int(rem % G);
+  rem /= G;
+  r.s = last - (G - 1) + member;
   r.p = int(rem & 1);
   rem >>= 1;
   r.h = int(rem % Hs);
@@ -143,7 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
   if (warp == kConsumerWarps) {
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
-      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_stream = policy_evict_first();  // offsets: read once per request
+      const uint64_t pol_shared = (variant & 4) ? policy_evict_first()
+                                  : (variant & 8) ? policy_evict_normal() : policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
           } else {
             const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
             mbar_arrive_expect_tx(&full[stage], bytes);
-            bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
+            bulk_g2s(dst, src, bytes, &full[stage], g.group_size > 1 ? pol_shared : pol_stream);
           }
           if (++stage == kNStage) { stage = 0; phase ^= 1u; }
         }

@@ -79,6 +79,77 @@ __global__ void tma_read(const uint8_t* src, int64_t nchunks, int chunk, int nst
   }
 }
 
+// Read stream of 16 KiB TMA tiles; every `wevery`-th tile is written back to a
+// distinct destination with a TMA bulk store (mode 0: no hint, 1: evict_first,
+// 2: evict_last, 3: per-thread st.global.cs, 4: per-thread st.global.wb).
+__global__ void tma_mix_store(const uint8_t* src, int64_t nchunks, int chunk, int nstage, uint8_t* wdst, int wevery,
+                              int mode) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(nstage) * chunk);
+  uint64_t* empty = full + nstage;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t pol, pst;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (mode == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pst));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pst));
+  if (threadIdx.x >= 32) {
+    if (threadIdx.x == 32) {
+      int st = 0; uint32_t ph = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_expect(&full[st], chunk);
+        bulk(sm + size_t(st) * chunk, src + c * chunk, chunk, &full[st], pol);
+        if (++st == nstage) { st = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  int st = 0; uint32_t ph = 0;
+  int64_t k = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++k) {
+    mbar_wait(&full[st], ph);
+    bool wrote = false;
+    if ((k % wevery) == 0) {
+      const int64_t wi = (k / wevery) * gridDim.x + blockIdx.x;
+      uint8_t* d = wdst + wi * chunk;
+      const uint8_t* sp = sm + size_t(st) * chunk;
+      if (mode <= 2) {
+        if (threadIdx.x == 0) {
+          if (mode == 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d), "r"(smem_u32(sp)),
+                         "r"(chunk) : "memory");
+          else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(d),
+                         "r"(smem_u32(sp)), "r"(chunk), "l"(pst) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        wrote = true;
+      } else {
+        const uint4* s4 = reinterpret_cast<const uint4*>(sp);
+        uint4* d4 = reinterpret_cast<uint4*>(d);
+        for (int i = threadIdx.x; i < chunk / 16; i += 32) {
+          uint4 v = s4[i];
+          if (mode == 3)
+            asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d4 + i), "r"(v.x), "r"(v.y), "r"(v.z),
+                         "r"(v.w) : "memory");
+          else
+            d4[i] = v;
+        }
+      }
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+    (void)wrote;
+    if (++st == nstage) { st = 0; ph ^= 1; }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int U>
 __global__ void ldg_read(const uint4* src, int64_t n, uint32_t* out) {
   uint32_t acc = 0;
@@ -159,6 +230,22 @@ int main() {
       snprintf(name, sizeof(name), "tma_mix %d:1 chunk=16K stages=11", we);
       timeit([&] { tma_read<<<sms, 64, smem>>>(src, n, chunk, nst, dst, we); }, double(bytes) * (1.0 + 1.0 / we),
              name);
+    }
+  }
+  {
+    int chunk = 16384, nst = 11;
+    size_t smem = size_t(nst) * chunk + 2 * nst * 8;
+    cudaFuncSetAttribute(tma_mix_store, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int64_t n = bytes / chunk;
+    const char* names[] = {"bulk store", "bulk store evict_first", "bulk store evict_last", "st.global.cs",
+                           "st.global (wb)"};
+    for (int we : {22, 17}) {
+      for (int mode = 0; mode < 5; ++mode) {
+        char name[96];
+        snprintf(name, sizeof(name), "mix %d:1 %s", we, names[mode]);
+        timeit([&] { tma_mix_store<<<sms, 64, smem>>>(src, n, chunk, nst, dst, we, mode); },
+               double(bytes) * (1.0 + 1.0 / we), name);
+      }
     }
   }
   int64_t nv = bytes / 16;
