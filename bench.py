@@ -375,9 +375,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # Test-only knob: KVCOMM_BENCH_SAME_GPU=1 puts every rank on cuda:0 over gloo so the
+    # multi-rank code path (layer shards, gather, max-over-ranks timing) can be exercised on
+    # a one-GPU box.  Numbers from such a run are not scaling numbers (flagged in config).
+    same_gpu = os.environ.get("KVCOMM_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import synth
     from synth.state import build_five_agent_state
     import paper_2510_12872_b200 as kv
@@ -494,7 +503,8 @@ def main():
                                    "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
                        "realigned_tokens_per_step": total_tokens, "anchors_blended": w.capacity,
                        "gamma": args.gamma, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
-                       "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed},
+                       "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed,
+                       **({"test_same_gpu_gloo": True} if same_gpu else {})},
             "roofline": {"kernel": "kvc::realign_kernel (30 segments + 5 p0 copies, one launch)", "bound": "hbm",
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,

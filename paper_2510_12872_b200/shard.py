@@ -40,6 +40,17 @@ def gather_to_consumers(agents: Sequence[int], shards: Sequence[Tuple[torch.Tens
     shards[i] = (K, V) of agents[i] on this rank, [Ls, Hs, N, d]
     full[i]   = (K, V) full-depth buffers on the consumer rank (ignored elsewhere)
     """
+    staged = dist.get_backend(group) == "gloo" and any(
+        t is not None and t.is_cuda for pair in shards for t in pair)
+    if staged:   # gloo moves host tensors only: stage through host memory (test path)
+        cpu_full = [(f[0].cpu(), f[1].cpu()) if f[0] is not None else (None, None) for f in full]
+        gather_to_consumers(agents, [(k.cpu(), v.cpu()) for k, v in shards], cpu_full, num_layers, rank, world,
+                            group)
+        for f, c in zip(full, cpu_full):
+            if f[0] is not None:
+                f[0].copy_(c[0])
+                f[1].copy_(c[1])
+        return
     ops = []
     for i, m in enumerate(agents):
         dst = consumer_rank(m, world)
