@@ -390,3 +390,73 @@ class PoolModel:
             if s not in self.slot_len:
                 raise KeyError(s)
             self.access[s] += 1
+
+
+# ---------------------------------------------------------------------------
+# Online pool maintenance over a request stream (Algorithm 1; SURVEY
+# §8(f) f1): one placeholder pool shared by several consumers (agents).
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ConsumerLayout:
+    """Where the placeholder and its following prefix sit in consumer c's prompt."""
+    t0: int                      # placeholder target start = |p_(c,0)|
+    pf_base_k: np.ndarray        # prefix base [L, H, P_c, d], at base position pf_base_start
+    pf_base_v: np.ndarray
+    pf_base_start: int           # = |p_(c,0)| (reading A11)
+
+
+class OnlinePoolOracle:
+    """Algorithm 1 for one placeholder pool, step by step in the paper's order.
+
+    step(): Eq. 5 prediction; if Shareable, the reuse branch realigns the
+    placeholder (Eq. 6) and its neighbouring prefix (Eq. 7) for every consumer
+     and counts an access for every candidate (reading A18); otherwise the
+    fallback branch takes the dense ("real") caches, measures placeholder and prefix
+    offsets against the bases, stores them in bf16 (reading A14) and
+    inserts the sample as a new anchor with LFU pruning (reading A17).
+    """
+
+    def __init__(self, capacity: int, layouts: Sequence[ConsumerLayout], inv_freq: np.ndarray, gamma: float,
+                 scalar: str = FROBENIUS):
+        self.pool = PoolModel(capacity)
+        self.layouts = list(layouts)
+        self.inv = inv_freq
+        self.gamma = gamma
+        self.scalar = scalar
+        self.emb: Dict[int, np.ndarray] = {}
+        self.off: Dict[int, list] = {}        # slot -> per consumer (dk_ph, dv_ph, dk_pf, dv_pf)
+
+    def step(self, h_phi, base_k, base_v, real):
+        """real(c) -> (k_ph, v_ph, k_pf, v_pf): the dense prefill of consumer c (fallback only).
+        Returns (MatchResult, outputs per consumer [(k_ph, v_ph, k_pf, v_pf)], (slot, evicted) or None)."""
+        L = h_phi.shape[0]
+        r = predict(h_phi, dict(self.pool.slot_len), self.emb, {s: True for s in self.pool.slot_len},
+                    self.gamma, 0, self.scalar)
+        outs = []
+        if r.verdict == SHAREABLE:
+            for c, lay in enumerate(self.layouts):
+                ph = realign_segment(r.W, base_k, base_v, [self.off[s][c][0] for s in r.candidates],
+                                     [self.off[s][c][1] for s in r.candidates], 0, lay.t0, self.inv)
+                pf = realign_segment(r.wbar, lay.pf_base_k, lay.pf_base_v,
+                                     [self.off[s][c][2] for s in r.candidates],
+                                     [self.off[s][c][3] for s in r.candidates], lay.pf_base_start, lay.t0 + L,
+                                     self.inv, kind="prefix")
+                outs.append((ph["k"], ph["v"], pf["k"], pf["v"]))
+            self.pool.record_access(r.candidates)
+            return r, outs, None
+        slot, ev = self.pool.insert(L)
+        if ev >= 0:
+            del self.emb[ev], self.off[ev]
+        self.emb[slot] = np.asarray(h_phi, np.float64)
+        offs = []
+        for c, lay in enumerate(self.layouts):
+            kph, vph, kpf, vpf = [np.asarray(x, np.float64) for x in real(c)]
+            dkp, dvp = measure_offset(kph, vph, lay.t0, base_k, base_v, 0, self.inv)
+            dkf, dvf = measure_offset(kpf, vpf, lay.t0 + L, lay.pf_base_k, lay.pf_base_v, lay.pf_base_start,
+                                      self.inv)
+            offs.append((bf16_round(dkp), bf16_round(dvp), bf16_round(dkf), bf16_round(dvf)))
+            outs.append((kph, vph, kpf, vpf))
+        self.off[slot] = offs
+        return r, outs, (slot, ev)

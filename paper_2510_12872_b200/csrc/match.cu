@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
     res->entropy = H;
     res->threshold = thr;
     res->verdict = H > thr ? 1 : 0;
-    res->tie_flag = fabs(H - thr) <= kTieRel * thr ? 1 : 0;
+    res->tie_flag = (a.n_cand > 1 && fabs(H - thr) <= kTieRel * thr) ? 1 : 0;  // |𝒜|=1: H = 0 = thr exactly
     res->tie_count = ties[blockIdx.x];
   }
 }

@@ -266,3 +266,107 @@ def five_agent_workload(L: int = 32, H: int = 8, d: int = 128, D_e: int = 4096,
             pos += ps.prefix_len[c]
         agents.append(AgentSpec(m, pos, p0, segs))
     return Workload("llama3-8b-5agent", L, H, d, D_e, capacity, pools, agents)
+
+
+# ----------------------------------------------------------------------------
+# Request streams and a synthetic "dense prefill" (stand-in for the model) for the
+# online pool maintenance of Algorithm 1.  Inputs only: the
+# "true" in-context caches a model would produce, which both the oracle and the
+# CUDA path receive; no KVComm arithmetic.
+# ----------------------------------------------------------------------------
+
+
+@dataclass
+class StreamSpec:
+    L: int = 2
+    H: int = 2
+    d: int = 32
+    D_e: int = 32
+    n_vocab: int = 64
+    consumers: int = 2
+    p0: Tuple[int, ...] = (12, 20)          # |p_(c,0)| per consumer (placeholder target position)
+    prefix: Tuple[int, ...] = (4, 6)        # |p_(c,1)| per consumer
+    lengths: Tuple[int, ...] = (16, 20, 24, 28, 32, 36, 40)  # sample lengths drawn per request
+    n_clusters: int = 3
+    p_swap: float = 0.15
+
+
+def clustered_stream(spec: StreamSpec, n_requests: int, seed: int = 0) -> List[torch.Tensor]:
+    """Token-id sequences: each request picks a cluster (a fixed id sequence), a length,
+    and re-draws each position with probability p_swap."""
+    g = make_gen(seed)
+    Lmax = max(spec.lengths)
+    centers = [torch.randint(0, spec.n_vocab, (Lmax,), generator=g) for _ in range(spec.n_clusters)]
+    out = []
+    for _ in range(n_requests):
+        c = int(torch.randint(0, spec.n_clusters, (1,), generator=g))
+        L = spec.lengths[int(torch.randint(0, len(spec.lengths), (1,), generator=g))]
+        ids = centers[c][:L].clone()
+        swap = torch.rand(L, generator=g) < spec.p_swap
+        ids = torch.where(swap, torch.randint(0, spec.n_vocab, (L,), generator=g), ids)
+        out.append(ids)
+    return out
+
+
+class SyntheticPrefill:
+    """Deterministic stand-in for the model's caches (CPU, float64 -> bf16):
+      base (standalone) cache of a sample: K_b, V_b = E·Wk_b, E·Wv_b (+ RoPE at its own positions
+      is irrelevant: the base frame is position 0 for both sides)
+      in-context cache for consumer c: base + a context offset tanh(E·A_c)·0.15 that varies
+      smoothly with the token embedding (Prop. 2's premise), keys rotated to the target
+      positions by RoPE with the given inv_freq.
+    Everything is an INPUT to both the oracle and the CUDA path."""
+
+    def __init__(self, spec: StreamSpec, inv_freq: np.ndarray, seed: int = 0):
+        g = make_gen(seed + 4242)
+        s = spec
+        self.spec, self.inv = s, np.asarray(inv_freq, np.float64)
+        self.table = vocab_table(s.n_vocab, s.D_e, g).double()
+        sc = 1.0 / math.sqrt(s.D_e)
+        self.Wk = torch.randn(s.L, s.H, s.D_e, s.d, generator=g, dtype=torch.float64) * sc * 4
+        self.Wv = torch.randn(s.L, s.H, s.D_e, s.d, generator=g, dtype=torch.float64) * sc * 4
+        self.A = torch.randn(s.consumers, 2, s.L, s.H, s.D_e, s.d, generator=g, dtype=torch.float64) * sc * 4
+        self.B = torch.randn(s.consumers, 2, s.L, s.H, s.D_e, s.d, generator=g, dtype=torch.float64) * sc * 4
+        self.pf_base = [[randn_bf16((s.L, s.H, P, s.d), g) for _ in range(2)] for P in s.prefix]
+
+    def emb(self, ids: torch.Tensor) -> torch.Tensor:
+        return self.table[ids].to(torch.bfloat16)
+
+    def _rot(self, x: torch.Tensor, pos0: int, per_row: bool = True) -> torch.Tensor:
+        """The model's RoPE (rotate_half): row i of the token axis goes to absolute position
+        pos0 + i (per_row) or every row is moved by pos0 (a uniform shift)."""
+        n, d = x.shape[-2], x.shape[-1]
+        pos = torch.arange(pos0, pos0 + n, dtype=torch.float64) if per_row else torch.full((n,), float(pos0),
+                                                                                            dtype=torch.float64)
+        ang = pos[:, None] * torch.from_numpy(self.inv)[None, :]
+        c, s_ = torch.cos(ang), torch.sin(ang)
+        x1, x2 = x[..., : d // 2], x[..., d // 2:]
+        return torch.cat([x1 * c - x2 * s_, x2 * c + x1 * s_], dim=-1)
+
+    def base(self, ids: torch.Tensor):
+        """Standalone prefill of the sample at positions 0..L-1 (the anchor/base cache)."""
+        E = self.table[ids]
+        k = self._rot(torch.einsum("ie,lhed->lhid", E, self.Wk), 0)
+        v = torch.einsum("ie,lhed->lhid", E, self.Wv)
+        return k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous()
+
+    def real(self, ids: torch.Tensor, c: int):
+        """(placeholder K, V, prefix K, V) of the sample inside consumer c's prompt: the
+        sample at positions p0_c.., its context deviation a smooth function of the token
+        embeddings; the prefix p_(c,1) right after it, shifted by L from its base position."""
+        s = self.spec
+        E = self.table[ids]
+        L = len(ids)
+        ok = 0.15 * torch.tanh(torch.einsum("ie,lhed->lhid", E, self.A[c, 0]))
+        ov = 0.15 * torch.tanh(torch.einsum("ie,lhed->lhid", E, self.A[c, 1]))
+        t0 = s.p0[c]
+        kph = self._rot(torch.einsum("ie,lhed->lhid", E, self.Wk) + ok, t0).to(torch.bfloat16)
+        vph = (torch.einsum("ie,lhed->lhid", E, self.Wv) + ov).to(torch.bfloat16)
+        m = E.mean(0, keepdim=True)
+        P = s.prefix[c]
+        pk = 0.15 * torch.tanh(torch.einsum("ie,lhed->lhid", m.expand(P, -1), self.B[c, 0]))
+        pv = 0.15 * torch.tanh(torch.einsum("ie,lhed->lhid", m.expand(P, -1), self.B[c, 1]))
+        pbk, pbv = self.pf_base[c]
+        kpf = self._rot(pbk.double() + pk, L, per_row=False).to(torch.bfloat16)
+        vpf = (pbv.double() + pv).to(torch.bfloat16)
+        return tuple(x.contiguous() for x in (kph, vph, kpf, vpf))

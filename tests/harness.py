@@ -188,7 +188,7 @@ def compare(gpu: Dict, ora: Dict, p: synth.Problem, check_values: bool = True) -
     assert np.all(np.abs(gwb - owb) <= 1e-5 * np.abs(owb) + 1e-7)
     assert abs(gm.entropy - om.H) <= 1e-6 * abs(om.H) + 1e-9, (gm.entropy, om.H)
     assert abs(gm.threshold - om.threshold) <= 1e-6 * om.threshold + 1e-12, (gm.threshold, om.threshold)
-    in_band = abs(om.H - om.threshold) <= TIE_REL * max(om.threshold, 1e-300)
+    in_band = len(om.candidates) > 1 and abs(om.H - om.threshold) <= TIE_REL * om.threshold
     if not in_band:
         assert gm.verdict == om.verdict and gm.reason == names[om.reason], (gm.reason, om.reason)
     stats["verdict_in_band"] = in_band

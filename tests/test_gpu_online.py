@@ -1,0 +1,110 @@
+"""Online pool maintenance (Algorithm 1 over a request stream):
+the CUDA path (paper_2510_12872_b200.online.OnlinePool: match, gated realign,
+device-side offset measurement on insert, LFU pruning) against the oracle's
+OnlinePoolOracle on the same clustered stream — verdict by verdict, slot by slot,
+cache by cache.  (-m gpu)"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import kvcomm_oracle as O
+from tests import harness
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(gamma, capacity, seed=1, n=40):
+    from paper_2510_12872_b200 import kvcomm as K
+    from paper_2510_12872_b200.online import ConsumerSlot, OnlinePool
+    spec = synth.StreamSpec()
+    inv = synth.plain_inv_freq(spec.d)
+    sp = synth.SyntheticPrefill(spec, inv)
+    Lmax = max(spec.lengths)
+    pool = K.AnchorPool(num_layers=spec.L, num_kv_heads=spec.H, head_dim=spec.d, emb_dim=spec.D_e,
+                        capacity=capacity, max_anchor_len=Lmax, prefix_len=list(spec.prefix), inv_freq=inv)
+    cons = []
+    for c in range(spec.consumers):
+        N = spec.p0[c] + Lmax + spec.prefix[c]
+        dk = torch.zeros(spec.L, spec.H, N, spec.d, dtype=torch.bfloat16, device="cuda")
+        cons.append(ConsumerSlot(spec.p0[c], sp.pf_base[c][0].cuda(), sp.pf_base[c][1].cuda(), spec.p0[c], dk,
+                                 torch.zeros_like(dk)))
+    online = OnlinePool(pool, cons, gamma=gamma)
+    f64 = harness.f64
+    lay = [O.ConsumerLayout(spec.p0[c], f64(sp.pf_base[c][0]), f64(sp.pf_base[c][1]), spec.p0[c])
+           for c in range(spec.consumers)]
+    orc = O.OnlinePoolOracle(capacity, lay, inv, gamma)
+    return spec, sp, online, orc, synth.clustered_stream(spec, n, seed=seed)
+
+
+@pytest.mark.parametrize("gamma,capacity", [(0.5, 4), (0.9, 2), (0.3, 6)])
+def test_online_stream_matches_oracle(gamma, capacity):
+    spec, sp, online, orc, stream = _setup(gamma, capacity)
+    f64 = harness.f64
+    n_new = n_evict = n_reuse = 0
+    for step, ids in enumerate(stream):
+        emb = sp.emb(ids)
+        bk, bv = sp.base(ids)
+        reals = [sp.real(ids, c) for c in range(spec.consumers)]
+        g = online.step(emb.cuda(), bk.cuda(), bv.cuda(), lambda c: tuple(x.cuda() for x in reals[c]))
+        torch.cuda.synchronize()
+        r, outs, ins = orc.step(f64(emb), f64(bk), f64(bv), lambda c: [f64(x) for x in reals[c]])
+        if len(r.candidates) > 1 and abs(r.H - r.threshold) <= 1e-6 * r.threshold:
+            pytest.skip(f"step {step}: oracle verdict inside the tie band")
+        assert g.verdict == r.verdict, (step, g.reason, r.reason, g.entropy, r.H)
+        assert g.candidates == r.candidates, step
+        L = len(ids)
+        for c, cs in enumerate(online.consumers):
+            t0, P = spec.p0[c], spec.prefix[c]
+            gk = f64(cs.dst_k[:, :, t0:t0 + L])
+            gv = f64(cs.dst_v[:, :, t0:t0 + L])
+            gpk = f64(cs.dst_k[:, :, t0 + L:t0 + L + P])
+            gpv = f64(cs.dst_v[:, :, t0 + L:t0 + L + P])
+            ok, ov, opk, opv = outs[c]
+            if ins is not None:            # fallback: the dense caches, copied bit-exactly
+                assert np.array_equal(gk, ok) and np.array_equal(gv, ov)
+                assert np.array_equal(gpk, opk) and np.array_equal(gpv, opv)
+            else:                          # reuse: Eq. 6 / Eq. 7 realignment
+                offs = [orc.off[s][c] for s in r.candidates]
+                absk = O.blend_placeholder(r.W, [np.abs(o[0]) for o in offs])
+                absv = O.blend_placeholder(r.W, [np.abs(o[1]) for o in offs])
+                harness.check_kv(gk, ok, f64(bk), absk, f"step {step} K ph c{c}")
+                harness.check_kv(gv, ov, f64(bv), absv, f"step {step} V ph c{c}")
+                pabsk = O.blend_prefix(r.wbar, [np.abs(o[2]) for o in offs])
+                pabsv = O.blend_prefix(r.wbar, [np.abs(o[3]) for o in offs])
+                harness.check_kv(gpk, opk, f64(sp.pf_base[c][0]), pabsk, f"step {step} K pf c{c}")
+                harness.check_kv(gpv, opv, f64(sp.pf_base[c][1]), pabsv, f"step {step} V pf c{c}")
+        if ins is not None:
+            assert (g.slot, g.evicted) == ins, step
+            n_new += 1
+            n_evict += ins[1] >= 0
+            # offsets measured on the device == oracle's measurement (bf16, ≤ 1 ulp)
+            for c in range(spec.consumers):
+                gk_off, gv_off = online.pool.offset_view(g.slot, c, "ph", rows=L)
+                odk, odv = orc.off[g.slot][c][0], orc.off[g.slot][c][1]
+                harness.check_kv(f64(gk_off), odk, np.zeros_like(odk), np.abs(odk) + 4.0, f"measured dK c{c}")
+                assert np.array_equal(f64(gv_off), odv)
+        else:
+            n_reuse += 1
+    for s in range(capacity):
+        info = online.pool.slot_info(s)
+        assert info["occupied"] == (s in orc.pool.slot_len)
+        if info["occupied"]:
+            assert info["access_count"] == orc.pool.access[s] and info["length"] == orc.pool.slot_len[s]
+    assert n_new > 1 and n_reuse > 1
+    assert online.reuse_rate == pytest.approx(n_reuse / len(stream))
+
+
+def test_online_reuse_rate_non_decreasing_in_gamma():
+    """Table 6 direction: on a fixed seeded stream the reuse rate does not
+    decrease as the entropy threshold γ grows."""
+    rates = []
+    for gamma in (0.0, 0.1, 0.3, 0.5, 0.7, 0.9):
+        spec, sp, online, orc, stream = _setup(gamma, 4, seed=2, n=30)
+        for ids in stream:
+            bk, bv = sp.base(ids)
+            online.step(sp.emb(ids).cuda(), bk.cuda(), bv.cuda(),
+                        lambda c, ids=ids: tuple(x.cuda() for x in sp.real(ids, c)))
+        rates.append(online.reuse_rate)
+    assert all(b >= a for a, b in zip(rates, rates[1:])), rates
+    assert rates[-1] > rates[0]

@@ -431,3 +431,52 @@ def test_table_a5_latency_linear_in_anchors_times_tokens():
             per_unit.append(lat / (m * seq))
     per_unit = np.array(per_unit)
     assert per_unit.max() / per_unit.min() < 1.35
+
+
+# ---------------------------------------------------------------- online loop (f1)
+
+def _online(gamma, capacity, seed=1, n=30):
+    spec = synth.StreamSpec()
+    inv = synth.plain_inv_freq(spec.d)
+    sp = synth.SyntheticPrefill(spec, inv)
+    f64 = lambda t: t.double().numpy()
+    lay = [O.ConsumerLayout(spec.p0[c], f64(sp.pf_base[c][0]), f64(sp.pf_base[c][1]), spec.p0[c])
+           for c in range(spec.consumers)]
+    return spec, sp, f64, O.OnlinePoolOracle(capacity, lay, inv, gamma), synth.clustered_stream(spec, n, seed)
+
+
+def test_online_first_request_falls_back_and_replay_reproduces_dense_cache():
+    # Alg. 1: an empty pool forces the fallback; the sample becomes an anchor
+    # whose offsets are measured against its base.  Replaying the same sample against that
+    # single anchor (|A| = 1 -> weight exactly 1, H = 0 -> Shareable) applies exactly the
+    # measured offsets, so the realigned cache equals the dense cache up to the bf16
+    # storage of the offsets (SPEC acceptance #3, exact-anchor fidelity).
+    spec, sp, f64, orc, stream = _online(0.3, 4)
+    ids = stream[0]
+    h = f64(sp.emb(ids))
+    bk, bv = [f64(x) for x in sp.base(ids)]
+    reals = [[f64(x) for x in sp.real(ids, c)] for c in range(spec.consumers)]
+    r, outs, ins = orc.step(h, bk, bv, lambda c: reals[c])
+    assert r.reason == O.R_EMPTY_POOL and ins == (0, -1)
+    r, outs, ins = orc.step(h, bk, bv, lambda c: reals[c])
+    assert r.verdict == O.SHAREABLE and ins is None and np.all(r.W == 1.0) and r.H == 0.0
+    for c in range(spec.consumers):
+        for got, dense in zip(outs[c], reals[c]):
+            # the stored offset is rounded to bf16 (<= 2^-9 relative of |Δ| <= ~0.2 + |x| terms)
+            np.testing.assert_allclose(got, dense, atol=2e-2, rtol=1e-2)
+    assert orc.pool.access[0] == 1
+
+
+def test_online_reuse_non_decreasing_in_gamma_and_capacity_bound():
+    rates = []
+    for gamma in (0.0, 0.1, 0.3, 0.5, 0.7, 0.9):
+        spec, sp, f64, orc, stream = _online(gamma, 4, seed=2)
+        reused = 0
+        for ids in stream:
+            bk, bv = [f64(x) for x in sp.base(ids)]
+            r, outs, ins = orc.step(f64(sp.emb(ids)), bk, bv,
+                                    lambda c, ids=ids: [f64(x) for x in sp.real(ids, c)])
+            reused += ins is None
+            assert len(orc.pool.slot_len) <= 4                  # capacity invariant
+        rates.append(reused / len(stream))
+    assert all(b >= a for a, b in zip(rates, rates[1:])) and rates[-1] > rates[0], rates
