@@ -75,6 +75,7 @@ typedef enum {
 } kvcomm_reason;
 
 typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_scalar_distance;
+typedef enum { KVCOMM_SIM_L2 = 0, KVCOMM_SIM_COSINE = 1 } kvcomm_similarity;
 /* COPY: rows copied verbatim (no offsets, no rotation; bit-exact), e.g. p_(m,0) of the
  * concatenation (reading A20) riding in the same launch as the realignment. */
 typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1, KVCOMM_COPY = 2 } kvcomm_segment_kind;
@@ -100,6 +101,10 @@ typedef struct {
   int32_t scalar_distance; /* sample-level distance d̄ of Eq. 5/7 (reading A4):
                               KVCOMM_SCALAR_FROBENIUS (0, default) d̄_j = sqrt(Σ_i d[i,j]²),
                               KVCOMM_SCALAR_MEAN_L2  (1)           d̄_j = mean_i d[i,j]     */
+  int32_t similarity;      /* matching score (Table A.4):
+                              KVCOMM_SIM_L2 (0, paper default): d = ‖h_φ[i] - h_ψ[i]‖₂, w = softmax(-d);
+                              KVCOMM_SIM_COSINE (1): d = 1 - cos(h_φ[i], h_ψ[i]), w = softmax(cos);
+                              sample level: 1 - <h_φ,h_ψ>_F / (‖h_φ‖_F ‖h_ψ‖_F)            */
   const int32_t* prefix_len; /* host [num_consumers]: |p_(m,i)| following this placeholder */
   const double* inv_freq;  /* host [head_dim/2]: RoPE inverse frequencies (copied)        */
 } kvcomm_pool_config;

@@ -139,6 +139,38 @@ def distances(h_phi: np.ndarray, h_anchor: Sequence[np.ndarray]) -> np.ndarray:
     return np.stack(cols, axis=1)
 
 
+L2, COSINE = "l2", "cosine"
+
+
+def cosine_distances(h_phi: np.ndarray, h_anchor: Sequence[np.ndarray]) -> np.ndarray:
+    """Table A.4's "Cosine Similarity" variant: per position
+    d[i, j] = 1 - cos(h_φ[i], h_ψj[i]) (cos = 0 for a zero row), so that
+    softmax(-d) = softmax(cos).  Anchors truncated to the first L_φ rows (A8)."""
+    h_phi = np.asarray(h_phi, dtype=np.float64)
+    L_phi = h_phi.shape[0]
+    cols = []
+    for h in h_anchor:
+        a = np.asarray(h, dtype=np.float64)[:L_phi]
+        num = np.sum(h_phi * a, axis=1)
+        den = np.sqrt(np.sum(h_phi * h_phi, axis=1) * np.sum(a * a, axis=1))
+        cols.append(1.0 - np.where(den > 0, num / np.where(den > 0, den, 1.0), 0.0))
+    if not cols:
+        return np.zeros((L_phi, 0))
+    return np.stack(cols, axis=1)
+
+
+def cosine_scalar(h_phi: np.ndarray, h_anchor: Sequence[np.ndarray]) -> np.ndarray:
+    """Sample-level cosine distance 1 - <h_φ, h_ψ>_F / (‖h_φ‖_F ‖h_ψ‖_F) (A4 analogue)."""
+    h_phi = np.asarray(h_phi, dtype=np.float64)
+    L_phi = h_phi.shape[0]
+    out = []
+    for h in h_anchor:
+        a = np.asarray(h, dtype=np.float64)[:L_phi]
+        den = np.sqrt(np.sum(h_phi * h_phi) * np.sum(a * a))
+        out.append(1.0 - (np.sum(h_phi * a) / den if den > 0 else 0.0))
+    return np.array(out)
+
+
 def softmax_neg(dist: np.ndarray, axis: int = -1) -> np.ndarray:
     """softmax(-dist) along `axis`, temperature 1, max-subtracted (reading A15)."""
     z = -np.asarray(dist, dtype=np.float64)
@@ -217,7 +249,7 @@ class MatchResult:
 
 def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int, np.ndarray],
             offsets_present: Dict[int, bool], gamma: float, top_k: int = 0,
-            scalar: str = FROBENIUS) -> MatchResult:
+            scalar: str = FROBENIUS, similarity: str = L2) -> MatchResult:
     """Eq. 5:  NewAnchor ⇔ (L_φ > max_{ψ∈𝒜} L_ψ) ∪ (H_{φ|𝒜} > γ log|𝒜_φ|).
 
     Readings: the max runs over the whole pool (A7); an empty pool or an empty 𝒜_φ
@@ -234,9 +266,17 @@ def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int,
     cand = candidate_slots(anchor_len, offsets_present, L_phi)
     if not cand:
         return MatchResult(NEW_ANCHOR, R_NO_CANDIDATES, [])
-    dist = distances(h_phi, [anchor_emb[s] for s in cand])
-    W, idx = position_weights(dist, top_k, cand)
-    dbar, wbar = scalar_weights(dist, scalar)
+    if similarity == L2:
+        dist = distances(h_phi, [anchor_emb[s] for s in cand])
+        W, idx = position_weights(dist, top_k, cand)
+        dbar, wbar = scalar_weights(dist, scalar)
+    elif similarity == COSINE:
+        dist = cosine_distances(h_phi, [anchor_emb[s] for s in cand])
+        W, idx = position_weights(dist, top_k, cand)
+        dbar = cosine_scalar(h_phi, [anchor_emb[s] for s in cand])
+        wbar = softmax_neg(dbar)
+    else:
+        raise ValueError(similarity)
     H = entropy(wbar)
     thr = gamma * math.log(len(cand))
     verdict = NEW_ANCHOR if H > thr else SHAREABLE

@@ -25,6 +25,7 @@ REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY"]
 PLACEHOLDER, PREFIX, COPY = 0, 1, 2
 OFFSET_GIVEN, OFFSET_MEASURE = 0, 1
 SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1
+SIM_L2, SIM_COSINE = 0, 1
 
 
 class PoolConfig(C.Structure):
@@ -32,7 +33,7 @@ class PoolConfig(C.Structure):
                 ("layer_end", C.c_int32), ("num_kv_heads", C.c_int32), ("head_begin", C.c_int32),
                 ("head_end", C.c_int32), ("head_dim", C.c_int32), ("emb_dim", C.c_int32),
                 ("capacity", C.c_int32), ("max_anchor_len", C.c_int32), ("num_consumers", C.c_int32),
-                ("scalar_distance", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
+                ("scalar_distance", C.c_int32), ("similarity", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
 
 
 class KVView(C.Structure):

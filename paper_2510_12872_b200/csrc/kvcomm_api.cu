@@ -184,6 +184,8 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   if (!c->prefix_len || !c->inv_freq) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null prefix_len/inv_freq");
   if (c->scalar_distance != KVCOMM_SCALAR_FROBENIUS && c->scalar_distance != KVCOMM_SCALAR_MEAN_L2)
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "scalar_distance %d", c->scalar_distance);
+  if (c->similarity != KVCOMM_SIM_L2 && c->similarity != KVCOMM_SIM_COSINE)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "similarity %d", c->similarity);
   for (int i = 0; i < c->num_consumers; ++i)
     if (c->prefix_len[i] < 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "prefix_len[%d] < 0", i);
   int ndev = 0;
@@ -219,7 +221,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   p->pf.assign(p->C, nullptr);
   for (int i = 0; i < p->C; ++i) ALLOC(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
   ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
-  ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * p->cap, "partial sums");
+  ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1), "partial sums");
 #undef ALLOC
   cudaError_t e = cudaMemcpy(p->inv_freq_dev, p->inv_freq.data(), sizeof(double) * (p->d / 2),
                              cudaMemcpyHostToDevice);
@@ -566,7 +568,7 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
     n_ints += it.info->n_candidates + it.p->cap;
     blocks += (it.L_phi + kMatchP - 1) / kMatchP;
     L.smem = std::max(L.smem, align_up(size_t(kMatchP) * it.p->De * 2, 16) +
-                                  size_t(kMatchP) * it.info->n_candidates * sizeof(double));
+                                  size_t(kMatchP) * (3 * it.info->n_candidates + 1) * sizeof(double));
   }
   L.hdr.total_blocks = blocks;
   size_t off = align_up(sizeof(MatchHdr), 64);
@@ -608,6 +610,7 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     a.L_phi = it.L_phi;
     a.De = p->De;
     a.scalar_mode = p->cfg.scalar_distance;
+    a.cosine = p->cfg.similarity == KVCOMM_SIM_COSINE;
     a.cand_off = ipos;
     std::memcpy(ints + ipos, it.info->candidates, sizeof(int32_t) * a.n_cand);
     ipos += a.n_cand;

@@ -67,12 +67,13 @@ struct MatchJob {
   int64_t ld_w;
   int32_t* idx;             // [L_phi][top_k] or null
   double* dist_user;        // optional [cap][ld_w]
-  double* partial;          // pool scratch [n_blocks][n_cand]
+  double* partial;          // pool scratch [n_blocks][stride]: stride n_cand (l2) or 2 n_cand + 1 (cosine)
   float* wbar;              // [cap]
   double gamma;
   int32_t n_cand, cap, L_phi, De;
   int32_t top_k;            // effective k (0 = dense, paper default)
   int32_t scalar_mode;      // 0 Frobenius: partial = Σ d², 1 mean-ℓ2: partial = Σ d
+  int32_t cosine;           // 1: d = 1 - cos; partials Σ q·a, Σ a·a (per candidate) and Σ q·q
   int32_t cand_off;         // into MatchHdr ints: candidate slot ids [n_cand]
   int32_t s2c_off;          // into MatchHdr ints: slot -> candidate index or -1 [cap]
   int32_t block_begin, n_blocks;

@@ -3,6 +3,7 @@
 //   d[i,j]  = ‖h_φ[i] - h_ψj[i]‖₂          i < L_φ, ψ_j ∈ 𝒜_φ (first L_φ rows, reading A8)
 //   W[j][i] = softmax_j(-d[i,j])            per position (reading A2); optional top-k (A16)
 //   d̄_j     = sqrt(Σ_i d[i,j]²)            Frobenius (reading A4; or mean_i d[i,j])
+//   (cosine variant, Table A.4: d = 1 - cos per position, d̄ = 1 - <h_φ,h_ψ>_F/(‖h_φ‖_F‖h_ψ‖_F))
 //   w̄ = softmax(-d̄),  H = -Σ w̄ log w̄,  NewAnchor ⇔ H > γ log|𝒜_φ|
 //
 // One launch covers every (sample, pool) job of a request: blocks of P positions of
@@ -62,6 +63,22 @@ __device__ __forceinline__ float sq_diff8(const uint4& qv, const uint4& av) {
   return part;
 }
 
+// q·a, a·a, q·q over 8 bf16 pairs (products of bf16 values are exact in fp32)
+__device__ __forceinline__ void dots8(const uint4& qv, const uint4& av, float& qa, float& aa, float& qq) {
+  const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+  const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const float a0 = bf_lo(aw[t]), a1 = bf_hi(aw[t]), q0 = bf_lo(qw[t]), q1 = bf_hi(qw[t]);
+    qa = fmaf(q0, a0, qa);
+    qa = fmaf(q1, a1, qa);
+    aa = fmaf(a0, a0, aa);
+    aa = fmaf(a1, a1, aa);
+    qq = fmaf(q0, q0, qq);
+    qq = fmaf(q1, q1, qq);
+  }
+}
+
 __device__ __forceinline__ int find_job(const MatchJob* jobs, int n, int b) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -88,6 +105,9 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
   const int n_cand = a.n_cand;
   bf16* q = reinterpret_cast<bf16*>(smem);
   double* sd = reinterpret_cast<double*>(smem + ((size_t(P) * De * 2 + 15) & ~size_t(15)));
+  double* s_qa = sd + P * n_cand;      // cosine only: Σ q·a, Σ a·a per (position, candidate), Σ q·q
+  double* s_aa = s_qa + P * n_cand;
+  double* s_qq = s_aa + P * n_cand;
   const int i0 = lb * P;
   const int np = min(P, a.L_phi - i0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,18 +128,39 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
     const int j = task - p * n_cand;
     const bf16* arow = a.emb + int64_t(cand[j]) * a.slot_stride + int64_t(i0 + p) * De;
     const bf16* qrow = q + size_t(p) * De;
-    double s = 0.0;
-    int e = lane * 8;
-    for (; e + 3 * 256 < De; e += 4 * 256) {  // 4 independent 16-byte loads in flight per lane
-      uint4 av[4];
+    if (!a.cosine) {
+      double s = 0.0;
+      int e = lane * 8;
+      for (; e + 3 * 256 < De; e += 4 * 256) {  // 4 independent 16-byte loads in flight per lane
+        uint4 av[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) av[r] = ldg128_nc(arow + e + r * 256);
+        for (int r = 0; r < 4; ++r) av[r] = ldg128_nc(arow + e + r * 256);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) s += double(sq_diff8(lds128(qrow + e + r * 256), av[r]));
+        for (int r = 0; r < 4; ++r) s += double(sq_diff8(lds128(qrow + e + r * 256), av[r]));
+      }
+      for (; e < De; e += 256) s += double(sq_diff8(lds128(qrow + e), ldg128_nc(arow + e)));
+      s = warp_sum_d(s);
+      if (lane == 0) sd[p * n_cand + j] = sqrt(s);
+    } else {
+      double qa = 0.0, aa = 0.0, qq = 0.0;
+      for (int e = lane * 8; e < De; e += 256) {
+        float fqa = 0.f, faa = 0.f, fqq = 0.f;
+        dots8(lds128(qrow + e), ldg128_nc(arow + e), fqa, faa, fqq);
+        qa += double(fqa);
+        aa += double(faa);
+        qq += double(fqq);
+      }
+      qa = warp_sum_d(qa);
+      aa = warp_sum_d(aa);
+      qq = warp_sum_d(qq);
+      if (lane == 0) {
+        const double den = sqrt(qq * aa);
+        sd[p * n_cand + j] = 1.0 - (den > 0.0 ? qa / den : 0.0);
+        s_qa[p * n_cand + j] = qa;
+        s_aa[p * n_cand + j] = aa;
+        if (j == 0) s_qq[p] = qq;
+      }
     }
-    for (; e < De; e += 256) s += double(sq_diff8(lds128(qrow + e), ldg128_nc(arow + e)));
-    s = warp_sum_d(s);
-    if (lane == 0) sd[p * n_cand + j] = sqrt(s);
   }
   __syncthreads();
 
@@ -185,14 +226,33 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
     }
   }
 
-  // deterministic per-block partial sums (Σ d² for Frobenius, Σ d for mean-ℓ2)
-  for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
-    double s = 0.0;
-    for (int p = 0; p < np; ++p) {
-      const double dv = sd[p * n_cand + j];
-      s += a.scalar_mode == 0 ? dv * dv : dv;
+  // deterministic per-block partial sums (Σ d² for Frobenius, Σ d for mean-ℓ2;
+  // cosine: Σ q·a and Σ a·a per candidate, Σ q·q once)
+  if (!a.cosine) {
+    for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
+      double s = 0.0;
+      for (int p = 0; p < np; ++p) {
+        const double dv = sd[p * n_cand + j];
+        s += a.scalar_mode == 0 ? dv * dv : dv;
+      }
+      a.partial[int64_t(lb) * n_cand + j] = s;
     }
-    a.partial[int64_t(lb) * n_cand + j] = s;
+  } else {
+    const int64_t stride = 2 * n_cand + 1;
+    for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
+      double sqa = 0.0, saa = 0.0;
+      for (int p = 0; p < np; ++p) {
+        sqa += s_qa[p * n_cand + j];
+        saa += s_aa[p * n_cand + j];
+      }
+      a.partial[int64_t(lb) * stride + j] = sqa;
+      a.partial[int64_t(lb) * stride + n_cand + j] = saa;
+    }
+    if (threadIdx.x == 0) {
+      double sqq = 0.0;
+      for (int p = 0; p < np; ++p) sqq += s_qq[p];
+      a.partial[int64_t(lb) * stride + 2 * n_cand] = sqq;
+    }
   }
 }
 
@@ -223,11 +283,29 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // per candidate: lanes stride over the position blocks in a fixed order, then a
   // butterfly (identical in every lane, deterministic)
-  for (int j = warp; j < a.n_cand; j += 32) {
-    double s = 0.0;
-    for (int b = lane; b < a.n_blocks; b += 32) s += a.partial[int64_t(b) * a.n_cand + j];
-    s = warp_sum_d(s);
-    if (lane == 0) dsh[j] = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
+  if (!a.cosine) {
+    for (int j = warp; j < a.n_cand; j += 32) {
+      double s = 0.0;
+      for (int b = lane; b < a.n_blocks; b += 32) s += a.partial[int64_t(b) * a.n_cand + j];
+      s = warp_sum_d(s);
+      if (lane == 0) dsh[j] = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
+    }
+  } else {
+    const int64_t stride = 2 * a.n_cand + 1;
+    double sqq = 0.0;  // every warp sums Σ q·q in the same order (identical values)
+    for (int b = lane; b < a.n_blocks; b += 32) sqq += a.partial[int64_t(b) * stride + 2 * a.n_cand];
+    sqq = warp_sum_d(sqq);
+    for (int j = warp; j < a.n_cand; j += 32) {
+      double sqa = 0.0, saa = 0.0;
+      for (int b = lane; b < a.n_blocks; b += 32) {
+        sqa += a.partial[int64_t(b) * stride + j];
+        saa += a.partial[int64_t(b) * stride + a.n_cand + j];
+      }
+      sqa = warp_sum_d(sqa);
+      saa = warp_sum_d(saa);
+      const double den = sqrt(sqq * saa);
+      if (lane == 0) dsh[j] = 1.0 - (den > 0.0 ? sqa / den : 0.0);
+    }
   }
   __syncthreads();
   const int j = threadIdx.x;

@@ -129,7 +129,7 @@ class AnchorPool:
     def __init__(self, *, num_layers: int, num_kv_heads: int, head_dim: int, emb_dim: int, capacity: int,
                  max_anchor_len: int, prefix_len: Sequence[int], inv_freq, device: int = 0,
                  layer_range: Optional[Tuple[int, int]] = None, head_range: Optional[Tuple[int, int]] = None,
-                 scalar_distance: str = "frobenius"):
+                 scalar_distance: str = "frobenius", similarity: str = "l2"):
         lb, le = layer_range or (0, num_layers)
         hb, he = head_range or (0, num_kv_heads)
         self.Ls, self.Hs, self.d, self.De = le - lb, he - hb, head_dim, emb_dim
@@ -140,7 +140,8 @@ class AnchorPool:
         inv = np.ascontiguousarray(np.asarray(inv_freq, dtype=np.float64))
         cfg = L.PoolConfig(device, num_layers, lb, le, num_kv_heads, hb, he, head_dim, emb_dim, capacity,
                            max_anchor_len, len(self.prefix_len),
-                           {"frobenius": L.SCALAR_FROBENIUS, "mean_l2": L.SCALAR_MEAN_L2}[scalar_distance], pl,
+                           {"frobenius": L.SCALAR_FROBENIUS, "mean_l2": L.SCALAR_MEAN_L2}[scalar_distance],
+                           {"l2": L.SIM_L2, "cosine": L.SIM_COSINE}[similarity], pl,
                            inv.ctypes.data_as(C.POINTER(C.c_double)))
         h = C.c_void_p()
         L.check(L.lib().kvcomm_anchor_pool_create(C.byref(cfg), C.byref(h)))

@@ -34,7 +34,8 @@ def f64(t: torch.Tensor) -> np.ndarray:
 # --------------------------------------------------------------------------- GPU
 
 def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Optional[int] = None,
-            measure: bool = False, consumer: int = 0, device: int = 0, scalar: str = "frobenius") -> Dict:
+            measure: bool = False, consumer: int = 0, device: int = 0, scalar: str = "frobenius",
+            similarity: str = "l2") -> Dict:
     """Insert p's anchors, match p's query, realign its placeholder + prefix for
     `consumer`, copy a synthetic p_(m,0) and check the ledger.  Returns CPU tensors."""
     from paper_2510_12872_b200 import kvcomm as K
@@ -42,7 +43,7 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
     cap = capacity or len(p.anchor_lens)
     pool = K.AnchorPool(num_layers=p.L, num_kv_heads=p.H, head_dim=p.d, emb_dim=p.D_e, capacity=cap,
                         max_anchor_len=max(p.anchor_lens), prefix_len=p.prefix_lens, inv_freq=p.inv_freq,
-                        device=device, scalar_distance=scalar)
+                        device=device, scalar_distance=scalar, similarity=similarity)
     slots = []
     for j, Lj in enumerate(p.anchor_lens):
         offs = []
@@ -85,12 +86,12 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
 # ------------------------------------------------------------------------ oracle
 
 def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: int = 0,
-               slots=None, scalar: str = "frobenius") -> Dict:
+               slots=None, scalar: str = "frobenius", similarity: str = "l2") -> Dict:
     slots = slots or list(range(len(p.anchor_lens)))
     lens = {s: L for s, L in zip(slots, p.anchor_lens)}
     embs = {s: f64(e) for s, e in zip(slots, p.emb_anchor)}
     present = {s: True for s in slots}
-    r = O.predict(f64(p.emb_query), lens, embs, present, gamma, top_k, scalar)
+    r = O.predict(f64(p.emb_query), lens, embs, present, gamma, top_k, scalar, similarity)
     out = {"match": r}
     if not r.candidates:
         return out

@@ -270,3 +270,14 @@ def test_match_many_equals_individual_matches():
         assert torch.equal(m.W, one.W) and torch.equal(m.wbar, one.wbar) and torch.equal(m.dist, one.dist)
     with pytest.raises(K.KVCommError, match="twice"):
         K.match_many([(pools[0], qs[0]), (pools[0], qs[0])])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("top_k", [0, 2])
+def test_cosine_similarity_variant(seed, top_k):
+    """Table A.4's cosine-similarity weighting on the device vs the oracle."""
+    p = synth.make_problem(60 + seed, L=2, H=2, d=64, D_e=256, L_phi=90, anchor_lens=[90, 100, 95, 130, 90],
+                           prefix_lens=[12], target_start=20, pf_base_start=20, inv_freq=synth.llama3_inv_freq(64))
+    gpu = harness.run_gpu(p, gamma=1.0, top_k=top_k, similarity="cosine")
+    ora = harness.run_oracle(p, gamma=1.0, top_k=top_k, similarity="cosine")
+    harness.compare(gpu, ora, p)

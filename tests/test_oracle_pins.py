@@ -480,3 +480,24 @@ def test_online_reuse_non_decreasing_in_gamma_and_capacity_bound():
             assert len(orc.pool.slot_len) <= 4                  # capacity invariant
         rates.append(reused / len(stream))
     assert all(b >= a for a, b in zip(rates, rates[1:])) and rates[-1] > rates[0], rates
+
+
+# ---------------------------------------------------------------- cosine variant (f2)
+
+def test_cosine_variant_matches_library_cosine():
+    # Table A.4 "Cosine Similarity": scipy's cosine distance (1 - cos)
+    import scipy.spatial.distance as ssd
+    h = bf16_values((9, 16))
+    anchors = [bf16_values((9 + e, 16)) for e in (0, 4)]
+    d = O.cosine_distances(h, anchors)
+    for j, a in enumerate(anchors):
+        for i in range(9):
+            assert d[i, j] == pytest.approx(ssd.cosine(h[i], a[i]), abs=1e-14)
+        assert O.cosine_scalar(h, [a])[0] == pytest.approx(ssd.cosine(h.ravel(), a[:9].ravel()), abs=1e-14)
+    # identical -> 0, orthogonal -> 1, opposite -> 2; weights = softmax(cos)
+    e0, e1 = np.eye(2)
+    dd = O.cosine_distances(np.array([e0, e0, e0]), [np.array([e0, e1, -e0])])
+    np.testing.assert_allclose(dd[:, 0], [0.0, 1.0, 2.0], atol=1e-15)
+    r = O.predict(h, {0: 9, 1: 13}, dict(enumerate(anchors)), {0: True, 1: True}, 0.5, similarity=O.COSINE)
+    cos = 1 - O.cosine_distances(h, anchors)
+    np.testing.assert_allclose(r.W, scipy.special.softmax(cos, axis=1), rtol=1e-13)
