@@ -111,7 +111,7 @@ struct kvcomm_pool_s {
   int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * prefix_len[c] * d; }
 };
 
-static constexpr int kMatchP = 4;  // positions per match block
+static constexpr int kMatchP = 2;  // positions per match work item
 
 static void pool_free(kvcomm_pool_s* p) {
   if (!p) return;
@@ -579,7 +579,7 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
   L.hdr.res_off = int64_t(off);
   off = align_up(off + sizeof(MatchResultDev) * nj, 64);
   L.hdr.tie_off = int64_t(off);
-  off = align_up(off + sizeof(int32_t) * nj, 64);
+  off = align_up(off + sizeof(int32_t) * (nj + 1), 64);  // per-job tie counters + the item counter
   L.bytes = off;
   return L;
 }

@@ -23,6 +23,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cfloat>
+#include <algorithm>
 #include "kvcomm_internal.h"
 #include "ptx.cuh"
 
@@ -88,15 +89,16 @@ __device__ __forceinline__ int find_job(const MatchJob* jobs, int n, int b) {
   return lo;
 }
 
-__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t* __restrict__ tab) {
+// One work item = P consecutive positions of one job.
+__device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, const int item) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
   const MatchJob* jobs = reinterpret_cast<const MatchJob*>(tab + hdr->job_off);
   const int32_t* ints = reinterpret_cast<const int32_t*>(tab + hdr->int_off);
   int32_t* ties = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off);
-  const int jb = find_job(jobs, hdr->n_jobs, blockIdx.x);
+  const int jb = find_job(jobs, hdr->n_jobs, item);
   const MatchJob& a = jobs[jb];
   const int P = hdr->P;
-  const int lb = blockIdx.x - a.block_begin;
+  const int lb = item - a.block_begin;
   const int32_t* cand = ints + a.cand_off;
   const int32_t* slot2cand = ints + a.s2c_off;
 
@@ -256,6 +258,24 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
   }
 }
 
+// Persistent blocks pull items from an atomic counter (the table's word after the
+// per-job tie counters, zeroed by the host upload), so the last wave has no tail of
+// idle SMs.  The processing order does not affect any result: every item writes its
+// own W columns and partial sums.
+__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t* __restrict__ tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  int32_t* counter = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off) + hdr->n_jobs;
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= hdr->total_blocks) break;
+    match_item(tab, item);
+    __syncthreads();  // shared memory is reused by the next item
+  }
+}
+
 // Fixed-order tree reduction over 1024 entries in shared memory.
 template <bool kMin>
 __device__ double block_reduce_1024(double* buf, double v) {
@@ -341,7 +361,12 @@ cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_
     if (e != cudaSuccess) return e;
   }
   uint8_t* t = reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev));
-  match_dist_kernel<<<hdr.total_blocks, kMatchThreads, smem, s>>>(t);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_dist_kernel, kMatchThreads, smem);
+  const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));
+  match_dist_kernel<<<grid, kMatchThreads, smem, s>>>(t);
   match_finalize_kernel<<<hdr.n_jobs, 1024, 0, s>>>(t);
   return cudaGetLastError();
 }
