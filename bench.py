@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--offsets", default="bf16", choices=["bf16", "fp8"],
+                    help="anchor offset storage; the headline line is bf16 (fp8 = SURVEY f3, lossy)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -394,7 +396,8 @@ def main():
 
     w = synth.five_agent_workload()
     lr = shard.layer_shard(w.L, rank, world)
-    st = build_five_agent_state(w, seed=args.seed, device=local, gamma=args.gamma, layer_range=lr)
+    st = build_five_agent_state(w, seed=args.seed, device=local, gamma=args.gamma, layer_range=lr,
+                                offset_format=args.offsets)
     req = st.request
     stream = torch.cuda.current_stream()
     Ls = lr[1] - lr[0]
@@ -444,7 +447,10 @@ def main():
         for sg in a.segments:
             uniq_base[sg.base_k.data_ptr()] = sg.base_k.shape[2]
     base_tokens = sum(uniq_base.values())
-    alg_bytes = (res.blended_rows + res.realigned_tokens + base_tokens + 2 * res.copied_tokens) * Ls * row_bytes * 2
+    # an offset row is d bf16 values, or (fp8 pools) d e4m3 codes + one fp32 scale
+    off_row = row_bytes if args.offsets == "bf16" else w.H * (w.d + 4)
+    alg_bytes = (res.blended_rows * off_row + (res.realigned_tokens + base_tokens + 2 * res.copied_tokens) * row_bytes
+                 ) * Ls * 2
 
     if world > 1:
         dist.barrier()
@@ -498,11 +504,12 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.offsets == "bf16" else "bf16 (fp8-e4m3 offsets)",
+            "data": "synthetic",
             "config": {"workload": "llama3-8b-shape (32 layers, 8 KV heads x 128) 5-agent fully-connected, "
                                    "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
                        "realigned_tokens_per_step": total_tokens, "anchors_blended": w.capacity,
-                       "gamma": args.gamma, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
+                       "gamma": args.gamma, "offset_storage": args.offsets, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
                        "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed,
                        **({"test_same_gpu_gloo": True} if same_gpu else {})},
             "roofline": {"kernel": "kvc::realign_kernel (30 segments + 5 p0 copies, one launch)", "bound": "hbm",

@@ -76,6 +76,8 @@ typedef enum {
 
 typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_scalar_distance;
 typedef enum { KVCOMM_SIM_L2 = 0, KVCOMM_SIM_COSINE = 1 } kvcomm_similarity;
+typedef enum { KVCOMM_OFFSET_BF16 = 0, KVCOMM_OFFSET_FP8_E4M3 = 1 } kvcomm_offset_format;
+typedef enum { KVCOMM_PLACE_DEVICE = 0, KVCOMM_PLACE_HOST = 1 } kvcomm_placement;
 /* COPY: rows copied verbatim (no offsets, no rotation; bit-exact), e.g. p_(m,0) of the
  * concatenation (reading A20) riding in the same launch as the realignment. */
 typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1, KVCOMM_COPY = 2 } kvcomm_segment_kind;
@@ -105,6 +107,15 @@ typedef struct {
                               KVCOMM_SIM_L2 (0, paper default): d = ‖h_φ[i] - h_ψ[i]‖₂, w = softmax(-d);
                               KVCOMM_SIM_COSINE (1): d = 1 - cos(h_φ[i], h_ψ[i]), w = softmax(cos);
                               sample level: 1 - <h_φ,h_ψ>_F / (‖h_φ‖_F ‖h_ψ‖_F)            */
+  int32_t offset_format;   /* KVCOMM_OFFSET_BF16 (0, default, exact storage) |
+                              KVCOMM_OFFSET_FP8_E4M3 (1): each stored offset row of d values is
+                              e4m3 codes + one fp32 scale = max|x|/448, code = RNE_sat(x/scale)
+                              (the compression P:1518 names as future work; lossy, ~1.9x fewer
+                              offset bytes; requires head_dim >= 64)                      */
+  int32_t placement;       /* KVCOMM_PLACE_DEVICE (0, default) | KVCOMM_PLACE_HOST (1): the offset
+                              slabs live in pinned, mapped host memory and the same kernels
+                              stream them over the host link (the CPU-offloaded anchors of
+                              A.4.4: pools larger than HBM)                  */
   const int32_t* prefix_len; /* host [num_consumers]: |p_(m,i)| following this placeholder */
   const double* inv_freq;  /* host [head_dim/2]: RoPE inverse frequencies (copied)        */
 } kvcomm_pool_config;
@@ -232,11 +243,17 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_record_access(kvcomm_pool_t pool,
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t pool, int32_t slot,
                                                       kvcomm_slot_info* info);
 /* Device view of a stored offset (which: 0 placeholder, 1 prefix) for inspection:
- * *k, *v point at [Ls][Hs][*ld][d] bf16 rows of the slot. */
+ * *k, *v point at [Ls][Hs][*ld][d] rows of the slot (bf16, or e4m3 codes in fp8 pools). */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t pool, int32_t slot,
                                                         int32_t consumer, int32_t which,
                                                         const void** k, const void** v,
                                                         int64_t* ld);
+
+/* fp8 pools: device view of the per-row fp32 scales of a stored offset, [Ls][Hs][*ld]. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_scales(kvcomm_pool_t pool, int32_t slot,
+                                                          int32_t consumer, int32_t which,
+                                                          const float** sk, const float** sv,
+                                                          int64_t* ld);
 
 /* ---- a1-a3: anchor matching (Eq. 5, Eq. 6 weights) -------------------------- */
 /* query_emb: device bf16 [L_phi][D_e] (the sample's token embeddings h_φ).

@@ -26,6 +26,8 @@ PLACEHOLDER, PREFIX, COPY = 0, 1, 2
 OFFSET_GIVEN, OFFSET_MEASURE = 0, 1
 SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1
 SIM_L2, SIM_COSINE = 0, 1
+OFFSET_BF16, OFFSET_FP8_E4M3 = 0, 1
+PLACE_DEVICE, PLACE_HOST = 0, 1
 
 
 class PoolConfig(C.Structure):
@@ -33,7 +35,8 @@ class PoolConfig(C.Structure):
                 ("layer_end", C.c_int32), ("num_kv_heads", C.c_int32), ("head_begin", C.c_int32),
                 ("head_end", C.c_int32), ("head_dim", C.c_int32), ("emb_dim", C.c_int32),
                 ("capacity", C.c_int32), ("max_anchor_len", C.c_int32), ("num_consumers", C.c_int32),
-                ("scalar_distance", C.c_int32), ("similarity", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
+                ("scalar_distance", C.c_int32), ("similarity", C.c_int32),
+                ("offset_format", C.c_int32), ("placement", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
 
 
 class KVView(C.Structure):
@@ -110,6 +113,9 @@ _SIGS = {
     "kvcomm_anchor_pool_offset_view": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                                  C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                                  C.POINTER(C.c_int64)]),
+    "kvcomm_anchor_pool_offset_scales": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                                   C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                                   C.POINTER(C.c_int64)]),
     "kvcomm_match_anchors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_int32,
                                        C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(MatchInfo), C.c_void_p]),

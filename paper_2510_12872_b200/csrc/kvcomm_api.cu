@@ -93,8 +93,14 @@ struct kvcomm_pool_s {
   std::vector<double> inv_freq;
   // device slabs
   bf16* emb = nullptr;                 // [cap][maxlen][De]
-  bf16* ph = nullptr;                  // [C][cap][2][Ls][Hs][maxlen][d]
+  bool fp8 = false;                    // offset_format == KVCOMM_OFFSET_FP8_E4M3
+  bf16* ph = nullptr;                  // [C][cap][2][Ls][Hs][ph_ld][d]  (bf16 pools)
   std::vector<bf16*> pf;               // per consumer: [cap][2][Ls][Hs][P_c][d]
+  uint8_t* ph8 = nullptr;              // fp8 pools: e4m3 codes, same element indexing
+  std::vector<uint8_t*> pf8;
+  float* ph_sc = nullptr;              // fp8 pools: one fp32 scale per row (element index / d)
+  std::vector<float*> pf_sc;
+  std::vector<void*> host_allocs;      // offset slabs placed in pinned host memory (f4)
   double* inv_freq_dev = nullptr;
   // match scratch
   double* d_partial = nullptr;         // [n_blocks_max][cap]
@@ -107,8 +113,13 @@ struct kvcomm_pool_s {
   int64_t ph_slot_stride() const { return int64_t(2) * Ls * Hs * ph_ld * d + slot_pad; }
   int64_t ph_plane_stride() const { return int64_t(Ls) * Hs * ph_ld * d; }
   bf16* ph_base(int c) const { return ph + int64_t(c) * cap * ph_slot_stride(); }
-  int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * prefix_len[c] * d; }
-  int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * prefix_len[c] * d; }
+  uint8_t* ph8_base(int c) const { return ph8 + int64_t(c) * cap * ph_slot_stride(); }
+  float* ph_sc_base(int c) const { return ph_sc + int64_t(c) * cap * ph_slot_stride() / d; }
+  // prefix rows per (layer, head) block; fp8 pools round to 4 so per-row scale tiles are
+  // 16-byte aligned for TMA
+  int64_t pf_ld(int c) const { return fp8 ? (prefix_len[c] + 3) / 4 * 4 : prefix_len[c]; }
+  int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * pf_ld(c) * d; }
+  int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * pf_ld(c) * d; }
 };
 
 static constexpr int kMatchP = 2;  // positions per match work item
@@ -116,18 +127,30 @@ static constexpr int kMatchP = 2;  // positions per match work item
 static void pool_free(kvcomm_pool_s* p) {
   if (!p) return;
   DeviceGuard g(p->cfg.device);
+  auto release = [p](void* x) {
+    if (!x) return;
+    if (std::find(p->host_allocs.begin(), p->host_allocs.end(), x) != p->host_allocs.end()) cudaFreeHost(x);
+    else cudaFree(x);
+  };
   cudaFree(p->emb);
-  cudaFree(p->ph);
-  for (auto* x : p->pf) cudaFree(x);
+  release(p->ph);
+  for (auto* x : p->pf) release(x);
+  release(p->ph8);
+  for (auto* x : p->pf8) release(x);
+  release(p->ph_sc);
+  for (auto* x : p->pf_sc) release(x);
   cudaFree(p->inv_freq_dev);
   cudaFree(p->d_partial);
   delete p;
 }
 
 template <typename T>
-static kvcomm_status dev_alloc(kvcomm_pool_s* p, T** out, int64_t count, const char* what) {
+static kvcomm_status dev_alloc(kvcomm_pool_s* p, T** out, int64_t count, const char* what, bool host = false) {
   const size_t bytes = size_t(std::max<int64_t>(count, 1)) * sizeof(T);
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(out), bytes);
+  // host placement (f4): pinned, mapped host memory; with UVA the pointer is valid on the device
+  cudaError_t e = host ? cudaHostAlloc(reinterpret_cast<void**>(out), bytes, cudaHostAllocMapped)
+                       : cudaMalloc(reinterpret_cast<void**>(out), bytes);
+  if (e == cudaSuccess && host) p->host_allocs.push_back(*out);
   if (e != cudaSuccess) {
     cudaGetLastError();
     *out = nullptr;
@@ -186,6 +209,12 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "scalar_distance %d", c->scalar_distance);
   if (c->similarity != KVCOMM_SIM_L2 && c->similarity != KVCOMM_SIM_COSINE)
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "similarity %d", c->similarity);
+  if (c->offset_format != KVCOMM_OFFSET_BF16 && c->offset_format != KVCOMM_OFFSET_FP8_E4M3)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "offset_format %d", c->offset_format);
+  if (c->placement != KVCOMM_PLACE_DEVICE && c->placement != KVCOMM_PLACE_HOST)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "placement %d", c->placement);
+  if (c->offset_format == KVCOMM_OFFSET_FP8_E4M3 && c->head_dim < 64)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "fp8 offsets need head_dim >= 64 (got %d)", c->head_dim);
   for (int i = 0; i < c->num_consumers; ++i)
     if (c->prefix_len[i] < 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "prefix_len[%d] < 0", i);
   int ndev = 0;
@@ -200,6 +229,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   p->cfg = *c;
   p->Ls = Ls; p->Hs = Hs; p->d = c->head_dim; p->De = c->emb_dim; p->cap = c->capacity;
   p->maxlen = c->max_anchor_len; p->C = c->num_consumers;
+  p->fp8 = c->offset_format == KVCOMM_OFFSET_FP8_E4M3;
   {
     // Tuning knobs: KVCOMM_PH_PAD_ROWS pads each (layer, head) block of a
     // stored offset, KVCOMM_SLOT_PAD_ROWS adds rows between anchor slots.
@@ -207,6 +237,10 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     const char* e2 = getenv("KVCOMM_SLOT_PAD_ROWS");
     p->ph_ld = p->maxlen + (e1 ? atoi(e1) : 0);
     p->slot_pad = int64_t(e2 ? atoi(e2) : 0) * p->d;
+    if (c->offset_format == KVCOMM_OFFSET_FP8_E4M3) {  // 16-byte aligned per-row scale tiles
+      p->ph_ld = (p->ph_ld + 3) / 4 * 4;
+      p->slot_pad = (p->slot_pad / p->d + 3) / 4 * 4 * p->d;
+    }
   }
   p->prefix_len.assign(c->prefix_len, c->prefix_len + c->num_consumers);
   p->inv_freq.assign(c->inv_freq, c->inv_freq + c->head_dim / 2);
@@ -216,13 +250,28 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   kvcomm_status st;
 #define ALLOC(ptr, n, what)                          \
   if ((st = dev_alloc(p, &(ptr), (n), what)) != KVCOMM_OK) { pool_free(p); return st; }
+  const bool host = c->placement == KVCOMM_PLACE_HOST;
+#define ALLOC_OFF(ptr, n, what)                      \
+  if ((st = dev_alloc(p, &(ptr), (n), what, host)) != KVCOMM_OK) { pool_free(p); return st; }
   ALLOC(p->emb, int64_t(p->cap) * p->maxlen * p->De, "embedding slab");
-  ALLOC(p->ph, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab");
-  p->pf.assign(p->C, nullptr);
-  for (int i = 0; i < p->C; ++i) ALLOC(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
+  if (!p->fp8) {
+    ALLOC_OFF(p->ph, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab");
+    p->pf.assign(p->C, nullptr);
+    for (int i = 0; i < p->C; ++i) ALLOC_OFF(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
+  } else {
+    ALLOC_OFF(p->ph8, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab (e4m3)");
+    ALLOC_OFF(p->ph_sc, int64_t(p->C) * p->cap * p->ph_slot_stride() / p->d, "placeholder offset scales");
+    p->pf8.assign(p->C, nullptr);
+    p->pf_sc.assign(p->C, nullptr);
+    for (int i = 0; i < p->C; ++i) {
+      ALLOC_OFF(p->pf8[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab (e4m3)");
+      ALLOC_OFF(p->pf_sc[i], int64_t(p->cap) * p->pf_slot_stride(i) / p->d, "prefix offset scales");
+    }
+  }
   ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
   ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1), "partial sums");
 #undef ALLOC
+#undef ALLOC_OFF
   cudaError_t e = cudaMemcpy(p->inv_freq_dev, p->inv_freq.data(), sizeof(double) * (p->d / 2),
                              cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -261,54 +310,98 @@ static kvcomm_status check_view(const kvcomm_kv_view& v, int rows, const char* w
 static int64_t ld_of(const kvcomm_kv_view& v, int rows) { return v.ld ? v.ld : rows; }
 
 // Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
+// Where the offsets of (slot, consumer) live: bf16 rows, or e4m3 codes + row scales.
+struct OffDst {
+  bf16 *k = nullptr, *v = nullptr;
+  uint8_t *k8 = nullptr, *v8 = nullptr;
+  float *sk = nullptr, *sv = nullptr;
+  int64_t ld = 0;
+};
+
+static OffDst offsets_of(const kvcomm_pool_s* p, int c, int slot, bool prefix) {
+  OffDst o;
+  const int64_t e0 = prefix ? int64_t(slot) * p->pf_slot_stride(c)
+                            : int64_t(c) * p->cap * p->ph_slot_stride() + int64_t(slot) * p->ph_slot_stride();
+  const int64_t plane = prefix ? p->pf_plane_stride(c) : p->ph_plane_stride();
+  o.ld = prefix ? p->pf_ld(c) : p->ph_ld;
+  if (!p->fp8) {
+    bf16* b = prefix ? p->pf[c] : p->ph;
+    o.k = b + e0;
+    o.v = o.k + plane;
+  } else {
+    uint8_t* b = prefix ? p->pf8[c] : p->ph8;
+    float* sc = prefix ? p->pf_sc[c] : p->ph_sc;
+    o.k8 = b + e0;
+    o.v8 = o.k8 + plane;
+    o.sk = sc + e0 / p->d;
+    o.sv = o.sk + plane / p->d;
+  }
+  return o;
+}
+
+static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int rows, const OffDst& d,
+                               cudaStream_t s) {
+  const int64_t ld = ld_of(src, rows);
+  const bf16* k = static_cast<const bf16*>(src.k);
+  const bf16* v = static_cast<const bf16*>(src.v);
+  if (!p->fp8) {
+    KV_CUDA(launch_copy_rows(k, ld, d.k, d.ld, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_copy_rows(v, ld, d.v, d.ld, p->Ls, p->Hs, rows, p->d, s));
+  } else {
+    KV_CUDA(launch_quantize_rows(k, ld, d.k8, d.sk, d.ld, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_quantize_rows(v, ld, d.v8, d.sv, d.ld, p->Ls, p->Hs, rows, p->d, s));
+  }
+  g_launches += 2;
+  return KVCOMM_OK;
+}
+
+static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, const kvcomm_kv_view& base,
+                                  int rows, const OffDst& d, cudaStream_t s) {
+  const int delta = -(real.start - base.start);
+  const auto* kr = static_cast<const bf16*>(real.k);
+  const auto* vr = static_cast<const bf16*>(real.v);
+  const auto* kb = static_cast<const bf16*>(base.k);
+  const auto* vb = static_cast<const bf16*>(base.v);
+  if (!p->fp8)
+    KV_CUDA(launch_measure(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d, delta,
+                           p->inv_freq_dev, d.k, d.v, d.ld, s));
+  else
+    KV_CUDA(launch_measure_fp8(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d,
+                               delta, p->inv_freq_dev, d.k8, d.v8, d.sk, d.sv, d.ld, s));
+  g_launches += 1;
+  return KVCOMM_OK;
+}
+
+// Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
 static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const kvcomm_offset_desc& o,
                                    cudaStream_t s, uint64_t* ph_set, uint64_t* pf_set) {
   const int c = o.consumer;
   if (c < 0 || c >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d outside [0,%d)", c, p->C);
   const int P = p->prefix_len[c];
-  bf16* phk = p->ph_base(c) + int64_t(slot) * p->ph_slot_stride();
-  bf16* phv = phk + p->ph_plane_stride();
-  bf16* pfk = p->pf[c] + int64_t(slot) * p->pf_slot_stride(c);
-  bf16* pfv = pfk + p->pf_plane_stride(c);
+  const OffDst ph = offsets_of(p, c, slot, false), pf = offsets_of(p, c, slot, true);
   if (P == 0) *pf_set |= 1ull << c;  // an empty prefix segment needs no offsets
   if (o.mode == KVCOMM_OFFSET_GIVEN) {
     if (o.ph_delta.k) {
       KV_TRY(check_view(o.ph_delta, L_psi, "ph_delta"));
-      const int64_t ld = ld_of(o.ph_delta, L_psi);
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.k), ld, phk, p->ph_ld, p->Ls, p->Hs, L_psi,
-                               p->d, s));
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.ph_delta.v), ld, phv, p->ph_ld, p->Ls, p->Hs, L_psi,
-                               p->d, s));
-      g_launches += 2;
+      KV_TRY(put_given(p, o.ph_delta, L_psi, ph, s));
       *ph_set |= 1ull << c;
     }
     if (o.pf_delta.k) {
       KV_TRY(check_view(o.pf_delta, P, "pf_delta"));
-      const int64_t ld = ld_of(o.pf_delta, P);
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.pf_delta.k), ld, pfk, P, p->Ls, p->Hs, P, p->d, s));
-      KV_CUDA(launch_copy_rows(static_cast<const bf16*>(o.pf_delta.v), ld, pfv, P, p->Ls, p->Hs, P, p->d, s));
-      g_launches += 2;
+      KV_TRY(put_given(p, o.pf_delta, P, pf, s));
       *pf_set |= 1ull << c;
     }
   } else if (o.mode == KVCOMM_OFFSET_MEASURE) {
     if (o.ph_real.k) {
       KV_TRY(check_view(o.ph_real, L_psi, "ph_real"));
       KV_TRY(check_view(o.ph_base, L_psi, "ph_base"));
-      KV_CUDA(launch_measure(static_cast<const bf16*>(o.ph_real.k), static_cast<const bf16*>(o.ph_real.v),
-                             ld_of(o.ph_real, L_psi), static_cast<const bf16*>(o.ph_base.k),
-                             static_cast<const bf16*>(o.ph_base.v), ld_of(o.ph_base, L_psi), L_psi, p->Ls, p->Hs,
-                             p->d, -(o.ph_real.start - o.ph_base.start), p->inv_freq_dev, phk, phv, p->ph_ld, s));
-      g_launches += 1;
+      KV_TRY(put_measured(p, o.ph_real, o.ph_base, L_psi, ph, s));
       *ph_set |= 1ull << c;
     }
     if (o.pf_real.k) {
       KV_TRY(check_view(o.pf_real, P, "pf_real"));
       KV_TRY(check_view(o.pf_base, P, "pf_base"));
-      KV_CUDA(launch_measure(static_cast<const bf16*>(o.pf_real.k), static_cast<const bf16*>(o.pf_real.v),
-                             ld_of(o.pf_real, P), static_cast<const bf16*>(o.pf_base.k),
-                             static_cast<const bf16*>(o.pf_base.v), ld_of(o.pf_base, P), P, p->Ls, p->Hs, p->d,
-                             -(o.pf_real.start - o.pf_base.start), p->inv_freq_dev, pfk, pfv, P, s));
-      g_launches += 1;
+      KV_TRY(put_measured(p, o.pf_real, o.pf_base, P, pf, s));
       *pf_set |= 1ull << c;
     }
   } else {
@@ -424,17 +517,24 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t p, int32_t
   if (!p || !k || !v || !ld) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
   if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d", slot);
   if (consumer < 0 || consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
-  if (which == 0) {
-    const bf16* b = p->ph_base(consumer) + int64_t(slot) * p->ph_slot_stride();
-    *k = b;
-    *v = b + p->ph_plane_stride();
-    *ld = p->ph_ld;
-  } else {
-    const bf16* b = p->pf[consumer] + int64_t(slot) * p->pf_slot_stride(consumer);
-    *k = b;
-    *v = b + p->pf_plane_stride(consumer);
-    *ld = p->prefix_len[consumer];
-  }
+  const OffDst o = offsets_of(p, consumer, slot, which != 0);
+  *k = p->fp8 ? static_cast<const void*>(o.k8) : static_cast<const void*>(o.k);
+  *v = p->fp8 ? static_cast<const void*>(o.v8) : static_cast<const void*>(o.v);
+  *ld = o.ld;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_scales(kvcomm_pool_t p, int32_t slot, int32_t consumer,
+                                                          int32_t which, const float** sk, const float** sv,
+                                                          int64_t* ld) {
+  if (!p || !sk || !sv || !ld) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (!p->fp8) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "pool stores bf16 offsets (no scales)");
+  if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d", slot);
+  if (consumer < 0 || consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
+  const OffDst o = offsets_of(p, consumer, slot, which != 0);
+  *sk = o.sk;
+  *sv = o.sv;
+  *ld = o.ld;
   return ok();
 }
 
@@ -889,10 +989,12 @@ static HostSeg host_segment(const kvcomm_realign_desc& g) {
   x.delta = g.target_start - g.base_start;
   x.n_cand = g.n_candidates;
   h.cand = g.candidates;
+  x.fp8 = p->fp8 ? 1 : 0;
   if (g.kind == KVCOMM_PLACEHOLDER) {
     x.w = g.weights;
     x.ld_w = g.ld_w;
-    x.off = p->ph_base(g.consumer);
+    x.off = p->fp8 ? reinterpret_cast<const bf16*>(p->ph8_base(g.consumer)) : p->ph_base(g.consumer);
+    x.scales = p->fp8 ? p->ph_sc_base(g.consumer) : nullptr;
     x.slot_stride = p->ph_slot_stride();
     x.plane_stride = p->ph_plane_stride();
     x.off_ld = p->ph_ld;
@@ -900,11 +1002,14 @@ static HostSeg host_segment(const kvcomm_realign_desc& g) {
     h.prefix = true;
     x.w_by_slot = 0;
     x.wbar = g.weights;
-    x.off = p->pf[g.consumer];
+    x.off = p->fp8 ? reinterpret_cast<const bf16*>(p->pf8[g.consumer]) : p->pf[g.consumer];
+    x.scales = p->fp8 ? p->pf_sc[g.consumer] : nullptr;
     x.slot_stride = p->pf_slot_stride(g.consumer);
     x.plane_stride = p->pf_plane_stride(g.consumer);
-    x.off_ld = p->prefix_len[g.consumer];
+    x.off_ld = p->pf_ld(g.consumer);
   }
+  x.sc_slot_stride = x.slot_stride / p->d;
+  x.sc_plane_stride = x.plane_stride / p->d;
   return h;
 }
 

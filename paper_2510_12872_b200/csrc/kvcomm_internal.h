@@ -37,6 +37,10 @@ struct SegDev {
   int32_t gate_off;     //   branch of Alg. 1); indices into Table::cand area, n_gate = 0: always
   int32_t group_size;   // segments sharing this base tile (consecutive in the table; units interleave
                         //   members so the shared base tile is read from HBM once and hit in L2 after)
+  int32_t fp8;          // offsets stored as e4m3 codes (off is then a byte pointer, element index = byte)
+  int32_t _pad2;
+  const float* scales;  // fp8: one fp32 scale per offset row, index = element index / d
+  int64_t sc_slot_stride, sc_plane_stride;  // fp8: slot_stride / d, plane_stride / d (rows)
 };
 
 struct MatchResultDev {
@@ -93,6 +97,13 @@ cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t
                              int rows, int d, cudaStream_t s);
 // Contiguous copy of n bf16 elements (multiple of 8).
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
+// fp8 (e4m3 + per-row fp32 scale) offset storage: quantise bf16 rows / measure into codes.
+cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, float* scales, int64_t dst_ld,
+                                 int Ls, int Hs, int rows, int d, cudaStream_t s);
+cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
+                               const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
+                               const double* inv_freq, uint8_t* dk, uint8_t* dv, float* sk, float* sv,
+                               int64_t dst_ld, cudaStream_t s);
 // Offset measurement (insert path, step a0).
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                            const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,

@@ -125,3 +125,185 @@ cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_
 }
 
 }  // namespace kvc
+
+// ---------------------------------------------------------------------------
+// fp8 (e4m3) offset storage ("substantial headroom for
+// compression"): each token row of d offsets is stored as d e4m3 codes plus one
+// fp32 scale = max|x| / 448 (1 if the row is all zero); code = RNE_sat(x / scale)
+// with IEEE division, so the codes are reproducible bit for bit.
+// ---------------------------------------------------------------------------
+#include <cuda_fp8.h>
+
+namespace kvc {
+
+constexpr float kE4M3Max = 448.f;
+
+// max over the vph consecutive lanes that hold one row (groups are aligned and whole)
+__device__ __forceinline__ float group_max(float v, int vph) {
+  const int lane = threadIdx.x & 31;
+  const unsigned base = unsigned(lane & ~(vph - 1));
+  const unsigned gmask = (vph == 32 ? 0xffffffffu : (((1u << vph) - 1u) << base));
+  for (int o = vph >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(gmask, v, o));
+  return v;
+}
+
+// 16 floats of one item (8 of the first half, 8 of the second) -> codes into row pointers
+__device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1, float scale, uint8_t* o0,
+                                               uint8_t* o1) {
+  uint32_t w[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float* x = h ? x1 : x0;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float2 f = make_float2(__fdiv_rn(x[2 * t], scale), __fdiv_rn(x[2 * t + 1], scale));
+      const uint32_t p = uint32_t(__nv_cvt_float2_to_fp8x2(f, __NV_SATFINITE, __NV_E4M3));  // .x in low byte
+      if (t < 2) lo |= p << (16 * t); else hi |= p << (16 * (t - 2));
+    }
+    w[2 * h] = lo;
+    w[2 * h + 1] = hi;
+  }
+  *reinterpret_cast<uint2*>(o0) = make_uint2(w[0], w[1]);
+  *reinterpret_cast<uint2*>(o1) = make_uint2(w[2], w[3]);
+}
+
+__device__ __forceinline__ float row_scale(float amax) { return amax > 0.f ? __fdiv_rn(amax, kE4M3Max) : 1.f; }
+
+// bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool)
+__global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
+                                     float* __restrict__ scales, int64_t dst_ld, int rows, int d, int64_t total) {
+  const int vph = d / 16;
+  const int half = d / 2;
+  for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < total; base += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t x = base + threadIdx.x;
+    const bool active = x < total;
+    // whole row groups are in or out together (total % vph == 0, blockDim % 32 == 0)
+    if (!active && (base + (threadIdx.x & ~31)) >= total) continue;
+    float f0[8], f1[8];
+    int64_t r = 0;
+    int v = 0;
+    if (active) {
+      v = int(x % vph);
+      r = x / vph;
+      const int i = int(r % rows);
+      const int64_t lh = r / rows;
+      const bf16* s = src + (lh * src_ld + i) * d + v * 8;
+      const uint4 a = ldg128_nc(s), b = ldg128_nc(s + half);
+      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        f0[2 * t] = bf_lo(av[t]); f0[2 * t + 1] = bf_hi(av[t]);
+        f1[2 * t] = bf_lo(bv[t]); f1[2 * t + 1] = bf_hi(bv[t]);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) f0[t] = f1[t] = 0.f;
+    }
+    float m = 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) m = fmaxf(m, fmaxf(fabsf(f0[t]), fabsf(f1[t])));
+    m = group_max(m, vph);
+    if (!active) continue;
+    const float sc = row_scale(m);
+    const int i = int(r % rows);
+    const int64_t lh = r / rows;
+    const int64_t orow = lh * dst_ld + i;
+    store_fp8_item(f0, f1, sc, dst + orow * d + v * 8, dst + orow * d + half + v * 8);
+    if (v == 0) scales[orow] = sc;
+  }
+}
+
+// Offset measurement straight into an fp8 pool (fp32 Δ, one quantisation).
+__global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
+                                   const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
+                                   int rows, int d, int delta, const double* __restrict__ inv_freq,
+                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, float* __restrict__ sk,
+                                   float* __restrict__ sv, int64_t dst_ld, int64_t total) {
+  __shared__ float2 cs[128];
+  const int half = d / 2;
+  for (int f = threadIdx.x; f < half; f += blockDim.x) {
+    double sn, cn;
+    sincos(double(delta) * inv_freq[f], &sn, &cn);
+    cs[f] = make_float2(float(cn), float(sn));
+  }
+  __syncthreads();
+  const int vph = d / 16;
+  for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < total; base += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t x = base + threadIdx.x;
+    const bool active = x < total;
+    if (!active && (base + (threadIdx.x & ~31)) >= total) continue;
+    float k0[8], k1[8], v0[8], v1[8];
+    int v = 0;
+    int64_t r = 0;
+    if (active) {
+      v = int(x % vph);
+      r = x / vph;
+      const int i = int(r % rows);
+      const int64_t lh = r / rows;
+      const int64_t ro = (lh * real_ld + i) * d + v * 8;
+      const int64_t bo = (lh * base_ld + i) * d + v * 8;
+      const uint4 ka = ldg128_nc(kr + ro), kc = ldg128_nc(kr + ro + half);
+      const uint4 ba = ldg128_nc(kb + bo), bc = ldg128_nc(kb + bo + half);
+      const uint4 va = ldg128_nc(vr + ro), vc = ldg128_nc(vr + ro + half);
+      const uint4 wa = ldg128_nc(vb + bo), wc = ldg128_nc(vb + bo + half);
+      const uint32_t K0[4] = {ka.x, ka.y, ka.z, ka.w}, K1[4] = {kc.x, kc.y, kc.z, kc.w};
+      const uint32_t B0[4] = {ba.x, ba.y, ba.z, ba.w}, B1[4] = {bc.x, bc.y, bc.z, bc.w};
+      const uint32_t V0[4] = {va.x, va.y, va.z, va.w}, V1[4] = {vc.x, vc.y, vc.z, vc.w};
+      const uint32_t W0[4] = {wa.x, wa.y, wa.z, wa.w}, W1[4] = {wc.x, wc.y, wc.z, wc.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x0 = (e & 1) ? bf_hi(K0[e / 2]) : bf_lo(K0[e / 2]);
+        const float x1 = (e & 1) ? bf_hi(K1[e / 2]) : bf_lo(K1[e / 2]);
+        const float2 c = cs[v * 8 + e];
+        k0[e] = (x0 * c.x - x1 * c.y) - ((e & 1) ? bf_hi(B0[e / 2]) : bf_lo(B0[e / 2]));
+        k1[e] = (x1 * c.x + x0 * c.y) - ((e & 1) ? bf_hi(B1[e / 2]) : bf_lo(B1[e / 2]));
+        v0[e] = ((e & 1) ? bf_hi(V0[e / 2]) : bf_lo(V0[e / 2])) - ((e & 1) ? bf_hi(W0[e / 2]) : bf_lo(W0[e / 2]));
+        v1[e] = ((e & 1) ? bf_hi(V1[e / 2]) : bf_lo(V1[e / 2])) - ((e & 1) ? bf_hi(W1[e / 2]) : bf_lo(W1[e / 2]));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) k0[e] = k1[e] = v0[e] = v1[e] = 0.f;
+    }
+    float mk = 0.f, mv = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      mk = fmaxf(mk, fmaxf(fabsf(k0[e]), fabsf(k1[e])));
+      mv = fmaxf(mv, fmaxf(fabsf(v0[e]), fabsf(v1[e])));
+    }
+    mk = group_max(mk, vph);
+    mv = group_max(mv, vph);
+    if (!active) continue;
+    const int i = int(r % rows);
+    const int64_t lh = r / rows;
+    const int64_t orow = lh * dst_ld + i;
+    const float sck = row_scale(mk), scv = row_scale(mv);
+    store_fp8_item(k0, k1, sck, dk + orow * d + v * 8, dk + orow * d + half + v * 8);
+    store_fp8_item(v0, v1, scv, dv + orow * d + v * 8, dv + orow * d + half + v * 8);
+    if (v == 0) {
+      sk[orow] = sck;
+      sv[orow] = scv;
+    }
+  }
+}
+
+cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, float* scales, int64_t dst_ld,
+                                 int Ls, int Hs, int rows, int d, cudaStream_t s) {
+  const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
+  if (total == 0) return cudaSuccess;
+  quantize_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, src_ld, dst, scales, dst_ld, rows, d, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
+                               const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
+                               const double* inv_freq, uint8_t* dk, uint8_t* dv, float* sk, float* sv,
+                               int64_t dst_ld, cudaStream_t s) {
+  const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
+  if (total == 0) return cudaSuccess;
+  measure_fp8_kernel<<<grid_for(total, 256), 256, 0, s>>>(k_real, v_real, real_ld, k_base, v_base, base_ld, rows, d,
+                                                          delta, inv_freq, dk, dv, sk, sv, dst_ld, total);
+  return cudaGetLastError();
+}
+
+}  // namespace kvc

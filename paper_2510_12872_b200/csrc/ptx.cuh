@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace kvc {
 
@@ -71,6 +72,23 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "r"(smem_u32(p)));
   return r;
+}
+
+__device__ __forceinline__ uint2 lds64(const void* p) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(smem_u32(p)));
+  return r;
+}
+
+// four e4m3 codes (bytes 0..3 of u, element order) -> floats, exact
+__device__ __forceinline__ void e4m3x4_to_float(uint32_t u, float* f) {
+  uint32_t h01, h23;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h01) : "h"(static_cast<unsigned short>(u & 0xffffu)));
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h23) : "h"(static_cast<unsigned short>(u >> 16)));
+  const __half2 a = *reinterpret_cast<const __half2*>(&h01);
+  const __half2 b = *reinterpret_cast<const __half2*>(&h23);
+  const float2 fa = __half22float2(a), fb = __half22float2(b);
+  f[0] = fa.x; f[1] = fa.y; f[2] = fb.x; f[3] = fb.y;
 }
 
 __device__ __forceinline__ void stg128_cs(void* p, uint4 v) {

@@ -30,14 +30,9 @@
 
 namespace kvc {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kNStage = 11;
 constexpr int kItems = kStageBytes / 32;                         // 512 items of 32 B per stage
-constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);  // 2
 constexpr int kConsumerBar = 1;                                  // named barrier id (consumers only)
-
-static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
 
 constexpr size_t realign_smem_bytes() {
   return size_t(kNStage) * (kStageBytes + kStageWBytes) + 2 * kNStage * sizeof(uint64_t);
@@ -118,7 +113,13 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
 
 // variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
 // of the TMA bulk store; bit1 = skip output stores (bandwidth probe only, wrong results).
-__global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __restrict__ tab, int variant) {
+// kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread, twice the
+// issue slots for the e4m3 decode of fp8 pools) + one producer warp.
+template <int kConsumerWarps>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
+    realign_kernel(const uint8_t* __restrict__ tab, int variant) {
+  constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);
+  static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
   const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
   const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr.cand_off);
@@ -165,6 +166,40 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
         const uint32_t bytes = uint32_t(nrows) * row_bytes;
         const uint32_t wbytes = (uint32_t(nrows) * 4u + 15u) & ~15u;
         const int64_t lh = int64_t(un.l) * Hs + un.h;
+        if (g.fp8) {
+          // e4m3 anchor tiles are half a stage: two anchors per stage, each with its
+          // weight slice and its per-row scale slice in the stage's side area
+          const uint32_t cbytes = uint32_t(nrows) * d;
+          // per-unit parts of the addresses (rows of the tile; codes are 1 byte per element)
+          const int64_t unit_rows = int64_t(un.p) * g.sc_plane_stride + lh * g.off_ld + i0;
+          const uint8_t* code0 = reinterpret_cast<const uint8_t*>(g.off) + unit_rows * d;
+          const float* scale0 = g.scales + unit_rows;
+          const float* w0 = g.w + i0;
+          for (int c = 0; c < g.n_cand; c += 2) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            const int na = min(2, g.n_cand - c);
+            uint8_t* dst = sdata + size_t(stage) * kStageBytes;
+            float* swst = sw + size_t(stage) * (kStageWBytes / 4);
+            mbar_arrive_expect_tx(&full[stage], uint32_t(na) * (cbytes + 2 * wbytes));
+            for (int a = 0; a < na; ++a) {
+              const int slot = cand[g.cand_off + c + a];
+              bulk_g2s(dst + a * (kStageBytes / 2), code0 + int64_t(slot) * g.slot_stride, cbytes, &full[stage],
+                       pol_stream);
+              bulk_g2s(swst + a * rpt, w0 + int64_t(g.w_by_slot ? slot : c + a) * g.ld_w, wbytes, &full[stage],
+                       pol_stream);
+              bulk_g2s(swst + (2 + a) * rpt, scale0 + int64_t(slot) * g.sc_slot_stride, wbytes, &full[stage],
+                       pol_stream);
+            }
+            if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+          }
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(sdata + size_t(stage) * kStageBytes, src, bytes, &full[stage],
+                   g.group_size > 1 ? pol_shared : pol_stream);
+          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+          continue;
+        }
         for (int c = 0; c <= g.n_cand; ++c) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* dst = sdata + size_t(stage) * kStageBytes;
@@ -213,7 +248,38 @@ __global__ void __launch_bounds__(kThreads, 1) realign_kernel(const uint8_t* __r
       for (int e = 0; e < 16; ++e) acc[q][e] = 0.f;
 
     const int n_cand = g.n_cand;
-    for (int c = 0; c < n_cand; ++c) {
+    if (g.fp8) {
+      for (int c = 0; c < n_cand; c += 2) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
+        const float* swst = sw + size_t(stage) * (kStageWBytes / 4);
+        const int na = min(2, n_cand - c);
+        for (int a = 0; a < na; ++a) {
+          const uint8_t* ab = buf + a * (kStageBytes / 2);
+#pragma unroll
+          for (int q = 0; q < kItemsPerThread; ++q) {
+            const float w = swst[a * rpt + irow[q]] * swst[(2 + a) * rpt + irow[q]];  // weight x row scale
+            const uint2 lo = lds64(ab + irow[q] * d + ivec[q] * 8);
+            const uint2 hi = lds64(ab + irow[q] * d + d / 2 + ivec[q] * 8);
+            const uint32_t lw[2] = {lo.x, lo.y}, hw[2] = {hi.x, hi.y};
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              float f[4];
+              e4m3x4_to_float(lw[t], f);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[q][4 * t + e] = fmaf(w, f[e], acc[q][4 * t + e]);
+              e4m3x4_to_float(hw[t], f);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[q][8 + 4 * t + e] = fmaf(w, f[e], acc[q][8 + 4 * t + e]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+      }
+    }
+    for (int c = 0; c < (g.fp8 ? 0 : n_cand); ++c) {
       mbar_wait(&full[stage], phase);
       const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
       const float* wv = sw + size_t(stage) * (kStageWBytes / 4);
@@ -330,24 +396,32 @@ int realign_grid_size(int device) {
 
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
-  static int variant = -1;
+  static int variant = -1, cw = 16;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(realign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(realign_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(realign_smem_bytes()));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(realign_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(realign_smem_bytes()));
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
   if (variant < 0) {
     const char* v = getenv("KVCOMM_REALIGN_VARIANT");
     variant = v ? atoi(v) : 0;
+    const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
+    if (c && atoi(c) == 8) cw = 8;
   }
   realign_prep_kernel<<<hdr.n_seg, 128, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
-  realign_kernel<<<int(g), kThreads, realign_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(table_dev),
-                                                                   variant);
+  const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);
+  if (cw == 8)
+    realign_kernel<8><<<int(g), 9 * 32, realign_smem_bytes(), s>>>(t, variant);
+  else
+    realign_kernel<16><<<int(g), 17 * 32, realign_smem_bytes(), s>>>(t, variant);
   return cudaGetLastError();
 }
 

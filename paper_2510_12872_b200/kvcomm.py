@@ -129,19 +129,23 @@ class AnchorPool:
     def __init__(self, *, num_layers: int, num_kv_heads: int, head_dim: int, emb_dim: int, capacity: int,
                  max_anchor_len: int, prefix_len: Sequence[int], inv_freq, device: int = 0,
                  layer_range: Optional[Tuple[int, int]] = None, head_range: Optional[Tuple[int, int]] = None,
-                 scalar_distance: str = "frobenius", similarity: str = "l2"):
+                 scalar_distance: str = "frobenius", similarity: str = "l2", offset_format: str = "bf16",
+                 placement: str = "device"):
         lb, le = layer_range or (0, num_layers)
         hb, he = head_range or (0, num_kv_heads)
         self.Ls, self.Hs, self.d, self.De = le - lb, he - hb, head_dim, emb_dim
         self.capacity, self.max_anchor_len = capacity, max_anchor_len
         self.prefix_len = [int(x) for x in prefix_len]
         self.device = torch.device("cuda", device)
+        self.offset_format = offset_format
         pl = (C.c_int32 * len(self.prefix_len))(*self.prefix_len)
         inv = np.ascontiguousarray(np.asarray(inv_freq, dtype=np.float64))
         cfg = L.PoolConfig(device, num_layers, lb, le, num_kv_heads, hb, he, head_dim, emb_dim, capacity,
                            max_anchor_len, len(self.prefix_len),
                            {"frobenius": L.SCALAR_FROBENIUS, "mean_l2": L.SCALAR_MEAN_L2}[scalar_distance],
-                           {"l2": L.SIM_L2, "cosine": L.SIM_COSINE}[similarity], pl,
+                           {"l2": L.SIM_L2, "cosine": L.SIM_COSINE}[similarity],
+                           {"bf16": L.OFFSET_BF16, "fp8": L.OFFSET_FP8_E4M3}[offset_format],
+                           {"device": L.PLACE_DEVICE, "host": L.PLACE_HOST}[placement], pl,
                            inv.ctypes.data_as(C.POINTER(C.c_double)))
         h = C.c_void_p()
         L.check(L.lib().kvcomm_anchor_pool_create(C.byref(cfg), C.byref(h)))
@@ -208,10 +212,24 @@ class AnchorPool:
         rows = ld.value if rows is None else rows
         out = []
         for p in (k.value, v.value):
-            flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "<i2"),
-                                   device=self.device)
-            out.append(flat.view(torch.bfloat16).view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
+            if self.offset_format == "fp8":   # raw e4m3 codes
+                flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "|u1"),
+                                       device=self.device)
+                out.append(flat.view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
+            else:
+                flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "<i2"),
+                                       device=self.device)
+                out.append(flat.view(torch.bfloat16).view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
         return tuple(out)
+
+    def offset_scales(self, slot: int, consumer: int, which: str = "ph", rows: Optional[int] = None):
+        """fp8 pools: per-row fp32 scales (sK, sV) as [Ls, Hs, rows] views of pool memory."""
+        k, v, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
+        L.check(L.lib().kvcomm_anchor_pool_offset_scales(self.handle, slot, consumer, 0 if which == "ph" else 1,
+                                                         C.byref(k), C.byref(v), C.byref(ld)))
+        rows = ld.value if rows is None else rows
+        return tuple(torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value,), "<f4"), device=self.device)
+                     .view(self.Ls, self.Hs, ld.value)[:, :, :rows] for p in (k.value, v.value))
 
     # -- a1-a3 ---------------------------------------------------------------
     def _match_request(self, query_emb: torch.Tensor, consumer: int, gamma: float, top_k: int, want_dist: bool,

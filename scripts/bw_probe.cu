@@ -150,6 +150,47 @@ __global__ void tma_mix_store(const uint8_t* src, int64_t nchunks, int chunk, in
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// TMA read of `chunk`-byte tiles where every tile also pulls `nsmall` 256-byte side
+// slices (one from an L2-resident table, the rest from DRAM), as the fp8 realign does.
+__global__ void tma_read_side(const uint8_t* src, int64_t nchunks, int chunk, int nstage, const uint8_t* side,
+                              int64_t side_bytes, int nsmall) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int sstride = chunk + 1024;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(nstage) * sstride);
+  uint64_t* empty = full + nstage;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (threadIdx.x >= 32) {
+    if (threadIdx.x == 32) {
+      int st = 0; uint32_t ph = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_expect(&full[st], chunk + 256 * nsmall);
+        uint8_t* d = sm + size_t(st) * sstride;
+        bulk(d, src + c * chunk, chunk, &full[st], pol);
+        for (int k = 0; k < nsmall; ++k) {
+          const int64_t off = (k == 0) ? (c % 64) * 256 : ((c * 7919 + k * 104729) % (side_bytes / 256)) * 256;
+          bulk(d + chunk + 256 * k, side + off, 256, &full[st], pol);
+        }
+        if (++st == nstage) { st = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  int st = 0; uint32_t ph = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    mbar_wait(&full[st], ph);
+    __syncwarp();
+    if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+    if (++st == nstage) { st = 0; ph ^= 1; }
+  }
+}
+
 template <int U>
 __global__ void ldg_read(const uint4* src, int64_t n, uint32_t* out) {
   uint32_t acc = 0;
@@ -245,6 +286,20 @@ int main() {
         snprintf(name, sizeof(name), "mix %d:1 %s", we, names[mode]);
         timeit([&] { tma_mix_store<<<sms, 64, smem>>>(src, n, chunk, nst, dst, we, mode); },
                double(bytes) * (1.0 + 1.0 / we), name);
+      }
+    }
+  }
+  {
+    for (int chunk : {8192, 16384}) {
+      for (int nsmall : {0, 1, 2, 4}) {
+        const int nst = 11;
+        size_t smem = size_t(nst) * (chunk + 1024) + 2 * nst * 8;
+        cudaFuncSetAttribute(tma_read_side, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int64_t n = bytes / chunk;
+        char name[96];
+        snprintf(name, sizeof(name), "tma_read chunk=%d + %d x 256B side", chunk, nsmall);
+        timeit([&] { tma_read_side<<<sms, 64, smem>>>(src, n, chunk, nst, dst, bytes / 2, nsmall); },
+               double(bytes) * (1.0 + 256.0 * nsmall / chunk), name);
       }
     }
   }

@@ -113,7 +113,7 @@ class FiveAgentState:
 
 def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: int = 0, gamma: float = 0.3,
                            layer_range: Optional[Tuple[int, int]] = None, anchor_extra: int = 0,
-                           top_k: int = 0) -> FiveAgentState:
+                           top_k: int = 0, offset_format: str = "bf16") -> FiveAgentState:
     from paper_2510_12872_b200 import kvcomm as K
     from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
     w = w or five_agent_workload()
@@ -126,7 +126,7 @@ def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: 
     for name, ps in w.pools.items():
         pool = K.AnchorPool(num_layers=w.L, num_kv_heads=w.H, head_dim=w.d, emb_dim=w.D_e, capacity=w.capacity,
                             max_anchor_len=ps.L_phi + anchor_extra, prefix_len=ps.prefix_len, inv_freq=inv,
-                            device=device, layer_range=lr)
+                            device=device, layer_range=lr, offset_format=offset_format)
         for slot in range(w.capacity):
             emb = vocab[inp.anchor_ids(name, slot)]
             offs = [K.OffsetGiven(c, inp.offset(name, slot, c, "ph", 0), inp.offset(name, slot, c, "ph", 1),

@@ -35,7 +35,7 @@ def f64(t: torch.Tensor) -> np.ndarray:
 
 def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Optional[int] = None,
             measure: bool = False, consumer: int = 0, device: int = 0, scalar: str = "frobenius",
-            similarity: str = "l2") -> Dict:
+            similarity: str = "l2", offset_format: str = "bf16", placement: str = "device") -> Dict:
     """Insert p's anchors, match p's query, realign its placeholder + prefix for
     `consumer`, copy a synthetic p_(m,0) and check the ledger.  Returns CPU tensors."""
     from paper_2510_12872_b200 import kvcomm as K
@@ -43,7 +43,8 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
     cap = capacity or len(p.anchor_lens)
     pool = K.AnchorPool(num_layers=p.L, num_kv_heads=p.H, head_dim=p.d, emb_dim=p.D_e, capacity=cap,
                         max_anchor_len=max(p.anchor_lens), prefix_len=p.prefix_lens, inv_freq=p.inv_freq,
-                        device=device, scalar_distance=scalar, similarity=similarity)
+                        device=device, scalar_distance=scalar, similarity=similarity,
+                        offset_format=offset_format, placement=placement)
     slots = []
     for j, Lj in enumerate(p.anchor_lens):
         offs = []
@@ -86,7 +87,10 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
 # ------------------------------------------------------------------------ oracle
 
 def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: int = 0,
-               slots=None, scalar: str = "frobenius", similarity: str = "l2") -> Dict:
+               slots=None, scalar: str = "frobenius", similarity: str = "l2", fp8: bool = False) -> Dict:
+    """fp8=True: the offsets the blend sees are the e4m3-quantised ones (oracle's own
+    quantiser, O.quantize_rows_fp8), as stored by an fp8 pool."""
+    store = (lambda x: O.dequantize_rows_fp8(*O.quantize_rows_fp8(x))) if fp8 else (lambda x: x)
     slots = slots or list(range(len(p.anchor_lens)))
     lens = {s: L for s, L in zip(slots, p.anchor_lens)}
     embs = {s: f64(e) for s, e in zip(slots, p.emb_anchor)}
@@ -98,15 +102,15 @@ def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: i
     c = consumer
     j_of = {s: j for j, s in enumerate(slots)}
     js = [j_of[s] for s in r.candidates]
-    dk = [f64(p.dk_ph[c][j]) for j in js]
-    dv = [f64(p.dv_ph[c][j]) for j in js]
+    dk = [store(f64(p.dk_ph[c][j])) for j in js]
+    dv = [store(f64(p.dv_ph[c][j])) for j in js]
     ph = O.realign_segment(r.W, f64(p.base_k), f64(p.base_v), dk, dv, 0, p.target_start, p.inv_freq)
     ph["absk"] = O.blend_placeholder(r.W, [np.abs(x) for x in dk])
     ph["absv"] = O.blend_placeholder(r.W, [np.abs(x) for x in dv])
     out["ph"] = ph
     if p.prefix_lens[c] > 0:
-        pk = [f64(p.dk_pf[c][j]) for j in js]
-        pv = [f64(p.dv_pf[c][j]) for j in js]
+        pk = [store(f64(p.dk_pf[c][j])) for j in js]
+        pv = [store(f64(p.dv_pf[c][j])) for j in js]
         pf = O.realign_segment(r.wbar, f64(p.pf_base_k[c]), f64(p.pf_base_v[c]), pk, pv, p.pf_base_start,
                                p.pf_target_start[c], p.inv_freq, kind="prefix")
         pf["absk"] = O.blend_prefix(r.wbar, [np.abs(x) for x in pk])

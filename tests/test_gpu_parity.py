@@ -281,3 +281,67 @@ def test_cosine_similarity_variant(seed, top_k):
     gpu = harness.run_gpu(p, gamma=1.0, top_k=top_k, similarity="cosine")
     ora = harness.run_oracle(p, gamma=1.0, top_k=top_k, similarity="cosine")
     harness.compare(gpu, ora, p)
+
+
+def _fp8_codes(q: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(q.astype(np.float32)).to(torch.float8_e4m3fn).view(torch.uint8)
+
+
+@pytest.mark.parametrize("d,L_phi,P", [(128, 150, 37), (64, 200, 5), (256, 70, 32)])
+def test_fp8_offsets_codes_and_realign(d, L_phi, P):
+    """f3: e4m3 offset storage.  GIVEN offsets are quantised on the device to the same
+    codes and scales as the oracle's quantiser (bit-exact), and the realignment from
+    the fp8 pool matches the oracle run on the dequantised offsets."""
+    p = synth.make_problem(31, L=2, H=2, d=d, D_e=64, L_phi=L_phi, anchor_lens=[L_phi, L_phi + 9, L_phi + 40],
+                           prefix_lens=[P], target_start=25, pf_base_start=25, inv_freq=synth.llama3_inv_freq(d))
+    gpu = harness.run_gpu(p, gamma=1.0, offset_format="fp8")
+    pool = gpu["pool"]
+    for j, s in enumerate(gpu["slots"]):
+        for which, src in (("ph", p.dk_ph[0][j]), ("pf", p.dk_pf[0][j])):
+            rows = src.shape[2]
+            gk, _ = pool.offset_view(s, 0, which, rows=rows)
+            sk, _ = pool.offset_scales(s, 0, which, rows=rows)
+            q, sc = O.quantize_rows_fp8(harness.f64(src))
+            assert torch.equal(gk.cpu(), _fp8_codes(q)), (j, which)
+            assert torch.equal(sk.cpu(), torch.from_numpy(sc)), (j, which)
+    ora = harness.run_oracle(p, gamma=1.0, fp8=True)
+    harness.compare(gpu, ora, p)
+
+
+def test_fp8_measure_insert_close_to_oracle():
+    dev = torch.device("cuda", 0)
+    L_, H, d, T, P = 2, 2, 128, 70, 8
+    inv = synth.llama3_inv_freq(d)
+    g = synth.make_gen(22)
+    t = lambda n: synth.randn_bf16((L_, H, n, d), g)
+    kr, vr, kb, vb, pkr, pvr, pkb, pvb = t(T), t(T), t(T), t(T), t(P), t(P), t(P), t(P)
+    pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=64, capacity=1, max_anchor_len=T,
+                        prefix_len=[P], inv_freq=inv, offset_format="fp8")
+    off = K.OffsetMeasure(0, ph_real=(kr.to(dev), vr.to(dev), 300), ph_base=(kb.to(dev), vb.to(dev), 0),
+                          pf_real=(pkr.to(dev), pvr.to(dev), 300 + T), pf_base=(pkb.to(dev), pvb.to(dev), 40))
+    slot, _ = pool.insert(synth.randn_bf16((T, 64), g).to(dev), [off])
+    torch.cuda.synchronize()
+    f64 = harness.f64
+    for which, (a, b, c_, d_, sr, sb, n) in {"ph": (kr, vr, kb, vb, 300, 0, T),
+                                             "pf": (pkr, pvr, pkb, pvb, 300 + T, 40, P)}.items():
+        codes = pool.offset_view(slot, 0, which, rows=n)
+        scales = pool.offset_scales(slot, 0, which, rows=n)
+        odk, odv = O.measure_offset(f64(a), f64(b), sr, f64(c_), f64(d_), sb, inv)
+        for code, sc, ref in zip(codes, scales, (odk, odv)):
+            got = code.cpu().view(torch.float8_e4m3fn).double().numpy() * f64(sc)[..., None]
+            amax = np.max(np.abs(ref), axis=-1, keepdims=True)
+            # one e4m3 step at the value's magnitude (fp32 vs fp64 measurement can flip a rounding)
+            assert np.all(np.abs(got - ref) <= 2.0 ** -3 * np.abs(ref) + 2.0 ** -9 * amax / 448 + 1e-6), which
+
+
+@pytest.mark.parametrize("fmt", ["bf16", "fp8"])
+def test_host_resident_pool(fmt):
+    """f4: offset slabs in pinned host memory (A.4.4 CPU offload) streamed
+    by the same kernels; results identical to the device-resident pool."""
+    p = synth.make_problem(8, L=2, H=2, d=128, D_e=64, L_phi=100, anchor_lens=[100, 120, 140], prefix_lens=[16],
+                           target_start=30, pf_base_start=30, inv_freq=synth.llama3_inv_freq(128))
+    dev = harness.run_gpu(p, gamma=1.0, offset_format=fmt)
+    host = harness.run_gpu(p, gamma=1.0, offset_format=fmt, placement="host")
+    assert torch.equal(dev["dst_k"], host["dst_k"]) and torch.equal(dev["dst_v"], host["dst_v"])
+    ora = harness.run_oracle(p, gamma=1.0, fp8=(fmt == "fp8"))
+    harness.compare(host, ora, p)

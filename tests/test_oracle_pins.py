@@ -501,3 +501,31 @@ def test_cosine_variant_matches_library_cosine():
     r = O.predict(h, {0: 9, 1: 13}, dict(enumerate(anchors)), {0: True, 1: True}, 0.5, similarity=O.COSINE)
     cos = 1 - O.cosine_distances(h, anchors)
     np.testing.assert_allclose(r.W, scipy.special.softmax(cos, axis=1), rtol=1e-13)
+
+
+# ---------------------------------------------------------------- fp8 storage (f3)
+
+def test_e4m3_round_matches_torch_float8():
+    # torch's float32 -> float8_e4m3fn cast is RNE (library routine); in range it must agree
+    x = (rng.standard_normal(200000) * np.exp(rng.uniform(-12, 5, 200000))).astype(np.float32)
+    x = x[np.abs(x) <= 448]
+    ref = torch.from_numpy(x).to(torch.float8_e4m3fn).to(torch.float64).numpy()
+    np.testing.assert_array_equal(O.e4m3_round(x.astype(np.float64)), ref)
+    # grid facts: 448 is the max, 2^-9 the smallest subnormal, 1 + 2^-4 is a tie -> 1
+    assert O.e4m3_round(1000.0) == 448.0 and O.e4m3_round(-1e9) == -448.0
+    assert O.e4m3_round(2.0 ** -9 * 0.6) == 2.0 ** -9
+    assert O.e4m3_round(1 + 2.0 ** -4) == 1.0 and O.e4m3_round(1 + 3 * 2.0 ** -4) == 1.25
+
+
+def test_fp8_row_quantisation_bounds():
+    x = bf16_values((3, 4, 50, 128), 0.15)
+    q, s = O.quantize_rows_fp8(x)
+    assert np.all(np.abs(q) <= 448) and np.all(np.max(np.abs(q), axis=-1) == 448)   # amax maps to 448
+    xh = O.dequantize_rows_fp8(q, s)
+    # relative error <= 2^-4 for normal codes, absolute <= 2^-10 * scale below the normal range
+    err = np.abs(xh - x)
+    bound = np.maximum(np.abs(x) * 2.0 ** -4, 2.0 ** -10 * s[..., None])
+    assert np.all(err <= bound * (1 + 1e-6))
+    z = np.zeros((2, 16))
+    q, s = O.quantize_rows_fp8(z)
+    assert np.all(q == 0) and np.all(s == 1.0)
