@@ -242,18 +242,21 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_record_access(kvcomm_pool_t pool,
                                                           const int32_t* slots, int32_t n);
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t pool, int32_t slot,
                                                       kvcomm_slot_info* info);
-/* Device view of a stored offset (which: 0 placeholder, 1 prefix) for inspection:
- * *k, *v point at [Ls][Hs][*ld][d] rows of the slot (bf16, or e4m3 codes in fp8 pools). */
+/* Device view of a stored offset (which: 0 placeholder, 1 prefix) of a bf16 pool:
+ * *k, *v point at [Ls][Hs][*ld][d] bf16 rows of the slot (INVALID_ARGUMENT for fp8). */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t pool, int32_t slot,
                                                         int32_t consumer, int32_t which,
                                                         const void** k, const void** v,
                                                         int64_t* ld);
 
-/* fp8 pools: device view of the per-row fp32 scales of a stored offset, [Ls][Hs][*ld]. */
-KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_scales(kvcomm_pool_t pool, int32_t slot,
-                                                          int32_t consumer, int32_t which,
-                                                          const float** sk, const float** sv,
-                                                          int64_t* ld);
+/* Copy a stored offset of (slot, consumer) out for inspection (which: 0 placeholder,
+ * 1 prefix), first `rows` rows, stream-ordered: bf16 pools write bf16 [Ls][Hs][rows][d]
+ * to k_out/v_out; fp8 pools write the e4m3 codes (uint8 [Ls][Hs][rows][d]) and the row
+ * scales (fp32 [Ls][Hs][rows]) to sk_out/sv_out. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_read_offsets(kvcomm_pool_t pool, int32_t slot, int32_t consumer,
+                                                         int32_t which, int32_t rows, void* k_out,
+                                                         void* v_out, float* sk_out, float* sv_out,
+                                                         void* stream);
 
 /* ---- a1-a3: anchor matching (Eq. 5, Eq. 6 weights) -------------------------- */
 /* query_emb: device bf16 [L_phi][D_e] (the sample's token embeddings h_φ).

@@ -113,9 +113,8 @@ _SIGS = {
     "kvcomm_anchor_pool_offset_view": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                                  C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                                  C.POINTER(C.c_int64)]),
-    "kvcomm_anchor_pool_offset_scales": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                                                   C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
-                                                   C.POINTER(C.c_int64)]),
+    "kvcomm_anchor_pool_read_offsets": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvcomm_match_anchors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_int32,
                                        C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(MatchInfo), C.c_void_p]),

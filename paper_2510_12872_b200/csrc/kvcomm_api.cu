@@ -96,10 +96,8 @@ struct kvcomm_pool_s {
   bool fp8 = false;                    // offset_format == KVCOMM_OFFSET_FP8_E4M3
   bf16* ph = nullptr;                  // [C][cap][2][Ls][Hs][ph_ld][d]  (bf16 pools)
   std::vector<bf16*> pf;               // per consumer: [cap][2][Ls][Hs][P_c][d]
-  uint8_t* ph8 = nullptr;              // fp8 pools: e4m3 codes, same element indexing
-  std::vector<uint8_t*> pf8;
-  float* ph_sc = nullptr;              // fp8 pools: one fp32 scale per row (element index / d)
-  std::vector<float*> pf_sc;
+  uint8_t* ph8 = nullptr;              // fp8 pools: blocked e4m3 codes + row scales
+  std::vector<uint8_t*> pf8;           //   [C][cap][2][Ls][Hs][blocks][rpt*d codes | rpt fp32 scales]
   std::vector<void*> host_allocs;      // offset slabs placed in pinned host memory (f4)
   double* inv_freq_dev = nullptr;
   // match scratch
@@ -113,11 +111,13 @@ struct kvcomm_pool_s {
   int64_t ph_slot_stride() const { return int64_t(2) * Ls * Hs * ph_ld * d + slot_pad; }
   int64_t ph_plane_stride() const { return int64_t(Ls) * Hs * ph_ld * d; }
   bf16* ph_base(int c) const { return ph + int64_t(c) * cap * ph_slot_stride(); }
-  uint8_t* ph8_base(int c) const { return ph8 + int64_t(c) * cap * ph_slot_stride(); }
-  float* ph_sc_base(int c) const { return ph_sc + int64_t(c) * cap * ph_slot_stride() / d; }
-  // prefix rows per (layer, head) block; fp8 pools round to 4 so per-row scale tiles are
-  // 16-byte aligned for TMA
-  int64_t pf_ld(int c) const { return fp8 ? (prefix_len[c] + 3) / 4 * 4 : prefix_len[c]; }
+  int64_t pf_ld(int c) const { return prefix_len[c]; }
+  // fp8 blocked geometry (bytes): a (layer, head) region holds ceil(ld / rpt) blocks
+  int64_t f8_lh(int64_t ld) const { return (ld + rows_per_tile(d) - 1) / rows_per_tile(d) * fp8_block_bytes(d); }
+  int64_t f8_ph_plane() const { return int64_t(Ls) * Hs * f8_lh(ph_ld); }
+  int64_t f8_ph_slot() const { return 2 * f8_ph_plane(); }
+  int64_t f8_pf_plane(int c) const { return int64_t(Ls) * Hs * f8_lh(prefix_len[c]); }
+  int64_t f8_pf_slot(int c) const { return 2 * f8_pf_plane(c); }
   int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * pf_ld(c) * d; }
   int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * pf_ld(c) * d; }
 };
@@ -137,8 +137,6 @@ static void pool_free(kvcomm_pool_s* p) {
   for (auto* x : p->pf) release(x);
   release(p->ph8);
   for (auto* x : p->pf8) release(x);
-  release(p->ph_sc);
-  for (auto* x : p->pf_sc) release(x);
   cudaFree(p->inv_freq_dev);
   cudaFree(p->d_partial);
   delete p;
@@ -237,10 +235,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     const char* e2 = getenv("KVCOMM_SLOT_PAD_ROWS");
     p->ph_ld = p->maxlen + (e1 ? atoi(e1) : 0);
     p->slot_pad = int64_t(e2 ? atoi(e2) : 0) * p->d;
-    if (c->offset_format == KVCOMM_OFFSET_FP8_E4M3) {  // 16-byte aligned per-row scale tiles
-      p->ph_ld = (p->ph_ld + 3) / 4 * 4;
-      p->slot_pad = (p->slot_pad / p->d + 3) / 4 * 4 * p->d;
-    }
+
   }
   p->prefix_len.assign(c->prefix_len, c->prefix_len + c->num_consumers);
   p->inv_freq.assign(c->inv_freq, c->inv_freq + c->head_dim / 2);
@@ -259,14 +254,17 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     p->pf.assign(p->C, nullptr);
     for (int i = 0; i < p->C; ++i) ALLOC_OFF(p->pf[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab");
   } else {
-    ALLOC_OFF(p->ph8, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab (e4m3)");
-    ALLOC_OFF(p->ph_sc, int64_t(p->C) * p->cap * p->ph_slot_stride() / p->d, "placeholder offset scales");
+    ALLOC_OFF(p->ph8, int64_t(p->C) * p->cap * p->f8_ph_slot(), "placeholder offset slab (e4m3)");
     p->pf8.assign(p->C, nullptr);
-    p->pf_sc.assign(p->C, nullptr);
-    for (int i = 0; i < p->C; ++i) {
-      ALLOC_OFF(p->pf8[i], int64_t(p->cap) * p->pf_slot_stride(i), "prefix offset slab (e4m3)");
-      ALLOC_OFF(p->pf_sc[i], int64_t(p->cap) * p->pf_slot_stride(i) / p->d, "prefix offset scales");
-    }
+    for (int i = 0; i < p->C; ++i)
+      ALLOC_OFF(p->pf8[i], int64_t(p->cap) * p->f8_pf_slot(i), "prefix offset slab (e4m3)");
+    // blocks are read whole (tail rows past a segment's length included): keep them finite
+    auto zero = [&](uint8_t* x, int64_t n) {
+      if (host) std::memset(x, 0, size_t(n));
+      else cudaMemset(x, 0, size_t(n));
+    };
+    zero(p->ph8, int64_t(p->C) * p->cap * p->f8_ph_slot());
+    for (int i = 0; i < p->C; ++i) zero(p->pf8[i], int64_t(p->cap) * p->f8_pf_slot(i));
   }
   ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
   ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1), "partial sums");
@@ -310,31 +308,31 @@ static kvcomm_status check_view(const kvcomm_kv_view& v, int rows, const char* w
 static int64_t ld_of(const kvcomm_kv_view& v, int rows) { return v.ld ? v.ld : rows; }
 
 // Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
-// Where the offsets of (slot, consumer) live: bf16 rows, or e4m3 codes + row scales.
+// Where the offsets of (slot, consumer) live: bf16 rows, or blocked e4m3 codes + row scales.
 struct OffDst {
-  bf16 *k = nullptr, *v = nullptr;
-  uint8_t *k8 = nullptr, *v8 = nullptr;
-  float *sk = nullptr, *sv = nullptr;
-  int64_t ld = 0;
+  bf16 *k = nullptr, *v = nullptr;       // bf16: [Ls][Hs][ld][d]
+  uint8_t *k8 = nullptr, *v8 = nullptr;  // fp8: (layer, head) regions of lh_bytes
+  int64_t ld = 0, lh_bytes = 0;
 };
 
 static OffDst offsets_of(const kvcomm_pool_s* p, int c, int slot, bool prefix) {
   OffDst o;
-  const int64_t e0 = prefix ? int64_t(slot) * p->pf_slot_stride(c)
-                            : int64_t(c) * p->cap * p->ph_slot_stride() + int64_t(slot) * p->ph_slot_stride();
-  const int64_t plane = prefix ? p->pf_plane_stride(c) : p->ph_plane_stride();
   o.ld = prefix ? p->pf_ld(c) : p->ph_ld;
   if (!p->fp8) {
+    const int64_t e0 = prefix ? int64_t(slot) * p->pf_slot_stride(c)
+                              : int64_t(c) * p->cap * p->ph_slot_stride() + int64_t(slot) * p->ph_slot_stride();
+    const int64_t plane = prefix ? p->pf_plane_stride(c) : p->ph_plane_stride();
     bf16* b = prefix ? p->pf[c] : p->ph;
     o.k = b + e0;
     o.v = o.k + plane;
   } else {
+    const int64_t b0 = prefix ? int64_t(slot) * p->f8_pf_slot(c)
+                              : (int64_t(c) * p->cap + slot) * p->f8_ph_slot();
+    const int64_t plane = prefix ? p->f8_pf_plane(c) : p->f8_ph_plane();
     uint8_t* b = prefix ? p->pf8[c] : p->ph8;
-    float* sc = prefix ? p->pf_sc[c] : p->ph_sc;
-    o.k8 = b + e0;
+    o.k8 = b + b0;
     o.v8 = o.k8 + plane;
-    o.sk = sc + e0 / p->d;
-    o.sv = o.sk + plane / p->d;
+    o.lh_bytes = p->f8_lh(o.ld);
   }
   return o;
 }
@@ -348,8 +346,8 @@ static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int 
     KV_CUDA(launch_copy_rows(k, ld, d.k, d.ld, p->Ls, p->Hs, rows, p->d, s));
     KV_CUDA(launch_copy_rows(v, ld, d.v, d.ld, p->Ls, p->Hs, rows, p->d, s));
   } else {
-    KV_CUDA(launch_quantize_rows(k, ld, d.k8, d.sk, d.ld, p->Ls, p->Hs, rows, p->d, s));
-    KV_CUDA(launch_quantize_rows(v, ld, d.v8, d.sv, d.ld, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_quantize_rows(k, ld, d.k8, d.lh_bytes, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_quantize_rows(v, ld, d.v8, d.lh_bytes, p->Ls, p->Hs, rows, p->d, s));
   }
   g_launches += 2;
   return KVCOMM_OK;
@@ -367,7 +365,7 @@ static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, 
                            p->inv_freq_dev, d.k, d.v, d.ld, s));
   else
     KV_CUDA(launch_measure_fp8(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d,
-                               delta, p->inv_freq_dev, d.k8, d.v8, d.sk, d.sv, d.ld, s));
+                               delta, p->inv_freq_dev, d.k8, d.v8, d.lh_bytes, s));
   g_launches += 1;
   return KVCOMM_OK;
 }
@@ -515,26 +513,37 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_view(kvcomm_pool_t p, int32_t
                                                         int32_t which, const void** k, const void** v,
                                                         int64_t* ld) {
   if (!p || !k || !v || !ld) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (p->fp8) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "fp8 pools store blocked codes: use read_offsets");
   if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d", slot);
   if (consumer < 0 || consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
   const OffDst o = offsets_of(p, consumer, slot, which != 0);
-  *k = p->fp8 ? static_cast<const void*>(o.k8) : static_cast<const void*>(o.k);
-  *v = p->fp8 ? static_cast<const void*>(o.v8) : static_cast<const void*>(o.v);
+  *k = o.k;
+  *v = o.v;
   *ld = o.ld;
   return ok();
 }
 
-KVCOMM_API kvcomm_status kvcomm_anchor_pool_offset_scales(kvcomm_pool_t p, int32_t slot, int32_t consumer,
-                                                          int32_t which, const float** sk, const float** sv,
-                                                          int64_t* ld) {
-  if (!p || !sk || !sv || !ld) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
-  if (!p->fp8) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "pool stores bf16 offsets (no scales)");
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_read_offsets(kvcomm_pool_t p, int32_t slot, int32_t consumer,
+                                                         int32_t which, int32_t rows, void* k_out, void* v_out,
+                                                         float* sk_out, float* sv_out, void* stream) {
+  if (!p || !k_out || !v_out) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
+  if (p->fp8 && (!sk_out || !sv_out)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "fp8 pools need scale outputs");
   if (slot < 0 || slot >= p->cap) return fail(KVCOMM_ERR_NOT_FOUND, "slot %d", slot);
   if (consumer < 0 || consumer >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d", consumer);
   const OffDst o = offsets_of(p, consumer, slot, which != 0);
-  *sk = o.sk;
-  *sv = o.sv;
-  *ld = o.ld;
+  if (rows < 0 || rows > o.ld) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "rows %d outside [0,%lld]", rows,
+                                           (long long)o.ld);
+  DeviceGuard guard(p->cfg.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::shared_lock<std::shared_mutex> lk(p->mu);
+  if (!p->fp8) {
+    KV_CUDA(launch_copy_rows(o.k, o.ld, static_cast<bf16*>(k_out), rows, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_copy_rows(o.v, o.ld, static_cast<bf16*>(v_out), rows, p->Ls, p->Hs, rows, p->d, s));
+  } else {
+    KV_CUDA(launch_read_fp8(o.k8, o.lh_bytes, static_cast<uint8_t*>(k_out), sk_out, p->Ls, p->Hs, rows, p->d, s));
+    KV_CUDA(launch_read_fp8(o.v8, o.lh_bytes, static_cast<uint8_t*>(v_out), sv_out, p->Ls, p->Hs, rows, p->d, s));
+  }
+  g_launches += 2;
   return ok();
 }
 
@@ -740,17 +749,21 @@ struct RealignLayout {
 RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& hs) {
   RealignLayout L;
   const int n_seg = int(hs.size());
-  size_t n_ints = 0, n_wexp = 0;
+  const int rpt = rows_per_tile(d);
+  size_t n_ints = 0, n_wexp = 0, n_wt = 0;
   for (const HostSeg& g : hs) {
     n_ints += g.x.n_cand + g.gates.size();
-    if (g.prefix) n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
+    if (unit_weights_fit(g.x.n_cand, d))
+      n_wt += size_t((g.x.L_seg + rpt - 1) / rpt) * g.x.n_cand * weight_row_stride(d);
+    else if (g.prefix)
+      n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
   }
   TableHdr& hdr = L.hdr;
   hdr.n_seg = n_seg;
   hdr.d = d;
   hdr.Ls = Ls;
   hdr.Hs = Hs;
-  hdr.rows_per_tile = kStageBytes / (2 * d);
+  hdr.rows_per_tile = rpt;
   size_t off = align_up(sizeof(TableHdr), 64);
   hdr.seg_off = int64_t(off);
   off = align_up(off + sizeof(SegDev) * n_seg, 64);
@@ -760,6 +773,8 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
   hdr.wexp_off = int64_t(off);
   off = align_up(off + sizeof(float) * n_wexp, 64);
+  hdr.wt_off = int64_t(off);
+  off = align_up(off + sizeof(float) * n_wt, 64);
   L.bytes = off;
   return L;
 }
@@ -780,7 +795,8 @@ void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector
   SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
   int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.cand_off);
   float* dwexp = reinterpret_cast<float*>(dev + hdr.wexp_off);
-  int64_t units = 0;
+  const float* dwt = reinterpret_cast<const float*>(dev + hdr.wt_off);
+  int64_t units = 0, tpos = 0;
   int ipos = 0, wpos = 0;
   const int n = int(order.size());
   for (int t0 = 0; t0 < n;) {
@@ -804,7 +820,12 @@ void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector
       x.tiles = tiles;
       x.unit_begin = units;
       x.group_size = G;
-      if (src.prefix) {
+      x.uw = unit_weights_fit(x.n_cand, d) ? 1 : 0;
+      if (x.uw) {
+        x.wt = dwt + tpos;
+        x.wt_off = int32_t(tpos);
+        tpos += int64_t(tiles) * x.n_cand * weight_row_stride(d);
+      } else if (src.prefix) {
         x.ld_w = (x.L_seg + 3) & ~3;
         x.w = dwexp + wpos;
         x.wexp_off = wpos;
@@ -993,23 +1014,33 @@ static HostSeg host_segment(const kvcomm_realign_desc& g) {
   if (g.kind == KVCOMM_PLACEHOLDER) {
     x.w = g.weights;
     x.ld_w = g.ld_w;
-    x.off = p->fp8 ? reinterpret_cast<const bf16*>(p->ph8_base(g.consumer)) : p->ph_base(g.consumer);
-    x.scales = p->fp8 ? p->ph_sc_base(g.consumer) : nullptr;
-    x.slot_stride = p->ph_slot_stride();
-    x.plane_stride = p->ph_plane_stride();
-    x.off_ld = p->ph_ld;
+    if (!p->fp8) {
+      x.off = p->ph_base(g.consumer);
+      x.slot_stride = p->ph_slot_stride();
+      x.plane_stride = p->ph_plane_stride();
+      x.off_ld = p->ph_ld;
+    } else {
+      x.off = reinterpret_cast<const bf16*>(p->ph8 + int64_t(g.consumer) * p->cap * p->f8_ph_slot());
+      x.slot_stride = p->f8_ph_slot();
+      x.plane_stride = p->f8_ph_plane();
+      x.off_ld = p->f8_lh(p->ph_ld);
+    }
   } else {
     h.prefix = true;
     x.w_by_slot = 0;
     x.wbar = g.weights;
-    x.off = p->fp8 ? reinterpret_cast<const bf16*>(p->pf8[g.consumer]) : p->pf[g.consumer];
-    x.scales = p->fp8 ? p->pf_sc[g.consumer] : nullptr;
-    x.slot_stride = p->pf_slot_stride(g.consumer);
-    x.plane_stride = p->pf_plane_stride(g.consumer);
-    x.off_ld = p->pf_ld(g.consumer);
+    if (!p->fp8) {
+      x.off = p->pf[g.consumer];
+      x.slot_stride = p->pf_slot_stride(g.consumer);
+      x.plane_stride = p->pf_plane_stride(g.consumer);
+      x.off_ld = p->pf_ld(g.consumer);
+    } else {
+      x.off = reinterpret_cast<const bf16*>(p->pf8[g.consumer]);
+      x.slot_stride = p->f8_pf_slot(g.consumer);
+      x.plane_stride = p->f8_pf_plane(g.consumer);
+      x.off_ld = p->f8_lh(p->prefix_len[g.consumer]);
+    }
   }
-  x.sc_slot_stride = x.slot_stride / p->d;
-  x.sc_plane_stride = x.plane_stride / p->d;
   return h;
 }
 

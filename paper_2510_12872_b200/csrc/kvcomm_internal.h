@@ -11,21 +11,39 @@ using bf16 = __nv_bfloat16;
 // Bytes of data one realign pipeline stage carries (a tile of rows_per_tile token
 // rows of one (layer, head, K|V) plane): 16 KiB = 64 rows of d=128 bf16.
 constexpr int kStageBytes = 16384;
-constexpr int kStageWBytes = 2048;  // weight slice: up to kStageBytes/(2*16) floats
+constexpr int kStageStride = kStageBytes + 1024;  // + room for two fp8 blocks' row scales
+constexpr int kStageWBytes = 2048;  // per-stage weight slice (fallback path): up to 512 floats
+constexpr int kUnitWBytes = 8192;   // per-unit weight block [n_cand][rows_per_tile] floats
 constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
 constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
+
+// rows per realign tile (and per fp8 storage block) for head_dim d
+__host__ __device__ constexpr int rows_per_tile(int d) { return kStageBytes / (2 * d); }
+// fp8 storage block: rows_per_tile rows of d e4m3 codes, then their fp32 row scales,
+// padded to 16 bytes (TMA bulk granularity)
+__host__ __device__ constexpr int fp8_block_bytes(int d) { return (rows_per_tile(d) * (d + 4) + 15) & ~15; }
+// row stride of the weight slices in shared memory / weight blocks (16-byte multiple)
+__host__ __device__ constexpr int weight_row_stride(int d) { return (rows_per_tile(d) + 3) & ~3; }
+// a segment's unit weights travel as one block when they fit the unit weight buffer
+__host__ __device__ constexpr bool unit_weights_fit(int n_cand, int d) {
+  return n_cand > 0 && n_cand * weight_row_stride(d) * 4 <= kUnitWBytes;
+}
 
 // One segment of a realign batch, as the kernels see it (device resident).
 struct SegDev {
   const bf16* base[2];  // K, V base rows, [Ls][Hs][base_ld][d]
   bf16* dst[2];         // destination [Ls][Hs][dst_ld][d]
   float* dbg[2];        // optional fp32 blended offsets [Ls][Hs][L_seg][d]
-  const float* w;       // weight rows: row r at w + r*ld_w (r = slot or j, see w_by_slot)
-  const bf16* off;      // offsets of (consumer, kind): element (slot, plane, l, h, row, e)
+  const float* w;       // fallback weight rows: row r at w + r*ld_w (r = slot or j, see w_by_slot)
+  const float* wt;      // per-unit weight blocks [tiles][n_cand][weight_row_stride] (uw = 1)
+  const bf16* off;      // offsets of (consumer, kind).  bf16: element (slot, plane, l, h, row, e) at
+                        //   slot*slot_stride + plane*plane_stride + (lh*off_ld + row)*d + e;
+                        //   fp8: a byte pointer, block (slot, plane, lh, tile) at
+                        //   slot*slot_stride + plane*plane_stride + lh*off_ld + tile*fp8_block_bytes
   const double* inv_freq;  // [d/2] of the owning pool
   const float* wbar;    // PREFIX: scalar weights [capacity] (expanded by the prep kernel)
   int64_t base_ld, dst_ld, ld_w;
-  int64_t slot_stride, plane_stride, off_ld;  // elements
+  int64_t slot_stride, plane_stride, off_ld;  // bf16: elements / rows; fp8: bytes
   int64_t unit_begin;   // first work unit of this segment's group (same for every member)
   int32_t L_seg, target_start, delta, n_cand;
   int32_t cand_off;     // index of this segment's first candidate in Table::cand
@@ -37,10 +55,10 @@ struct SegDev {
   int32_t gate_off;     //   branch of Alg. 1); indices into Table::cand area, n_gate = 0: always
   int32_t group_size;   // segments sharing this base tile (consecutive in the table; units interleave
                         //   members so the shared base tile is read from HBM once and hit in L2 after)
-  int32_t fp8;          // offsets stored as e4m3 codes (off is then a byte pointer, element index = byte)
+  int32_t fp8;          // offsets stored as blocked e4m3 codes + row scales
+  int32_t uw;           // 1: the unit's weights arrive as one block (n_cand*rpt*4 <= kUnitWBytes)
+  int32_t wt_off;       // float offset of this segment's weight blocks in Table::wt
   int32_t _pad2;
-  const float* scales;  // fp8: one fp32 scale per offset row, index = element index / d
-  int64_t sc_slot_stride, sc_plane_stride;  // fp8: slot_stride / d, plane_stride / d (rows)
 };
 
 struct MatchResultDev {
@@ -54,7 +72,7 @@ struct TableHdr {
   int32_t rows_per_tile, _pad0;
   int64_t total_units;
   // byte offsets from the table base
-  int64_t seg_off, cand_off, cs_off, wexp_off;
+  int64_t seg_off, cand_off, cs_off, wexp_off, wt_off;
   const MatchResultDev* gate_results;  // verdicts the segments' gates index (device), or null
 };
 
@@ -97,13 +115,16 @@ cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t
                              int rows, int d, cudaStream_t s);
 // Contiguous copy of n bf16 elements (multiple of 8).
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
-// fp8 (e4m3 + per-row fp32 scale) offset storage: quantise bf16 rows / measure into codes.
-cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, float* scales, int64_t dst_ld,
-                                 int Ls, int Hs, int rows, int d, cudaStream_t s);
+// fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of rows_per_tile(d) rows
+// (codes, then the block's row scales); lh_bytes = bytes per (layer, head) region.
+cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
+                                 int rows, int d, cudaStream_t s);
 cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                                const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               const double* inv_freq, uint8_t* dk, uint8_t* dv, float* sk, float* sv,
-                               int64_t dst_ld, cudaStream_t s);
+                               const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes, cudaStream_t s);
+// blocked e4m3 rows -> dense codes [lh][rows][d] + scales [lh][rows] (inspection / tests)
+cudaError_t launch_read_fp8(const uint8_t* src, int64_t lh_bytes, uint8_t* codes, float* scales, int Ls, int Hs,
+                            int rows, int d, cudaStream_t s);
 // Offset measurement (insert path, step a0).
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                            const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,

@@ -170,9 +170,25 @@ __device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1,
 
 __device__ __forceinline__ float row_scale(float amax) { return amax > 0.f ? __fdiv_rn(amax, kE4M3Max) : 1.f; }
 
+// Blocked fp8 layout: row i of a (layer, head) region lives in block i / rpt at
+// codes + (i % rpt) * d, its scale at block + rpt * d + (i % rpt) * 4.  Within a row the
+// codes are stored in 16-byte chunks: chunk v = elements [8v, 8v+8) then [d/2+8v, d/2+8v+8)
+// (the rotate-half pairs the realign kernel's threads own).
+struct Fp8Row {
+  uint8_t* code;
+  float* scale;
+};
+
+__device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int d, int64_t lh_bytes) {
+  const int rpt = rows_per_tile(d);
+  uint8_t* blk = base + lh * lh_bytes + int64_t(i / rpt) * fp8_block_bytes(d);
+  const int r = i % rpt;
+  return {blk + r * d, reinterpret_cast<float*>(blk + rpt * d) + r};
+}
+
 // bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool)
 __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
-                                     float* __restrict__ scales, int64_t dst_ld, int rows, int d, int64_t total) {
+                                     int64_t lh_bytes, int rows, int d, int64_t total) {
   const int vph = d / 16;
   const int half = d / 2;
   for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < total; base += int64_t(gridDim.x) * blockDim.x) {
@@ -188,8 +204,8 @@ __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_l
       r = x / vph;
       const int i = int(r % rows);
       const int64_t lh = r / rows;
-      const bf16* s = src + (lh * src_ld + i) * d + v * 8;
-      const uint4 a = ldg128_nc(s), b = ldg128_nc(s + half);
+      const bf16* sp = src + (lh * src_ld + i) * d + v * 8;
+      const uint4 a = ldg128_nc(sp), b = ldg128_nc(sp + half);
       const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -206,11 +222,9 @@ __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_l
     m = group_max(m, vph);
     if (!active) continue;
     const float sc = row_scale(m);
-    const int i = int(r % rows);
-    const int64_t lh = r / rows;
-    const int64_t orow = lh * dst_ld + i;
-    store_fp8_item(f0, f1, sc, dst + orow * d + v * 8, dst + orow * d + half + v * 8);
-    if (v == 0) scales[orow] = sc;
+    const Fp8Row o = fp8_row(dst, r / rows, int(r % rows), d, lh_bytes);
+    store_fp8_item(f0, f1, sc, o.code + v * 16, o.code + v * 16 + 8);
+    if (v == 0) *o.scale = sc;
   }
 }
 
@@ -218,8 +232,8 @@ __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_l
 __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
                                    const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
                                    int rows, int d, int delta, const double* __restrict__ inv_freq,
-                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, float* __restrict__ sk,
-                                   float* __restrict__ sv, int64_t dst_ld, int64_t total) {
+                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes,
+                                   int64_t total) {
   __shared__ float2 cs[128];
   const int half = d / 2;
   for (int f = threadIdx.x; f < half; f += blockDim.x) {
@@ -276,33 +290,57 @@ __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __re
     if (!active) continue;
     const int i = int(r % rows);
     const int64_t lh = r / rows;
-    const int64_t orow = lh * dst_ld + i;
     const float sck = row_scale(mk), scv = row_scale(mv);
-    store_fp8_item(k0, k1, sck, dk + orow * d + v * 8, dk + orow * d + half + v * 8);
-    store_fp8_item(v0, v1, scv, dv + orow * d + v * 8, dv + orow * d + half + v * 8);
+    const Fp8Row ok = fp8_row(dk, lh, i, d, lh_bytes), ov = fp8_row(dv, lh, i, d, lh_bytes);
+    store_fp8_item(k0, k1, sck, ok.code + v * 16, ok.code + v * 16 + 8);
+    store_fp8_item(v0, v1, scv, ov.code + v * 16, ov.code + v * 16 + 8);
     if (v == 0) {
-      sk[orow] = sck;
-      sv[orow] = scv;
+      *ok.scale = sck;
+      *ov.scale = scv;
     }
   }
 }
 
-cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, float* scales, int64_t dst_ld,
-                                 int Ls, int Hs, int rows, int d, cudaStream_t s) {
+// blocked -> dense copy of stored fp8 offsets (inspection)
+__global__ void read_fp8_kernel(const uint8_t* __restrict__ src, int64_t lh_bytes, uint8_t* __restrict__ codes,
+                                float* __restrict__ scales, int rows, int d, int64_t total_rows) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < total_rows;
+       r += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(r % rows);
+    const int64_t lh = r / rows;
+    const Fp8Row o = fp8_row(const_cast<uint8_t*>(src), lh, i, d, lh_bytes);
+    for (int v = 0; v < d / 16; ++v) {
+      const uint4 c = *reinterpret_cast<const uint4*>(o.code + v * 16);
+      *reinterpret_cast<uint2*>(codes + r * d + v * 8) = make_uint2(c.x, c.y);
+      *reinterpret_cast<uint2*>(codes + r * d + d / 2 + v * 8) = make_uint2(c.z, c.w);
+    }
+    scales[r] = *o.scale;
+  }
+}
+
+cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
+                                 int rows, int d, cudaStream_t s) {
   const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
   if (total == 0) return cudaSuccess;
-  quantize_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, src_ld, dst, scales, dst_ld, rows, d, total);
+  quantize_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, src_ld, dst, lh_bytes, rows, d, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                                const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               const double* inv_freq, uint8_t* dk, uint8_t* dv, float* sk, float* sv,
-                               int64_t dst_ld, cudaStream_t s) {
+                               const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes, cudaStream_t s) {
   const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
   if (total == 0) return cudaSuccess;
   measure_fp8_kernel<<<grid_for(total, 256), 256, 0, s>>>(k_real, v_real, real_ld, k_base, v_base, base_ld, rows, d,
-                                                          delta, inv_freq, dk, dv, sk, sv, dst_ld, total);
+                                                          delta, inv_freq, dk, dv, lh_bytes, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_read_fp8(const uint8_t* src, int64_t lh_bytes, uint8_t* codes, float* scales, int Ls, int Hs,
+                            int rows, int d, cudaStream_t s) {
+  const int64_t total = int64_t(Ls) * Hs * rows;
+  if (total == 0) return cudaSuccess;
+  read_fp8_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, lh_bytes, codes, scales, rows, d, total);
   return cudaGetLastError();
 }
 

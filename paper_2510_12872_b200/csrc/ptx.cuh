@@ -91,6 +91,14 @@ __device__ __forceinline__ void e4m3x4_to_float(uint32_t u, float* f) {
   f[0] = fa.x; f[1] = fa.y; f[2] = fb.x; f[3] = fb.y;
 }
 
+// (d0, d1) += (a0, a1) * (b0, b1) as one packed FFMA2 (sm_100), each lane an IEEE fma.rn
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n .reg .b64 ra, rb, rc;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%0, %1};\n"
+      " fma.rn.f32x2 rc, ra, rb, rc;\n mov.b64 {%0, %1}, rc;\n}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 __device__ __forceinline__ void stg128_cs(void* p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

@@ -8,10 +8,12 @@
 // row and writes 1 row, ≈ k FMAs per 2(k+2) bytes.  Design:
 //   * one persistent CTA per SM walks a static round-robin list of work units
 //     (segment, layer, head, K|V plane, 16 KiB tile of token rows);
-//   * warp 8 (one elected lane) is the TMA producer: for every unit it streams the
-//     k anchor tiles (each with the matching weight slice) and finally the base
-//     tile into an 11-deep shared-memory ring with cp.async.bulk (UBLKCP) +
-//     mbarrier complete_tx, L2 evict-first;
+//   * the last warp (one elected lane) is the TMA producer: for every unit it streams
+//     the unit's weight block [n_cand][rows] (one copy, into a double-buffered side
+//     buffer), the k anchor tiles and finally the base tile into an 11-deep
+//     shared-memory ring with cp.async.bulk (UBLKCP) + mbarrier complete_tx, L2
+//     evict-first.  fp8 pools store offsets in blocks of one tile's e4m3 codes followed
+//     by their row scales, so an anchor tile is again ONE contiguous copy (two per stage);
 //   * warps 0-7 consume: each thread owns two 32-byte "items" (8 elements of the
 //     first half of a row and the matching 8 of the second half, so the
 //     rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
@@ -35,8 +37,10 @@ constexpr int kItems = kStageBytes / 32;                         // 512 items of
 constexpr int kConsumerBar = 1;                                  // named barrier id (consumers only)
 
 constexpr size_t realign_smem_bytes() {
-  return size_t(kNStage) * (kStageBytes + kStageWBytes) + 2 * kNStage * sizeof(uint64_t);
+  return size_t(kNStage) * (kStageStride + kStageWBytes) + 2 * kUnitWBytes +
+         (2 * kNStage + 4) * sizeof(uint64_t);
 }
+static_assert(realign_smem_bytes() <= 227 * 1024, "realign shared memory");
 
 __device__ __forceinline__ int find_segment(const SegDev* segs, int n_seg, int64_t u) {
   int lo = 0, hi = n_seg - 1;
@@ -83,38 +87,96 @@ __device__ __forceinline__ bool seg_open(const TableHdr& hdr, const int32_t* int
   return true;
 }
 
-// Per-segment preparation: cos/sin of δ·inv_freq (fp64 angle, reading A13) and,
-// for PREFIX segments, the scalar weights w̄[cand[j]] expanded into rows of the
-// same shape as a placeholder W slice so the main kernel treats both kinds alike.
+// Per-segment preparation (grid n_seg x kPrepY): cos/sin of δ·inv_freq (fp64 angle,
+// reading A13); for PREFIX segments without unit blocks, the scalar weights w̄[cand[j]]
+// expanded into rows shaped like a placeholder W slice; for segments with unit blocks,
+// the blocks [tile][j][row] = weight of candidate j at token row (0 past L_seg), taken
+// from W[slot] (PLACEHOLDER) or w̄[slot] (PREFIX).
+constexpr int kPrepY = 8;
 __global__ void realign_prep_kernel(uint8_t* tab) {
   const TableHdr* hdr = reinterpret_cast<const TableHdr*>(tab);
   SegDev* segs = reinterpret_cast<SegDev*>(tab + hdr->seg_off);
   const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr->cand_off);
   float2* cs = reinterpret_cast<float2*>(tab + hdr->cs_off);
   float* wexp = reinterpret_cast<float*>(tab + hdr->wexp_off);
+  float* wt = reinterpret_cast<float*>(tab + hdr->wt_off);
   const int s = blockIdx.x;
   const SegDev& g = segs[s];
   const int half = hdr->d / 2;
-  if (g.delta != 0) {
+  const int tid = blockIdx.y * blockDim.x + threadIdx.x;
+  const int nthr = gridDim.y * blockDim.x;
+  if (g.delta != 0 && blockIdx.y == 0) {
     for (int f = threadIdx.x; f < half; f += blockDim.x) {
       double sn, cn;
       sincos(double(g.delta) * g.inv_freq[f], &sn, &cn);
       cs[g.cs_off + f] = make_float2(float(cn), float(sn));
     }
   }
-  if (!g.w_by_slot && g.n_cand > 0) {
+  if (g.n_cand == 0) return;
+  if (g.uw) {
+    const int rpt = hdr->rows_per_tile;
+    const int rw = weight_row_stride(hdr->d);
+    const int64_t n = int64_t(g.tiles) * g.n_cand * rw;
+    for (int64_t x = tid; x < n; x += nthr) {
+      const int r = int(x % rw);
+      const int64_t tj = x / rw;
+      const int j = int(tj % g.n_cand);
+      const int row = int(tj / g.n_cand) * rpt + r;
+      const int slot = cand[g.cand_off + j];
+      float w = 0.f;
+      if (r < rpt && row < g.L_seg) w = g.w_by_slot ? g.w[int64_t(slot) * g.ld_w + row] : g.wbar[slot];
+      wt[g.wt_off + x] = w;
+    }
+  } else if (!g.w_by_slot) {
     const int ld = int(g.ld_w);
-    for (int x = threadIdx.x; x < g.n_cand * ld; x += blockDim.x) {
+    for (int x = tid; x < g.n_cand * ld; x += nthr) {
       const int j = x / ld;
       wexp[g.wexp_off + x] = g.wbar[cand[g.cand_off + j]];
     }
   }
 }
 
+// One pipeline stage of an fp8 pool: NA anchor blocks (codes, then row scales); every
+// thread's item is one 16-byte chunk of a row (8 codes of the first half of the row and
+// the matching 8 of the second half, stored interleaved), so a warp's loads are
+// contiguous and conflict-free.  Decode: F2FP (e4m3x2 -> f16x2, exact) + HADD2.F32
+// (f16 -> f32, exact), then packed FFMA2 with weight x row scale.  (An all-integer
+// decode with 2^120 folded into the weight measured 15 % slower: it loads the ALU pipe.)
+template <int NA, int NI>
+__device__ __forceinline__ void fp8_stage(float (&acc)[NI][16], const uint8_t* buf, const float* wv, int rw,
+                                          int fblk, int scale_off, const int (&irow)[NI], const int (&ivec)[NI],
+                                          int d) {
+  float w[NA][NI];
+  uint4 code[NA][NI];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    const uint8_t* ab = buf + a * fblk;
+    const float* scl = reinterpret_cast<const float*>(ab + scale_off);
+#pragma unroll
+    for (int q = 0; q < NI; ++q) {
+      w[a][q] = wv[a * rw + irow[q]] * scl[irow[q]];  // weight x row scale
+      code[a][q] = lds128(ab + irow[q] * d + ivec[q] * 16);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int q = 0; q < NI; ++q) {
+      const uint32_t cw[4] = {code[a][q].x, code[a][q].y, code[a][q].z, code[a][q].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {  // word t: elements 4t..4t+3 of the item's 16
+        float f[4];
+        e4m3x4_to_float(cw[t], f);
+        ffma2(acc[q][4 * t], acc[q][4 * t + 1], w[a][q], w[a][q], f[0], f[1]);
+        ffma2(acc[q][4 * t + 2], acc[q][4 * t + 3], w[a][q], w[a][q], f[2], f[3]);
+      }
+    }
+}
+
 // variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
 // of the TMA bulk store; bit1 = skip output stores (bandwidth probe only, wrong results).
-// kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread, twice the
-// issue slots for the e4m3 decode of fp8 pools) + one producer warp.
+// kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread) + one
+// producer warp.
 template <int kConsumerWarps>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     realign_kernel(const uint8_t* __restrict__ tab, int variant) {
@@ -126,10 +188,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const float2* cs = reinterpret_cast<const float2*>(tab + hdr.cs_off);
 
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sdata = smem;
-  float* sw = reinterpret_cast<float*>(smem + size_t(kNStage) * kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(kNStage) * (kStageBytes + kStageWBytes));
+  uint8_t* sdata = smem;                                                    // [kNStage][kStageStride]
+  float* sw = reinterpret_cast<float*>(smem + size_t(kNStage) * kStageStride);  // [kNStage][kStageWBytes/4]
+  float* suw = sw + size_t(kNStage) * (kStageWBytes / 4);                   // [2][kUnitWBytes/4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(suw + 2 * (kUnitWBytes / 4));
   uint64_t* empty = full + kNStage;
+  uint64_t* uw_full = empty + kNStage;
+  uint64_t* uw_empty = uw_full + 2;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -138,6 +203,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kConsumerWarps);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&uw_full[i], 1);
+      mbar_init(&uw_empty[i], kConsumerWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -145,6 +214,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const int d = hdr.d;
   const int Hs = hdr.Hs;
   const int rpt = hdr.rows_per_tile;
+  const int rw = weight_row_stride(d);
+  const int fblk = fp8_block_bytes(d);
   const int64_t total = hdr.total_units;
   const int row_bytes = 2 * d;
   const bool tma_store = !(variant & 3);
@@ -155,8 +226,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const uint64_t pol_stream = policy_evict_first();  // offsets: read once per request
       const uint64_t pol_shared = (variant & 4) ? policy_evict_first()
                                   : (variant & 8) ? policy_evict_normal() : policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
+      int stage = 0, ub = 0;
+      uint32_t phase = 0, uphase = 0;
       for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
         const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
         const SegDev& g = segs[un.s];
@@ -166,58 +237,54 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         const uint32_t bytes = uint32_t(nrows) * row_bytes;
         const uint32_t wbytes = (uint32_t(nrows) * 4u + 15u) & ~15u;
         const int64_t lh = int64_t(un.l) * Hs + un.h;
+        if (g.uw) {  // the unit's weights: one block for all its anchors
+          mbar_wait(&uw_empty[ub], uphase ^ 1u);
+          const uint32_t ubytes = uint32_t(g.n_cand * rw) * 4u;
+          mbar_arrive_expect_tx(&uw_full[ub], ubytes);
+          bulk_g2s(suw + ub * (kUnitWBytes / 4), g.wt + int64_t(un.t) * g.n_cand * rw, ubytes, &uw_full[ub],
+                   pol_stream);
+          if (++ub == 2) { ub = 0; uphase ^= 1u; }
+        }
         if (g.fp8) {
-          // e4m3 anchor tiles are half a stage: two anchors per stage, each with its
-          // weight slice and its per-row scale slice in the stage's side area
-          const uint32_t cbytes = uint32_t(nrows) * d;
-          // per-unit parts of the addresses (rows of the tile; codes are 1 byte per element)
-          const int64_t unit_rows = int64_t(un.p) * g.sc_plane_stride + lh * g.off_ld + i0;
-          const uint8_t* code0 = reinterpret_cast<const uint8_t*>(g.off) + unit_rows * d;
-          const float* scale0 = g.scales + unit_rows;
+          // one block (codes + row scales) per anchor, two anchors per stage
+          const uint8_t* blk0 = reinterpret_cast<const uint8_t*>(g.off) + int64_t(un.p) * g.plane_stride +
+                                lh * g.off_ld + int64_t(un.t) * fblk;
           const float* w0 = g.w + i0;
           for (int c = 0; c < g.n_cand; c += 2) {
             mbar_wait(&empty[stage], phase ^ 1u);
             const int na = min(2, g.n_cand - c);
-            uint8_t* dst = sdata + size_t(stage) * kStageBytes;
+            uint8_t* dst = sdata + size_t(stage) * kStageStride;
             float* swst = sw + size_t(stage) * (kStageWBytes / 4);
-            mbar_arrive_expect_tx(&full[stage], uint32_t(na) * (cbytes + 2 * wbytes));
+            mbar_arrive_expect_tx(&full[stage], uint32_t(na) * (fblk + (g.uw ? 0u : wbytes)));
             for (int a = 0; a < na; ++a) {
               const int slot = cand[g.cand_off + c + a];
-              bulk_g2s(dst + a * (kStageBytes / 2), code0 + int64_t(slot) * g.slot_stride, cbytes, &full[stage],
-                       pol_stream);
-              bulk_g2s(swst + a * rpt, w0 + int64_t(g.w_by_slot ? slot : c + a) * g.ld_w, wbytes, &full[stage],
-                       pol_stream);
-              bulk_g2s(swst + (2 + a) * rpt, scale0 + int64_t(slot) * g.sc_slot_stride, wbytes, &full[stage],
-                       pol_stream);
+              bulk_g2s(dst + a * fblk, blk0 + int64_t(slot) * g.slot_stride, fblk, &full[stage], pol_stream);
+              if (!g.uw)
+                bulk_g2s(swst + a * rw, w0 + int64_t(g.w_by_slot ? slot : c + a) * g.ld_w, wbytes, &full[stage],
+                         pol_stream);
             }
             if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           }
-          mbar_wait(&empty[stage], phase ^ 1u);
-          const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          bulk_g2s(sdata + size_t(stage) * kStageBytes, src, bytes, &full[stage],
-                   g.group_size > 1 ? pol_shared : pol_stream);
-          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
-          continue;
-        }
-        for (int c = 0; c <= g.n_cand; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          uint8_t* dst = sdata + size_t(stage) * kStageBytes;
-          if (c < g.n_cand) {
+        } else {
+          for (int c = 0; c < g.n_cand; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
             const int slot = cand[g.cand_off + c];
             const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
                               (lh * g.off_ld + i0) * d;
-            const float* wsrc = g.w + int64_t(g.w_by_slot ? slot : c) * g.ld_w + i0;
-            mbar_arrive_expect_tx(&full[stage], bytes + wbytes);
-            bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
-            bulk_g2s(sw + size_t(stage) * (kStageWBytes / 4), wsrc, wbytes, &full[stage], pol_stream);
-          } else {
-            const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
-            mbar_arrive_expect_tx(&full[stage], bytes);
-            bulk_g2s(dst, src, bytes, &full[stage], g.group_size > 1 ? pol_shared : pol_stream);
+            mbar_arrive_expect_tx(&full[stage], bytes + (g.uw ? 0u : wbytes));
+            bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage], pol_stream);
+            if (!g.uw)
+              bulk_g2s(sw + size_t(stage) * (kStageWBytes / 4), g.w + int64_t(g.w_by_slot ? slot : c) * g.ld_w + i0,
+                       wbytes, &full[stage], pol_stream);
+            if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           }
-          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
         }
+        mbar_wait(&empty[stage], phase ^ 1u);
+        const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage],
+                 g.group_size > 1 ? pol_shared : pol_stream);
+        if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
     }
     return;
@@ -233,8 +300,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     irow[q] = it / vpr;
     ivec[q] = it - irow[q] * vpr;
   }
-  int stage = 0;
-  uint32_t phase = 0;
+  int stage = 0, ub = 0;
+  uint32_t phase = 0, uphase = 0;
   for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
     const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
     const SegDev& g = segs[un.s];
@@ -248,30 +315,39 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       for (int e = 0; e < 16; ++e) acc[q][e] = 0.f;
 
     const int n_cand = g.n_cand;
+    const float* uwb = suw + ub * (kUnitWBytes / 4);
+    if (g.uw) mbar_wait(&uw_full[ub], uphase);
     if (g.fp8) {
       for (int c = 0; c < n_cand; c += 2) {
         mbar_wait(&full[stage], phase);
-        const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
-        const float* swst = sw + size_t(stage) * (kStageWBytes / 4);
-        const int na = min(2, n_cand - c);
-        for (int a = 0; a < na; ++a) {
-          const uint8_t* ab = buf + a * (kStageBytes / 2);
+        const uint8_t* buf = sdata + size_t(stage) * kStageStride;
+        const float* wv = g.uw ? uwb + c * rw : sw + size_t(stage) * (kStageWBytes / 4);
+        if (n_cand - c >= 2)
+          fp8_stage<2, kItemsPerThread>(acc, buf, wv, rw, fblk, rpt * d, irow, ivec, d);
+        else
+          fp8_stage<1, kItemsPerThread>(acc, buf, wv, rw, fblk, rpt * d, irow, ivec, d);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+      }
+    } else {
+      for (int c = 0; c < n_cand; ++c) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* buf = sdata + size_t(stage) * kStageStride;
+        const float* wv = g.uw ? uwb + c * rw : sw + size_t(stage) * (kStageWBytes / 4);
 #pragma unroll
-          for (int q = 0; q < kItemsPerThread; ++q) {
-            const float w = swst[a * rpt + irow[q]] * swst[(2 + a) * rpt + irow[q]];  // weight x row scale
-            const uint2 lo = lds64(ab + irow[q] * d + ivec[q] * 8);
-            const uint2 hi = lds64(ab + irow[q] * d + d / 2 + ivec[q] * 8);
-            const uint32_t lw[2] = {lo.x, lo.y}, hw[2] = {hi.x, hi.y};
+        for (int q = 0; q < kItemsPerThread; ++q) {
+          const float w = wv[irow[q]];
+          const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
+          const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+          const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+          const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              float f[4];
-              e4m3x4_to_float(lw[t], f);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) acc[q][4 * t + e] = fmaf(w, f[e], acc[q][4 * t + e]);
-              e4m3x4_to_float(hw[t], f);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) acc[q][8 + 4 * t + e] = fmaf(w, f[e], acc[q][8 + 4 * t + e]);
-            }
+          for (int e = 0; e < 4; ++e) {
+            acc[q][2 * e] = fmaf(w, bf_lo(av[e]), acc[q][2 * e]);
+            acc[q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[q][2 * e + 1]);
+            acc[q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[q][8 + 2 * e]);
+            acc[q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[q][8 + 2 * e + 1]);
           }
         }
         __syncwarp();
@@ -279,33 +355,15 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
     }
-    for (int c = 0; c < (g.fp8 ? 0 : n_cand); ++c) {
-      mbar_wait(&full[stage], phase);
-      const uint8_t* buf = sdata + size_t(stage) * kStageBytes;
-      const float* wv = sw + size_t(stage) * (kStageWBytes / 4);
-#pragma unroll
-      for (int q = 0; q < kItemsPerThread; ++q) {
-        const float w = wv[irow[q]];
-        const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
-        const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
-        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-        const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[q][2 * e] = fmaf(w, bf_lo(av[e]), acc[q][2 * e]);
-          acc[q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[q][2 * e + 1]);
-          acc[q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[q][8 + 2 * e]);
-          acc[q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[q][8 + 2 * e + 1]);
-        }
-      }
+    if (g.uw) {  // unit weight buffer free for the producer's unit after next
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+      if (lane == 0) mbar_arrive(&uw_empty[ub]);
+      if (++ub == 2) { ub = 0; uphase ^= 1u; }
     }
 
     // base tile: add, rotate (K), round, store
     mbar_wait(&full[stage], phase);
-    uint8_t* buf = sdata + size_t(stage) * kStageBytes;
+    uint8_t* buf = sdata + size_t(stage) * kStageStride;
     const int64_t lh = int64_t(un.l) * Hs + un.h;
     const bool rotate = un.p == 0 && g.delta != 0;
     if (n_cand > 0 || rotate) {  // COPY segments leave the staged rows untouched (bit-exact)
@@ -396,7 +454,7 @@ int realign_grid_size(int device) {
 
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
-  static int variant = -1, cw = 16;
+  static int variant = -1, cw = 8;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
@@ -412,9 +470,9 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
     const char* v = getenv("KVCOMM_REALIGN_VARIANT");
     variant = v ? atoi(v) : 0;
     const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
-    if (c && atoi(c) == 8) cw = 8;
+    if (c && atoi(c) == 16) cw = 16;
   }
-  realign_prep_kernel<<<hdr.n_seg, 128, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
+  realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
   const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);

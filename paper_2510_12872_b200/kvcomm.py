@@ -205,31 +205,36 @@ class AnchorPool:
                 "pf_present_mask": s.pf_present_mask}
 
     def offset_view(self, slot: int, consumer: int, which: str = "ph", rows: Optional[int] = None):
-        """(ΔK, ΔV) stored for (slot, consumer) as [Ls, Hs, rows, d] bf16 views of pool memory."""
+        """bf16 pools: (ΔK, ΔV) stored for (slot, consumer) as [Ls, Hs, rows, d] views of pool memory."""
         k, v, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
         L.check(L.lib().kvcomm_anchor_pool_offset_view(self.handle, slot, consumer, 0 if which == "ph" else 1,
                                                        C.byref(k), C.byref(v), C.byref(ld)))
         rows = ld.value if rows is None else rows
         out = []
         for p in (k.value, v.value):
-            if self.offset_format == "fp8":   # raw e4m3 codes
-                flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "|u1"),
-                                       device=self.device)
-                out.append(flat.view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
-            else:
-                flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "<i2"),
-                                       device=self.device)
-                out.append(flat.view(torch.bfloat16).view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
+            flat = torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value * self.d,), "<i2"), device=self.device)
+            out.append(flat.view(torch.bfloat16).view(self.Ls, self.Hs, ld.value, self.d)[:, :, :rows])
         return tuple(out)
 
-    def offset_scales(self, slot: int, consumer: int, which: str = "ph", rows: Optional[int] = None):
-        """fp8 pools: per-row fp32 scales (sK, sV) as [Ls, Hs, rows] views of pool memory."""
-        k, v, ld = C.c_void_p(), C.c_void_p(), C.c_int64()
-        L.check(L.lib().kvcomm_anchor_pool_offset_scales(self.handle, slot, consumer, 0 if which == "ph" else 1,
-                                                         C.byref(k), C.byref(v), C.byref(ld)))
-        rows = ld.value if rows is None else rows
-        return tuple(torch.as_tensor(_DevView(p, (self.Ls * self.Hs * ld.value,), "<f4"), device=self.device)
-                     .view(self.Ls, self.Hs, ld.value)[:, :, :rows] for p in (k.value, v.value))
+    def read_offsets(self, slot: int, consumer: int, which: str, rows: int, stream=None):
+        """Copies of the stored offsets: bf16 pools -> (ΔK, ΔV) bf16 [Ls, Hs, rows, d];
+        fp8 pools -> (codes_K, codes_V uint8 [Ls, Hs, rows, d], scales_K, scales_V fp32 [Ls, Hs, rows])."""
+        shape = (self.Ls, self.Hs, rows, self.d)
+        if self.offset_format == "fp8":
+            k = torch.empty(shape, dtype=torch.uint8, device=self.device)
+            v = torch.empty_like(k)
+            sk = torch.empty(shape[:3], dtype=torch.float32, device=self.device)
+            sv = torch.empty_like(sk)
+            L.check(L.lib().kvcomm_anchor_pool_read_offsets(self.handle, slot, consumer, 0 if which == "ph" else 1,
+                                                            rows, k.data_ptr(), v.data_ptr(), sk.data_ptr(),
+                                                            sv.data_ptr(), _stream_handle(stream)))
+            return k, v, sk, sv
+        k = torch.empty(shape, dtype=torch.bfloat16, device=self.device)
+        v = torch.empty_like(k)
+        L.check(L.lib().kvcomm_anchor_pool_read_offsets(self.handle, slot, consumer, 0 if which == "ph" else 1, rows,
+                                                        k.data_ptr(), v.data_ptr(), None, None,
+                                                        _stream_handle(stream)))
+        return k, v
 
     # -- a1-a3 ---------------------------------------------------------------
     def _match_request(self, query_emb: torch.Tensor, consumer: int, gamma: float, top_k: int, want_dist: bool,

@@ -299,8 +299,7 @@ def test_fp8_offsets_codes_and_realign(d, L_phi, P):
     for j, s in enumerate(gpu["slots"]):
         for which, src in (("ph", p.dk_ph[0][j]), ("pf", p.dk_pf[0][j])):
             rows = src.shape[2]
-            gk, _ = pool.offset_view(s, 0, which, rows=rows)
-            sk, _ = pool.offset_scales(s, 0, which, rows=rows)
+            gk, _, sk, _ = pool.read_offsets(s, 0, which, rows)
             q, sc = O.quantize_rows_fp8(harness.f64(src))
             assert torch.equal(gk.cpu(), _fp8_codes(q)), (j, which)
             assert torch.equal(sk.cpu(), torch.from_numpy(sc)), (j, which)
@@ -324,8 +323,8 @@ def test_fp8_measure_insert_close_to_oracle():
     f64 = harness.f64
     for which, (a, b, c_, d_, sr, sb, n) in {"ph": (kr, vr, kb, vb, 300, 0, T),
                                              "pf": (pkr, pvr, pkb, pvb, 300 + T, 40, P)}.items():
-        codes = pool.offset_view(slot, 0, which, rows=n)
-        scales = pool.offset_scales(slot, 0, which, rows=n)
+        ck, cv, sk, sv = pool.read_offsets(slot, 0, which, n)
+        codes, scales = (ck, cv), (sk, sv)
         odk, odv = O.measure_offset(f64(a), f64(b), sr, f64(c_), f64(d_), sb, inv)
         for code, sc, ref in zip(codes, scales, (odk, odv)):
             got = code.cpu().view(torch.float8_e4m3fn).double().numpy() * f64(sc)[..., None]
@@ -345,3 +344,28 @@ def test_host_resident_pool(fmt):
     assert torch.equal(dev["dst_k"], host["dst_k"]) and torch.equal(dev["dst_v"], host["dst_v"])
     ora = harness.run_oracle(p, gamma=1.0, fp8=(fmt == "fp8"))
     harness.compare(host, ora, p)
+
+
+@pytest.mark.parametrize("fmt,d,n_anchor", [("bf16", 128, 40), ("fp8", 64, 20), ("fp8", 128, 3)])
+def test_weight_block_fallback(fmt, d, n_anchor):
+    """Units whose weight block [n_cand][rows] exceeds the kernel's unit buffer take the
+    per-anchor weight-slice path; both paths agree with the oracle."""
+    lens = [60 + 7 * (j % 5) for j in range(n_anchor)]
+    p = synth.make_problem(40 + n_anchor, L=2, H=2, d=d, D_e=64, L_phi=60, anchor_lens=lens, prefix_lens=[11],
+                           target_start=9, pf_base_start=9, inv_freq=synth.llama3_inv_freq(d))
+    gpu = harness.run_gpu(p, gamma=1.0, offset_format=fmt)
+    ora = harness.run_oracle(p, gamma=1.0, fp8=(fmt == "fp8"))
+    harness.compare(gpu, ora, p)
+
+
+def test_fp8_large_row_scale():
+    """Offsets of very large magnitude (row scales amax/448 far above 1) quantise and
+    realign like any other rows: no overflow in weight x row scale or the decode."""
+    d = 128
+    p = synth.make_problem(77, L=2, H=2, d=d, D_e=64, L_phi=90, anchor_lens=[90, 95, 130], prefix_lens=[20],
+                           target_start=5, pf_base_start=5, inv_freq=synth.llama3_inv_freq(d))
+    for lst in (p.dk_ph, p.dv_ph, p.dk_pf, p.dv_pf):
+        lst[0][1] = (lst[0][1].float() * 4e6).to(torch.bfloat16)
+    gpu = harness.run_gpu(p, gamma=1.0, offset_format="fp8")
+    ora = harness.run_oracle(p, gamma=1.0, fp8=True)
+    harness.compare(gpu, ora, p)
