@@ -9,7 +9,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libkvcomm.so")
+# KVCOMM_LIB: probe builds of the same library (scripts/tune_realign.sh); default in-tree
+LIB_PATH = os.environ.get("KVCOMM_LIB") or os.path.join(HERE, "lib", "libkvcomm.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "kvcomm.h")
 
 MAX_CAPACITY = 1024
@@ -146,8 +147,13 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         raise RuntimeError(f"libkvcomm.so not found at {path}: build it with "
                            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
     lib = C.CDLL(path)
+    probe = os.environ.get("KVCOMM_LIB") is not None  # probe builds of older revisions may lack symbols
     for name, (res, args) in _SIGS.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and probe:
+            continue
+        if fn is None:
+            raise RuntimeError(f"{path} does not export {name}: stale build")
         fn.restype = res
         fn.argtypes = args
     return lib

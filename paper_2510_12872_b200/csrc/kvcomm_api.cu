@@ -113,7 +113,9 @@ struct kvcomm_pool_s {
   bf16* ph_base(int c) const { return ph + int64_t(c) * cap * ph_slot_stride(); }
   int64_t pf_ld(int c) const { return prefix_len[c]; }
   // fp8 blocked geometry (bytes): a (layer, head) region holds ceil(ld / rpt) blocks
-  int64_t f8_lh(int64_t ld) const { return (ld + rows_per_tile(d) - 1) / rows_per_tile(d) * fp8_block_bytes(d); }
+  int64_t f8_lh(int64_t ld) const {
+    return (ld + fp8_rows_per_block(d) - 1) / fp8_rows_per_block(d) * fp8_block_bytes(d);
+  }
   int64_t f8_ph_plane() const { return int64_t(Ls) * Hs * f8_lh(ph_ld); }
   int64_t f8_ph_slot() const { return 2 * f8_ph_plane(); }
   int64_t f8_pf_plane(int c) const { return int64_t(Ls) * Hs * f8_lh(prefix_len[c]); }
@@ -750,13 +752,11 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   RealignLayout L;
   const int n_seg = int(hs.size());
   const int rpt = rows_per_tile(d);
-  size_t n_ints = 0, n_wexp = 0, n_wt = 0;
+  size_t n_ints = 0, n_wt = 0;
   for (const HostSeg& g : hs) {
     n_ints += g.x.n_cand + g.gates.size();
-    if (unit_weights_fit(g.x.n_cand, d))
-      n_wt += size_t((g.x.L_seg + rpt - 1) / rpt) * g.x.n_cand * weight_row_stride(d);
-    else if (g.prefix)
-      n_wexp += size_t(g.x.n_cand) * ((g.x.L_seg + 3) & ~3);
+    const int rpu = unit_rows(d, g.x.fp8);
+    n_wt += size_t((g.x.L_seg + rpu - 1) / rpu) * g.x.n_cand * weight_row_stride(rpu);
   }
   TableHdr& hdr = L.hdr;
   hdr.n_seg = n_seg;
@@ -771,8 +771,6 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   off = align_up(off + sizeof(int32_t) * std::max<size_t>(n_ints, 1), 64);
   hdr.cs_off = int64_t(off);
   off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
-  hdr.wexp_off = int64_t(off);
-  off = align_up(off + sizeof(float) * n_wexp, 64);
   hdr.wt_off = int64_t(off);
   off = align_up(off + sizeof(float) * n_wt, 64);
   L.bytes = off;
@@ -783,30 +781,32 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
 void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector<HostSeg>& hs_in,
                    const MatchResultDev* gate_results) {
   TableHdr& hdr = L.hdr;
-  const int d = hdr.d, rpt = hdr.rows_per_tile;
+  const int d = hdr.d;
   // group segments that share a base cache (and hence its tiles): consecutive in the table
   std::vector<int> order(hs_in.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     const SegDev &x = hs_in[a].x, &y = hs_in[b].x;
     if (x.base[0] != y.base[0]) return x.base[0] < y.base[0];
+    if (x.fp8 != y.fp8) return x.fp8 < y.fp8;
     return x.L_seg < y.L_seg;
   });
   SegDev* segs = reinterpret_cast<SegDev*>(h + hdr.seg_off);
   int32_t* ints = reinterpret_cast<int32_t*>(h + hdr.cand_off);
-  float* dwexp = reinterpret_cast<float*>(dev + hdr.wexp_off);
   const float* dwt = reinterpret_cast<const float*>(dev + hdr.wt_off);
   int64_t units = 0, tpos = 0;
-  int ipos = 0, wpos = 0;
+  int ipos = 0;
   const int n = int(order.size());
   for (int t0 = 0; t0 < n;) {
     int t1 = t0 + 1;
     const SegDev& lead = hs_in[order[t0]].x;
     while (t1 < n && hs_in[order[t1]].x.base[0] == lead.base[0] && hs_in[order[t1]].x.base[1] == lead.base[1] &&
-           hs_in[order[t1]].x.base_ld == lead.base_ld && hs_in[order[t1]].x.L_seg == lead.L_seg)
+           hs_in[order[t1]].x.base_ld == lead.base_ld && hs_in[order[t1]].x.L_seg == lead.L_seg &&
+           hs_in[order[t1]].x.fp8 == lead.fp8)
       ++t1;
     const int G = t1 - t0;
-    const int tiles = (lead.L_seg + rpt - 1) / rpt;
+    const int rpu = unit_rows(d, lead.fp8);  // equal tiles for every member
+    const int tiles = (lead.L_seg + rpu - 1) / rpu;
     for (int t = t0; t < t1; ++t) {
       const HostSeg& src = hs_in[order[t]];
       SegDev x = src.x;
@@ -820,17 +820,9 @@ void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector
       x.tiles = tiles;
       x.unit_begin = units;
       x.group_size = G;
-      x.uw = unit_weights_fit(x.n_cand, d) ? 1 : 0;
-      if (x.uw) {
-        x.wt = dwt + tpos;
-        x.wt_off = int32_t(tpos);
-        tpos += int64_t(tiles) * x.n_cand * weight_row_stride(d);
-      } else if (src.prefix) {
-        x.ld_w = (x.L_seg + 3) & ~3;
-        x.w = dwexp + wpos;
-        x.wexp_off = wpos;
-        wpos += int(x.ld_w) * x.n_cand;
-      }
+      x.wt = dwt + tpos;
+      x.wt_off = tpos;
+      tpos += int64_t(tiles) * x.n_cand * weight_row_stride(rpu);
       segs[t] = x;
     }
     units += int64_t(hdr.Ls) * hdr.Hs * 2 * tiles * G;

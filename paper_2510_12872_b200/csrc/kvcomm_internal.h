@@ -11,31 +11,29 @@ using bf16 = __nv_bfloat16;
 // Bytes of data one realign pipeline stage carries (a tile of rows_per_tile token
 // rows of one (layer, head, K|V) plane): 16 KiB = 64 rows of d=128 bf16.
 constexpr int kStageBytes = 16384;
-constexpr int kStageStride = kStageBytes + 1024;  // + room for two fp8 blocks' row scales
-constexpr int kStageWBytes = 2048;  // per-stage weight slice (fallback path): up to 512 floats
-constexpr int kUnitWBytes = 8192;   // per-unit weight block [n_cand][rows_per_tile] floats
+constexpr int kStageStride = kStageBytes + 1024;  // an fp8 block (codes + row scales) fits too
+constexpr int kUnitWBytes = 16384;  // weight chunk buffer: [anchors][weight_row_stride] floats
 constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
 constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
 
-// rows per realign tile (and per fp8 storage block) for head_dim d
+// rows per realign tile (16 KiB of bf16 rows) for head_dim d
 __host__ __device__ constexpr int rows_per_tile(int d) { return kStageBytes / (2 * d); }
-// fp8 storage block: rows_per_tile rows of d e4m3 codes, then their fp32 row scales,
-// padded to 16 bytes (TMA bulk granularity)
-__host__ __device__ constexpr int fp8_block_bytes(int d) { return (rows_per_tile(d) * (d + 4) + 15) & ~15; }
-// row stride of the weight slices in shared memory / weight blocks (16-byte multiple)
-__host__ __device__ constexpr int weight_row_stride(int d) { return (rows_per_tile(d) + 3) & ~3; }
-// a segment's unit weights travel as one block when they fit the unit weight buffer
-__host__ __device__ constexpr bool unit_weights_fit(int n_cand, int d) {
-  return n_cand > 0 && n_cand * weight_row_stride(d) * 4 <= kUnitWBytes;
-}
+// fp8 storage block: two tiles' rows of d e4m3 codes, then their fp32 row scales, padded
+// to 16 bytes (TMA bulk granularity) — about 16 KiB, one contiguous copy per anchor tile
+__host__ __device__ constexpr int fp8_rows_per_block(int d) { return 2 * rows_per_tile(d); }
+__host__ __device__ constexpr int fp8_block_bytes(int d) { return (fp8_rows_per_block(d) * (d + 4) + 15) & ~15; }
+// token rows of one realign work unit: one bf16 tile, or one fp8 block
+__host__ __device__ constexpr int unit_rows(int d, int fp8) { return fp8 ? fp8_rows_per_block(d) : rows_per_tile(d); }
+// row stride of the weight blocks (16-byte multiple)
+__host__ __device__ constexpr int weight_row_stride(int rows) { return (rows + 3) & ~3; }
 
 // One segment of a realign batch, as the kernels see it (device resident).
 struct SegDev {
   const bf16* base[2];  // K, V base rows, [Ls][Hs][base_ld][d]
   bf16* dst[2];         // destination [Ls][Hs][dst_ld][d]
   float* dbg[2];        // optional fp32 blended offsets [Ls][Hs][L_seg][d]
-  const float* w;       // fallback weight rows: row r at w + r*ld_w (r = slot or j, see w_by_slot)
-  const float* wt;      // per-unit weight blocks [tiles][n_cand][weight_row_stride] (uw = 1)
+  const float* w;       // PLACEHOLDER: W rows by slot, row r at w + r*ld_w (w_by_slot = 1)
+  const float* wt;      // weight blocks [tiles][n_cand][weight_row_stride(unit rows)] (prep kernel)
   const bf16* off;      // offsets of (consumer, kind).  bf16: element (slot, plane, l, h, row, e) at
                         //   slot*slot_stride + plane*plane_stride + (lh*off_ld + row)*d + e;
                         //   fp8: a byte pointer, block (slot, plane, lh, tile) at
@@ -48,17 +46,14 @@ struct SegDev {
   int32_t L_seg, target_start, delta, n_cand;
   int32_t cand_off;     // index of this segment's first candidate in Table::cand
   int32_t cs_off;       // index (in float2) of its cos/sin table in Table::cs
-  int32_t w_by_slot;    // 1: weight row = slot (PLACEHOLDER W); 0: row = j (expanded w̄)
-  int32_t tiles;        // ceil(L_seg / rows_per_tile)
-  int32_t wexp_off;     // PREFIX: float offset of the expanded weights in Table::wexp
+  int32_t w_by_slot;    // 1: weights from W[slot] (PLACEHOLDER); 0: from w̄[slot] (PREFIX)
+  int32_t tiles;        // ceil(L_seg / unit_rows)
   int32_t n_gate;       // segment runs iff every listed match verdict is SHAREABLE (device-side
   int32_t gate_off;     //   branch of Alg. 1); indices into Table::cand area, n_gate = 0: always
   int32_t group_size;   // segments sharing this base tile (consecutive in the table; units interleave
                         //   members so the shared base tile is read from HBM once and hit in L2 after)
   int32_t fp8;          // offsets stored as blocked e4m3 codes + row scales
-  int32_t uw;           // 1: the unit's weights arrive as one block (n_cand*rpt*4 <= kUnitWBytes)
-  int32_t wt_off;       // float offset of this segment's weight blocks in Table::wt
-  int32_t _pad2;
+  int64_t wt_off;       // float offset of this segment's weight blocks in Table::wt
 };
 
 struct MatchResultDev {
@@ -72,7 +67,7 @@ struct TableHdr {
   int32_t rows_per_tile, _pad0;
   int64_t total_units;
   // byte offsets from the table base
-  int64_t seg_off, cand_off, cs_off, wexp_off, wt_off;
+  int64_t seg_off, cand_off, cs_off, wt_off;
   const MatchResultDev* gate_results;  // verdicts the segments' gates index (device), or null
 };
 
@@ -115,7 +110,7 @@ cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t
                              int rows, int d, cudaStream_t s);
 // Contiguous copy of n bf16 elements (multiple of 8).
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
-// fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of rows_per_tile(d) rows
+// fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of fp8_rows_per_block(d) rows
 // (codes, then the block's row scales); lh_bytes = bytes per (layer, head) region.
 cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
                                  int rows, int d, cudaStream_t s);

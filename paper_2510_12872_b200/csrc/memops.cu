@@ -170,8 +170,8 @@ __device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1,
 
 __device__ __forceinline__ float row_scale(float amax) { return amax > 0.f ? __fdiv_rn(amax, kE4M3Max) : 1.f; }
 
-// Blocked fp8 layout: row i of a (layer, head) region lives in block i / rpt at
-// codes + (i % rpt) * d, its scale at block + rpt * d + (i % rpt) * 4.  Within a row the
+// Blocked fp8 layout: row i of a (layer, head) region lives in block i / rpb at
+// codes + (i % rpb) * d, its scale at block + rpb * d + (i % rpb) * 4 (rpb = fp8_rows_per_block).  Within a row the
 // codes are stored in 16-byte chunks: chunk v = elements [8v, 8v+8) then [d/2+8v, d/2+8v+8)
 // (the rotate-half pairs the realign kernel's threads own).
 struct Fp8Row {
@@ -180,10 +180,10 @@ struct Fp8Row {
 };
 
 __device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int d, int64_t lh_bytes) {
-  const int rpt = rows_per_tile(d);
-  uint8_t* blk = base + lh * lh_bytes + int64_t(i / rpt) * fp8_block_bytes(d);
-  const int r = i % rpt;
-  return {blk + r * d, reinterpret_cast<float*>(blk + rpt * d) + r};
+  const int rpb = fp8_rows_per_block(d);
+  uint8_t* blk = base + lh * lh_bytes + int64_t(i / rpb) * fp8_block_bytes(d);
+  const int r = i % rpb;
+  return {blk + r * d, reinterpret_cast<float*>(blk + rpb * d) + r};
 }
 
 // bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool)

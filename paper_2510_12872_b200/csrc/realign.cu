@@ -5,22 +5,22 @@
 //   V̂[l,h,i,:] =      V_base[l,h,i,:] + Σ_j w[i,j] ΔV_j[l,h,i,:]        alignment P:141)
 //
 // The path is pure HBM streaming: per output row it reads k offset rows + 1 base
-// row and writes 1 row, ≈ k FMAs per 2(k+2) bytes.  Design (DESIGN.md §Kernels):
+// row and writes 1 row, ≈ k FMAs per 2(k+2) bytes.  Design (DESIGN.md §7):
 //   * one persistent CTA per SM walks a static round-robin list of work units
-//     (segment, layer, head, K|V plane, 16 KiB tile of token rows);
-//   * the last warp (one elected lane) is the TMA producer: for every unit it streams
-//     the unit's weight block [n_cand][rows] (one copy, into a double-buffered side
-//     buffer), the k anchor tiles and finally the base tile into an 11-deep
-//     shared-memory ring with cp.async.bulk (UBLKCP) + mbarrier complete_tx, L2
-//     evict-first.  fp8 pools store offsets in blocks of one tile's e4m3 codes followed
-//     by their row scales, so an anchor tile is again ONE contiguous copy (two per stage);
-//   * warps 0-7 consume: each thread owns two 32-byte "items" (8 elements of the
-//     first half of a row and the matching 8 of the second half, so the
-//     rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
-//     registers; on the base tile it adds, rotates (K only), rounds to bf16 (RNE)
-//     in place in shared memory, and one thread writes the whole tile back with a
-//     single TMA bulk store (cp.async.bulk.global.shared), which measured 2-3 %
-//     faster than per-thread STG (profiles/).
+//     (segment, layer, head, K|V plane, tile of token rows: 16 KiB of bf16 rows, or
+//     two such tiles for fp8 pools so that each anchor tile is again ~16 KiB);
+//   * the last warp (one elected lane) is the TMA producer: it streams the unit's
+//     weights [n_cand][rows] in chunks of up to 16 KiB (one copy each, double
+//     buffered), then the anchor tiles (one contiguous copy per anchor: bf16 rows, or
+//     an fp8 block of e4m3 codes followed by their row scales) and finally the base
+//     tile(s) into an 11-deep shared-memory ring with cp.async.bulk (UBLKCP) + mbarrier
+//     complete_tx, L2 evict-first;
+//   * warps 0-7 consume: each thread owns two 32-byte "items" per 64-row tile (8
+//     elements of the first half of a row and the matching 8 of the second half, so
+//     the rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
+//     registers; on a base tile it adds, rotates (K only), rounds to bf16 (RNE) in
+//     place in shared memory, and one thread writes the whole tile back with a single
+//     TMA bulk store (cp.async.bulk.global.shared), 2-3 % faster than per-thread STG.
 //   * COPY segments (n_cand = 0, δ = 0) move rows verbatim through the same ring
 //     (bit-exact: no arithmetic is applied), so p_(m,0) rides in the same launch.
 #include <cuda_runtime.h>
@@ -33,12 +33,14 @@
 namespace kvc {
 
 constexpr int kNStage = 11;
-constexpr int kItems = kStageBytes / 32;                         // 512 items of 32 B per stage
-constexpr int kConsumerBar = 1;                                  // named barrier id (consumers only)
+constexpr int kItems = kStageBytes / 32;  // 512 items of 32 B per 16 KiB bf16 tile
+constexpr int kConsumerBar = 1;           // named barrier id (consumers only)
+#ifndef KVC_BF16_FFMA2
+#define KVC_BF16_FFMA2 1
+#endif
 
 constexpr size_t realign_smem_bytes() {
-  return size_t(kNStage) * (kStageStride + kStageWBytes) + 2 * kUnitWBytes +
-         (2 * kNStage + 4) * sizeof(uint64_t);
+  return size_t(kNStage) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * kNStage + 4) * sizeof(uint64_t);
 }
 static_assert(realign_smem_bytes() <= 227 * 1024, "realign shared memory");
 
@@ -56,8 +58,8 @@ struct Unit {
 };
 
 // unit -> (segment, layer, head, plane, tile), tile fastest so that neighbouring CTAs
-// stream neighbouring 16 KiB tiles of the same anchor at the same time.  Segments that
-// share one base cache (one sample realigned for several consumers) form a group whose
+// stream neighbouring tiles of the same anchor at the same time.  Segments that share
+// one base cache (one sample realigned for several consumers) form a group whose
 // members are interleaved just outside the tile index: all members' units of one
 // (layer, head, plane) fall in the same round of CTAs, so the shared base tile is
 // fetched from HBM once and hit in L2 by the other members.
@@ -88,23 +90,18 @@ __device__ __forceinline__ bool seg_open(const TableHdr& hdr, const int32_t* int
 }
 
 // Per-segment preparation (grid n_seg x kPrepY): cos/sin of δ·inv_freq (fp64 angle,
-// reading A13); for PREFIX segments without unit blocks, the scalar weights w̄[cand[j]]
-// expanded into rows shaped like a placeholder W slice; for segments with unit blocks,
-// the blocks [tile][j][row] = weight of candidate j at token row (0 past L_seg), taken
-// from W[slot] (PLACEHOLDER) or w̄[slot] (PREFIX).
+// reading A13) and the weight blocks wt[tile][j][row] = weight of candidate j at the
+// tile's token row (0 past L_seg), from W[slot] (PLACEHOLDER) or w̄[slot] (PREFIX),
+// so the main kernel fetches a unit's weights as contiguous chunks.
 constexpr int kPrepY = 8;
 __global__ void realign_prep_kernel(uint8_t* tab) {
   const TableHdr* hdr = reinterpret_cast<const TableHdr*>(tab);
   SegDev* segs = reinterpret_cast<SegDev*>(tab + hdr->seg_off);
   const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr->cand_off);
   float2* cs = reinterpret_cast<float2*>(tab + hdr->cs_off);
-  float* wexp = reinterpret_cast<float*>(tab + hdr->wexp_off);
   float* wt = reinterpret_cast<float*>(tab + hdr->wt_off);
-  const int s = blockIdx.x;
-  const SegDev& g = segs[s];
+  const SegDev& g = segs[blockIdx.x];
   const int half = hdr->d / 2;
-  const int tid = blockIdx.y * blockDim.x + threadIdx.x;
-  const int nthr = gridDim.y * blockDim.x;
   if (g.delta != 0 && blockIdx.y == 0) {
     for (int f = threadIdx.x; f < half; f += blockDim.x) {
       double sn, cn;
@@ -113,68 +110,60 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
     }
   }
   if (g.n_cand == 0) return;
-  if (g.uw) {
-    const int rpt = hdr->rows_per_tile;
-    const int rw = weight_row_stride(hdr->d);
-    const int64_t n = int64_t(g.tiles) * g.n_cand * rw;
-    for (int64_t x = tid; x < n; x += nthr) {
-      const int r = int(x % rw);
-      const int64_t tj = x / rw;
-      const int j = int(tj % g.n_cand);
-      const int row = int(tj / g.n_cand) * rpt + r;
-      const int slot = cand[g.cand_off + j];
-      float w = 0.f;
-      if (r < rpt && row < g.L_seg) w = g.w_by_slot ? g.w[int64_t(slot) * g.ld_w + row] : g.wbar[slot];
-      wt[g.wt_off + x] = w;
-    }
-  } else if (!g.w_by_slot) {
-    const int ld = int(g.ld_w);
-    for (int x = tid; x < g.n_cand * ld; x += nthr) {
-      const int j = x / ld;
-      wexp[g.wexp_off + x] = g.wbar[cand[g.cand_off + j]];
-    }
+  const int rpu = unit_rows(hdr->d, g.fp8);
+  const int rw = weight_row_stride(rpu);
+  const int64_t n = int64_t(g.tiles) * g.n_cand * rw;
+  for (int64_t x = blockIdx.y * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.y) * blockDim.x) {
+    const int r = int(x % rw);
+    const int64_t tj = x / rw;
+    const int j = int(tj % g.n_cand);
+    const int row = int(tj / g.n_cand) * rpu + r;
+    const int slot = cand[g.cand_off + j];
+    float w = 0.f;
+    if (r < rpu && row < g.L_seg) w = g.w_by_slot ? g.w[int64_t(slot) * g.ld_w + row] : g.wbar[slot];
+    wt[g.wt_off + x] = w;
   }
 }
 
-// One pipeline stage of an fp8 pool: NA anchor blocks (codes, then row scales); every
-// thread's item is one 16-byte chunk of a row (8 codes of the first half of the row and
-// the matching 8 of the second half, stored interleaved), so a warp's loads are
-// contiguous and conflict-free.  Decode: F2FP (e4m3x2 -> f16x2, exact) + HADD2.F32
-// (f16 -> f32, exact), then packed FFMA2 with weight x row scale.  (An all-integer
-// decode with 2^120 folded into the weight measured 15 % slower: it loads the ALU pipe.)
-template <int NA, int NI>
-__device__ __forceinline__ void fp8_stage(float (&acc)[NI][16], const uint8_t* buf, const float* wv, int rw,
-                                          int fblk, int scale_off, const int (&irow)[NI], const int (&ivec)[NI],
-                                          int d) {
-  float w[NA][NI];
-  uint4 code[NA][NI];
+// One anchor tile of an fp8 pool: kSub 64-row halves of a 2x64-row block (codes, then
+// row scales); every thread's item is one 16-byte chunk of a row (8 codes of the
+// first half of the row and the matching 8 of the second half, stored interleaved),
+// so a warp's loads are contiguous and conflict-free.  Decode: F2FP (e4m3x2 -> f16x2,
+// exact) + HADD2.F32 (f16 -> f32, exact), then packed FFMA2 with weight x row scale.
+// (An all-integer decode with 2^120 folded into the weight measured 15 % slower: it
+// loads the ALU pipe.)
+template <int NI>
+__device__ __forceinline__ void fp8_anchor(float (&acc)[2][NI][16], const uint8_t* blk, const float* wv, int rpt,
+                                           const int (&irow)[NI], const int (&ivec)[NI], int d) {
+  const float* scl = reinterpret_cast<const float*>(blk + 2 * rpt * d);
+  float w[2][NI];
+  uint4 code[2][NI];
 #pragma unroll
-  for (int a = 0; a < NA; ++a) {
-    const uint8_t* ab = buf + a * fblk;
-    const float* scl = reinterpret_cast<const float*>(ab + scale_off);
+  for (int s = 0; s < 2; ++s)
 #pragma unroll
     for (int q = 0; q < NI; ++q) {
-      w[a][q] = wv[a * rw + irow[q]] * scl[irow[q]];  // weight x row scale
-      code[a][q] = lds128(ab + irow[q] * d + ivec[q] * 16);
+      const int row = s * rpt + irow[q];
+      w[s][q] = wv[row] * scl[row];  // weight x row scale
+      code[s][q] = lds128(blk + row * d + ivec[q] * 16);
     }
-  }
 #pragma unroll
-  for (int a = 0; a < NA; ++a)
+  for (int s = 0; s < 2; ++s)
 #pragma unroll
     for (int q = 0; q < NI; ++q) {
-      const uint32_t cw[4] = {code[a][q].x, code[a][q].y, code[a][q].z, code[a][q].w};
+      const uint32_t cw[4] = {code[s][q].x, code[s][q].y, code[s][q].z, code[s][q].w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {  // word t: elements 4t..4t+3 of the item's 16
         float f[4];
         e4m3x4_to_float(cw[t], f);
-        ffma2(acc[q][4 * t], acc[q][4 * t + 1], w[a][q], w[a][q], f[0], f[1]);
-        ffma2(acc[q][4 * t + 2], acc[q][4 * t + 3], w[a][q], w[a][q], f[2], f[3]);
+        ffma2(acc[s][q][4 * t], acc[s][q][4 * t + 1], w[s][q], w[s][q], f[0], f[1]);
+        ffma2(acc[s][q][4 * t + 2], acc[s][q][4 * t + 3], w[s][q], w[s][q], f[2], f[3]);
       }
     }
 }
 
 // variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
-// of the TMA bulk store; bit1 = skip output stores (bandwidth probe only, wrong results).
+// of the TMA bulk store; bit1 = skip output stores; bit5 = skip the anchor math
+// (bit1/bit5: bandwidth probes only, wrong results).
 // kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread) + one
 // producer warp.
 template <int kConsumerWarps>
@@ -188,9 +177,8 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const float2* cs = reinterpret_cast<const float2*>(tab + hdr.cs_off);
 
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sdata = smem;                                                    // [kNStage][kStageStride]
-  float* sw = reinterpret_cast<float*>(smem + size_t(kNStage) * kStageStride);  // [kNStage][kStageWBytes/4]
-  float* suw = sw + size_t(kNStage) * (kStageWBytes / 4);                   // [2][kUnitWBytes/4]
+  uint8_t* sdata = smem;                                                       // [kNStage][kStageStride]
+  float* suw = reinterpret_cast<float*>(smem + size_t(kNStage) * kStageStride);  // [2][kUnitWBytes/4]
   uint64_t* full = reinterpret_cast<uint64_t*>(suw + 2 * (kUnitWBytes / 4));
   uint64_t* empty = full + kNStage;
   uint64_t* uw_full = empty + kNStage;
@@ -214,7 +202,6 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const int d = hdr.d;
   const int Hs = hdr.Hs;
   const int rpt = hdr.rows_per_tile;
-  const int rw = weight_row_stride(d);
   const int fblk = fp8_block_bytes(d);
   const int64_t total = hdr.total_units;
   const int row_bytes = 2 * d;
@@ -232,59 +219,48 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
         const SegDev& g = segs[un.s];
         if (!seg_open(hdr, cand, g)) continue;
-        const int i0 = un.t * rpt;
-        const int nrows = min(rpt, g.L_seg - i0);
-        const uint32_t bytes = uint32_t(nrows) * row_bytes;
-        const uint32_t wbytes = (uint32_t(nrows) * 4u + 15u) & ~15u;
+        const int rpu = unit_rows(d, g.fp8);
+        const int i0 = un.t * rpu;
+        const int nrows = min(rpu, g.L_seg - i0);
         const int64_t lh = int64_t(un.l) * Hs + un.h;
-        if (g.uw) {  // the unit's weights: one block for all its anchors
+        const int rw = weight_row_stride(rpu);
+        const int chunk = kUnitWBytes / (rw * 4);  // anchors per weight chunk
+        const float* wt = g.wt + int64_t(un.t) * g.n_cand * rw;
+        const uint8_t* blk0 = reinterpret_cast<const uint8_t*>(g.off) + int64_t(un.p) * g.plane_stride +
+                              lh * g.off_ld + int64_t(un.t) * fblk;  // fp8 pools
+        for (int c0 = 0; c0 < g.n_cand; c0 += chunk) {
+          const int c1 = min(g.n_cand, c0 + chunk);
           mbar_wait(&uw_empty[ub], uphase ^ 1u);
-          const uint32_t ubytes = uint32_t(g.n_cand * rw) * 4u;
-          mbar_arrive_expect_tx(&uw_full[ub], ubytes);
-          bulk_g2s(suw + ub * (kUnitWBytes / 4), g.wt + int64_t(un.t) * g.n_cand * rw, ubytes, &uw_full[ub],
-                   pol_stream);
+          const uint32_t wbytes = uint32_t((c1 - c0) * rw) * 4u;
+          mbar_arrive_expect_tx(&uw_full[ub], wbytes);
+          bulk_g2s(suw + ub * (kUnitWBytes / 4), wt + int64_t(c0) * rw, wbytes, &uw_full[ub], pol_stream);
           if (++ub == 2) { ub = 0; uphase ^= 1u; }
-        }
-        if (g.fp8) {
-          // one block (codes + row scales) per anchor, two anchors per stage
-          const uint8_t* blk0 = reinterpret_cast<const uint8_t*>(g.off) + int64_t(un.p) * g.plane_stride +
-                                lh * g.off_ld + int64_t(un.t) * fblk;
-          const float* w0 = g.w + i0;
-          for (int c = 0; c < g.n_cand; c += 2) {
+          for (int c = c0; c < c1; ++c) {
             mbar_wait(&empty[stage], phase ^ 1u);
-            const int na = min(2, g.n_cand - c);
+            const int slot = cand[g.cand_off + c];
             uint8_t* dst = sdata + size_t(stage) * kStageStride;
-            float* swst = sw + size_t(stage) * (kStageWBytes / 4);
-            mbar_arrive_expect_tx(&full[stage], uint32_t(na) * (fblk + (g.uw ? 0u : wbytes)));
-            for (int a = 0; a < na; ++a) {
-              const int slot = cand[g.cand_off + c + a];
-              bulk_g2s(dst + a * fblk, blk0 + int64_t(slot) * g.slot_stride, fblk, &full[stage], pol_stream);
-              if (!g.uw)
-                bulk_g2s(swst + a * rw, w0 + int64_t(g.w_by_slot ? slot : c + a) * g.ld_w, wbytes, &full[stage],
-                         pol_stream);
+            if (g.fp8) {
+              mbar_arrive_expect_tx(&full[stage], uint32_t(fblk));
+              bulk_g2s(dst, blk0 + int64_t(slot) * g.slot_stride, uint32_t(fblk), &full[stage], pol_stream);
+            } else {
+              const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
+                                (lh * g.off_ld + i0) * d;
+              const uint32_t bytes = uint32_t(nrows) * row_bytes;
+              mbar_arrive_expect_tx(&full[stage], bytes);
+              bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
             }
             if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           }
-        } else {
-          for (int c = 0; c < g.n_cand; ++c) {
-            mbar_wait(&empty[stage], phase ^ 1u);
-            const int slot = cand[g.cand_off + c];
-            const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
-                              (lh * g.off_ld + i0) * d;
-            mbar_arrive_expect_tx(&full[stage], bytes + (g.uw ? 0u : wbytes));
-            bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage], pol_stream);
-            if (!g.uw)
-              bulk_g2s(sw + size_t(stage) * (kStageWBytes / 4), g.w + int64_t(g.w_by_slot ? slot : c) * g.ld_w + i0,
-                       wbytes, &full[stage], pol_stream);
-            if (++stage == kNStage) { stage = 0; phase ^= 1u; }
-          }
         }
-        mbar_wait(&empty[stage], phase ^ 1u);
-        const bf16* src = g.base[un.p] + (lh * g.base_ld + i0) * d;
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage],
-                 g.group_size > 1 ? pol_shared : pol_stream);
-        if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+        for (int r0 = 0; r0 < nrows; r0 += rpt) {  // base tile(s)
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const bf16* src = g.base[un.p] + (lh * g.base_ld + i0 + r0) * d;
+          const uint32_t bytes = uint32_t(min(rpt, nrows - r0)) * row_bytes;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage],
+                   g.group_size > 1 ? pol_shared : pol_stream);
+          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+        }
       }
     }
     return;
@@ -306,142 +282,149 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
     const SegDev& g = segs[un.s];
     if (!seg_open(hdr, cand, g)) continue;
-    const int i0 = un.t * rpt;
-    const int nrows = min(rpt, g.L_seg - i0);
-    float acc[kItemsPerThread][16];
+    const int rpu = unit_rows(d, g.fp8);
+    const int i0 = un.t * rpu;
+    const int nrows = min(rpu, g.L_seg - i0);
+    const int rw = weight_row_stride(rpu);
+    const int chunk = kUnitWBytes / (rw * 4);
+    float acc[2][kItemsPerThread][16];  // [64-row tile of the unit][item][element]
 #pragma unroll
-    for (int q = 0; q < kItemsPerThread; ++q)
+    for (int s = 0; s < 2; ++s)
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc[q][e] = 0.f;
+      for (int q = 0; q < kItemsPerThread; ++q)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[s][q][e] = 0.f;
 
     const int n_cand = g.n_cand;
-    const float* uwb = suw + ub * (kUnitWBytes / 4);
-    if (g.uw) mbar_wait(&uw_full[ub], uphase);
-    if (g.fp8) {
-      for (int c = 0; c < n_cand; c += 2) {
+    for (int c0 = 0; c0 < n_cand; c0 += chunk) {
+      const int c1 = min(n_cand, c0 + chunk);
+      mbar_wait(&uw_full[ub], uphase);
+      const float* wv = suw + ub * (kUnitWBytes / 4);
+      for (int c = c0; c < c1; ++c, wv += rw) {
         mbar_wait(&full[stage], phase);
         const uint8_t* buf = sdata + size_t(stage) * kStageStride;
-        const float* wv = g.uw ? uwb + c * rw : sw + size_t(stage) * (kStageWBytes / 4);
-        if (n_cand - c >= 2)
-          fp8_stage<2, kItemsPerThread>(acc, buf, wv, rw, fblk, rpt * d, irow, ivec, d);
-        else
-          fp8_stage<1, kItemsPerThread>(acc, buf, wv, rw, fblk, rpt * d, irow, ivec, d);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == kNStage) { stage = 0; phase ^= 1u; }
-      }
-    } else {
-      for (int c = 0; c < n_cand; ++c) {
-        mbar_wait(&full[stage], phase);
-        const uint8_t* buf = sdata + size_t(stage) * kStageStride;
-        const float* wv = g.uw ? uwb + c * rw : sw + size_t(stage) * (kStageWBytes / 4);
+        if (variant & 32) {
+        } else if (g.fp8) {
+          fp8_anchor<kItemsPerThread>(acc, buf, wv, rpt, irow, ivec, d);
+        } else {
 #pragma unroll
-        for (int q = 0; q < kItemsPerThread; ++q) {
-          const float w = wv[irow[q]];
-          const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
-          const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
-          const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-          const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+          for (int q = 0; q < kItemsPerThread; ++q) {
+            const float w = wv[irow[q]];
+            const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
+            const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+            const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+            const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc[q][2 * e] = fmaf(w, bf_lo(av[e]), acc[q][2 * e]);
-            acc[q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[q][2 * e + 1]);
-            acc[q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[q][8 + 2 * e]);
-            acc[q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[q][8 + 2 * e + 1]);
+            for (int e = 0; e < 4; ++e) {
+#if KVC_BF16_FFMA2
+              ffma2(acc[0][q][2 * e], acc[0][q][2 * e + 1], w, w, bf_lo(av[e]), bf_hi(av[e]));
+              ffma2(acc[0][q][8 + 2 * e], acc[0][q][8 + 2 * e + 1], w, w, bf_lo(bv[e]), bf_hi(bv[e]));
+#else
+              acc[0][q][2 * e] = fmaf(w, bf_lo(av[e]), acc[0][q][2 * e]);
+              acc[0][q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[0][q][2 * e + 1]);
+              acc[0][q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[0][q][8 + 2 * e]);
+              acc[0][q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[0][q][8 + 2 * e + 1]);
+#endif
+            }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
-    }
-    if (g.uw) {  // unit weight buffer free for the producer's unit after next
-      __syncwarp();
+      __syncwarp();  // weight chunk consumed
       if (lane == 0) mbar_arrive(&uw_empty[ub]);
       if (++ub == 2) { ub = 0; uphase ^= 1u; }
     }
 
-    // base tile: add, rotate (K), round, store
-    mbar_wait(&full[stage], phase);
-    uint8_t* buf = sdata + size_t(stage) * kStageStride;
+    // base tile(s): add, rotate (K), round, store
     const int64_t lh = int64_t(un.l) * Hs + un.h;
     const bool rotate = un.p == 0 && g.delta != 0;
-    if (n_cand > 0 || rotate) {  // COPY segments leave the staged rows untouched (bit-exact)
 #pragma unroll
-      for (int q = 0; q < kItemsPerThread; ++q) {
-        if (irow[q] >= nrows) continue;
-        uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
-        uint8_t* pb = pa + d;
-        const uint4 a = lds128(pa);
-        const uint4 b = lds128(pb);
-        const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-        const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
-        float y0[8], y1[8];
+    for (int s = 0; s < 2; ++s) {
+      const int r0 = s * rpt;
+      if (r0 >= nrows) break;
+      const int srows = min(rpt, nrows - r0);
+      mbar_wait(&full[stage], phase);
+      uint8_t* buf = sdata + size_t(stage) * kStageStride;
+      if (n_cand > 0 || rotate) {  // COPY segments leave the staged rows untouched (bit-exact)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          y0[2 * e] = bf_lo(av[e]) + acc[q][2 * e];
-          y0[2 * e + 1] = bf_hi(av[e]) + acc[q][2 * e + 1];
-          y1[2 * e] = bf_lo(bv[e]) + acc[q][8 + 2 * e];
-          y1[2 * e + 1] = bf_hi(bv[e]) + acc[q][8 + 2 * e + 1];
-        }
-        if (rotate) {
-          const float2* csr = cs + g.cs_off + ivec[q] * 8;
+        for (int q = 0; q < kItemsPerThread; ++q) {
+          if (irow[q] >= srows) continue;
+          uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
+          uint8_t* pb = pa + d;
+          const uint4 a = lds128(pa);
+          const uint4 b = lds128(pb);
+          const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+          const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+          float y0[8], y1[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float2 r = csr[e];
-            const float x0 = y0[e], x1 = y1[e];
-            y0[e] = x0 * r.x - x1 * r.y;
-            y1[e] = x1 * r.x + x0 * r.y;
+          for (int e = 0; e < 4; ++e) {
+            y0[2 * e] = bf_lo(av[e]) + acc[s][q][2 * e];
+            y0[2 * e + 1] = bf_hi(av[e]) + acc[s][q][2 * e + 1];
+            y1[2 * e] = bf_lo(bv[e]) + acc[s][q][8 + 2 * e];
+            y1[2 * e + 1] = bf_hi(bv[e]) + acc[s][q][8 + 2 * e + 1];
+          }
+          if (rotate) {
+            const float2* csr = cs + g.cs_off + ivec[q] * 8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float2 r = csr[e];
+              const float x0 = y0[e], x1 = y1[e];
+              y0[e] = x0 * r.x - x1 * r.y;
+              y1[e] = x1 * r.x + x0 * r.y;
+            }
+          }
+          const uint4 o0 = make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),
+                                      pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7]));
+          const uint4 o1 = make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
+                                      pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7]));
+          const int row = i0 + r0 + irow[q];
+          if (tma_store) {
+            sts128(pa, o0);  // in place; the whole tile leaves with one bulk store below
+            sts128(pb, o1);
+          } else if (!(variant & 2)) {
+            bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + row) * d + ivec[q] * 8;
+            stg128_cs(o, o0);
+            stg128_cs(o + d / 2, o1);
+          }
+          if (g.dbg[un.p] != nullptr) {
+            float* od = g.dbg[un.p] + (lh * g.L_seg + row) * d + ivec[q] * 8;
+            float4* p0 = reinterpret_cast<float4*>(od);
+            float4* p1 = reinterpret_cast<float4*>(od + d / 2);
+            p0[0] = make_float4(acc[s][q][0], acc[s][q][1], acc[s][q][2], acc[s][q][3]);
+            p0[1] = make_float4(acc[s][q][4], acc[s][q][5], acc[s][q][6], acc[s][q][7]);
+            p1[0] = make_float4(acc[s][q][8], acc[s][q][9], acc[s][q][10], acc[s][q][11]);
+            p1[1] = make_float4(acc[s][q][12], acc[s][q][13], acc[s][q][14], acc[s][q][15]);
           }
         }
-        const uint4 r0 = make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),
-                                    pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7]));
-        const uint4 r1 = make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
-                                    pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7]));
-        if (tma_store) {
-          sts128(pa, r0);  // in place; the whole tile leaves with one bulk store below
-          sts128(pb, r1);
-        } else if (!(variant & 2)) {
-          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + irow[q]) * d + ivec[q] * 8;
-          stg128_cs(o, r0);
-          stg128_cs(o + d / 2, r1);
-        }
-        if (g.dbg[un.p] != nullptr) {
-          float* od = g.dbg[un.p] + (lh * g.L_seg + i0 + irow[q]) * d + ivec[q] * 8;
-          float4* o0 = reinterpret_cast<float4*>(od);
-          float4* o1 = reinterpret_cast<float4*>(od + d / 2);
-          o0[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-          o0[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
-          o1[0] = make_float4(acc[q][8], acc[q][9], acc[q][10], acc[q][11]);
-          o1[1] = make_float4(acc[q][12], acc[q][13], acc[q][14], acc[q][15]);
-        }
-      }
-    } else if (!tma_store && !(variant & 2)) {
+      } else if (!tma_store && !(variant & 2)) {
 #pragma unroll
-      for (int q = 0; q < kItemsPerThread; ++q) {
-        if (irow[q] >= nrows) continue;
-        const uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
-        bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + irow[q]) * d + ivec[q] * 8;
-        stg128_cs(o, lds128(pa));
-        stg128_cs(o + d / 2, lds128(pa + d));
+        for (int q = 0; q < kItemsPerThread; ++q) {
+          if (irow[q] >= srows) continue;
+          const uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
+          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + r0 + irow[q]) * d + ivec[q] * 8;
+          stg128_cs(o, lds128(pa));
+          stg128_cs(o + d / 2, lds128(pa + d));
+        }
       }
-    }
-    if (tma_store) {
-      // all consumer writes of the tile -> visible to the async proxy, then one bulk store;
-      // the stage is released only once the store has finished reading shared memory
-      fence_proxy_async_smem();
-      named_bar_sync(kConsumerBar, kConsumerWarps * 32);
-      if (threadIdx.x == 0) {
-        bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
-        bulk_s2g(o, buf, uint32_t(nrows) * row_bytes);
-        bulk_wait_read_all();
-        mbar_arrive_cnt(&empty[stage], kConsumerWarps);
+      if (tma_store) {
+        // all consumer writes of the tile -> visible to the async proxy, then one bulk store;
+        // the stage is released only once the store has finished reading shared memory
+        fence_proxy_async_smem();
+        named_bar_sync(kConsumerBar, kConsumerWarps * 32);
+        if (threadIdx.x == 0) {
+          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + r0) * d;
+          bulk_s2g(o, buf, uint32_t(srows) * row_bytes);
+          bulk_wait_read_all();
+          mbar_arrive_cnt(&empty[stage], kConsumerWarps);
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
       }
-    } else {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kNStage) { stage = 0; phase ^= 1u; }
     }
-    if (++stage == kNStage) { stage = 0; phase ^= 1u; }
   }
   if (tma_store && threadIdx.x == 0) bulk_wait_all();  // global writes complete before exit
 }
@@ -472,6 +455,7 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
     const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
     if (c && atoi(c) == 16) cw = 16;
   }
+  if (hdr.n_seg <= 0) return cudaSuccess;
   realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
