@@ -240,8 +240,16 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             const int slot = cand[g.cand_off + c];
             uint8_t* dst = sdata + size_t(stage) * kStageStride;
             if (g.fp8) {
-              mbar_arrive_expect_tx(&full[stage], uint32_t(fblk));
-              bulk_g2s(dst, blk0 + int64_t(slot) * g.slot_stride, uint32_t(fblk), &full[stage], pol_stream);
+              const uint8_t* src = blk0 + int64_t(slot) * g.slot_stride;
+              if (nrows == rpu) {  // whole block: one copy
+                mbar_arrive_expect_tx(&full[stage], uint32_t(fblk));
+                bulk_g2s(dst, src, uint32_t(fblk), &full[stage], pol_stream);
+              } else {             // tail tile: only its rows' codes and scales
+                const uint32_t cb = (uint32_t(nrows * d) + 15u) & ~15u, sb = (uint32_t(nrows) * 4u + 15u) & ~15u;
+                mbar_arrive_expect_tx(&full[stage], cb + sb);
+                bulk_g2s(dst, src, cb, &full[stage], pol_stream);
+                bulk_g2s(dst + rpu * d, src + rpu * d, sb, &full[stage], pol_stream);
+              }
             } else {
               const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
                                 (lh * g.off_ld + i0) * d;
