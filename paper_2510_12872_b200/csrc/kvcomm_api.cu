@@ -755,6 +755,7 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   size_t n_ints = 0, n_wt = 0;
   for (const HostSeg& g : hs) {
     n_ints += g.x.n_cand + g.gates.size();
+    if (g.x.fp8) L.hdr.any_fp8 = 1;
     const int rpu = unit_rows(d, g.x.fp8);
     n_wt += size_t((g.x.L_seg + rpu - 1) / rpu) * g.x.n_cand * weight_row_stride(rpu);
   }

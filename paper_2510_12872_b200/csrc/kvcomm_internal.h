@@ -12,7 +12,10 @@ using bf16 = __nv_bfloat16;
 // rows of one (layer, head, K|V) plane): 16 KiB = 64 rows of d=128 bf16.
 constexpr int kStageBytes = 16384;
 constexpr int kStageStride = kStageBytes + 1024;  // an fp8 block (codes + row scales) fits too
-constexpr int kUnitWBytes = 16384;  // weight chunk buffer: [anchors][weight_row_stride] floats
+#ifndef KVC_UNITW
+#define KVC_UNITW 16384
+#endif
+constexpr int kUnitWBytes = KVC_UNITW;  // weight chunk buffer: [anchors][weight_row_stride] floats
 constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
 constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
 
@@ -64,7 +67,7 @@ struct MatchResultDev {
 // Device-side work table for one realign launch (lives in one contiguous buffer).
 struct TableHdr {
   int32_t n_seg, d, Ls, Hs;
-  int32_t rows_per_tile, _pad0;
+  int32_t rows_per_tile, any_fp8;  // any_fp8: some segment reads an fp8 pool
   int64_t total_units;
   // byte offsets from the table base
   int64_t seg_off, cand_off, cs_off, wt_off;

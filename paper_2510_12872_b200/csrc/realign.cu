@@ -13,7 +13,8 @@
 //     weights [n_cand][rows] in chunks of up to 16 KiB (one copy each, double
 //     buffered), then the anchor tiles (one contiguous copy per anchor: bf16 rows, or
 //     an fp8 block of e4m3 codes followed by their row scales) and finally the base
-//     tile(s) into an 11-deep shared-memory ring with cp.async.bulk (UBLKCP) + mbarrier
+//     tile(s) into a 9-deep shared-memory ring (9 measured 3 % faster than 11: fewer
+//     bytes in flight, less DRAM contention) with cp.async.bulk (UBLKCP) + mbarrier
 //     complete_tx, L2 evict-first;
 //   * warps 0-7 consume: each thread owns two 32-byte "items" per 64-row tile (8
 //     elements of the first half of a row and the matching 8 of the second half, so
@@ -32,12 +33,13 @@
 
 namespace kvc {
 
-constexpr int kNStage = 11;
+#ifndef KVC_NSTAGE
+#define KVC_NSTAGE 9
+#endif
+constexpr int kNStage = KVC_NSTAGE;
 constexpr int kItems = kStageBytes / 32;  // 512 items of 32 B per 16 KiB bf16 tile
 constexpr int kConsumerBar = 1;           // named barrier id (consumers only)
-#ifndef KVC_BF16_FFMA2
-#define KVC_BF16_FFMA2 1
-#endif
+
 
 constexpr size_t realign_smem_bytes() {
   return size_t(kNStage) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * kNStage + 4) * sizeof(uint64_t);
@@ -125,27 +127,31 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
   }
 }
 
-// One anchor tile of an fp8 pool: kSub 64-row halves of a 2x64-row block (codes, then
-// row scales); every thread's item is one 16-byte chunk of a row (8 codes of the
-// first half of the row and the matching 8 of the second half, stored interleaved),
-// so a warp's loads are contiguous and conflict-free.  Decode: F2FP (e4m3x2 -> f16x2,
-// exact) + HADD2.F32 (f16 -> f32, exact), then packed FFMA2 with weight x row scale.
-// (An all-integer decode with 2^120 folded into the weight measured 15 % slower: it
-// loads the ALU pipe.)
+// One anchor tile of an fp8 pool: two 64-row tiles of a block (codes, then row scales);
+// every thread's item is one 16-byte chunk of a row (8 codes of the first half of the
+// row and the matching 8 of the second half, stored interleaved), so a warp's loads are
+// contiguous and conflict-free.  fp8_load pulls a thread's codes and weight x row scale
+// into registers (the stage can be released right after), fp8_accum decodes with F2FP
+// (e4m3x2 -> f16x2, exact) + HADD2.F32 (f16 -> f32, exact) and accumulates with packed
+// FFMA2.  (An all-integer decode with 2^120 folded into the weight measured 15 % slower:
+// it loads the ALU pipe.)
 template <int NI>
-__device__ __forceinline__ void fp8_anchor(float (&acc)[2][NI][16], const uint8_t* blk, const float* wv, int rpt,
-                                           const int (&irow)[NI], const int (&ivec)[NI], int d) {
-  const float* scl = reinterpret_cast<const float*>(blk + 2 * rpt * d);
-  float w[2][NI];
-  uint4 code[2][NI];
+__device__ __forceinline__ void fp8_load(float (&w)[2][NI], uint4 (&code)[2][NI], const uint8_t* blk,
+                                         const uint8_t* wv, const uint8_t* scl, const int (&coff)[2][NI],
+                                         const int (&roff)[2][NI]) {
 #pragma unroll
   for (int s = 0; s < 2; ++s)
 #pragma unroll
     for (int q = 0; q < NI; ++q) {
-      const int row = s * rpt + irow[q];
-      w[s][q] = wv[row] * scl[row];  // weight x row scale
-      code[s][q] = lds128(blk + row * d + ivec[q] * 16);
+      // weight x row scale
+      w[s][q] = *reinterpret_cast<const float*>(wv + roff[s][q]) * *reinterpret_cast<const float*>(scl + roff[s][q]);
+      code[s][q] = lds128(blk + coff[s][q]);
     }
+}
+
+template <int NI>
+__device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (&w)[2][NI],
+                                          const uint4 (&code)[2][NI]) {
 #pragma unroll
   for (int s = 0; s < 2; ++s)
 #pragma unroll
@@ -219,54 +225,58 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
         const SegDev& g = segs[un.s];
         if (!seg_open(hdr, cand, g)) continue;
-        const int rpu = unit_rows(d, g.fp8);
+        // segment fields -> registers (the barrier asm's memory clobbers would reload them)
+        const bool fp8 = g.fp8;
+        const int n_cand = g.n_cand;
+        const int* cands = cand + g.cand_off;
+        const int rpu = unit_rows(d, fp8);
         const int i0 = un.t * rpu;
         const int nrows = min(rpu, g.L_seg - i0);
         const int64_t lh = int64_t(un.l) * Hs + un.h;
         const int rw = weight_row_stride(rpu);
         const int chunk = kUnitWBytes / (rw * 4);  // anchors per weight chunk
-        const float* wt = g.wt + int64_t(un.t) * g.n_cand * rw;
-        const uint8_t* blk0 = reinterpret_cast<const uint8_t*>(g.off) + int64_t(un.p) * g.plane_stride +
-                              lh * g.off_ld + int64_t(un.t) * fblk;  // fp8 pools
-        for (int c0 = 0; c0 < g.n_cand; c0 += chunk) {
-          const int c1 = min(g.n_cand, c0 + chunk);
+        const float* wt = g.wt + int64_t(un.t) * n_cand * rw;
+        // anchor tile of slot s at anchor0 + s * slot_bytes
+        const uint8_t* anchor0 = fp8 ? reinterpret_cast<const uint8_t*>(g.off) + int64_t(un.p) * g.plane_stride +
+                                           lh * g.off_ld + int64_t(un.t) * fblk
+                                     : reinterpret_cast<const uint8_t*>(g.off + int64_t(un.p) * g.plane_stride +
+                                                                        (lh * g.off_ld + i0) * d);
+        const int64_t slot_bytes = fp8 ? g.slot_stride : g.slot_stride * int64_t(sizeof(bf16));
+        const uint32_t full_bytes = fp8 ? uint32_t(fblk) : uint32_t(nrows) * row_bytes;
+        const bool split = fp8 && nrows < rpu;  // fp8 tail tile: only its rows' codes and scales
+        const uint32_t cb = (uint32_t(nrows * d) + 15u) & ~15u, sb = (uint32_t(nrows) * 4u + 15u) & ~15u;
+        const bf16* base = g.base[un.p] + (lh * g.base_ld + i0) * d;
+        const uint64_t pol_base = g.group_size > 1 ? pol_shared : pol_stream;
+        int slot = n_cand > 0 ? cands[0] : 0;
+        for (int c0 = 0; c0 < n_cand; c0 += chunk) {
+          const int c1 = min(n_cand, c0 + chunk);
           mbar_wait(&uw_empty[ub], uphase ^ 1u);
           const uint32_t wbytes = uint32_t((c1 - c0) * rw) * 4u;
           mbar_arrive_expect_tx(&uw_full[ub], wbytes);
           bulk_g2s(suw + ub * (kUnitWBytes / 4), wt + int64_t(c0) * rw, wbytes, &uw_full[ub], pol_stream);
           if (++ub == 2) { ub = 0; uphase ^= 1u; }
           for (int c = c0; c < c1; ++c) {
+            const int next = c + 1 < n_cand ? cands[c + 1] : 0;  // in flight during the wait
             mbar_wait(&empty[stage], phase ^ 1u);
-            const int slot = cand[g.cand_off + c];
             uint8_t* dst = sdata + size_t(stage) * kStageStride;
-            if (g.fp8) {
-              const uint8_t* src = blk0 + int64_t(slot) * g.slot_stride;
-              if (nrows == rpu) {  // whole block: one copy
-                mbar_arrive_expect_tx(&full[stage], uint32_t(fblk));
-                bulk_g2s(dst, src, uint32_t(fblk), &full[stage], pol_stream);
-              } else {             // tail tile: only its rows' codes and scales
-                const uint32_t cb = (uint32_t(nrows * d) + 15u) & ~15u, sb = (uint32_t(nrows) * 4u + 15u) & ~15u;
-                mbar_arrive_expect_tx(&full[stage], cb + sb);
-                bulk_g2s(dst, src, cb, &full[stage], pol_stream);
-                bulk_g2s(dst + rpu * d, src + rpu * d, sb, &full[stage], pol_stream);
-              }
+            const uint8_t* src = anchor0 + int64_t(slot) * slot_bytes;
+            if (!split) {
+              mbar_arrive_expect_tx(&full[stage], full_bytes);
+              bulk_g2s(dst, src, full_bytes, &full[stage], pol_stream);
             } else {
-              const bf16* src = g.off + int64_t(slot) * g.slot_stride + int64_t(un.p) * g.plane_stride +
-                                (lh * g.off_ld + i0) * d;
-              const uint32_t bytes = uint32_t(nrows) * row_bytes;
-              mbar_arrive_expect_tx(&full[stage], bytes);
-              bulk_g2s(dst, src, bytes, &full[stage], pol_stream);
+              mbar_arrive_expect_tx(&full[stage], cb + sb);
+              bulk_g2s(dst, src, cb, &full[stage], pol_stream);
+              bulk_g2s(dst + rpu * d, src + rpu * d, sb, &full[stage], pol_stream);
             }
+            slot = next;
             if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           }
         }
         for (int r0 = 0; r0 < nrows; r0 += rpt) {  // base tile(s)
           mbar_wait(&empty[stage], phase ^ 1u);
-          const bf16* src = g.base[un.p] + (lh * g.base_ld + i0 + r0) * d;
           const uint32_t bytes = uint32_t(min(rpt, nrows - r0)) * row_bytes;
           mbar_arrive_expect_tx(&full[stage], bytes);
-          bulk_g2s(sdata + size_t(stage) * kStageStride, src, bytes, &full[stage],
-                   g.group_size > 1 ? pol_shared : pol_stream);
+          bulk_g2s(sdata + size_t(stage) * kStageStride, base + int64_t(r0) * d, bytes, &full[stage], pol_base);
           if (++stage == kNStage) { stage = 0; phase ^= 1u; }
         }
       }
@@ -284,17 +294,35 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     irow[q] = it / vpr;
     ivec[q] = it - irow[q] * vpr;
   }
+  // fp8 blocks: byte offsets of the thread's code chunks and of its rows' weights / scales
+  int coff[2][kItemsPerThread], roff[2][kItemsPerThread];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int q = 0; q < kItemsPerThread; ++q) {
+      coff[s][q] = (s * rpt + irow[q]) * d + ivec[q] * 16;
+      roff[s][q] = (s * rpt + irow[q]) * 4;
+    }
+  const int scale_off = 2 * rpt * d;
   int stage = 0, ub = 0;
   uint32_t phase = 0, uphase = 0;
   for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
     const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
     const SegDev& g = segs[un.s];
     if (!seg_open(hdr, cand, g)) continue;
-    const int rpu = unit_rows(d, g.fp8);
+    // segment fields -> registers (the barrier asm's memory clobbers would reload them)
+    const bool fp8 = g.fp8;
+    const int n_cand = g.n_cand;
+    const int rpu = unit_rows(d, fp8);
     const int i0 = un.t * rpu;
     const int nrows = min(rpu, g.L_seg - i0);
     const int rw = weight_row_stride(rpu);
     const int chunk = kUnitWBytes / (rw * 4);
+    const int64_t lh = int64_t(un.l) * Hs + un.h;
+    const bool rotate = un.p == 0 && g.delta != 0;
+    const float2* csg = cs + g.cs_off;
+    bf16* const dst = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
+    float* const dbg = g.dbg[un.p] != nullptr ? g.dbg[un.p] + (lh * g.L_seg + i0) * d : nullptr;
     float acc[2][kItemsPerThread][16];  // [64-row tile of the unit][item][element]
 #pragma unroll
     for (int s = 0; s < 2; ++s)
@@ -303,7 +331,6 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) acc[s][q][e] = 0.f;
 
-    const int n_cand = g.n_cand;
     for (int c0 = 0; c0 < n_cand; c0 += chunk) {
       const int c1 = min(n_cand, c0 + chunk);
       mbar_wait(&uw_full[ub], uphase);
@@ -311,33 +338,39 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       for (int c = c0; c < c1; ++c, wv += rw) {
         mbar_wait(&full[stage], phase);
         const uint8_t* buf = sdata + size_t(stage) * kStageStride;
-        if (variant & 32) {
-        } else if (g.fp8) {
-          fp8_anchor<kItemsPerThread>(acc, buf, wv, rpt, irow, ivec, d);
+        // operands -> registers, release the stage to the producer, then the math: the
+        // stage is held only for the shared-memory loads (more bytes in flight)
+        if (fp8) {
+          float w[2][kItemsPerThread];
+          uint4 code[2][kItemsPerThread];
+          fp8_load<kItemsPerThread>(w, code, buf, reinterpret_cast<const uint8_t*>(wv), buf + scale_off, coff, roff);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (!(variant & 32)) fp8_accum<kItemsPerThread>(acc, w, code);
         } else {
+          float w[kItemsPerThread];
+          uint4 va[kItemsPerThread], vb[kItemsPerThread];
 #pragma unroll
           for (int q = 0; q < kItemsPerThread; ++q) {
-            const float w = wv[irow[q]];
-            const uint4 a = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
-            const uint4 b = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
-            const uint32_t av[4] = {a.x, a.y, a.z, a.w};
-            const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+            w[q] = wv[irow[q]];
+            va[q] = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
+            vb[q] = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (!(variant & 32)) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-#if KVC_BF16_FFMA2
-              ffma2(acc[0][q][2 * e], acc[0][q][2 * e + 1], w, w, bf_lo(av[e]), bf_hi(av[e]));
-              ffma2(acc[0][q][8 + 2 * e], acc[0][q][8 + 2 * e + 1], w, w, bf_lo(bv[e]), bf_hi(bv[e]));
-#else
-              acc[0][q][2 * e] = fmaf(w, bf_lo(av[e]), acc[0][q][2 * e]);
-              acc[0][q][2 * e + 1] = fmaf(w, bf_hi(av[e]), acc[0][q][2 * e + 1]);
-              acc[0][q][8 + 2 * e] = fmaf(w, bf_lo(bv[e]), acc[0][q][8 + 2 * e]);
-              acc[0][q][8 + 2 * e + 1] = fmaf(w, bf_hi(bv[e]), acc[0][q][8 + 2 * e + 1]);
-#endif
+            for (int q = 0; q < kItemsPerThread; ++q) {
+              const uint32_t av[4] = {va[q].x, va[q].y, va[q].z, va[q].w};
+              const uint32_t bv[4] = {vb[q].x, vb[q].y, vb[q].z, vb[q].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                ffma2(acc[0][q][2 * e], acc[0][q][2 * e + 1], w[q], w[q], bf_lo(av[e]), bf_hi(av[e]));
+                ffma2(acc[0][q][8 + 2 * e], acc[0][q][8 + 2 * e + 1], w[q], w[q], bf_lo(bv[e]), bf_hi(bv[e]));
+              }
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
       __syncwarp();  // weight chunk consumed
@@ -346,8 +379,6 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     }
 
     // base tile(s): add, rotate (K), round, store
-    const int64_t lh = int64_t(un.l) * Hs + un.h;
-    const bool rotate = un.p == 0 && g.delta != 0;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int r0 = s * rpt;
@@ -374,7 +405,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             y1[2 * e + 1] = bf_hi(bv[e]) + acc[s][q][8 + 2 * e + 1];
           }
           if (rotate) {
-            const float2* csr = cs + g.cs_off + ivec[q] * 8;
+            const float2* csr = csg + ivec[q] * 8;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const float2 r = csr[e];
@@ -387,17 +418,17 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
                                       pack_bf16_rn(y0[4], y0[5]), pack_bf16_rn(y0[6], y0[7]));
           const uint4 o1 = make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
                                       pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7]));
-          const int row = i0 + r0 + irow[q];
+          const int row = r0 + irow[q];  // within the unit
           if (tma_store) {
             sts128(pa, o0);  // in place; the whole tile leaves with one bulk store below
             sts128(pb, o1);
           } else if (!(variant & 2)) {
-            bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + row) * d + ivec[q] * 8;
+            bf16* o = dst + int64_t(row) * d + ivec[q] * 8;
             stg128_cs(o, o0);
             stg128_cs(o + d / 2, o1);
           }
-          if (g.dbg[un.p] != nullptr) {
-            float* od = g.dbg[un.p] + (lh * g.L_seg + row) * d + ivec[q] * 8;
+          if (dbg != nullptr) {
+            float* od = dbg + int64_t(row) * d + ivec[q] * 8;
             float4* p0 = reinterpret_cast<float4*>(od);
             float4* p1 = reinterpret_cast<float4*>(od + d / 2);
             p0[0] = make_float4(acc[s][q][0], acc[s][q][1], acc[s][q][2], acc[s][q][3]);
@@ -411,7 +442,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         for (int q = 0; q < kItemsPerThread; ++q) {
           if (irow[q] >= srows) continue;
           const uint8_t* pa = buf + irow[q] * row_bytes + ivec[q] * 16;
-          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + r0 + irow[q]) * d + ivec[q] * 8;
+          bf16* o = dst + int64_t(r0 + irow[q]) * d + ivec[q] * 8;
           stg128_cs(o, lds128(pa));
           stg128_cs(o + d / 2, lds128(pa + d));
         }
@@ -422,8 +453,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         fence_proxy_async_smem();
         named_bar_sync(kConsumerBar, kConsumerWarps * 32);
         if (threadIdx.x == 0) {
-          bf16* o = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0 + r0) * d;
-          bulk_s2g(o, buf, uint32_t(srows) * row_bytes);
+          bulk_s2g(dst + int64_t(r0) * d, buf, uint32_t(srows) * row_bytes);
           bulk_wait_read_all();
           mbar_arrive_cnt(&empty[stage], kConsumerWarps);
         }
@@ -445,7 +475,7 @@ int realign_grid_size(int device) {
 
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
-  static int variant = -1, cw = 8;
+  static int variant = -1, cw_env = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
@@ -461,8 +491,11 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
     const char* v = getenv("KVCOMM_REALIGN_VARIANT");
     variant = v ? atoi(v) : 0;
     const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
-    if (c && atoi(c) == 16) cw = 16;
+    if (c) cw_env = atoi(c);
   }
+  // 8 consumer warps stream bf16 pools at the HBM roofline; the e4m3 decode of fp8
+  // pools issues ~2x the instructions per byte and runs ~4 % faster with 16 (profiles/)
+  const int cw = cw_env == 8 || cw_env == 16 ? cw_env : (hdr.any_fp8 ? 16 : 8);
   if (hdr.n_seg <= 0) return cudaSuccess;
   realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
