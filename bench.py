@@ -486,7 +486,8 @@ def main():
     achieved = alg_bytes / (realign_avg / 1e3) / 1e9
     traffic = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "realign_ncu.json")))
+        name = "realign_ncu.json" if args.offsets == "bf16" else f"realign_ncu_{args.offsets}.json"
+        prof = json.load(open(os.path.join(ROOT, "profiles", name)))
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:  # noqa: BLE001
         pass

@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Summarise gpurun_out/ ncu artefacts into tracked files under profiles/.
 
-  python scripts/summarize_profiles.py <round-tag>
+  python scripts/summarize_profiles.py <round-tag> [suffix]
+
+suffix (e.g. _fp8) selects the files profile_box.sh wrote with TAG=<suffix>.
 
 Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of
 `bench.py --profile`) and gpurun_out/prof_{realign,match}.ncu-rep (ncu --set full),
@@ -35,8 +37,8 @@ def to_us(v, unit):
     return {"ns": v / 1e3, "nsecond": v / 1e3, "us": v, "usecond": v, "ms": v * 1e3, "msecond": v * 1e3}.get(unit, v)
 
 
-def launches(tag):
-    path = os.path.join(OUT, "launches.csv")
+def launches(tag, sfx=""):
+    path = os.path.join(OUT, f"launches{sfx}.csv")
     rows = [r for r in csv.reader(open(path)) if len(r) > 5]
     hdr, data = rows[0], rows[1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
@@ -47,7 +49,7 @@ def launches(tag):
         a[0] += 1
         a[1] += to_us(r[vi], r[ui])
     tot = sum(v[1] for v in agg.values())
-    steps = json.loads(open(os.path.join(OUT, "launches.log")).read().strip().splitlines()[-1]).get("profile_steps", 1)
+    steps = json.loads(open(os.path.join(OUT, f"launches{sfx}.log")).read().strip().splitlines()[-1]).get("profile_steps", 1)
     lines = [f"# {tag}: kernel launch list of `bench.py --profile` ({steps} steps)", "",
              "ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off "
              "(serialised, cold-cache per launch: compare SHARES, not absolutes).", "",
@@ -55,7 +57,7 @@ def launches(tag):
     for n, (c, t) in agg.items():
         lines.append(f"| `{n}` | {c} | {t:.1f} | {t / steps:.1f} | {100 * t / tot:.1f}% |")
     lines.append(f"| **all** | {sum(v[0] for v in agg.values())} | {tot:.1f} | {tot / steps:.1f} | 100% |")
-    open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(PROF, f"{tag}{sfx}_launches.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
@@ -88,8 +90,8 @@ def details(rep):
     return lines
 
 
-def kernel_summary(tag, name):
-    rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
+def kernel_summary(tag, name, sfx=""):
+    rep = os.path.join(OUT, f"prof_{name}{sfx}.ncu-rep")
     if not os.path.exists(rep):
         return None
     rs = raw(rep)
@@ -101,16 +103,17 @@ def kernel_summary(tag, name):
                 lines.append(f"{k:60s} {d[k][0]:>20s} {d[k][1]}")
         lines.append("")
     lines += ["## details", ""] + details(rep)
-    open(os.path.join(PROF, f"{tag}_ncu_{name}.txt"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(PROF, f"{tag}{sfx}_ncu_{name}.txt"), "w").write("\n".join(lines) + "\n")
     return rs
 
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    sfx = sys.argv[2] if len(sys.argv) > 2 else ""
     os.makedirs(PROF, exist_ok=True)
-    launches(tag)
-    rs = kernel_summary(tag, "realign")
-    kernel_summary(tag, "match")
+    launches(tag, sfx)
+    rs = kernel_summary(tag, "realign", sfx)
+    kernel_summary(tag, "match", sfx)
     if rs:
         d = rs[0]
 
@@ -121,10 +124,10 @@ def main():
 
         rd, wr = val("dram__bytes_read.sum", 1), val("dram__bytes_write.sum", 1)
         t_ms = to_us(*d["gpu__time_duration.sum"]) / 1e3
-        js = {"source": f"profiles/{tag}_ncu_realign.txt (ncu --set full, 1 launch, bench.py --profile)",
+        js = {"source": f"profiles/{tag}{sfx}_ncu_realign.txt (ncu --set full, 1 launch, bench.py --profile)",
               "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
               "duration_ms_under_ncu": t_ms, "dram_gbs_under_ncu": (rd + wr) / (t_ms / 1e3) / 1e9}
-        json.dump(js, open(os.path.join(PROF, "realign_ncu.json"), "w"), indent=1)
+        json.dump(js, open(os.path.join(PROF, f"realign_ncu{sfx}.json"), "w"), indent=1)
         print(json.dumps(js, indent=1))
 
 
