@@ -170,6 +170,10 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
 // variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
 // of the TMA bulk store; bit1 = skip output stores; bit5 = skip the anchor math
 // (bit1/bit5: bandwidth probes only, wrong results).
+// Stage release: every consumer thread arrives on the empty barrier itself after its own
+// shared-memory reads (same speed as a warp-elected arrive after __syncwarp, and the
+// ordering is then visible to compute-sanitizer racecheck, which does not model the
+// __syncwarp hand-off).
 // kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread) + one
 // producer warp.
 template <int kConsumerWarps>
@@ -195,11 +199,11 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNStage; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps);
+      mbar_init(&empty[i], kConsumerWarps * 32);  // every consumer thread arrives
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&uw_full[i], 1);
-      mbar_init(&uw_empty[i], kConsumerWarps);
+      mbar_init(&uw_empty[i], kConsumerWarps * 32);
     }
     fence_mbar_init();
   }
@@ -344,8 +348,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           float w[2][kItemsPerThread];
           uint4 code[2][kItemsPerThread];
           fp8_load<kItemsPerThread>(w, code, buf, reinterpret_cast<const uint8_t*>(wv), buf + scale_off, coff, roff);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+          mbar_arrive(&empty[stage]);  // this thread's reads of the stage are done
           if (!(variant & 32)) fp8_accum<kItemsPerThread>(acc, w, code);
         } else {
           float w[kItemsPerThread];
@@ -356,8 +359,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             va[q] = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
             vb[q] = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+          mbar_arrive(&empty[stage]);  // this thread's reads of the stage are done
           if (!(variant & 32)) {
 #pragma unroll
             for (int q = 0; q < kItemsPerThread; ++q) {
@@ -373,8 +375,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         }
         if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
-      __syncwarp();  // weight chunk consumed
-      if (lane == 0) mbar_arrive(&uw_empty[ub]);
+      mbar_arrive(&uw_empty[ub]);  // weight chunk consumed
       if (++ub == 2) { ub = 0; uphase ^= 1u; }
     }
 
@@ -455,11 +456,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (threadIdx.x == 0) {
           bulk_s2g(dst + int64_t(r0) * d, buf, uint32_t(srows) * row_bytes);
           bulk_wait_read_all();
-          mbar_arrive_cnt(&empty[stage], kConsumerWarps);
+          mbar_arrive_cnt(&empty[stage], kConsumerWarps * 32);  // for all consumers (named barrier above)
         }
       } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        mbar_arrive(&empty[stage]);
       }
       if (++stage == kNStage) { stage = 0; phase ^= 1u; }
     }

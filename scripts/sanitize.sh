@@ -1,0 +1,13 @@
+#!/bin/bash
+# compute-sanitizer over smoke() and a few small parity tests that reach the other
+# realign paths (fp8 blocks, weight chunks of a large pool, host-resident pool).
+# Run on the GPU box; prints one summary line per (tool, target).
+T1='python -c "import __graft_entry__ as g; g.smoke()"'
+T2='python -m pytest -q -x -m gpu tests/test_gpu_parity.py -k "test_weight_block_fallback or test_fp8_offsets_codes_and_realign or test_host_resident_pool" -p no:cacheprovider'
+for tool in memcheck racecheck synccheck initcheck; do
+  for t in "$T1" "$T2"; do
+    out=$(eval compute-sanitizer --tool $tool --error-exitcode 9 $t 2>&1)
+    rc=$?
+    echo "== $tool rc=$rc :: ${t:0:60} :: $(echo "$out" | grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|passed|failed' | tr '\n' ' ')"
+  done
+done

@@ -5,7 +5,7 @@ P:1456-1469) for a like-for-like comparison with the paper's H100 numbers.
 
 For each point one placeholder segment of T tokens is realigned against m anchors
 (all layers/heads, K and V) through kvcomm_realign_segment; device time by CUDA
-events over 10 back-to-back launches after 3 warm-ups.  Prints JSON lines.
+events: median of 5 batches of 10 back-to-back launches after 5 warm-ups.  Prints JSON lines.
 Grid points that do not fit one GPU's HBM are reported as OOM.
 
   python scripts/sweep.py [--quick]
@@ -56,18 +56,23 @@ def time_point(pool, m, T, reps=10):
     W = torch.full((pool.capacity, ldw), 1.0 / m, dtype=torch.float32, device="cuda")
     seg = kv.Segment(pool, 0, kv.PLACEHOLDER, W, list(range(m)), base_k, base_v, 0, 512, dst_k, dst_v)
     prep = kv.prepare_segments([seg])
-    for _ in range(3):
+    for _ in range(5):
         kv.realign_prepared(prep)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        kv.realign_prepared(prep)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    # median of 5 batches: the first launches over freshly allocated buffers are
+    # sometimes 2-10x slower (seen with old and new kernels alike), a warm-up effect
+    batches = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            kv.realign_prepared(prep)
+        e1.record()
+        torch.cuda.synchronize()
+        batches.append(e0.elapsed_time(e1) / reps)
+    ms = sorted(batches)[len(batches) // 2]
     byts = (m + 2) * T * TOKEN_BYTES
-    return {"anchors": m, "tokens": T, "ms": ms, "tokens_per_s": T / (ms / 1e3), "GBps": byts / (ms / 1e3) / 1e9,
+    return {"anchors": m, "tokens": T, "ms": ms, "ms_batches": [round(b, 4) for b in batches], "tokens_per_s": T / (ms / 1e3), "GBps": byts / (ms / 1e3) / 1e9,
             "alg_bytes": byts}
 
 
