@@ -369,3 +369,30 @@ def test_fp8_large_row_scale():
     gpu = harness.run_gpu(p, gamma=1.0, offset_format="fp8")
     ora = harness.run_oracle(p, gamma=1.0, fp8=True)
     harness.compare(gpu, ora, p)
+
+
+@pytest.mark.parametrize("n_anchor", [8, 9, 17])
+def test_weight_chunk_boundaries(n_anchor):
+    """d = 16: a 512-row tile takes 2 KiB of weights per anchor, so a 16 KiB weight chunk
+    holds 8 anchors; n_cand = 8, 9, 17 hit the exact-fit, one-over and multi-chunk cases."""
+    lens = [40 + 3 * (j % 4) for j in range(n_anchor)]
+    p = synth.make_problem(60 + n_anchor, L=2, H=2, d=16, D_e=32, L_phi=40, anchor_lens=lens, prefix_lens=[6],
+                           target_start=8, pf_base_start=4)
+    gpu = harness.run_gpu(p, gamma=1.0)
+    ora = harness.run_oracle(p, gamma=1.0)
+    harness.compare(gpu, ora, p)
+
+
+@pytest.mark.parametrize("fmt,top_k", [("bf16", 0), ("bf16", 32), ("fp8", 0)])
+def test_maximum_capacity_1024_anchors(fmt, top_k):
+    """KVCOMM_MAX_CAPACITY = 1024 candidates (config 5's largest pool) through match,
+    weights (dense and the maximum top-k of 32) and realign (128 weight chunks at d=16;
+    64 at d=64 fp8), against the oracle."""
+    d = 16 if fmt == "bf16" else 64
+    n = 1024
+    lens = [24 + (j % 3) for j in range(n)]
+    p = synth.make_problem(1024 + top_k, L=1, H=1, d=d, D_e=32, L_phi=24, anchor_lens=lens, prefix_lens=[4],
+                           target_start=3, pf_base_start=2, inv_freq=synth.llama3_inv_freq(d), n_vocab=64)
+    gpu = harness.run_gpu(p, gamma=1.0, top_k=top_k, offset_format=fmt)
+    ora = harness.run_oracle(p, gamma=1.0, top_k=top_k, fp8=(fmt == "fp8"))
+    harness.compare(gpu, ora, p)
