@@ -176,6 +176,16 @@ def _cpu_model():
     return None
 
 
+def arm_config(args, world, w):
+    """The `config` object both arms print (same workload, metric and unit)."""
+    return {"workload": "llama3-8b-shape (32 layers, 8 KV heads x 128) 5-agent fully-connected, "
+                        "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
+            "realigned_tokens_per_step": w.realigned_tokens, "anchors_blended": w.capacity,
+            "gamma": args.gamma, "offset_storage": args.offsets,
+            "parallelism": f"layer-shard x{world}" if world > 1 else "single",
+            "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
+
+
 # ---------------------------------------------------------------------- reference arm
 
 def run_reference(args):
@@ -215,10 +225,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "llama3-8b-shape 5-agent fully-connected (Table 2), oracle sample",
-                   "sample_tokens_per_step": T},
+        "config": arm_config(args, args.gpus, w),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{T} tokens x 32x8 layer/head rows x 20 anchors per step (match + Eq.6 + RoPE)",
+                         "sample": f"each step: {T} tokens of agent 1's user_question placeholder x 32x8 layer/head "
+                                   f"rows x 20 anchors (distances, Eq. 5/6 weights, blend, RoPE-delta, add), "
+                                   f"float64 NumPy; value = sampled tokens / step time",
                          "cpu": _cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -507,12 +518,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.offsets == "bf16" else "bf16 (fp8-e4m3 offsets)",
             "data": "synthetic",
-            "config": {"workload": "llama3-8b-shape (32 layers, 8 KV heads x 128) 5-agent fully-connected, "
-                                   "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
-                       "realigned_tokens_per_step": total_tokens, "anchors_blended": w.capacity,
-                       "gamma": args.gamma, "offset_storage": args.offsets, "parallelism": f"layer-shard x{world}" if world > 1 else "single",
-                       "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed,
-                       **({"test_same_gpu_gloo": True} if same_gpu else {})},
+            "config": {**arm_config(args, world, w), **({"test_same_gpu_gloo": True} if same_gpu else {})},
             "roofline": {"kernel": "kvc::realign_kernel (30 segments + 5 p0 copies, one launch)", "bound": "hbm",
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
