@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--offsets", default="bf16", choices=["bf16", "fp8"],
                     help="anchor offset storage; the headline line is bf16 (fp8 = SURVEY f3, lossy)")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N>1: realign writes each layer block straight into the consumer GPU's cache over "
+                         "NVLink (fused, default) or a separate NCCL send/recv gather pass (baseline)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -182,7 +185,7 @@ def arm_config(args, world, w):
                         "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
             "realigned_tokens_per_step": w.realigned_tokens, "anchors_blended": w.capacity,
             "gamma": args.gamma, "offset_storage": args.offsets,
-            "parallelism": f"layer-shard x{world}" if world > 1 else "single",
+            "parallelism": f"layer-shard x{world}, {args.gather} gather" if world > 1 else "single",
             "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
 
 
@@ -237,7 +240,7 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- e2e
 
-def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, shard):
+def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, deliver):
     """The same step through the public API with HOST buffers: every step copies the
     request's inputs (query embeddings of the 5 samples + their base caches; the
     prefix / p_(m,0) caches are per-template and stay resident) from pinned host
@@ -264,7 +267,6 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
                 if sg.kind == kv.PLACEHOLDER:
                     dev_bases[sg.pool] = (sg.base_k, sg.base_v)
         qlist = [st.queries[n] for n in req.names]
-        agents_all = [a.agent for a in st.agents]
 
         def e2e_step():
             for n, q in pinned_q.items():
@@ -273,7 +275,7 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
                 dev_bases[n][0].copy_(hk, non_blocking=True)
                 dev_bases[n][1].copy_(hv, non_blocking=True)
             req.plan.run(qlist, sync=False, stream=stream)
-            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
+            deliver()
             for f, ho in zip(full, host_out):
                 if ho is not None:
                     ho[0].copy_(f[0], non_blocking=True)
@@ -414,9 +416,20 @@ def main():
     Ls = lr[1] - lr[0]
     row_bytes = w.H * w.d * 2  # one token of one plane over the shard's heads, per layer
 
-    # full-depth receive buffers for the agents this rank hosts (N>1)
+    # full-depth caches of the agents this rank hosts (N>1).  fused: allocated by the
+    # consumer rank, IPC-mapped everywhere, and used directly as the realign destinations
+    # of every rank's layer block (the kernel delivers over NVLink); nccl: local shard
+    # outputs + a send/recv gather pass.
     full = []
-    if world > 1:
+    peer = None
+    if world > 1 and args.gather == "fused":
+        from paper_2510_12872_b200.request import AgentLayout, ReuseRequest
+        peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, local)
+        agents_f = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
+                    for i, a in enumerate(st.agents)]
+        req = ReuseRequest(st.pools, agents_f, gamma=req.gamma, top_k=req.top_k)
+        full = [peer.full(i) for i in range(len(st.agents))]
+    elif world > 1:
         for a in st.agents:
             if shard.consumer_rank(a.agent, world) == rank:
                 full.append((torch.empty(w.L, w.H, a.N, w.d, dtype=torch.bfloat16, device="cuda"),
@@ -428,12 +441,17 @@ def main():
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
 
+    def deliver():
+        if peer is not None:
+            peer.sync()
+        elif world > 1:
+            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
+
     def step(events=None):
         if events is not None:
             plan.set_events(*events)     # recorded right before / after the realign launch
         plan.run(qlist, sync=False, stream=stream)   # no host synchronisation inside a step
-        if world > 1:
-            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
+        deliver()
 
     for _ in range(args.warmup):
         step()
@@ -506,7 +524,7 @@ def main():
     # ------------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, shard)
+        e2e = run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, deliver)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -382,6 +382,31 @@ KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before
 KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, const float** W,
                                              int64_t* ld_w, const float** wbar);
 
+/* ---- the fused gather (SURVEY §8(e) "fuse the gather into the realign epilogue with
+ * NVLink P2P stores"; north star: realigned caches land on the GPU that prefills the
+ * consuming agent) ------------------------------------------------------------------
+ * With the path layer-sharded over G GPUs (one process each), the rank hosting agent m
+ * allocates m's full-depth caches with kvcomm_ipc_alloc and shares the 64-byte handles
+ * over any host channel; every other rank maps them with kvcomm_ipc_open and passes
+ * (mapped pointer + its layer block's offset) as the destination of its segments.  The
+ * library detects destinations that live on another GPU (cudaPointerGetAttributes) and
+ * the realign kernel writes those rows with per-thread stores straight into the peer's
+ * HBM over NVLink, then fences system-wide before it exits: there is no separate gather
+ * pass.  The caller orders the consumer's reads after every writer's launch (e.g. a
+ * stream-ordered all-reduce of one word).  Setting KVCOMM_STORE_STG=1 in the
+ * environment forces the per-thread store path for every destination (tests). */
+typedef struct kvcomm_ipc_handle {
+  char bytes[64]; /* cudaIpcMemHandle_t */
+} kvcomm_ipc_handle;
+
+/* cudaMalloc `bytes` on `device` (owned by the caller until kvcomm_ipc_free) and export it. */
+KVCOMM_API kvcomm_status kvcomm_ipc_alloc(int32_t device, int64_t bytes, void** ptr, kvcomm_ipc_handle* handle);
+KVCOMM_API kvcomm_status kvcomm_ipc_free(void* ptr);
+/* Map another process's allocation into this process (peer access enabled lazily);
+ * *ptr is valid on `device` until kvcomm_ipc_close. */
+KVCOMM_API kvcomm_status kvcomm_ipc_open(int32_t device, const kvcomm_ipc_handle* handle, void** ptr);
+KVCOMM_API kvcomm_status kvcomm_ipc_close(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

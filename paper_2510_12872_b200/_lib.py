@@ -92,6 +92,10 @@ class PlanAgent(C.Structure):
                 ("dst_ld", C.c_int64)]
 
 
+class IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_char * 64)]
+
+
 class SegmentRef(C.Structure):
     _fields_ = [("start", C.c_int32), ("length", C.c_int32), ("src", KVView)]
 
@@ -133,6 +137,10 @@ _SIGS = {
     "kvcomm_plan_set_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvcomm_plan_weights": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_void_p)]),
+    "kvcomm_ipc_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
+    "kvcomm_ipc_free": (C.c_int, [C.c_void_p]),
+    "kvcomm_ipc_open": (C.c_int, [C.c_int32, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),
+    "kvcomm_ipc_close": (C.c_int, [C.c_void_p]),
 }
 
 

@@ -756,6 +756,7 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   for (const HostSeg& g : hs) {
     n_ints += g.x.n_cand + g.gates.size();
     if (g.x.fp8) L.hdr.any_fp8 = 1;
+    if (g.x.dst_stg) L.hdr.any_stg = 1;
     const int rpu = unit_rows(d, g.x.fp8);
     n_wt += size_t((g.x.L_seg + rpu - 1) / rpu) * g.x.n_cand * weight_row_stride(rpu);
   }
@@ -983,7 +984,21 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
   return KVCOMM_OK;
 }
 
-static HostSeg host_segment(const kvcomm_realign_desc& g) {
+// Destinations on another GPU (a consumer's cache mapped by CUDA IPC: the fused gather,
+// SURVEY §8(e)) are written with per-thread stores; KVCOMM_STORE_STG=1 forces that path
+// everywhere (tests compare it with the TMA bulk-store path bit for bit).
+static int32_t dst_store_mode(const void* dst, int device) {
+  const char* e = getenv("KVCOMM_STORE_STG");
+  if (e && atoi(e) == 1) return 1;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, dst) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return (at.type == cudaMemoryTypeDevice && at.device != device) ? 1 : 0;
+}
+
+static HostSeg host_segment(const kvcomm_realign_desc& g, int32_t dst_stg = -1) {
   kvcomm_pool_s* p = g.pool;
   HostSeg h{};
   SegDev& x = h.x;
@@ -993,6 +1008,7 @@ static HostSeg host_segment(const kvcomm_realign_desc& g) {
   x.dst[0] = static_cast<bf16*>(g.dst_k);
   x.dst[1] = static_cast<bf16*>(g.dst_v);
   x.dst_ld = g.dst_ld;
+  x.dst_stg = dst_stg >= 0 ? dst_stg : dst_store_mode(g.dst_k, p->cfg.device);
   x.inv_freq = p->inv_freq_dev;
   x.L_seg = g.L_seg;
   x.target_start = g.target_start;
@@ -1117,6 +1133,7 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
   if (!dst_k || !dst_v || !aligned16(dst_k) || !aligned16(dst_v))
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "dst null or misaligned");
   std::vector<HostSeg> hs;
+  const int32_t stg = dst_store_mode(dst_k, device);
   for (int i = 0; i < n; ++i) {
     if (!segs[i].src.k || segs[i].length == 0) continue;
     KV_TRY(check_view(segs[i].src, segs[i].length, "concat src"));
@@ -1128,6 +1145,7 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
     x.dst[0] = static_cast<bf16*>(dst_k);
     x.dst[1] = static_cast<bf16*>(dst_v);
     x.dst_ld = dst_ld;
+    x.dst_stg = stg;
     x.L_seg = segs[i].length;
     x.target_start = segs[i].start;
     x.w_by_slot = 1;
@@ -1155,6 +1173,7 @@ struct kvcomm_plan_s {
   std::vector<kvcomm_match_info> infos;
   std::vector<int> job_of;        // match -> job index in the last run (-1: decided on host)
   std::vector<int32_t> agent_state;  // 0 reuse pending/ok, 1 fallback (host-decided)
+  std::vector<int32_t> agent_stg;    // destination store mode per agent (dst_store_mode at create)
   int64_t res_off = 0;
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
   std::mutex mu;
@@ -1239,6 +1258,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
   pl->matches.assign(matches, matches + n_matches);
   pl->segs.assign(segs, segs + n_segs);
   pl->agents.assign(agents, agents + n_agents);
+  for (int a = 0; a < n_agents; ++a) pl->agent_stg.push_back(dst_store_mode(agents[a].dst_k, p0->cfg.device));
   pl->agent_matches = am;
   pl->infos.resize(n_matches);
   pl->job_of.assign(n_matches, -1);
@@ -1330,7 +1350,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
       d.n_candidates = info->n_candidates;
       KV_TRY(validate_segment(d, int(&g - pl->segs.data())));
     }
-    HostSeg h = host_segment(d);
+    HostSeg h = host_segment(d, pl->agent_stg[g.agent]);
     for (int mi : pl->agent_matches[g.agent]) h.gates.push_back(pl->job_of[mi]);
     hs.push_back(std::move(h));
   }
@@ -1407,6 +1427,54 @@ KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t pl, int32_t match, co
   if (W) *W = pl->W[match];
   if (ld_w) *ld_w = pl->ld_w[match];
   if (wbar) *wbar = pl->wbar[match];
+  return ok();
+}
+
+// ---- fused gather: IPC-shared destinations ------------------------------------
+static_assert(sizeof(kvcomm_ipc_handle) == sizeof(cudaIpcMemHandle_t), "ipc handle size");
+
+KVCOMM_API kvcomm_status kvcomm_ipc_alloc(int32_t device, int64_t bytes, void** ptr, kvcomm_ipc_handle* handle) {
+  if (!ptr || !handle || bytes <= 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad ipc_alloc arguments");
+  DeviceGuard guard(device);
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, size_t(bytes));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *ptr = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? KVCOMM_ERR_OUT_OF_MEMORY : KVCOMM_ERR_CUDA, "ipc_alloc %lld bytes: %s",
+                (long long)bytes, cudaGetErrorString(e));
+  }
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return fail(KVCOMM_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_ipc_free(void* ptr) {
+  if (!ptr) return ok();
+  KV_CUDA(cudaFree(ptr));
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_ipc_open(int32_t device, const kvcomm_ipc_handle* handle, void** ptr) {
+  if (!ptr || !handle) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad ipc_open arguments");
+  DeviceGuard guard(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle->bytes, sizeof(h));
+  *ptr = nullptr;
+  KV_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_ipc_close(void* ptr) {
+  if (!ptr) return ok();
+  KV_CUDA(cudaIpcCloseMemHandle(ptr));
   return ok();
 }
 

@@ -326,6 +326,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const bool rotate = un.p == 0 && g.delta != 0;
     const float2* csg = cs + g.cs_off;
     bf16* const dst = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
+    const bool tstore = tma_store && !g.dst_stg;  // peer destinations: per-thread stores
     float* const dbg = g.dbg[un.p] != nullptr ? g.dbg[un.p] + (lh * g.L_seg + i0) * d : nullptr;
     float acc[2][kItemsPerThread][16];  // [64-row tile of the unit][item][element]
 #pragma unroll
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           const uint4 o1 = make_uint4(pack_bf16_rn(y1[0], y1[1]), pack_bf16_rn(y1[2], y1[3]),
                                       pack_bf16_rn(y1[4], y1[5]), pack_bf16_rn(y1[6], y1[7]));
           const int row = r0 + irow[q];  // within the unit
-          if (tma_store) {
+          if (tstore) {
             sts128(pa, o0);  // in place; the whole tile leaves with one bulk store below
             sts128(pb, o1);
           } else if (!(variant & 2)) {
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             p1[1] = make_float4(acc[s][q][12], acc[s][q][13], acc[s][q][14], acc[s][q][15]);
           }
         }
-      } else if (!tma_store && !(variant & 2)) {
+      } else if (!tstore && !(variant & 2)) {
 #pragma unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
           if (irow[q] >= srows) continue;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           stg128_cs(o + d / 2, lds128(pa + d));
         }
       }
-      if (tma_store) {
+      if (tstore) {
         // all consumer writes of the tile -> visible to the async proxy, then one bulk store;
         // the stage is released only once the store has finished reading shared memory
         fence_proxy_async_smem();
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     }
   }
   if (tma_store && threadIdx.x == 0) bulk_wait_all();  // global writes complete before exit
+  if (hdr.any_stg) __threadfence_system();  // peer-GPU rows: visible system-wide before the kernel ends
 }
 
 int realign_grid_size(int device) {

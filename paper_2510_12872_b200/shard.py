@@ -70,3 +70,115 @@ def gather_to_consumers(agents: Sequence[int], shards: Sequence[Tuple[torch.Tens
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+
+
+class PeerRows:
+    """[Ls, Hs, N, d] bf16 rows at a raw device address that may live on a peer GPU (a
+    consumer's cache mapped by CUDA IPC).  Carries just what the plan reads from a
+    destination (data_ptr, shape, strides, dtype) — no torch storage is created over
+    peer memory."""
+
+    is_cuda = True
+    dtype = torch.bfloat16
+
+    def __init__(self, ptr: int, shape: Tuple[int, int, int, int]):
+        self._ptr = int(ptr)
+        self.shape = torch.Size(shape)
+
+    def dim(self) -> int:
+        return 4
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+    def stride(self) -> Tuple[int, int, int, int]:
+        _, Hs, N, d = self.shape
+        return (Hs * N * d, N * d, d, 1)
+
+
+class PeerCaches:
+    """The fused gather: every agent's full-depth [L, H, N, d] K/V caches
+    are allocated on the agent's consumer rank (kvcomm_ipc_alloc), their IPC handles are
+    exchanged once with all_gather_object, and every rank maps the other ranks' buffers
+    (kvcomm_ipc_open).  `destinations(i, layer_range)` gives the slice this rank's realign
+    writes — local memory on the consumer rank, peer memory over NVLink elsewhere — so the
+    realign kernel itself delivers each layer block to its consumer and no gather pass
+    follows.  `sync()` orders the consumers' reads after every rank's launch."""
+
+    def __init__(self, agents: Sequence[Tuple[int, int]], num_layers: int, num_heads: int, head_dim: int,
+                 rank: int, world: int, device: int, group=None):
+        import ctypes as C
+        from . import _lib as L
+        self._L, self._C = L, C
+        self.L, self.H, self.d, self.rank, self.world, self.device = num_layers, num_heads, head_dim, rank, world, device
+        self.group = group
+        self.agents = list(agents)
+        self._owned, self._opened = [], []
+        local = []
+        for agent, N in self.agents:
+            if consumer_rank(agent, world) == rank:
+                nbytes = num_layers * num_heads * N * head_dim * 2
+                pair = []
+                for _ in range(2):
+                    ptr, h = C.c_void_p(), L.IpcHandle()
+                    L.check(L.lib().kvcomm_ipc_alloc(device, nbytes, C.byref(ptr), C.byref(h)))
+                    self._owned.append(ptr.value)
+                    pair.append((ptr.value, C.string_at(C.addressof(h), 64)))  # raw: may hold NULs
+                local.append(pair)
+            else:
+                local.append(None)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, [None if p is None else [hb for _, hb in p] for p in local], group=group)
+        self.ptrs = []   # per agent: (k_ptr, v_ptr) valid in this process
+        for i, (agent, N) in enumerate(self.agents):
+            c = consumer_rank(agent, world)
+            if c == rank:
+                self.ptrs.append((local[i][0][0], local[i][1][0]))
+            else:
+                pair = []
+                for hb in everyone[c][i]:
+                    h = L.IpcHandle()
+                    assert len(hb) == 64
+                    C.memmove(C.addressof(h), hb, 64)
+                    ptr = C.c_void_p()
+                    L.check(L.lib().kvcomm_ipc_open(device, C.byref(h), C.byref(ptr)))
+                    self._opened.append(ptr.value)
+                    pair.append(ptr.value)
+                self.ptrs.append(tuple(pair))
+        nccl = dist.get_backend(group) == "nccl"
+        self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}") if nccl else None
+
+    def destinations(self, i: int, layer_range: Tuple[int, int]):
+        """(K, V) destinations of this rank's layer block of agent i's cache."""
+        agent, N = self.agents[i]
+        lb, le = layer_range
+        off = lb * self.H * N * self.d * 2
+        shape = (le - lb, self.H, N, self.d)
+        return tuple(PeerRows(p + off, shape) for p in self.ptrs[i])
+
+    def full(self, i: int):
+        """Agent i's full caches as torch tensors on its consumer rank, else (None, None)."""
+        agent, N = self.agents[i]
+        if consumer_rank(agent, self.world) != self.rank:
+            return None, None
+        from .kvcomm import _DevView
+        n = self.L * self.H * N * self.d
+        return tuple(torch.as_tensor(_DevView(p, (n,), "<i2"), device=f"cuda:{self.device}")
+                     .view(torch.bfloat16).view(self.L, self.H, N, self.d) for p in self.ptrs[i])
+
+    def sync(self) -> None:
+        """Consumers' later reads are ordered after every rank's realign launch: a
+        stream-ordered all-reduce of one word over NCCL (gloo test path: host barrier)."""
+        if self._flag is not None:
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
+
+    def close(self) -> None:
+        L = self._L
+        for p in self._opened:
+            L.lib().kvcomm_ipc_close(self._C.c_void_p(p))
+        for p in self._owned:
+            L.lib().kvcomm_ipc_free(self._C.c_void_p(p))
+        self._opened, self._owned = [], []

@@ -1,0 +1,62 @@
+"""Worker for tests/test_gpu_peer.py (launched by torch.distributed.run, not collected by
+pytest): the fused gather on one GPU with 2 ranks over gloo.
+
+Each rank realigns its layer block of a small 5-agent workload straight into the
+consumer rank's IPC-shared full-depth caches (shard.PeerCaches); every consumer rank
+then checks its agents' caches bit for bit against an unsharded single-process run of
+the same seeded inputs.  On one GPU the IPC mapping is same-device memory, so this
+exercises the handle exchange, the layer offsets and the ordering, not NVLink."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch
+import torch.distributed as dist
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo")
+    import synth
+    from synth.state import build_five_agent_state
+    from paper_2510_12872_b200 import shard
+    from paper_2510_12872_b200.request import AgentLayout, ReuseRequest
+
+    w = synth.five_agent_workload(L=5, H=2, d=64, D_e=64, user_len=96, resp_len=40, prefix_total=64,
+                                  slot_prefix=8, capacity=4)
+    ref = build_five_agent_state(w, seed=3, device=0, gamma=1.0, offset_format=fmt)
+    ref.request.plan.run([ref.queries[n] for n in ref.request.names], sync=True)
+    _, reused = ref.request.plan.results()
+    assert all(reused), reused
+
+    lr = shard.layer_shard(w.L, rank, world)
+    st = build_five_agent_state(w, seed=3, device=0, gamma=1.0, layer_range=lr, offset_format=fmt)
+    peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, 0)
+    agents = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
+              for i, a in enumerate(st.agents)]
+    req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=0)
+    for _ in range(2):  # twice: the second run overwrites the same rows
+        req.plan.run([st.queries[n] for n in req.names], sync=True)
+        peer.sync()
+    _, reused = req.plan.results()
+    assert all(reused), reused
+    checked = 0
+    for i, a in enumerate(ref.agents):
+        fk, fv = peer.full(i)
+        if fk is None:
+            continue
+        assert torch.equal(fk, a.dst_k), f"rank {rank} agent {a.agent} K differs"
+        assert torch.equal(fv, a.dst_v), f"rank {rank} agent {a.agent} V differs"
+        checked += 1
+    dist.barrier()
+    peer.close()
+    print(f"rank {rank}: {checked} agents bit-exact", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

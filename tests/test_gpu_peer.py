@@ -1,0 +1,53 @@
+"""The fused gather (include/kvcomm.h kvcomm_ipc_*, shard.PeerCaches): 2 ranks on one
+GPU over gloo write their layer blocks into the consumer rank's IPC-shared caches; the
+result equals the unsharded run bit for bit (tests/peer_worker.py)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["bf16", "fp8"])
+def test_fused_gather_two_ranks_bit_exact(fmt):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
+           fmt]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "rank 0: 3 agents bit-exact" in r.stdout and "rank 1: 2 agents bit-exact" in r.stdout, r.stdout
+
+
+@pytest.mark.gpu
+def test_per_thread_store_path_equals_bulk_store():
+    """KVCOMM_STORE_STG=1 forces the peer-destination store path (per-thread STG) for
+    every segment; it must write exactly the bytes the TMA bulk-store path writes."""
+    code = ("import sys, torch; sys.path.insert(0, %r); sys.path.insert(0, %r); import synth, harness; "
+            "p = synth.make_problem(5, L=2, H=2, d=64, D_e=64, L_phi=150, anchor_lens=[150, 170, 190], "
+            "prefix_lens=[20], target_start=30, pf_base_start=30, inv_freq=synth.llama3_inv_freq(64)); "
+            "g = harness.run_gpu(p, gamma=1.0); torch.save((g['dst_k'], g['dst_v']), sys.argv[1])"
+            % (ROOT, os.path.join(ROOT, "tests")))
+    import tempfile
+    import torch
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for stg in ("0", "1"):
+            f = os.path.join(td, f"out{stg}.pt")
+            env = dict(os.environ, KVCOMM_STORE_STG=stg)
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=ROOT, env=env, capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0, r.stderr[-3000:]
+            outs.append(torch.load(f))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
