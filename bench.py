@@ -424,7 +424,12 @@ def main():
     peer = None
     if world > 1 and args.gather == "fused":
         from paper_2510_12872_b200.request import AgentLayout, ReuseRequest
-        peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, local)
+        try:
+            peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, local)
+        except RuntimeError as e:  # all ranks raise together (agreed collectively)
+            print(f"[bench] {e}; using the NCCL gather", file=sys.stderr, flush=True)
+            args.gather = "nccl (ipc unavailable)"
+    if peer is not None:
         agents_f = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
                     for i, a in enumerate(st.agents)]
         req = ReuseRequest(st.pools, agents_f, gamma=req.gamma, top_k=req.top_k)

@@ -114,37 +114,53 @@ class PeerCaches:
         self.group = group
         self.agents = list(agents)
         self._owned, self._opened = [], []
-        local = []
-        for agent, N in self.agents:
-            if consumer_rank(agent, world) == rank:
-                nbytes = num_layers * num_heads * N * head_dim * 2
-                pair = []
-                for _ in range(2):
-                    ptr, h = C.c_void_p(), L.IpcHandle()
-                    L.check(L.lib().kvcomm_ipc_alloc(device, nbytes, C.byref(ptr), C.byref(h)))
-                    self._owned.append(ptr.value)
-                    pair.append((ptr.value, C.string_at(C.addressof(h), 64)))  # raw: may hold NULs
-                local.append(pair)
-            else:
-                local.append(None)
+        # every failure is agreed on collectively (all ranks raise together, none hangs)
+        local, err = [], None
+        try:
+            for agent, N in self.agents:
+                if consumer_rank(agent, world) == rank:
+                    nbytes = num_layers * num_heads * N * head_dim * 2
+                    pair = []
+                    for _ in range(2):
+                        ptr, h = C.c_void_p(), L.IpcHandle()
+                        L.check(L.lib().kvcomm_ipc_alloc(device, nbytes, C.byref(ptr), C.byref(h)))
+                        self._owned.append(ptr.value)
+                        pair.append((ptr.value, C.string_at(C.addressof(h), 64)))  # raw: may hold NULs
+                    local.append(pair)
+                else:
+                    local.append(None)
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank}: {e}"
         everyone = [None] * world
-        dist.all_gather_object(everyone, [None if p is None else [hb for _, hb in p] for p in local], group=group)
+        dist.all_gather_object(everyone, (err, None if err else [None if p is None else [hb for _, hb in p]
+                                                                  for p in local]), group=group)
+        errs = [e for e, _ in everyone if e]
         self.ptrs = []   # per agent: (k_ptr, v_ptr) valid in this process
-        for i, (agent, N) in enumerate(self.agents):
-            c = consumer_rank(agent, world)
-            if c == rank:
-                self.ptrs.append((local[i][0][0], local[i][1][0]))
-            else:
-                pair = []
-                for hb in everyone[c][i]:
-                    h = L.IpcHandle()
-                    assert len(hb) == 64
-                    C.memmove(C.addressof(h), hb, 64)
-                    ptr = C.c_void_p()
-                    L.check(L.lib().kvcomm_ipc_open(device, C.byref(h), C.byref(ptr)))
-                    self._opened.append(ptr.value)
-                    pair.append(ptr.value)
-                self.ptrs.append(tuple(pair))
+        if not errs:
+            try:
+                for i, (agent, N) in enumerate(self.agents):
+                    c = consumer_rank(agent, world)
+                    if c == rank:
+                        self.ptrs.append((local[i][0][0], local[i][1][0]))
+                        continue
+                    pair = []
+                    for hb in everyone[c][1][i]:
+                        h = L.IpcHandle()
+                        assert len(hb) == 64
+                        C.memmove(C.addressof(h), hb, 64)
+                        ptr = C.c_void_p()
+                        L.check(L.lib().kvcomm_ipc_open(device, C.byref(h), C.byref(ptr)))
+                        self._opened.append(ptr.value)
+                        pair.append(ptr.value)
+                    self.ptrs.append(tuple(pair))
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {rank}: {e}"
+            status = [None] * world
+            dist.all_gather_object(status, err, group=group)
+            errs = [e for e in status if e]
+        if errs:
+            self.close()
+            raise RuntimeError("fused gather unavailable: " + "; ".join(errs))
         nccl = dist.get_backend(group) == "nccl"
         self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}") if nccl else None
 
