@@ -1,0 +1,102 @@
+#!/usr/bin/env python
+"""BASELINE.json configs[3] on one B200: one 1/8 shard of the Llama-3-70B-shape request
+(layers [0,20) x KV heads [0,4) of 80 x 8; a 3072-token shared segment + 32-token
+prefix + 200-token p_(m,0) copy; 256-anchor pool, k = 256) through the plan, the same
+launch configuration tests/test_gpu_config4.py checks against the oracle.
+
+Prints one JSON line: per-request-shard device time (CUDA events, median of batches),
+the realign kernel alone, its algorithmic bytes and GB/s.  The 8-GPU aggregate is not
+measured here (one GPU per gpurun call): each of the 8 shards does the same work with
+no communication before the delivery of the realigned blocks.
+
+  python scripts/config4_bench.py
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
+import synth
+from synth.state import keyed_gen
+
+L, H, D, DE = 80, 8, 128, 8192
+LAYERS, HEADS = (0, 20), (0, 4)
+T, P, M, P0, N_VOCAB = 3072, 32, 256, 200, 128256
+SEED = 70
+
+
+def main():
+    import paper_2510_12872_b200 as kv
+    Ls, Hs = LAYERS[1] - LAYERS[0], HEADS[1] - HEADS[0]
+    g = keyed_gen(SEED, "c4vocab")
+    vocab = (torch.randn(N_VOCAB, DE, generator=g, device="cuda") / np.sqrt(DE)).to(torch.bfloat16)
+    pool = kv.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=M, max_anchor_len=T,
+                         prefix_len=[P], inv_freq=synth.llama3_inv_freq(D), layer_range=LAYERS, head_range=HEADS)
+    go = keyed_gen(SEED, "c4off-bench")
+    rnd = lambda n: (torch.randn(Ls, Hs, n, D, generator=go, device="cuda") * synth.OFFSET_STD).to(torch.bfloat16)
+    ids0 = None
+    for s in range(M):
+        ids = torch.randint(0, N_VOCAB, (T,), generator=keyed_gen(SEED, "c4ids", s), device="cuda")
+        ids0 = ids if s == 0 else ids0
+        pool.insert(vocab[ids], [kv.OffsetGiven(0, rnd(T), rnd(T), rnd(P), rnd(P))])
+    gq = keyed_gen(SEED, "c4query")
+    swap = torch.rand(T, generator=gq, device="cuda") < 0.3
+    query = vocab[torch.where(swap, torch.randint(0, N_VOCAB, (T,), generator=gq, device="cuda"), ids0)].contiguous()
+    del vocab
+    gb = keyed_gen(SEED, "c4base")
+    base = [torch.randn(Ls, Hs, T, D, generator=gb, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    pfb = [torch.randn(Ls, Hs, P, D, generator=gb, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    p0 = [torch.randn(Ls, Hs, P0, D, generator=gb, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    N = P0 + T + P
+    dst = [torch.empty(Ls, Hs, N, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    segs = [kv.PlanSegment(0, 0, kv.PLACEHOLDER, 0, base[0], base[1], 0, P0),
+            kv.PlanSegment(0, 0, kv.PREFIX, 0, pfb[0], pfb[1], P0, P0 + T),
+            kv.PlanSegment(0, 0, kv.COPY, 0, p0[0], p0[1], 0, 0)]
+    plan = kv.Plan([(pool, T, 0.3, 0)], segs, [(N, dst[0], dst[1])])
+    stream = torch.cuda.current_stream()
+    for _ in range(5):
+        plan.run([query], stream=stream)
+    torch.cuda.synchronize()
+    _, reused = plan.results()
+    if not all(reused):
+        raise SystemExit("request fell back: the timing needs the reuse branch")
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    plan.set_events(*ev)
+    steps, realign = [], []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ks = []
+        e0.record(stream)
+        for _ in range(4):
+            plan.run([query], stream=stream)
+            ev[1].synchronize()
+            ks.append(ev[0].elapsed_time(ev[1]))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        steps.append(e0.elapsed_time(e1) / 4)
+        realign.extend(ks)
+    step_ms = sorted(steps)[len(steps) // 2]
+    rl_ms = sorted(realign)[len(realign) // 2]
+    tok = Ls * Hs * D * 2 * 2  # one token row, K+V, this shard
+    alg = ((M + 2) * T + (M + 2) * P + 2 * P0) * tok
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+    print(json.dumps({
+        "workload": "BASELINE configs[3] shard: llama3-70b-shape layers [0,20) x kv heads [0,4), 3072-token "
+                    "segment + 32-token prefix + 200-token p0, 256-anchor pool, k=256",
+        "realigned_tokens": T + P, "step_ms": step_ms, "realign_ms": rl_ms,
+        "shard_tokens_per_s": (T + P) / (step_ms / 1e3),
+        "realign_alg_bytes": alg, "realign_GBps": alg / (rl_ms / 1e3) / 1e9,
+        "frac_of_measured_peak": (alg / (rl_ms / 1e3) / 1e9 / peak) if peak else None,
+        "note": "one of 8 shards measured on one B200; the 8-GPU run is not measured here"}))
+    plan.destroy()
+    pool.destroy()
+
+
+if __name__ == "__main__":
+    main()
