@@ -16,12 +16,17 @@
 //     tile(s) into a 9-deep shared-memory ring (9 measured 3 % faster than 11: fewer
 //     bytes in flight, less DRAM contention) with cp.async.bulk (UBLKCP) + mbarrier
 //     complete_tx, L2 evict-first;
-//   * warps 0-7 consume: each thread owns two 32-byte "items" per 64-row tile (8
-//     elements of the first half of a row and the matching 8 of the second half, so
-//     the rotate_half pair (f, f+d/2) sits in one thread), accumulates Σ w Δ in fp32
-//     registers; on a base tile it adds, rotates (K only), rounds to bf16 (RNE) in
-//     place in shared memory, and one thread writes the whole tile back with a single
-//     TMA bulk store (cp.async.bulk.global.shared), 2-3 % faster than per-thread STG.
+//   * 8 consumer warps (16 for tables that read fp8 pools): each thread owns two
+//     32-byte "items" per 64-row tile (8 elements of the first half of a row and the
+//     matching 8 of the second half, so the rotate_half pair (f, f+d/2) sits in one
+//     thread).  Per anchor tile it loads its operands into registers, arrives on the
+//     stage's empty barrier (the stage is held only for the shared-memory loads),
+//     then accumulates Σ w Δ in fp32 registers with packed FFMA2 (fp8 codes decoded
+//     exactly by F2FP + HADD2.F32).  On a base tile it adds, rotates (K only), rounds
+//     to bf16 (RNE) in place in shared memory, and one thread writes the whole tile
+//     back with a single TMA bulk store (cp.async.bulk.global.shared, 2-3 % faster than
+//     per-thread STG); rows bound for a peer GPU (the fused gather) use per-thread
+//     stores over NVLink instead.
 //   * COPY segments (n_cand = 0, δ = 0) move rows verbatim through the same ring
 //     (bit-exact: no arithmetic is applied), so p_(m,0) rides in the same launch.
 #include <cuda_runtime.h>
@@ -39,7 +44,6 @@ namespace kvc {
 constexpr int kNStage = KVC_NSTAGE;
 constexpr int kItems = kStageBytes / 32;  // 512 items of 32 B per 16 KiB bf16 tile
 constexpr int kConsumerBar = 1;           // named barrier id (consumers only)
-
 
 constexpr size_t realign_smem_bytes() {
   return size_t(kNStage) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * kNStage + 4) * sizeof(uint64_t);
