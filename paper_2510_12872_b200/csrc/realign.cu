@@ -180,7 +180,9 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
 // __syncwarp hand-off).
 // kConsumerWarps consumer warps (8: two items per thread; 16: one item per thread) + one
 // producer warp.
-template <int kConsumerWarps>
+// kD: head_dim fixed at compile time (128: the Llama shapes; all tile geometry and
+// thread offsets fold into immediates), 0: read from the table (any supported d).
+template <int kConsumerWarps, int kD>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     realign_kernel(const uint8_t* __restrict__ tab, int variant) {
   constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);
@@ -213,9 +215,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   }
   __syncthreads();
 
-  const int d = hdr.d;
+  const int d = kD ? kD : hdr.d;
   const int Hs = hdr.Hs;
-  const int rpt = hdr.rows_per_tile;
+  const int rpt = kD ? rows_per_tile(kD) : hdr.rows_per_tile;
   const int fblk = fp8_block_bytes(d);
   const int64_t total = hdr.total_units;
   const int row_bytes = 2 * d;
@@ -485,11 +487,14 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(realign_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(realign_smem_bytes()));
+    const int smem = int(realign_smem_bytes());
+    cudaError_t e = cudaFuncSetAttribute(realign_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(realign_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(realign_smem_bytes()));
+      e = cudaFuncSetAttribute(realign_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(realign_kernel<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(realign_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
@@ -507,10 +512,16 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
   const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);
-  if (cw == 8)
-    realign_kernel<8><<<int(g), 9 * 32, realign_smem_bytes(), s>>>(t, variant);
+  const size_t smem = realign_smem_bytes();
+  const bool d128 = hdr.d == 128 && !(variant & 256);  // bit8: generic-d kernel (probe)
+  if (cw == 8 && d128)
+    realign_kernel<8, 128><<<int(g), 9 * 32, smem, s>>>(t, variant);
+  else if (cw == 8)
+    realign_kernel<8, 0><<<int(g), 9 * 32, smem, s>>>(t, variant);
+  else if (d128)
+    realign_kernel<16, 128><<<int(g), 17 * 32, smem, s>>>(t, variant);
   else
-    realign_kernel<16><<<int(g), 17 * 32, realign_smem_bytes(), s>>>(t, variant);
+    realign_kernel<16, 0><<<int(g), 17 * 32, smem, s>>>(t, variant);
   return cudaGetLastError();
 }
 
