@@ -346,7 +346,30 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const int c1 = min(n_cand, c0 + chunk);
       mbar_wait(&uw_full[ub], uphase);
       const float* wv = suw + ub * (kUnitWBytes / 4);
-      for (int c = c0; c < c1; ++c, wv += rw) {
+      int c = c0;
+      if (fp8) {
+        // two anchor tiles per iteration: both loaded and released before the decode
+        for (; c + 1 < c1; c += 2, wv += 2 * rw) {
+          float w0[2][kItemsPerThread], w1[2][kItemsPerThread];
+          uint4 code0[2][kItemsPerThread], code1[2][kItemsPerThread];
+          mbar_wait(&full[stage], phase);
+          const uint8_t* b0 = sdata + size_t(stage) * kStageStride;
+          fp8_load<kItemsPerThread>(w0, code0, b0, reinterpret_cast<const uint8_t*>(wv), b0 + scale_off, coff, roff);
+          mbar_arrive(&empty[stage]);
+          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+          mbar_wait(&full[stage], phase);
+          const uint8_t* b1 = sdata + size_t(stage) * kStageStride;
+          fp8_load<kItemsPerThread>(w1, code1, b1, reinterpret_cast<const uint8_t*>(wv + rw), b1 + scale_off, coff,
+                                    roff);
+          mbar_arrive(&empty[stage]);
+          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+          if (!(variant & 32)) {
+            fp8_accum<kItemsPerThread>(acc, w0, code0);
+            fp8_accum<kItemsPerThread>(acc, w1, code1);
+          }
+        }
+      }
+      for (; c < c1; ++c, wv += rw) {
         mbar_wait(&full[stage], phase);
         const uint8_t* buf = sdata + size_t(stage) * kStageStride;
         // operands -> registers, release the stage to the producer, then the math: the
