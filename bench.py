@@ -515,6 +515,9 @@ def main():
     value = total_tokens * args.steps / (elapsed / 1e3)
 
     realign_avg = sum(realign_ms) / len(realign_ms)
+    # fused gather: output rows of agents hosted elsewhere leave this rank over NVLink
+    peer_bytes = sum(a.N * row_bytes * Ls * 2 for a in st.agents
+                     if world > 1 and shard.consumer_rank(a.agent, world) != rank)
     P = peaks()
     peak = P.get("hbm_gbs")
     achieved = alg_bytes / (realign_avg / 1e3) / 1e9
@@ -549,7 +552,12 @@ def main():
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,
                          "realign_share_of_step": realign_avg / ms_per_step,
                          "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "
-                                        "base once + 2 per copied p0 token, x 128 KiB"},
+                                        "base once + 2 per copied p0 token, x 128 KiB",
+                         **({"peer_bytes_per_launch": peer_bytes, "peer_ref_gbs": 770.0,
+                             "peer_bound_ms": peer_bytes / 770e9 * 1e3,
+                             "peer_note": "fused gather: rows this rank stores into consumer GPUs over NVLink; "
+                                          "ref = measured peer copy per direction (B200_PROFILING.md)"}
+                            if peer is not None else {})},
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": int(n_launch),
