@@ -2,6 +2,7 @@
 // slabs), argument validation, work-table construction and kernel launches.
 // No exception crosses the ABI; every entry point returns a kvcomm_status.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -58,6 +59,12 @@ kvcomm_status ok() {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Makes `dev` current for the scope of a call and restores the caller's device.
+// NVTX range per public call (header-only nvtx3: a no-op unless a profiler attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct DeviceGuard {
   int prev = -1;
   bool ok = true;
@@ -425,6 +432,7 @@ static int lfu_victim(const kvcomm_pool_s* p) {
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_psi, const void* emb,
                                                    const kvcomm_offset_desc* offs, int32_t n_offs, void* stream,
                                                    int32_t* slot_out, int32_t* evicted_out) {
+  NvtxRange nvtx_("kvcomm_anchor_pool_insert");
   if (!p || !emb || (n_offs > 0 && !offs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null argument");
   if (L_psi < 1 || L_psi > p->maxlen)
     return fail(KVCOMM_ERR_SHAPE_MISMATCH, "L_psi %d outside [1,%d]", L_psi, p->maxlen);
@@ -868,6 +876,7 @@ static kvcomm_status check_match_buffers(const kvcomm_match_request& q, int r) {
 }
 
 KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* reqs, int32_t n, void* stream) {
+  NvtxRange nvtx_("kvcomm_match_anchors_batch");
   if (n < 0 || (n > 0 && !reqs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad request list");
   std::vector<kvcomm_pool_s*> pools;
   for (int r = 0; r < n; ++r) {
@@ -1073,6 +1082,7 @@ static kvcomm_status launch_segments(int dev, int d, int Ls, int Hs, const std::
 }
 
 KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs, int32_t n, void* stream) {
+  NvtxRange nvtx_("kvcomm_realign_segments");
   if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
   kvcomm_pool_s* p0 = nullptr;
   std::vector<kvcomm_pool_s*> pools;
@@ -1120,6 +1130,7 @@ static kvcomm_status check_ledger(const int32_t* starts, const int32_t* lengths,
 KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n, int32_t N_total,
                                                      int32_t Ls, int32_t Hs, int32_t d, void* dst_k, void* dst_v,
                                                      int64_t dst_ld, int32_t device, void* stream) {
+  NvtxRange nvtx_("kvcomm_concat_prefill_cache");
   if (n < 0 || (n > 0 && !segs)) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad segment list");
   if (Ls < 1 || Hs < 1 || d < 16 || d % 16 != 0 || d > 256) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad geometry");
   if (N_total < 0 || dst_ld < N_total)
@@ -1290,6 +1301,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_destroy(kvcomm_plan_t pl) {
 
 KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* query_embs, int32_t sync,
                                          void* stream) {
+  NvtxRange nvtx_("kvcomm_plan_run");
   if (!pl || !query_embs) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/queries");
   std::lock_guard<std::mutex> plk(pl->mu);
   const int nm = int(pl->matches.size());

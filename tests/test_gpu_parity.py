@@ -396,3 +396,52 @@ def test_maximum_capacity_1024_anchors(fmt, top_k):
     gpu = harness.run_gpu(p, gamma=1.0, top_k=top_k, offset_format=fmt)
     ora = harness.run_oracle(p, gamma=1.0, top_k=top_k, fp8=(fmt == "fp8"))
     harness.compare(gpu, ora, p)
+
+
+@pytest.mark.parametrize("kind", ["placeholder", "prefix"])
+def test_dyadic_inputs_are_bit_exact(kind):
+    """with dyadic weights (1/2, 1/4, 1/4 permuted per position), dyadic
+    offsets and bases and δ = 0, every product and partial sum is exact in fp32, so
+    the single RNE rounding to bf16 must give the oracle's bf16 result bit for bit."""
+    dev = torch.device("cuda", 0)
+    L_, H, d, T, P = 2, 2, 64, 40, 8
+    g = torch.Generator().manual_seed(11)
+    dy = lambda shape, den, lim: (torch.randint(-lim, lim + 1, shape, generator=g).double() / den).to(torch.bfloat16)
+    n = 3
+    dk = [dy((L_, H, T, d), 16, 16) for _ in range(n)]
+    dv = [dy((L_, H, T, d), 16, 16) for _ in range(n)]
+    pk = [dy((L_, H, P, d), 16, 16) for _ in range(n)]
+    pv = [dy((L_, H, P, d), 16, 16) for _ in range(n)]
+    inv = synth.llama3_inv_freq(d)
+    pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=64, capacity=n, max_anchor_len=T,
+                        prefix_len=[P], inv_freq=inv)
+    for j in range(n):
+        pool.insert(torch.zeros(T, 64, dtype=torch.bfloat16, device=dev),
+                    [K.OffsetGiven(0, dk[j].to(dev), dv[j].to(dev), pk[j].to(dev), pv[j].to(dev))])
+    rows = T if kind == "placeholder" else P
+    base_k, base_v = dy((L_, H, rows, d), 8, 32), dy((L_, H, rows, d), 8, 32)
+    perms = [(0.5, 0.25, 0.25), (0.25, 0.5, 0.25), (0.25, 0.25, 0.5)]
+    if kind == "placeholder":
+        Wt = np.array([perms[i % 3] for i in range(T)])                      # [T, n]
+        weights = torch.zeros(n, T, dtype=torch.float32)
+        weights[:, :] = torch.from_numpy(Wt.T)
+        ora = O.realign_segment(Wt, harness.f64(base_k), harness.f64(base_v), [harness.f64(x) for x in dk],
+                                [harness.f64(x) for x in dv], 5, 5, inv, "placeholder")
+        kkind = K.PLACEHOLDER
+    else:
+        wb = np.array(perms[1])
+        weights = torch.from_numpy(wb).float()
+        ora = O.realign_segment(wb, harness.f64(base_k), harness.f64(base_v), [harness.f64(x) for x in pk],
+                                [harness.f64(x) for x in pv], 5, 5, inv, "prefix")
+        kkind = K.PREFIX
+    dst_k = torch.zeros(L_, H, rows + 5, d, dtype=torch.bfloat16, device=dev)
+    dst_v = torch.zeros_like(dst_k)
+    seg = K.Segment(pool, 0, kkind, weights.to(dev), [0, 1, 2], base_k.to(dev), base_v.to(dev), 5, 5, dst_k, dst_v)
+    K.realign_segment(seg)
+    torch.cuda.synchronize()
+    gk = dst_k[:, :, 5:].cpu().view(torch.int16)
+    gv = dst_v[:, :, 5:].cpu().view(torch.int16)
+    ok = torch.from_numpy(ora["k"]).to(torch.bfloat16).view(torch.int16)
+    ov = torch.from_numpy(ora["v"]).to(torch.bfloat16).view(torch.int16)
+    assert torch.equal(gk, ok) and torch.equal(gv, ov)
+    pool.destroy()
