@@ -2,9 +2,11 @@
 //   * measure_kernel — offset measurement of Algorithm 1's fallback branch:
 //       ΔK = R_{-(s_real - s_base)} K_real - K_base,  ΔV = V_real - V_base   (step a0)
 //     written straight into the pool slab, fp32 math, one RNE rounding to bf16.
-//   * copy_rows_kernel — strided [Ls][Hs][rows][d] row-block copy (p_(m,0) into the
-//     consumer's prompt cache for the concatenation, P:304 / Alg. 1; GIVEN
-//     offsets and embeddings into the pool slab).
+//   * copy_rows_kernel — strided [Ls][Hs][rows][d] row-block copy (GIVEN offsets into
+//     the pool slab; offsets read back for inspection).
+//   * fp8 variants of the insert path.
+// Grids are 2-D: blockIdx.y walks the (layer, head) blocks, x the rows of one block,
+// so the per-element index math is 32-bit (no 64-bit division per vector).
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -13,17 +15,23 @@
 
 namespace kvc {
 
-// One thread per 16-byte vector; rows are d elements = d/8 vectors.
+static dim3 grid2d(int64_t per_block, int threads, int n_lh) {
+  int64_t gx = (per_block + threads - 1) / threads;
+  const int64_t cap = (148 * 16 + n_lh - 1) / n_lh;  // ~16 CTAs per SM overall
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  return dim3(unsigned(gx), unsigned(n_lh < 65535 ? n_lh : 65535));
+}
+
+// One (layer, head) block of rows is contiguous in both src and dst: a flat 16-byte copy.
 __global__ void copy_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, bf16* __restrict__ dst,
-                                 int64_t dst_ld, int Hs, int rows, int vpr, int64_t total) {
-  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < total;
-       x += int64_t(gridDim.x) * blockDim.x) {
-    const int v = int(x % vpr);
-    int64_t r = x / vpr;
-    const int i = int(r % rows);
-    const int64_t lh = r / rows;
-    const uint4 val = ldg128_nc(src + (lh * src_ld + i) * (vpr * 8) + v * 8);
-    *reinterpret_cast<uint4*>(dst + (lh * dst_ld + i) * (vpr * 8) + v * 8) = val;
+                                 int64_t dst_ld, int n_lh, int rows, int d) {
+  const int nvec = rows * (d / 8);
+  for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
+    const uint4* s = reinterpret_cast<const uint4*>(src + int64_t(lh) * src_ld * d);
+    uint4* t = reinterpret_cast<uint4*>(dst + int64_t(lh) * dst_ld * d);
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nvec; x += gridDim.x * blockDim.x)
+      t[x] = ldg128_nc(s + x);
   }
 }
 
@@ -42,10 +50,10 @@ static int grid_for(int64_t work, int threads) {
 
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,
                              int rows, int d, cudaStream_t s) {
-  const int vpr = d / 8;
-  const int64_t total = int64_t(Ls) * Hs * rows * vpr;
-  if (total == 0) return cudaSuccess;
-  copy_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, src_ld, dst, dst_ld, Hs, rows, vpr, total);
+  const int n_lh = Ls * Hs;
+  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
+  copy_rows_kernel<<<grid2d(int64_t(rows) * (d / 8), 256, n_lh), 256, 0, s>>>(src, src_ld, dst, dst_ld, n_lh,
+                                                                              rows, d);
   return cudaGetLastError();
 }
 
@@ -62,8 +70,8 @@ cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t
 // one thread.  cos/sin of δ·inv_freq[f] (fp64 angle) are tabled in shared memory.
 __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
                                const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                               int rows, int Hs, int d, int delta, const double* __restrict__ inv_freq,
-                               bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld, int64_t total) {
+                               int rows, int n_lh, int d, int delta, const double* __restrict__ inv_freq,
+                               bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld) {
   __shared__ float2 cs[128];
   const int half = d / 2;
   for (int f = threadIdx.x; f < half; f += blockDim.x) {
@@ -73,54 +81,54 @@ __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restri
   }
   __syncthreads();
   const int vph = d / 16;  // vector pairs per row
-  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < total;
-       x += int64_t(gridDim.x) * blockDim.x) {
-    const int v = int(x % vph);
-    const int64_t r = x / vph;
-    const int i = int(r % rows);
-    const int64_t lh = r / rows;
-    const int64_t ro = (lh * real_ld + i) * d + v * 8;
-    const int64_t bo = (lh * base_ld + i) * d + v * 8;
-    const int64_t oo = (lh * dst_ld + i) * d + v * 8;
-    const uint4 ka = ldg128_nc(kr + ro), kb2 = ldg128_nc(kr + ro + half);
-    const uint4 ba = ldg128_nc(kb + bo), bb = ldg128_nc(kb + bo + half);
-    const uint4 va = ldg128_nc(vr + ro), vb2 = ldg128_nc(vr + ro + half);
-    const uint4 wa = ldg128_nc(vb + bo), wb = ldg128_nc(vb + bo + half);
-    const uint32_t k0[4] = {ka.x, ka.y, ka.z, ka.w}, k1[4] = {kb2.x, kb2.y, kb2.z, kb2.w};
-    const uint32_t b0[4] = {ba.x, ba.y, ba.z, ba.w}, b1[4] = {bb.x, bb.y, bb.z, bb.w};
-    const uint32_t v0[4] = {va.x, va.y, va.z, va.w}, v1[4] = {vb2.x, vb2.y, vb2.z, vb2.w};
-    const uint32_t w0[4] = {wa.x, wa.y, wa.z, wa.w}, w1[4] = {wb.x, wb.y, wb.z, wb.w};
-    uint32_t ok0[4], ok1[4], ov0[4], ov1[4];
+  const int n = rows * vph;
+  for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+      const int i = x / vph;
+      const int v = x - i * vph;
+      const int64_t ro = (int64_t(lh) * real_ld + i) * d + v * 8;
+      const int64_t bo = (int64_t(lh) * base_ld + i) * d + v * 8;
+      const int64_t oo = (int64_t(lh) * dst_ld + i) * d + v * 8;
+      const uint4 ka = ldg128_nc(kr + ro), kb2 = ldg128_nc(kr + ro + half);
+      const uint4 ba = ldg128_nc(kb + bo), bb = ldg128_nc(kb + bo + half);
+      const uint4 va = ldg128_nc(vr + ro), vb2 = ldg128_nc(vr + ro + half);
+      const uint4 wa = ldg128_nc(vb + bo), wb = ldg128_nc(vb + bo + half);
+      const uint32_t k0[4] = {ka.x, ka.y, ka.z, ka.w}, k1[4] = {kb2.x, kb2.y, kb2.z, kb2.w};
+      const uint32_t b0[4] = {ba.x, ba.y, ba.z, ba.w}, b1[4] = {bb.x, bb.y, bb.z, bb.w};
+      const uint32_t v0[4] = {va.x, va.y, va.z, va.w}, v1[4] = {vb2.x, vb2.y, vb2.z, vb2.w};
+      const uint32_t w0[4] = {wa.x, wa.y, wa.z, wa.w}, w1[4] = {wb.x, wb.y, wb.z, wb.w};
+      uint32_t ok0[4], ok1[4], ov0[4], ov1[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float y0[2], y1[2];
-      const float x0[2] = {bf_lo(k0[e]), bf_hi(k0[e])};
-      const float x1[2] = {bf_lo(k1[e]), bf_hi(k1[e])};
+      for (int e = 0; e < 4; ++e) {
+        float y0[2], y1[2];
+        const float x0[2] = {bf_lo(k0[e]), bf_hi(k0[e])};
+        const float x1[2] = {bf_lo(k1[e]), bf_hi(k1[e])};
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const float2 c = cs[v * 8 + 2 * e + t];
-        y0[t] = x0[t] * c.x - x1[t] * c.y;
-        y1[t] = x1[t] * c.x + x0[t] * c.y;
+        for (int t = 0; t < 2; ++t) {
+          const float2 c = cs[v * 8 + 2 * e + t];
+          y0[t] = x0[t] * c.x - x1[t] * c.y;
+          y1[t] = x1[t] * c.x + x0[t] * c.y;
+        }
+        ok0[e] = pack_bf16_rn(y0[0] - bf_lo(b0[e]), y0[1] - bf_hi(b0[e]));
+        ok1[e] = pack_bf16_rn(y1[0] - bf_lo(b1[e]), y1[1] - bf_hi(b1[e]));
+        ov0[e] = pack_bf16_rn(bf_lo(v0[e]) - bf_lo(w0[e]), bf_hi(v0[e]) - bf_hi(w0[e]));
+        ov1[e] = pack_bf16_rn(bf_lo(v1[e]) - bf_lo(w1[e]), bf_hi(v1[e]) - bf_hi(w1[e]));
       }
-      ok0[e] = pack_bf16_rn(y0[0] - bf_lo(b0[e]), y0[1] - bf_hi(b0[e]));
-      ok1[e] = pack_bf16_rn(y1[0] - bf_lo(b1[e]), y1[1] - bf_hi(b1[e]));
-      ov0[e] = pack_bf16_rn(bf_lo(v0[e]) - bf_lo(w0[e]), bf_hi(v0[e]) - bf_hi(w0[e]));
-      ov1[e] = pack_bf16_rn(bf_lo(v1[e]) - bf_lo(w1[e]), bf_hi(v1[e]) - bf_hi(w1[e]));
+      *reinterpret_cast<uint4*>(dk + oo) = make_uint4(ok0[0], ok0[1], ok0[2], ok0[3]);
+      *reinterpret_cast<uint4*>(dk + oo + half) = make_uint4(ok1[0], ok1[1], ok1[2], ok1[3]);
+      *reinterpret_cast<uint4*>(dv + oo) = make_uint4(ov0[0], ov0[1], ov0[2], ov0[3]);
+      *reinterpret_cast<uint4*>(dv + oo + half) = make_uint4(ov1[0], ov1[1], ov1[2], ov1[3]);
     }
-    *reinterpret_cast<uint4*>(dk + oo) = make_uint4(ok0[0], ok0[1], ok0[2], ok0[3]);
-    *reinterpret_cast<uint4*>(dk + oo + half) = make_uint4(ok1[0], ok1[1], ok1[2], ok1[3]);
-    *reinterpret_cast<uint4*>(dv + oo) = make_uint4(ov0[0], ov0[1], ov0[2], ov0[3]);
-    *reinterpret_cast<uint4*>(dv + oo + half) = make_uint4(ov1[0], ov1[1], ov1[2], ov1[3]);
   }
 }
 
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                            const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
                            const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld, cudaStream_t s) {
-  const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
-  if (total == 0) return cudaSuccess;
-  measure_kernel<<<grid_for(total, 256), 256, 0, s>>>(k_real, v_real, real_ld, k_base, v_base, base_ld, rows,
-                                                       Hs, d, delta, inv_freq, dk, dv, dst_ld, total);
+  const int n_lh = Ls * Hs;
+  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
+  measure_kernel<<<grid2d(int64_t(rows) * (d / 16), 256, n_lh), 256, 0, s>>>(
+      k_real, v_real, real_ld, k_base, v_base, base_ld, rows, n_lh, d, delta, inv_freq, dk, dv, dst_ld);
   return cudaGetLastError();
 }
 
@@ -138,12 +146,17 @@ namespace kvc {
 
 constexpr float kE4M3Max = 448.f;
 
-// max over the vph consecutive lanes that hold one row (groups are aligned and whole)
-__device__ __forceinline__ float group_max(float v, int vph) {
+// A row's vph items sit in a group of G consecutive lanes (G = vph rounded up to a
+// power of two, <= 16: groups never straddle a warp); lanes past vph hold 0.
+__host__ __device__ constexpr int row_group(int vph) {
+  return vph <= 1 ? 1 : vph <= 2 ? 2 : vph <= 4 ? 4 : vph <= 8 ? 8 : 16;
+}
+
+__device__ __forceinline__ float group_max(float v, int G) {
   const int lane = threadIdx.x & 31;
-  const unsigned base = unsigned(lane & ~(vph - 1));
-  const unsigned gmask = (vph == 32 ? 0xffffffffu : (((1u << vph) - 1u) << base));
-  for (int o = vph >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(gmask, v, o));
+  const unsigned base = unsigned(lane & ~(G - 1));
+  const unsigned gmask = (G == 32 ? 0xffffffffu : (((1u << G) - 1u) << base));
+  for (int o = G >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(gmask, v, o));
   return v;
 }
 
@@ -171,9 +184,10 @@ __device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1,
 __device__ __forceinline__ float row_scale(float amax) { return amax > 0.f ? __fdiv_rn(amax, kE4M3Max) : 1.f; }
 
 // Blocked fp8 layout: row i of a (layer, head) region lives in block i / rpb at
-// codes + (i % rpb) * d, its scale at block + rpb * d + (i % rpb) * 4 (rpb = fp8_rows_per_block).  Within a row the
-// codes are stored in 16-byte chunks: chunk v = elements [8v, 8v+8) then [d/2+8v, d/2+8v+8)
-// (the rotate-half pairs the realign kernel's threads own).
+// codes + (i % rpb) * d, its scale at block + rpb * d + (i % rpb) * 4 (rpb =
+// fp8_rows_per_block).  Within a row the codes are stored in 16-byte chunks: chunk v =
+// elements [8v, 8v+8) then [d/2+8v, d/2+8v+8) (the rotate-half pairs the realign
+// kernel's threads own).
 struct Fp8Row {
   uint8_t* code;
   float* scale;
@@ -186,54 +200,53 @@ __device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int 
   return {blk + r * d, reinterpret_cast<float*>(blk + rpb * d) + r};
 }
 
-// bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool)
+// bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool).  x walks
+// (row, lane-in-group); every lane of a group runs the loop body together (the
+// shuffles of group_max), idle lanes with zeros.
 __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
-                                     int64_t lh_bytes, int rows, int d, int64_t total) {
+                                     int64_t lh_bytes, int n_lh, int rows, int d) {
   const int vph = d / 16;
+  const int G = row_group(vph);
   const int half = d / 2;
-  for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < total; base += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t x = base + threadIdx.x;
-    const bool active = x < total;
-    // whole row groups are in or out together (total % vph == 0, blockDim % 32 == 0)
-    if (!active && (base + (threadIdx.x & ~31)) >= total) continue;
-    float f0[8], f1[8];
-    int64_t r = 0;
-    int v = 0;
-    if (active) {
-      v = int(x % vph);
-      r = x / vph;
-      const int i = int(r % rows);
-      const int64_t lh = r / rows;
-      const bf16* sp = src + (lh * src_ld + i) * d + v * 8;
-      const uint4 a = ldg128_nc(sp), b = ldg128_nc(sp + half);
-      const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+  const int n = rows * G;
+  for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+      const int x = base + threadIdx.x;
+      const int i = x / G;
+      const int v = x - i * G;
+      const bool active = i < rows && v < vph;
+      float f0[8], f1[8];
+      if (active) {
+        const bf16* sp = src + (int64_t(lh) * src_ld + i) * d + v * 8;
+        const uint4 a = ldg128_nc(sp), b = ldg128_nc(sp + half);
+        const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        f0[2 * t] = bf_lo(av[t]); f0[2 * t + 1] = bf_hi(av[t]);
-        f1[2 * t] = bf_lo(bv[t]); f1[2 * t + 1] = bf_hi(bv[t]);
+        for (int t = 0; t < 4; ++t) {
+          f0[2 * t] = bf_lo(av[t]); f0[2 * t + 1] = bf_hi(av[t]);
+          f1[2 * t] = bf_lo(bv[t]); f1[2 * t + 1] = bf_hi(bv[t]);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f0[t] = f1[t] = 0.f;
       }
-    } else {
+      float m = 0.f;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) f0[t] = f1[t] = 0.f;
+      for (int t = 0; t < 8; ++t) m = fmaxf(m, fmaxf(fabsf(f0[t]), fabsf(f1[t])));
+      m = group_max(m, G);
+      if (!active) continue;
+      const float sc = row_scale(m);
+      const Fp8Row o = fp8_row(dst, lh, i, d, lh_bytes);
+      store_fp8_item(f0, f1, sc, o.code + v * 16, o.code + v * 16 + 8);
+      if (v == 0) *o.scale = sc;
     }
-    float m = 0.f;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) m = fmaxf(m, fmaxf(fabsf(f0[t]), fabsf(f1[t])));
-    m = group_max(m, vph);
-    if (!active) continue;
-    const float sc = row_scale(m);
-    const Fp8Row o = fp8_row(dst, r / rows, int(r % rows), d, lh_bytes);
-    store_fp8_item(f0, f1, sc, o.code + v * 16, o.code + v * 16 + 8);
-    if (v == 0) *o.scale = sc;
   }
 }
 
 // Offset measurement straight into an fp8 pool (fp32 Δ, one quantisation).
 __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
                                    const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                                   int rows, int d, int delta, const double* __restrict__ inv_freq,
-                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes,
-                                   int64_t total) {
+                                   int n_lh, int rows, int d, int delta, const double* __restrict__ inv_freq,
+                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes) {
   __shared__ float2 cs[128];
   const int half = d / 2;
   for (int f = threadIdx.x; f < half; f += blockDim.x) {
@@ -243,60 +256,57 @@ __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __re
   }
   __syncthreads();
   const int vph = d / 16;
-  for (int64_t base = blockIdx.x * int64_t(blockDim.x); base < total; base += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t x = base + threadIdx.x;
-    const bool active = x < total;
-    if (!active && (base + (threadIdx.x & ~31)) >= total) continue;
-    float k0[8], k1[8], v0[8], v1[8];
-    int v = 0;
-    int64_t r = 0;
-    if (active) {
-      v = int(x % vph);
-      r = x / vph;
-      const int i = int(r % rows);
-      const int64_t lh = r / rows;
-      const int64_t ro = (lh * real_ld + i) * d + v * 8;
-      const int64_t bo = (lh * base_ld + i) * d + v * 8;
-      const uint4 ka = ldg128_nc(kr + ro), kc = ldg128_nc(kr + ro + half);
-      const uint4 ba = ldg128_nc(kb + bo), bc = ldg128_nc(kb + bo + half);
-      const uint4 va = ldg128_nc(vr + ro), vc = ldg128_nc(vr + ro + half);
-      const uint4 wa = ldg128_nc(vb + bo), wc = ldg128_nc(vb + bo + half);
-      const uint32_t K0[4] = {ka.x, ka.y, ka.z, ka.w}, K1[4] = {kc.x, kc.y, kc.z, kc.w};
-      const uint32_t B0[4] = {ba.x, ba.y, ba.z, ba.w}, B1[4] = {bc.x, bc.y, bc.z, bc.w};
-      const uint32_t V0[4] = {va.x, va.y, va.z, va.w}, V1[4] = {vc.x, vc.y, vc.z, vc.w};
-      const uint32_t W0[4] = {wa.x, wa.y, wa.z, wa.w}, W1[4] = {wc.x, wc.y, wc.z, wc.w};
+  const int G = row_group(vph);
+  const int n = rows * G;
+  for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+      const int x = base + threadIdx.x;
+      const int i = x / G;
+      const int v = x - i * G;
+      const bool active = i < rows && v < vph;
+      float k0[8], k1[8], v0[8], v1[8];
+      if (active) {
+        const int64_t ro = (int64_t(lh) * real_ld + i) * d + v * 8;
+        const int64_t bo = (int64_t(lh) * base_ld + i) * d + v * 8;
+        const uint4 ka = ldg128_nc(kr + ro), kc = ldg128_nc(kr + ro + half);
+        const uint4 ba = ldg128_nc(kb + bo), bc = ldg128_nc(kb + bo + half);
+        const uint4 va = ldg128_nc(vr + ro), vc = ldg128_nc(vr + ro + half);
+        const uint4 wa = ldg128_nc(vb + bo), wc = ldg128_nc(vb + bo + half);
+        const uint32_t K0[4] = {ka.x, ka.y, ka.z, ka.w}, K1[4] = {kc.x, kc.y, kc.z, kc.w};
+        const uint32_t B0[4] = {ba.x, ba.y, ba.z, ba.w}, B1[4] = {bc.x, bc.y, bc.z, bc.w};
+        const uint32_t V0[4] = {va.x, va.y, va.z, va.w}, V1[4] = {vc.x, vc.y, vc.z, vc.w};
+        const uint32_t W0[4] = {wa.x, wa.y, wa.z, wa.w}, W1[4] = {wc.x, wc.y, wc.z, wc.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x0 = (e & 1) ? bf_hi(K0[e / 2]) : bf_lo(K0[e / 2]);
+          const float x1 = (e & 1) ? bf_hi(K1[e / 2]) : bf_lo(K1[e / 2]);
+          const float2 c = cs[v * 8 + e];
+          k0[e] = (x0 * c.x - x1 * c.y) - ((e & 1) ? bf_hi(B0[e / 2]) : bf_lo(B0[e / 2]));
+          k1[e] = (x1 * c.x + x0 * c.y) - ((e & 1) ? bf_hi(B1[e / 2]) : bf_lo(B1[e / 2]));
+          v0[e] = ((e & 1) ? bf_hi(V0[e / 2]) : bf_lo(V0[e / 2])) - ((e & 1) ? bf_hi(W0[e / 2]) : bf_lo(W0[e / 2]));
+          v1[e] = ((e & 1) ? bf_hi(V1[e / 2]) : bf_lo(V1[e / 2])) - ((e & 1) ? bf_hi(W1[e / 2]) : bf_lo(W1[e / 2]));
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) k0[e] = k1[e] = v0[e] = v1[e] = 0.f;
+      }
+      float mk = 0.f, mv = 0.f;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float x0 = (e & 1) ? bf_hi(K0[e / 2]) : bf_lo(K0[e / 2]);
-        const float x1 = (e & 1) ? bf_hi(K1[e / 2]) : bf_lo(K1[e / 2]);
-        const float2 c = cs[v * 8 + e];
-        k0[e] = (x0 * c.x - x1 * c.y) - ((e & 1) ? bf_hi(B0[e / 2]) : bf_lo(B0[e / 2]));
-        k1[e] = (x1 * c.x + x0 * c.y) - ((e & 1) ? bf_hi(B1[e / 2]) : bf_lo(B1[e / 2]));
-        v0[e] = ((e & 1) ? bf_hi(V0[e / 2]) : bf_lo(V0[e / 2])) - ((e & 1) ? bf_hi(W0[e / 2]) : bf_lo(W0[e / 2]));
-        v1[e] = ((e & 1) ? bf_hi(V1[e / 2]) : bf_lo(V1[e / 2])) - ((e & 1) ? bf_hi(W1[e / 2]) : bf_lo(W1[e / 2]));
+        mk = fmaxf(mk, fmaxf(fabsf(k0[e]), fabsf(k1[e])));
+        mv = fmaxf(mv, fmaxf(fabsf(v0[e]), fabsf(v1[e])));
       }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) k0[e] = k1[e] = v0[e] = v1[e] = 0.f;
-    }
-    float mk = 0.f, mv = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      mk = fmaxf(mk, fmaxf(fabsf(k0[e]), fabsf(k1[e])));
-      mv = fmaxf(mv, fmaxf(fabsf(v0[e]), fabsf(v1[e])));
-    }
-    mk = group_max(mk, vph);
-    mv = group_max(mv, vph);
-    if (!active) continue;
-    const int i = int(r % rows);
-    const int64_t lh = r / rows;
-    const float sck = row_scale(mk), scv = row_scale(mv);
-    const Fp8Row ok = fp8_row(dk, lh, i, d, lh_bytes), ov = fp8_row(dv, lh, i, d, lh_bytes);
-    store_fp8_item(k0, k1, sck, ok.code + v * 16, ok.code + v * 16 + 8);
-    store_fp8_item(v0, v1, scv, ov.code + v * 16, ov.code + v * 16 + 8);
-    if (v == 0) {
-      *ok.scale = sck;
-      *ov.scale = scv;
+      mk = group_max(mk, G);
+      mv = group_max(mv, G);
+      if (!active) continue;
+      const float sck = row_scale(mk), scv = row_scale(mv);
+      const Fp8Row ok = fp8_row(dk, lh, i, d, lh_bytes), ov = fp8_row(dv, lh, i, d, lh_bytes);
+      store_fp8_item(k0, k1, sck, ok.code + v * 16, ok.code + v * 16 + 8);
+      store_fp8_item(v0, v1, scv, ov.code + v * 16, ov.code + v * 16 + 8);
+      if (v == 0) {
+        *ok.scale = sck;
+        *ov.scale = scv;
+      }
     }
   }
 }
@@ -320,19 +330,20 @@ __global__ void read_fp8_kernel(const uint8_t* __restrict__ src, int64_t lh_byte
 
 cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
                                  int rows, int d, cudaStream_t s) {
-  const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
-  if (total == 0) return cudaSuccess;
-  quantize_rows_kernel<<<grid_for(total, 256), 256, 0, s>>>(src, src_ld, dst, lh_bytes, rows, d, total);
+  const int n_lh = Ls * Hs;
+  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
+  quantize_rows_kernel<<<grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh), 256, 0, s>>>(
+      src, src_ld, dst, lh_bytes, n_lh, rows, d);
   return cudaGetLastError();
 }
 
 cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                                const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
                                const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes, cudaStream_t s) {
-  const int64_t total = int64_t(Ls) * Hs * rows * (d / 16);
-  if (total == 0) return cudaSuccess;
-  measure_fp8_kernel<<<grid_for(total, 256), 256, 0, s>>>(k_real, v_real, real_ld, k_base, v_base, base_ld, rows, d,
-                                                          delta, inv_freq, dk, dv, lh_bytes, total);
+  const int n_lh = Ls * Hs;
+  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
+  measure_fp8_kernel<<<grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh), 256, 0, s>>>(
+      k_real, v_real, real_ld, k_base, v_base, base_ld, n_lh, rows, d, delta, inv_freq, dk, dv, lh_bytes);
   return cudaGetLastError();
 }
 

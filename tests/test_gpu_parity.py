@@ -287,7 +287,8 @@ def _fp8_codes(q: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(q.astype(np.float32)).to(torch.float8_e4m3fn).view(torch.uint8)
 
 
-@pytest.mark.parametrize("d,L_phi,P", [(128, 150, 37), (64, 200, 5), (256, 70, 32)])
+@pytest.mark.parametrize("d,L_phi,P", [(128, 150, 37), (64, 200, 5), (256, 70, 32), (80, 100, 7), (96, 90, 11),
+                                        (192, 50, 40)])
 def test_fp8_offsets_codes_and_realign(d, L_phi, P):
     """f3: e4m3 offset storage.  GIVEN offsets are quantised on the device to the same
     codes and scales as the oracle's quantiser (bit-exact), and the realignment from
