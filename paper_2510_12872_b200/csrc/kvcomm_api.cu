@@ -276,7 +276,9 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     for (int i = 0; i < p->C; ++i) zero(p->pf8[i], int64_t(p->cap) * p->f8_pf_slot(i));
   }
   ALLOC(p->inv_freq_dev, p->d / 2, "inv_freq");
-  ALLOC(p->d_partial, int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1), "partial sums");
+  // [position blocks][2cap+1] partial sums, then [kMatchChunks][2cap+1] chunk sums
+  ALLOC(p->d_partial, (int64_t((p->maxlen + kMatchP - 1) / kMatchP) + kMatchChunks) * (2 * p->cap + 1),
+        "partial sums");
 #undef ALLOC
 #undef ALLOC_OFF
   cudaError_t e = cudaMemcpy(p->inv_freq_dev, p->inv_freq.data(), sizeof(double) * (p->d / 2),
@@ -722,6 +724,7 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     a.idx = it.top_k > 0 ? it.idx : nullptr;
     a.dist_user = it.dist;
     a.partial = p->d_partial;
+    a.chunks = p->d_partial + int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1);
     a.wbar = it.wbar;
     a.gamma = double(it.gamma);
     a.n_cand = it.info->n_candidates;
@@ -918,7 +921,7 @@ KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* 
   write_match(h, L, items);
   KV_CUDA(cudaMemcpyAsync(E.dev, E.host, L.bytes, cudaMemcpyHostToDevice, s));
   KV_CUDA(launch_match_batch(E.dev, L.hdr, L.smem, s));
-  g_launches += 2;
+  g_launches += 3;  // distances + weights, chunk sums, finalize
   KV_CUDA(cudaMemcpyAsync(h + L.hdr.res_off, static_cast<uint8_t*>(E.dev) + L.hdr.res_off,
                           L.bytes - size_t(L.hdr.res_off), cudaMemcpyDeviceToHost, s));
   KV_CUDA(cudaEventRecord(E.done, s));
@@ -1382,7 +1385,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
   KV_CUDA(cudaMemcpyAsync(dv, h, hs.empty() ? ML.bytes : roff + size_t(RL.hdr.cs_off), cudaMemcpyHostToDevice, s));
   if (!items.empty()) {
     KV_CUDA(launch_match_batch(dv, ML.hdr, ML.smem, s));
-    g_launches += 2;
+    g_launches += 3;
   }
   if (pl->ev_before) KV_CUDA(cudaEventRecord(pl->ev_before, s));
   if (!hs.empty()) {

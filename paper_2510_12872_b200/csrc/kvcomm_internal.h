@@ -18,6 +18,7 @@ constexpr int kStageStride = kStageBytes + 1024;  // an fp8 block (codes + row s
 constexpr int kUnitWBytes = KVC_UNITW;  // weight chunk buffer: [anchors][weight_row_stride] floats
 constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
 constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
+constexpr int kMatchChunks = 32;    // position-block chunks of the two-pass d̄ reduction
 
 // rows per realign tile (16 KiB of bf16 rows) for head_dim d
 __host__ __device__ constexpr int rows_per_tile(int d) { return kStageBytes / (2 * d); }
@@ -92,6 +93,7 @@ struct MatchJob {
   int32_t* idx;             // [L_phi][top_k] or null
   double* dist_user;        // optional [cap][ld_w]
   double* partial;          // pool scratch [n_blocks][stride]: stride n_cand (l2) or 2 n_cand + 1 (cosine)
+  double* chunks;           // pool scratch [kMatchChunks][stride]: fixed-order sums of chunks of blocks
   float* wbar;              // [cap]
   double gamma;
   int32_t n_cand, cap, L_phi, De;

@@ -276,6 +276,30 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
   }
 }
 
+// First pass of d̄ (and the cosine sums): block (job, c) sums position blocks
+// [c*per, (c+1)*per) of every partial column in order (4 interleaved accumulators,
+// combined in order) into chunk row c.  Columns are coalesced across threads.
+__global__ void __launch_bounds__(256) match_chunk_kernel(const uint8_t* __restrict__ tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  const MatchJob& a = reinterpret_cast<const MatchJob*>(tab + hdr->job_off)[blockIdx.x];
+  const int c = blockIdx.y;
+  const int per = (a.n_blocks + kMatchChunks - 1) / kMatchChunks;
+  const int b0 = c * per, b1 = min(a.n_blocks, b0 + per);
+  const int stride = a.cosine ? 2 * a.n_cand + 1 : a.n_cand;
+  for (int col = threadIdx.x; col < stride; col += blockDim.x) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    int b = b0;
+    for (; b + 4 <= b1; b += 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s[k] += a.partial[int64_t(b + k) * stride + col];
+    }
+    if (b < b1) s[0] += a.partial[int64_t(b) * stride + col];
+    if (b + 1 < b1) s[1] += a.partial[int64_t(b + 1) * stride + col];
+    if (b + 2 < b1) s[2] += a.partial[int64_t(b + 2) * stride + col];
+    a.chunks[int64_t(c) * stride + col] = (s[0] + s[1]) + (s[2] + s[3]);
+  }
+}
+
 // Fixed-order tree reduction over 1024 entries in shared memory.
 template <bool kMin>
 __device__ double block_reduce_1024(double* buf, double v) {
@@ -304,23 +328,19 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
   // per candidate: lanes stride over the position blocks in a fixed order, then a
   // butterfly (identical in every lane, deterministic)
   if (!a.cosine) {
+    static_assert(kMatchChunks == 32, "one chunk per lane");
     for (int j = warp; j < a.n_cand; j += 32) {
-      double s = 0.0;
-      for (int b = lane; b < a.n_blocks; b += 32) s += a.partial[int64_t(b) * a.n_cand + j];
+      double s = a.chunks[int64_t(lane) * a.n_cand + j];
       s = warp_sum_d(s);
       if (lane == 0) dsh[j] = a.scalar_mode == 0 ? sqrt(s) : s / double(a.L_phi);
     }
   } else {
     const int64_t stride = 2 * a.n_cand + 1;
-    double sqq = 0.0;  // every warp sums Σ q·q in the same order (identical values)
-    for (int b = lane; b < a.n_blocks; b += 32) sqq += a.partial[int64_t(b) * stride + 2 * a.n_cand];
+    double sqq = a.chunks[int64_t(lane) * stride + 2 * a.n_cand];  // every warp: same order, same value
     sqq = warp_sum_d(sqq);
     for (int j = warp; j < a.n_cand; j += 32) {
-      double sqa = 0.0, saa = 0.0;
-      for (int b = lane; b < a.n_blocks; b += 32) {
-        sqa += a.partial[int64_t(b) * stride + j];
-        saa += a.partial[int64_t(b) * stride + a.n_cand + j];
-      }
+      double sqa = a.chunks[int64_t(lane) * stride + j];
+      double saa = a.chunks[int64_t(lane) * stride + a.n_cand + j];
       sqa = warp_sum_d(sqa);
       saa = warp_sum_d(saa);
       const double den = sqrt(sqq * saa);
@@ -367,6 +387,7 @@ cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_dist_kernel, kMatchThreads, smem);
   const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));
   match_dist_kernel<<<grid, kMatchThreads, smem, s>>>(t);
+  match_chunk_kernel<<<dim3(hdr.n_jobs, kMatchChunks), 256, 0, s>>>(t);
   match_finalize_kernel<<<hdr.n_jobs, 1024, 0, s>>>(t);
   return cudaGetLastError();
 }
