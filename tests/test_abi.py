@@ -37,7 +37,7 @@ def test_ctypes_layout_matches_c_header():
 int main(void) {
   S(kvcomm_pool_config) S(kvcomm_kv_view) S(kvcomm_offset_desc) S(kvcomm_slot_info)
   S(kvcomm_match_info) S(kvcomm_realign_desc) S(kvcomm_segment_ref) S(kvcomm_match_request)
-  S(kvcomm_plan_match) S(kvcomm_plan_segment) S(kvcomm_plan_agent)
+  S(kvcomm_plan_match) S(kvcomm_plan_segment) S(kvcomm_plan_agent) S(kvcomm_ipc_handle)
   O(kvcomm_plan_segment, base) O(kvcomm_plan_segment, target_start) O(kvcomm_plan_agent, dst_ld)
   O(kvcomm_pool_config, prefix_len) O(kvcomm_pool_config, inv_freq)
   O(kvcomm_match_info, entropy) O(kvcomm_match_info, tie_band_count)
@@ -56,7 +56,8 @@ int main(void) {
     py = {"kvcomm_pool_config": L.PoolConfig, "kvcomm_kv_view": L.KVView, "kvcomm_offset_desc": L.OffsetDesc,
           "kvcomm_slot_info": L.SlotInfo, "kvcomm_match_info": L.MatchInfo, "kvcomm_realign_desc": L.RealignDesc,
           "kvcomm_segment_ref": L.SegmentRef, "kvcomm_match_request": L.MatchRequest,
-          "kvcomm_plan_match": L.PlanMatch, "kvcomm_plan_segment": L.PlanSegment, "kvcomm_plan_agent": L.PlanAgent}
+          "kvcomm_plan_match": L.PlanMatch, "kvcomm_plan_segment": L.PlanSegment, "kvcomm_plan_agent": L.PlanAgent,
+          "kvcomm_ipc_handle": L.IpcHandle}
     for k, T in py.items():
         assert int(got[k]) == C.sizeof(T), k
     for key, v in got.items():
@@ -105,3 +106,14 @@ def test_pool_create_rejects_bad_geometry_before_touching_a_device():
 def test_binding_fails_loudly_without_library(tmp_path):
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         L.load(str(tmp_path / "missing.so"))
+
+
+def test_ipc_calls_validate_arguments_before_any_device_work():
+    """The fused-gather handle calls reject null/size errors with a status (no crash)."""
+    lib = L.load()
+    ptr = C.c_void_p()
+    h = L.IpcHandle()
+    assert lib.kvcomm_ipc_alloc(0, 0, C.byref(ptr), C.byref(h)) == 1            # INVALID_ARGUMENT: size
+    assert lib.kvcomm_ipc_alloc(0, 64, None, C.byref(h)) == 1                   # null out pointer
+    assert lib.kvcomm_ipc_open(0, None, C.byref(ptr)) == 1
+    assert lib.kvcomm_ipc_free(None) == 0 and lib.kvcomm_ipc_close(None) == 0   # no-ops
