@@ -78,6 +78,7 @@ typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_s
 typedef enum { KVCOMM_SIM_L2 = 0, KVCOMM_SIM_COSINE = 1 } kvcomm_similarity;
 typedef enum { KVCOMM_OFFSET_BF16 = 0, KVCOMM_OFFSET_FP8_E4M3 = 1 } kvcomm_offset_format;
 typedef enum { KVCOMM_PLACE_DEVICE = 0, KVCOMM_PLACE_HOST = 1 } kvcomm_placement;
+typedef enum { KVCOMM_ROPE_HALF = 0, KVCOMM_ROPE_INTERLEAVED = 1 } kvcomm_rope_layout;
 /* COPY: rows copied verbatim (no offsets, no rotation; bit-exact), e.g. p_(m,0) of the
  * concatenation (reading A20) riding in the same launch as the realignment. */
 typedef enum { KVCOMM_PLACEHOLDER = 0, KVCOMM_PREFIX = 1, KVCOMM_COPY = 2 } kvcomm_segment_kind;
@@ -116,6 +117,11 @@ typedef struct {
                               slabs live in pinned, mapped host memory and the same kernels
                               stream them over the host link (the CPU-offloaded anchors of
                               A.4.4: pools larger than HBM)                  */
+  int32_t rope_layout;     /* RoPE pairing of K's head dimension (reading A12):
+                              KVCOMM_ROPE_HALF (0, default): HF rotate_half, pairs (f, f + d/2);
+                              KVCOMM_ROPE_INTERLEAVED (1): GPT-J style, pairs (2f, 2f + 1).
+                              Both rotate pair f by δ·inv_freq[f].                        */
+  int32_t _reserved;       /* 0 */
   const int32_t* prefix_len; /* host [num_consumers]: |p_(m,i)| following this placeholder */
   const double* inv_freq;  /* host [head_dim/2]: RoPE inverse frequencies (copied)        */
 } kvcomm_pool_config;

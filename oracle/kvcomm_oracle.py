@@ -73,12 +73,17 @@ def bf16_round(x) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
-def rope_rotate(x: np.ndarray, delta: int, inv_freq: np.ndarray) -> np.ndarray:
-    """Apply R_δ to key vectors x[..., d] (HF `rotate_half` pairing, reading A12).
+HALF, INTERLEAVED = "half", "interleaved"  # RoPE pairings (reading A12)
 
-    For f < d/2 with angle a_f = δ · inv_freq[f] (float64, reading A13):
-        y[f]       = x[f]       cos a_f - x[f + d/2] sin a_f
-        y[f + d/2] = x[f + d/2] cos a_f + x[f]       sin a_f
+
+def rope_rotate(x: np.ndarray, delta: int, inv_freq: np.ndarray, layout: str = HALF) -> np.ndarray:
+    """Apply R_δ to key vectors x[..., d] (reading A12).
+
+    For f < d/2 with angle a_f = δ · inv_freq[f] (float64, reading A13), pair f is
+    (f, f + d/2) for HF `rotate_half` (default) or (2f, 2f + 1) for the interleaved
+    (GPT-J) layout; with (u, w) the pair:
+        u' = u cos a_f - w sin a_f
+        w' = w cos a_f + u sin a_f
     R_0 = I exactly; R_a R_b = R_{a+b}; R_δ is orthogonal ("orthogonal rotation").
     """
     x = np.asarray(x, dtype=np.float64)
@@ -88,8 +93,16 @@ def rope_rotate(x: np.ndarray, delta: int, inv_freq: np.ndarray) -> np.ndarray:
         return x.copy()
     a = float(delta) * np.asarray(inv_freq, dtype=np.float64)
     c, s = np.cos(a), np.sin(a)
-    x1, x2 = x[..., : d // 2], x[..., d // 2:]
-    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+    if layout == HALF:
+        x1, x2 = x[..., : d // 2], x[..., d // 2:]
+        return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+    if layout == INTERLEAVED:
+        u, w = x[..., 0::2], x[..., 1::2]
+        y = np.empty_like(x)
+        y[..., 0::2] = u * c - w * s
+        y[..., 1::2] = w * c + u * s
+        return y
+    raise ValueError(layout)
 
 
 # ---------------------------------------------------------------------------
@@ -98,14 +111,14 @@ def rope_rotate(x: np.ndarray, delta: int, inv_freq: np.ndarray) -> np.ndarray:
 
 
 def measure_offset(k_real, v_real, s_real: int, k_base, v_base, s_base: int,
-                   inv_freq: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+                   inv_freq: np.ndarray, layout: str = HALF) -> Tuple[np.ndarray, np.ndarray]:
     """Δk = R_{-(s_real - s_base)} k_real - k_base ;  Δv = v_real - v_base.
 
     Keys are de-rotated into the base frame before differencing ("always
     de-rotates the stored key by R_{-Δ}", reading A10).  Returns float64; the
     stored pool value is bf16_round of it.
     """
-    dk = rope_rotate(k_real, -(s_real - s_base), inv_freq) - np.asarray(k_base, np.float64)
+    dk = rope_rotate(k_real, -(s_real - s_base), inv_freq, layout) - np.asarray(k_base, np.float64)
     dv = np.asarray(v_real, np.float64) - np.asarray(v_base, np.float64)
     return dk, dv
 
@@ -314,7 +327,7 @@ def blend_prefix(wbar: np.ndarray, offsets: Sequence[np.ndarray]) -> np.ndarray:
 
 
 def apply_offset(k_base, v_base, dk_hat, dv_hat, delta: int,
-                 inv_freq: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+                 inv_freq: np.ndarray, layout: str = HALF) -> Tuple[np.ndarray, np.ndarray]:
     """K̂ = R_δ(K_base + Δ̂K),  V̂ = V_base + Δ̂V   (reading A10).
 
     Offsets live in the base frame, so the sum is re-rotated by δ = target_start -
@@ -322,14 +335,14 @@ def apply_offset(k_base, v_base, dk_hat, dv_hat, delta: int,
     de-rotation/re-rotation, adding the estimated Key/Value offsets").
     Returns float64 (caller rounds with bf16_round).
     """
-    k = rope_rotate(np.asarray(k_base, np.float64) + dk_hat, delta, inv_freq)
+    k = rope_rotate(np.asarray(k_base, np.float64) + dk_hat, delta, inv_freq, layout)
     v = np.asarray(v_base, np.float64) + dv_hat
     return k, v
 
 
 def realign_segment(weights: np.ndarray, k_base, v_base, dk: Sequence[np.ndarray],
                     dv: Sequence[np.ndarray], base_start: int, target_start: int,
-                    inv_freq: np.ndarray, kind: str = "placeholder"):
+                    inv_freq: np.ndarray, kind: str = "placeholder", layout: str = HALF):
     """One segment of Algorithm 1's reuse branch.
 
     kind = "placeholder": weights is W [L_seg, n] and Eq. 6 applies;
@@ -344,7 +357,7 @@ def realign_segment(weights: np.ndarray, k_base, v_base, dk: Sequence[np.ndarray
         dv_hat = blend_prefix(weights, dv)
     else:
         raise ValueError(kind)
-    k, v = apply_offset(k_base, v_base, dk_hat, dv_hat, target_start - base_start, inv_freq)
+    k, v = apply_offset(k_base, v_base, dk_hat, dv_hat, target_start - base_start, inv_freq, layout)
     return {"dk_hat": dk_hat, "dv_hat": dv_hat, "k": bf16_round(k), "v": bf16_round(v),
             "k64": k, "v64": v}
 

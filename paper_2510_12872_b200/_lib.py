@@ -29,6 +29,7 @@ SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1
 SIM_L2, SIM_COSINE = 0, 1
 OFFSET_BF16, OFFSET_FP8_E4M3 = 0, 1
 PLACE_DEVICE, PLACE_HOST = 0, 1
+ROPE_HALF, ROPE_INTERLEAVED = 0, 1
 
 
 class PoolConfig(C.Structure):
@@ -37,7 +38,8 @@ class PoolConfig(C.Structure):
                 ("head_end", C.c_int32), ("head_dim", C.c_int32), ("emb_dim", C.c_int32),
                 ("capacity", C.c_int32), ("max_anchor_len", C.c_int32), ("num_consumers", C.c_int32),
                 ("scalar_distance", C.c_int32), ("similarity", C.c_int32),
-                ("offset_format", C.c_int32), ("placement", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
+                ("offset_format", C.c_int32), ("placement", C.c_int32), ("rope_layout", C.c_int32),
+                ("_reserved", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
 
 
 class KVView(C.Structure):

@@ -220,6 +220,8 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "offset_format %d", c->offset_format);
   if (c->placement != KVCOMM_PLACE_DEVICE && c->placement != KVCOMM_PLACE_HOST)
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "placement %d", c->placement);
+  if (c->rope_layout != KVCOMM_ROPE_HALF && c->rope_layout != KVCOMM_ROPE_INTERLEAVED)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "rope_layout %d", c->rope_layout);
   if (c->offset_format == KVCOMM_OFFSET_FP8_E4M3 && c->head_dim < 64)
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "fp8 offsets need head_dim >= 64 (got %d)", c->head_dim);
   for (int i = 0; i < c->num_consumers; ++i)
@@ -371,12 +373,13 @@ static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, 
   const auto* vr = static_cast<const bf16*>(real.v);
   const auto* kb = static_cast<const bf16*>(base.k);
   const auto* vb = static_cast<const bf16*>(base.v);
+  const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
   if (!p->fp8)
     KV_CUDA(launch_measure(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d, delta,
-                           p->inv_freq_dev, d.k, d.v, d.ld, s));
+                           il, p->inv_freq_dev, d.k, d.v, d.ld, s));
   else
     KV_CUDA(launch_measure_fp8(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d,
-                               delta, p->inv_freq_dev, d.k8, d.v8, d.lh_bytes, s));
+                               delta, il, p->inv_freq_dev, d.k8, d.v8, d.lh_bytes, s));
   g_launches += 1;
   return KVCOMM_OK;
 }
@@ -1021,6 +1024,7 @@ static HostSeg host_segment(const kvcomm_realign_desc& g, int32_t dst_stg = -1) 
   x.dst[1] = static_cast<bf16*>(g.dst_v);
   x.dst_ld = g.dst_ld;
   x.dst_stg = dst_stg >= 0 ? dst_stg : dst_store_mode(g.dst_k, p->cfg.device);
+  x.rope_il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
   x.inv_freq = p->inv_freq_dev;
   x.L_seg = g.L_seg;
   x.target_start = g.target_start;

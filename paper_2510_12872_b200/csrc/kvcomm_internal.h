@@ -60,7 +60,7 @@ struct SegDev {
   int64_t wt_off;       // float offset of this segment's weight blocks in Table::wt
   int32_t dst_stg;      // 1: write rows with per-thread stores (destination on a peer GPU, mapped by
                         //   CUDA IPC: the fused gather of SURVEY §8(e)), 0: TMA bulk store
-  int32_t _pad3;
+  int32_t rope_il;      // K's RoPE pairs: 0 (f, f + d/2) rotate_half, 1 (2f, 2f + 1) interleaved
 };
 
 struct MatchResultDev {
@@ -125,13 +125,15 @@ cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, 
                                  int rows, int d, cudaStream_t s);
 cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                                const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes, cudaStream_t s);
+                               int interleaved, const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes,
+                               cudaStream_t s);
 // blocked e4m3 rows -> dense codes [lh][rows][d] + scales [lh][rows] (inspection / tests)
 cudaError_t launch_read_fp8(const uint8_t* src, int64_t lh_bytes, uint8_t* codes, float* scales, int Ls, int Hs,
                             int rows, int d, cudaStream_t s);
 // Offset measurement (insert path, step a0).
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                            const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                           const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld, cudaStream_t s);
+                           int interleaved, const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld,
+                           cudaStream_t s);
 
 }  // namespace kvc

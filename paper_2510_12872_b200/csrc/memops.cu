@@ -70,7 +70,7 @@ cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t
 // one thread.  cos/sin of δ·inv_freq[f] (fp64 angle) are tabled in shared memory.
 __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
                                const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                               int rows, int n_lh, int d, int delta, const double* __restrict__ inv_freq,
+                               int rows, int n_lh, int d, int delta, int il, const double* __restrict__ inv_freq,
                                bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld) {
   __shared__ float2 cs[128];
   const int half = d / 2;
@@ -103,11 +103,19 @@ __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restri
         float y0[2], y1[2];
         const float x0[2] = {bf_lo(k0[e]), bf_hi(k0[e])};
         const float x1[2] = {bf_lo(k1[e]), bf_hi(k1[e])};
+        if (!il) {  // rotate_half: pair (f, f + d/2)
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const float2 c = cs[v * 8 + 2 * e + t];
-          y0[t] = x0[t] * c.x - x1[t] * c.y;
-          y1[t] = x1[t] * c.x + x0[t] * c.y;
+          for (int t = 0; t < 2; ++t) {
+            const float2 c = cs[v * 8 + 2 * e + t];
+            y0[t] = x0[t] * c.x - x1[t] * c.y;
+            y1[t] = x1[t] * c.x + x0[t] * c.y;
+          }
+        } else {    // interleaved: (lo, hi) of one word are the pair (2f, 2f + 1)
+          const float2 ca = cs[4 * v + e], cb = cs[d / 4 + 4 * v + e];
+          y0[0] = x0[0] * ca.x - x0[1] * ca.y;
+          y0[1] = x0[1] * ca.x + x0[0] * ca.y;
+          y1[0] = x1[0] * cb.x - x1[1] * cb.y;
+          y1[1] = x1[1] * cb.x + x1[0] * cb.y;
         }
         ok0[e] = pack_bf16_rn(y0[0] - bf_lo(b0[e]), y0[1] - bf_hi(b0[e]));
         ok1[e] = pack_bf16_rn(y1[0] - bf_lo(b1[e]), y1[1] - bf_hi(b1[e]));
@@ -124,11 +132,12 @@ __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restri
 
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                            const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                           const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld, cudaStream_t s) {
+                           int interleaved, const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld,
+                           cudaStream_t s) {
   const int n_lh = Ls * Hs;
   if (int64_t(n_lh) * rows == 0) return cudaSuccess;
   measure_kernel<<<grid2d(int64_t(rows) * (d / 16), 256, n_lh), 256, 0, s>>>(
-      k_real, v_real, real_ld, k_base, v_base, base_ld, rows, n_lh, d, delta, inv_freq, dk, dv, dst_ld);
+      k_real, v_real, real_ld, k_base, v_base, base_ld, rows, n_lh, d, delta, interleaved, inv_freq, dk, dv, dst_ld);
   return cudaGetLastError();
 }
 
@@ -245,7 +254,7 @@ __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_l
 // Offset measurement straight into an fp8 pool (fp32 Δ, one quantisation).
 __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
                                    const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                                   int n_lh, int rows, int d, int delta, const double* __restrict__ inv_freq,
+                                   int n_lh, int rows, int d, int delta, int il, const double* __restrict__ inv_freq,
                                    uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes) {
   __shared__ float2 cs[128];
   const int half = d / 2;
@@ -280,9 +289,20 @@ __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __re
         for (int e = 0; e < 8; ++e) {
           const float x0 = (e & 1) ? bf_hi(K0[e / 2]) : bf_lo(K0[e / 2]);
           const float x1 = (e & 1) ? bf_hi(K1[e / 2]) : bf_lo(K1[e / 2]);
-          const float2 c = cs[v * 8 + e];
-          k0[e] = (x0 * c.x - x1 * c.y) - ((e & 1) ? bf_hi(B0[e / 2]) : bf_lo(B0[e / 2]));
-          k1[e] = (x1 * c.x + x0 * c.y) - ((e & 1) ? bf_hi(B1[e / 2]) : bf_lo(B1[e / 2]));
+          float r0, r1;
+          if (!il) {  // rotate_half: pair (f, f + d/2)
+            const float2 c = cs[v * 8 + e];
+            r0 = x0 * c.x - x1 * c.y;
+            r1 = x1 * c.x + x0 * c.y;
+          } else {    // interleaved: pair (2f, 2f + 1) inside each half
+            const float p0 = (e & 1) ? bf_lo(K0[e / 2]) : bf_hi(K0[e / 2]);  // partner of x0
+            const float p1 = (e & 1) ? bf_lo(K1[e / 2]) : bf_hi(K1[e / 2]);
+            const float2 ca = cs[4 * v + e / 2], cb = cs[d / 4 + 4 * v + e / 2];
+            r0 = (e & 1) ? x0 * ca.x + p0 * ca.y : x0 * ca.x - p0 * ca.y;
+            r1 = (e & 1) ? x1 * cb.x + p1 * cb.y : x1 * cb.x - p1 * cb.y;
+          }
+          k0[e] = r0 - ((e & 1) ? bf_hi(B0[e / 2]) : bf_lo(B0[e / 2]));
+          k1[e] = r1 - ((e & 1) ? bf_hi(B1[e / 2]) : bf_lo(B1[e / 2]));
           v0[e] = ((e & 1) ? bf_hi(V0[e / 2]) : bf_lo(V0[e / 2])) - ((e & 1) ? bf_hi(W0[e / 2]) : bf_lo(W0[e / 2]));
           v1[e] = ((e & 1) ? bf_hi(V1[e / 2]) : bf_lo(V1[e / 2])) - ((e & 1) ? bf_hi(W1[e / 2]) : bf_lo(W1[e / 2]));
         }
@@ -339,11 +359,13 @@ cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, 
 
 cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
                                const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes, cudaStream_t s) {
+                               int interleaved, const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes,
+                               cudaStream_t s) {
   const int n_lh = Ls * Hs;
   if (int64_t(n_lh) * rows == 0) return cudaSuccess;
   measure_fp8_kernel<<<grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh), 256, 0, s>>>(
-      k_real, v_real, real_ld, k_base, v_base, base_ld, n_lh, rows, d, delta, inv_freq, dk, dv, lh_bytes);
+      k_real, v_real, real_ld, k_base, v_base, base_ld, n_lh, rows, d, delta, interleaved, inv_freq, dk, dv,
+      lh_bytes);
   return cudaGetLastError();
 }
 

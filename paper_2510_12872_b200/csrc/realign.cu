@@ -330,6 +330,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const int chunk = kUnitWBytes / (rw * 4);
     const int64_t lh = int64_t(un.l) * Hs + un.h;
     const bool rotate = un.p == 0 && g.delta != 0;
+    const bool rope_il = g.rope_il;
     const float2* csg = cs + g.cs_off;
     bf16* const dst = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
     const bool tstore = tma_store && !g.dst_stg;  // peer destinations: per-thread stores
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             y1[2 * e] = bf_lo(bv[e]) + acc[s][q][8 + 2 * e];
             y1[2 * e + 1] = bf_hi(bv[e]) + acc[s][q][8 + 2 * e + 1];
           }
-          if (rotate) {
+          if (rotate && !rope_il) {  // rotate_half: pair (f, f + d/2), f = 8·ivec + e
             const float2* csr = csg + ivec[q] * 8;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -443,6 +444,18 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
               const float x0 = y0[e], x1 = y1[e];
               y0[e] = x0 * r.x - x1 * r.y;
               y1[e] = x1 * r.x + x0 * r.y;
+            }
+          } else if (rotate) {       // interleaved: pairs (2f, 2f + 1) inside each half
+            const float2* ca = csg + ivec[q] * 4;           // f = 4·ivec + e/2
+            const float2* cb = csg + (d >> 2) + ivec[q] * 4;  // f = d/4 + 4·ivec + e/2
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float2 ra = ca[e >> 1], rb = cb[e >> 1];
+              const float a0 = y0[e], a1 = y0[e + 1], b0 = y1[e], b1 = y1[e + 1];
+              y0[e] = a0 * ra.x - a1 * ra.y;
+              y0[e + 1] = a1 * ra.x + a0 * ra.y;
+              y1[e] = b0 * rb.x - b1 * rb.y;
+              y1[e + 1] = b1 * rb.x + b0 * rb.y;
             }
           }
           const uint4 o0 = make_uint4(pack_bf16_rn(y0[0], y0[1]), pack_bf16_rn(y0[2], y0[3]),

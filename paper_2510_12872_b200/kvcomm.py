@@ -130,7 +130,7 @@ class AnchorPool:
                  max_anchor_len: int, prefix_len: Sequence[int], inv_freq, device: int = 0,
                  layer_range: Optional[Tuple[int, int]] = None, head_range: Optional[Tuple[int, int]] = None,
                  scalar_distance: str = "frobenius", similarity: str = "l2", offset_format: str = "bf16",
-                 placement: str = "device"):
+                 placement: str = "device", rope_layout: str = "half"):
         lb, le = layer_range or (0, num_layers)
         hb, he = head_range or (0, num_kv_heads)
         self.Ls, self.Hs, self.d, self.De = le - lb, he - hb, head_dim, emb_dim
@@ -138,6 +138,7 @@ class AnchorPool:
         self.prefix_len = [int(x) for x in prefix_len]
         self.device = torch.device("cuda", device)
         self.offset_format = offset_format
+        self.rope_layout = rope_layout
         pl = (C.c_int32 * len(self.prefix_len))(*self.prefix_len)
         inv = np.ascontiguousarray(np.asarray(inv_freq, dtype=np.float64))
         cfg = L.PoolConfig(device, num_layers, lb, le, num_kv_heads, hb, he, head_dim, emb_dim, capacity,
@@ -145,7 +146,8 @@ class AnchorPool:
                            {"frobenius": L.SCALAR_FROBENIUS, "mean_l2": L.SCALAR_MEAN_L2}[scalar_distance],
                            {"l2": L.SIM_L2, "cosine": L.SIM_COSINE}[similarity],
                            {"bf16": L.OFFSET_BF16, "fp8": L.OFFSET_FP8_E4M3}[offset_format],
-                           {"device": L.PLACE_DEVICE, "host": L.PLACE_HOST}[placement], pl,
+                           {"device": L.PLACE_DEVICE, "host": L.PLACE_HOST}[placement],
+                           {"half": L.ROPE_HALF, "interleaved": L.ROPE_INTERLEAVED}[rope_layout], 0, pl,
                            inv.ctypes.data_as(C.POINTER(C.c_double)))
         h = C.c_void_p()
         L.check(L.lib().kvcomm_anchor_pool_create(C.byref(cfg), C.byref(h)))

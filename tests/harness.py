@@ -35,7 +35,8 @@ def f64(t: torch.Tensor) -> np.ndarray:
 
 def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Optional[int] = None,
             measure: bool = False, consumer: int = 0, device: int = 0, scalar: str = "frobenius",
-            similarity: str = "l2", offset_format: str = "bf16", placement: str = "device") -> Dict:
+            similarity: str = "l2", offset_format: str = "bf16", placement: str = "device",
+            rope_layout: str = "half") -> Dict:
     """Insert p's anchors, match p's query, realign its placeholder + prefix for
     `consumer`, copy a synthetic p_(m,0) and check the ledger.  Returns CPU tensors."""
     from paper_2510_12872_b200 import kvcomm as K
@@ -44,7 +45,7 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
     pool = K.AnchorPool(num_layers=p.L, num_kv_heads=p.H, head_dim=p.d, emb_dim=p.D_e, capacity=cap,
                         max_anchor_len=max(p.anchor_lens), prefix_len=p.prefix_lens, inv_freq=p.inv_freq,
                         device=device, scalar_distance=scalar, similarity=similarity,
-                        offset_format=offset_format, placement=placement)
+                        offset_format=offset_format, placement=placement, rope_layout=rope_layout)
     slots = []
     for j, Lj in enumerate(p.anchor_lens):
         offs = []
@@ -54,7 +55,7 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
         s, ev = pool.insert(p.emb_anchor[j].to(dev), offs)
         slots.append(s)
     m = pool.match(p.emb_query.to(dev), consumer=consumer, gamma=gamma, top_k=top_k, want_dist=True)
-    out = {"pool": pool, "slots": slots, "match": m}
+    out = {"pool": pool, "slots": slots, "match": m, "rope_layout": rope_layout}
     if not m.candidates:
         return out
     c = consumer
@@ -87,7 +88,8 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
 # ------------------------------------------------------------------------ oracle
 
 def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: int = 0,
-               slots=None, scalar: str = "frobenius", similarity: str = "l2", fp8: bool = False) -> Dict:
+               slots=None, scalar: str = "frobenius", similarity: str = "l2", fp8: bool = False,
+               rope_layout: str = "half") -> Dict:
     """fp8=True: the offsets the blend sees are the e4m3-quantised ones (oracle's own
     quantiser, O.quantize_rows_fp8), as stored by an fp8 pool."""
     store = (lambda x: O.dequantize_rows_fp8(*O.quantize_rows_fp8(x))) if fp8 else (lambda x: x)
@@ -104,7 +106,8 @@ def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: i
     js = [j_of[s] for s in r.candidates]
     dk = [store(f64(p.dk_ph[c][j])) for j in js]
     dv = [store(f64(p.dv_ph[c][j])) for j in js]
-    ph = O.realign_segment(r.W, f64(p.base_k), f64(p.base_v), dk, dv, 0, p.target_start, p.inv_freq)
+    ph = O.realign_segment(r.W, f64(p.base_k), f64(p.base_v), dk, dv, 0, p.target_start, p.inv_freq,
+                           layout=rope_layout)
     ph["absk"] = O.blend_placeholder(r.W, [np.abs(x) for x in dk])
     ph["absv"] = O.blend_placeholder(r.W, [np.abs(x) for x in dv])
     out["ph"] = ph
@@ -112,7 +115,7 @@ def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: i
         pk = [store(f64(p.dk_pf[c][j])) for j in js]
         pv = [store(f64(p.dv_pf[c][j])) for j in js]
         pf = O.realign_segment(r.wbar, f64(p.pf_base_k[c]), f64(p.pf_base_v[c]), pk, pv, p.pf_base_start,
-                               p.pf_target_start[c], p.inv_freq, kind="prefix")
+                               p.pf_target_start[c], p.inv_freq, kind="prefix", layout=rope_layout)
         pf["absk"] = O.blend_prefix(r.wbar, [np.abs(x) for x in pk])
         pf["absv"] = O.blend_prefix(r.wbar, [np.abs(x) for x in pv])
         out["pf"] = pf
@@ -121,8 +124,13 @@ def run_oracle(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, consumer: i
 
 # ------------------------------------------------------------------------ compare
 
-def _partner(x: np.ndarray) -> np.ndarray:
+def _partner(x: np.ndarray, layout: str = "half") -> np.ndarray:
+    """The RoPE partner of every element: f <-> f + d/2 (half) or 2f <-> 2f + 1."""
     d = x.shape[-1]
+    if layout == "interleaved":
+        y = np.empty_like(x)
+        y[..., 0::2], y[..., 1::2] = x[..., 1::2], x[..., 0::2]
+        return y
     return np.concatenate([x[..., d // 2:], x[..., : d // 2]], axis=-1)
 
 
@@ -137,17 +145,18 @@ def check_offsets(g: np.ndarray, o: np.ndarray, absblend: np.ndarray, what: str)
     return float((err / np.maximum(np.abs(o) + absblend, 1e-30)).max()) if err.size else 0.0
 
 
-def kv_tolerance(o: np.ndarray, base: np.ndarray, absblend: np.ndarray) -> np.ndarray:
+def kv_tolerance(o: np.ndarray, base: np.ndarray, absblend: np.ndarray, layout: str = "half") -> np.ndarray:
     ao = np.abs(o)
     with np.errstate(divide="ignore"):
         ulp = np.where(ao > 0, 2.0 ** (np.floor(np.log2(np.where(ao > 0, ao, 1.0))) - 7), 0.0)
     M = np.abs(base) + absblend
-    M = M + _partner(M)
+    M = M + _partner(M, layout)
     return np.maximum(1e-2 * ao, ulp) + 1e-5 * M
 
 
-def check_kv(g: np.ndarray, o: np.ndarray, base: np.ndarray, absblend: np.ndarray, what: str) -> int:
-    tol = kv_tolerance(o, base, absblend)
+def check_kv(g: np.ndarray, o: np.ndarray, base: np.ndarray, absblend: np.ndarray, what: str,
+             layout: str = "half") -> int:
+    tol = kv_tolerance(o, base, absblend, layout)
     err = np.abs(g - o)
     bad = ~(err <= tol)
     if bad.any():
@@ -207,10 +216,12 @@ def compare(gpu: Dict, ora: Dict, p: synth.Problem, check_values: bool = True) -
     if not check_values or "dst_k" not in gpu:
         return stats
     ph = ora["ph"]
+    lay = gpu.get("rope_layout", "half")
     stats["ph_dk_rel"] = check_offsets(f64(gpu["dbg_k"]), ph["dk_hat"], ph["absk"], "placeholder ΔK̂")
     stats["ph_dv_rel"] = check_offsets(f64(gpu["dbg_v"]), ph["dv_hat"], ph["absv"], "placeholder ΔV̂")
     t0, t1 = p.target_start, p.target_start + p.L_phi
-    stats["ph_k_ulps"] = check_kv(f64(gpu["dst_k"])[:, :, t0:t1], ph["k"], f64(p.base_k), ph["absk"], "K̂ placeholder")
+    stats["ph_k_ulps"] = check_kv(f64(gpu["dst_k"])[:, :, t0:t1], ph["k"], f64(p.base_k), ph["absk"], "K̂ placeholder",
+                                  lay)
     stats["ph_v_ulps"] = check_kv(f64(gpu["dst_v"])[:, :, t0:t1], ph["v"], f64(p.base_v), ph["absv"], "V̂ placeholder")
     if "pf" in ora:
         pf = ora["pf"]
@@ -220,7 +231,7 @@ def compare(gpu: Dict, ora: Dict, p: synth.Problem, check_values: bool = True) -
         s0 = p.pf_target_start[c]
         s1 = s0 + p.prefix_lens[c]
         stats["pf_k_ulps"] = check_kv(f64(gpu["dst_k"])[:, :, s0:s1], pf["k"], f64(p.pf_base_k[c]), pf["absk"],
-                                      "K̂ prefix")
+                                      "K̂ prefix", lay)
         stats["pf_v_ulps"] = check_kv(f64(gpu["dst_v"])[:, :, s0:s1], pf["v"], f64(p.pf_base_v[c]), pf["absv"],
                                       "V̂ prefix")
     # p_(m,0) copied verbatim (bit-exact)

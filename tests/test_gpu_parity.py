@@ -104,7 +104,8 @@ def test_unchanged_prefix_reproduces_identical_cache():
     assert torch.equal(dk, base_k) and torch.equal(dv, base_v)
 
 
-def test_measure_insert_matches_oracle():
+@pytest.mark.parametrize("layout", ["half", "interleaved"])
+def test_measure_insert_matches_oracle(layout):
     dev = torch.device("cuda", 0)
     L_, H, d, De, T, P = 2, 3, 128, 64, 90, 20
     inv = synth.llama3_inv_freq(d)
@@ -113,7 +114,7 @@ def test_measure_insert_matches_oracle():
     kr, vr, kb, vb = t(T), t(T), t(T), t(T)
     pkr, pvr, pkb, pvb = t(P), t(P), t(P), t(P)
     pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=De, capacity=2, max_anchor_len=T + 5,
-                        prefix_len=[P], inv_freq=inv)
+                        prefix_len=[P], inv_freq=inv, rope_layout=layout)
     off = K.OffsetMeasure(0, ph_real=(kr.to(dev), vr.to(dev), 731), ph_base=(kb.to(dev), vb.to(dev), 0),
                           pf_real=(pkr.to(dev), pvr.to(dev), 731 + T), pf_base=(pkb.to(dev), pvb.to(dev), 40))
     slot, ev = pool.insert(synth.randn_bf16((T, De), g).to(dev), [off])
@@ -121,9 +122,10 @@ def test_measure_insert_matches_oracle():
     for which, (a, b, c_, d_, sr, sb, n) in {"ph": (kr, vr, kb, vb, 731, 0, T),
                                              "pf": (pkr, pvr, pkb, pvb, 731 + T, 40, P)}.items():
         gk, gv = pool.offset_view(slot, 0, which, rows=n)
-        odk, odv = O.measure_offset(harness.f64(a), harness.f64(b), sr, harness.f64(c_), harness.f64(d_), sb, inv)
+        odk, odv = O.measure_offset(harness.f64(a), harness.f64(b), sr, harness.f64(c_), harness.f64(d_), sb, inv,
+                                    layout)
         harness.check_kv(harness.f64(gk), O.bf16_round(odk), np.zeros_like(odk),
-                         np.abs(harness.f64(a)) + np.abs(harness.f64(c_)), f"measured ΔK {which}")
+                         np.abs(harness.f64(a)) + np.abs(harness.f64(c_)), f"measured ΔK {which}", layout)
         # ΔV: a difference of two bf16 values, rounded once -> bit-exact
         assert np.array_equal(harness.f64(gv), O.bf16_round(odv)), which
 
@@ -446,3 +448,34 @@ def test_dyadic_inputs_are_bit_exact(kind):
     ov = torch.from_numpy(ora["v"]).to(torch.bfloat16).view(torch.int16)
     assert torch.equal(gk, ok) and torch.equal(gv, ov)
     pool.destroy()
+
+
+@pytest.mark.parametrize("fmt,d", [("bf16", 16), ("bf16", 128), ("bf16", 80), ("fp8", 128), ("fp8", 64)])
+def test_interleaved_rope_layout(fmt, d):
+    """rope_layout = INTERLEAVED (GPT-J pairs (2f, 2f+1)): realign with
+    δ != 0 on placeholder and prefix against the oracle's interleaved rotation."""
+    p = synth.make_problem(90 + d, L=2, H=2, d=d, D_e=64, L_phi=70, anchor_lens=[70, 80, 95], prefix_lens=[9],
+                           target_start=37, pf_base_start=21, inv_freq=synth.llama3_inv_freq(d))
+    gpu = harness.run_gpu(p, gamma=1.0, offset_format=fmt, rope_layout="interleaved")
+    ora = harness.run_oracle(p, gamma=1.0, fp8=(fmt == "fp8"), rope_layout="interleaved")
+    harness.compare(gpu, ora, p)
+
+
+def test_fp8_measure_interleaved_close_to_oracle():
+    dev = torch.device("cuda", 0)
+    L_, H, d, T = 2, 2, 128, 40
+    inv = synth.llama3_inv_freq(d)
+    g = synth.make_gen(23)
+    t = lambda n: synth.randn_bf16((L_, H, n, d), g)
+    kr, vr, kb, vb = t(T), t(T), t(T), t(T)
+    pool = K.AnchorPool(num_layers=L_, num_kv_heads=H, head_dim=d, emb_dim=64, capacity=1, max_anchor_len=T,
+                        prefix_len=[0], inv_freq=inv, offset_format="fp8", rope_layout="interleaved")
+    off = K.OffsetMeasure(0, ph_real=(kr.to(dev), vr.to(dev), 500), ph_base=(kb.to(dev), vb.to(dev), 0))
+    slot, _ = pool.insert(synth.randn_bf16((T, 64), g).to(dev), [off])
+    torch.cuda.synchronize()
+    ck, cv, sk, sv = pool.read_offsets(slot, 0, "ph", T)
+    odk, _ = O.measure_offset(harness.f64(kr), harness.f64(vr), 500, harness.f64(kb), harness.f64(vb), 0, inv,
+                              O.INTERLEAVED)
+    got = ck.cpu().view(torch.float8_e4m3fn).double().numpy() * harness.f64(sk)[..., None]
+    amax = np.max(np.abs(odk), axis=-1, keepdims=True)
+    assert np.all(np.abs(got - odk) <= 2.0 ** -3 * np.abs(odk) + 2.0 ** -9 * amax / 448 + 1e-6)

@@ -529,3 +529,38 @@ def test_fp8_row_quantisation_bounds():
     z = np.zeros((2, 16))
     q, s = O.quantize_rows_fp8(z)
     assert np.all(q == 0) and np.all(s == 1.0)
+
+
+def test_rope_interleaved_is_complex_multiplication_and_a_permuted_rotate_half():
+    """Interleaved (GPT-J) pairing (reading A12, SURVEY §8(b) rope_layout): pair f is
+    (x[2f], x[2f+1]) rotated as the complex number x[2f] + i x[2f+1] times e^{i a_f}; it
+    equals rotate_half conjugated by the permutation that sends 2f -> f, 2f+1 -> f+d/2."""
+    rng = np.random.default_rng(5)
+    d = 16
+    inv = synth.plain_inv_freq(d)
+    x = rng.standard_normal((3, d))
+    for delta in (1, -7, 300):
+        y = O.rope_rotate(x, delta, inv, O.INTERLEAVED)
+        z = (x[:, 0::2] + 1j * x[:, 1::2]) * np.exp(1j * delta * inv)
+        np.testing.assert_allclose(y[:, 0::2], z.real, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(y[:, 1::2], z.imag, rtol=0, atol=1e-12)
+        perm = np.concatenate([np.arange(0, d, 2), np.arange(1, d, 2)])   # interleaved -> half order
+        yh = O.rope_rotate(x[:, perm], delta, inv, O.HALF)
+        np.testing.assert_allclose(y[:, perm], yh, rtol=0, atol=1e-12)
+    assert np.array_equal(O.rope_rotate(x, 0, inv, O.INTERLEAVED), x)
+    back = O.rope_rotate(O.rope_rotate(x, 9, inv, O.INTERLEAVED), -9, inv, O.INTERLEAVED)
+    np.testing.assert_allclose(back, x, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.linalg.norm(O.rope_rotate(x, 4, inv, O.INTERLEAVED), axis=-1),
+                               np.linalg.norm(x, axis=-1), rtol=1e-13)
+
+
+def test_measure_apply_round_trip_interleaved():
+    rng = np.random.default_rng(6)
+    d = 32
+    inv = synth.llama3_inv_freq(d)
+    kr, vr = rng.standard_normal((2, 2, 5, d)), rng.standard_normal((2, 2, 5, d))
+    kb, vb = rng.standard_normal((2, 2, 5, d)), rng.standard_normal((2, 2, 5, d))
+    dk, dv = O.measure_offset(kr, vr, 40, kb, vb, 3, inv, O.INTERLEAVED)
+    k, v = O.apply_offset(kb, vb, dk, dv, 37, inv, O.INTERLEAVED)
+    np.testing.assert_allclose(k, kr, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(v, vr, rtol=0, atol=1e-12)
