@@ -64,19 +64,19 @@ __device__ __forceinline__ float sq_diff8(const uint4& qv, const uint4& av) {
   return part;
 }
 
-// q·a, a·a, q·q over 8 bf16 pairs (products of bf16 values are exact in fp32)
-__device__ __forceinline__ void dots8(const uint4& qv, const uint4& av, float& qa, float& aa, float& qq) {
+// q·a, a·a, q·q over 8 bf16 pairs.  A product of two bf16 values is exact in fp32
+// (8 + 8 significant bits); the products are summed in fp64, so 1 - cos keeps ~1e-12
+// absolute accuracy and the 1e-6 relative tie band holds down to tiny distances (an
+// fp32 running sum lost ~1e-7 absolute, > 1e-6 relative once 1 - cos < 0.1).
+__device__ __forceinline__ void dots8(const uint4& qv, const uint4& av, double& qa, double& aa, double& qq) {
   const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
   const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const float a0 = bf_lo(aw[t]), a1 = bf_hi(aw[t]), q0 = bf_lo(qw[t]), q1 = bf_hi(qw[t]);
-    qa = fmaf(q0, a0, qa);
-    qa = fmaf(q1, a1, qa);
-    aa = fmaf(a0, a0, aa);
-    aa = fmaf(a1, a1, aa);
-    qq = fmaf(q0, q0, qq);
-    qq = fmaf(q1, q1, qq);
+    qa += double(q0 * a0) + double(q1 * a1);
+    aa += double(a0 * a0) + double(a1 * a1);
+    qq += double(q0 * q0) + double(q1 * q1);
   }
 }
 
@@ -146,11 +146,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
     } else {
       double qa = 0.0, aa = 0.0, qq = 0.0;
       for (int e = lane * 8; e < De; e += 256) {
-        float fqa = 0.f, faa = 0.f, fqq = 0.f;
-        dots8(lds128(qrow + e), ldg128_nc(arow + e), fqa, faa, fqq);
-        qa += double(fqa);
-        aa += double(faa);
-        qq += double(fqq);
+        dots8(lds128(qrow + e), ldg128_nc(arow + e), qa, aa, qq);
       }
       qa = warp_sum_d(qa);
       aa = warp_sum_d(aa);

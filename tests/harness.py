@@ -55,7 +55,7 @@ def run_gpu(p: synth.Problem, gamma: float = 0.3, top_k: int = 0, capacity: Opti
         s, ev = pool.insert(p.emb_anchor[j].to(dev), offs)
         slots.append(s)
     m = pool.match(p.emb_query.to(dev), consumer=consumer, gamma=gamma, top_k=top_k, want_dist=True)
-    out = {"pool": pool, "slots": slots, "match": m, "rope_layout": rope_layout}
+    out = {"pool": pool, "slots": slots, "match": m, "rope_layout": rope_layout, "consumer": consumer}
     if not m.candidates:
         return out
     c = consumer
@@ -225,7 +225,7 @@ def compare(gpu: Dict, ora: Dict, p: synth.Problem, check_values: bool = True) -
     stats["ph_v_ulps"] = check_kv(f64(gpu["dst_v"])[:, :, t0:t1], ph["v"], f64(p.base_v), ph["absv"], "V̂ placeholder")
     if "pf" in ora:
         pf = ora["pf"]
-        c = 0
+        c = gpu.get("consumer", 0)
         stats["pf_dk_rel"] = check_offsets(f64(gpu["dbgp_k"]), pf["dk_hat"], pf["absk"], "prefix ΔK̂")
         stats["pf_dv_rel"] = check_offsets(f64(gpu["dbgp_v"]), pf["dv_hat"], pf["absv"], "prefix ΔV̂")
         s0 = p.pf_target_start[c]
