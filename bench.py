@@ -442,7 +442,7 @@ def main():
             else:
                 full.append((None, None))
 
-    plan = req.plan                      # native executor: 1 match launch + 1 gated realign launch per step
+    plan = req.plan                      # native executor: one batched match + one gated realign launch per step
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
 
