@@ -225,6 +225,26 @@ def test_determinism_and_batch_equals_single_and_layer_sharding():
         torch.cuda.synchronize()
         assert torch.equal(dk[:, :, 50:].cpu(), full1["dst_k"][lb:le, :, 50:])
         assert torch.equal(dv[:, :, 50:].cpu(), full1["dst_v"][lb:le, :, 50:])
+    # layer x KV-head shards (config 4's 70B partitioning): [0,2)x[0,1), [2,4)x[1,2), ...
+    for (lb, le), (hb, he) in [((0, 2), (0, 1)), ((0, 2), (1, 2)), ((2, 4), (0, 1)), ((2, 4), (1, 2))]:
+        pool = K.AnchorPool(num_layers=4, num_kv_heads=2, head_dim=128, emb_dim=128, capacity=4,
+                            max_anchor_len=190, prefix_len=[32], inv_freq=p.inv_freq, layer_range=(lb, le),
+                            head_range=(hb, he))
+        sl = lambda t: t[lb:le, hb:he].contiguous().to(dev)
+        for j in range(4):
+            pool.insert(p.emb_anchor[j].to(dev), [K.OffsetGiven(0, sl(p.dk_ph[0][j]), sl(p.dv_ph[0][j]),
+                                                                sl(p.dk_pf[0][j]), sl(p.dv_pf[0][j]))])
+        m = pool.match(p.emb_query.to(dev), consumer=0, gamma=1.0)
+        N = full1["N"]
+        dk = torch.zeros(le - lb, he - hb, N, 128, dtype=torch.bfloat16, device=dev)
+        dv = torch.zeros_like(dk)
+        K.realign_segments([K.Segment(pool, 0, K.PLACEHOLDER, m.W, m.candidates, sl(p.base_k), sl(p.base_v), 0, 50,
+                                      dk, dv),
+                            K.Segment(pool, 0, K.PREFIX, m.wbar, m.candidates, sl(p.pf_base_k[0]), sl(p.pf_base_v[0]),
+                                      50, 180, dk, dv)])
+        torch.cuda.synchronize()
+        assert torch.equal(dk[:, :, 50:].cpu(), full1["dst_k"][lb:le, hb:he, 50:])
+        assert torch.equal(dv[:, :, 50:].cpu(), full1["dst_v"][lb:le, hb:he, 50:])
 
 
 def test_copy_segments_are_bit_exact_for_any_bit_pattern():
