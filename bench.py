@@ -144,11 +144,15 @@ def oracle_sample(st, n_tokens: int, rng_seed: int = 0):
 
 
 def oracle_run(sample):
+    """The oracle as it stands, pinned to one host thread (any BLAS pool NumPy may use is
+    limited to 1 thread, so `cores: 1` is what actually ran)."""
+    from threadpoolctl import threadpool_limits
     from oracle import kvcomm_oracle as O
     q, anchors, dk, dv, bk, bv, target, inv = sample
-    dist = O.distances(q, anchors)
-    W, _ = O.position_weights(dist)
-    return O.realign_segment(W, bk, bv, dk, dv, 0, target, inv)
+    with threadpool_limits(limits=1):
+        dist = O.distances(q, anchors)
+        W, _ = O.position_weights(dist)
+        return O.realign_segment(W, bk, bv, dk, dv, 0, target, inv)
 
 
 def cpu_baseline(st, budget_s: float):
