@@ -673,6 +673,7 @@ struct MatchItem {
   float* wbar;
   double* dist;
   const kvcomm_match_info* info;  // candidates
+  double* scratch = nullptr;      // partial + chunk sums owned by the caller (plans), else the pool's
 };
 
 struct MatchLayout {
@@ -726,8 +727,13 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     a.top_k = it.top_k;
     a.idx = it.top_k > 0 ? it.idx : nullptr;
     a.dist_user = it.dist;
-    a.partial = p->d_partial;
-    a.chunks = p->d_partial + int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1);
+    if (it.scratch) {  // plan-owned: concurrent plans sharing a pool never share scratch
+      a.partial = it.scratch;
+      a.chunks = it.scratch + int64_t((it.L_phi + kMatchP - 1) / kMatchP) * (2 * p->cap + 1);
+    } else {           // the pool's (guarded by its match-scratch lock until the results are read)
+      a.partial = p->d_partial;
+      a.chunks = p->d_partial + int64_t((p->maxlen + kMatchP - 1) / kMatchP) * (2 * p->cap + 1);
+    }
     a.wbar = it.wbar;
     a.gamma = double(it.gamma);
     a.n_cand = it.info->n_candidates;
@@ -1183,6 +1189,7 @@ struct kvcomm_plan_s {
   std::vector<kvcomm_plan_agent> agents;
   std::vector<std::vector<int>> agent_matches;  // distinct matches each agent depends on
   std::vector<float*> W, wbar;
+  std::vector<double*> scratch;   // per match: [ceil(L_phi/P) + kMatchChunks][2 cap + 1]
   std::vector<int64_t> ld_w;
   RingEntry tab[2];
   int next = 0;
@@ -1203,6 +1210,7 @@ static void plan_free(kvcomm_plan_s* pl) {
   for (auto& e : pl->tab) entry_free(e);
   for (float* x : pl->W) cudaFree(x);
   for (float* x : pl->wbar) cudaFree(x);
+  for (double* x : pl->scratch) cudaFree(x);
   delete pl;
 }
 
@@ -1284,16 +1292,22 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
   for (int i = 0; i < n_matches; ++i) {
     const int64_t ldw = (matches[i].L_phi + 3) & ~3;
     float *w = nullptr, *wb = nullptr;
+    double* sc = nullptr;
+    const int64_t sc_n = (int64_t((matches[i].L_phi + kMatchP - 1) / kMatchP) + kMatchChunks) *
+                         (2 * matches[i].pool->cap + 1);
     if (cudaMalloc(&w, sizeof(float) * ldw * matches[i].pool->cap) != cudaSuccess ||
-        cudaMalloc(&wb, sizeof(float) * matches[i].pool->cap) != cudaSuccess) {
+        cudaMalloc(&wb, sizeof(float) * matches[i].pool->cap) != cudaSuccess ||
+        cudaMalloc(&sc, sizeof(double) * sc_n) != cudaSuccess) {
       cudaGetLastError();
       cudaFree(w);
       cudaFree(wb);
+      cudaFree(sc);
       plan_free(pl);
       return fail(KVCOMM_ERR_OUT_OF_MEMORY, "plan weight buffers");
     }
     pl->W.push_back(w);
     pl->wbar.push_back(wb);
+    pl->scratch.push_back(sc);
     pl->ld_w.push_back(ldw);
   }
   *out = pl;
@@ -1338,7 +1352,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
     info->top_k = k_eff > 0 ? k_eff : info->n_candidates;
     pl->job_of[i] = int(items.size());
     items.push_back({m.pool, query_embs[i], m.L_phi, m.gamma, k_eff, pl->W[i], pl->ld_w[i], nullptr, pl->wbar[i],
-                     nullptr, info});
+                     nullptr, info, pl->scratch[i]});
   }
   // segments of agents not already decided by the length clause, gated on device
   std::vector<HostSeg> hs;
@@ -1380,8 +1394,6 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
   KV_TRY(entry_reserve(E, roff + RL.bytes));
   uint8_t* h = static_cast<uint8_t*>(E.host);
   uint8_t* dv = static_cast<uint8_t*>(E.dev);
-  std::vector<std::unique_lock<std::mutex>> mlocks;
-  lock_match_scratch(pools, mlocks);
   if (!items.empty()) write_match(h, ML, items);
   const MatchResultDev* gres = items.empty() ? nullptr
                                              : reinterpret_cast<const MatchResultDev*>(dv + ML.hdr.res_off);

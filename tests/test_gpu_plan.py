@@ -77,3 +77,38 @@ def test_device_side_branch_skips_agents_of_a_new_anchor_pool():
         assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
     for a in st.agents[2:]:
         assert torch.all(a.dst_k == 5.0)          # fallback agents untouched
+
+
+def test_two_plans_sharing_pools_run_concurrently_on_two_streams():
+    """Plans own their match scratch: two requests over the same pools, in flight on
+    two streams at once (different queries: one has a NewAnchor pool), each give
+    the result of running alone."""
+    from paper_2510_12872_b200.request import AgentLayout, ReuseRequest
+    st = _small_state(seed=7)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    q2 = dict(st.queries)
+    q2["agent_1_current"] = (torch.randn(q2["agent_1_current"].shape, generator=g, device="cuda") * 0.125
+                             ).to(torch.bfloat16)
+    agents2 = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, torch.full_like(a.dst_k, 9.0),
+                           torch.full_like(a.dst_v, 9.0)) for a in st.agents]
+    req2 = ReuseRequest(st.pools, agents2, gamma=st.request.gamma, top_k=st.request.top_k)
+    # references: each alone
+    st.request.run(st.queries)
+    ref1 = _snap(st)
+    req2.run(q2)
+    ref2 = [(a.dst_k.clone(), a.dst_v.clone()) for a in agents2]
+    for a in list(st.agents) + agents2:
+        a.dst_k.fill_(1.0)
+        a.dst_v.fill_(1.0)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(4):
+        st.request.run(st.queries, sync=False, stream=s1)
+        req2.run(q2, sync=False, stream=s2)
+    torch.cuda.synchronize()
+    assert st.request.results().reused_agents == [1, 2, 3, 4, 5]
+    assert req2.results().fallback_agents == [2, 3, 4, 5]
+    for (k, v), a in zip(ref1, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+    for (k, v), a in zip(ref2, agents2):
+        if a.agent == 1:
+            assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
