@@ -30,10 +30,10 @@ TABLE_A5 = {5: (0.894, 1.719, 3.552), 10: (1.773, 3.576, 7.128), 15: (2.620, 5.3
             20: (3.933, 7.859, 15.624), 25: (4.435, 9.614, 18.113)}
 
 
-def build_pool(cap, maxlen):
+def build_pool(cap, maxlen, placement="device", offsets="bf16"):
     inv = synth.llama3_inv_freq(D)
     pool = kv.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=cap, max_anchor_len=maxlen,
-                         prefix_len=[0], inv_freq=inv)
+                         prefix_len=[0], inv_freq=inv, placement=placement, offset_format=offsets)
     g = torch.Generator(device="cuda").manual_seed(0)
     src_k = (torch.randn(L, H, maxlen, D, generator=g, device="cuda") * synth.OFFSET_STD).to(torch.bfloat16)
     src_v = (torch.randn(L, H, maxlen, D, generator=g, device="cuda") * synth.OFFSET_STD).to(torch.bfloat16)
@@ -46,7 +46,7 @@ def build_pool(cap, maxlen):
     return pool
 
 
-def time_point(pool, m, T, reps=10):
+def time_point(pool, m, T, reps=10, offsets="bf16"):
     g = torch.Generator(device="cuda").manual_seed(m * 7 + T)
     base_k = torch.randn(L, H, T, D, generator=g, device="cuda").to(torch.bfloat16)
     base_v = torch.randn(L, H, T, D, generator=g, device="cuda").to(torch.bfloat16)
@@ -71,7 +71,8 @@ def time_point(pool, m, T, reps=10):
         torch.cuda.synchronize()
         batches.append(e0.elapsed_time(e1) / reps)
     ms = sorted(batches)[len(batches) // 2]
-    byts = (m + 2) * T * TOKEN_BYTES
+    off_tok = TOKEN_BYTES if offsets == "bf16" else L * H * (D + 4) * 2  # e4m3 codes + row scale, K+V
+    byts = m * T * off_tok + 2 * T * TOKEN_BYTES
     return {"anchors": m, "tokens": T, "ms": ms, "ms_batches": [round(b, 4) for b in batches], "tokens_per_s": T / (ms / 1e3), "GBps": byts / (ms / 1e3) / 1e9,
             "alg_bytes": byts}
 
@@ -79,6 +80,9 @@ def time_point(pool, m, T, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--placement", default="device", choices=["device", "host"],
+                    help="host: offset slabs in pinned host memory (f4), a few points only")
+    ap.add_argument("--offsets", default="bf16", choices=["bf16", "fp8"])
     args = ap.parse_args()
     free = torch.cuda.mem_get_info()[0]
     plans = [  # (capacity, maxlen, points)
@@ -89,6 +93,8 @@ def main():
     ]
     if args.quick:
         plans = plans[:1]
+    if args.placement == "host":  # offsets stream over the host link: a few small points
+        plans = [(16, 1024, [(4, 1024), (16, 1024)])]
     for cap, maxlen, pts in plans:
         need = cap * maxlen * TOKEN_BYTES * 1.02 + 6e9
         if need > free:
@@ -96,9 +102,10 @@ def main():
                 print(json.dumps({"anchors": m, "tokens": T, "status": "OOM",
                                   "need_GiB": round(cap * maxlen * TOKEN_BYTES / 2**30, 1)}))
             continue
-        pool = build_pool(cap, maxlen)
+        pool = build_pool(cap, maxlen, args.placement, args.offsets)
         for m, T in pts:
-            r = time_point(pool, m, T)
+            r = time_point(pool, m, T, offsets=args.offsets)
+            r.update(placement=args.placement, offsets=args.offsets)
             if m in TABLE_A5 and T in (1024, 2048, 4096):
                 h100 = TABLE_A5[m][(1024, 2048, 4096).index(T)]
                 r["paper_h100_softmax_ms"] = h100
@@ -107,6 +114,8 @@ def main():
         pool.destroy()
         torch.cuda.empty_cache()
     # infeasible corners of the full grid on one GPU (1024 anchors x >= 2K, 256 x 8K)
+    if args.placement == "host":
+        return
     for m, T in [(1024, 2048), (1024, 4096), (1024, 8192), (256, 8192)]:
         print(json.dumps({"anchors": m, "tokens": T, "status": "OOM",
                           "need_GiB": round(m * T * TOKEN_BYTES / 2**30, 1)}))
