@@ -378,8 +378,12 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
         res = S["req"].results()
         if res.fallback_agents:
             raise SystemExit(f"e2e: agents {res.fallback_agents} fell back")
+        # what reached the host is what the device computed last in this buffer set
+        for a, (hk, hv) in zip(S["agents"], S["host_out"]):
+            if not (torch.equal(hk, a.dst_k.cpu()) and torch.equal(hv, a.dst_v.cpu())):
+                raise SystemExit(f"e2e: host copy of agent {a.agent} differs from the device result")
     return {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": True}
+            "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": True, "host_result_checked": True}
 
 
 # --------------------------------------------------------------------------- ours
