@@ -350,11 +350,45 @@ static OffDst offsets_of(const kvcomm_pool_s* p, int c, int slot, bool prefix) {
   return o;
 }
 
+// bf16 pools: every copy / measurement of one insert is collected and issued as one
+// batched launch of each kind (flush_insert) instead of one launch per (consumer,
+// kind, plane); fp8 pools launch per job.
+struct InsertJobs {
+  std::vector<CopyJob> copies;
+  std::vector<MeasureJob> measures;
+};
+
+static kvcomm_status flush_insert(kvcomm_pool_s* p, InsertJobs& jobs, cudaStream_t s) {
+  for (size_t i = 0; i < jobs.copies.size(); i += kMaxCopyJobs) {
+    CopyJobs b{};
+    const int n = int(std::min<size_t>(kMaxCopyJobs, jobs.copies.size() - i));
+    for (int k = 0; k < n; ++k) b.j[k] = jobs.copies[i + k];
+    KV_CUDA(launch_copy_rows_batch(b, n, p->Ls, p->Hs, p->d, s));
+    g_launches += 1;
+  }
+  const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
+  for (size_t i = 0; i < jobs.measures.size(); i += kMaxMeasureJobs) {
+    MeasureJobs b{};
+    const int n = int(std::min<size_t>(kMaxMeasureJobs, jobs.measures.size() - i));
+    for (int k = 0; k < n; ++k) b.j[k] = jobs.measures[i + k];
+    KV_CUDA(launch_measure_batch(b, n, p->Ls, p->Hs, p->d, il, p->inv_freq_dev, s));
+    g_launches += 1;
+  }
+  jobs.copies.clear();
+  jobs.measures.clear();
+  return KVCOMM_OK;
+}
+
 static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int rows, const OffDst& d,
-                               cudaStream_t s) {
+                               cudaStream_t s, InsertJobs* jobs = nullptr) {
   const int64_t ld = ld_of(src, rows);
   const bf16* k = static_cast<const bf16*>(src.k);
   const bf16* v = static_cast<const bf16*>(src.v);
+  if (!p->fp8 && jobs) {
+    jobs->copies.push_back({k, d.k, ld, d.ld, rows, 0});
+    jobs->copies.push_back({v, d.v, ld, d.ld, rows, 0});
+    return KVCOMM_OK;
+  }
   if (!p->fp8) {
     KV_CUDA(launch_copy_rows(k, ld, d.k, d.ld, p->Ls, p->Hs, rows, p->d, s));
     KV_CUDA(launch_copy_rows(v, ld, d.v, d.ld, p->Ls, p->Hs, rows, p->d, s));
@@ -367,13 +401,17 @@ static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int 
 }
 
 static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, const kvcomm_kv_view& base,
-                                  int rows, const OffDst& d, cudaStream_t s) {
+                                  int rows, const OffDst& d, cudaStream_t s, InsertJobs* jobs = nullptr) {
   const int delta = -(real.start - base.start);
   const auto* kr = static_cast<const bf16*>(real.k);
   const auto* vr = static_cast<const bf16*>(real.v);
   const auto* kb = static_cast<const bf16*>(base.k);
   const auto* vb = static_cast<const bf16*>(base.v);
   const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
+  if (!p->fp8 && jobs) {
+    jobs->measures.push_back({kr, vr, kb, vb, d.k, d.v, ld_of(real, rows), ld_of(base, rows), d.ld, rows, delta});
+    return KVCOMM_OK;
+  }
   if (!p->fp8)
     KV_CUDA(launch_measure(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d, delta,
                            il, p->inv_freq_dev, d.k, d.v, d.ld, s));
@@ -386,7 +424,7 @@ static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, 
 
 // Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
 static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const kvcomm_offset_desc& o,
-                                   cudaStream_t s, uint64_t* ph_set, uint64_t* pf_set) {
+                                   cudaStream_t s, uint64_t* ph_set, uint64_t* pf_set, InsertJobs* jobs) {
   const int c = o.consumer;
   if (c < 0 || c >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d outside [0,%d)", c, p->C);
   const int P = p->prefix_len[c];
@@ -395,25 +433,25 @@ static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const 
   if (o.mode == KVCOMM_OFFSET_GIVEN) {
     if (o.ph_delta.k) {
       KV_TRY(check_view(o.ph_delta, L_psi, "ph_delta"));
-      KV_TRY(put_given(p, o.ph_delta, L_psi, ph, s));
+      KV_TRY(put_given(p, o.ph_delta, L_psi, ph, s, jobs));
       *ph_set |= 1ull << c;
     }
     if (o.pf_delta.k) {
       KV_TRY(check_view(o.pf_delta, P, "pf_delta"));
-      KV_TRY(put_given(p, o.pf_delta, P, pf, s));
+      KV_TRY(put_given(p, o.pf_delta, P, pf, s, jobs));
       *pf_set |= 1ull << c;
     }
   } else if (o.mode == KVCOMM_OFFSET_MEASURE) {
     if (o.ph_real.k) {
       KV_TRY(check_view(o.ph_real, L_psi, "ph_real"));
       KV_TRY(check_view(o.ph_base, L_psi, "ph_base"));
-      KV_TRY(put_measured(p, o.ph_real, o.ph_base, L_psi, ph, s));
+      KV_TRY(put_measured(p, o.ph_real, o.ph_base, L_psi, ph, s, jobs));
       *ph_set |= 1ull << c;
     }
     if (o.pf_real.k) {
       KV_TRY(check_view(o.pf_real, P, "pf_real"));
       KV_TRY(check_view(o.pf_base, P, "pf_base"));
-      KV_TRY(put_measured(p, o.pf_real, o.pf_base, P, pf, s));
+      KV_TRY(put_measured(p, o.pf_real, o.pf_base, P, pf, s, jobs));
       *pf_set |= 1ull << c;
     }
   } else {
@@ -458,13 +496,15 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_ps
                            int64_t(L_psi) * p->De, s));
   g_launches += 1;
   uint64_t phm = 0, pfm = 0;
+  InsertJobs jobs;
   for (int i = 0; i < n_offs; ++i) {
-    kvcomm_status st = write_offsets(p, slot, L_psi, offs[i], s, &phm, &pfm);
+    kvcomm_status st = write_offsets(p, slot, L_psi, offs[i], s, &phm, &pfm, &jobs);
     if (st != KVCOMM_OK) {
       if (evicted < 0) p->slots[slot] = SlotMeta();  // leave the pool as it was (minus the victim)
       return st;
     }
   }
+  KV_TRY(flush_insert(p, jobs, s));
   SlotMeta& m = p->slots[slot];
   m.occupied = true;
   m.length = L_psi;
@@ -486,8 +526,13 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_set_offsets(kvcomm_pool_t p, int32_t
     return fail(KVCOMM_ERR_NOT_FOUND, "slot %d is empty", slot);
   DeviceGuard guard(p->cfg.device);
   SlotMeta& m = p->slots[slot];
+  InsertJobs jobs;
+  uint64_t phm = m.ph_mask, pfm = m.pf_mask;  // published only once every job is issued
   for (int i = 0; i < n_offs; ++i)
-    KV_TRY(write_offsets(p, slot, m.length, offs[i], static_cast<cudaStream_t>(stream), &m.ph_mask, &m.pf_mask));
+    KV_TRY(write_offsets(p, slot, m.length, offs[i], static_cast<cudaStream_t>(stream), &phm, &pfm, &jobs));
+  KV_TRY(flush_insert(p, jobs, static_cast<cudaStream_t>(stream)));
+  m.ph_mask = phm;
+  m.pf_mask = pfm;
   return ok();
 }
 

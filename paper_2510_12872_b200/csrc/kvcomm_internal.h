@@ -117,6 +117,31 @@ cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_
 // Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,
                              int rows, int d, cudaStream_t s);
+// Batched insert-path jobs (one launch per insert instead of one per (consumer, kind,
+// plane)); passed by value as kernel parameters.
+struct CopyJob {
+  const bf16* src;
+  bf16* dst;
+  int64_t src_ld, dst_ld;
+  int32_t rows, _pad;
+};
+constexpr int kMaxCopyJobs = 64;
+struct CopyJobs {
+  CopyJob j[kMaxCopyJobs];
+};
+struct MeasureJob {
+  const bf16 *kr, *vr, *kb, *vb;
+  bf16 *dk, *dv;
+  int64_t real_ld, base_ld, dst_ld;
+  int32_t rows, delta;
+};
+constexpr int kMaxMeasureJobs = 32;
+struct MeasureJobs {
+  MeasureJob j[kMaxMeasureJobs];
+};
+cudaError_t launch_copy_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, int d, cudaStream_t s);
+cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
+                                 const double* inv_freq, cudaStream_t s);
 // Contiguous copy of n bf16 elements (multiple of 8).
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
 // fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of fp8_rows_per_block(d) rows

@@ -57,6 +57,29 @@ cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t
   return cudaGetLastError();
 }
 
+__global__ void copy_rows_batch_kernel(const __grid_constant__ CopyJobs jobs, int n_lh, int d) {
+  const CopyJob& J = jobs.j[blockIdx.z];
+  const int nvec = J.rows * (d / 8);
+  for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
+    const uint4* s = reinterpret_cast<const uint4*>(J.src + int64_t(lh) * J.src_ld * d);
+    uint4* t = reinterpret_cast<uint4*>(J.dst + int64_t(lh) * J.dst_ld * d);
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nvec; x += gridDim.x * blockDim.x)
+      t[x] = ldg128_nc(s + x);
+  }
+}
+
+cudaError_t launch_copy_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, int d, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int rows = 0;
+  for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
+  const int n_lh = Ls * Hs;
+  dim3 g = grid2d(int64_t(rows) * (d / 8), 256, n_lh);
+  g.x = max(1u, g.x / unsigned(n) + 1u);  // the jobs share the machine
+  g.z = unsigned(n);
+  copy_rows_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s) {
   const int64_t nvec = n / 8;
   if (nvec == 0) return cudaSuccess;
@@ -68,18 +91,12 @@ cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t
 // Items = (row, vector-pair v): 8 elements of the first half and the matching 8 of
 // the second half of a d-element row, so the rotate_half pair (f, f+d/2) stays in
 // one thread.  cos/sin of δ·inv_freq[f] (fp64 angle) are tabled in shared memory.
-__global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
-                               const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                               int rows, int n_lh, int d, int delta, int il, const double* __restrict__ inv_freq,
-                               bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld) {
-  __shared__ float2 cs[128];
+__device__ __forceinline__ void measure_rows(const bf16* __restrict__ kr, const bf16* __restrict__ vr,
+                                             int64_t real_ld, const bf16* __restrict__ kb,
+                                             const bf16* __restrict__ vb, int64_t base_ld, int rows, int n_lh, int d,
+                                             int il, const float2* cs, bf16* __restrict__ dk, bf16* __restrict__ dv,
+                                             int64_t dst_ld) {
   const int half = d / 2;
-  for (int f = threadIdx.x; f < half; f += blockDim.x) {
-    double sn, cn;
-    sincos(double(delta) * inv_freq[f], &sn, &cn);
-    cs[f] = make_float2(float(cn), float(sn));
-  }
-  __syncthreads();
   const int vph = d / 16;  // vector pairs per row
   const int n = rows * vph;
   for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
@@ -128,6 +145,49 @@ __global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restri
       *reinterpret_cast<uint4*>(dv + oo + half) = make_uint4(ov1[0], ov1[1], ov1[2], ov1[3]);
     }
   }
+}
+
+__device__ __forceinline__ void rope_table(float2* cs, int d, int delta, const double* __restrict__ inv_freq) {
+  for (int f = threadIdx.x; f < d / 2; f += blockDim.x) {
+    double sn, cn;
+    sincos(double(delta) * inv_freq[f], &sn, &cn);
+    cs[f] = make_float2(float(cn), float(sn));
+  }
+  __syncthreads();
+}
+
+// Items = (row, vector-pair v): 8 elements of the first half and the matching 8 of
+// the second half of a d-element row, so the rotate_half pair (f, f+d/2) stays in
+// one thread.  cos/sin of δ·inv_freq[f] (fp64 angle) are tabled in shared memory.
+__global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
+                               const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
+                               int rows, int n_lh, int d, int delta, int il, const double* __restrict__ inv_freq,
+                               bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld) {
+  __shared__ float2 cs[128];
+  rope_table(cs, d, delta, inv_freq);
+  measure_rows(kr, vr, real_ld, kb, vb, base_ld, rows, n_lh, d, il, cs, dk, dv, dst_ld);
+}
+
+// All measured offsets of one insert in one launch: blockIdx.z = job.
+__global__ void measure_batch_kernel(const __grid_constant__ MeasureJobs jobs, int n_lh, int d, int il,
+                                     const double* __restrict__ inv_freq) {
+  __shared__ float2 cs[128];
+  const MeasureJob& J = jobs.j[blockIdx.z];
+  rope_table(cs, d, J.delta, inv_freq);
+  measure_rows(J.kr, J.vr, J.real_ld, J.kb, J.vb, J.base_ld, J.rows, n_lh, d, il, cs, J.dk, J.dv, J.dst_ld);
+}
+
+cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
+                                 const double* inv_freq, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int rows = 0;
+  for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
+  const int n_lh = Ls * Hs;
+  dim3 g = grid2d(int64_t(rows) * (d / 16), 256, n_lh);
+  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.z = unsigned(n);
+  measure_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
