@@ -350,9 +350,9 @@ static OffDst offsets_of(const kvcomm_pool_s* p, int c, int slot, bool prefix) {
   return o;
 }
 
-// bf16 pools: every copy / measurement of one insert is collected and issued as one
-// batched launch of each kind (flush_insert) instead of one launch per (consumer,
-// kind, plane); fp8 pools launch per job.
+// Every copy (or quantisation) and measurement of one insert is collected and issued
+// as one batched launch of each kind (flush_insert) instead of one launch per
+// (consumer, kind, plane).
 struct InsertJobs {
   std::vector<CopyJob> copies;
   std::vector<MeasureJob> measures;
@@ -363,7 +363,8 @@ static kvcomm_status flush_insert(kvcomm_pool_s* p, InsertJobs& jobs, cudaStream
     CopyJobs b{};
     const int n = int(std::min<size_t>(kMaxCopyJobs, jobs.copies.size() - i));
     for (int k = 0; k < n; ++k) b.j[k] = jobs.copies[i + k];
-    KV_CUDA(launch_copy_rows_batch(b, n, p->Ls, p->Hs, p->d, s));
+    if (!p->fp8) KV_CUDA(launch_copy_rows_batch(b, n, p->Ls, p->Hs, p->d, s));
+    else KV_CUDA(launch_quantize_rows_batch(b, n, p->Ls, p->Hs, p->d, s));
     g_launches += 1;
   }
   const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
@@ -371,7 +372,8 @@ static kvcomm_status flush_insert(kvcomm_pool_s* p, InsertJobs& jobs, cudaStream
     MeasureJobs b{};
     const int n = int(std::min<size_t>(kMaxMeasureJobs, jobs.measures.size() - i));
     for (int k = 0; k < n; ++k) b.j[k] = jobs.measures[i + k];
-    KV_CUDA(launch_measure_batch(b, n, p->Ls, p->Hs, p->d, il, p->inv_freq_dev, s));
+    if (!p->fp8) KV_CUDA(launch_measure_batch(b, n, p->Ls, p->Hs, p->d, il, p->inv_freq_dev, s));
+    else KV_CUDA(launch_measure_fp8_batch(b, n, p->Ls, p->Hs, p->d, il, p->inv_freq_dev, s));
     g_launches += 1;
   }
   jobs.copies.clear();
@@ -384,9 +386,14 @@ static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int 
   const int64_t ld = ld_of(src, rows);
   const bf16* k = static_cast<const bf16*>(src.k);
   const bf16* v = static_cast<const bf16*>(src.v);
-  if (!p->fp8 && jobs) {
-    jobs->copies.push_back({k, d.k, ld, d.ld, rows, 0});
-    jobs->copies.push_back({v, d.v, ld, d.ld, rows, 0});
+  if (jobs) {
+    if (!p->fp8) {
+      jobs->copies.push_back({k, d.k, ld, d.ld, rows, 0});
+      jobs->copies.push_back({v, d.v, ld, d.ld, rows, 0});
+    } else {
+      jobs->copies.push_back({k, d.k8, ld, d.lh_bytes, rows, 0});
+      jobs->copies.push_back({v, d.v8, ld, d.lh_bytes, rows, 0});
+    }
     return KVCOMM_OK;
   }
   if (!p->fp8) {
@@ -408,8 +415,12 @@ static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, 
   const auto* kb = static_cast<const bf16*>(base.k);
   const auto* vb = static_cast<const bf16*>(base.v);
   const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
-  if (!p->fp8 && jobs) {
-    jobs->measures.push_back({kr, vr, kb, vb, d.k, d.v, ld_of(real, rows), ld_of(base, rows), d.ld, rows, delta});
+  if (jobs) {
+    if (!p->fp8)
+      jobs->measures.push_back({kr, vr, kb, vb, d.k, d.v, ld_of(real, rows), ld_of(base, rows), d.ld, rows, delta});
+    else
+      jobs->measures.push_back({kr, vr, kb, vb, d.k8, d.v8, ld_of(real, rows), ld_of(base, rows), d.lh_bytes, rows,
+                                delta});
     return KVCOMM_OK;
   }
   if (!p->fp8)

@@ -121,8 +121,8 @@ cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t
 // plane)); passed by value as kernel parameters.
 struct CopyJob {
   const bf16* src;
-  bf16* dst;
-  int64_t src_ld, dst_ld;
+  void* dst;                // bf16 rows, or (fp8 pools) the blocked e4m3 region
+  int64_t src_ld, dst_ld;   // rows; fp8: dst_ld = bytes per (layer, head) region
   int32_t rows, _pad;
 };
 constexpr int kMaxCopyJobs = 64;
@@ -131,8 +131,8 @@ struct CopyJobs {
 };
 struct MeasureJob {
   const bf16 *kr, *vr, *kb, *vb;
-  bf16 *dk, *dv;
-  int64_t real_ld, base_ld, dst_ld;
+  void *dk, *dv;            // bf16 rows, or (fp8 pools) blocked e4m3 regions
+  int64_t real_ld, base_ld, dst_ld;  // fp8: dst_ld = bytes per (layer, head) region
   int32_t rows, delta;
 };
 constexpr int kMaxMeasureJobs = 32;
@@ -142,6 +142,9 @@ struct MeasureJobs {
 cudaError_t launch_copy_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, int d, cudaStream_t s);
 cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
                                  const double* inv_freq, cudaStream_t s);
+cudaError_t launch_quantize_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, int d, cudaStream_t s);
+cudaError_t launch_measure_fp8_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
+                                     const double* inv_freq, cudaStream_t s);
 // Contiguous copy of n bf16 elements (multiple of 8).
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
 // fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of fp8_rows_per_block(d) rows

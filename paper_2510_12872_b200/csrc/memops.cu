@@ -62,7 +62,7 @@ __global__ void copy_rows_batch_kernel(const __grid_constant__ CopyJobs jobs, in
   const int nvec = J.rows * (d / 8);
   for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
     const uint4* s = reinterpret_cast<const uint4*>(J.src + int64_t(lh) * J.src_ld * d);
-    uint4* t = reinterpret_cast<uint4*>(J.dst + int64_t(lh) * J.dst_ld * d);
+    uint4* t = reinterpret_cast<uint4*>(static_cast<bf16*>(J.dst) + int64_t(lh) * J.dst_ld * d);
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nvec; x += gridDim.x * blockDim.x)
       t[x] = ldg128_nc(s + x);
   }
@@ -174,7 +174,8 @@ __global__ void measure_batch_kernel(const __grid_constant__ MeasureJobs jobs, i
   __shared__ float2 cs[128];
   const MeasureJob& J = jobs.j[blockIdx.z];
   rope_table(cs, d, J.delta, inv_freq);
-  measure_rows(J.kr, J.vr, J.real_ld, J.kb, J.vb, J.base_ld, J.rows, n_lh, d, il, cs, J.dk, J.dv, J.dst_ld);
+  measure_rows(J.kr, J.vr, J.real_ld, J.kb, J.vb, J.base_ld, J.rows, n_lh, d, il, cs, static_cast<bf16*>(J.dk),
+               static_cast<bf16*>(J.dv), J.dst_ld);
 }
 
 cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
@@ -272,8 +273,8 @@ __device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int 
 // bf16 rows -> e4m3 codes + per-row scales (GIVEN offsets into an fp8 pool).  x walks
 // (row, lane-in-group); every lane of a group runs the loop body together (the
 // shuffles of group_max), idle lanes with zeros.
-__global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
-                                     int64_t lh_bytes, int n_lh, int rows, int d) {
+__device__ __forceinline__ void quantize_rows(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
+                                              int64_t lh_bytes, int n_lh, int rows, int d) {
   const int vph = d / 16;
   const int G = row_group(vph);
   const int half = d / 2;
@@ -312,18 +313,12 @@ __global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_l
 }
 
 // Offset measurement straight into an fp8 pool (fp32 Δ, one quantisation).
-__global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
-                                   const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                                   int n_lh, int rows, int d, int delta, int il, const double* __restrict__ inv_freq,
-                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes) {
-  __shared__ float2 cs[128];
+__device__ __forceinline__ void measure_fp8_rows(const bf16* __restrict__ kr, const bf16* __restrict__ vr,
+                                                 int64_t real_ld, const bf16* __restrict__ kb,
+                                                 const bf16* __restrict__ vb, int64_t base_ld, int n_lh, int rows,
+                                                 int d, int il, const float2* cs, uint8_t* __restrict__ dk,
+                                                 uint8_t* __restrict__ dv, int64_t lh_bytes) {
   const int half = d / 2;
-  for (int f = threadIdx.x; f < half; f += blockDim.x) {
-    double sn, cn;
-    sincos(double(delta) * inv_freq[f], &sn, &cn);
-    cs[f] = make_float2(float(cn), float(sn));
-  }
-  __syncthreads();
   const int vph = d / 16;
   const int G = row_group(vph);
   const int n = rows * G;
@@ -389,6 +384,60 @@ __global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __re
       }
     }
   }
+}
+
+__global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
+                                     int64_t lh_bytes, int n_lh, int rows, int d) {
+  quantize_rows(src, src_ld, dst, lh_bytes, n_lh, rows, d);
+}
+
+__global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
+                                   const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
+                                   int n_lh, int rows, int d, int delta, int il, const double* __restrict__ inv_freq,
+                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes) {
+  __shared__ float2 cs[128];
+  rope_table(cs, d, delta, inv_freq);
+  measure_fp8_rows(kr, vr, real_ld, kb, vb, base_ld, n_lh, rows, d, il, cs, dk, dv, lh_bytes);
+}
+
+// One launch per insert (fp8 pools): blockIdx.z = job; dst_ld carries lh_bytes.
+__global__ void quantize_rows_batch_kernel(const __grid_constant__ CopyJobs jobs, int n_lh, int d) {
+  const CopyJob& J = jobs.j[blockIdx.z];
+  quantize_rows(J.src, J.src_ld, static_cast<uint8_t*>(J.dst), J.dst_ld, n_lh, J.rows, d);
+}
+
+__global__ void measure_fp8_batch_kernel(const __grid_constant__ MeasureJobs jobs, int n_lh, int d, int il,
+                                         const double* __restrict__ inv_freq) {
+  __shared__ float2 cs[128];
+  const MeasureJob& J = jobs.j[blockIdx.z];
+  rope_table(cs, d, J.delta, inv_freq);
+  measure_fp8_rows(J.kr, J.vr, J.real_ld, J.kb, J.vb, J.base_ld, n_lh, J.rows, d, il, cs,
+                   static_cast<uint8_t*>(J.dk), static_cast<uint8_t*>(J.dv), J.dst_ld);
+}
+
+cudaError_t launch_quantize_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, int d, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int rows = 0;
+  for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
+  const int n_lh = Ls * Hs;
+  dim3 g = grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh);
+  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.z = unsigned(n);
+  quantize_rows_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_measure_fp8_batch(const MeasureJobs& jobs, int n, int Ls, int Hs, int d, int interleaved,
+                                     const double* inv_freq, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int rows = 0;
+  for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
+  const int n_lh = Ls * Hs;
+  dim3 g = grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh);
+  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.z = unsigned(n);
+  measure_fp8_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
+  return cudaGetLastError();
 }
 
 // blocked -> dense copy of stored fp8 offsets (inspection)
