@@ -381,61 +381,37 @@ static kvcomm_status flush_insert(kvcomm_pool_s* p, InsertJobs& jobs, cudaStream
   return KVCOMM_OK;
 }
 
-static kvcomm_status put_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int rows, const OffDst& d,
-                               cudaStream_t s, InsertJobs* jobs = nullptr) {
+// Queue the copies (bf16) or quantisations (fp8) of GIVEN offsets.
+static void queue_given(kvcomm_pool_s* p, const kvcomm_kv_view& src, int rows, const OffDst& d, InsertJobs& jobs) {
   const int64_t ld = ld_of(src, rows);
   const bf16* k = static_cast<const bf16*>(src.k);
   const bf16* v = static_cast<const bf16*>(src.v);
-  if (jobs) {
-    if (!p->fp8) {
-      jobs->copies.push_back({k, d.k, ld, d.ld, rows, 0});
-      jobs->copies.push_back({v, d.v, ld, d.ld, rows, 0});
-    } else {
-      jobs->copies.push_back({k, d.k8, ld, d.lh_bytes, rows, 0});
-      jobs->copies.push_back({v, d.v8, ld, d.lh_bytes, rows, 0});
-    }
-    return KVCOMM_OK;
-  }
   if (!p->fp8) {
-    KV_CUDA(launch_copy_rows(k, ld, d.k, d.ld, p->Ls, p->Hs, rows, p->d, s));
-    KV_CUDA(launch_copy_rows(v, ld, d.v, d.ld, p->Ls, p->Hs, rows, p->d, s));
+    jobs.copies.push_back({k, d.k, ld, d.ld, rows, 0});
+    jobs.copies.push_back({v, d.v, ld, d.ld, rows, 0});
   } else {
-    KV_CUDA(launch_quantize_rows(k, ld, d.k8, d.lh_bytes, p->Ls, p->Hs, rows, p->d, s));
-    KV_CUDA(launch_quantize_rows(v, ld, d.v8, d.lh_bytes, p->Ls, p->Hs, rows, p->d, s));
+    jobs.copies.push_back({k, d.k8, ld, d.lh_bytes, rows, 0});
+    jobs.copies.push_back({v, d.v8, ld, d.lh_bytes, rows, 0});
   }
-  g_launches += 2;
-  return KVCOMM_OK;
 }
 
-static kvcomm_status put_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, const kvcomm_kv_view& base,
-                                  int rows, const OffDst& d, cudaStream_t s, InsertJobs* jobs = nullptr) {
+// Queue a device measurement ΔK = R_{-(s_real - s_base)} K_real - K_base, ΔV = V_real - V_base.
+static void queue_measured(kvcomm_pool_s* p, const kvcomm_kv_view& real, const kvcomm_kv_view& base, int rows,
+                           const OffDst& d, InsertJobs& jobs) {
   const int delta = -(real.start - base.start);
   const auto* kr = static_cast<const bf16*>(real.k);
   const auto* vr = static_cast<const bf16*>(real.v);
   const auto* kb = static_cast<const bf16*>(base.k);
   const auto* vb = static_cast<const bf16*>(base.v);
-  const int il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
-  if (jobs) {
-    if (!p->fp8)
-      jobs->measures.push_back({kr, vr, kb, vb, d.k, d.v, ld_of(real, rows), ld_of(base, rows), d.ld, rows, delta});
-    else
-      jobs->measures.push_back({kr, vr, kb, vb, d.k8, d.v8, ld_of(real, rows), ld_of(base, rows), d.lh_bytes, rows,
-                                delta});
-    return KVCOMM_OK;
-  }
   if (!p->fp8)
-    KV_CUDA(launch_measure(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d, delta,
-                           il, p->inv_freq_dev, d.k, d.v, d.ld, s));
+    jobs.measures.push_back({kr, vr, kb, vb, d.k, d.v, ld_of(real, rows), ld_of(base, rows), d.ld, rows, delta});
   else
-    KV_CUDA(launch_measure_fp8(kr, vr, ld_of(real, rows), kb, vb, ld_of(base, rows), rows, p->Ls, p->Hs, p->d,
-                               delta, il, p->inv_freq_dev, d.k8, d.v8, d.lh_bytes, s));
-  g_launches += 1;
-  return KVCOMM_OK;
+    jobs.measures.push_back({kr, vr, kb, vb, d.k8, d.v8, ld_of(real, rows), ld_of(base, rows), d.lh_bytes, rows,
+                             delta});
 }
 
-// Writes the offsets of one consumer into slot `slot` (caller holds the writer lock).
 static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const kvcomm_offset_desc& o,
-                                   cudaStream_t s, uint64_t* ph_set, uint64_t* pf_set, InsertJobs* jobs) {
+                                   uint64_t* ph_set, uint64_t* pf_set, InsertJobs& jobs) {
   const int c = o.consumer;
   if (c < 0 || c >= p->C) return fail(KVCOMM_ERR_NOT_FOUND, "consumer %d outside [0,%d)", c, p->C);
   const int P = p->prefix_len[c];
@@ -444,25 +420,25 @@ static kvcomm_status write_offsets(kvcomm_pool_s* p, int slot, int L_psi, const 
   if (o.mode == KVCOMM_OFFSET_GIVEN) {
     if (o.ph_delta.k) {
       KV_TRY(check_view(o.ph_delta, L_psi, "ph_delta"));
-      KV_TRY(put_given(p, o.ph_delta, L_psi, ph, s, jobs));
+      queue_given(p, o.ph_delta, L_psi, ph, jobs);
       *ph_set |= 1ull << c;
     }
     if (o.pf_delta.k) {
       KV_TRY(check_view(o.pf_delta, P, "pf_delta"));
-      KV_TRY(put_given(p, o.pf_delta, P, pf, s, jobs));
+      queue_given(p, o.pf_delta, P, pf, jobs);
       *pf_set |= 1ull << c;
     }
   } else if (o.mode == KVCOMM_OFFSET_MEASURE) {
     if (o.ph_real.k) {
       KV_TRY(check_view(o.ph_real, L_psi, "ph_real"));
       KV_TRY(check_view(o.ph_base, L_psi, "ph_base"));
-      KV_TRY(put_measured(p, o.ph_real, o.ph_base, L_psi, ph, s, jobs));
+      queue_measured(p, o.ph_real, o.ph_base, L_psi, ph, jobs);
       *ph_set |= 1ull << c;
     }
     if (o.pf_real.k) {
       KV_TRY(check_view(o.pf_real, P, "pf_real"));
       KV_TRY(check_view(o.pf_base, P, "pf_base"));
-      KV_TRY(put_measured(p, o.pf_real, o.pf_base, P, pf, s, jobs));
+      queue_measured(p, o.pf_real, o.pf_base, P, pf, jobs);
       *pf_set |= 1ull << c;
     }
   } else {
@@ -509,7 +485,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_ps
   uint64_t phm = 0, pfm = 0;
   InsertJobs jobs;
   for (int i = 0; i < n_offs; ++i) {
-    kvcomm_status st = write_offsets(p, slot, L_psi, offs[i], s, &phm, &pfm, &jobs);
+    kvcomm_status st = write_offsets(p, slot, L_psi, offs[i], &phm, &pfm, jobs);
     if (st != KVCOMM_OK) {
       if (evicted < 0) p->slots[slot] = SlotMeta();  // leave the pool as it was (minus the victim)
       return st;
@@ -540,7 +516,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_set_offsets(kvcomm_pool_t p, int32_t
   InsertJobs jobs;
   uint64_t phm = m.ph_mask, pfm = m.pf_mask;  // published only once every job is issued
   for (int i = 0; i < n_offs; ++i)
-    KV_TRY(write_offsets(p, slot, m.length, offs[i], static_cast<cudaStream_t>(stream), &phm, &pfm, &jobs));
+    KV_TRY(write_offsets(p, slot, m.length, offs[i], &phm, &pfm, jobs));
   KV_TRY(flush_insert(p, jobs, static_cast<cudaStream_t>(stream)));
   m.ph_mask = phm;
   m.pf_mask = pfm;

@@ -149,19 +149,7 @@ cudaError_t launch_measure_fp8_batch(const MeasureJobs& jobs, int n, int Ls, int
 cudaError_t launch_copy_flat(const bf16* src, bf16* dst, int64_t n, cudaStream_t s);
 // fp8 (e4m3 + per-row fp32 scale) offset storage in blocks of fp8_rows_per_block(d) rows
 // (codes, then the block's row scales); lh_bytes = bytes per (layer, head) region.
-cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
-                                 int rows, int d, cudaStream_t s);
-cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
-                               const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               int interleaved, const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes,
-                               cudaStream_t s);
-// blocked e4m3 rows -> dense codes [lh][rows][d] + scales [lh][rows] (inspection / tests)
+// Blocked e4m3 rows -> dense codes [lh][rows][d] + scales [lh][rows] (inspection / tests).
 cudaError_t launch_read_fp8(const uint8_t* src, int64_t lh_bytes, uint8_t* codes, float* scales, int Ls, int Hs,
                             int rows, int d, cudaStream_t s);
-// Offset measurement (insert path, step a0).
-cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
-                           const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                           int interleaved, const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld,
-                           cudaStream_t s);
-
 }  // namespace kvc

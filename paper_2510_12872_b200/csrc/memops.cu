@@ -1,10 +1,12 @@
-// Insert-path and concatenation kernels:
-//   * measure_kernel — offset measurement of Algorithm 1's fallback branch:
-//       ΔK = R_{-(s_real - s_base)} K_real - K_base,  ΔV = V_real - V_base   (step a0)
-//     written straight into the pool slab, fp32 math, one RNE rounding to bf16.
-//   * copy_rows_kernel — strided [Ls][Hs][rows][d] row-block copy (GIVEN offsets into
-//     the pool slab; offsets read back for inspection).
-//   * fp8 variants of the insert path.
+// Insert-path kernels (step a0), each batched over all jobs of one insert
+// (blockIdx.z = job):
+//   * measure_batch_kernel — offset measurement of Algorithm 1's fallback branch
+//     (P:789-790): ΔK = R_{-(s_real - s_base)} K_real - K_base, ΔV = V_real - V_base,
+//     written straight into the pool slab, fp32 math, one RNE rounding to bf16;
+//   * copy_rows_batch_kernel — GIVEN offsets into the slab;
+//   * fp8 variants: quantize_rows_batch_kernel, measure_fp8_batch_kernel.
+// copy_rows_kernel reads stored offsets back for inspection; copy_flat_kernel copies
+// embeddings.
 // Grids are 2-D: blockIdx.y walks the (layer, head) blocks, x the rows of one block,
 // so the per-element index math is 32-bit (no 64-bit division per vector).
 #include <cuda_runtime.h>
@@ -156,18 +158,6 @@ __device__ __forceinline__ void rope_table(float2* cs, int d, int delta, const d
   __syncthreads();
 }
 
-// Items = (row, vector-pair v): 8 elements of the first half and the matching 8 of
-// the second half of a d-element row, so the rotate_half pair (f, f+d/2) stays in
-// one thread.  cos/sin of δ·inv_freq[f] (fp64 angle) are tabled in shared memory.
-__global__ void measure_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
-                               const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                               int rows, int n_lh, int d, int delta, int il, const double* __restrict__ inv_freq,
-                               bf16* __restrict__ dk, bf16* __restrict__ dv, int64_t dst_ld) {
-  __shared__ float2 cs[128];
-  rope_table(cs, d, delta, inv_freq);
-  measure_rows(kr, vr, real_ld, kb, vb, base_ld, rows, n_lh, d, il, cs, dk, dv, dst_ld);
-}
-
 // All measured offsets of one insert in one launch: blockIdx.z = job.
 __global__ void measure_batch_kernel(const __grid_constant__ MeasureJobs jobs, int n_lh, int d, int il,
                                      const double* __restrict__ inv_freq) {
@@ -188,17 +178,6 @@ cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs,
   g.x = max(1u, g.x / unsigned(n) + 1u);
   g.z = unsigned(n);
   measure_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_measure(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
-                           const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                           int interleaved, const double* inv_freq, bf16* dk, bf16* dv, int64_t dst_ld,
-                           cudaStream_t s) {
-  const int n_lh = Ls * Hs;
-  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
-  measure_kernel<<<grid2d(int64_t(rows) * (d / 16), 256, n_lh), 256, 0, s>>>(
-      k_real, v_real, real_ld, k_base, v_base, base_ld, rows, n_lh, d, delta, interleaved, inv_freq, dk, dv, dst_ld);
   return cudaGetLastError();
 }
 
@@ -386,20 +365,6 @@ __device__ __forceinline__ void measure_fp8_rows(const bf16* __restrict__ kr, co
   }
 }
 
-__global__ void quantize_rows_kernel(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
-                                     int64_t lh_bytes, int n_lh, int rows, int d) {
-  quantize_rows(src, src_ld, dst, lh_bytes, n_lh, rows, d);
-}
-
-__global__ void measure_fp8_kernel(const bf16* __restrict__ kr, const bf16* __restrict__ vr, int64_t real_ld,
-                                   const bf16* __restrict__ kb, const bf16* __restrict__ vb, int64_t base_ld,
-                                   int n_lh, int rows, int d, int delta, int il, const double* __restrict__ inv_freq,
-                                   uint8_t* __restrict__ dk, uint8_t* __restrict__ dv, int64_t lh_bytes) {
-  __shared__ float2 cs[128];
-  rope_table(cs, d, delta, inv_freq);
-  measure_fp8_rows(kr, vr, real_ld, kb, vb, base_ld, n_lh, rows, d, il, cs, dk, dv, lh_bytes);
-}
-
 // One launch per insert (fp8 pools): blockIdx.z = job; dst_ld carries lh_bytes.
 __global__ void quantize_rows_batch_kernel(const __grid_constant__ CopyJobs jobs, int n_lh, int d) {
   const CopyJob& J = jobs.j[blockIdx.z];
@@ -455,27 +420,6 @@ __global__ void read_fp8_kernel(const uint8_t* __restrict__ src, int64_t lh_byte
     }
     scales[r] = *o.scale;
   }
-}
-
-cudaError_t launch_quantize_rows(const bf16* src, int64_t src_ld, uint8_t* dst, int64_t lh_bytes, int Ls, int Hs,
-                                 int rows, int d, cudaStream_t s) {
-  const int n_lh = Ls * Hs;
-  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
-  quantize_rows_kernel<<<grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh), 256, 0, s>>>(
-      src, src_ld, dst, lh_bytes, n_lh, rows, d);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_measure_fp8(const bf16* k_real, const bf16* v_real, int64_t real_ld, const bf16* k_base,
-                               const bf16* v_base, int64_t base_ld, int rows, int Ls, int Hs, int d, int delta,
-                               int interleaved, const double* inv_freq, uint8_t* dk, uint8_t* dv, int64_t lh_bytes,
-                               cudaStream_t s) {
-  const int n_lh = Ls * Hs;
-  if (int64_t(n_lh) * rows == 0) return cudaSuccess;
-  measure_fp8_kernel<<<grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh), 256, 0, s>>>(
-      k_real, v_real, real_ld, k_base, v_base, base_ld, n_lh, rows, d, delta, interleaved, inv_freq, dk, dv,
-      lh_bytes);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_read_fp8(const uint8_t* src, int64_t lh_bytes, uint8_t* codes, float* scales, int Ls, int Hs,
