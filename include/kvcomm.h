@@ -242,10 +242,14 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t pool, int32_t L
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_set_offsets(kvcomm_pool_t pool, int32_t slot,
                                                         const kvcomm_offset_desc* offs,
                                                         int32_t n_offs, void* stream);
+/* Drop an anchor (LFU pruning, happens inside insert when the pool is full;
+ * this is the explicit form).  NOT_FOUND if the slot is empty. */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_evict(kvcomm_pool_t pool, int32_t slot);
 /* +1 access for each listed slot (reading A18: once per Shareable turn). */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_record_access(kvcomm_pool_t pool,
                                                           const int32_t* slots, int32_t n);
+/* Host metadata of one slot (occupancy, length, access count, insertion index,
+ * per-consumer offset-presence masks). */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t pool, int32_t slot,
                                                       kvcomm_slot_info* info);
 /* Device view of a stored offset (which: 0 placeholder, 1 prefix) of a bf16 pool:
@@ -303,10 +307,16 @@ typedef struct {
   kvcomm_match_info* info;   /* host, filled on return */
 } kvcomm_match_request;
 
+/* kvcomm_match_anchors for n requests in one batched launch (distances + weights,
+ * chunk sums, finalize), then one host synchronisation to fill every info.  Each pool
+ * may appear once per batch (its match scratch is per pool); all pools on one device. */
 KVCOMM_API kvcomm_status kvcomm_match_anchors_batch(const kvcomm_match_request* reqs, int32_t n,
                                                     void* stream);
 
 /* ---- a4-a5: fused blend + RoPE-δ + add ------------------------------------ */
+/* One segment (Eq. 6 placeholder, Eq. 7 prefix, or a verbatim COPY) into its
+ * destination rows, stream-ordered, no host synchronisation.  Validation errors
+ * (SHAPE_MISMATCH, NO_CANDIDATES, MISSING_OFFSET, ...) return before any launch. */
 KVCOMM_API kvcomm_status kvcomm_realign_segment(const kvcomm_realign_desc* seg, void* stream);
 /* All segments of one request in ONE persistent kernel launch.  Segments may come
  * from different pools but must share (Ls, Hs, d) and device. */
@@ -367,10 +377,16 @@ typedef struct {
   int64_t dst_ld;
 } kvcomm_plan_agent;
 
+/* Compile a request layout into a native executor: validates every segment and
+ * checks each agent's ledger (segments tile [0, N) exactly) once; allocates the
+ * plan's weight buffers and match scratch (owned by the plan, so plans over shared
+ * pools may run concurrently on different streams).  Destinations may be peer-GPU
+ * memory mapped with kvcomm_ipc_open (the fused gather). */
 KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, int32_t n_matches,
                                             const kvcomm_plan_segment* segs, int32_t n_segs,
                                             const kvcomm_plan_agent* agents, int32_t n_agents,
                                             kvcomm_plan_t* out);
+/* Waits for in-flight runs, frees the plan's buffers. */
 KVCOMM_API kvcomm_status kvcomm_plan_destroy(kvcomm_plan_t plan);
 /* query_embs: host array of n_matches device pointers (bf16 [L_phi][D_e]).  sync != 0
  * waits for the run to finish.  Pool metadata is read at call time. */
