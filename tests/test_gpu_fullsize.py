@@ -18,11 +18,14 @@ from tests import harness
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def state():
+@pytest.fixture(scope="module", params=["bf16", "fp8"])
+def state(request):
+    """The request with bf16 pools (the bench) and with fp8-e4m3 pools (f3; the oracle
+    then blends its own quantise/dequantise of the same offsets)."""
     assert torch.cuda.is_available()
     from synth.state import build_five_agent_state
-    st = build_five_agent_state(seed=0, gamma=0.3, anchor_extra=16)
+    st = build_five_agent_state(seed=0, gamma=0.3, anchor_extra=16, offset_format=request.param)
+    st.offset_format = request.param
     res = st.request.run(st.queries)
     torch.cuda.synchronize()
     yield st, res
@@ -78,8 +81,10 @@ def _sample_rows(st, res, agent, seg_idx, tokens, lh_pairs):
         kindkey = "pf"
         base_k = harness.f64(inp.prefix_base(s.pool, s.consumer, 0)[:, :, tokens])
         base_v = harness.f64(inp.prefix_base(s.pool, s.consumer, 1)[:, :, tokens])
-    dk = [harness.f64(inp.offset(s.pool, j, s.consumer, kindkey, 0)[:, :, tokens]) for j in cands]
-    dv = [harness.f64(inp.offset(s.pool, j, s.consumer, kindkey, 1)[:, :, tokens]) for j in cands]
+    store = ((lambda x: O.dequantize_rows_fp8(*O.quantize_rows_fp8(x))) if st.offset_format == "fp8"
+             else (lambda x: x))
+    dk = [store(harness.f64(inp.offset(s.pool, j, s.consumer, kindkey, 0)[:, :, tokens])) for j in cands]
+    dv = [store(harness.f64(inp.offset(s.pool, j, s.consumer, kindkey, 1)[:, :, tokens])) for j in cands]
     ora = O.realign_segment(wts, base_k, base_v, dk, dv, s.base_start, s.target_start, st.inv_freq)
     absk = O.blend_placeholder(wts, [np.abs(x) for x in dk])
     absv = O.blend_placeholder(wts, [np.abs(x) for x in dv])
