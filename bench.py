@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
                     help="N>1: realign writes each layer block straight into the consumer GPU's cache over "
                          "NVLink (fused, default) or a separate NCCL send/recv gather pass (baseline)")
+    ap.add_argument("--match", default="sharded", choices=["sharded", "replicated"],
+                    help="N>1: each rank computes 1/N of the match positions and stores them into every rank "
+                         "(sharded, default) or every rank matches every position (replicated)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -189,7 +192,8 @@ def arm_config(args, world, w):
                         "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
             "realigned_tokens_per_step": w.realigned_tokens, "anchors_blended": w.capacity,
             "gamma": args.gamma, "offset_storage": args.offsets,
-            "parallelism": f"layer-shard x{world}, {args.gather} gather" if world > 1 else "single",
+            "parallelism": (f"layer-shard x{world}, {args.gather} gather, {args.match} matching" if world > 1
+                            else "single"),
             "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
 
 
@@ -278,7 +282,7 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
             for n, (hk, hv) in bases.items():
                 dev_bases[n][0].copy_(hk, non_blocking=True)
                 dev_bases[n][1].copy_(hv, non_blocking=True)
-            req.plan.run(qlist, sync=False, stream=stream)
+            req.launch(qlist, stream=stream)
             deliver()
             for f, ho in zip(full, host_out):
                 if ho is not None:
@@ -451,6 +455,12 @@ def main():
                 full.append((None, None))
 
     plan = req.plan                      # native executor: one batched match + one gated realign launch per step
+    if world > 1 and args.match == "sharded":
+        try:   # 1/G of the match positions per rank, exchanged over NVLink
+            req.shard_matching(rank, world, local)
+        except RuntimeError as e:   # all ranks raise together
+            print(f"[bench] {e}; every rank matches every position", file=sys.stderr, flush=True)
+            args.match = "replicated (ipc unavailable)"
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
 
@@ -463,7 +473,7 @@ def main():
     def step(events=None):
         if events is not None:
             plan.set_events(*events)     # recorded right before / after the realign launch
-        plan.run(qlist, sync=False, stream=stream)   # no host synchronisation inside a step
+        req.launch(qlist, stream=stream)   # no host synchronisation inside a step
         deliver()
 
     for _ in range(args.warmup):

@@ -400,9 +400,42 @@ KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t plan, kvcomm_match_in
  * stream immediately before and after the realign launch of every later run; NULL
  * disables.  Lets a caller time the realign kernel alone inside a pipelined run. */
 KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before_realign, void* after_realign);
-/* Device pointers of the plan's weights for match `match` (W [capacity][ld_w], w̄). */
+/* Device pointers of the LAST run's weights for match `match` (W [capacity][ld_w], w̄;
+ * runs alternate between two buffer sets). */
 KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, const float** W,
                                              int64_t* ld_w, const float** wbar);
+
+/* ---- sharded matching across the ranks of a layer-sharded request -------
+ * The weights of Eq. 5/6 depend only on the sample, so a plan replicated on
+ * G ranks (same pools' slots and lengths, same matches, each rank its own layer block)
+ * would compute the same distances G times.  After kvcomm_plan_match_shard, each rank
+ * computes only its contiguous 1/G range of every job's position blocks and stores those
+ * W columns and d̄ partial rows into its own buffers AND every peer's (NVLink stores into
+ * the peers' match buffers, mapped by CUDA IPC); the fixed-order d̄ reduction, w̄, H and
+ * the verdict then run on the complete arrays on every rank, so every rank's weights and
+ * verdicts are bit-identical to an unsharded run.  A sharded run is split in two:
+ *   kvcomm_plan_run_begin  (candidate filter, table upload, distance+weight kernel)
+ *   -- caller: a stream-ordered cross-rank barrier, e.g. an NCCL all-reduce of one word --
+ *   kvcomm_plan_run_end    (d̄ reduction + verdict, gated realign)
+ * and kvcomm_plan_run refuses a sharded plan.  Every rank must call begin/end once per
+ * request in lockstep (buffer parities alternate; kvcomm_plan_match_shard resets them).
+ * The per-job tie_band_count then counts this rank's positions only. */
+/* Export the plan's match buffers (W, w̄ and scratch of both parities, one allocation):
+ * `bytes` (may be NULL) lets ranks check that their plans have the same layout. */
+struct kvcomm_ipc_handle;  /* defined with the fused gather below */
+KVCOMM_API kvcomm_status kvcomm_plan_match_handle(kvcomm_plan_t plan, struct kvcomm_ipc_handle* handle,
+                                                  int64_t* bytes);
+/* handles[world]: every rank's kvcomm_plan_match_handle (this rank's entry ignored).
+ * Opens the peers' buffers (closing any earlier mapping, after in-flight runs finish).
+ * world = 1 returns the plan to unsharded matching (handles may be NULL).
+ * INVALID_ARGUMENT: world outside [1, 8], rank outside [0, world), a run begun; CUDA:
+ * a handle cannot be opened (nothing stays mapped). */
+KVCOMM_API kvcomm_status kvcomm_plan_match_shard(kvcomm_plan_t plan, int32_t rank, int32_t world,
+                                                 const struct kvcomm_ipc_handle* handles);
+/* The two halves of kvcomm_plan_run (same arguments); also usable unsharded.
+ * INVALID_ARGUMENT: begin twice, or end without begin. */
+KVCOMM_API kvcomm_status kvcomm_plan_run_begin(kvcomm_plan_t plan, const void* const* query_embs, void* stream);
+KVCOMM_API kvcomm_status kvcomm_plan_run_end(kvcomm_plan_t plan, int32_t sync, void* stream);
 
 /* ---- the fused gather (SURVEY §8(e) "fuse the gather into the realign epilogue with
  * NVLink P2P stores"; north star: realigned caches land on the GPU that prefills the

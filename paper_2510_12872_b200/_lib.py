@@ -139,6 +139,10 @@ _SIGS = {
     "kvcomm_plan_set_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvcomm_plan_weights": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_void_p)]),
+    "kvcomm_plan_match_handle": (C.c_int, [C.c_void_p, C.POINTER(IpcHandle), C.POINTER(C.c_int64)]),
+    "kvcomm_plan_match_shard": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(IpcHandle)]),
+    "kvcomm_plan_run_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
+    "kvcomm_plan_run_end": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "kvcomm_ipc_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
     "kvcomm_ipc_free": (C.c_int, [C.c_void_p]),
     "kvcomm_ipc_open": (C.c_int, [C.c_int32, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),

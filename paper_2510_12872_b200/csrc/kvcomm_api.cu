@@ -706,7 +706,14 @@ struct MatchItem {
   double* dist;
   const kvcomm_match_info* info;  // candidates
   double* scratch = nullptr;      // partial + chunk sums owned by the caller (plans), else the pool's
+  // sharded matching (plans only): own position blocks [own_lo, own_lo + n_own), n_own < 0 = all;
+  // W columns and partial rows also stored into the peers' copies
+  int own_lo = 0, n_own = -1, n_peer = 0;
+  float* W_peer[kMaxMatchPeers] = {};
+  double* partial_peer[kMaxMatchPeers] = {};
 };
+
+static int match_blocks(int L_phi) { return (L_phi + kMatchP - 1) / kMatchP; }
 
 struct MatchLayout {
   MatchHdr hdr{};
@@ -723,7 +730,8 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
   int blocks = 0;
   for (const MatchItem& it : items) {
     n_ints += it.info->n_candidates + it.p->cap;
-    blocks += (it.L_phi + kMatchP - 1) / kMatchP;
+    blocks += it.n_own >= 0 ? it.n_own : match_blocks(it.L_phi);
+    if (it.n_peer > 0) L.hdr.any_peer = 1;
     L.smem = std::max(L.smem, align_up(size_t(kMatchP) * it.p->De * 2, 16) +
                                   size_t(kMatchP) * (3 * it.info->n_candidates + 1) * sizeof(double));
   }
@@ -781,9 +789,16 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     for (int sl = 0; sl < p->cap; ++sl) ints[ipos + sl] = -1;
     for (int j = 0; j < a.n_cand; ++j) ints[ipos + it.info->candidates[j]] = j;
     ipos += p->cap;
-    a.n_blocks = (it.L_phi + kMatchP - 1) / kMatchP;
+    a.n_blocks = match_blocks(it.L_phi);
     a.block_begin = blocks;
-    blocks += a.n_blocks;
+    a.own_lo = it.n_own >= 0 ? it.own_lo : 0;
+    a.n_own = it.n_own >= 0 ? it.n_own : a.n_blocks;
+    blocks += a.n_own;
+    a.n_peer = it.n_peer;
+    for (int r = 0; r < it.n_peer; ++r) {
+      a.W_peer[r] = it.W_peer[r];
+      a.partial_peer[r] = it.partial_peer[r];
+    }
   }
 }
 
@@ -1220,11 +1235,24 @@ struct kvcomm_plan_s {
   std::vector<kvcomm_plan_segment> segs;
   std::vector<kvcomm_plan_agent> agents;
   std::vector<std::vector<int>> agent_matches;  // distinct matches each agent depends on
-  std::vector<float*> W, wbar;
-  std::vector<double*> scratch;   // per match: [ceil(L_phi/P) + kMatchChunks][2 cap + 1]
+  // Match buffers, one set per table parity (run t uses set t % 2), all in ONE allocation
+  // (`xbuf`, exportable by CUDA IPC for sharded matching): per parity and match
+  // W [cap][ld_w] f32, w̄ [cap] f32, scratch [ceil(L_phi/P) + kMatchChunks][2 cap + 1] f64.
+  void* xbuf = nullptr;
+  int64_t xbytes = 0;
+  std::vector<int64_t> W_off[2], wbar_off[2], sc_off[2];  // byte offsets into xbuf
   std::vector<int64_t> ld_w;
+  // sharded matching: this rank's position blocks, and the peers' xbuf mappings
+  int rank = 0, world = 1;
+  std::vector<char*> peer_x;   // world - 1 mapped peer buffers (this process's addresses)
   RingEntry tab[2];
   int next = 0;
+  // a run between kvcomm_plan_run_begin and kvcomm_plan_run_end
+  bool pending = false;
+  MatchLayout pML;
+  RealignLayout pRL;
+  size_t proff = 0;
+  size_t n_items = 0, n_hs = 0;
   // last run
   int last = -1;
   std::vector<kvcomm_match_info> infos;
@@ -1234,15 +1262,26 @@ struct kvcomm_plan_s {
   int64_t res_off = 0;
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
   std::mutex mu;
+
+  char* xb() const { return static_cast<char*>(xbuf); }
+  float* W(int par, int i) const { return reinterpret_cast<float*>(xb() + W_off[par][i]); }
+  float* wbar(int par, int i) const { return reinterpret_cast<float*>(xb() + wbar_off[par][i]); }
+  double* scratch(int par, int i) const { return reinterpret_cast<double*>(xb() + sc_off[par][i]); }
 };
+
+static void plan_close_peers(kvcomm_plan_s* pl) {
+  for (char* x : pl->peer_x) cudaIpcCloseMemHandle(x);
+  pl->peer_x.clear();
+  pl->rank = 0;
+  pl->world = 1;
+}
 
 static void plan_free(kvcomm_plan_s* pl) {
   if (!pl) return;
   DeviceGuard g(pl->dev);
   for (auto& e : pl->tab) entry_free(e);
-  for (float* x : pl->W) cudaFree(x);
-  for (float* x : pl->wbar) cudaFree(x);
-  for (double* x : pl->scratch) cudaFree(x);
+  plan_close_peers(pl);
+  cudaFree(pl->xbuf);
   delete pl;
 }
 
@@ -1321,26 +1360,26 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
   pl->infos.resize(n_matches);
   pl->job_of.assign(n_matches, -1);
   pl->agent_state.assign(n_agents, 1);
-  for (int i = 0; i < n_matches; ++i) {
-    const int64_t ldw = (matches[i].L_phi + 3) & ~3;
-    float *w = nullptr, *wb = nullptr;
-    double* sc = nullptr;
-    const int64_t sc_n = (int64_t((matches[i].L_phi + kMatchP - 1) / kMatchP) + kMatchChunks) *
-                         (2 * matches[i].pool->cap + 1);
-    if (cudaMalloc(&w, sizeof(float) * ldw * matches[i].pool->cap) != cudaSuccess ||
-        cudaMalloc(&wb, sizeof(float) * matches[i].pool->cap) != cudaSuccess ||
-        cudaMalloc(&sc, sizeof(double) * sc_n) != cudaSuccess) {
-      cudaGetLastError();
-      cudaFree(w);
-      cudaFree(wb);
-      cudaFree(sc);
-      plan_free(pl);
-      return fail(KVCOMM_ERR_OUT_OF_MEMORY, "plan weight buffers");
+  int64_t off = 0;
+  for (int i = 0; i < n_matches; ++i) pl->ld_w.push_back((matches[i].L_phi + 3) & ~3);
+  for (int par = 0; par < 2; ++par)
+    for (int i = 0; i < n_matches; ++i) {
+      const int cap = matches[i].pool->cap;
+      pl->W_off[par].push_back(off);
+      off = int64_t(align_up(size_t(off + int64_t(sizeof(float)) * pl->ld_w[i] * cap), 256));
+      pl->wbar_off[par].push_back(off);
+      off = int64_t(align_up(size_t(off + int64_t(sizeof(float)) * cap), 256));
+      pl->sc_off[par].push_back(off);
+      off = int64_t(align_up(size_t(off + int64_t(sizeof(double)) * (match_blocks(matches[i].L_phi) + kMatchChunks) *
+                                              (2 * cap + 1)),
+                             256));
     }
-    pl->W.push_back(w);
-    pl->wbar.push_back(wb);
-    pl->scratch.push_back(sc);
-    pl->ld_w.push_back(ldw);
+  pl->xbytes = off;
+  if (cudaMalloc(&pl->xbuf, size_t(off)) != cudaSuccess) {
+    cudaGetLastError();
+    pl->xbuf = nullptr;
+    plan_free(pl);
+    return fail(KVCOMM_ERR_OUT_OF_MEMORY, "plan weight buffers (%lld bytes)", (long long)off);
   }
   *out = pl;
   return ok();
@@ -1352,11 +1391,10 @@ KVCOMM_API kvcomm_status kvcomm_plan_destroy(kvcomm_plan_t pl) {
   return ok();
 }
 
-KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* query_embs, int32_t sync,
-                                         void* stream) {
-  NvtxRange nvtx_("kvcomm_plan_run");
-  if (!pl || !query_embs) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/queries");
-  std::lock_guard<std::mutex> plk(pl->mu);
+// First half of a run: the candidate filter (a1, host), the work table upload and the
+// distance + weight kernel over this rank's position blocks.
+static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs, cudaStream_t s) {
+  if (pl->pending) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "plan run already begun (call kvcomm_plan_run_end)");
   const int nm = int(pl->matches.size());
   for (int i = 0; i < nm; ++i)
     if (!query_embs[i] || !aligned16(query_embs[i]))
@@ -1366,8 +1404,8 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
   std::vector<std::shared_lock<std::shared_mutex>> rlocks;
   lock_readers(pools, rlocks);
   DeviceGuard guard(pl->dev);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  RingEntry& E = pl->tab[pl->next];
+  const int par = pl->next;
+  RingEntry& E = pl->tab[par];
   KV_TRY(entry_reserve(E, 0));  // waits for the run that used this table two runs ago
   // a1 on the host; jobs for the entropy clause
   std::vector<MatchItem> items;
@@ -1383,8 +1421,19 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
     const int k_eff = m.top_k > 0 ? std::min(m.top_k, info->n_candidates) : 0;
     info->top_k = k_eff > 0 ? k_eff : info->n_candidates;
     pl->job_of[i] = int(items.size());
-    items.push_back({m.pool, query_embs[i], m.L_phi, m.gamma, k_eff, pl->W[i], pl->ld_w[i], nullptr, pl->wbar[i],
-                     nullptr, info, pl->scratch[i]});
+    MatchItem it{m.pool, query_embs[i], m.L_phi, m.gamma, k_eff, pl->W(par, i), pl->ld_w[i], nullptr,
+                 pl->wbar(par, i), nullptr, info, pl->scratch(par, i)};
+    if (pl->world > 1) {  // this rank's contiguous range of position blocks; the rest comes from the peers
+      const int nb = match_blocks(m.L_phi);
+      it.own_lo = int(int64_t(pl->rank) * nb / pl->world);
+      it.n_own = int(int64_t(pl->rank + 1) * nb / pl->world) - it.own_lo;
+      it.n_peer = int(pl->peer_x.size());
+      for (int r = 0; r < it.n_peer; ++r) {
+        it.W_peer[r] = reinterpret_cast<float*>(pl->peer_x[r] + pl->W_off[par][i]);
+        it.partial_peer[r] = reinterpret_cast<double*>(pl->peer_x[r] + pl->sc_off[par][i]);
+      }
+    }
+    items.push_back(it);
   }
   // segments of agents not already decided by the length clause, gated on device
   std::vector<HostSeg> hs;
@@ -1409,7 +1458,7 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
     d.dst_ld = a.dst_ld;
     if (g.kind != KVCOMM_COPY) {
       const kvcomm_match_info* info = &pl->infos[g.match];
-      d.weights = g.kind == KVCOMM_PLACEHOLDER ? pl->W[g.match] : pl->wbar[g.match];
+      d.weights = g.kind == KVCOMM_PLACEHOLDER ? pl->W(par, g.match) : pl->wbar(par, g.match);
       d.ld_w = pl->ld_w[g.match];
       d.candidates = info->candidates;
       d.n_candidates = info->n_candidates;
@@ -1432,25 +1481,75 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* qu
   if (!hs.empty()) write_realign(h + roff, dv + roff, RL, hs, gres);
   KV_CUDA(cudaMemcpyAsync(dv, h, hs.empty() ? ML.bytes : roff + size_t(RL.hdr.cs_off), cudaMemcpyHostToDevice, s));
   if (!items.empty()) {
-    KV_CUDA(launch_match_batch(dv, ML.hdr, ML.smem, s));
-    g_launches += 3;
+    KV_CUDA(launch_match_dist(dv, ML.hdr, ML.smem, s));
+    if (ML.hdr.total_blocks > 0) g_launches += 1;
+  }
+  pl->pML = ML;
+  pl->pRL = RL;
+  pl->proff = roff;
+  pl->n_items = items.size();
+  pl->n_hs = hs.size();
+  pl->pending = true;
+  return ok();
+}
+
+// Second half: d̄ / w̄ / H / verdict (chunk + finalize), then the gated realign.
+static kvcomm_status plan_end(kvcomm_plan_s* pl, int32_t sync, cudaStream_t s) {
+  if (!pl->pending) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "plan run not begun (call kvcomm_plan_run_begin)");
+  pl->pending = false;
+  DeviceGuard guard(pl->dev);
+  RingEntry& E = pl->tab[pl->next];
+  uint8_t* h = static_cast<uint8_t*>(E.host);
+  uint8_t* dv = static_cast<uint8_t*>(E.dev);
+  const MatchLayout& ML = pl->pML;
+  const RealignLayout& RL = pl->pRL;
+  const size_t roff = pl->proff;
+  if (pl->n_items) {
+    KV_CUDA(launch_match_reduce(dv, ML.hdr, s));
+    g_launches += 2;
   }
   if (pl->ev_before) KV_CUDA(cudaEventRecord(pl->ev_before, s));
-  if (!hs.empty()) {
+  if (pl->n_hs) {
     KV_CUDA(launch_realign(dv + roff, RL.hdr, grid_for_device(pl->dev), s));
     g_launches += RL.hdr.total_units > 0 ? 2 : 1;
   }
   if (pl->ev_after) KV_CUDA(cudaEventRecord(pl->ev_after, s));
-  if (!items.empty())
+  if (pl->n_items)
     KV_CUDA(cudaMemcpyAsync(h + ML.hdr.res_off, dv + ML.hdr.res_off, ML.bytes - size_t(ML.hdr.res_off),
                             cudaMemcpyDeviceToHost, s));
   KV_CUDA(cudaEventRecord(E.done, s));
   E.used = true;
-  pl->res_off = items.empty() ? -1 : ML.hdr.res_off;
+  pl->res_off = pl->n_items ? ML.hdr.res_off : -1;
   pl->last = pl->next;
   pl->next ^= 1;
   if (sync) KV_CUDA(cudaEventSynchronize(E.done));
   return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t pl, const void* const* query_embs, int32_t sync,
+                                         void* stream) {
+  NvtxRange nvtx_("kvcomm_plan_run");
+  if (!pl || !query_embs) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/queries");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  if (pl->world > 1)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "sharded plan: use kvcomm_plan_run_begin / sync / kvcomm_plan_run_end");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  KV_TRY(plan_begin(pl, query_embs, s));
+  return plan_end(pl, sync, s);
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_run_begin(kvcomm_plan_t pl, const void* const* query_embs, void* stream) {
+  NvtxRange nvtx_("kvcomm_plan_run_begin");
+  if (!pl || !query_embs) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/queries");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  return plan_begin(pl, query_embs, static_cast<cudaStream_t>(stream));
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_run_end(kvcomm_plan_t pl, int32_t sync, void* stream) {
+  NvtxRange nvtx_("kvcomm_plan_run_end");
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  return plan_end(pl, sync, static_cast<cudaStream_t>(stream));
 }
 
 KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t pl, kvcomm_match_info* infos, int32_t* agent_reused) {
@@ -1487,9 +1586,54 @@ KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t pl, void* before_r
 KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t pl, int32_t match, const float** W, int64_t* ld_w,
                                              const float** wbar) {
   if (!pl || match < 0 || match >= int32_t(pl->matches.size())) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "bad match");
-  if (W) *W = pl->W[match];
+  std::lock_guard<std::mutex> plk(pl->mu);
+  const int par = pl->last >= 0 ? pl->last : 0;  // the last run's buffers
+  if (W) *W = pl->W(par, match);
   if (ld_w) *ld_w = pl->ld_w[match];
-  if (wbar) *wbar = pl->wbar[match];
+  if (wbar) *wbar = pl->wbar(par, match);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_match_handle(kvcomm_plan_t pl, kvcomm_ipc_handle* handle, int64_t* bytes) {
+  if (!pl || !handle) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan/handle");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  DeviceGuard guard(pl->dev);
+  cudaIpcMemHandle_t h;
+  KV_CUDA(cudaIpcGetMemHandle(&h, pl->xbuf));
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  if (bytes) *bytes = pl->xbytes;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_match_shard(kvcomm_plan_t pl, int32_t rank, int32_t world,
+                                                 const kvcomm_ipc_handle* handles) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  if (world < 1 || world > kMaxMatchPeers + 1 || rank < 0 || rank >= world)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "rank %d / world %d (world <= %d)", rank, world, kMaxMatchPeers + 1);
+  if (world > 1 && !handles) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null handles");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  if (pl->pending) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "plan run in progress");
+  DeviceGuard guard(pl->dev);
+  for (auto& e : pl->tab)  // no run may still read the old mappings
+    if (e.used) KV_CUDA(cudaEventSynchronize(e.done));
+  plan_close_peers(pl);
+  pl->next = 0;  // every rank's runs use buffer parity 0, 1, 0, ... in lockstep from here
+  if (world == 1) return ok();
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles[r].bytes, sizeof(h));
+    void* x = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&x, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      plan_close_peers(pl);
+      return fail(KVCOMM_ERR_CUDA, "rank %d: opening peer %d's match buffers: %s", rank, r, cudaGetErrorString(e));
+    }
+    pl->peer_x.push_back(static_cast<char*>(x));
+  }
+  pl->rank = rank;
+  pl->world = world;
   return ok();
 }
 

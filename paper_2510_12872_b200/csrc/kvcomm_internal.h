@@ -83,6 +83,8 @@ struct TableHdr {
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s);
 int realign_grid_size(int device);
 
+constexpr int kMaxMatchPeers = 7;   // one box: 8 GPUs
+
 // One matching job (one query sample against one pool), as the kernels see it.
 struct MatchJob {
   const bf16* query;        // [L_phi][De]
@@ -102,17 +104,29 @@ struct MatchJob {
   int32_t cosine;           // 1: d = 1 - cos; partials Σ q·a, Σ a·a (per candidate) and Σ q·q
   int32_t cand_off;         // into MatchHdr ints: candidate slot ids [n_cand]
   int32_t s2c_off;          // into MatchHdr ints: slot -> candidate index or -1 [cap]
-  int32_t block_begin, n_blocks;
+  int32_t block_begin, n_blocks;  // block_begin: first work item of this job; n_blocks: ALL position blocks
+  // Sharded matching: this launch computes position blocks
+  // [own_lo, own_lo + n_own) only and stores their W columns and partial rows into
+  // this GPU's buffers AND every peer's copy (IPC-mapped) — the chunk/finalize passes
+  // then run on the complete arrays on every rank.  Unsharded: own_lo 0, n_own =
+  // n_blocks, n_peer 0.
+  int32_t own_lo, n_own;
+  int32_t n_peer, _pad_peer;
+  float* W_peer[kMaxMatchPeers];
+  double* partial_peer[kMaxMatchPeers];
 };
 
 // Device-side table of one batched match launch.
 struct MatchHdr {
-  int32_t n_jobs, total_blocks, P, _pad;
+  int32_t n_jobs, total_blocks, P, any_peer;   // total_blocks: work items of this launch (owned blocks)
   int64_t job_off, int_off, res_off, tie_off;   // byte offsets from the table base
 };
 
 // distance + per-position weights over all jobs' blocks, then one finalize block per job
 cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_t smem_bytes, cudaStream_t s);
+// the two halves of launch_match_batch (sharded plans put the cross-rank sync between them)
+cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem_bytes, cudaStream_t s);
+cudaError_t launch_match_reduce(const void* table_dev, const MatchHdr& hdr, cudaStream_t s);
 
 // Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,

@@ -98,7 +98,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
   const int jb = find_job(jobs, hdr->n_jobs, item);
   const MatchJob& a = jobs[jb];
   const int P = hdr->P;
-  const int lb = item - a.block_begin;
+  const int lb = a.own_lo + (item - a.block_begin);  // position block (sharded: inside this rank's range)
   const int32_t* cand = ints + a.cand_off;
   const int32_t* slot2cand = ints + a.s2c_off;
 
@@ -177,7 +177,10 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
       sum = warp_sum_d(sum);
       for (int sl = lane; sl < a.cap; sl += 32) {
         const int j = slot2cand[sl];
-        a.W[int64_t(sl) * a.ld_w + i] = j >= 0 ? float(exp(-(dr[j] - mn)) / sum) : 0.f;
+        const float w = j >= 0 ? float(exp(-(dr[j] - mn)) / sum) : 0.f;
+        const int64_t o = int64_t(sl) * a.ld_w + i;
+        a.W[o] = w;
+        for (int r = 0; r < a.n_peer; ++r) a.W_peer[r][o] = w;
       }
     } else {
       // top-k: k rounds of lexicographic (distance, slot) argmin over the unselected
@@ -220,7 +223,15 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
         a.W[int64_t(sel_s) * a.ld_w + i] = float(ev / sum);
         if (a.idx) a.idx[int64_t(i) * k + lane] = sel_s;
       }
-      if (lane == 0 && tie) atomicAdd(&ties[jb], 1);
+      if (a.n_peer > 0) {  // peers receive the finished column: one store per address
+        __syncwarp();
+        for (int sl = lane; sl < a.cap; sl += 32) {
+          const int64_t o = int64_t(sl) * a.ld_w + i;
+          const float w = a.W[o];
+          for (int r = 0; r < a.n_peer; ++r) a.W_peer[r][o] = w;
+        }
+      }
+      if (lane == 0 && tie) atomicAdd(&ties[jb], 1);  // sharded: this rank's positions only
     }
   }
 
@@ -234,6 +245,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
         s += a.scalar_mode == 0 ? dv * dv : dv;
       }
       a.partial[int64_t(lb) * n_cand + j] = s;
+      for (int r = 0; r < a.n_peer; ++r) a.partial_peer[r][int64_t(lb) * n_cand + j] = s;
     }
   } else {
     const int64_t stride = 2 * n_cand + 1;
@@ -245,18 +257,23 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
       }
       a.partial[int64_t(lb) * stride + j] = sqa;
       a.partial[int64_t(lb) * stride + n_cand + j] = saa;
+      for (int r = 0; r < a.n_peer; ++r) {
+        a.partial_peer[r][int64_t(lb) * stride + j] = sqa;
+        a.partial_peer[r][int64_t(lb) * stride + n_cand + j] = saa;
+      }
     }
     if (threadIdx.x == 0) {
       double sqq = 0.0;
       for (int p = 0; p < np; ++p) sqq += s_qq[p];
       a.partial[int64_t(lb) * stride + 2 * n_cand] = sqq;
+      for (int r = 0; r < a.n_peer; ++r) a.partial_peer[r][int64_t(lb) * stride + 2 * n_cand] = sqq;
     }
   }
 }
 
 // Persistent blocks pull items from an atomic counter (the table's word after the
 // per-job tie counters, zeroed by the host upload), so the last wave has no tail of
-// idle SMs.  The processing order does not affect any result: every item writes its
+// idle SMs.  Sharded matching: the items are this rank's position blocks only.  The processing order does not affect any result: every item writes its
 // own W columns and partial sums.
 __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t* __restrict__ tab) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
@@ -270,6 +287,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
     match_item(tab, item);
     __syncthreads();  // shared memory is reused by the next item
   }
+  if (hdr->any_peer) __threadfence_system();  // peer stores visible before the caller's cross-rank sync
 }
 
 // First pass of d̄ (and the cosine sums): block (job, c) sums position blocks
@@ -370,7 +388,8 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
   }
 }
 
-cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
+cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
+  if (hdr.total_blocks == 0) return cudaSuccess;  // sharded: this rank owns no block
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
@@ -383,9 +402,19 @@ cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_dist_kernel, kMatchThreads, smem);
   const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));
   match_dist_kernel<<<grid, kMatchThreads, smem, s>>>(t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_match_reduce(const void* table_dev, const MatchHdr& hdr, cudaStream_t s) {
+  uint8_t* t = reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev));
   match_chunk_kernel<<<dim3(hdr.n_jobs, kMatchChunks), 256, 0, s>>>(t);
   match_finalize_kernel<<<hdr.n_jobs, 1024, 0, s>>>(t);
   return cudaGetLastError();
+}
+
+cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
+  cudaError_t e = launch_match_dist(table_dev, hdr, smem, s);
+  return e != cudaSuccess ? e : launch_match_reduce(table_dev, hdr, s);
 }
 
 }  // namespace kvc

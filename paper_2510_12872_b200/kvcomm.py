@@ -419,12 +419,40 @@ class Plan:
         self.n_matches, self.n_agents = len(matches), len(agents)
         self._events = None
 
-    def run(self, queries: Sequence[torch.Tensor], sync: bool = False, stream=None) -> None:
+    def _queries(self, queries: Sequence[torch.Tensor]):
         for q in queries:
             if q.dtype != torch.bfloat16 or not q.is_cuda or not q.is_contiguous():
                 raise ValueError("queries must be contiguous bf16 CUDA tensors")
-        arr = (C.c_void_p * self.n_matches)(*[q.data_ptr() for q in queries])
-        L.check(L.lib().kvcomm_plan_run(self._h, arr, 1 if sync else 0, _stream_handle(stream)))
+        return (C.c_void_p * self.n_matches)(*[q.data_ptr() for q in queries])
+
+    def run(self, queries: Sequence[torch.Tensor], sync: bool = False, stream=None) -> None:
+        L.check(L.lib().kvcomm_plan_run(self._h, self._queries(queries), 1 if sync else 0, _stream_handle(stream)))
+
+    def run_begin(self, queries: Sequence[torch.Tensor], stream=None) -> None:
+        """First half of a run (candidate filter, table upload, distance kernel); a
+        sharded plan needs a cross-rank barrier before run_end."""
+        L.check(L.lib().kvcomm_plan_run_begin(self._h, self._queries(queries), _stream_handle(stream)))
+
+    def run_end(self, sync: bool = False, stream=None) -> None:
+        L.check(L.lib().kvcomm_plan_run_end(self._h, 1 if sync else 0, _stream_handle(stream)))
+
+    def match_handle(self) -> Tuple[bytes, int]:
+        """(64-byte IPC handle, size) of the plan's match buffers, for kvcomm_plan_match_shard."""
+        h, n = L.IpcHandle(), C.c_int64()
+        L.check(L.lib().kvcomm_plan_match_handle(self._h, C.byref(h), C.byref(n)))
+        return C.string_at(C.addressof(h), 64), n.value
+
+    def match_shard(self, rank: int, world: int, handles: Sequence[bytes] = ()) -> None:
+        """Shard matching over `world` ranks (handles: every rank's match_handle()[0])."""
+        arr = None
+        if world > 1:
+            if len(handles) != world:
+                raise ValueError("one handle per rank")
+            arr = (L.IpcHandle * world)()
+            for r, hb in enumerate(handles):
+                assert len(hb) == 64
+                C.memmove(C.addressof(arr[r]), hb, 64)
+        L.check(L.lib().kvcomm_plan_match_shard(self._h, int(rank), int(world), arr))
 
     def set_events(self, before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]) -> None:
         """Record `before`/`after` around the realign launch of later runs (kernel timing)."""

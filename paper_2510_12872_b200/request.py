@@ -89,10 +89,24 @@ class ReuseRequest:
             self._plan = K.Plan(matches, segs, [(a.N, a.dst_k, a.dst_v) for a in self.agents])
         return self._plan
 
+    def shard_matching(self, rank: int, world: int, device: int, group=None) -> None:
+        """Layer-sharded request on `world` ranks: compute 1/world of the match positions
+        here and exchange them (shard.MatchShard) instead of recomputing every distance."""
+        from .shard import MatchShard
+        self._mshard = MatchShard(self.plan, rank, world, device, group) if world > 1 else None
+
     def run(self, queries: Dict[str, torch.Tensor], stream=None, sync: bool = True) -> Optional["RequestResult"]:
         """Plan path.  sync=False only enqueues (collect with results())."""
-        self.plan.run([queries[n] for n in self.names], sync=sync, stream=stream)
+        self.launch([queries[n] for n in self.names], stream=stream, sync=sync)
         return self.results() if sync else None
+
+    def launch(self, qlist: List[torch.Tensor], stream=None, sync: bool = False) -> None:
+        """Enqueue one run of the plan (queries in self.names order); sharded matching
+        when shard_matching() was called."""
+        if getattr(self, "_mshard", None) is not None:
+            self._mshard.run(qlist, stream=stream, sync=sync)
+        else:
+            self.plan.run(qlist, sync=sync, stream=stream)
 
     def results(self) -> "RequestResult":
         ms, reused_flags = self.plan.results()

@@ -11,7 +11,7 @@ torch.distributed; no all-gather, which would move G times the bytes).
 """
 from __future__ import annotations
 
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
@@ -70,6 +70,71 @@ def gather_to_consumers(agents: Sequence[int], shards: Sequence[Tuple[torch.Tens
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+
+
+def stream_barrier(flag: Optional[torch.Tensor], group=None) -> None:
+    """Cross-rank barrier ordered on the current CUDA stream: an NCCL all-reduce of one
+    word (`flag`, a 1-element CUDA tensor) completes on a rank only once every rank's
+    earlier work on its stream — including its peer stores — has finished.  gloo (the
+    CPU-box / same-GPU test path): drain the stream, then a host barrier."""
+    if flag is not None:
+        dist.all_reduce(flag, group=group)
+    else:
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
+
+
+class MatchShard:
+    """Sharded matching: the weights of Eq. 5/6 depend only on the sample,
+    so instead of every rank recomputing every distance, rank r computes its 1/G of each
+    match job's position blocks and stores the W columns and d̄ partials into every
+    rank's plan buffers (kvcomm_plan_match_shard: IPC-mapped, written over NVLink by the
+    distance kernel itself).  A run is then run_begin → stream_barrier → run_end; every
+    rank reduces the complete partials in the same fixed order, so weights and verdicts
+    are bit-identical on all ranks and to an unsharded run.  Handles are exchanged once;
+    failures are agreed on collectively (all ranks raise together)."""
+
+    def __init__(self, plan, rank: int, world: int, device: int, group=None):
+        self.plan, self.rank, self.world, self.group = plan, rank, world, group
+        err, mine = None, None
+        try:
+            mine = plan.match_handle()
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank}: {e}"
+        everyone = [None] * world
+        dist.all_gather_object(everyone, (err, mine), group=group)
+        errs = [e for e, _ in everyone if e]
+        if not errs:
+            sizes = {m[1] for _, m in everyone}
+            if len(sizes) != 1:
+                errs = [f"plans differ across ranks (match buffer sizes {sorted(sizes)})"]
+        if not errs:
+            try:
+                plan.match_shard(rank, world, [m[0] for _, m in everyone])
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {rank}: {e}"
+            status = [None] * world
+            dist.all_gather_object(status, err, group=group)
+            errs = [e for e in status if e]
+            if errs and err is None:
+                plan.match_shard(0, 1)
+        if errs:
+            raise RuntimeError("sharded matching unavailable: " + "; ".join(errs))
+        nccl = dist.get_backend(group) == "nccl"
+        self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}") if nccl else None
+
+    def run(self, queries, stream=None, sync: bool = False) -> None:
+        """One request: this rank's distances (+ peer stores), barrier, reduction + realign."""
+        self.plan.run_begin(queries, stream=stream)
+        if stream is None:
+            stream_barrier(self._flag, self.group)
+        else:
+            with torch.cuda.stream(stream):
+                stream_barrier(self._flag, self.group)
+        self.plan.run_end(sync=sync, stream=stream)
+
+    def close(self) -> None:
+        self.plan.match_shard(0, 1)
 
 
 class PeerRows:
@@ -185,11 +250,7 @@ class PeerCaches:
     def sync(self) -> None:
         """Consumers' later reads are ordered after every rank's realign launch: a
         stream-ordered all-reduce of one word over NCCL (gloo test path: host barrier)."""
-        if self._flag is not None:
-            dist.all_reduce(self._flag, group=self.group)
-        else:
-            torch.cuda.current_stream().synchronize()
-            dist.barrier(group=self.group)
+        stream_barrier(self._flag, self.group)
 
     def close(self) -> None:
         L = self._L

@@ -81,6 +81,34 @@ def main():
         steps.append(e0.elapsed_time(e1) / 4)
         realign.extend(ks)
     step_ms = sorted(steps)[len(steps) // 2]
+
+    # Sharded matching: with G ranks each computes T/G positions of the match.
+    # One rank's share is timed here as a match-only plan over the first T/G positions of
+    # the same query and pool (one 1-token COPY segment keeps the plan well-formed), with
+    # the device kept busy while the host prepares the run so that the events see device
+    # time only.  The peer stores of the W columns and partials (7/G of ~M*T*12 B) and the
+    # cross-rank barrier are not in this number (no second GPU here).
+    match_ms = {}
+    one = [torch.zeros(Ls, Hs, 1, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    tiny = [torch.empty(Ls, Hs, 1, D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    for G in (1, 2, 4, 8):
+        Tg = T // G
+        mp = kv.Plan([(pool, Tg, 0.3, 0)], [kv.PlanSegment(0, 0, kv.COPY, 0, one[0], one[1], 0, 0)],
+                     [(1, tiny[0], tiny[1])])
+        qg = query[:Tg].contiguous()
+        for _ in range(3):
+            mp.run([qg], stream=stream)
+        ts = []
+        for _ in range(7):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(2_000_000)       # ~1 ms of device work hides the host-side preparation
+            e0.record(stream)
+            mp.run([qg], stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        match_ms[G] = sorted(ts)[len(ts) // 2]
+        mp.destroy()
     rl_ms = sorted(realign)[len(realign) // 2]
     tok = Ls * Hs * D * 2 * 2  # one token row, K+V, this shard
     alg = ((M + 2) * T + (M + 2) * P + 2 * P0) * tok
@@ -93,6 +121,10 @@ def main():
         "shard_tokens_per_s": (T + P) / (step_ms / 1e3),
         "realign_alg_bytes": alg, "realign_GBps": alg / (rl_ms / 1e3) / 1e9,
         "frac_of_measured_peak": (alg / (rl_ms / 1e3) / 1e9 / peak) if peak else None,
+        "match_only_ms_by_G": match_ms,
+        "match_note": "match-only plan over T/G positions (+1-token copy): one rank's share of sharded "
+                      "matching, without its NVLink stores and the barrier",
+        "step_ms_sharded_match_G8_est": step_ms - match_ms[1] + match_ms[8],
         "note": "one of 8 shards measured on one B200; the 8-GPU run is not measured here"}))
     plan.destroy()
     pool.destroy()

@@ -19,6 +19,8 @@ import torch.distributed as dist
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
+    shard_match = len(sys.argv) > 2 and sys.argv[2] == "shard-match"
+    top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
     import synth
@@ -29,8 +31,9 @@ def main():
     w = synth.five_agent_workload(L=5, H=2, d=64, D_e=64, user_len=96, resp_len=40, prefix_total=64,
                                   slot_prefix=8, capacity=4)
     ref = build_five_agent_state(w, seed=3, device=0, gamma=1.0, offset_format=fmt)
-    ref.request.plan.run([ref.queries[n] for n in ref.request.names], sync=True)
-    _, reused = ref.request.plan.results()
+    ref_req = ReuseRequest(ref.pools, ref.agents, gamma=1.0, top_k=top_k)
+    ref_req.plan.run([ref.queries[n] for n in ref_req.names], sync=True)
+    ref_ms, reused = ref_req.plan.results()
     assert all(reused), reused
 
     lr = shard.layer_shard(w.L, rank, world)
@@ -38,12 +41,21 @@ def main():
     peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, 0)
     agents = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
               for i, a in enumerate(st.agents)]
-    req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=0)
-    for _ in range(2):  # twice: the second run overwrites the same rows
-        req.plan.run([st.queries[n] for n in req.names], sync=True)
+    req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=top_k)
+    if shard_match:  # each rank computes half the match positions, stored into both ranks' buffers
+        req.shard_matching(rank, world, 0)
+    for _ in range(3):  # the later runs overwrite the same rows (and alternate the match buffers)
+        if shard_match:
+            req._mshard.run([st.queries[n] for n in req.names], sync=True)
+        else:
+            req.plan.run([st.queries[n] for n in req.names], sync=True)
         peer.sync()
-    _, reused = req.plan.results()
+    ms, reused = req.plan.results()
     assert all(reused), reused
+    for a, b in zip(ms, ref_ms):   # weights and verdicts bit-identical to the unsharded run
+        assert a.candidates == b.candidates and a.verdict == b.verdict
+        assert a.entropy == b.entropy and a.threshold == b.threshold, (a.entropy, b.entropy)
+        assert torch.equal(a.W, b.W) and torch.equal(a.wbar, b.wbar), f"rank {rank}: weights differ"
     checked = 0
     for i, a in enumerate(ref.agents):
         fk, fv = peer.full(i)
@@ -53,6 +65,8 @@ def main():
         assert torch.equal(fv, a.dst_v), f"rank {rank} agent {a.agent} V differs"
         checked += 1
     dist.barrier()
+    if shard_match:
+        req._mshard.close()
     peer.close()
     print(f"rank {rank}: {checked} agents bit-exact", flush=True)
     dist.destroy_process_group()

@@ -20,11 +20,15 @@ def _free_port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fmt", ["bf16", "fp8"])
-def test_fused_gather_two_ranks_bit_exact(fmt):
+@pytest.mark.parametrize("fmt,match,top_k", [("bf16", "replicated", 0), ("fp8", "replicated", 0),
+                                             ("bf16", "shard-match", 0), ("fp8", "shard-match", 0),
+                                             ("bf16", "shard-match", 2)])
+def test_fused_gather_two_ranks_bit_exact(fmt, match, top_k):
+    """Also: sharded matching (kvcomm_plan_match_shard) gives weights, verdicts and
+    caches bit-identical to the unsharded run (dense and top-k weights)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
-           fmt]
+           fmt, match, str(top_k)]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "rank 0: 3 agents bit-exact" in r.stdout and "rank 1: 2 agents bit-exact" in r.stdout, r.stdout

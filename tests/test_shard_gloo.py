@@ -99,3 +99,86 @@ def test_gather_to_consumers_world2_gloo_equals_unsharded():
     res = dict(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
     assert res == {0: True, 1: True}
+
+
+class _FakePlan:
+    """Stands in for kvcomm.Plan in the host-logic test of shard.MatchShard."""
+
+    def __init__(self, rank, size, fail_shard=False):
+        self.rank, self.size, self.fail_shard = rank, size, fail_shard
+        self.calls = []
+
+    def match_handle(self):
+        return bytes([self.rank]) * 64, self.size
+
+    def match_shard(self, rank, world, handles=()):
+        if self.fail_shard and world > 1:
+            raise RuntimeError("cannot open peer buffers")
+        self.calls.append(("shard", rank, world, [h[0] for h in handles]))
+
+    def run_begin(self, queries, stream=None):
+        self.calls.append(("begin",))
+
+    def run_end(self, sync=False, stream=None):
+        self.calls.append(("end",))
+
+
+def _match_shard_worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        size = 100 + (rank if case == "size" else 0)
+        plan = _FakePlan(rank, size, fail_shard=(case == "fail" and rank == 1))
+        try:
+            ms = shard.MatchShard(plan, rank, world, device=0)
+        except RuntimeError as e:
+            q.put((rank, "raised", str(e), plan.calls))
+            return
+        orig = shard.stream_barrier
+        shard.stream_barrier = lambda flag, group=None: (plan.calls.append(("barrier",)), dist.barrier(group=group))
+        try:
+            ms.run([None])
+        finally:
+            shard.stream_barrier = orig
+        ms.close()
+        q.put((rank, "ok", "", plan.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["ok", "fail", "size"])
+def test_match_shard_handshake_gloo(case):
+    """shard.MatchShard: every rank receives the handles in rank order and its own rank /
+    world; a failure on one rank (or plans of different layouts) raises on ALL ranks and
+    leaves no rank sharded; a run is begin -> cross-rank barrier -> end."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_match_shard_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, status, msg, calls = q.get(timeout=120)
+        out[r] = (status, msg, calls)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if case == "ok":
+        for r in range(world):
+            status, _, calls = out[r]
+            assert status == "ok"
+            assert calls[0] == ("shard", r, world, [0, 1])
+            assert calls[1:4] == [("begin",), ("barrier",), ("end",)]
+            assert calls[4] == ("shard", 0, 1, [])
+    else:
+        for r in range(world):
+            status, msg, calls = out[r]
+            assert status == "raised", out
+            assert "sharded matching unavailable" in msg
+            sharded = [c for c in calls if c[0] == "shard" and c[2] > 1]
+            unsharded_after = [c for c in calls if c[0] == "shard" and c[2] == 1]
+            assert not sharded or unsharded_after, calls   # nobody left sharded
+        if case == "size":
+            assert "differ across ranks" in out[0][1]
