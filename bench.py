@@ -540,7 +540,9 @@ def main():
     peak = P.get("hbm_gbs")
     achieved = alg_bytes / (realign_avg / 1e3) / 1e9
     traffic = None
-    try:
+    try:   # the committed full capture is of the N=1 launch; a layer shard moves 1/N of it
+        if world > 1:
+            raise LookupError("no per-shard capture")
         name = "realign_ncu.json" if args.offsets == "bf16" else f"realign_ncu_{args.offsets}.json"
         prof = json.load(open(os.path.join(ROOT, "profiles", name)))
         traffic = prof.get("dram_bytes_per_launch")

@@ -2,12 +2,15 @@
 
 Every (layer, KV-head, token) unit of a4/a5 is independent and the matching
 weights depend only on (sample, pool), so each rank holds a contiguous block of
-layers of every pool and base cache, computes the weights redundantly from the
-replicated embeddings, and realigns its block with no communication.  The only
-exchange is the targeted gather of each consuming agent's realigned cache onto the
-GPU that prefills/decodes that agent: agent m lives on rank (m-1) mod G and
-receives the G layer blocks of its prompt cache (NCCL grouped send/recv through
-torch.distributed; no all-gather, which would move G times the bytes).
+layers of every pool and base cache plus the replicated embeddings, and realigns
+its block with no communication.  Two exchanges remain:
+  * matching (MatchShard, default): each rank computes 1/G of the match positions and
+    stores those W columns and d̄ partials into every rank's buffers (one barrier per
+    request) — or every rank recomputes every distance (replicated);
+  * delivery of each consuming agent's realigned cache to the GPU that prefills/decodes
+    that agent (agent m lives on rank (m-1) mod G): fused into the realign epilogue
+    (PeerCaches, NVLink stores) or a targeted NCCL grouped send/recv
+    (gather_to_consumers; no all-gather, which would move G times the bytes).
 """
 from __future__ import annotations
 
