@@ -20,18 +20,21 @@ def _free_port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fmt,match,top_k", [("bf16", "replicated", 0), ("fp8", "replicated", 0),
-                                             ("bf16", "shard-match", 0), ("fp8", "shard-match", 0),
-                                             ("bf16", "shard-match", 2)])
-def test_fused_gather_two_ranks_bit_exact(fmt, match, top_k):
+@pytest.mark.parametrize("fmt,match,top_k,world", [("bf16", "replicated", 0, 2), ("fp8", "replicated", 0, 2),
+                                                   ("bf16", "shard-match", 0, 2), ("fp8", "shard-match", 0, 2),
+                                                   ("bf16", "shard-match", 2, 2), ("bf16", "shard-match", 0, 3)])
+def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world):
     """Also: sharded matching (kvcomm_plan_match_shard) gives weights, verdicts and
-    caches bit-identical to the unsharded run (dense and top-k weights)."""
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    caches bit-identical to the unsharded run (dense and top-k weights; 3 ranks split
+    the 48 and 20 position blocks of the two sample lengths unevenly)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
            fmt, match, str(top_k)]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert "rank 0: 3 agents bit-exact" in r.stdout and "rank 1: 2 agents bit-exact" in r.stdout, r.stdout
+    hosted = [sum(1 for m in range(1, 6) if (m - 1) % world == rank) for rank in range(world)]
+    for rank in range(world):
+        assert f"rank {rank}: {hosted[rank]} agents bit-exact" in r.stdout, r.stdout
 
 
 @pytest.mark.gpu
