@@ -61,7 +61,8 @@ typedef enum {
   KVCOMM_ERR_NOT_FOUND = 7,        /* empty slot / unknown consumer                                  */
   KVCOMM_ERR_OUT_OF_MEMORY = 8,
   KVCOMM_ERR_CUDA = 9,
-  KVCOMM_ERR_NCCL = 10
+  KVCOMM_ERR_NCCL = 10,
+  KVCOMM_ERR_IO = 11               /* checkpoint file missing, unreadable, truncated or corrupt       */
 } kvcomm_status;
 
 typedef enum { KVCOMM_SHAREABLE = 0, KVCOMM_NEW_ANCHOR = 1 } kvcomm_verdict;
@@ -267,6 +268,27 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_read_offsets(kvcomm_pool_t pool, int
                                                          int32_t which, int32_t rows, void* k_out,
                                                          void* v_out, float* sk_out, float* sv_out,
                                                          void* stream);
+
+/* ---- pool checkpoint (SURVEY §5 "optional pool dump/load"; SPEC S:293 dumps pools
+ * for its CPU program) ---------------------------------------------------------------
+ * save: synchronises `stream` (so inserts issued on it are included), then writes the
+ * pool's configuration, LFU metadata (lengths, access counts, insertion indices and
+ * counter, offset-presence masks) and every occupied slot's embeddings and present
+ * offsets, exactly as stored (bf16 rows, or fp8 codes + row scales), to `path`.  The
+ * caller orders any other stream's writes to the pool before the call.  Holds the
+ * pool's reader lock.  IO: the file cannot be created or written. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_save(kvcomm_pool_t pool, const char* path, void* stream);
+/* load: creates a pool on `device` with the saved configuration (layer/head shard,
+ * capacity, formats, placement) and restores every slot bit for bit at its saved slot
+ * index with its metadata, so later matches, realignments and LFU evictions behave
+ * exactly as in the saved pool.  IO: missing, truncated, corrupt or wrong-version file;
+ * OUT_OF_MEMORY / CUDA as for create.  Synchronous. */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_load(const char* path, int32_t device, kvcomm_pool_t* out);
+/* The pool's configuration; prefix_len (host int32 [num_consumers]) and inv_freq (host
+ * double [head_dim/2]) are filled when non-NULL (config->prefix_len / inv_freq are set
+ * to NULL). */
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_get_config(kvcomm_pool_t pool, kvcomm_pool_config* config,
+                                                       int32_t* prefix_len, double* inv_freq);
 
 /* ---- a1-a3: anchor matching (Eq. 5, Eq. 6 weights) -------------------------- */
 /* query_emb: device bf16 [L_phi][D_e] (the sample's token embeddings h_φ).

@@ -20,7 +20,7 @@ ALL_CONSUMERS = -1
 
 OK = 0
 STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE_MISMATCH", "NO_CANDIDATES", "MISSING_OFFSET",
-                "POSITION_GAP", "POSITION_OVERLAP", "NOT_FOUND", "OUT_OF_MEMORY", "CUDA", "NCCL"]
+                "POSITION_GAP", "POSITION_OVERLAP", "NOT_FOUND", "OUT_OF_MEMORY", "CUDA", "NCCL", "IO"]
 SHAREABLE, NEW_ANCHOR = 0, 1
 REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY"]
 PLACEHOLDER, PREFIX, COPY = 0, 1, 2
@@ -143,6 +143,10 @@ _SIGS = {
     "kvcomm_plan_match_shard": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(IpcHandle)]),
     "kvcomm_plan_run_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_void_p]),
     "kvcomm_plan_run_end": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "kvcomm_anchor_pool_save": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p]),
+    "kvcomm_anchor_pool_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "kvcomm_anchor_pool_get_config": (C.c_int, [C.c_void_p, C.POINTER(PoolConfig), C.POINTER(C.c_int32),
+                                                C.POINTER(C.c_double)]),
     "kvcomm_ipc_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
     "kvcomm_ipc_free": (C.c_int, [C.c_void_p]),
     "kvcomm_ipc_open": (C.c_int, [C.c_int32, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),

@@ -183,6 +183,7 @@ KVCOMM_API const char* kvcomm_status_string(kvcomm_status s) {
     case KVCOMM_ERR_OUT_OF_MEMORY: return "OUT_OF_MEMORY";
     case KVCOMM_ERR_CUDA: return "CUDA";
     case KVCOMM_ERR_NCCL: return "NCCL";
+    case KVCOMM_ERR_IO: return "IO";
   }
   return "UNKNOWN";
 }
@@ -553,6 +554,188 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t p, int32_t s
   info->insertion_index = m.inserted;
   info->ph_present_mask = m.ph_mask;
   info->pf_present_mask = m.pf_mask;
+  return ok();
+}
+
+// ---- pool checkpoint (SURVEY §5 "pool dump/load"): host file IO ------------------
+// File layout (native endianness): "KVCPOOL1", u32 version, the config's integer fields,
+// prefix_len[C], inv_freq[d/2], next insertion index, per-slot metadata, then for every
+// occupied slot: its L_ψ embedding rows (bf16 [L_ψ][D_e]) and, per consumer whose bit
+// is set, the placeholder region (bf16: rows [0, L_ψ) of every (plane, layer, head)
+// block; fp8: the blocks holding those rows, codes + scales as stored) and the prefix
+// region (whole).  Rows are written in a dense canonical layout, so a checkpoint loads
+// into a pool whose row padding (KVCOMM_PH_PAD_ROWS / KVCOMM_SLOT_PAD_ROWS) differs.
+namespace {
+constexpr char kCkptMagic[8] = {'K', 'V', 'C', 'P', 'O', 'O', 'L', '1'};
+constexpr uint32_t kCkptVersion = 1;
+
+struct File {
+  FILE* f = nullptr;
+  ~File() {
+    if (f) fclose(f);
+  }
+};
+
+kvcomm_status fwrite_all(FILE* f, const void* p, size_t n, const char* what) {
+  if (n && fwrite(p, 1, n, f) != n) return fail(KVCOMM_ERR_IO, "writing %s", what);
+  return KVCOMM_OK;
+}
+kvcomm_status fread_all(FILE* f, void* p, size_t n, const char* what) {
+  if (n && fread(p, 1, n, f) != n) return fail(KVCOMM_ERR_IO, "reading %s: truncated or not a pool checkpoint", what);
+  return KVCOMM_OK;
+}
+
+// One region of a slot as `rows` strided blocks of `width` bytes (dense in the file).
+struct Region {
+  void* base;
+  size_t width, pitch, rows;
+};
+
+// Regions of (slot, consumer, prefix?) holding rows [0, len).
+Region offset_region(const kvcomm_pool_s* p, int c, int slot, bool prefix, int len) {
+  const OffDst o = offsets_of(p, c, slot, prefix);
+  const size_t blocks = size_t(2) * p->Ls * p->Hs;  // K plane then V plane: uniformly spaced
+  if (!p->fp8) {
+    return {o.k, size_t(len) * p->d * sizeof(bf16), size_t(o.ld) * p->d * sizeof(bf16), blocks};
+  }
+  const int rpb = fp8_rows_per_block(p->d);
+  return {o.k8, size_t((len + rpb - 1) / rpb) * fp8_block_bytes(p->d), size_t(o.lh_bytes), blocks};
+}
+
+kvcomm_status region_io(const Region& r, std::vector<uint8_t>& buf, bool save, FILE* f) {
+  const size_t n = r.width * r.rows;
+  if (n == 0) return KVCOMM_OK;
+  buf.resize(n);
+  if (save) {
+    KV_CUDA(cudaMemcpy2D(buf.data(), r.width, r.base, r.pitch, r.width, r.rows, cudaMemcpyDefault));
+    return fwrite_all(f, buf.data(), n, "offset region");
+  }
+  KV_TRY(fread_all(f, buf.data(), n, "offset region"));
+  KV_CUDA(cudaMemcpy2D(r.base, r.pitch, buf.data(), r.width, r.width, r.rows, cudaMemcpyDefault));
+  return KVCOMM_OK;
+}
+
+int32_t* cfg_ints(kvcomm_pool_config& c, int i) {
+  int32_t* f[] = {&c.num_layers, &c.layer_begin, &c.layer_end, &c.num_kv_heads, &c.head_begin, &c.head_end,
+                  &c.head_dim, &c.emb_dim, &c.capacity, &c.max_anchor_len, &c.num_consumers, &c.scalar_distance,
+                  &c.similarity, &c.offset_format, &c.placement, &c.rope_layout};
+  return i < int(sizeof(f) / sizeof(f[0])) ? f[i] : nullptr;
+}
+constexpr int kCfgInts = 16;
+
+// the slot data of one pool, saved or loaded in file order
+kvcomm_status slots_io(kvcomm_pool_s* p, bool save, FILE* f) {
+  std::vector<uint8_t> buf;
+  for (int s = 0; s < p->cap; ++s) {
+    const SlotMeta& m = p->slots[s];
+    if (!m.occupied) continue;
+    const size_t ew = size_t(m.length) * p->De * sizeof(bf16);
+    const Region er{p->emb + int64_t(s) * p->maxlen * p->De, ew, ew, 1};
+    KV_TRY(region_io(er, buf, save, f));
+    for (int c = 0; c < p->C; ++c) {
+      if (m.ph_mask >> c & 1) KV_TRY(region_io(offset_region(p, c, s, false, m.length), buf, save, f));
+      if (m.pf_mask >> c & 1) KV_TRY(region_io(offset_region(p, c, s, true, p->prefix_len[c]), buf, save, f));
+    }
+  }
+  return KVCOMM_OK;
+}
+}  // namespace
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_save(kvcomm_pool_t p, const char* path, void* stream) {
+  NvtxRange nvtx_("kvcomm_anchor_pool_save");
+  if (!p || !path) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool/path");
+  std::shared_lock<std::shared_mutex> lk(p->mu);
+  DeviceGuard guard(p->cfg.device);
+  KV_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));  // prior inserts on `stream` land first
+  File F;
+  F.f = fopen(path, "wb");
+  if (!F.f) return fail(KVCOMM_ERR_IO, "cannot create %s", path);
+  kvcomm_pool_config c = p->cfg;
+  KV_TRY(fwrite_all(F.f, kCkptMagic, sizeof(kCkptMagic), "magic"));
+  KV_TRY(fwrite_all(F.f, &kCkptVersion, sizeof(kCkptVersion), "version"));
+  for (int i = 0; i < kCfgInts; ++i) KV_TRY(fwrite_all(F.f, cfg_ints(c, i), sizeof(int32_t), "config"));
+  KV_TRY(fwrite_all(F.f, p->prefix_len.data(), sizeof(int32_t) * p->C, "prefix_len"));
+  KV_TRY(fwrite_all(F.f, p->inv_freq.data(), sizeof(double) * (p->d / 2), "inv_freq"));
+  KV_TRY(fwrite_all(F.f, &p->next_index, sizeof(int64_t), "insertion counter"));
+  for (const SlotMeta& m : p->slots) {
+    const int32_t occ = m.occupied ? 1 : 0;
+    KV_TRY(fwrite_all(F.f, &occ, sizeof(occ), "slot"));
+    KV_TRY(fwrite_all(F.f, &m.length, sizeof(m.length), "slot"));
+    KV_TRY(fwrite_all(F.f, &m.access, sizeof(m.access), "slot"));
+    KV_TRY(fwrite_all(F.f, &m.inserted, sizeof(m.inserted), "slot"));
+    KV_TRY(fwrite_all(F.f, &m.ph_mask, sizeof(m.ph_mask), "slot"));
+    KV_TRY(fwrite_all(F.f, &m.pf_mask, sizeof(m.pf_mask), "slot"));
+  }
+  KV_TRY(slots_io(p, true, F.f));
+  if (fflush(F.f) != 0) return fail(KVCOMM_ERR_IO, "flushing %s", path);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_load(const char* path, int32_t device, kvcomm_pool_t* out) {
+  NvtxRange nvtx_("kvcomm_anchor_pool_load");
+  if (!path || !out) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null path/out");
+  *out = nullptr;
+  File F;
+  F.f = fopen(path, "rb");
+  if (!F.f) return fail(KVCOMM_ERR_IO, "cannot open %s", path);
+  char magic[8];
+  uint32_t ver = 0;
+  KV_TRY(fread_all(F.f, magic, sizeof(magic), "magic"));
+  if (std::memcmp(magic, kCkptMagic, sizeof(magic)) != 0) return fail(KVCOMM_ERR_IO, "%s: not a pool checkpoint", path);
+  KV_TRY(fread_all(F.f, &ver, sizeof(ver), "version"));
+  if (ver != kCkptVersion) return fail(KVCOMM_ERR_IO, "%s: checkpoint version %u (expected %u)", path, ver, kCkptVersion);
+  kvcomm_pool_config c{};
+  for (int i = 0; i < kCfgInts; ++i) KV_TRY(fread_all(F.f, cfg_ints(c, i), sizeof(int32_t), "config"));
+  if (c.num_consumers < 1 || c.num_consumers > KVCOMM_MAX_CONSUMERS || c.head_dim < 2 || c.head_dim > 256 ||
+      c.capacity < 1 || c.capacity > KVCOMM_MAX_CAPACITY)
+    return fail(KVCOMM_ERR_IO, "%s: corrupt configuration", path);
+  std::vector<int32_t> plen(c.num_consumers);
+  std::vector<double> inv(c.head_dim / 2);
+  KV_TRY(fread_all(F.f, plen.data(), sizeof(int32_t) * plen.size(), "prefix_len"));
+  KV_TRY(fread_all(F.f, inv.data(), sizeof(double) * inv.size(), "inv_freq"));
+  c.device = device;
+  c.prefix_len = plen.data();
+  c.inv_freq = inv.data();
+  kvcomm_pool_t p = nullptr;
+  KV_TRY(kvcomm_anchor_pool_create(&c, &p));
+  auto bail = [&](kvcomm_status st) {
+    const std::string msg = g_err;
+    pool_free(p);
+    g_err = msg;
+    return st;
+  };
+  kvcomm_status st;
+  if ((st = fread_all(F.f, &p->next_index, sizeof(int64_t), "insertion counter")) != KVCOMM_OK) return bail(st);
+  for (SlotMeta& m : p->slots) {
+    int32_t occ = 0;
+    if ((st = fread_all(F.f, &occ, sizeof(occ), "slot")) != KVCOMM_OK ||
+        (st = fread_all(F.f, &m.length, sizeof(m.length), "slot")) != KVCOMM_OK ||
+        (st = fread_all(F.f, &m.access, sizeof(m.access), "slot")) != KVCOMM_OK ||
+        (st = fread_all(F.f, &m.inserted, sizeof(m.inserted), "slot")) != KVCOMM_OK ||
+        (st = fread_all(F.f, &m.ph_mask, sizeof(m.ph_mask), "slot")) != KVCOMM_OK ||
+        (st = fread_all(F.f, &m.pf_mask, sizeof(m.pf_mask), "slot")) != KVCOMM_OK)
+      return bail(st);
+    m.occupied = occ != 0;
+    if (m.occupied && (m.length < 1 || m.length > p->maxlen)) return bail(fail(KVCOMM_ERR_IO, "%s: corrupt slot", path));
+  }
+  {
+    DeviceGuard guard(device);
+    if ((st = slots_io(p, false, F.f)) != KVCOMM_OK) return bail(st);
+  }
+  char extra;
+  if (fread(&extra, 1, 1, F.f) != 0) return bail(fail(KVCOMM_ERR_IO, "%s: trailing bytes", path));
+  *out = p;
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_anchor_pool_get_config(kvcomm_pool_t p, kvcomm_pool_config* config,
+                                                       int32_t* prefix_len, double* inv_freq) {
+  if (!p || !config) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null pool/config");
+  *config = p->cfg;
+  config->prefix_len = nullptr;
+  config->inv_freq = nullptr;
+  if (prefix_len) std::memcpy(prefix_len, p->prefix_len.data(), sizeof(int32_t) * p->C);
+  if (inv_freq) std::memcpy(inv_freq, p->inv_freq.data(), sizeof(double) * (p->d / 2));
   return ok();
 }
 

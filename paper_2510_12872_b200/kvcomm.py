@@ -12,6 +12,7 @@ fine: the (layer, head) row stride is read from the tensor's strides).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
@@ -158,6 +159,34 @@ class AnchorPool:
         if self._h is None:
             raise RuntimeError("pool destroyed")
         return self._h.value
+
+    # -- checkpoint ------------------------------------------------------------
+    def save(self, path: str, stream=None) -> None:
+        """Write the pool (configuration, LFU metadata, every stored anchor) to `path`
+        (kvcomm_anchor_pool_save)."""
+        L.check(L.lib().kvcomm_anchor_pool_save(self.handle, os.fsencode(path), _stream_handle(stream)))
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "AnchorPool":
+        """Recreate a saved pool on `device`, slot for slot (kvcomm_anchor_pool_load)."""
+        h = C.c_void_p()
+        L.check(L.lib().kvcomm_anchor_pool_load(os.fsencode(path), device, C.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        cfg = L.PoolConfig()
+        L.check(L.lib().kvcomm_anchor_pool_get_config(h, C.byref(cfg), None, None))
+        pl = (C.c_int32 * cfg.num_consumers)()
+        inv = (C.c_double * (cfg.head_dim // 2))()
+        L.check(L.lib().kvcomm_anchor_pool_get_config(h, C.byref(cfg), pl, inv))
+        self.Ls, self.Hs = cfg.layer_end - cfg.layer_begin, cfg.head_end - cfg.head_begin
+        self.d, self.De = cfg.head_dim, cfg.emb_dim
+        self.capacity, self.max_anchor_len = cfg.capacity, cfg.max_anchor_len
+        self.prefix_len = list(pl)
+        self.device = torch.device("cuda", device)
+        self.offset_format = {L.OFFSET_BF16: "bf16", L.OFFSET_FP8_E4M3: "fp8"}[cfg.offset_format]
+        self.rope_layout = {L.ROPE_HALF: "half", L.ROPE_INTERLEAVED: "interleaved"}[cfg.rope_layout]
+        self.inv_freq = list(inv)
+        return self
 
     def destroy(self) -> None:
         if self._h is not None:

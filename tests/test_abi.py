@@ -117,3 +117,25 @@ def test_ipc_calls_validate_arguments_before_any_device_work():
     assert lib.kvcomm_ipc_alloc(0, 64, None, C.byref(h)) == 1                   # null out pointer
     assert lib.kvcomm_ipc_open(0, None, C.byref(ptr)) == 1
     assert lib.kvcomm_ipc_free(None) == 0 and lib.kvcomm_ipc_close(None) == 0   # no-ops
+
+
+def test_pool_checkpoint_errors_before_any_device_work(tmp_path):
+    """kvcomm_anchor_pool_load: a missing file, a foreign file and a wrong version are
+    IO errors raised before any CUDA call; save/load validate their arguments."""
+    lib = L.load()
+    out = C.c_void_p()
+    missing = str(tmp_path / "none.kvc").encode()
+    assert lib.kvcomm_anchor_pool_load(missing, 0, C.byref(out)) == L.STATUS_NAMES.index("IO")
+    assert b"cannot open" in lib.kvcomm_last_error_message()
+    junk = tmp_path / "junk.kvc"
+    junk.write_bytes(b"not a checkpoint at all")
+    assert lib.kvcomm_anchor_pool_load(str(junk).encode(), 0, C.byref(out)) == L.STATUS_NAMES.index("IO")
+    assert b"not a pool checkpoint" in lib.kvcomm_last_error_message()
+    old = tmp_path / "old.kvc"
+    old.write_bytes(b"KVCPOOL1" + (7).to_bytes(4, "little"))
+    assert lib.kvcomm_anchor_pool_load(str(old).encode(), 0, C.byref(out)) == L.STATUS_NAMES.index("IO")
+    assert b"version" in lib.kvcomm_last_error_message()
+    assert out.value is None
+    assert lib.kvcomm_anchor_pool_load(None, 0, C.byref(out)) == L.STATUS_NAMES.index("INVALID_ARGUMENT")
+    assert lib.kvcomm_anchor_pool_save(None, b"x", None) == L.STATUS_NAMES.index("INVALID_ARGUMENT")
+    assert lib.kvcomm_status_string(L.STATUS_NAMES.index("IO")) == b"IO"

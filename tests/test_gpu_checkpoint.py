@@ -1,0 +1,125 @@
+"""Pool checkpoint (kvcomm_anchor_pool_save / kvcomm_anchor_pool_load; SURVEY §5 "pool
+dump/load"): a reloaded pool holds the same slots, metadata and stored offsets bit for
+bit, matches and realigns exactly like the saved one, and evicts the same anchor next
+(LFU state restored) — bf16 and fp8 pools, device and host placement, and into a pool
+whose row padding differs."""
+import os
+
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+L, H, D, DE, CAP, MAXLEN, P = 3, 2, 64, 64, 5, 80, [6, 9]
+
+
+def _pool(fmt, placement):
+    from paper_2510_12872_b200 import kvcomm as K
+    return K.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=CAP, max_anchor_len=MAXLEN,
+                        prefix_len=P, inv_freq=synth.llama3_inv_freq(D), layer_range=(1, 3), offset_format=fmt,
+                        placement=placement)
+
+
+def _fill(pool, g):
+    from paper_2510_12872_b200 import kvcomm as K
+    rnd = lambda *s: (torch.randn(*s, generator=g, device="cuda") * 0.15).to(torch.bfloat16)
+    Ls = pool.Ls
+    lens = [80, 64, 77, 80]
+    for i, n in enumerate(lens):
+        emb = (torch.randn(n, DE, generator=g, device="cuda") / 8).to(torch.bfloat16)
+        offs = [K.OffsetGiven(0, rnd(Ls, H, n, D), rnd(Ls, H, n, D), rnd(Ls, H, P[0], D), rnd(Ls, H, P[0], D))]
+        if i != 2:   # slot 2 lacks consumer 1's offsets (presence mask bit clear)
+            offs.append(K.OffsetGiven(1, rnd(Ls, H, n, D), rnd(Ls, H, n, D), rnd(Ls, H, P[1], D), rnd(Ls, H, P[1], D)))
+        pool.insert(emb, offs)
+    pool.record_access([0, 0, 3, 1])
+    pool.evict(1)                     # a hole at slot 1
+    return rnd
+
+
+def _state(pool):
+    out = []
+    for s in range(CAP):
+        info = pool.slot_info(s)
+        rows = []
+        if info["occupied"]:
+            for c in range(2):
+                if info["ph_present_mask"] >> c & 1:
+                    rows.append(pool.read_offsets(s, c, "ph", info["length"]))
+                if info["pf_present_mask"] >> c & 1:
+                    rows.append(pool.read_offsets(s, c, "pf", P[c]))
+        out.append((info, rows))
+    return out
+
+
+def _same(a, b):
+    for (ia, ra), (ib, rb) in zip(a, b):
+        assert ia == ib
+        assert len(ra) == len(rb)
+        for x, y in zip(ra, rb):
+            for u, v in zip(x, y):
+                assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("fmt,placement,pad", [("bf16", "device", 0), ("fp8", "device", 0), ("bf16", "host", 0),
+                                               ("bf16", "device", 8), ("fp8", "device", 8)])
+def test_pool_checkpoint_round_trip(tmp_path, monkeypatch, fmt, placement, pad):
+    from paper_2510_12872_b200 import kvcomm as K
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = _pool(fmt, placement)
+    rnd = _fill(a, g)
+    path = str(tmp_path / "pool.kvc")
+    a.save(path)
+    if pad:   # the loading process pads its rows differently: the file's dense layout still fits
+        monkeypatch.setenv("KVCOMM_PH_PAD_ROWS", str(pad))
+    b = K.AnchorPool.load(path, device=0)
+    monkeypatch.delenv("KVCOMM_PH_PAD_ROWS", raising=False)
+    assert (b.Ls, b.Hs, b.d, b.De, b.capacity, b.max_anchor_len, b.prefix_len, b.offset_format) == \
+        (a.Ls, a.Hs, a.d, a.De, a.capacity, a.max_anchor_len, a.prefix_len, a.offset_format)
+    _same(_state(a), _state(b))
+
+    # matching and realignment through the reloaded pool are bit-identical
+    q = (torch.randn(60, DE, generator=g, device="cuda") / 8).to(torch.bfloat16)
+    ma, mb = a.match(q, consumer=0, gamma=1.0), b.match(q, consumer=0, gamma=1.0)
+    assert ma.candidates == mb.candidates and ma.verdict == mb.verdict and ma.entropy == mb.entropy
+    assert torch.equal(ma.W, mb.W) and torch.equal(ma.wbar, mb.wbar)
+    base = [torch.randn(a.Ls, H, 60, D, generator=g, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    outs = []
+    for pool, m in ((a, ma), (b, mb)):
+        dk = torch.zeros(a.Ls, H, 90, D, dtype=torch.bfloat16, device="cuda")
+        dv = torch.zeros_like(dk)
+        K.realign_segment(K.Segment(pool, 0, K.PLACEHOLDER, m.W, m.candidates, base[0], base[1], 0, 20, dk, dv))
+        outs.append((dk, dv))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+    # LFU state: the next inserts fill the hole, then evict the same victim in both pools
+    for _ in range(2):
+        emb = (torch.randn(50, DE, generator=g, device="cuda") / 8).to(torch.bfloat16)
+        offs = [K.OffsetGiven(0, rnd(a.Ls, H, 50, D), rnd(a.Ls, H, 50, D), rnd(a.Ls, H, P[0], D),
+                              rnd(a.Ls, H, P[0], D))]
+        assert a.insert(emb, offs) == b.insert(emb, offs)
+    _same(_state(a), _state(b))
+    a.destroy()
+    b.destroy()
+
+
+def test_pool_load_rejects_truncated_file(tmp_path):
+    from paper_2510_12872_b200 import kvcomm as K
+    from paper_2510_12872_b200._lib import KVCommError
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = _pool("bf16", "device")
+    _fill(a, g)
+    path = str(tmp_path / "pool.kvc")
+    a.save(path)
+    data = open(path, "rb").read()
+    open(path, "wb").write(data[: len(data) // 2])
+    with pytest.raises(KVCommError) as e:
+        K.AnchorPool.load(path)
+    assert e.value.status_name == "IO"
+    open(path, "wb").write(data + b"x")
+    with pytest.raises(KVCommError) as e:
+        K.AnchorPool.load(path)
+    assert e.value.status_name == "IO"
+    a.destroy()
