@@ -152,8 +152,8 @@ def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: 
                 bk, bv = inp.prefix_base(s.pool, s.consumer, 0), inp.prefix_base(s.pool, s.consumer, 1)
                 kind = K.PREFIX
             segs.append(SegmentLayout(kind, s.pool, s.consumer, bk, bv, s.base_start, s.target_start))
-        dst_k = torch.empty(inp.Ls, w.H, a.N, w.d, dtype=torch.bfloat16, device=dev)
-        dst_v = torch.empty_like(dst_k)
+        dst_k = torch.zeros(inp.Ls, w.H, a.N, w.d, dtype=torch.bfloat16, device=dev)
+        dst_v = torch.zeros_like(dst_k)
         agents.append(AgentLayout(a.agent, a.N, inp.p0(a.agent, 0), inp.p0(a.agent, 1), segs, dst_k, dst_v))
     req = ReuseRequest(pools, agents, gamma=gamma, top_k=top_k)
     torch.cuda.synchronize()

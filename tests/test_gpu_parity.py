@@ -330,6 +330,52 @@ def test_fp8_offsets_codes_and_realign(d, L_phi, P):
     harness.compare(gpu, ora, p)
 
 
+def _e4m3_hard_rows(d):
+    """Rows on which x * fl(1/scale) and the IEEE quotient x / scale round to DIFFERENT
+    e4m3 codes: for row maxima whose fp32 reciprocal scale is inexact enough, every
+    positive bf16 x <= amax is tried and the ones that flip are kept (with their
+    negatives), found with the oracle's own rounding.  Returns (rows, flips)."""
+    allb = torch.arange(1, 0x7f80, dtype=torch.int32).to(torch.int16).view(torch.bfloat16).float().numpy()
+    rows, flips = [], 0
+    for amax in (2.15625, 1.296875, 2.84375, 1.2734375, 0.98046875, 3.328125, 0.021240234375):
+        sc = np.float32(amax) / np.float32(448)
+        xs = allb[allb <= amax].astype(np.float32)
+        exact = O.e4m3_round((xs / sc).astype(np.float32).astype(np.float64))
+        recip = O.e4m3_round((xs * (np.float32(1) / sc)).astype(np.float32).astype(np.float64))
+        hard = xs[exact != recip]
+        flips += len(hard)
+        vals = [v for h in hard for v in (float(h), -float(h))]
+        for i in range(0, max(len(vals), 1), d - 1):
+            chunk = vals[i:i + d - 1]
+            rows.append([amax] + chunk + [0.0] * (d - 1 - len(chunk)))
+    return torch.tensor(rows, dtype=torch.float32).to(torch.bfloat16), flips
+
+
+def test_fp8_quantiser_exact_on_rounding_ties():
+    """The quantiser's reciprocal fast path (memops.cu quot_for_e4m3) must give the codes
+    of an IEEE division exactly, also on the elements where a plain reciprocal multiply
+    rounds to a different e4m3 code."""
+    d = 128
+    rows, flips = _e4m3_hard_rows(d)
+    assert flips >= 20          # a plain reciprocal multiply would get these codes wrong
+    n = rows.shape[0]
+    x = rows.view(1, 1, n, d).expand(2, 2, n, d).contiguous()
+    dev = torch.device("cuda", 0)
+    pool = K.AnchorPool(num_layers=2, num_kv_heads=2, head_dim=d, emb_dim=64, capacity=1, max_anchor_len=n,
+                        prefix_len=[n], inv_freq=synth.llama3_inv_freq(d), offset_format="fp8")
+    xd = x.to(dev)
+    slot, _ = pool.insert(torch.zeros(n, 64, dtype=torch.bfloat16, device=dev), [K.OffsetGiven(0, xd, -xd, xd, xd)])
+    q, sc = O.quantize_rows_fp8(harness.f64(x))
+    qn, _ = O.quantize_rows_fp8(harness.f64(-x))
+    for which in ("ph", "pf"):
+        gk, gv, sk, sv = pool.read_offsets(slot, 0, which, n)
+        assert torch.equal(gk.cpu(), _fp8_codes(q)), which
+        assert torch.equal(sk.cpu(), torch.from_numpy(sc)), which
+        if which == "ph":
+            assert torch.equal(gv.cpu(), _fp8_codes(qn))
+    pool.destroy()
+
+
 def test_fp8_measure_insert_close_to_oracle():
     dev = torch.device("cuda", 0)
     L_, H, d, T, P = 2, 2, 128, 70, 8
