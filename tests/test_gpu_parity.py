@@ -364,9 +364,11 @@ def test_fp8_quantiser_exact_on_rounding_ties():
     pool = K.AnchorPool(num_layers=2, num_kv_heads=2, head_dim=d, emb_dim=64, capacity=1, max_anchor_len=n,
                         prefix_len=[n], inv_freq=synth.llama3_inv_freq(d), offset_format="fp8")
     xd = x.to(dev)
-    slot, _ = pool.insert(torch.zeros(n, 64, dtype=torch.bfloat16, device=dev), [K.OffsetGiven(0, xd, -xd, xd, xd)])
+    xn = torch.where(x == 0, x, -x)     # negatives; the zero padding stays +0
+    slot, _ = pool.insert(torch.zeros(n, 64, dtype=torch.bfloat16, device=dev),
+                          [K.OffsetGiven(0, xd, xn.to(dev), xd, xd)])
     q, sc = O.quantize_rows_fp8(harness.f64(x))
-    qn, _ = O.quantize_rows_fp8(harness.f64(-x))
+    qn, _ = O.quantize_rows_fp8(harness.f64(xn))
     for which in ("ph", "pf"):
         gk, gv, sk, sv = pool.read_offsets(slot, 0, which, n)
         assert torch.equal(gk.cpu(), _fp8_codes(q)), which
