@@ -352,9 +352,8 @@ def _e4m3_hard_rows(d):
 
 
 def test_fp8_quantiser_exact_on_rounding_ties():
-    """The quantiser's reciprocal fast path (memops.cu quot_for_e4m3) must give the codes
-    of an IEEE division exactly, also on the elements where a plain reciprocal multiply
-    rounds to a different e4m3 code."""
+    """The device quantiser gives the codes of an IEEE division exactly, also on the
+    elements where a reciprocal multiply would round to a different e4m3 code."""
     d = 128
     rows, flips = _e4m3_hard_rows(d)
     assert flips >= 20          # a plain reciprocal multiply would get these codes wrong
