@@ -187,10 +187,10 @@ cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs,
 // fp8 (e4m3) offset storage ("substantial headroom for
 // compression"): each token row of d offsets is stored as d e4m3 codes plus one
 // fp32 scale = max|x| / 448 (1 if the row is all zero); code = RNE_sat(x / scale)
-// with IEEE division, so the codes are reproducible bit for bit.  (An exact reciprocal
-// multiply — the division kept only next to e4m3 rounding boundaries — measured slower.)
+// as with IEEE division (store_fp8_item: bracketed reciprocal products, division only
+// next to e4m3 rounding boundaries), so the codes are reproducible bit for bit.
 // The kernels are instantiated for head_dim 128 (lane-group size, block geometry and
-// row addressing fold into shifts: 4.2 -> 5.6 TB/s measured, 3.0 -> 4.1 TB/s given).
+// row addressing fold into shifts).
 // ---------------------------------------------------------------------------
 #include <cuda_fp8.h>
 
@@ -213,22 +213,64 @@ __device__ __forceinline__ float group_max(float v, int G) {
 }
 
 // 16 floats of one item (8 of the first half, 8 of the second) -> codes into row pointers
-__device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1, float scale, uint8_t* o0,
-                                               uint8_t* o1) {
-  uint32_t w[4];
+// e4m3 codes of x / scale without a division per element.  q = x * fl(1/scale) is
+// within a relative 2^-23 of the exact quotient t, so t lies between q(1 - 2^-21) and
+// q(1 + 2^-21) (both products rounded outward of that band).  Rounding to e4m3 (RNE,
+// satfinite) is monotonic, so when those two bounds convert to the same code, t has
+// that code too — exactly the code RNE_sat(x / scale) of an IEEE division.  When they
+// differ (t near an e4m3 rounding boundary: ~1e-5 of elements) or 1/scale is not
+// finite, the item is recomputed with IEEE divisions out of line.
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n .reg .b64 ra, rb, rc;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n"
+      " mul.rn.f32x2 rc, ra, rb;\n mov.b64 {%0, %1}, rc;\n}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t e4m3x2(float2 f) {
+  return uint32_t(__nv_cvt_float2_to_fp8x2(f, __NV_SATFINITE, __NV_E4M3));  // .x in the low byte
+}
+
+__device__ __forceinline__ void fp8_item_div(const float* x0, const float* x1, float scale, uint32_t* w) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float* x = h ? x1 : x0;
     uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      float2 f = make_float2(__fdiv_rn(x[2 * t], scale), __fdiv_rn(x[2 * t + 1], scale));
-      const uint32_t p = uint32_t(__nv_cvt_float2_to_fp8x2(f, __NV_SATFINITE, __NV_E4M3));  // .x in low byte
+      const uint32_t p = e4m3x2(make_float2(__fdiv_rn(x[2 * t], scale), __fdiv_rn(x[2 * t + 1], scale)));
       if (t < 2) lo |= p << (16 * t); else hi |= p << (16 * (t - 2));
     }
     w[2 * h] = lo;
     w[2 * h + 1] = hi;
   }
+}
+
+// 16 floats of one item (8 of the first half, 8 of the second) -> codes into row pointers
+__device__ __forceinline__ void store_fp8_item(const float* x0, const float* x1, float scale, uint8_t* o0,
+                                               uint8_t* o1) {
+  const float rcp = __frcp_rn(scale);
+  const float2 r = make_float2(rcp, rcp);
+  const float2 dn = make_float2(1.f - 0x1p-21f, 1.f - 0x1p-21f), up = make_float2(1.f + 0x1p-21f, 1.f + 0x1p-21f);
+  uint32_t w[4];
+  uint32_t diff = rcp < INFINITY ? 0u : 1u;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float* x = h ? x1 : x0;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 q = fmul2(make_float2(x[2 * t], x[2 * t + 1]), r);
+      const uint32_t a = e4m3x2(fmul2(q, dn)), b = e4m3x2(fmul2(q, up));
+      diff |= a ^ b;
+      if (t < 2) lo |= a << (16 * t); else hi |= a << (16 * (t - 2));
+    }
+    w[2 * h] = lo;
+    w[2 * h + 1] = hi;
+  }
+  if (__builtin_expect(diff != 0u, 0)) fp8_item_div(x0, x1, scale, w);
   *reinterpret_cast<uint2*>(o0) = make_uint2(w[0], w[1]);
   *reinterpret_cast<uint2*>(o1) = make_uint2(w[2], w[3]);
 }
@@ -258,40 +300,50 @@ __device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int 
 template <int kD>  // head_dim fixed at compile time (128), or 0 = runtime d
 __device__ __forceinline__ void quantize_rows(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
                                               int64_t lh_bytes, int n_lh, int rows, int d_arg) {
+  constexpr int U = 2;  // items per thread per iteration: both loads in flight before any math
   const int d = kD ? kD : d_arg;
   const int vph = d / 16;
   const int G = row_group(vph);
   const int half = d / 2;
   const int n = rows * G;
   for (int lh = blockIdx.y; lh < n_lh; lh += gridDim.y) {
-    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-      const int x = base + threadIdx.x;
-      const int i = x / G;
-      const int v = x - i * G;
-      const bool active = i < rows && v < vph;
-      float f0[8], f1[8];
-      if (active) {
-        const bf16* sp = src + (int64_t(lh) * src_ld + i) * d + v * 8;
-        const uint4 a = ldg128_nc(sp), b = ldg128_nc(sp + half);
-        const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    for (int base = blockIdx.x * blockDim.x * U; base < n; base += gridDim.x * blockDim.x * U) {
+      uint4 a[U], b[U];
+      bool active[U];
+      int ii[U], vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = base + u * blockDim.x + threadIdx.x;
+        ii[u] = x / G;
+        vv[u] = x - ii[u] * G;
+        active[u] = ii[u] < rows && vv[u] < vph;
+        if (active[u]) {
+          const bf16* sp = src + (int64_t(lh) * src_ld + ii[u]) * d + vv[u] * 8;
+          a[u] = ldg128_nc(sp);
+          b[u] = ldg128_nc(sp + half);
+        } else {
+          a[u] = b[u] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float f0[8], f1[8];
+        const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w}, bv[4] = {b[u].x, b[u].y, b[u].z, b[u].w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           f0[2 * t] = bf_lo(av[t]); f0[2 * t + 1] = bf_hi(av[t]);
           f1[2 * t] = bf_lo(bv[t]); f1[2 * t + 1] = bf_hi(bv[t]);
         }
-      } else {
+        float m = 0.f;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) f0[t] = f1[t] = 0.f;
+        for (int t = 0; t < 8; ++t) m = fmaxf(m, fmaxf(fabsf(f0[t]), fabsf(f1[t])));
+        m = group_max(m, G);
+        if (!active[u]) continue;
+        const float sc = row_scale(m);
+        const Fp8Row o = fp8_row(dst, lh, ii[u], d, lh_bytes);
+        store_fp8_item(f0, f1, sc, o.code + vv[u] * 16, o.code + vv[u] * 16 + 8);
+        if (vv[u] == 0) *o.scale = sc;
       }
-      float m = 0.f;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) m = fmaxf(m, fmaxf(fabsf(f0[t]), fabsf(f1[t])));
-      m = group_max(m, G);
-      if (!active) continue;
-      const float sc = row_scale(m);
-      const Fp8Row o = fp8_row(dst, lh, i, d, lh_bytes);
-      store_fp8_item(f0, f1, sc, o.code + v * 16, o.code + v * 16 + 8);
-      if (v == 0) *o.scale = sc;
     }
   }
 }
