@@ -21,6 +21,9 @@ def main():
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
     shard_match = len(sys.argv) > 2 and sys.argv[2] == "shard-match"
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
+    scal = sys.argv[5] if len(sys.argv) > 5 else "frobenius"
+    pk = dict(offset_format=fmt, similarity=sim, scalar_distance=scal)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
     import synth
@@ -30,14 +33,14 @@ def main():
 
     w = synth.five_agent_workload(L=5, H=2, d=64, D_e=64, user_len=96, resp_len=40, prefix_total=64,
                                   slot_prefix=8, capacity=4)
-    ref = build_five_agent_state(w, seed=3, device=0, gamma=1.0, offset_format=fmt)
+    ref = build_five_agent_state(w, seed=3, device=0, gamma=1.0, **pk)
     ref_req = ReuseRequest(ref.pools, ref.agents, gamma=1.0, top_k=top_k)
     ref_req.plan.run([ref.queries[n] for n in ref_req.names], sync=True)
     ref_ms, reused = ref_req.plan.results()
     assert all(reused), reused
 
     lr = shard.layer_shard(w.L, rank, world)
-    st = build_five_agent_state(w, seed=3, device=0, gamma=1.0, layer_range=lr, offset_format=fmt)
+    st = build_five_agent_state(w, seed=3, device=0, gamma=1.0, layer_range=lr, **pk)
     peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, 0)
     agents = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
               for i, a in enumerate(st.agents)]
