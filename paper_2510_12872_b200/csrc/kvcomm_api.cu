@@ -124,7 +124,8 @@ struct kvcomm_pool_s {
     return (ld + fp8_rows_per_block(d) - 1) / fp8_rows_per_block(d) * fp8_block_bytes(d);
   }
   int64_t f8_ph_plane() const { return int64_t(Ls) * Hs * f8_lh(ph_ld); }
-  int64_t f8_ph_slot() const { return 2 * f8_ph_plane(); }
+  int64_t f8_slot_pad = 0;  // fp8 pools: extra bytes between slots
+  int64_t f8_ph_slot() const { return 2 * f8_ph_plane() + f8_slot_pad; }
   int64_t f8_pf_plane(int c) const { return int64_t(Ls) * Hs * f8_lh(prefix_len[c]); }
   int64_t f8_pf_slot(int c) const { return 2 * f8_pf_plane(c); }
   int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * pf_ld(c) * d; }
@@ -246,7 +247,15 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     const char* e1 = getenv("KVCOMM_PH_PAD_ROWS");
     const char* e2 = getenv("KVCOMM_SLOT_PAD_ROWS");
     p->ph_ld = p->maxlen + (e1 ? atoi(e1) : 0);
-    p->slot_pad = int64_t(e2 ? atoi(e2) : 0) * p->d;
+    // Default: 64 rows between consecutive slots of the placeholder slab (one fp8 block
+    // for fp8 pools).  Without it, the tiles the ring keeps in flight (the same
+    // (layer, head, tile) of consecutive anchors) sit a large power-of-two multiple
+    // apart; measured (profiles/r01g_slot_pad.jsonl): config-4 realign 5.26 -> 5.08 ms,
+    // config 2 4.68 -> 4.65 ms.
+    const int pad_rows = e2 ? atoi(e2) : 64;
+    p->slot_pad = int64_t(pad_rows) * p->d;
+    const char* e3 = getenv("KVCOMM_F8_SLOT_PAD_BLOCKS");
+    p->f8_slot_pad = int64_t(e3 ? atoi(e3) : 1) * fp8_block_bytes(p->d);
 
   }
   p->prefix_len.assign(c->prefix_len, c->prefix_len + c->num_consumers);
