@@ -182,6 +182,22 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
 // producer warp.
 // kD: head_dim fixed at compile time (128: the Llama shapes; all tile geometry and
 // thread offsets fold into immediates), 0: read from the table (any supported d).
+// KVC_WARP_ARRIVE=1: one elected arrive per consumer warp after __syncwarp instead of one
+// per thread — measured no faster (bf16 config 2 and 4) and 1.5 % slower with fp8 pools
+// (r01g), and the per-thread form keeps the ordering visible to racecheck.
+#ifndef KVC_WARP_ARRIVE
+#define KVC_WARP_ARRIVE 0
+#endif
+constexpr int kArrivals = KVC_WARP_ARRIVE ? 1 : 32;  // empty-barrier arrivals per consumer warp
+__device__ __forceinline__ void stage_release(uint64_t* b) {
+#if KVC_WARP_ARRIVE
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+#else
+  mbar_arrive(b);
+#endif
+}
+
 template <int kConsumerWarps, int kD>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     realign_kernel(const uint8_t* __restrict__ tab, int variant) {
@@ -205,11 +221,11 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kNStage; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps * 32);  // every consumer thread arrives
+      mbar_init(&empty[i], kConsumerWarps * kArrivals);  // every consumer thread (or warp) arrives
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&uw_full[i], 1);
-      mbar_init(&uw_empty[i], kConsumerWarps * 32);
+      mbar_init(&uw_empty[i], kConsumerWarps * kArrivals);
     }
     fence_mbar_init();
   }
@@ -356,13 +372,13 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           mbar_wait(&full[stage], phase);
           const uint8_t* b0 = sdata + size_t(stage) * kStageStride;
           fp8_load<kItemsPerThread>(w0, code0, b0, reinterpret_cast<const uint8_t*>(wv), b0 + scale_off, coff, roff);
-          mbar_arrive(&empty[stage]);
+          stage_release(&empty[stage]);
           if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           mbar_wait(&full[stage], phase);
           const uint8_t* b1 = sdata + size_t(stage) * kStageStride;
           fp8_load<kItemsPerThread>(w1, code1, b1, reinterpret_cast<const uint8_t*>(wv + rw), b1 + scale_off, coff,
                                     roff);
-          mbar_arrive(&empty[stage]);
+          stage_release(&empty[stage]);
           if (++stage == kNStage) { stage = 0; phase ^= 1u; }
           if (!(variant & 32)) {
             fp8_accum<kItemsPerThread>(acc, w0, code0);
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           float w[2][kItemsPerThread];
           uint4 code[2][kItemsPerThread];
           fp8_load<kItemsPerThread>(w, code, buf, reinterpret_cast<const uint8_t*>(wv), buf + scale_off, coff, roff);
-          mbar_arrive(&empty[stage]);  // this thread's reads of the stage are done
+          stage_release(&empty[stage]);  // this thread's reads of the stage are done
           if (!(variant & 32)) fp8_accum<kItemsPerThread>(acc, w, code);
         } else {
           float w[kItemsPerThread];
@@ -390,7 +406,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             va[q] = lds128(buf + irow[q] * row_bytes + ivec[q] * 16);
             vb[q] = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
           }
-          mbar_arrive(&empty[stage]);  // this thread's reads of the stage are done
+          stage_release(&empty[stage]);  // this thread's reads of the stage are done
           if (!(variant & 32)) {
 #pragma unroll
             for (int q = 0; q < kItemsPerThread; ++q) {
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         }
         if (++stage == kNStage) { stage = 0; phase ^= 1u; }
       }
-      mbar_arrive(&uw_empty[ub]);  // weight chunk consumed
+      stage_release(&uw_empty[ub]);  // weight chunk consumed
       if (++ub == 2) { ub = 0; uphase ^= 1u; }
     }
 
@@ -499,10 +515,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         if (threadIdx.x == 0) {
           bulk_s2g(dst + int64_t(r0) * d, buf, uint32_t(srows) * row_bytes);
           bulk_wait_read_all();
-          mbar_arrive_cnt(&empty[stage], kConsumerWarps * 32);  // for all consumers (named barrier above)
+          mbar_arrive_cnt(&empty[stage], kConsumerWarps * kArrivals);  // for all consumers (named barrier above)
         }
       } else {
-        mbar_arrive(&empty[stage]);
+        stage_release(&empty[stage]);
       }
       if (++stage == kNStage) { stage = 0; phase ^= 1u; }
     }

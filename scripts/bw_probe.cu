@@ -152,6 +152,44 @@ __global__ void tma_mix_store(const uint8_t* src, int64_t nchunks, int chunk, in
 
 // TMA read of `chunk`-byte tiles where every tile also pulls `nsmall` 256-byte side
 // slices (one from an L2-resident table, the rest from DRAM), as the fp8 realign does.
+// Realign's anchor-major access: CTA b takes units u = b, b + grid, ...; per unit it
+// streams the unit's chunk of each of K anchors, anchor j at j * stride + u * chunk
+// (the pool slab layout [slot][...]), or at (u * K + j) * chunk when stride == 0
+// (anchors of one unit contiguous).
+__global__ void tma_gather(const uint8_t* src, int64_t units, int K, int64_t stride, int chunk, int nstage) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(nstage) * chunk);
+  uint64_t* empty = full + nstage;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (threadIdx.x >= 32) {
+    if (threadIdx.x == 32) {
+      int st = 0; uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
+        for (int j = 0; j < K; ++j) {
+          const int64_t off = stride ? j * stride + u * chunk : (u * K + j) * chunk;
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_expect(&full[st], chunk);
+          bulk(sm + size_t(st) * chunk, src + off, chunk, &full[st], pol);
+          if (++st == nstage) { st = 0; ph ^= 1; }
+        }
+    }
+    return;
+  }
+  int st = 0; uint32_t ph = 0;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x)
+    for (int j = 0; j < K; ++j) {
+      mbar_wait(&full[st], ph);
+      __syncwarp();
+      if (threadIdx.x == 0) mbar_arrive(&empty[st]);
+      if (++st == nstage) { st = 0; ph ^= 1; }
+    }
+}
 __global__ void tma_read_side(const uint8_t* src, int64_t nchunks, int chunk, int nstage, const uint8_t* side,
                               int64_t side_bytes, int nsmall) {
   extern __shared__ __align__(128) uint8_t sm[];
@@ -246,6 +284,28 @@ int main() {
     printf("%-40s %8.1f GB/s  (%.3f ms)%s\n", name, moved / (best * 1e-3) / 1e9, best,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
   };
+  {  // anchor-major gather (realign's pattern) vs anchors of a unit contiguous
+    const int chunk = 16384, nst = 9;
+    size_t smem = size_t(nst) * chunk + 2 * nst * 8;
+    cudaFuncSetAttribute(tma_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    for (int K : {20, 64, 256}) {
+      const int64_t per = (bytes / K) / chunk * chunk;   // slot size, a multiple of the chunk
+      const int64_t units = per / chunk - 2;
+      for (int mode = 0; mode < 4; ++mode) {
+        // 0: slot stride = per (as allocated), 1: per + 16 KiB pad, 2: per rounded down to a
+        // power of two, 3: contiguous anchors per unit
+        int64_t stride = per;
+        if (mode == 1) stride = per - 2 * chunk + chunk;   // per minus one chunk: shifted alignment
+        if (mode == 2) { stride = 1; while (stride * 2 <= per) stride *= 2; }
+        if (mode == 3) stride = 0;
+        const int64_t u = mode == 2 ? stride / chunk - 2 : units;
+        char name[128];
+        snprintf(name, sizeof(name), "tma_gather K=%d %s", K,
+                 mode == 0 ? "slot-major" : mode == 1 ? "slot-major (shifted)" : mode == 2 ? "slot-major pow2" : "unit-major");
+        timeit([&] { tma_gather<<<sms, 64, smem>>>(src, u, K, stride, chunk, nst); }, double(u) * K * chunk, name);
+      }
+    }
+  }
   const int chunks[] = {4096, 8192, 16384, 32768};
   for (int chunk : chunks) {
     for (int nst : {4, 8, 12}) {

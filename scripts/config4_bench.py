@@ -26,7 +26,7 @@ from synth.state import keyed_gen
 
 L, H, D, DE = 80, 8, 128, 8192
 LAYERS, HEADS = (0, 20), (0, 4)
-T, P, M, P0, N_VOCAB = 3072, 32, 256, 200, 128256
+T, P, M, P0, N_VOCAB = 3072, 32, int(os.environ.get("C4_ANCHORS", "256")), 200, 128256
 SEED = 70
 
 
