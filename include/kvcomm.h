@@ -72,7 +72,9 @@ typedef enum {
   KVCOMM_REASON_EMPTY_POOL = 1,     /* pool holds no anchor                                   */
   KVCOMM_REASON_TOO_LONG = 2,       /* L_φ > max_{ψ∈𝒜} L_ψ  (Eq. 5 first clause)             */
   KVCOMM_REASON_NO_CANDIDATES = 3,  /* no anchor with L_ψ >= L_φ and the consumer's offsets  */
-  KVCOMM_REASON_HIGH_ENTROPY = 4    /* H_{φ|𝒜} > γ log|𝒜_φ|  (Eq. 5 second clause)           */
+  KVCOMM_REASON_HIGH_ENTROPY = 4,   /* H_{φ|𝒜} > γ log|𝒜_φ|  (Eq. 5 second clause)           */
+  KVCOMM_REASON_SHARD_MISMATCH = 5  /* sharded matching: the ranks' job layouts differ (pools
+                                       out of step across ranks); treated as NewAnchor        */
 } kvcomm_reason;
 
 typedef enum { KVCOMM_SCALAR_FROBENIUS = 0, KVCOMM_SCALAR_MEAN_L2 = 1 } kvcomm_scalar_distance;
@@ -441,7 +443,11 @@ KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, 
  *   kvcomm_plan_run_end    (d̄ reduction + verdict, gated realign)
  * and kvcomm_plan_run refuses a sharded plan.  Every rank must call begin/end once per
  * request in lockstep (buffer parities alternate; kvcomm_plan_match_shard resets them).
- * The per-job tie_band_count then counts this rank's positions only. */
+ * The per-job tie_band_count then counts this rank's positions only.  Every rank also
+ * publishes a fingerprint of its job layout (candidate slots, lengths, k, γ, modes) into
+ * every rank's buffers; a job whose fingerprints differ across ranks is reported
+ * NewAnchor with reason SHARD_MISMATCH (its agents are not realigned) and
+ * kvcomm_plan_results returns SHAPE_MISMATCH — never silently blended weights. */
 /* Export the plan's match buffers (W, w̄ and scratch of both parities, one allocation):
  * `bytes` (may be NULL) lets ranks check that their plans have the same layout. */
 struct kvcomm_ipc_handle;  /* defined with the fused gather below */

@@ -22,7 +22,7 @@ OK = 0
 STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE_MISMATCH", "NO_CANDIDATES", "MISSING_OFFSET",
                 "POSITION_GAP", "POSITION_OVERLAP", "NOT_FOUND", "OUT_OF_MEMORY", "CUDA", "NCCL", "IO"]
 SHAREABLE, NEW_ANCHOR = 0, 1
-REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY"]
+REASONS = ["OK", "EMPTY_POOL", "TOO_LONG", "NO_CANDIDATES", "HIGH_ENTROPY", "SHARD_MISMATCH"]
 PLACEHOLDER, PREFIX, COPY = 0, 1, 2
 OFFSET_GIVEN, OFFSET_MEASURE = 0, 1
 SCALAR_FROBENIUS, SCALAR_MEAN_L2 = 0, 1

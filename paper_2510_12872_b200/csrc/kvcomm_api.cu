@@ -879,7 +879,9 @@ void fill_info_from_result(kvcomm_match_info* info, const MatchResultDev& r) {
   info->entropy = r.entropy;
   info->threshold = r.threshold;
   info->verdict = r.verdict ? KVCOMM_NEW_ANCHOR : KVCOMM_SHAREABLE;
-  info->reason = r.verdict ? KVCOMM_REASON_HIGH_ENTROPY : KVCOMM_REASON_OK;
+  info->reason = r.shard_mismatch ? KVCOMM_REASON_SHARD_MISMATCH
+                 : r.verdict      ? KVCOMM_REASON_HIGH_ENTROPY
+                                  : KVCOMM_REASON_OK;
   info->verdict_in_tie_band = r.tie_flag;
   info->tie_band_count = r.tie_count;
 }
@@ -1433,6 +1435,7 @@ struct kvcomm_plan_s {
   void* xbuf = nullptr;
   int64_t xbytes = 0;
   std::vector<int64_t> W_off[2], wbar_off[2], sc_off[2];  // byte offsets into xbuf
+  int64_t fp_off[2] = {0, 0};     // per parity: uint64 fingerprints [kMaxMatchPeers + 1] (sharded runs)
   std::vector<int64_t> ld_w;
   // sharded matching: this rank's position blocks, and the peers' xbuf mappings
   int rank = 0, world = 1;
@@ -1566,9 +1569,15 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
                                               (2 * cap + 1)),
                              256));
     }
+  for (int par = 0; par < 2; ++par) {
+    pl->fp_off[par] = off;
+    off += int64_t(align_up(sizeof(uint64_t) * (kMaxMatchPeers + 1), 256));
+  }
   pl->xbytes = off;
-  if (cudaMalloc(&pl->xbuf, size_t(off)) != cudaSuccess) {
+  if (cudaMalloc(&pl->xbuf, size_t(off)) != cudaSuccess ||
+      cudaMemset(static_cast<char*>(pl->xbuf) + pl->fp_off[0], 0, size_t(off - pl->fp_off[0])) != cudaSuccess) {
     cudaGetLastError();
+    cudaFree(pl->xbuf);
     pl->xbuf = nullptr;
     plan_free(pl);
     return fail(KVCOMM_ERR_OUT_OF_MEMORY, "plan weight buffers (%lld bytes)", (long long)off);
@@ -1661,7 +1670,34 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
     hs.push_back(std::move(h));
   }
   // one table: [match part][realign part]
-  const MatchLayout ML = items.empty() ? MatchLayout() : layout_match(items);
+  MatchLayout ML = items.empty() ? MatchLayout() : layout_match(items);
+  if (pl->world > 1 && !items.empty()) {  // layout fingerprint, compared across ranks by finalize
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](uint64_t v) {
+      for (int b = 0; b < 8; ++b) {
+        h ^= (v >> (8 * b)) & 0xffu;
+        h *= 1099511628211ull;
+      }
+    };
+    mix(items.size());
+    for (const MatchItem& it : items) {
+      uint32_t gb;
+      std::memcpy(&gb, &it.gamma, sizeof(gb));
+      mix(uint64_t(it.p->cap) << 32 | uint32_t(it.L_phi));
+      mix(uint64_t(it.top_k) << 32 | gb);
+      mix(uint64_t(it.p->cfg.scalar_distance) << 32 | uint32_t(it.p->cfg.similarity));
+      mix(uint64_t(it.info->n_candidates));
+      for (int j = 0; j < it.info->n_candidates; ++j) mix(uint64_t(uint32_t(it.info->candidates[j])));
+    }
+    ML.hdr.fingerprint = h;
+    ML.hdr.shard_rank = pl->rank;
+    ML.hdr.shard_world = pl->world;
+    for (int r = 0, q = 0; r < pl->world; ++r) {
+      char* base = r == pl->rank ? pl->xb() : pl->peer_x[q++];
+      ML.hdr.fp_dst[r] = reinterpret_cast<uint64_t*>(base + pl->fp_off[par]) + pl->rank;
+    }
+    ML.hdr.fp_mine = reinterpret_cast<const uint64_t*>(pl->xb() + pl->fp_off[par]);
+  }
   RealignLayout RL = layout_realign(pl->d, pl->Ls, pl->Hs, hs);
   const size_t roff = align_up(ML.bytes, 256);
   KV_TRY(entry_reserve(E, roff + RL.bytes));
@@ -1751,10 +1787,14 @@ KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t pl, kvcomm_match_info
   RingEntry& E = pl->tab[pl->last];
   KV_CUDA(cudaEventSynchronize(E.done));
   const int nm = int(pl->matches.size());
+  bool mismatch = false;
   if (pl->res_off >= 0) {
     const MatchResultDev* res = reinterpret_cast<const MatchResultDev*>(static_cast<uint8_t*>(E.host) + pl->res_off);
     for (int i = 0; i < nm; ++i)
-      if (pl->job_of[i] >= 0) fill_info_from_result(&pl->infos[i], res[pl->job_of[i]]);
+      if (pl->job_of[i] >= 0) {
+        fill_info_from_result(&pl->infos[i], res[pl->job_of[i]]);
+        mismatch |= res[pl->job_of[i]].shard_mismatch != 0;
+      }
   }
   if (infos)
     for (int i = 0; i < nm; ++i) infos[i] = pl->infos[i];
@@ -1764,6 +1804,10 @@ KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t pl, kvcomm_match_info
       for (int mi : pl->agent_matches[a]) okk &= pl->infos[mi].verdict == KVCOMM_SHAREABLE;
       agent_reused[a] = okk ? 1 : 0;
     }
+  if (mismatch)
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH,
+                "sharded matching: the ranks matched different candidate sets or lengths (pools out of step); "
+                "those agents were not realigned");
   return ok();
 }
 

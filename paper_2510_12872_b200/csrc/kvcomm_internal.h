@@ -65,7 +65,8 @@ struct SegDev {
 
 struct MatchResultDev {
   double entropy, threshold;
-  int32_t verdict, tie_flag, tie_count, _pad;
+  int32_t verdict, tie_flag, tie_count;
+  int32_t shard_mismatch;  // sharded matching: another rank matched a different job layout
 };
 
 // Device-side work table for one realign launch (lives in one contiguous buffer).
@@ -120,6 +121,14 @@ struct MatchJob {
 struct MatchHdr {
   int32_t n_jobs, total_blocks, P, any_peer;   // total_blocks: work items of this launch (owned blocks)
   int64_t job_off, int_off, res_off, tie_off;   // byte offsets from the table base
+  // Sharded matching: every rank stores a fingerprint of its job layout (candidates,
+  // lengths, modes) into slot `shard_rank` of every rank's fingerprint array; finalize
+  // compares all `shard_world` slots with its own and, on any difference, reports the
+  // job NewAnchor with shard_mismatch set (the realign gate then skips its segments).
+  uint64_t fingerprint;
+  int32_t shard_rank, shard_world;
+  uint64_t* fp_dst[kMaxMatchPeers + 1];   // [r]: this rank's slot in rank r's array
+  const uint64_t* fp_mine;                // this rank's array [shard_world]
 };
 
 // distance + per-position weights over all jobs' blocks, then one finalize block per job

@@ -279,6 +279,8 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
   int32_t* counter = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off) + hdr->n_jobs;
   __shared__ int s_item;
+  if (hdr->shard_world > 1 && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int r = 0; r < hdr->shard_world; ++r) *hdr->fp_dst[r] = hdr->fingerprint;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -380,16 +382,19 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
   }
   if (threadIdx.x == 0) {
     const double thr = a.gamma * log(double(a.n_cand));
+    int mismatch = 0;
+    for (int r = 0; r < hdr->shard_world && hdr->shard_world > 1; ++r) mismatch |= hdr->fp_mine[r] != hdr->fingerprint;
     res->entropy = H;
     res->threshold = thr;
-    res->verdict = H > thr ? 1 : 0;
+    res->verdict = (H > thr || mismatch) ? 1 : 0;
+    res->shard_mismatch = mismatch;
     res->tie_flag = (a.n_cand > 1 && fabs(H - thr) <= kTieRel * thr) ? 1 : 0;  // |𝒜|=1: H = 0 = thr exactly
     res->tie_count = ties[blockIdx.x];
   }
 }
 
 cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
-  if (hdr.total_blocks == 0) return cudaSuccess;  // sharded: this rank owns no block
+  // (a rank that owns no position block still launches one block: it publishes its fingerprint)
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
@@ -400,7 +405,7 @@ cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_dist_kernel, kMatchThreads, smem);
-  const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));
+  const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));  // >= 1
   match_dist_kernel<<<grid, kMatchThreads, smem, s>>>(t);
   return cudaGetLastError();
 }

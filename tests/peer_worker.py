@@ -19,7 +19,8 @@ import torch.distributed as dist
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
-    shard_match = len(sys.argv) > 2 and sys.argv[2] == "shard-match"
+    shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch")
+    mismatch = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch"
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
     scal = sys.argv[5] if len(sys.argv) > 5 else "frobenius"
@@ -45,6 +46,32 @@ def main():
     agents = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
               for i, a in enumerate(st.agents)]
     req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=top_k)
+    if mismatch:   # the ranks' pools out of step: rank 1 lacks one user_question anchor
+        if rank == 1:
+            st.pools["user_question"].evict(0)
+        req.shard_matching(rank, world, 0)
+        for _ in range(2):
+            req._mshard.run([st.queries[n] for n in req.names], sync=True)
+            peer.sync()
+        from paper_2510_12872_b200._lib import KVCommError
+        try:
+            req.plan.results()
+            raise AssertionError("out-of-step pools were not detected")
+        except KVCommError as e:
+            assert e.status_name == "SHAPE_MISMATCH" and "sharded matching" in str(e), e
+        checked = 0
+        for i, a in enumerate(ref.agents):   # no agent was realigned: the caches stay zero
+            fk, fv = peer.full(i)
+            if fk is None:
+                continue
+            assert not fk.any() and not fv.any(), f"rank {rank}: agent {a.agent} written"
+            checked += 1
+        dist.barrier()
+        req._mshard.close()
+        peer.close()
+        print(f"rank {rank}: {checked} agents untouched, mismatch reported", flush=True)
+        dist.destroy_process_group()
+        return
     if shard_match:  # each rank computes half the match positions, stored into both ranks' buffers
         req.shard_matching(rank, world, 0)
     for _ in range(3):  # the later runs overwrite the same rows (and alternate the match buffers)
