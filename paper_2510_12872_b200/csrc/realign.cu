@@ -243,6 +243,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
       const uint64_t pol_stream = policy_evict_first();  // offsets: read once per request
+      // weight blocks: re-read by every (layer, head, plane) unit of the same tile, so they
+      // stay in L2 (evict_first measured 0.4 % slower at config 2, 0.9 % at config 4)
+      const uint64_t pol_weights = policy_evict_last();
       const uint64_t pol_shared = (variant & 4) ? policy_evict_first()
                                   : (variant & 8) ? policy_evict_normal() : policy_evict_last();
       int stage = 0, ub = 0;
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           mbar_wait(&uw_empty[ub], uphase ^ 1u);
           const uint32_t wbytes = uint32_t((c1 - c0) * rw) * 4u;
           mbar_arrive_expect_tx(&uw_full[ub], wbytes);
-          bulk_g2s(suw + ub * (kUnitWBytes / 4), wt + int64_t(c0) * rw, wbytes, &uw_full[ub], pol_stream);
+          bulk_g2s(suw + ub * (kUnitWBytes / 4), wt + int64_t(c0) * rw, wbytes, &uw_full[ub], pol_weights);
           if (++ub == 2) { ub = 0; uphase ^= 1u; }
           for (int c = c0; c < c1; ++c) {
             const int next = c + 1 < n_cand ? cands[c + 1] : 0;  // in flight during the wait
