@@ -124,7 +124,14 @@ typedef struct {
                               KVCOMM_ROPE_HALF (0, default): HF rotate_half, pairs (f, f + d/2);
                               KVCOMM_ROPE_INTERLEAVED (1): GPT-J style, pairs (2f, 2f + 1).
                               Both rotate pair f by δ·inv_freq[f].                        */
-  int32_t _reserved;       /* 0 */
+  int16_t emb_shard_rank;  /* embedding rows held by this pool ("sharded
+                              embeddings").  emb_shard_world <= 1 (default 0): every row.  G =
+                              emb_shard_world in [2, 8]: only rows i with (i / 2) mod G ==
+                              emb_shard_rank — the position blocks this rank matches under
+                              sharded matching (kvcomm_plan_match_shard with the same rank and
+                              world; any other match of the pool is INVALID_ARGUMENT) — so each
+                              of G GPUs stores 1/G of the embeddings instead of all of them.   */
+  int16_t emb_shard_world;
   const int32_t* prefix_len; /* host [num_consumers]: |p_(m,i)| following this placeholder */
   const double* inv_freq;  /* host [head_dim/2]: RoPE inverse frequencies (copied)        */
 } kvcomm_pool_config;

@@ -39,7 +39,7 @@ class PoolConfig(C.Structure):
                 ("capacity", C.c_int32), ("max_anchor_len", C.c_int32), ("num_consumers", C.c_int32),
                 ("scalar_distance", C.c_int32), ("similarity", C.c_int32),
                 ("offset_format", C.c_int32), ("placement", C.c_int32), ("rope_layout", C.c_int32),
-                ("_reserved", C.c_int32), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
+                ("emb_shard_rank", C.c_int16), ("emb_shard_world", C.c_int16), ("prefix_len", C.POINTER(C.c_int32)), ("inv_freq", C.POINTER(C.c_double))]
 
 
 class KVView(C.Structure):

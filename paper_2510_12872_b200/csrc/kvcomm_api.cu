@@ -98,8 +98,12 @@ struct kvcomm_pool_s {
   int64_t slot_pad = 0;     // extra elements between slots (breaks power-of-two strides)
   std::vector<int32_t> prefix_len;
   std::vector<double> inv_freq;
+  // embedding sharding (config emb_shard_*): rows of position blocks b with b % emb_world ==
+  // emb_rank only, block b stored at b / emb_world; emb_rows = stored rows per slot
+  int emb_rank = 0, emb_world = 1;
+  int64_t emb_rows = 0;
   // device slabs
-  bf16* emb = nullptr;                 // [cap][maxlen][De]
+  bf16* emb = nullptr;                 // [cap][emb_rows][De]
   bool fp8 = false;                    // offset_format == KVCOMM_OFFSET_FP8_E4M3
   bf16* ph = nullptr;                  // [C][cap][2][Ls][Hs][ph_ld][d]  (bf16 pools)
   std::vector<bf16*> pf;               // per consumer: [cap][2][Ls][Hs][P_c][d]
@@ -129,10 +133,18 @@ struct kvcomm_pool_s {
   int64_t f8_pf_plane(int c) const { return int64_t(Ls) * Hs * f8_lh(prefix_len[c]); }
   int64_t f8_pf_slot(int c) const { return 2 * f8_pf_plane(c); }
   int64_t pf_slot_stride(int c) const { return int64_t(2) * Ls * Hs * pf_ld(c) * d; }
+  // rows stored for an anchor of length L (all of them unless the embeddings are sharded)
+  int64_t emb_row_count(int64_t L) const;
   int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * pf_ld(c) * d; }
 };
 
 static constexpr int kMatchP = 2;  // positions per match work item
+
+int64_t kvcomm_pool_s::emb_row_count(int64_t L) const {
+  if (emb_world <= 1) return L;
+  const int64_t cyc = int64_t(kMatchP) * emb_world, rem = L % cyc;
+  return L / cyc * kMatchP + std::max<int64_t>(0, std::min<int64_t>(kMatchP, rem - int64_t(emb_rank) * kMatchP));
+}
 
 static void pool_free(kvcomm_pool_s* p) {
   if (!p) return;
@@ -228,6 +240,12 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "fp8 offsets need head_dim >= 64 (got %d)", c->head_dim);
   for (int i = 0; i < c->num_consumers; ++i)
     if (c->prefix_len[i] < 0) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "prefix_len[%d] < 0", i);
+  if (c->emb_shard_world > 1 &&
+      (c->emb_shard_world > kMaxMatchPeers + 1 || c->emb_shard_rank < 0 || c->emb_shard_rank >= c->emb_shard_world))
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "emb_shard rank %d / world %d (world <= %d)", c->emb_shard_rank,
+                c->emb_shard_world, kMaxMatchPeers + 1);
+  if (c->emb_shard_world <= 1 && c->emb_shard_rank != 0)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT, "emb_shard_rank %d without emb_shard_world", c->emb_shard_rank);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device < 0 || c->device >= ndev) {
     cudaGetLastError();
@@ -269,7 +287,15 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   const bool host = c->placement == KVCOMM_PLACE_HOST;
 #define ALLOC_OFF(ptr, n, what)                      \
   if ((st = dev_alloc(p, &(ptr), (n), what, host)) != KVCOMM_OK) { pool_free(p); return st; }
-  ALLOC(p->emb, int64_t(p->cap) * p->maxlen * p->De, "embedding slab");
+  if (c->emb_shard_world > 1) {
+    p->emb_rank = c->emb_shard_rank;
+    p->emb_world = c->emb_shard_world;
+  }
+  {
+    const int64_t cyc = int64_t(kMatchP) * p->emb_world;
+    p->emb_rows = p->emb_world > 1 ? (p->maxlen + cyc - 1) / cyc * kMatchP : p->maxlen;
+  }
+  ALLOC(p->emb, int64_t(p->cap) * p->emb_rows * p->De, "embedding slab");
   if (!p->fp8) {
     ALLOC_OFF(p->ph, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab");
     p->pf.assign(p->C, nullptr);
@@ -489,9 +515,21 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_ps
     p->slots[evicted] = SlotMeta();
     slot = evicted;
   }
-  KV_CUDA(launch_copy_flat(static_cast<const bf16*>(emb), p->emb + int64_t(slot) * p->maxlen * p->De,
-                           int64_t(L_psi) * p->De, s));
-  g_launches += 1;
+  bf16* edst = p->emb + int64_t(slot) * p->emb_rows * p->De;
+  if (p->emb_world <= 1) {
+    KV_CUDA(launch_copy_flat(static_cast<const bf16*>(emb), edst, int64_t(L_psi) * p->De, s));
+    g_launches += 1;
+  } else {  // this rank's position blocks only: block b = rank + k * world -> stored block k
+    const int64_t P = kMatchP, G = p->emb_world, row = int64_t(p->De) * sizeof(bf16);
+    const int64_t stored = p->emb_row_count(L_psi), full = stored / P, tail = stored - full * P;
+    const uint8_t* src = static_cast<const uint8_t*>(emb) + int64_t(p->emb_rank) * P * row;
+    if (full > 0)
+      KV_CUDA(cudaMemcpy2DAsync(edst, size_t(P * row), src, size_t(G * P * row), size_t(P * row), size_t(full),
+                                cudaMemcpyDeviceToDevice, s));
+    if (tail > 0)
+      KV_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(edst) + full * P * row, src + full * G * P * row,
+                              size_t(tail * row), cudaMemcpyDeviceToDevice, s));
+  }
   uint64_t phm = 0, pfm = 0;
   InsertJobs jobs;
   for (int i = 0; i < n_offs; ++i) {
@@ -576,7 +614,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_slot_info(kvcomm_pool_t p, int32_t s
 // into a pool whose row padding (KVCOMM_PH_PAD_ROWS / KVCOMM_SLOT_PAD_ROWS) differs.
 namespace {
 constexpr char kCkptMagic[8] = {'K', 'V', 'C', 'P', 'O', 'O', 'L', '1'};
-constexpr uint32_t kCkptVersion = 1;
+constexpr uint32_t kCkptVersion = 2;  // 2: + embedding shard (rank, world)
 
 struct File {
   FILE* f = nullptr;
@@ -638,8 +676,8 @@ kvcomm_status slots_io(kvcomm_pool_s* p, bool save, FILE* f) {
   for (int s = 0; s < p->cap; ++s) {
     const SlotMeta& m = p->slots[s];
     if (!m.occupied) continue;
-    const size_t ew = size_t(m.length) * p->De * sizeof(bf16);
-    const Region er{p->emb + int64_t(s) * p->maxlen * p->De, ew, ew, 1};
+    const size_t ew = size_t(p->emb_row_count(m.length)) * p->De * sizeof(bf16);  // rows as stored
+    const Region er{p->emb + int64_t(s) * p->emb_rows * p->De, ew, ew, 1};
     KV_TRY(region_io(er, buf, save, f));
     for (int c = 0; c < p->C; ++c) {
       if (m.ph_mask >> c & 1) KV_TRY(region_io(offset_region(p, c, s, false, m.length), buf, save, f));
@@ -663,6 +701,8 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_save(kvcomm_pool_t p, const char* pa
   KV_TRY(fwrite_all(F.f, kCkptMagic, sizeof(kCkptMagic), "magic"));
   KV_TRY(fwrite_all(F.f, &kCkptVersion, sizeof(kCkptVersion), "version"));
   for (int i = 0; i < kCfgInts; ++i) KV_TRY(fwrite_all(F.f, cfg_ints(c, i), sizeof(int32_t), "config"));
+  const int32_t es[2] = {c.emb_shard_rank, c.emb_shard_world};
+  KV_TRY(fwrite_all(F.f, es, sizeof(es), "config"));
   KV_TRY(fwrite_all(F.f, p->prefix_len.data(), sizeof(int32_t) * p->C, "prefix_len"));
   KV_TRY(fwrite_all(F.f, p->inv_freq.data(), sizeof(double) * (p->d / 2), "inv_freq"));
   KV_TRY(fwrite_all(F.f, &p->next_index, sizeof(int64_t), "insertion counter"));
@@ -695,6 +735,10 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_load(const char* path, int32_t devic
   if (ver != kCkptVersion) return fail(KVCOMM_ERR_IO, "%s: checkpoint version %u (expected %u)", path, ver, kCkptVersion);
   kvcomm_pool_config c{};
   for (int i = 0; i < kCfgInts; ++i) KV_TRY(fread_all(F.f, cfg_ints(c, i), sizeof(int32_t), "config"));
+  int32_t es[2];
+  KV_TRY(fread_all(F.f, es, sizeof(es), "config"));
+  c.emb_shard_rank = int16_t(es[0]);
+  c.emb_shard_world = int16_t(es[1]);
   if (c.num_consumers < 1 || c.num_consumers > KVCOMM_MAX_CONSUMERS || c.head_dim < 2 || c.head_dim > 256 ||
       c.capacity < 1 || c.capacity > KVCOMM_MAX_CAPACITY)
     return fail(KVCOMM_ERR_IO, "%s: corrupt configuration", path);
@@ -902,7 +946,7 @@ struct MatchItem {
   double* scratch = nullptr;      // partial + chunk sums owned by the caller (plans), else the pool's
   // sharded matching (plans only): own position blocks [own_lo, own_lo + n_own), n_own < 0 = all;
   // W columns and partial rows also stored into the peers' copies
-  int own_lo = 0, n_own = -1, n_peer = 0;
+  int own_lo = 0, n_own = -1, own_step = 1, n_peer = 0;
   float* W_peer[kMaxMatchPeers] = {};
   double* partial_peer[kMaxMatchPeers] = {};
 };
@@ -955,7 +999,8 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     MatchJob& a = jobs[t];
     a.query = static_cast<const bf16*>(it.query);
     a.emb = p->emb;
-    a.slot_stride = int64_t(p->maxlen) * p->De;
+    a.slot_stride = p->emb_rows * p->De;
+    a.emb_world = p->emb_world;
     a.W = it.W;
     a.ld_w = it.ld_w;
     a.top_k = it.top_k;
@@ -986,6 +1031,7 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     a.n_blocks = match_blocks(it.L_phi);
     a.block_begin = blocks;
     a.own_lo = it.n_own >= 0 ? it.own_lo : 0;
+    a.own_step = it.n_own >= 0 ? it.own_step : 1;
     a.n_own = it.n_own >= 0 ? it.n_own : a.n_blocks;
     blocks += a.n_own;
     a.n_peer = it.n_peer;
@@ -1108,6 +1154,10 @@ int grid_for_device(int dev) {
 static kvcomm_status check_match_request(const kvcomm_match_request& q, int r) {
   kvcomm_pool_s* p = q.pool;
   if (!p || !q.info) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: null pool/info", r);
+  if (p->emb_world > 1)
+    return fail(KVCOMM_ERR_INVALID_ARGUMENT,
+                "request %d: the pool holds 1/%d of the embedding rows; match it through a plan sharded the same way "
+                "(kvcomm_plan_match_shard)", r, p->emb_world);
   if (!(q.gamma >= 0.f && q.gamma <= 1.f))
     return fail(KVCOMM_ERR_INVALID_ARGUMENT, "request %d: gamma %g outside [0,1]", r, q.gamma);
   if (q.L_phi < 1) return fail(KVCOMM_ERR_SHAPE_MISMATCH, "request %d: L_phi %d < 1", r, q.L_phi);
@@ -1624,10 +1674,15 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
     pl->job_of[i] = int(items.size());
     MatchItem it{m.pool, query_embs[i], m.L_phi, m.gamma, k_eff, pl->W(par, i), pl->ld_w[i], nullptr,
                  pl->wbar(par, i), nullptr, info, pl->scratch(par, i)};
-    if (pl->world > 1) {  // this rank's contiguous range of position blocks; the rest comes from the peers
+    if (m.pool->emb_world > 1 && (m.pool->emb_world != pl->world || m.pool->emb_rank != pl->rank))
+      return fail(KVCOMM_ERR_INVALID_ARGUMENT,
+                  "match %d: the pool holds the embeddings of rank %d of %d; the plan matches as rank %d of %d", i,
+                  m.pool->emb_rank, m.pool->emb_world, pl->rank, pl->world);
+    if (pl->world > 1) {  // position blocks b = rank (mod world); the rest comes from the peers
       const int nb = match_blocks(m.L_phi);
-      it.own_lo = int(int64_t(pl->rank) * nb / pl->world);
-      it.n_own = int(int64_t(pl->rank + 1) * nb / pl->world) - it.own_lo;
+      it.own_lo = pl->rank;
+      it.own_step = pl->world;
+      it.n_own = pl->rank < nb ? (nb - pl->rank + pl->world - 1) / pl->world : 0;
       it.n_peer = int(pl->peer_x.size());
       for (int r = 0; r < it.n_peer; ++r) {
         it.W_peer[r] = reinterpret_cast<float*>(pl->peer_x[r] + pl->W_off[par][i]);

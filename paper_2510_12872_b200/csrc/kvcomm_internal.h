@@ -107,11 +107,13 @@ struct MatchJob {
   int32_t s2c_off;          // into MatchHdr ints: slot -> candidate index or -1 [cap]
   int32_t block_begin, n_blocks;  // block_begin: first work item of this job; n_blocks: ALL position blocks
   // Sharded matching: this launch computes position blocks
-  // [own_lo, own_lo + n_own) only and stores their W columns and partial rows into
+  // own_lo + k * own_step (k < n_own) only and stores their W columns and partial rows into
   // this GPU's buffers AND every peer's copy (IPC-mapped) — the chunk/finalize passes
-  // then run on the complete arrays on every rank.  Unsharded: own_lo 0, n_own =
-  // n_blocks, n_peer 0.
-  int32_t own_lo, n_own;
+  // then run on the complete arrays on every rank.  Unsharded: own_lo 0, own_step 1,
+  // n_own = n_blocks, n_peer 0.
+  int32_t own_lo, n_own;    // position blocks own_lo, own_lo + own_step, ... (n_own of them)
+  int32_t own_step;
+  int32_t emb_world;        // > 1: the pool stores only its blocks' rows, compacted (emb_shard)
   int32_t n_peer, _pad_peer;
   float* W_peer[kMaxMatchPeers];
   double* partial_peer[kMaxMatchPeers];

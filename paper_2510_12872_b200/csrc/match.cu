@@ -98,7 +98,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
   const int jb = find_job(jobs, hdr->n_jobs, item);
   const MatchJob& a = jobs[jb];
   const int P = hdr->P;
-  const int lb = a.own_lo + (item - a.block_begin);  // position block (sharded: inside this rank's range)
+  const int lb = a.own_lo + (item - a.block_begin) * a.own_step;  // position block (sharded: this rank's)
   const int32_t* cand = ints + a.cand_off;
   const int32_t* slot2cand = ints + a.s2c_off;
 
@@ -128,7 +128,9 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
   for (int task = warp; task < ntask; task += kMatchWarps) {
     const int p = task / n_cand;
     const int j = task - p * n_cand;
-    const bf16* arow = a.emb + int64_t(cand[j]) * a.slot_stride + int64_t(i0 + p) * De;
+    // anchor row i0 + p; a pool holding only this rank's blocks stores block lb at lb / G
+    const int64_t erow = a.emb_world > 1 ? int64_t(lb / a.emb_world) * P + p : int64_t(i0 + p);
+    const bf16* arow = a.emb + int64_t(cand[j]) * a.slot_stride + erow * De;
     const bf16* qrow = q + size_t(p) * De;
     if (!a.cosine) {
       double s = 0.0;

@@ -131,7 +131,10 @@ class AnchorPool:
                  max_anchor_len: int, prefix_len: Sequence[int], inv_freq, device: int = 0,
                  layer_range: Optional[Tuple[int, int]] = None, head_range: Optional[Tuple[int, int]] = None,
                  scalar_distance: str = "frobenius", similarity: str = "l2", offset_format: str = "bf16",
-                 placement: str = "device", rope_layout: str = "half"):
+                 placement: str = "device", rope_layout: str = "half",
+                 emb_shard: Optional[Tuple[int, int]] = None):
+        """emb_shard = (rank, world): hold only the embedding rows of the position blocks
+        this rank matches under sharded matching (1/world of them)."""
         lb, le = layer_range or (0, num_layers)
         hb, he = head_range or (0, num_kv_heads)
         self.Ls, self.Hs, self.d, self.De = le - lb, he - hb, head_dim, emb_dim
@@ -148,8 +151,10 @@ class AnchorPool:
                            {"l2": L.SIM_L2, "cosine": L.SIM_COSINE}[similarity],
                            {"bf16": L.OFFSET_BF16, "fp8": L.OFFSET_FP8_E4M3}[offset_format],
                            {"device": L.PLACE_DEVICE, "host": L.PLACE_HOST}[placement],
-                           {"half": L.ROPE_HALF, "interleaved": L.ROPE_INTERLEAVED}[rope_layout], 0, pl,
+                           {"half": L.ROPE_HALF, "interleaved": L.ROPE_INTERLEAVED}[rope_layout],
+                           emb_shard[0] if emb_shard else 0, emb_shard[1] if emb_shard else 0, pl,
                            inv.ctypes.data_as(C.POINTER(C.c_double)))
+        self.emb_shard = tuple(emb_shard) if emb_shard else None
         h = C.c_void_p()
         L.check(L.lib().kvcomm_anchor_pool_create(C.byref(cfg), C.byref(h)))
         self._h = h
@@ -186,6 +191,7 @@ class AnchorPool:
         self.offset_format = {L.OFFSET_BF16: "bf16", L.OFFSET_FP8_E4M3: "fp8"}[cfg.offset_format]
         self.rope_layout = {L.ROPE_HALF: "half", L.ROPE_INTERLEAVED: "interleaved"}[cfg.rope_layout]
         self.inv_freq = list(inv)
+        self.emb_shard = (cfg.emb_shard_rank, cfg.emb_shard_world) if cfg.emb_shard_world > 1 else None
         return self
 
     def destroy(self) -> None:

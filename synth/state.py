@@ -114,7 +114,8 @@ class FiveAgentState:
 def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: int = 0, gamma: float = 0.3,
                            layer_range: Optional[Tuple[int, int]] = None, anchor_extra: int = 0,
                            top_k: int = 0, offset_format: str = "bf16", similarity: str = "l2",
-                           scalar_distance: str = "frobenius") -> FiveAgentState:
+                           scalar_distance: str = "frobenius",
+                           emb_shard: Optional[Tuple[int, int]] = None) -> FiveAgentState:
     from paper_2510_12872_b200 import kvcomm as K
     from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
     w = w or five_agent_workload()
@@ -128,7 +129,7 @@ def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: 
         pool = K.AnchorPool(num_layers=w.L, num_kv_heads=w.H, head_dim=w.d, emb_dim=w.D_e, capacity=w.capacity,
                             max_anchor_len=ps.L_phi + anchor_extra, prefix_len=ps.prefix_len, inv_freq=inv,
                             device=device, layer_range=lr, offset_format=offset_format, similarity=similarity,
-                            scalar_distance=scalar_distance)
+                            scalar_distance=scalar_distance, emb_shard=emb_shard)
         for slot in range(w.capacity):
             emb = vocab[inp.anchor_ids(name, slot)]
             offs = [K.OffsetGiven(c, inp.offset(name, slot, c, "ph", 0), inp.offset(name, slot, c, "ph", 1),

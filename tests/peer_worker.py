@@ -19,7 +19,8 @@ import torch.distributed as dist
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
-    shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch")
+    shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch", "shard-match-emb")
+    emb_shard = len(sys.argv) > 2 and sys.argv[2] == "shard-match-emb"
     mismatch = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch"
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
@@ -41,7 +42,8 @@ def main():
     assert all(reused), reused
 
     lr = shard.layer_shard(w.L, rank, world)
-    st = build_five_agent_state(w, seed=3, device=0, gamma=1.0, layer_range=lr, **pk)
+    st = build_five_agent_state(w, seed=3, device=0, gamma=1.0, layer_range=lr,
+                                emb_shard=(rank, world) if emb_shard else None, **pk)
     peer = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, 0)
     agents = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
               for i, a in enumerate(st.agents)]

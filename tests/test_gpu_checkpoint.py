@@ -123,3 +123,34 @@ def test_pool_load_rejects_truncated_file(tmp_path):
         K.AnchorPool.load(path)
     assert e.value.status_name == "IO"
     a.destroy()
+
+
+def test_embedding_sharded_pool(tmp_path):
+    """A pool created with emb_shard=(rank, world) holds only its rank's embedding rows
+    (fewer bytes), refuses unsharded matching, and checkpoints exactly (save -> load ->
+    save gives the same file, the shard is kept)."""
+    from paper_2510_12872_b200 import kvcomm as K
+    from paper_2510_12872_b200._lib import KVCommError
+    mk = lambda es: K.AnchorPool(num_layers=2, num_kv_heads=2, head_dim=64, emb_dim=64, capacity=3,
+                                 max_anchor_len=81, prefix_len=[4], inv_freq=synth.llama3_inv_freq(64),
+                                 emb_shard=es)
+    dense, shard = mk(None), mk((1, 3))
+    assert shard.nbytes() < dense.nbytes()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for n in (81, 77, 2):   # partial cycles: rank 1 of 3 holds rows 2-3 of every 6
+        emb = torch.randn(n, 64, generator=g, device="cuda").to(torch.bfloat16)
+        off = [K.OffsetGiven(0, *(torch.randn(2, 2, m, 64, generator=g, device="cuda").to(torch.bfloat16)
+                                  for m in (n, n, 4, 4)))]
+        shard.insert(emb, off)
+    with pytest.raises(KVCommError) as e:
+        shard.match(torch.zeros(10, 64, dtype=torch.bfloat16, device="cuda"))
+    assert e.value.status_name == "INVALID_ARGUMENT" and "1/3 of the embedding rows" in str(e.value)
+    p1, p2 = str(tmp_path / "a.kvc"), str(tmp_path / "b.kvc")
+    shard.save(p1)
+    back = K.AnchorPool.load(p1)
+    assert back.emb_shard == (1, 3)
+    back.save(p2)
+    assert open(p1, "rb").read() == open(p2, "rb").read()
+    with pytest.raises(KVCommError):
+        mk((3, 3))
+    dense.destroy(); shard.destroy(); back.destroy()

@@ -24,12 +24,14 @@ def _free_port():
     ("bf16", "replicated", 0, 2, "l2", "frobenius"), ("fp8", "replicated", 0, 2, "l2", "frobenius"),
     ("bf16", "shard-match", 0, 2, "l2", "frobenius"), ("fp8", "shard-match", 0, 2, "l2", "frobenius"),
     ("bf16", "shard-match", 2, 2, "l2", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "frobenius"),
-    ("bf16", "shard-match", 0, 2, "cosine", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "mean_l2")])
+    ("bf16", "shard-match", 0, 2, "cosine", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "mean_l2"),
+    ("bf16", "shard-match-emb", 0, 2, "l2", "frobenius"), ("fp8", "shard-match-emb", 2, 3, "cosine", "frobenius")])
 def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal):
     """Also: sharded matching (kvcomm_plan_match_shard) gives weights, verdicts and
     caches bit-identical to the unsharded run (dense and top-k weights; 3 ranks split
     the 48 and 20 position blocks of the two sample lengths unevenly; the cosine
-    variant's three partial sums and the mean-l2 scalar distance)."""
+    variant's three partial sums and the mean-l2 scalar distance; pools that hold only
+    their rank's embedding rows, shard-match-emb)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
            fmt, match, str(top_k), sim, scal]
