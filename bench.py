@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--match", default="sharded", choices=["sharded", "replicated"],
                     help="N>1: each rank computes 1/N of the match positions and stores them into every rank "
                          "(sharded, default) or every rank matches every position (replicated)")
+    ap.add_argument("--emb-shard", action="store_true",
+                    help="N>1 with sharded matching: each rank's pools hold only the embedding rows of the "
+                         "position blocks it matches (1/N of them)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -207,8 +210,9 @@ def arm_config(args, world, w):
                         "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
             "realigned_tokens_per_step": w.realigned_tokens, "anchors_blended": w.capacity,
             "gamma": args.gamma, "offset_storage": args.offsets,
-            "parallelism": (f"layer-shard x{world}, {args.gather} gather, {args.match} matching" if world > 1
-                            else "single"),
+            "parallelism": (f"layer-shard x{world}, {args.gather} gather, {args.match} matching"
+                            + (", sharded embeddings" if args.emb_shard and args.match == "sharded" else "")
+                            if world > 1 else "single"),
             "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
 
 
@@ -436,8 +440,9 @@ def main():
 
     w = synth.five_agent_workload()
     lr = shard.layer_shard(w.L, rank, world)
+    emb_shard = (rank, world) if world > 1 and args.match == "sharded" and args.emb_shard else None
     st = build_five_agent_state(w, seed=args.seed, device=local, gamma=args.gamma, layer_range=lr,
-                                offset_format=args.offsets)
+                                offset_format=args.offsets, emb_shard=emb_shard)
     req = st.request
     stream = torch.cuda.current_stream()
     Ls = lr[1] - lr[0]
@@ -474,6 +479,8 @@ def main():
         try:   # 1/G of the match positions per rank, exchanged over NVLink
             req.shard_matching(rank, world, local)
         except RuntimeError as e:   # all ranks raise together
+            if emb_shard:
+                raise SystemExit(f"[bench] {e}; the pools hold sharded embeddings, rerun without --emb-shard")
             print(f"[bench] {e}; every rank matches every position", file=sys.stderr, flush=True)
             args.match = "replicated (ipc unavailable)"
     qlist = [st.queries[n] for n in req.names]

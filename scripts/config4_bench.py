@@ -109,6 +109,16 @@ def main():
             ts.append(e0.elapsed_time(e1))
         match_ms[G] = sorted(ts)[len(ts) // 2]
         mp.destroy()
+    # embedding memory per GPU: every row (replicated) vs emb_shard=(0, 8) (sharded matching)
+    emb_bytes = {}
+    for name, es in (("replicated", None), ("sharded_G8", (0, 8))):
+        q = kv.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=M, max_anchor_len=T,
+                          prefix_len=[P], inv_freq=synth.llama3_inv_freq(D), layer_range=(0, 1), head_range=(0, 1),
+                          emb_shard=es)
+        emb_bytes[name] = q.nbytes()
+        q.destroy()
+    emb_note = ("pool bytes of a 1-layer x 1-head pool of the same capacity/length (offsets identical, so the "
+                "difference is the embedding slab: 256 anchors x 3072 rows x 8192 x 2 B, or 1/8 of the rows)")
     rl_ms = sorted(realign)[len(realign) // 2]
     tok = Ls * Hs * D * 2 * 2  # one token row, K+V, this shard
     alg = ((M + 2) * T + (M + 2) * P + 2 * P0) * tok
@@ -125,6 +135,7 @@ def main():
         "match_note": "match-only plan over T/G positions (+1-token copy): one rank's share of sharded "
                       "matching, without its NVLink stores and the barrier",
         "step_ms_sharded_match_G8_est": step_ms - match_ms[1] + match_ms[8],
+        "pool_bytes_small_shard": emb_bytes, "pool_bytes_note": emb_note,
         "note": "one of 8 shards measured on one B200; the 8-GPU run is not measured here"}))
     plan.destroy()
     pool.destroy()
