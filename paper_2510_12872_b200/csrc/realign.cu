@@ -533,7 +533,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 int realign_grid_size(int device) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return sms > 0 ? sms : 148;
+  if (sms <= 0) sms = 148;
+  const char* e = getenv("KVCOMM_REALIGN_GRID");  // measurement knob: persistent CTAs (<= SMs)
+  const int g = e ? atoi(e) : 0;
+  return g > 0 && g < sms ? g : sms;
 }
 
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
