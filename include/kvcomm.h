@@ -440,7 +440,8 @@ KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, 
  * The weights of Eq. 5/6 depend only on the sample, so a plan replicated on
  * G ranks (same pools' slots and lengths, same matches, each rank its own layer block)
  * would compute the same distances G times.  After kvcomm_plan_match_shard, each rank
- * computes only its contiguous 1/G range of every job's position blocks and stores those
+ * computes only the position blocks b = rank (mod G) of every job (2 positions per block;
+ * a pool created with emb_shard_rank/world = rank/G needs only those embedding rows) and stores those
  * W columns and d̄ partial rows into its own buffers AND every peer's (NVLink stores into
  * the peers' match buffers, mapped by CUDA IPC); the fixed-order d̄ reduction, w̄, H and
  * the verdict then run on the complete arrays on every rank, so every rank's weights and
