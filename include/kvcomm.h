@@ -228,8 +228,11 @@ KVCOMM_API int64_t kvcomm_kernel_launch_count(void);
 
 /* ---- a0: anchor-pool store ------------------------------------------------- */
 /* Allocates the pool's device slabs (embeddings [𝒱][max_len][D_e], placeholder
- * offsets [C][𝒱][2][Ls][Hs][max_len][d], prefix offsets [C][𝒱][2][Ls][Hs][P_c][d],
- * bf16) on config->device.  OUT_OF_MEMORY if they do not fit. */
+ * offsets [C][𝒱][2][Ls][Hs][max_len][d] with 64 rows of padding between slots, prefix
+ * offsets [C][𝒱][2][Ls][Hs][P_c][d], bf16; fp8 pools: blocked e4m3 codes + row scales) on
+ * config->device (offset slabs in pinned host memory with placement HOST).  With
+ * emb_shard_world G > 1 the embedding slab holds ceil(max_len / 2G) * 2 rows per slot.
+ * OUT_OF_MEMORY if they do not fit. */
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* config,
                                                    kvcomm_pool_t* out);
 KVCOMM_API kvcomm_status kvcomm_anchor_pool_destroy(kvcomm_pool_t pool);
