@@ -25,7 +25,8 @@ def _free_port():
     ("bf16", "shard-match", 0, 2, "l2", "frobenius"), ("fp8", "shard-match", 0, 2, "l2", "frobenius"),
     ("bf16", "shard-match", 2, 2, "l2", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "frobenius"),
     ("bf16", "shard-match", 0, 2, "cosine", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "mean_l2"),
-    ("bf16", "shard-match-emb", 0, 2, "l2", "frobenius"), ("fp8", "shard-match-emb", 2, 3, "cosine", "frobenius")])
+    ("bf16", "shard-match-emb", 0, 2, "l2", "frobenius"), ("fp8", "shard-match-emb", 2, 3, "cosine", "frobenius"),
+    ("bf16", "shard-match-emb", 1, 4, "l2", "mean_l2")])
 def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal):
     """Also: sharded matching (kvcomm_plan_match_shard) gives weights, verdicts and
     caches bit-identical to the unsharded run (dense and top-k weights; 3 ranks split
