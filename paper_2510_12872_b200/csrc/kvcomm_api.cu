@@ -1725,8 +1725,11 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
     hs.push_back(std::move(h));
   }
   // one table: [match part][realign part]
-  MatchLayout ML = items.empty() ? MatchLayout() : layout_match(items);
-  if (pl->world > 1 && !items.empty()) {  // layout fingerprint, compared across ranks by finalize
+  // Sharded plans always launch the distance kernel, even with no job (every match decided
+  // on the host): its fingerprint tells the peers this rank's layout differs from theirs.
+  const bool match_table = !items.empty() || pl->world > 1;
+  MatchLayout ML = match_table ? layout_match(items) : MatchLayout();
+  if (pl->world > 1) {  // layout fingerprint, compared across ranks by finalize
     uint64_t h = 1469598103934665603ull;
     auto mix = [&h](uint64_t v) {
       for (int b = 0; b < 8; ++b) {
@@ -1752,20 +1755,21 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
       ML.hdr.fp_dst[r] = reinterpret_cast<uint64_t*>(base + pl->fp_off[par]) + pl->rank;
     }
     ML.hdr.fp_mine = reinterpret_cast<const uint64_t*>(pl->xb() + pl->fp_off[par]);
+    ML.hdr.any_peer = 1;  // system-scope fence after the (peer) fingerprint stores
   }
   RealignLayout RL = layout_realign(pl->d, pl->Ls, pl->Hs, hs);
   const size_t roff = align_up(ML.bytes, 256);
   KV_TRY(entry_reserve(E, roff + RL.bytes));
   uint8_t* h = static_cast<uint8_t*>(E.host);
   uint8_t* dv = static_cast<uint8_t*>(E.dev);
-  if (!items.empty()) write_match(h, ML, items);
+  if (match_table) write_match(h, ML, items);
   const MatchResultDev* gres = items.empty() ? nullptr
                                              : reinterpret_cast<const MatchResultDev*>(dv + ML.hdr.res_off);
   if (!hs.empty()) write_realign(h + roff, dv + roff, RL, hs, gres);
   KV_CUDA(cudaMemcpyAsync(dv, h, hs.empty() ? ML.bytes : roff + size_t(RL.hdr.cs_off), cudaMemcpyHostToDevice, s));
-  if (!items.empty()) {
+  if (match_table) {
     KV_CUDA(launch_match_dist(dv, ML.hdr, ML.smem, s));
-    if (ML.hdr.total_blocks > 0) g_launches += 1;
+    g_launches += 1;
   }
   pl->pML = ML;
   pl->pRL = RL;

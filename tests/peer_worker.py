@@ -19,9 +19,11 @@ import torch.distributed as dist
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
-    shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch", "shard-match-emb")
+    shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch", "shard-match-emb",
+                                                          "shard-mismatch-empty")
+    empty_rank1 = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch-empty"
     emb_shard = len(sys.argv) > 2 and sys.argv[2] == "shard-match-emb"
-    mismatch = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch"
+    mismatch = len(sys.argv) > 2 and sys.argv[2] in ("shard-mismatch", "shard-mismatch-empty")
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
     scal = sys.argv[5] if len(sys.argv) > 5 else "frobenius"
@@ -49,18 +51,27 @@ def main():
               for i, a in enumerate(st.agents)]
     req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=top_k)
     if mismatch:   # the ranks' pools out of step: rank 1 lacks one user_question anchor
-        if rank == 1:
+        if rank == 1 and not empty_rank1:
             st.pools["user_question"].evict(0)
+        if rank == 1 and empty_rank1:   # every pool empty: rank 1 decides everything on the host
+            for pool in st.pools.values():
+                for slot in range(pool.capacity):
+                    if pool.slot_info(slot)["occupied"]:
+                        pool.evict(slot)
         req.shard_matching(rank, world, 0)
         for _ in range(2):
             req._mshard.run([st.queries[n] for n in req.names], sync=True)
             peer.sync()
         from paper_2510_12872_b200._lib import KVCommError
-        try:
-            req.plan.results()
-            raise AssertionError("out-of-step pools were not detected")
-        except KVCommError as e:
-            assert e.status_name == "SHAPE_MISMATCH" and "sharded matching" in str(e), e
+        if empty_rank1 and rank == 1:   # no job here: host verdicts, all agents fall back
+            ms, reused = req.plan.results()
+            assert not any(reused) and all(m.reason == "EMPTY_POOL" for m in ms), [m.reason for m in ms]
+        else:
+            try:
+                req.plan.results()
+                raise AssertionError("out-of-step pools were not detected")
+            except KVCommError as e:
+                assert e.status_name == "SHAPE_MISMATCH" and "sharded matching" in str(e), e
         checked = 0
         for i, a in enumerate(ref.agents):   # no agent was realigned: the caches stay zero
             fk, fv = peer.full(i)

@@ -44,13 +44,15 @@ def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal):
 
 
 @pytest.mark.gpu
-def test_sharded_matching_detects_out_of_step_pools():
-    """Ranks whose pools differ (rank 1 evicted an anchor) must not blend with each
-    other's weights: every job whose layout fingerprints differ is NewAnchor
-    (SHARD_MISMATCH), no agent is realigned, and results() raises SHAPE_MISMATCH."""
+@pytest.mark.parametrize("mode", ["shard-mismatch", "shard-mismatch-empty"])
+def test_sharded_matching_detects_out_of_step_pools(mode):
+    """Ranks whose pools differ (rank 1 evicted an anchor, or every anchor so that it has
+    no job at all) must not blend with each other's weights: every job whose layout
+    fingerprints differ is NewAnchor (SHARD_MISMATCH), no agent is realigned, and
+    results() raises SHAPE_MISMATCH (rank 1 with empty pools: host verdicts EMPTY_POOL)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
-           "bf16", "shard-mismatch", "0"]
+           "bf16", mode, "0"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "rank 0: 3 agents untouched, mismatch reported" in r.stdout, r.stdout
