@@ -93,7 +93,9 @@ def test_pool_create_rejects_bad_geometry_before_touching_a_device():
     inv = (C.c_double * 8)(*([1.0] * 8))
     h = C.c_void_p()
     for bad in [dict(head_dim=17), dict(head_dim=0), dict(emb_dim=12), dict(capacity=0),
-                dict(capacity=2048), dict(layer_end=3), dict(num_consumers=0)]:
+                dict(capacity=2048), dict(layer_end=3), dict(num_consumers=0),
+                dict(emb_shard_world=9), dict(emb_shard_rank=2, emb_shard_world=2),
+                dict(emb_shard_rank=-1, emb_shard_world=2), dict(emb_shard_rank=1)]:
         cfg = dict(device=0, num_layers=2, layer_begin=0, layer_end=2, num_kv_heads=2, head_begin=0,
                    head_end=2, head_dim=16, emb_dim=32, capacity=4, max_anchor_len=48, num_consumers=1)
         cfg.update(bad)

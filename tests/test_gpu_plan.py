@@ -112,3 +112,33 @@ def test_two_plans_sharing_pools_run_concurrently_on_two_streams():
     for (k, v), a in zip(ref2, agents2):
         if a.agent == 1:
             assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+
+
+def test_split_run_and_shard_argument_contracts():
+    """kvcomm_plan_run_begin/run_end pair up (begin twice, end without begin:
+    INVALID_ARGUMENT), begin+end equals run bit for bit, and kvcomm_plan_match_shard
+    validates rank/world before touching any peer."""
+    from paper_2510_12872_b200 import kvcomm as K
+    st = _small_state(seed=2, gamma=1.0)
+    plan, q = st.request.plan, [st.queries[n] for n in st.request.names]
+    plan.run(q, sync=True)
+    torch.cuda.synchronize()
+    ref = _snap(st)
+    for a in st.agents:
+        a.dst_k.fill_(0.5)
+        a.dst_v.fill_(0.5)
+    with pytest.raises(K.KVCommError, match="not begun"):
+        plan.run_end()
+    plan.run_begin(q)
+    with pytest.raises(K.KVCommError, match="already begun"):
+        plan.run_begin(q)
+    plan.run_end(sync=True)
+    for (k, v), a in zip(ref, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+    for rank, world in ((0, 9), (2, 2), (-1, 2)):
+        with pytest.raises(K.KVCommError, match="INVALID_ARGUMENT"):
+            plan.match_shard(rank, world, [b"\0" * 64] * max(world, 1) if world > 0 else [])
+    with pytest.raises(ValueError):
+        plan.match_shard(0, 2, [b"\0" * 64])     # one handle per rank
+    plan.match_shard(0, 1)                         # back to unsharded: runs still work
+    plan.run(q, sync=True)
