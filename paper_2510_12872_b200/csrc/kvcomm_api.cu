@@ -1261,6 +1261,10 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
     return fail(KVCOMM_ERR_NO_CANDIDATES, "segment %d: empty candidate set", idx);
   if (g.n_candidates > p->cap) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: n_candidates", idx);
   if (!g.weights) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "segment %d: null weights", idx);
+  // the per-tile weight blocks are indexed in 32 bits (realign_prep_kernel)
+  if ((int64_t(g.L_seg) + 2 * rows_per_tile(p->d)) * g.n_candidates * 2 >= (int64_t(1) << 31))
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: %d rows x %d anchors exceeds the weight table", idx,
+                g.L_seg, g.n_candidates);
   if (g.kind == KVCOMM_PREFIX) {
     if (g.L_seg != p->prefix_len[g.consumer])
       return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: prefix L_seg %d != prefix_len %d", idx, g.L_seg,

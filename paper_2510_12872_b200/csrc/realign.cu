@@ -118,12 +118,15 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
   if (g.n_cand == 0) return;
   const int rpu = unit_rows(hdr->d, g.fp8);
   const int rw = weight_row_stride(rpu);
-  const int64_t n = int64_t(g.tiles) * g.n_cand * rw;
-  for (int64_t x = blockIdx.y * blockDim.x + threadIdx.x; x < n; x += int64_t(gridDim.y) * blockDim.x) {
-    const int r = int(x % rw);
-    const int64_t tj = x / rw;
-    const int j = int(tj % g.n_cand);
-    const int row = int(tj / g.n_cand) * rpu + r;
+  // 32-bit index math (tiles * n_cand * rw < 2^31: at most 128 tiles x 1024 anchors x 260)
+  const uint32_t n = uint32_t(g.tiles) * uint32_t(g.n_cand) * uint32_t(rw);
+  const uint32_t urw = uint32_t(rw), unc = uint32_t(g.n_cand);
+  for (uint32_t x = blockIdx.y * blockDim.x + threadIdx.x; x < n; x += gridDim.y * blockDim.x) {
+    const uint32_t tj = x / urw;
+    const int r = int(x - tj * urw);
+    const uint32_t t = tj / unc;
+    const int j = int(tj - t * unc);
+    const int row = int(t) * rpu + r;
     const int slot = cand[g.cand_off + j];
     float w = 0.f;
     if (r < rpu && row < g.L_seg) w = g.w_by_slot ? g.w[int64_t(slot) * g.ld_w + row] : g.wbar[slot];
