@@ -15,7 +15,10 @@
 //     an fp8 block of e4m3 codes followed by their row scales) and finally the base
 //     tile(s) into a 9-deep shared-memory ring (9 measured 3 % faster than 11: fewer
 //     bytes in flight, less DRAM contention) with cp.async.bulk (UBLKCP) + mbarrier
-//     complete_tx, L2 evict-first;
+//     complete_tx, L2 evict-first for anchor tiles, evict-last for the weight blocks
+//     (re-read by every (layer, head, plane) unit of a tile) and for shared bases; the
+//     pool's slab pads 64 rows between slots so that consecutive anchors' tiles do not
+//     sit a power-of-two multiple apart (config 4: +3.5 %);
 //   * 8 consumer warps (16 for tables that read fp8 pools): each thread owns two
 //     32-byte "items" per 64-row tile (8 elements of the first half of a row and the
 //     matching 8 of the second half, so the rotate_half pair (f, f+d/2) sits in one
