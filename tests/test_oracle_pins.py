@@ -564,3 +564,21 @@ def test_measure_apply_round_trip_interleaved():
     k, v = O.apply_offset(kb, vb, dk, dv, 37, inv, O.INTERLEAVED)
     np.testing.assert_allclose(k, kr, rtol=0, atol=1e-12)
     np.testing.assert_allclose(v, vr, rtol=0, atol=1e-12)
+
+
+def test_bench_paper_context_matches_table2():
+    """bench.py's `paper_context` block restates Table 2 (tests/golden/table2_ttft.txt,
+    P:383-393): the per-agent KVComm rows, their sum, the derived tokens/s of the same
+    10,720-token request, and agent 5's TTFT and speedup."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(GOLDEN), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    ctx = bench.PAPER_CONTEXT
+    t = _load("table2_ttft.txt")
+    assert ctx["kvcomm_op_ms_per_agent"] == list(t[:, 2])
+    assert ctx["kvcomm_op_ms_per_request"] == pytest.approx(t[:, 2].sum())
+    assert ctx["derived_realigned_tokens_per_s"] == pytest.approx(10720 / (t[:, 2].sum() / 1e3), rel=1e-3)
+    assert ctx["ttft_ms_agent5_dense_vs_kvcomm"][0] == t[4, 1]
+    assert ctx["ttft_ms_agent5_dense_vs_kvcomm"][1] == pytest.approx(t[4, 2] + t[4, 3] + t[4, 4])
+    assert ctx["ttft_speedup_agent5"] == t[4, 5]
