@@ -44,7 +44,6 @@ def parse():
     ap.add_argument("--gamma", type=float, default=0.3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--offsets", default="bf16", choices=["bf16", "fp8"],
                     help="anchor offset storage; the headline line is bf16 (fp8 = SURVEY f3, lossy)")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
@@ -56,6 +55,13 @@ def parse():
     ap.add_argument("--emb-shard", action="store_true",
                     help="N>1 with sharded matching: each rank's pools hold only the embedding rows of the "
                          "position blocks it matches (1/N of them)")
+    ap.add_argument("--workload", default="8b-5agent", choices=["8b-5agent", "70b"],
+                    help="8b-5agent: BASELINE configs[1] (configs[2] at N>1, layer shards), the headline; "
+                         "70b: configs[3] (Llama-3-70B shape, one 3K-token segment, 256-anchor pool; its pool "
+                         "needs 240 GiB of offsets, so N >= 2; layer x KV-head grid at N = 8)")
+    ap.add_argument("--head-groups", type=int, default=0,
+                    help="N>1: KV-head groups of the layer x head shard grid (0 = auto: 2 for --workload 70b "
+                         "at N = 8 (SURVEY §8(e) 4 x 2), else 1)")
     ap.add_argument("--profile", action="store_true",
                     help="after warm-up run --steps steps between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -125,57 +131,105 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------- CPU oracle
+#
+# The oracle (oracle/kvcomm_oracle.py, float64 NumPy) as it stands, timed on the host's
+# cores over the same request the GPU arm runs: Eq. 5 (distances, weights, entropy,
+# verdict) per pool, then Eq. 6 / Eq. 7 + R_δ + add + bf16 rounding per (segment, layer,
+# KV head) block on a thread pool (NumPy releases the GIL inside its array loops; BLAS pools are
+# pinned to 1 thread, so `cores` = the pool's threads).  Inputs are regenerated from their
+# keyed seeds (synth.state.StateInputs) and copied to host memory BEFORE the clock starts;
+# the oracle widens the bf16 inputs to float64 itself, inside the timed region.
 
-def oracle_sample(st, n_tokens: int, rng_seed: int = 0):
-    """Host inputs for the oracle on a bounded sample of the workload: n_tokens
-    consecutive tokens of agent 1's user_question placeholder, all layers/heads of
-    this rank's shard, all 20 anchors (distances for those positions + Eq. 6 blend
-    + RoPE δ + add).  Inputs are regenerated from their keyed seeds (never read
-    back from the CUDA path)."""
-    inp = st.inputs
-    w = st.w
-    name = "user_question"
-    L_phi = w.pools[name].L_phi
-    i0 = 0
+
+def _bf16_bits(t: torch.Tensor) -> np.ndarray:
+    """Host bf16 tensor -> its uint16 bit patterns (zero copy)."""
+    return t.contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def _widen(bits: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns -> float64 (exact: bf16 is the top half of an fp32)."""
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def oracle_inputs(inp, w, agents, pools):
+    """Host copies (bf16 bits) of every input of the given agents' segments and pools."""
     vocab = inp.vocab()
-    q = vocab[inp.query_ids(name)][i0:i0 + n_tokens].double().cpu().numpy()
-    anchors = [vocab[inp.anchor_ids(name, s)][i0:i0 + n_tokens].double().cpu().numpy() for s in range(w.capacity)]
+    P = {}
+    for name in pools:
+        P[name] = {"q": _bf16_bits(vocab[inp.query_ids(name)].cpu()),
+                   "anchors": [_bf16_bits(vocab[inp.anchor_ids(name, s)].cpu()) for s in range(w.capacity)]}
     del vocab
-    dk = [inp.offset(name, s, 0, "ph", 0)[:, :, i0:i0 + n_tokens].double().cpu().numpy() for s in range(w.capacity)]
-    dv = [inp.offset(name, s, 0, "ph", 1)[:, :, i0:i0 + n_tokens].double().cpu().numpy() for s in range(w.capacity)]
-    bk = inp.base(name, 0)[:, :, i0:i0 + n_tokens].double().cpu().numpy()
-    bv = inp.base(name, 1)[:, :, i0:i0 + n_tokens].double().cpu().numpy()
-    target = w.agents[0].p0
-    return q, anchors, dk, dv, bk, bv, target, st.inv_freq
+    S = []
+    for a in w.agents:
+        if a.agent not in agents:
+            continue
+        for sg in a.segments:
+            if sg.kind == "p0" or sg.pool not in pools:
+                continue
+            kind = "ph" if sg.kind == "placeholder" else "pf"
+            if kind == "ph":
+                base = [_bf16_bits(inp.base(sg.pool, pl).cpu()) for pl in range(2)]
+            else:
+                base = [_bf16_bits(inp.prefix_base(sg.pool, sg.consumer, pl).cpu()) for pl in range(2)]
+            offs = [[_bf16_bits(inp.offset(sg.pool, s, sg.consumer, kind, pl)[:, :, :sg.length].cpu())
+                     for s in range(w.capacity)] for pl in range(2)]
+            S.append({"seg": sg, "kind": kind, "base": base, "offs": offs})
+    return P, S
 
 
-def oracle_run(sample):
-    """The oracle as it stands, pinned to one host thread (any BLAS pool NumPy may use is
-    limited to 1 thread, so `cores: 1` is what actually ran)."""
+def oracle_request(P, S, inv, gamma, threads):
+    """One timed pass of the oracle over pools P and segments S; returns (seconds, tokens)."""
+    from concurrent.futures import ThreadPoolExecutor
     from threadpoolctl import threadpool_limits
     from oracle import kvcomm_oracle as O
-    q, anchors, dk, dv, bk, bv, target, inv = sample
-    with threadpool_limits(limits=1):
-        dist = O.distances(q, anchors)
-        W, _ = O.position_weights(dist)
-        return O.realign_segment(W, bk, bv, dk, dv, 0, target, inv)
+
+    def match(name):
+        p = P[name]
+        embs = {s: _widen(a) for s, a in enumerate(p["anchors"])}
+        return O.predict(_widen(p["q"]), {s: e.shape[0] for s, e in embs.items()}, embs,
+                         {s: True for s in embs}, gamma)
+
+    def realign(job, m, l, h):
+        sg = job["seg"]
+        wts = m.W if job["kind"] == "ph" else m.wbar
+        dk = [_widen(job["offs"][0][s][l, h]) for s in m.candidates]
+        dv = [_widen(job["offs"][1][s][l, h]) for s in m.candidates]
+        O.realign_segment(wts, _widen(job["base"][0][l, h]), _widen(job["base"][1][l, h]), dk, dv,
+                          sg.base_start, sg.target_start, inv,
+                          kind="placeholder" if job["kind"] == "ph" else "prefix")
+
+    with threadpool_limits(limits=1), ThreadPoolExecutor(max_workers=threads) as ex:
+        t0 = time.perf_counter()
+        ms = dict(zip(P, ex.map(match, list(P))))
+        futs = [ex.submit(realign, job, ms[job["seg"].pool], l, h) for job in S
+                for l in range(job["base"][0].shape[0]) for h in range(job["base"][0].shape[1])]
+        for f in futs:
+            f.result()
+        dt = time.perf_counter() - t0
+    if any(m.verdict != O.SHAREABLE for m in ms.values()):
+        raise SystemExit("oracle: a pool of the bench request is NewAnchor")
+    return dt, sum(job["seg"].length for job in S)
 
 
-def cpu_baseline(st, budget_s: float):
-    n = 4
-    sample = oracle_sample(st, n)
-    t0 = time.perf_counter()
-    oracle_run(sample)
-    per_tok = (time.perf_counter() - t0) / n
-    n = max(4, min(st.w.pools["user_question"].L_phi, int(budget_s / max(per_tok, 1e-6))))
-    sample = oracle_sample(st, n)
-    t0 = time.perf_counter()
-    oracle_run(sample)
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n} tokens of agent 1's 1024-token user_question placeholder, all "
-                      f"{st.inputs.Ls}x{st.w.H} layer/head rows, 20 anchors: distances + Eq.6 weights + "
-                      f"blend + RoPE-delta + add, float64 NumPy single thread ({dt:.1f} s)",
+def cpu_baseline(st, gamma):
+    """The whole config-2 request on every host core, plus agent 1 alone on one core."""
+    w, inp = st.w, st.inputs
+    threads = os.cpu_count() or 1
+    P, S = oracle_inputs(inp, w, {a.agent for a in w.agents}, list(w.pools))
+    n_seg = len(S)
+    dt, toks = oracle_request(P, S, st.inv_freq, gamma, threads)
+    del P, S
+    P1, S1 = oracle_inputs(inp, w, {1}, list(w.pools)[:1])
+    dt1, toks1 = oracle_request(P1, S1, st.inv_freq, gamma, 1)
+    return {"value": toks / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"the whole request ({toks} realigned tokens: {len(w.pools)} pool matches + {n_seg} segments x "
+                      f"{inp.Ls} layers x {inp.Hs} heads, {w.capacity} anchors; distances, Eq. 5/6/7 weights, blend, "
+                      f"RoPE-delta, "
+                      f"add, bf16 rounding), float64 NumPy on {threads} threads over (segment, layer, head) blocks "
+                      f"({dt:.1f} s)",
+            "single_thread": {"value": toks1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"agent 1 alone ({toks1} tokens: the user_question match + its placeholder "
+                                        f"and prefix), one thread ({dt1:.1f} s)"},
             "cpu": _cpu_model()}
 
 
@@ -204,63 +258,105 @@ PAPER_CONTEXT = {
 }
 
 
+def verdict_summary(res, args):
+    """Eq. 5 per pool on the timed request: entropy H, threshold γ log|𝒜_φ| and the
+    margin threshold - H (> 0: Shareable).  The verdicts depend on reading A4 (the
+    sample-level distance behind w̄): under SPEC's mean-ℓ2 reading no sample
+    of this workload passes at γ = 0.3 (tests/test_oracle_pins.py::
+    test_config2_verdicts_under_both_scalar_distance_readings)."""
+    pools = {}
+    for name, m in res.matches.items():
+        pools[name] = {"verdict": "Shareable" if m.shareable else f"NewAnchor ({m.reason})",
+                       "n_candidates": len(m.candidates), "H": m.entropy, "threshold": m.threshold,
+                       "margin": m.threshold - m.entropy}
+    return {"scalar_distance": "frobenius (reading A4)", "gamma": args.gamma, "pools": pools}
+
+
+def make_workload(args):
+    import synth
+    return synth.five_agent_workload() if args.workload == "8b-5agent" else synth.shared_segment_workload()
+
+
+WORKLOAD_TEXT = {
+    "8b-5agent": "llama3-8b-shape (32 layers, 8 KV heads x 128) 5-agent fully-connected, 1K input / 512 prefix / "
+                 "512 output (PAPER Table 2), 20-anchor pools",
+    "70b": "llama3-70b-shape (80 layers, 8 KV heads x 128, D_e 8192), one 3072-token shared segment + 32-token "
+           "prefix + 200-token p0 for one consumer, 256-anchor pool, k = 256 (BASELINE configs[3])",
+}
+
+
+def head_groups(args, world):
+    if args.head_groups:
+        return args.head_groups
+    return 2 if args.workload == "70b" and world == 8 else 1
+
+
 def arm_config(args, world, w):
     """The `config` object both arms print (same workload, metric and unit)."""
-    return {"workload": "llama3-8b-shape (32 layers, 8 KV heads x 128) 5-agent fully-connected, "
-                        "1K input / 512 prefix / 512 output (PAPER Table 2), 20-anchor pools",
+    hg = head_groups(args, world)
+    grid = f"layer-shard x{world}" if hg == 1 else f"layer x KV-head grid {world // hg} x {hg}"
+    return {"workload": WORKLOAD_TEXT[args.workload],
             "realigned_tokens_per_step": w.realigned_tokens, "anchors_blended": w.capacity,
             "gamma": args.gamma, "offset_storage": args.offsets,
-            "parallelism": (f"layer-shard x{world}, {args.gather} gather, {args.match} matching"
+            "parallelism": (f"{grid}, {args.gather} gather, {args.match} matching"
                             + (", sharded embeddings" if args.emb_shard and args.match == "sharded" else "")
                             if world > 1 else "single"),
-            "l2": "step streams ~32 GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
+            "l2": "each step streams tens of GB >> 126 MB L2 (no flush needed)", "seed": args.seed}
 
 
 # ---------------------------------------------------------------------- reference arm
 
 def run_reference(args):
+    """The reference arm is the oracle (tier framing: the paper ships no code).  Each step
+    is one bounded sample of the same request, rotating over its 15 (placeholder, prefix)
+    segment pairs: the pair's pool matched (Eq. 5), both segments realigned at full depth
+    (all layers and heads) on every host core.  Inputs: the GPU arm's keyed recipe (same
+    seed, workload and shapes), generated before each step's clock starts."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.workload != "8b-5agent":
+        print(json.dumps({"impl": "reference", "unavailable": "the float64 oracle needs about 1.5 core-hours per "
+                                                              "70b request (3072 tokens x 256 anchors x 80x8 rows); "
+                                                              "its arm runs the 8b-5agent workload"}))
+        return
     import synth
     from synth.state import StateInputs
-    from oracle import kvcomm_oracle as O
-    w = synth.five_agent_workload()
-
-    # The reference arm is the CPU oracle.  Inputs are generated on the host with the
-    # same keyed recipe at a bounded per-step sample: T tokens of agent 1's
-    # user_question placeholder, all 32x8 layer/head rows, 20 anchors.
-    T = 16
-    g = synth.make_gen(args.seed)
-    table = synth.vocab_table(4096, w.D_e, g)
-    ids = [torch.randint(0, 4096, (T,), generator=g) for _ in range(w.capacity)]
-    anchors = [table[i].double().numpy() for i in ids]
-    q = table[synth.query_token_ids(ids[0], T, 4096, g)].double().numpy()
-    dk = [synth.randn_bf16((w.L, w.H, T, w.d), g, synth.OFFSET_STD).double().numpy() for _ in range(w.capacity)]
-    dv = [synth.randn_bf16((w.L, w.H, T, w.d), g, synth.OFFSET_STD).double().numpy() for _ in range(w.capacity)]
-    bk = synth.randn_bf16((w.L, w.H, T, w.d), g).double().numpy()
-    bv = synth.randn_bf16((w.L, w.H, T, w.d), g).double().numpy()
+    w = make_workload(args)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"   # where the inputs are drawn (not timed)
+    inp = StateInputs(w, args.seed, (0, w.L), dev)
     inv = synth.llama3_inv_freq(w.d)
-    sample = (q, anchors, dk, dv, bk, bv, w.agents[0].p0, inv)
-    for _ in range(args.warmup):
-        oracle_run(sample)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle_run(sample)
-        times.append(time.perf_counter() - t0)
-    dt = sum(times) / len(times)
-    v = T / dt
+    pairs = []
+    for a in w.agents:
+        for sg in a.segments:
+            if sg.kind == "placeholder":
+                pairs.append((a.agent, sg.pool))
+    threads = os.cpu_count() or 1
+
+    def step(t):
+        agent, pool = pairs[t % len(pairs)]
+        P, S = oracle_inputs(inp, w, {agent}, [pool])
+        S = [j for j in S if j["seg"].pool == pool]
+        return oracle_request(P, S, inv, args.gamma, threads)
+
+    for t in range(args.warmup):
+        step(t)
+    times, toks = [], 0
+    for t in range(args.steps):
+        dt, n = step(args.warmup + t)
+        times.append(dt)
+        toks += n
+    v = toks / sum(times)
+    cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": f"each step: one (placeholder, prefix) segment pair of the request, rotating over its 15 pairs "
+                     f"(the pool's Eq. 5 match + both segments at full depth, 32x8 layer/head rows, 20 anchors), "
+                     f"float64 NumPy on {threads} threads; inputs drawn on {dev} with the GPU arm's keyed recipe",
+           "cpu": _cpu_model()}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": arm_config(args, args.gpus, w),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step: {T} tokens of agent 1's user_question placeholder x 32x8 layer/head "
-                                   f"rows x 20 anchors (distances, Eq. 5/6 weights, blend, RoPE-delta, add), "
-                                   f"float64 NumPy; value = sampled tokens / step time",
-                         "cpu": _cpu_model()},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": arm_config(args, args.gpus, w), "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -438,15 +534,27 @@ def main():
     import paper_2510_12872_b200 as kv
     from paper_2510_12872_b200 import shard
 
-    w = synth.five_agent_workload()
-    lr = shard.layer_shard(w.L, rank, world)
+    w = make_workload(args)
+    hg = head_groups(args, world)
+    if world % hg:
+        raise SystemExit(f"--head-groups {hg} does not divide N={world}")
+    lr, hr = shard.grid_shard(w.L, w.H, rank, world // hg, hg)
+    Hs = hr[1] - hr[0]
+    need = w.capacity * sum(p.L_phi * len(p.consumers) for p in w.pools.values()) * w.token_bytes / world
+    if args.workload == "70b" and need > 170e9:
+        if rank == 0:   # configs[3] is an 8-GPU configuration: say so instead of OOM-ing
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                              "config": arm_config(args, world, w),
+                              "skipped": f"the 256-anchor pool holds {need / 2**30:.0f} GiB of offsets per GPU at "
+                                         f"N={world} (> 178 GiB of HBM); run with --gpus >= 2 (8 in BASELINE)"}))
+        return
     emb_shard = (rank, world) if world > 1 and args.match == "sharded" and args.emb_shard else None
     st = build_five_agent_state(w, seed=args.seed, device=local, gamma=args.gamma, layer_range=lr,
-                                offset_format=args.offsets, emb_shard=emb_shard)
+                                offset_format=args.offsets, emb_shard=emb_shard, head_range=hr)
     req = st.request
     stream = torch.cuda.current_stream()
     Ls = lr[1] - lr[0]
-    row_bytes = w.H * w.d * 2  # one token of one plane over the shard's heads, per layer
+    row_bytes = Hs * w.d * 2  # one token of one plane over the shard's heads, per layer
 
     # full-depth caches of the agents this rank hosts (N>1).  fused: allocated by the
     # consumer rank, IPC-mapped everywhere, and used directly as the realign destinations
@@ -462,7 +570,7 @@ def main():
             print(f"[bench] {e}; using the NCCL gather", file=sys.stderr, flush=True)
             args.gather = "nccl (ipc unavailable)"
     if peer is not None:
-        agents_f = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr))
+        agents_f = [AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, a.segments, *peer.destinations(i, lr, hr))
                     for i, a in enumerate(st.agents)]
         req = ReuseRequest(st.pools, agents_f, gamma=req.gamma, top_k=req.top_k)
         full = [peer.full(i) for i in range(len(st.agents))]
@@ -490,7 +598,8 @@ def main():
         if peer is not None:
             peer.sync()
         elif world > 1:
-            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world)
+            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world,
+                                      head_groups=hg)
 
     # With sharded matching and the fused gather, the cross-rank barrier inside step t+1
     # (after every rank's distance kernel, hence after its realign of step t) already
@@ -529,7 +638,7 @@ def main():
             uniq_base[sg.base_k.data_ptr()] = sg.base_k.shape[2]
     base_tokens = sum(uniq_base.values())
     # an offset row is d bf16 values, or (fp8 pools) d e4m3 codes + one fp32 scale
-    off_row = row_bytes if args.offsets == "bf16" else w.H * (w.d + 4)
+    off_row = row_bytes if args.offsets == "bf16" else Hs * (w.d + 4)
     alg_bytes = (res.blended_rows * off_row + (res.realigned_tokens + base_tokens + 2 * res.copied_tokens) * row_bytes
                  ) * Ls * 2
 
@@ -585,8 +694,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(st, args.cpu_budget_s)
+        cpu = cpu_baseline(st, args.gamma)
 
+    n_segs = sum(1 for a in st.agents for _ in a.segments)
+    n_copy = sum(1 for a in st.agents if a.p0_k.shape[2] > 0)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -594,24 +705,27 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16" if args.offsets == "bf16" else "bf16 (fp8-e4m3 offsets)",
             "data": "synthetic",
             "config": {**arm_config(args, world, w), **({"test_same_gpu_gloo": True} if same_gpu else {})},
-            "roofline": {"kernel": "kvc::realign_kernel (30 segments + 5 p0 copies, one launch)", "bound": "hbm",
+            "roofline": {"kernel": f"kvc::realign_kernel ({n_segs} segments + {n_copy} p0 copies, one launch)",
+                         "bound": "hbm",
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
                          "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,
                          "realign_share_of_step": realign_avg / ms_per_step,
                          "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "
-                                        "base once + 2 per copied p0 token, x 128 KiB",
+                                        f"base once + 2 per copied p0 token, x {row_bytes * Ls * 2 // 1024} KiB "
+                                        "(K+V of this rank's layers and heads)",
                          **({"peer_bytes_per_launch": peer_bytes, "peer_ref_gbs": 770.0,
                              "peer_bound_ms": peer_bytes / 770e9 * 1e3,
                              "peer_note": "fused gather: rows this rank stores into consumer GPUs over NVLink; "
                                           "ref = measured peer copy per direction (B200_PROFILING.md)"}
                             if peer is not None else {})},
+            "verdicts": verdict_summary(res, args),
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": int(n_launch),
             "cpu_baseline": cpu,
-            "paper_context": PAPER_CONTEXT,
+            "paper_context": PAPER_CONTEXT if args.workload == "8b-5agent" else None,
         }
         print(json.dumps(out))
     if world > 1:

@@ -208,6 +208,13 @@ typedef struct {
   int64_t dst_ld;          /* prompt length N of the consumer                             */
   float* debug_delta_k;    /* optional device fp32 [Ls,Hs,L_seg,d]: Σ_j w_j ΔK_j (parity) */
   float* debug_delta_v;
+  int32_t dst_heads;       /* heads per layer of the destination layout; 0 = the pool's Hs.
+                              Element (l, h, row) of this shard lands at
+                              dst + ((l*dst_heads + h)*dst_ld + row)*d, so a KV-head shard
+                              (pool head_range [h0,h1)) writes straight into a consumer's full
+                              [L][H][N][d] cache: dst = cache + ((l0*H + h0)*N)*d, dst_heads = H
+                              (SURVEY §8(e) 70B layer x KV-head grid).  SHAPE_MISMATCH if < Hs. */
+  int32_t _pad;
 } kvcomm_realign_desc;
 
 /* A segment of the consumer's prompt for the concatenation ledger (step a6).
@@ -405,8 +412,9 @@ typedef struct {
 
 typedef struct {
   int32_t N;               /* prompt length                                              */
-  int32_t _pad;
-  void* dst_k;             /* device bf16 [Ls,Hs,dst_ld,d]                               */
+  int32_t dst_heads;       /* heads per layer of the destination layout, 0 = the pools' Hs
+                              (kvcomm_realign_desc.dst_heads: head shards of a full cache) */
+  void* dst_k;             /* device bf16 [Ls,dst_heads,dst_ld,d] (this shard's block)   */
   void* dst_v;
   int64_t dst_ld;
 } kvcomm_plan_agent;

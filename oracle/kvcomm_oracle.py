@@ -266,7 +266,8 @@ def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int,
     """Eq. 5:  NewAnchor ⇔ (L_φ > max_{ψ∈𝒜} L_ψ) ∪ (H_{φ|𝒜} > γ log|𝒜_φ|).
 
     Readings: the max runs over the whole pool (A7); an empty pool or an empty 𝒜_φ
-    is NewAnchor (A19); |𝒜_φ| = 1 gives H = 0 = threshold → Shareable.
+    is NewAnchor (A19); |𝒜_φ| = 1 gives H = 0 = threshold → Shareable for γ > 0;
+    γ = 0 is the no-sharing method of Table 6 → always NewAnchor (A19).
     Weights for Eq. 6/7 are returned alongside (Alg. 1).
     """
     if not (0.0 <= gamma <= 1.0):
@@ -292,7 +293,9 @@ def predict(h_phi: np.ndarray, anchor_len: Dict[int, int], anchor_emb: Dict[int,
         raise ValueError(similarity)
     H = entropy(wbar)
     thr = gamma * math.log(len(cand))
-    verdict = NEW_ANCHOR if H > thr else SHAREABLE
+    # γ = 0 "refers to the original no-cache-sharing method" (Table 6; reading A19):
+    # NewAnchor even for |𝒜_φ| = 1, where Eq. 5 alone gives H = 0 = threshold
+    verdict = NEW_ANCHOR if (H > thr or gamma == 0.0) else SHAREABLE
     return MatchResult(verdict, R_HIGH_ENTROPY if verdict == NEW_ANCHOR else R_OK, cand,
                        W, idx, dist, dbar, wbar, H, thr)
 

@@ -69,7 +69,8 @@ class RealignDesc(C.Structure):
                 ("ld_w", C.c_int64), ("candidates", C.POINTER(C.c_int32)), ("n_candidates", C.c_int32),
                 ("L_seg", C.c_int32), ("base", KVView), ("base_start", C.c_int32), ("target_start", C.c_int32),
                 ("dst_k", C.c_void_p), ("dst_v", C.c_void_p), ("dst_ld", C.c_int64),
-                ("debug_delta_k", C.c_void_p), ("debug_delta_v", C.c_void_p)]
+                ("debug_delta_k", C.c_void_p), ("debug_delta_v", C.c_void_p), ("dst_heads", C.c_int32),
+                ("_pad", C.c_int32)]
 
 
 class MatchRequest(C.Structure):
@@ -90,7 +91,7 @@ class PlanSegment(C.Structure):
 
 
 class PlanAgent(C.Structure):
-    _fields_ = [("N", C.c_int32), ("_pad", C.c_int32), ("dst_k", C.c_void_p), ("dst_v", C.c_void_p),
+    _fields_ = [("N", C.c_int32), ("dst_heads", C.c_int32), ("dst_k", C.c_void_p), ("dst_v", C.c_void_p),
                 ("dst_ld", C.c_int64)]
 
 

@@ -694,6 +694,9 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_save(kvcomm_pool_t p, const char* pa
   std::shared_lock<std::shared_mutex> lk(p->mu);
   DeviceGuard guard(p->cfg.device);
   KV_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));  // prior inserts on `stream` land first
+  // ... and those issued on any other stream of the pool's device (a checkpoint must never
+  // capture half-written embedding or offset rows)
+  KV_CUDA(cudaDeviceSynchronize());
   File F;
   F.f = fopen(path, "wb");
   if (!F.f) return fail(KVCOMM_ERR_IO, "cannot create %s", path);
@@ -770,6 +773,21 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_load(const char* path, int32_t devic
       return bail(st);
     m.occupied = occ != 0;
     if (m.occupied && (m.length < 1 || m.length > p->maxlen)) return bail(fail(KVCOMM_ERR_IO, "%s: corrupt slot", path));
+  }
+  {  // the LFU metadata must describe a pool this library could have produced (reading A17's
+     // tie-break runs on insertion indices): unique indices below the counter, masks < 2^C
+    const uint64_t cmask = p->C >= 64 ? ~0ull : (1ull << p->C) - 1;
+    std::vector<int64_t> seen;
+    for (const SlotMeta& m : p->slots) {
+      if (!m.occupied) continue;
+      if (m.inserted < 0 || m.inserted >= p->next_index || m.access < 0 || (m.ph_mask & ~cmask) ||
+          (m.pf_mask & ~cmask))
+        return bail(fail(KVCOMM_ERR_IO, "%s: corrupt slot metadata", path));
+      seen.push_back(m.inserted);
+    }
+    std::sort(seen.begin(), seen.end());
+    if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+      return bail(fail(KVCOMM_ERR_IO, "%s: two slots share an insertion index", path));
   }
   {
     DeviceGuard guard(device);
@@ -1254,6 +1272,8 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
   if (g.target_start < 0 || int64_t(g.target_start) + g.L_seg > g.dst_ld)
     return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: rows [%d,%d) outside dst_ld %lld", idx, g.target_start,
                 g.target_start + g.L_seg, (long long)g.dst_ld);
+  if (g.dst_heads != 0 && (g.dst_heads < p->Hs || g.dst_heads > 1 << 20))
+    return fail(KVCOMM_ERR_SHAPE_MISMATCH, "segment %d: dst_heads %d < the pool's %d heads", idx, g.dst_heads, p->Hs);
   if (g.kind == KVCOMM_COPY) return KVCOMM_OK;
   if (g.consumer < 0 || g.consumer >= p->C)
     return fail(KVCOMM_ERR_NOT_FOUND, "segment %d: consumer %d outside [0,%d)", idx, g.consumer, p->C);
@@ -1324,6 +1344,7 @@ static HostSeg host_segment(const kvcomm_realign_desc& g, int32_t dst_stg = -1) 
   x.dst[0] = static_cast<bf16*>(g.dst_k);
   x.dst[1] = static_cast<bf16*>(g.dst_v);
   x.dst_ld = g.dst_ld;
+  x.dst_heads = g.dst_heads > 0 ? g.dst_heads : p->Hs;
   x.dst_stg = dst_stg >= 0 ? dst_stg : dst_store_mode(g.dst_k, p->cfg.device);
   x.rope_il = p->cfg.rope_layout == KVCOMM_ROPE_INTERLEAVED;
   x.inv_freq = p->inv_freq_dev;
@@ -1464,6 +1485,7 @@ KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* s
     x.dst[0] = static_cast<bf16*>(dst_k);
     x.dst[1] = static_cast<bf16*>(dst_v);
     x.dst_ld = dst_ld;
+    x.dst_heads = Hs;
     x.dst_stg = stg;
     x.L_seg = segs[i].length;
     x.target_start = segs[i].start;
@@ -1579,6 +1601,9 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
     if (s.L_seg > 0) KV_TRY(check_view(s.base, s.L_seg, "plan segment base"));
     if (!a.dst_k || !a.dst_v || !aligned16(a.dst_k) || !aligned16(a.dst_v) || a.dst_ld < a.N)
       return fail(KVCOMM_ERR_INVALID_ARGUMENT, "agent %d: bad destination", s.agent);
+    if (a.dst_heads != 0 && (a.dst_heads < p0->Hs || a.dst_heads > 1 << 20))
+      return fail(KVCOMM_ERR_SHAPE_MISMATCH, "agent %d: dst_heads %d < the pools' %d heads", s.agent, a.dst_heads,
+                  p0->Hs);
     ledger[s.agent].push_back({s.target_start, s.L_seg});
   }
   for (int a = 0; a < n_agents; ++a) {  // every prompt must be tiled exactly (reading A20 + P:304)
@@ -1662,6 +1687,9 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
   const int par = pl->next;
   RingEntry& E = pl->tab[par];
   KV_TRY(entry_reserve(E, 0));  // waits for the run that used this table two runs ago
+  // job_of / infos are rebuilt below; until this run completes there is no result to report
+  // (a failure part-way must not leave plan_results reading the old table through new jobs)
+  pl->last = -1;
   // a1 on the host; jobs for the entropy clause
   std::vector<MatchItem> items;
   std::vector<bool> host_new(nm, false);
@@ -1716,6 +1744,7 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
     d.dst_k = a.dst_k;
     d.dst_v = a.dst_v;
     d.dst_ld = a.dst_ld;
+    d.dst_heads = a.dst_heads;
     if (g.kind != KVCOMM_COPY) {
       const kvcomm_match_info* info = &pl->infos[g.match];
       d.weights = g.kind == KVCOMM_PLACEHOLDER ? pl->W(par, g.match) : pl->wbar(par, g.match);
@@ -1748,8 +1777,15 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
       mix(uint64_t(it.p->cap) << 32 | uint32_t(it.L_phi));
       mix(uint64_t(it.top_k) << 32 | gb);
       mix(uint64_t(it.p->cfg.scalar_distance) << 32 | uint32_t(it.p->cfg.similarity));
-      mix(uint64_t(it.info->n_candidates));
-      for (int j = 0; j < it.info->n_candidates; ++j) mix(uint64_t(uint32_t(it.info->candidates[j])));
+      mix(uint64_t(it.info->n_candidates) << 32 | uint32_t(it.p->emb_world));
+      // which anchor occupies each candidate slot: once a pool is full every insert reuses an
+      // evicted slot id, so the ids alone would not tell two ranks' different anchors apart
+      // (a missed or reordered insert, or LFU counts that diverged and evicted other victims)
+      for (int j = 0; j < it.info->n_candidates; ++j) {
+        const SlotMeta& sm = it.p->slots[it.info->candidates[j]];
+        mix(uint64_t(uint32_t(it.info->candidates[j])) << 32 | uint32_t(sm.length));
+        mix(uint64_t(sm.inserted));
+      }
     }
     ML.hdr.fingerprint = h;
     ML.hdr.shard_rank = pl->rank;

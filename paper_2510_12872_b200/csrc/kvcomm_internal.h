@@ -34,7 +34,7 @@ __host__ __device__ constexpr int weight_row_stride(int rows) { return (rows + 3
 // One segment of a realign batch, as the kernels see it (device resident).
 struct SegDev {
   const bf16* base[2];  // K, V base rows, [Ls][Hs][base_ld][d]
-  bf16* dst[2];         // destination [Ls][Hs][dst_ld][d]
+  bf16* dst[2];         // destination rows: (l, h, row) at ((l*dst_heads + h)*dst_ld + row)*d
   float* dbg[2];        // optional fp32 blended offsets [Ls][Hs][L_seg][d]
   const float* w;       // PLACEHOLDER: W rows by slot, row r at w + r*ld_w (w_by_slot = 1)
   const float* wt;      // weight blocks [tiles][n_cand][weight_row_stride(unit rows)] (prep kernel)
@@ -61,6 +61,9 @@ struct SegDev {
   int32_t dst_stg;      // 1: write rows with per-thread stores (destination on a peer GPU, mapped by
                         //   CUDA IPC: the fused gather of SURVEY §8(e)), 0: TMA bulk store
   int32_t rope_il;      // K's RoPE pairs: 0 (f, f + d/2) rotate_half, 1 (2f, 2f + 1) interleaved
+  int32_t dst_heads;    // heads per layer of the destination layout (>= Hs): a head shard writes its
+                        //   [Ls][Hs] block into a consumer's full [L][H][N][d] cache (70B grid, §9)
+  int32_t _pad_dst;
 };
 
 struct MatchResultDev {

@@ -392,7 +392,9 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
     for (int r = 0; r < hdr->shard_world && hdr->shard_world > 1; ++r) mismatch |= hdr->fp_mine[r] != hdr->fingerprint;
     res->entropy = H;
     res->threshold = thr;
-    res->verdict = (H > thr || mismatch) ? 1 : 0;
+    // γ = 0 is "the original no-cache-sharing method" (Table 6; reading A19): NewAnchor
+    // even when |𝒜_φ| = 1 makes H = 0 = threshold
+    res->verdict = (H > thr || a.gamma == 0.0 || mismatch) ? 1 : 0;
     res->shard_mismatch = mismatch;
     res->tie_flag = (a.n_cand > 1 && fabs(H - thr) <= kTieRel * thr) ? 1 : 0;  // |𝒜|=1: H = 0 = thr exactly
     res->tie_count = ties[blockIdx.x];

@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include "kvcomm_internal.h"
 #include "ptx.cuh"
@@ -121,7 +122,10 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
   if (g.n_cand == 0) return;
   const int rpu = unit_rows(hdr->d, g.fp8);
   const int rw = weight_row_stride(rpu);
-  // 32-bit index math (tiles * n_cand * rw < 2^31: at most 128 tiles x 1024 anchors x 260)
+  // 32-bit index math: with rpu >= 4 rows per unit (rpu <= 2 * rows_per_tile), tiles * rw <=
+  // (L_seg / rpu + 1) * (rpu + 3) < 2 * (L_seg + 2 * rows_per_tile), and validate_segment
+  // (kvcomm_api.cu) rejects any segment with (L_seg + 2 * rows_per_tile) * n_cand * 2 >= 2^31
+  // before a launch, so tiles * n_cand * rw < 2^31
   const uint32_t n = uint32_t(g.tiles) * uint32_t(g.n_cand) * uint32_t(rw);
   const uint32_t urw = uint32_t(rw), unc = uint32_t(g.n_cand);
   for (uint32_t x = blockIdx.y * blockDim.x + threadIdx.x; x < n; x += gridDim.y * blockDim.x) {
@@ -177,9 +181,12 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
     }
 }
 
-// variant (probe knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores instead
-// of the TMA bulk store; bit1 = skip output stores; bit5 = skip the anchor math
-// (bit1/bit5: bandwidth probes only, wrong results).
+// variant (measurement knob, KVCOMM_REALIGN_VARIANT): bit0 = per-thread STG.cs stores
+// instead of the TMA bulk store; bits 2/3 = L2 policy of shared bases; bit8 = generic-d
+// kernel — all of them give the same results.  Bandwidth probes that give WRONG results
+// (bit1 = skip the output stores, bit5 = skip the anchor math) exist only in probe builds
+// (make EXTRA=-DKVC_PROBE_VARIANTS=1 OUT=<dir>/libkvcomm.so OBJDIR=<dir>/obj); the product
+// library compiles them out, so no environment variable can make it write wrong caches.
 // Stage release: every consumer thread arrives on the empty barrier itself after its own
 // shared-memory reads (same speed as a warp-elected arrive after __syncwarp, and the
 // ordering is then visible to compute-sanitizer racecheck, which does not model the
@@ -194,7 +201,11 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
 #ifndef KVC_WARP_ARRIVE
 #define KVC_WARP_ARRIVE 0
 #endif
-constexpr int kArrivals = KVC_WARP_ARRIVE ? 1 : 32;  // empty-barrier arrivals per consumer warp
+constexpr int kArrivals = KVC_WARP_ARRIVE ? 1 : 32;
+#ifndef KVC_PROBE_VARIANTS
+#define KVC_PROBE_VARIANTS 0
+#endif
+constexpr bool kProbeVariants = KVC_PROBE_VARIANTS != 0;  // empty-barrier arrivals per consumer warp
 __device__ __forceinline__ void stage_release(uint64_t* b) {
 #if KVC_WARP_ARRIVE
   __syncwarp();
@@ -243,7 +254,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const int fblk = fp8_block_bytes(d);
   const int64_t total = hdr.total_units;
   const int row_bytes = 2 * d;
-  const bool tma_store = !(variant & 3);
+  const bool skip_store = kProbeVariants && (variant & 2);  // probe builds only
+  const bool skip_math = kProbeVariants && (variant & 32);   // probe builds only
+  const bool tma_store = !(variant & 1) && !skip_store;
 
   if (warp == kConsumerWarps) {
     // ---------------- TMA producer (one lane) ----------------
@@ -357,7 +370,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const bool rotate = un.p == 0 && g.delta != 0;
     const bool rope_il = g.rope_il;
     const float2* csg = cs + g.cs_off;
-    bf16* const dst = g.dst[un.p] + (lh * g.dst_ld + g.target_start + i0) * d;
+    bf16* const dst = g.dst[un.p] + ((int64_t(un.l) * g.dst_heads + un.h) * g.dst_ld + g.target_start + i0) * d;
     const bool tstore = tma_store && !g.dst_stg;  // peer destinations: per-thread stores
     float* const dbg = g.dbg[un.p] != nullptr ? g.dbg[un.p] + (lh * g.L_seg + i0) * d : nullptr;
     float acc[2][kItemsPerThread][16];  // [64-row tile of the unit][item][element]
@@ -389,7 +402,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
                                     roff);
           stage_release(&empty[stage]);
           if (++stage == kNStage) { stage = 0; phase ^= 1u; }
-          if (!(variant & 32)) {
+          if (!skip_math) {
             fp8_accum<kItemsPerThread>(acc, w0, code0);
             fp8_accum<kItemsPerThread>(acc, w1, code1);
           }
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           uint4 code[2][kItemsPerThread];
           fp8_load<kItemsPerThread>(w, code, buf, reinterpret_cast<const uint8_t*>(wv), buf + scale_off, coff, roff);
           stage_release(&empty[stage]);  // this thread's reads of the stage are done
-          if (!(variant & 32)) fp8_accum<kItemsPerThread>(acc, w, code);
+          if (!skip_math) fp8_accum<kItemsPerThread>(acc, w, code);
         } else {
           float w[kItemsPerThread];
           uint4 va[kItemsPerThread], vb[kItemsPerThread];
@@ -416,7 +429,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             vb[q] = lds128(buf + irow[q] * row_bytes + d + ivec[q] * 16);
           }
           stage_release(&empty[stage]);  // this thread's reads of the stage are done
-          if (!(variant & 32)) {
+          if (!skip_math) {
 #pragma unroll
             for (int q = 0; q < kItemsPerThread; ++q) {
               const uint32_t av[4] = {va[q].x, va[q].y, va[q].z, va[q].w};
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           if (tstore) {
             sts128(pa, o0);  // in place; the whole tile leaves with one bulk store below
             sts128(pb, o1);
-          } else if (!(variant & 2)) {
+          } else if (!skip_store) {
             bf16* o = dst + int64_t(row) * d + ivec[q] * 8;
             stg128_cs(o, o0);
             stg128_cs(o + d / 2, o1);
@@ -506,7 +519,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
             p1[1] = make_float4(acc[s][q][12], acc[s][q][13], acc[s][q][14], acc[s][q][15]);
           }
         }
-      } else if (!tstore && !(variant & 2)) {
+      } else if (!tstore && !skip_store) {
 #pragma unroll
         for (int q = 0; q < kItemsPerThread; ++q) {
           if (irow[q] >= srows) continue;
@@ -565,6 +578,9 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   if (variant < 0) {
     const char* v = getenv("KVCOMM_REALIGN_VARIANT");
     variant = v ? atoi(v) : 0;
+    if (!kProbeVariants && (variant & (2 | 32)))
+      fprintf(stderr, "libkvcomm: KVCOMM_REALIGN_VARIANT bits 1/5 (skip stores / math) exist only in probe "
+                      "builds; ignored\n");
     const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
     if (c) cw_env = atoi(c);
   }

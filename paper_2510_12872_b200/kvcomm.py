@@ -46,6 +46,25 @@ def _rows_ld(t: torch.Tensor, what: str) -> int:
     return s1 // d
 
 
+def _dst_layout(t, what: str) -> Tuple[int, int]:
+    """(row stride between heads, heads per layer) of a destination [Ls, Hs, N, d]: a
+    row-major tensor, or a head slice full[l0:l1, h0:h1] of a consumer's [L, H, N, d]
+    cache (layer stride = H heads; kvcomm_realign_desc.dst_heads)."""
+    if t.dim() != 4:
+        raise ValueError(f"{what}: expected [Ls, Hs, N, d], got {tuple(t.shape)}")
+    if not t.is_cuda or t.dtype != torch.bfloat16:
+        raise ValueError(f"{what}: expected a bf16 CUDA tensor")
+    Ls, Hs, N, d = t.shape
+    s0, s1, s2, s3 = t.stride()
+    if s3 != 1 or (N > 1 and s2 != d) or s1 % d != 0 or s1 < N * d:
+        raise ValueError(f"{what}: strides {t.stride()} are not [Ls,Hs,ld,d] row-major")
+    if Ls == 1:
+        return s1 // d, Hs
+    if s0 % s1 != 0 or s0 // s1 < Hs:
+        raise ValueError(f"{what}: layer stride {s0} is not a whole number (>= {Hs}) of head blocks of {s1}")
+    return s1 // d, s0 // s1
+
+
 def _view(k: Optional[torch.Tensor], v: Optional[torch.Tensor], start: int = 0, what: str = "kv") -> L.KVView:
     if k is None:
         return L.KVView()
@@ -358,8 +377,8 @@ class Segment:
             raise ValueError("weights must be fp32 CUDA")
         ld_w = self.weights.shape[1] if self.kind == PLACEHOLDER else 0
         wptr = self.weights.data_ptr() if self.weights is not None else None
-        dst_ld = _rows_ld(self.dst_k, "dst_k")
-        if _rows_ld(self.dst_v, "dst_v") != dst_ld:
+        dst_ld, dst_heads = _dst_layout(self.dst_k, "dst_k")
+        if _dst_layout(self.dst_v, "dst_v") != (dst_ld, dst_heads):
             raise ValueError("dst_k/dst_v strides differ")
         for t in (self.debug_k, self.debug_v):
             if t is not None and (t.dtype != torch.float32 or not t.is_contiguous()):
@@ -368,7 +387,7 @@ class Segment:
                              len(self.candidates), L_seg, _view(self.base_k, self.base_v, what="base"),
                              self.base_start, self.target_start, self.dst_k.data_ptr(), self.dst_v.data_ptr(),
                              dst_ld, self.debug_k.data_ptr() if self.debug_k is not None else None,
-                             self.debug_v.data_ptr() if self.debug_v is not None else None)
+                             self.debug_v.data_ptr() if self.debug_v is not None else None, dst_heads, 0)
 
 
 @dataclass
@@ -444,10 +463,10 @@ class Plan:
                                   s.base_k.shape[2], s.base_start, s.target_start, 0)
         ags = (L.PlanAgent * len(agents))()
         for i, (N, dk, dv) in enumerate(agents):
-            ld = _rows_ld(dk, "dst_k")
-            if _rows_ld(dv, "dst_v") != ld:
+            ld, heads = _dst_layout(dk, "dst_k")
+            if _dst_layout(dv, "dst_v") != (ld, heads):
                 raise ValueError("dst_k/dst_v strides differ")
-            ags[i] = L.PlanAgent(int(N), 0, dk.data_ptr(), dv.data_ptr(), ld)
+            ags[i] = L.PlanAgent(int(N), heads, dk.data_ptr(), dv.data_ptr(), ld)
         h = C.c_void_p()
         L.check(L.lib().kvcomm_plan_create(ms, len(matches), ss, len(segments), ags, len(agents), C.byref(h)))
         self._h = h

@@ -1,9 +1,10 @@
-"""Layer sharding of the realignment across the GPUs of one box.
+"""Layer (and KV-head) sharding of the realignment across the GPUs of one box.
 
 Every (layer, KV-head, token) unit of a4/a5 is independent and the matching
 weights depend only on (sample, pool), so each rank holds a contiguous block of
-layers of every pool and base cache plus the replicated embeddings, and realigns
-its block with no communication.  Two exchanges remain:
+layers — for large models a (layer group, KV-head group) block, grid_shard — of every
+pool and base cache plus the (replicated or sharded) embeddings, and realigns its
+block with no communication.  Two exchanges remain:
   * matching (MatchShard, default): each rank computes 1/G of the match positions and
     stores those W columns and d̄ partials into every rank's buffers (one barrier per
     request) — or every rank recomputes every distance (replicated);
@@ -29,6 +30,24 @@ def layer_shard(num_layers: int, rank: int, world: int) -> Tuple[int, int]:
     return begin, begin + base + (1 if rank < rem else 0)
 
 
+def head_shard(num_heads: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous [begin, end) KV-head block (same split rule as layer_shard)."""
+    return layer_shard(num_heads, rank, world)
+
+
+def grid_shard(num_layers: int, num_heads: int, rank: int, layer_groups: int,
+               head_groups: int = 1) -> Tuple[Tuple[int, int], Tuple[int, int]]:
+    """(layer range, head range) of `rank` on a layer_groups x head_groups grid (SURVEY
+    §8(e): 8B layer groups only; 70B "layer groups x KV-head groups", e.g. 4 x 2 on 8
+    GPUs).  rank = layer_group * head_groups + head_group, so the head groups of one
+    layer block are neighbouring ranks."""
+    world = layer_groups * head_groups
+    if not (0 <= rank < world) or head_groups < 1 or head_groups > num_heads or layer_groups > num_layers:
+        raise ValueError("bad grid")
+    lg, hg = divmod(rank, head_groups)
+    return layer_shard(num_layers, lg, layer_groups), head_shard(num_heads, hg, head_groups)
+
+
 def consumer_rank(agent: int, world: int) -> int:
     """GPU that hosts agent m (1-based): (m - 1) mod G."""
     return (agent - 1) % world
@@ -36,43 +55,58 @@ def consumer_rank(agent: int, world: int) -> int:
 
 def gather_to_consumers(agents: Sequence[int], shards: Sequence[Tuple[torch.Tensor, torch.Tensor]],
                         full: Sequence[Tuple[torch.Tensor, torch.Tensor]], num_layers: int, rank: int,
-                        world: int, group=None) -> None:
-    """Targeted gather: for each agent, every rank's layer block of (K, V) lands in
-    the consumer rank's full [L, Hs, N, d] buffers.
+                        world: int, group=None, head_groups: int = 1) -> None:
+    """Targeted gather (the NCCL baseline of the delivery step): for each agent, every
+    rank's (layer, head) block of (K, V) lands in the consumer rank's full [L, H, N, d]
+    buffers.  Blocks follow grid_shard(L, H, rank, world // head_groups, head_groups).
 
-    shards[i] = (K, V) of agents[i] on this rank, [Ls, Hs, N, d]
+    shards[i] = (K, V) of agents[i] on this rank, [Ls, Hs, N, d] contiguous
     full[i]   = (K, V) full-depth buffers on the consumer rank (ignored elsewhere)
+
+    A layer block of all heads is contiguous in [L, H, N, d] and is received in place; a
+    head block is not ("head sharding needs staging plus a local permute"),
+    so it is received into a staging buffer and copied into full[l0:l1, h0:h1].
     """
     staged = dist.get_backend(group) == "gloo" and any(
         t is not None and t.is_cuda for pair in shards for t in pair)
     if staged:   # gloo moves host tensors only: stage through host memory (test path)
         cpu_full = [(f[0].cpu(), f[1].cpu()) if f[0] is not None else (None, None) for f in full]
         gather_to_consumers(agents, [(k.cpu(), v.cpu()) for k, v in shards], cpu_full, num_layers, rank, world,
-                            group)
+                            group, head_groups)
         for f, c in zip(full, cpu_full):
             if f[0] is not None:
                 f[0].copy_(c[0])
                 f[1].copy_(c[1])
         return
-    ops = []
+    layer_groups = world // head_groups
+    if layer_groups * head_groups != world:
+        raise ValueError(f"world {world} is not a multiple of head_groups {head_groups}")
+    ops, permutes = [], []
     for i, m in enumerate(agents):
         dst = consumer_rank(m, world)
         kb, vb = shards[i]
         if rank == dst:
+            H = full[i][0].shape[1]
             for src in range(world):
-                lb, le = layer_shard(num_layers, src, world)
-                if src == rank:
-                    full[i][0][lb:le].copy_(kb)
-                    full[i][1][lb:le].copy_(vb)
-                else:
-                    ops.append(dist.P2POp(dist.irecv, full[i][0][lb:le], src, group))
-                    ops.append(dist.P2POp(dist.irecv, full[i][1][lb:le], src, group))
+                (lb, le), (hb, he) = grid_shard(num_layers, H, src, layer_groups, head_groups)
+                for plane in range(2):
+                    target = full[i][plane][lb:le, hb:he]
+                    if src == rank:
+                        target.copy_((kb, vb)[plane])
+                    elif (hb, he) == (0, H):
+                        ops.append(dist.P2POp(dist.irecv, target, src, group))
+                    else:
+                        stage = torch.empty(target.shape, dtype=target.dtype, device=target.device)
+                        ops.append(dist.P2POp(dist.irecv, stage, src, group))
+                        permutes.append((target, stage))
         else:
             ops.append(dist.P2POp(dist.isend, kb, dst, group))
             ops.append(dist.P2POp(dist.isend, vb, dst, group))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+    for target, stage in permutes:   # the local permute: staged head block -> its strided place
+        target.copy_(stage)
 
 
 def stream_barrier(flag: Optional[torch.Tensor], group=None) -> None:
@@ -149,9 +183,10 @@ class PeerRows:
     is_cuda = True
     dtype = torch.bfloat16
 
-    def __init__(self, ptr: int, shape: Tuple[int, int, int, int]):
+    def __init__(self, ptr: int, shape: Tuple[int, int, int, int], heads_total: Optional[int] = None):
         self._ptr = int(ptr)
         self.shape = torch.Size(shape)
+        self.heads_total = heads_total or shape[1]   # a head block of a full [L, H, N, d] cache
 
     def dim(self) -> int:
         return 4
@@ -160,8 +195,8 @@ class PeerRows:
         return self._ptr
 
     def stride(self) -> Tuple[int, int, int, int]:
-        _, Hs, N, d = self.shape
-        return (Hs * N * d, N * d, d, 1)
+        _, _, N, d = self.shape
+        return (self.heads_total * N * d, N * d, d, 1)
 
 
 class PeerCaches:
@@ -232,13 +267,16 @@ class PeerCaches:
         nccl = dist.get_backend(group) == "nccl"
         self._flag = torch.zeros(1, dtype=torch.int32, device=f"cuda:{device}") if nccl else None
 
-    def destinations(self, i: int, layer_range: Tuple[int, int]):
-        """(K, V) destinations of this rank's layer block of agent i's cache."""
+    def destinations(self, i: int, layer_range: Tuple[int, int], head_range: Optional[Tuple[int, int]] = None):
+        """(K, V) destinations of this rank's (layer, head) block of agent i's cache: rows
+        (l, h) of the block at ((l0 + l) * H + h0 + h) * N * d of the full cache, i.e. a
+        head block keeps the full cache's layer stride (kvcomm plan agent dst_heads = H)."""
         agent, N = self.agents[i]
         lb, le = layer_range
-        off = lb * self.H * N * self.d * 2
-        shape = (le - lb, self.H, N, self.d)
-        return tuple(PeerRows(p + off, shape) for p in self.ptrs[i])
+        hb, he = head_range or (0, self.H)
+        off = (lb * self.H + hb) * N * self.d * 2
+        shape = (le - lb, he - hb, N, self.d)
+        return tuple(PeerRows(p + off, shape, self.H) for p in self.ptrs[i])
 
     def full(self, i: int):
         """Agent i's full caches as torch tensors on its consumer rank, else (None, None)."""

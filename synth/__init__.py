@@ -268,6 +268,20 @@ def five_agent_workload(L: int = 32, H: int = 8, d: int = 128, D_e: int = 4096,
     return Workload("llama3-8b-5agent", L, H, d, D_e, capacity, pools, agents)
 
 
+def shared_segment_workload(L: int = 80, H: int = 8, d: int = 128, D_e: int = 8192, seg_len: int = 3072,
+                            prefix_len: int = 32, p0: int = 200, capacity: int = 256) -> Workload:
+    """BASELINE.json configs[3]: Llama-3-70B shape, one 3K-token
+    shared segment re-prefixed for one consumer agent with a 256-anchor pool, k = 256.
+    The agent's prompt: p_(1,0) [p0] | segment [seg_len] | p_(1,1) [prefix_len]; the
+    placeholder base at 0, the prefix base right after p_(1,0) (reading A11)."""
+    pools = {"segment": PoolSpec("segment", seg_len, [1], [prefix_len])}
+    segs = [SegmentSpec(1, "p0", None, -1, p0, 0, 0),
+            SegmentSpec(1, "placeholder", "segment", 0, seg_len, 0, p0),
+            SegmentSpec(1, "prefix", "segment", 0, prefix_len, p0, p0 + seg_len)]
+    return Workload("llama3-70b-shared-segment", L, H, d, D_e, capacity, pools,
+                    [AgentSpec(1, p0 + seg_len + prefix_len, p0, segs)])
+
+
 # ----------------------------------------------------------------------------
 # Request streams and a synthetic "dense prefill" (stand-in for the model) for the
 # online pool maintenance of Algorithm 1 (SURVEY §8(f) f1).  Inputs only: the

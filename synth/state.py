@@ -44,14 +44,23 @@ class StateInputs:
     layer_range: Tuple[int, int]
     device: str
     anchor_extra: int = 0
+    head_range: Optional[Tuple[int, int]] = None
 
     @property
     def Ls(self):
         return self.layer_range[1] - self.layer_range[0]
 
-    def _layers(self, t):  # generate full-L tensors so shards slice identical bytes
+    @property
+    def Hs(self):
+        hb, he = self.head_range or (0, self.w.H)
+        return he - hb
+
+    def _layers(self, t):  # generate full-L/H tensors so (layer, head) shards slice identical bytes
         lb, le = self.layer_range
-        return t[lb:le].contiguous() if (lb, le) != (0, self.w.L) else t
+        hb, he = self.head_range or (0, self.w.H)
+        if (lb, le) == (0, self.w.L) and (hb, he) == (0, self.w.H):
+            return t
+        return t[lb:le, hb:he].contiguous()
 
     def vocab(self) -> torch.Tensor:
         g = keyed_gen(self.seed, "vocab", device=self.device)
@@ -115,20 +124,22 @@ def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: 
                            layer_range: Optional[Tuple[int, int]] = None, anchor_extra: int = 0,
                            top_k: int = 0, offset_format: str = "bf16", similarity: str = "l2",
                            scalar_distance: str = "frobenius",
-                           emb_shard: Optional[Tuple[int, int]] = None) -> FiveAgentState:
+                           emb_shard: Optional[Tuple[int, int]] = None,
+                           head_range: Optional[Tuple[int, int]] = None) -> FiveAgentState:
     from paper_2510_12872_b200 import kvcomm as K
     from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
     w = w or five_agent_workload()
     dev = f"cuda:{device}"
     lr = layer_range or (0, w.L)
-    inp = StateInputs(w, seed, lr, dev, anchor_extra)
+    inp = StateInputs(w, seed, lr, dev, anchor_extra, head_range)
     inv = llama3_inv_freq(w.d)
     vocab = inp.vocab()
     pools = {}
     for name, ps in w.pools.items():
         pool = K.AnchorPool(num_layers=w.L, num_kv_heads=w.H, head_dim=w.d, emb_dim=w.D_e, capacity=w.capacity,
                             max_anchor_len=ps.L_phi + anchor_extra, prefix_len=ps.prefix_len, inv_freq=inv,
-                            device=device, layer_range=lr, offset_format=offset_format, similarity=similarity,
+                            device=device, layer_range=lr, head_range=head_range, offset_format=offset_format,
+                            similarity=similarity,
                             scalar_distance=scalar_distance, emb_shard=emb_shard)
         for slot in range(w.capacity):
             emb = vocab[inp.anchor_ids(name, slot)]
@@ -155,7 +166,7 @@ def build_five_agent_state(w: Optional[Workload] = None, seed: int = 0, device: 
                 bk, bv = inp.prefix_base(s.pool, s.consumer, 0), inp.prefix_base(s.pool, s.consumer, 1)
                 kind = K.PREFIX
             segs.append(SegmentLayout(kind, s.pool, s.consumer, bk, bv, s.base_start, s.target_start))
-        dst_k = torch.zeros(inp.Ls, w.H, a.N, w.d, dtype=torch.bfloat16, device=dev)
+        dst_k = torch.zeros(inp.Ls, inp.Hs, a.N, w.d, dtype=torch.bfloat16, device=dev)
         dst_v = torch.zeros_like(dst_k)
         agents.append(AgentLayout(a.agent, a.N, inp.p0(a.agent, 0), inp.p0(a.agent, 1), segs, dst_k, dst_v))
     req = ReuseRequest(pools, agents, gamma=gamma, top_k=top_k)

@@ -20,10 +20,12 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     fmt = sys.argv[1] if len(sys.argv) > 1 else "bf16"
     shard_match = len(sys.argv) > 2 and sys.argv[2] in ("shard-match", "shard-mismatch", "shard-match-emb",
-                                                          "shard-mismatch-empty")
+                                                          "shard-mismatch-empty", "shard-mismatch-replace")
     empty_rank1 = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch-empty"
     emb_shard = len(sys.argv) > 2 and sys.argv[2] == "shard-match-emb"
-    mismatch = len(sys.argv) > 2 and sys.argv[2] in ("shard-mismatch", "shard-mismatch-empty")
+    replace_rank1 = len(sys.argv) > 2 and sys.argv[2] == "shard-mismatch-replace"
+    mismatch = len(sys.argv) > 2 and sys.argv[2] in ("shard-mismatch", "shard-mismatch-empty",
+                                                      "shard-mismatch-replace")
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
     scal = sys.argv[5] if len(sys.argv) > 5 else "frobenius"
@@ -51,7 +53,19 @@ def main():
               for i, a in enumerate(st.agents)]
     req = ReuseRequest(st.pools, agents, gamma=1.0, top_k=top_k)
     if mismatch:   # the ranks' pools out of step: rank 1 lacks one user_question anchor
-        if rank == 1 and not empty_rank1:
+        if rank == 1 and replace_rank1:
+            # the full pool takes one more anchor: LFU evicts slot 0 and the newcomer reuses
+            # that slot id, so both ranks still list candidates 0..3 — but slot 0 now holds a
+            # different anchor (same length) on rank 1
+            from paper_2510_12872_b200 import kvcomm as K
+            inp, name = st.inputs, "user_question"
+            emb = inp.vocab()[inp.anchor_ids(name, 1)]
+            offs = [K.OffsetGiven(c, inp.offset(name, 1, c, "ph", 0), inp.offset(name, 1, c, "ph", 1),
+                                  inp.offset(name, 1, c, "pf", 0), inp.offset(name, 1, c, "pf", 1))
+                    for c in range(len(w.pools[name].consumers))]
+            slot, ev = st.pools[name].insert(emb, offs)
+            assert (slot, ev) == (0, 0), (slot, ev)
+        elif rank == 1 and not empty_rank1:
             st.pools["user_question"].evict(0)
         if rank == 1 and empty_rank1:   # every pool empty: rank 1 decides everything on the host
             for pool in st.pools.values():

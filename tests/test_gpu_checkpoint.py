@@ -154,3 +154,37 @@ def test_embedding_sharded_pool(tmp_path):
     with pytest.raises(KVCommError):
         mk((3, 3))
     dense.destroy(); shard.destroy(); back.destroy()
+
+
+def test_pool_load_rejects_corrupt_slot_metadata(tmp_path):
+    """A checkpoint whose LFU metadata no pool could have produced is an IO error: an
+    insertion index at or past the counter, two slots sharing an index, or a presence
+    bit at or above the consumer count (they would silently change the A17 tie-break)."""
+    import struct
+    from paper_2510_12872_b200 import kvcomm as K
+    from paper_2510_12872_b200._lib import KVCommError
+    g = torch.Generator(device="cuda").manual_seed(6)
+    a = _pool("bf16", "device")
+    _fill(a, g)
+    path = str(tmp_path / "pool.kvc")
+    a.save(path)
+    a.destroy()
+    data = bytearray(open(path, "rb").read())
+    # header: magic 8 + version 4 + 16 config ints + emb shard 2 x int32 + prefix_len[C] + inv_freq[d/2]
+    counter = 8 + 4 + 16 * 4 + 8 + 4 * len(P) + 8 * (D // 2)
+    slot0 = counter + 8   # per slot: occupied i32, length i32, access i64, inserted i64, ph/pf masks u64
+    next_index = struct.unpack_from("<q", data, counter)[0]
+    assert next_index == 4 and struct.unpack_from("<i", data, slot0)[0] == 1
+    back = K.AnchorPool.load(path)   # the unmodified file loads
+    back.destroy()
+    accepted = []
+    for field, value in ((16, next_index), (16, 1), (24, 1 << len(P))):
+        bad = bytearray(data)
+        struct.pack_into("<q", bad, slot0 + field, value)
+        open(path, "wb").write(bytes(bad))
+        try:
+            K.AnchorPool.load(path).destroy()
+            accepted.append((field, value))
+        except KVCommError as e:
+            assert e.status_name == "IO" and "slot" in str(e), (field, value, str(e))
+    assert not accepted, accepted

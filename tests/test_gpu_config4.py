@@ -142,8 +142,8 @@ def test_config4_sampled_rows(c4, kind):
     gk = harness.f64(c4["dst"][0][:, :, rows])
     gv = harness.f64(c4["dst"][1][:, :, rows])
     for (l, h) in lh:
-        harness.check_kv(gk[l, h], ora["k"][l, h], bk[l, h], absk[l, h], f"config4 {kind} K l{l} h{h}")
-        harness.check_kv(gv[l, h], ora["v"][l, h], bv[l, h], absv[l, h], f"config4 {kind} V l{l} h{h}")
+        harness.check_kv(gk[l, h], ora["k"][l, h], bk[l, h], absk[l, h], f"config4 {kind} K l{l} h{h}", n_terms=M)
+        harness.check_kv(gv[l, h], ora["v"][l, h], bv[l, h], absv[l, h], f"config4 {kind} V l{l} h{h}", n_terms=M)
 
 
 def test_config4_p0_copied(c4):

@@ -66,14 +66,15 @@ def test_online_stream_matches_oracle(gamma, capacity):
                 assert np.array_equal(gpk, opk) and np.array_equal(gpv, opv)
             else:                          # reuse: Eq. 6 / Eq. 7 realignment
                 offs = [orc.off[s][c] for s in r.candidates]
+                n = len(r.candidates)
                 absk = O.blend_placeholder(r.W, [np.abs(o[0]) for o in offs])
                 absv = O.blend_placeholder(r.W, [np.abs(o[1]) for o in offs])
-                harness.check_kv(gk, ok, f64(bk), absk, f"step {step} K ph c{c}")
-                harness.check_kv(gv, ov, f64(bv), absv, f"step {step} V ph c{c}")
+                harness.check_kv(gk, ok, f64(bk), absk, f"step {step} K ph c{c}", n_terms=n)
+                harness.check_kv(gv, ov, f64(bv), absv, f"step {step} V ph c{c}", n_terms=n)
                 pabsk = O.blend_prefix(r.wbar, [np.abs(o[2]) for o in offs])
                 pabsv = O.blend_prefix(r.wbar, [np.abs(o[3]) for o in offs])
-                harness.check_kv(gpk, opk, f64(sp.pf_base[c][0]), pabsk, f"step {step} K pf c{c}")
-                harness.check_kv(gpv, opv, f64(sp.pf_base[c][1]), pabsv, f"step {step} V pf c{c}")
+                harness.check_kv(gpk, opk, f64(sp.pf_base[c][0]), pabsk, f"step {step} K pf c{c}", n_terms=n)
+                harness.check_kv(gpv, opv, f64(sp.pf_base[c][1]), pabsv, f"step {step} V pf c{c}", n_terms=n)
         if ins is not None:
             assert (g.slot, g.evicted) == ins, step
             n_new += 1
@@ -82,7 +83,8 @@ def test_online_stream_matches_oracle(gamma, capacity):
             for c in range(spec.consumers):
                 gk_off, gv_off = online.pool.offset_view(g.slot, c, "ph", rows=L)
                 odk, odv = orc.off[g.slot][c][0], orc.off[g.slot][c][1]
-                harness.check_kv(f64(gk_off), odk, np.zeros_like(odk), np.abs(odk) + 4.0, f"measured dK c{c}")
+                # fp32 de-rotation of K_real minus K_base: M = |K_base| + |K_real| (+ RoPE partner)
+                harness.check_kv(f64(gk_off), odk, f64(bk), np.abs(f64(reals[c][0])), f"measured dK c{c}")
                 assert np.array_equal(f64(gv_off), odv)
         else:
             n_reuse += 1

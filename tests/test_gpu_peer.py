@@ -44,10 +44,11 @@ def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["shard-mismatch", "shard-mismatch-empty"])
+@pytest.mark.parametrize("mode", ["shard-mismatch", "shard-mismatch-empty", "shard-mismatch-replace"])
 def test_sharded_matching_detects_out_of_step_pools(mode):
-    """Ranks whose pools differ (rank 1 evicted an anchor, or every anchor so that it has
-    no job at all) must not blend with each other's weights: every job whose layout
+    """Ranks whose pools differ (rank 1 evicted an anchor; or every anchor so that it has
+    no job at all; or its full pool replaced the anchor in slot 0 by another of the same
+    length, so the candidate slot ids still agree) must not blend with each other's weights: every job whose layout
     fingerprints differ is NewAnchor (SHARD_MISMATCH), no agent is realigned, and
     results() raises SHAPE_MISMATCH (rank 1 with empty pools: host verdicts EMPTY_POOL)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",

@@ -271,8 +271,8 @@ def test_verdict_length_clause_candidates_and_gamma_range():
 
 
 def test_gamma_monotone_reuse():
-    # Table 6: reuse rate non-decreasing in gamma; gamma = 0 shares only
-    # when the weights are one-hot.  Pins the entropy sign (reading A5).
+    # Table 6: reuse rate non-decreasing in gamma; gamma = 0 shares nothing
+    # (reading A19).  Pins the entropy sign (reading A5).
     pool = [bf16_values((16, 32)) for _ in range(6)]
     queries = [pool[j % 6] + rng.standard_normal((16, 32)) * s
                for j, s in enumerate(np.linspace(0.0, 2.0, 30))]
@@ -282,7 +282,50 @@ def test_gamma_monotone_reuse():
         n = sum(O.predict(q, lens, embs, pres, g).verdict == O.SHAREABLE for q in queries)
         assert n >= prev
         prev = n
-    assert sum(O.predict(q, lens, embs, pres, 0.0).verdict == O.SHAREABLE for q in queries) < 30
+    assert sum(O.predict(q, lens, embs, pres, 0.0).verdict == O.SHAREABLE for q in queries) == 0
+
+
+def test_gamma_zero_is_no_sharing():
+    # Table 6: "γ=0 / V=0 refers to the original no-cache-sharing method" (reading
+    # A19): NewAnchor for every sample at γ = 0 — also with one candidate, where Eq. 5 alone
+    # gives H = 0 = threshold — while any γ > 0 keeps Eq. 5's |𝒜_φ| = 1 → Shareable.
+    h = bf16_values((8, 16))
+    for pool in ([h + 1.0], [h.copy()], [h, h + 5.0]):
+        r = O.predict(h, *_pool(pool), 0.0)
+        assert r.verdict == O.NEW_ANCHOR and r.reason == O.R_HIGH_ENTROPY and r.threshold == 0.0
+    r = O.predict(h, *_pool([h + 1.0]), 1e-6)
+    assert r.verdict == O.SHAREABLE and r.H == 0.0
+
+
+def test_config2_verdicts_under_both_scalar_distance_readings():
+    """What reading A4 decides on the bench workload (SURVEY §8(d) recipe at config 2's
+    user_question shape: L_φ = 1024, D_e = 4096, 20 anchors of rows ~ N(0, 1/D_e), the
+    query = anchor 0 with each position re-drawn w.p. 0.3) at the paper's γ = 0.3.
+    Independent rows sit ≈ √2 apart, so d[i, 0] ≈ 0 at ~70 % of positions and ≈ √2
+    elsewhere.  Closed forms:
+      Frobenius: d̄_0 ≈ √(0.3·1024·2) ≈ 24.8, d̄_j ≈ √(1024·2) ≈ 45.3 → w̄_0 ≈ 1 - 19 e^-20.5,
+                 H ≈ 0 → Shareable (the bench's verdicts);
+      mean-ℓ2:   d̄_0 ≈ 0.3√2, d̄_j ≈ √2 → w̄_0 = 1 / (1 + 19 e^-(0.7√2)) ≈ 0.124,
+                 H ≈ 2.95 > 0.3 log 20 = 0.899 → NewAnchor; no sample can pass: even d̄_0 = 0
+                 gives w̄_0 ≈ 0.18, H ≈ 2.8, so mean-ℓ2 reuses nothing at γ = 0.3 (DESIGN A4)."""
+    g = torch.Generator().manual_seed(2)
+    L, De, n = 1024, 4096, 20
+    anchors = [synth.randn_bf16((L, De), g, 1.0 / math.sqrt(De)).double().numpy() for _ in range(n)]
+    swap = (torch.rand(L, generator=g) < 0.3).numpy()
+    q = anchors[0].copy()
+    q[swap] = synth.randn_bf16((int(swap.sum()), De), g, 1.0 / math.sqrt(De)).double().numpy()
+    lens, embs, pres = _pool(anchors)
+    fro = O.predict(q, lens, embs, pres, 0.3, scalar=O.FROBENIUS)
+    m2 = O.predict(q, lens, embs, pres, 0.3, scalar=O.MEAN_L2)
+    p = swap.mean()
+    assert fro.verdict == O.SHAREABLE and fro.H < 1e-5
+    assert fro.dbar[0] == pytest.approx(math.sqrt(p * L * 2), rel=0.02)
+    assert np.allclose(fro.dbar[1:], math.sqrt(2 * L), rtol=0.02)
+    assert m2.verdict == O.NEW_ANCHOR and m2.reason == O.R_HIGH_ENTROPY
+    w0 = 1.0 / (1.0 + (n - 1) * math.exp(-(1 - p) * math.sqrt(2)))
+    H = -w0 * math.log(w0) - (1 - w0) * math.log((1 - w0) / (n - 1))
+    assert m2.wbar[0] == pytest.approx(w0, rel=0.05) and m2.H == pytest.approx(H, rel=0.02)
+    assert m2.H > 0.9 * math.log(n)          # NewAnchor for every γ <= 0.9 (Table 6's grid)
 
 
 # ---------------------------------------------------------------- blend / realign

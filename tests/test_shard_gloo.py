@@ -101,6 +101,62 @@ def test_gather_to_consumers_world2_gloo_equals_unsharded():
     assert res == {0: True, 1: True}
 
 
+def test_grid_shard_partitions_layers_and_heads():
+    """70B runs layer groups x KV-head groups (4 x 2 on 8 GPUs)."""
+    for L, H, lg, hg in ((80, 8, 4, 2), (32, 8, 8, 1), (4, 4, 1, 4), (5, 3, 2, 3)):
+        cover = np.zeros((L, H), dtype=int)
+        for r in range(lg * hg):
+            (lb, le), (hb, he) = shard.grid_shard(L, H, r, lg, hg)
+            cover[lb:le, hb:he] += 1
+            assert (lb, le) == shard.layer_shard(L, r // hg, lg) and (hb, he) == shard.head_shard(H, r % hg, hg)
+        assert (cover == 1).all()
+    assert shard.grid_shard(80, 8, 5, 4, 2) == ((40, 60), (4, 8))
+    with pytest.raises(ValueError):
+        shard.grid_shard(8, 2, 0, 2, 3)
+
+
+def _oracle_realign_block(lb, le, hb, he, seed):
+    """Per-agent realigned caches of the (layer, head) block via the oracle."""
+    return [(k[:, hb:he].contiguous(), v[:, hb:he].contiguous()) for k, v in _oracle_realign_layers(lb, le, seed)]
+
+
+def _grid_worker(rank, world, hg, port, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L, H = 4, 2
+    (lb, le), (hb, he) = shard.grid_shard(L, H, rank, world // hg, hg)
+    mine = _oracle_realign_block(lb, le, hb, he, seed=9)
+    agents = [1, 2, 3]
+    full = [(torch.zeros((L, H) + tuple(k.shape[2:])), torch.zeros((L, H) + tuple(k.shape[2:])))
+            if shard.consumer_rank(a, world) == rank else (None, None) for a, (k, _) in zip(agents, mine)]
+    shard.gather_to_consumers(agents, mine, full, L, rank, world, head_groups=hg)
+    ref = _oracle_realign_layers(0, L, seed=9)
+    ok = True
+    for a, (fk, fv), (rk, rv) in zip(agents, full, ref):
+        if shard.consumer_rank(a, world) == rank:
+            ok &= torch.equal(fk, rk) and torch.equal(fv, rv)
+    result_q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,hg", [(2, 2), (4, 2)])
+def test_gather_head_blocks_gloo_equals_unsharded(world, hg):
+    """Head blocks are not contiguous in the consumer's [L, H, N, d] cache: they are
+    received into staging buffers and permuted into place."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grid_worker, args=(r, world, hg, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert res == {r: True for r in range(world)}
+
+
 class _FakePlan:
     """Stands in for kvcomm.Plan in the host-logic test of shard.MatchShard."""
 
@@ -182,3 +238,19 @@ def test_match_shard_handshake_gloo(case):
             assert not sharded or unsharded_after, calls   # nobody left sharded
         if case == "size":
             assert "differ across ranks" in out[0][1]
+
+
+def test_peer_destinations_of_a_head_block_keep_the_full_layer_stride():
+    """PeerCaches.destinations(i, layer_range, head_range): the block's first row sits at
+    ((l0 * H + h0) * N) * d of the consumer's full cache and its layers are H head
+    blocks apart, which the binding passes to the plan as dst_heads = H."""
+    from paper_2510_12872_b200 import kvcomm as K
+    pc = shard.PeerCaches.__new__(shard.PeerCaches)
+    pc.H, pc.d, pc.agents, pc.ptrs = 8, 128, [(1, 100)], [(1 << 20, 1 << 30)]
+    dk, dv = pc.destinations(0, (20, 40), (4, 8))
+    assert dk.data_ptr() == (1 << 20) + (20 * 8 + 4) * 100 * 128 * 2
+    assert dv.data_ptr() == (1 << 30) + (20 * 8 + 4) * 100 * 128 * 2
+    assert tuple(dk.shape) == (20, 4, 100, 128) and dk.stride() == (8 * 100 * 128, 100 * 128, 128, 1)
+    assert K._dst_layout(dk, "dst") == (100, 8)
+    full = pc.destinations(0, (0, 80))[0]
+    assert full.stride() == (8 * 100 * 128, 100 * 128, 128, 1) and K._dst_layout(full, "dst") == (100, 8)
