@@ -68,6 +68,15 @@ def parse():
     return ap.parse_args()
 
 
+def realign_src_hash():
+    """sha256 of the realign kernel's sources (as scripts/summarize_profiles.py records it)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("realign.cu", "kvcomm_internal.h", "ptx.cuh", "Makefile"):
+        h.update(open(os.path.join(ROOT, "paper_2510_12872_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -677,13 +686,16 @@ def main():
     P = peaks()
     peak = P.get("hbm_gbs")
     achieved = alg_bytes / (realign_avg / 1e3) / 1e9
-    traffic = None
-    try:   # the committed full capture is of the N=1 launch; a layer shard moves 1/N of it
-        if world > 1:
-            raise LookupError("no per-shard capture")
+    traffic, traffic_src = None, None
+    try:   # the committed full capture is of the N=1 config-2 launch of THIS kernel source
+        if world > 1 or args.workload != "8b-5agent":
+            raise LookupError("no capture of this configuration")
         name = "realign_ncu.json" if args.offsets == "bf16" else f"realign_ncu_{args.offsets}.json"
         prof = json.load(open(os.path.join(ROOT, "profiles", name)))
-        traffic = prof.get("dram_bytes_per_launch")
+        if prof.get("realign_src_sha") != realign_src_hash():
+            traffic_src = f"profiles/{name} was captured on another realign kernel source: not reported"
+            raise LookupError(traffic_src)
+        traffic, traffic_src = prof.get("dram_bytes_per_launch"), prof.get("source")
     except Exception:  # noqa: BLE001
         pass
 
@@ -709,7 +721,7 @@ def main():
                          "bound": "hbm",
                          "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if peak else None,
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,
                          "realign_share_of_step": realign_avg / ms_per_step,
                          "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "

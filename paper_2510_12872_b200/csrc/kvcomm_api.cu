@@ -992,6 +992,34 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
                                   size_t(kMatchP) * (3 * it.info->n_candidates + 1) * sizeof(double));
   }
   L.hdr.total_blocks = blocks;
+  {  // the TMA-streamed distance kernel takes l2 jobs up to 256 candidates and D_e 8192
+    static const int tma_env = [] {
+      // measurement knob, off by default: 1 = the TMA-ring distance kernel, measured SLOWER than the
+      // register-streaming kernel (config 4: 3.13 vs 1.99 ms; one config-2 pool: 86 vs 60 us;
+      // profiles/r02_match_tma.json) — DESIGN §7
+      const char* e = getenv("KVCOMM_MATCH_TMA");
+      return e ? atoi(e) : 0;
+    }();
+    bool ok = tma_env != 0 && kMatchP == 2 && nj > 0;
+    int de = 0, cm = 1;
+    for (const MatchItem& it : items) {
+      ok = ok && it.p->cfg.similarity == KVCOMM_SIM_L2 && it.info->n_candidates <= kMatchTmaMaxCand &&
+           it.p->De <= kMatchTmaMaxDe;
+      de = std::max(de, it.p->De);
+      cm = std::max(cm, it.info->n_candidates);
+    }
+    if (ok) {
+      const int qb = int(align_up(size_t(kMatchP) * de * 2, 16));
+      const size_t fixed = match_tma_smem(0, qb, cm);
+      const int stages = int(std::min<size_t>(8, (227 * 1024 - fixed) / (kMatchStageBytes + 16)));
+      if (stages >= 3) {
+        L.hdr.tma = 1;
+        L.hdr.tma_stages = stages;
+        L.hdr.tma_qbytes = qb;
+        L.hdr.tma_cmax = cm;
+      }
+    }
+  }
   size_t off = align_up(sizeof(MatchHdr), 64);
   L.hdr.job_off = int64_t(off);
   off = align_up(off + sizeof(MatchJob) * nj, 64);

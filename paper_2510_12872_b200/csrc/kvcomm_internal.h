@@ -19,6 +19,9 @@ constexpr int kUnitWBytes = KVC_UNITW;  // weight chunk buffer: [anchors][weight
 constexpr int kMaxCapDev = 1024;    // == KVCOMM_MAX_CAPACITY
 constexpr int kMaxTopK = 32;        // == KVCOMM_MAX_TOPK
 constexpr int kMatchChunks = 32;    // position-block chunks of the two-pass d̄ reduction
+constexpr int kMatchStageBytes = 16384;  // TMA distance kernel: bytes per ring stage
+constexpr int kMatchTmaMaxCand = 256;    // TMA distance kernel: candidates per job
+constexpr int kMatchTmaMaxDe = 8192;     // TMA distance kernel: embedding width
 
 // rows per realign tile (16 KiB of bf16 rows) for head_dim d
 __host__ __device__ constexpr int rows_per_tile(int d) { return kStageBytes / (2 * d); }
@@ -132,6 +135,10 @@ struct MatchHdr {
   // job NewAnchor with shard_mismatch set (the realign gate then skips its segments).
   uint64_t fingerprint;
   int32_t shard_rank, shard_world;
+  // TMA-streamed distance kernel (l2 jobs with n_cand <= kMatchTmaMaxCand, D_e <= 8192): ring
+  // stages of kMatchStageBytes, query double buffer of tma_qbytes each, partial table for
+  // tma_cmax candidates; tma = 0 selects the register-streaming kernel
+  int32_t tma, tma_stages, tma_qbytes, tma_cmax;
   uint64_t* fp_dst[kMaxMatchPeers + 1];   // [r]: this rank's slot in rank r's array
   const uint64_t* fp_mine;                // this rank's array [shard_world]
 };
@@ -141,6 +148,8 @@ cudaError_t launch_match_batch(const void* table_dev, const MatchHdr& hdr, size_
 // the two halves of launch_match_batch (sharded plans put the cross-rank sync between them)
 cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem_bytes, cudaStream_t s);
 cudaError_t launch_match_reduce(const void* table_dev, const MatchHdr& hdr, cudaStream_t s);
+// dynamic shared memory of the TMA distance kernel (ring stages, query buffers, partials)
+size_t match_tma_smem(int stages, int qbytes, int cmax);
 
 // Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,

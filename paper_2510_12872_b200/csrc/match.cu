@@ -93,6 +93,11 @@ __device__ __forceinline__ int find_job(const MatchJob* jobs, int n, int b) {
   return lo;
 }
 
+__device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, int i0, int np, const double* sd,
+                                           const double* s_qa, const double* s_aa, const double* s_qq,
+                                           const int32_t* cand, const int32_t* slot2cand, int32_t* ties, int warp,
+                                           int lane, int tid);
+
 // One work item = P consecutive positions of one job.
 __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, const int item) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
@@ -167,7 +172,17 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
     }
   }
   __syncthreads();
+  match_tail(a, jb, lb, i0, np, sd, s_qa, s_aa, s_qq, cand, slot2cand, ties, warp, lane, threadIdx.x);
+}
 
+// Per-position weights (Eq. 6 / top-k) and the block's deterministic partial sums of
+// d̄, from this block's distances sd[p * n_cand + j] (both distance kernels end here).
+// 8 warps (threads 0..255) take part; no block-level barrier inside.
+__device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, int i0, int np, const double* sd,
+                                           const double* s_qa, const double* s_aa, const double* s_qq,
+                                           const int32_t* cand, const int32_t* slot2cand, int32_t* ties, int warp,
+                                           int lane, int tid) {
+  const int n_cand = a.n_cand;
   // per-position weights (one warp per position)
   for (int p = warp; p < np; p += kMatchWarps) {
     const int i = i0 + p;
@@ -244,7 +259,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
   // deterministic per-block partial sums (Σ d² for Frobenius, Σ d for mean-ℓ2;
   // cosine: Σ q·a and Σ a·a per candidate, Σ q·q once)
   if (!a.cosine) {
-    for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
+    for (int j = tid; j < n_cand; j += kMatchThreads) {
       double s = 0.0;
       for (int p = 0; p < np; ++p) {
         const double dv = sd[p * n_cand + j];
@@ -255,7 +270,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
     }
   } else {
     const int64_t stride = 2 * n_cand + 1;
-    for (int j = threadIdx.x; j < n_cand; j += kMatchThreads) {
+    for (int j = tid; j < n_cand; j += kMatchThreads) {
       double sqa = 0.0, saa = 0.0;
       for (int p = 0; p < np; ++p) {
         sqa += s_qa[p * n_cand + j];
@@ -268,7 +283,7 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
         a.partial_peer[r][int64_t(lb) * stride + n_cand + j] = saa;
       }
     }
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       double sqq = 0.0;
       for (int p = 0; p < np; ++p) sqq += s_qq[p];
       a.partial[int64_t(lb) * stride + 2 * n_cand] = sqq;
@@ -296,6 +311,177 @@ __global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t
     __syncthreads();  // shared memory is reused by the next item
   }
   if (hdr->any_peer) __threadfence_system();  // peer stores visible before the caller's cross-rank sync
+}
+
+// ---- TMA-streamed distance kernel (l2 jobs) --------------------------------------
+// Persistent CTAs of 8 consumer warps + 1 producer warp walk the work items (P = 2
+// positions of one job) round-robin.  The producer's elected lane copies each item's
+// query rows (one bulk copy into a double buffer) and, per candidate anchor, the
+// anchor's P contiguous embedding rows (the same positions, reading A8) as 16 KiB
+// chunks into a ring of stages (cp.async.bulk + mbarrier complete_tx, L2 evict-first),
+// running ahead across items so the stream has no per-item bubble.  Consumer thread t
+// keeps its query vectors of the item in registers (vectors g = c * 1024 + t + 256 k of
+// the flattened [P][De] tile) and, per anchor, accumulates Σ (q - a)² per position with
+// the same numerics as the register kernel (groups of 8 in fp32 FMA, fp64 beyond), warp-
+// reduces, and stores one fp64 partial per (anchor, warp, position); the item's
+// distances are the fixed-order sums of the 8 warp partials, so results are
+// deterministic and independent of the grid (sharded ranks agree bit for bit).
+constexpr int kMatchTmaVec = 8;  // query vectors per thread: P * De * 2 / (16 * 256) <= 8 at De 8192
+
+__device__ __forceinline__ void match_tma_geom(const MatchHdr* hdr, const MatchJob* jobs, int item, int& jb,
+                                               int& lb, int& i0, int& np) {
+  jb = find_job(jobs, hdr->n_jobs, item);
+  const MatchJob& a = jobs[jb];
+  lb = a.own_lo + (item - a.block_begin) * a.own_step;
+  i0 = lb * hdr->P;
+  np = min(hdr->P, a.L_phi - i0);
+}
+
+__global__ void __launch_bounds__(kMatchThreads + 32, 1) match_dist_tma_kernel(const uint8_t* __restrict__ tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  const MatchJob* jobs = reinterpret_cast<const MatchJob*>(tab + hdr->job_off);
+  const int32_t* ints = reinterpret_cast<const int32_t*>(tab + hdr->int_off);
+  int32_t* ties = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off);
+  const int NS = hdr->tma_stages, QB = hdr->tma_qbytes, CM = hdr->tma_cmax;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;                                                  // [NS][kMatchStageBytes]
+  uint8_t* qbuf = ring + size_t(NS) * kMatchStageBytes;                  // [2][QB]
+  double* part = reinterpret_cast<double*>(qbuf + 2 * size_t(QB));       // [CM][kMatchWarps][2]
+  double* sd = part + size_t(CM) * kMatchWarps * 2;                      // [2][CM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sd + 2 * size_t(CM));
+  uint64_t* empty = full + NS;
+  uint64_t* qfull = empty + NS;
+  uint64_t* qempty = qfull + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kMatchThreads);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (hdr->shard_world > 1 && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int r = 0; r < hdr->shard_world; ++r) *hdr->fp_dst[r] = hdr->fingerprint;
+  __syncthreads();
+  const int total = hdr->total_blocks;
+
+  if (warp == kMatchWarps) {
+    // ---------------- TMA producer (one lane) ----------------
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      int stage = 0, qb = 0;
+      uint32_t phase = 0, qphase = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        int jb, lb, i0, np;
+        match_tma_geom(hdr, jobs, item, jb, lb, i0, np);
+        const MatchJob& a = jobs[jb];
+        const uint32_t tile = uint32_t(np) * uint32_t(a.De) * 2u;
+        mbar_wait(&qempty[qb], qphase ^ 1u);
+        mbar_arrive_expect_tx(&qfull[qb], tile);
+        bulk_g2s(qbuf + size_t(qb) * QB, a.query + int64_t(i0) * a.De, tile, &qfull[qb], pol_stream);
+        if (++qb == 2) { qb = 0; qphase ^= 1u; }
+        const int32_t* cand = ints + a.cand_off;
+        const int64_t erow = a.emb_world > 1 ? int64_t(lb / a.emb_world) * hdr->P : int64_t(i0);
+        for (int j = 0; j < a.n_cand; ++j) {
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(a.emb + int64_t(cand[j]) * a.slot_stride + erow * a.De);
+          for (uint32_t off = 0; off < tile; off += kMatchStageBytes) {
+            const uint32_t bytes = min(uint32_t(kMatchStageBytes), tile - off);
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            bulk_g2s(ring + size_t(stage) * kMatchStageBytes, src + off, bytes, &full[stage], pol_stream);
+            if (++stage == NS) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers (threads 0..255) ----------------
+  const int tid = threadIdx.x;
+  int stage = 0, qb = 0;
+  uint32_t phase = 0, qphase = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int jb, lb, i0, np;
+    match_tma_geom(hdr, jobs, item, jb, lb, i0, np);
+    const MatchJob& a = jobs[jb];
+    const int De = a.De;
+    const int n_cand = a.n_cand;
+    const int tile_vec = np * De / 8;                    // 16-byte vectors of the [np][De] tile
+    const int chunks = (tile_vec + 1023) / 1024;         // 16 KiB chunks per anchor
+    mbar_wait(&qfull[qb], qphase);
+    const uint8_t* qsm = qbuf + size_t(qb) * QB;
+    uint4 qv[kMatchTmaVec];
+    int qpos = 0;                                        // bit v: vector v lies in position 1
+#pragma unroll
+    for (int v = 0; v < kMatchTmaVec; ++v) {
+      const int g = (v >> 2) * 1024 + tid + 256 * (v & 3);
+      qv[v] = g < tile_vec ? lds128(qsm + size_t(g) * 16) : make_uint4(0, 0, 0, 0);
+      qpos |= (g * 8 >= De ? 1 : 0) << v;
+    }
+    named_bar_sync(1, kMatchThreads);                   // every consumer holds its query vectors
+    if (tid == 0) mbar_arrive(&qempty[qb]);              // the producer may refill this buffer
+    if (++qb == 2) { qb = 0; qphase ^= 1u; }
+    for (int j = 0; j < n_cand; ++j) {
+      double acc0 = 0.0, acc1 = 0.0;
+      for (int c = 0; c < chunks; ++c) {
+        mbar_wait(&full[stage], phase);
+        const uint8_t* buf = ring + size_t(stage) * kMatchStageBytes;
+        float part8[4];
+        bool has[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int g = c * 1024 + tid + 256 * k;
+          has[k] = g < tile_vec;
+          part8[k] = 0.f;
+        }
+        uint4 av[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          av[k] = has[k] ? lds128(buf + size_t(tid + 256 * k) * 16) : make_uint4(0, 0, 0, 0);
+        mbar_arrive(&empty[stage]);                      // this thread's reads of the stage are done
+        if (++stage == NS) { stage = 0; phase ^= 1u; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int cc = 0; cc < kMatchTmaVec / 4; ++cc) {  // select the query vector of chunk c (unrolled)
+            if (cc == c && has[k]) {
+              part8[k] = sq_diff8(qv[cc * 4 + k], av[k]);
+              if ((qpos >> (cc * 4 + k)) & 1) acc1 += double(part8[k]); else acc0 += double(part8[k]);
+            }
+          }
+        }
+      }
+      acc0 = warp_sum_d(acc0);
+      acc1 = warp_sum_d(acc1);
+      if (lane == 0) {
+        part[(size_t(j) * kMatchWarps + warp) * 2] = acc0;
+        part[(size_t(j) * kMatchWarps + warp) * 2 + 1] = acc1;
+      }
+    }
+    named_bar_sync(1, kMatchThreads);                   // all warp partials of the item are in place
+    for (int t = tid; t < np * n_cand; t += kMatchThreads) {
+      const int p = t / n_cand, j = t - p * n_cand;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kMatchWarps; ++w) s += part[(size_t(j) * kMatchWarps + w) * 2 + p];
+      sd[p * n_cand + j] = sqrt(s);
+    }
+    named_bar_sync(1, kMatchThreads);
+    match_tail(a, jb, lb, i0, np, sd, nullptr, nullptr, nullptr, ints + a.cand_off, ints + a.s2c_off, ties, warp,
+               lane, tid);
+    named_bar_sync(1, kMatchThreads);                   // sd / part are reused by the next item
+  }
+  if (hdr->any_peer) __threadfence_system();
+}
+
+size_t match_tma_smem(int stages, int qbytes, int cmax) {
+  return size_t(stages) * kMatchStageBytes + 2 * size_t(qbytes) + size_t(cmax) * kMatchWarps * 2 * sizeof(double) +
+         2 * size_t(cmax) * sizeof(double) + (2 * size_t(stages) + 4) * sizeof(uint64_t);
 }
 
 // First pass of d̄ (and the cosine sums): block (job, c) sums position blocks
@@ -403,6 +589,22 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
 
 cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
   // (a rank that owns no position block still launches one block: it publishes its fingerprint)
+  if (hdr.tma) {
+    const size_t sm = match_tma_smem(hdr.tma_stages, hdr.tma_qbytes, hdr.tma_cmax);
+    static bool attr[64] = {false};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+      cudaError_t e = cudaFuncSetAttribute(match_dist_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(227 * 1024));
+      if (e != cudaSuccess) return e;
+      attr[dev & 63] = true;
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(hdr.total_blocks, sms));
+    match_dist_tma_kernel<<<grid, kMatchThreads + 32, sm, s>>>(reinterpret_cast<const uint8_t*>(table_dev));
+    return cudaGetLastError();
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));

@@ -201,11 +201,15 @@ __device__ __forceinline__ void fp8_accum(float (&acc)[2][NI][16], const float (
 #ifndef KVC_WARP_ARRIVE
 #define KVC_WARP_ARRIVE 0
 #endif
-constexpr int kArrivals = KVC_WARP_ARRIVE ? 1 : 32;
+constexpr int kArrivals = KVC_WARP_ARRIVE ? 1 : 32;  // empty-barrier arrivals per consumer warp
 #ifndef KVC_PROBE_VARIANTS
 #define KVC_PROBE_VARIANTS 0
 #endif
-constexpr bool kProbeVariants = KVC_PROBE_VARIANTS != 0;  // empty-barrier arrivals per consumer warp
+constexpr bool kProbeVariants = KVC_PROBE_VARIANTS != 0;
+#ifndef KVC_FP8_UNROLL
+#define KVC_FP8_UNROLL 2
+#endif
+constexpr int kFp8Unroll = KVC_FP8_UNROLL;  // fp8 anchor tiles per iteration (4 measured no faster than 2, and spills)
 __device__ __forceinline__ void stage_release(uint64_t* b) {
 #if KVC_WARP_ARRIVE
   __syncwarp();
@@ -387,24 +391,23 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const float* wv = suw + ub * (kUnitWBytes / 4);
       int c = c0;
       if (fp8) {
-        // two anchor tiles per iteration: both loaded and released before the decode
-        for (; c + 1 < c1; c += 2, wv += 2 * rw) {
-          float w0[2][kItemsPerThread], w1[2][kItemsPerThread];
-          uint4 code0[2][kItemsPerThread], code1[2][kItemsPerThread];
-          mbar_wait(&full[stage], phase);
-          const uint8_t* b0 = sdata + size_t(stage) * kStageStride;
-          fp8_load<kItemsPerThread>(w0, code0, b0, reinterpret_cast<const uint8_t*>(wv), b0 + scale_off, coff, roff);
-          stage_release(&empty[stage]);
-          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
-          mbar_wait(&full[stage], phase);
-          const uint8_t* b1 = sdata + size_t(stage) * kStageStride;
-          fp8_load<kItemsPerThread>(w1, code1, b1, reinterpret_cast<const uint8_t*>(wv + rw), b1 + scale_off, coff,
-                                    roff);
-          stage_release(&empty[stage]);
-          if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+        // kFp8Unroll anchor tiles per iteration, all loaded and released before the decode
+        // (amortises the per-tile barrier / stage bookkeeping over more elements)
+        for (; c + kFp8Unroll - 1 < c1; c += kFp8Unroll, wv += kFp8Unroll * rw) {
+          float wq[kFp8Unroll][2][kItemsPerThread];
+          uint4 cq[kFp8Unroll][2][kItemsPerThread];
+#pragma unroll
+          for (int a = 0; a < kFp8Unroll; ++a) {
+            mbar_wait(&full[stage], phase);
+            const uint8_t* ba = sdata + size_t(stage) * kStageStride;
+            fp8_load<kItemsPerThread>(wq[a], cq[a], ba, reinterpret_cast<const uint8_t*>(wv + a * rw), ba + scale_off,
+                                      coff, roff);
+            stage_release(&empty[stage]);
+            if (++stage == kNStage) { stage = 0; phase ^= 1u; }
+          }
           if (!skip_math) {
-            fp8_accum<kItemsPerThread>(acc, w0, code0);
-            fp8_accum<kItemsPerThread>(acc, w1, code1);
+#pragma unroll
+            for (int a = 0; a < kFp8Unroll; ++a) fp8_accum<kItemsPerThread>(acc, wq[a], cq[a]);
           }
         }
       }

@@ -32,6 +32,16 @@ RAW_KEYS = [
 ]
 
 
+def realign_src_hash():
+    """sha256 of the sources that define the realign kernel (bench.py computes the same
+    hash and reports the committed DRAM traffic only for the build it was captured on)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("realign.cu", "kvcomm_internal.h", "ptx.cuh", "Makefile"):
+        h.update(open(os.path.join(ROOT, "paper_2510_12872_b200", "csrc", f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def to_us(v, unit):
     v = float(v.replace(",", ""))
     return {"ns": v / 1e3, "nsecond": v / 1e3, "us": v, "usecond": v, "ms": v * 1e3, "msecond": v * 1e3}.get(unit, v)
@@ -126,7 +136,8 @@ def main():
         t_ms = to_us(*d["gpu__time_duration.sum"]) / 1e3
         js = {"source": f"profiles/{tag}{sfx}_ncu_realign.txt (ncu --set full, 1 launch, bench.py --profile)",
               "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
-              "duration_ms_under_ncu": t_ms, "dram_gbs_under_ncu": (rd + wr) / (t_ms / 1e3) / 1e9}
+              "duration_ms_under_ncu": t_ms, "dram_gbs_under_ncu": (rd + wr) / (t_ms / 1e3) / 1e9,
+              "realign_src_sha": realign_src_hash()}
         json.dump(js, open(os.path.join(PROF, f"realign_ncu{sfx}.json"), "w"), indent=1)
         print(json.dumps(js, indent=1))
 

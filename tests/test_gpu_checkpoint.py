@@ -178,7 +178,7 @@ def test_pool_load_rejects_corrupt_slot_metadata(tmp_path):
     back = K.AnchorPool.load(path)   # the unmodified file loads
     back.destroy()
     accepted = []
-    for field, value in ((16, next_index), (16, 1), (24, 1 << len(P))):
+    for field, value in ((16, next_index), (16, 2), (24, 1 << len(P))):   # slot 2 holds index 2
         bad = bytearray(data)
         struct.pack_into("<q", bad, slot0 + field, value)
         open(path, "wb").write(bytes(bad))

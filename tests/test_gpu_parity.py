@@ -546,3 +546,23 @@ def test_fp8_measure_interleaved_close_to_oracle():
     got = ck.cpu().view(torch.float8_e4m3fn).double().numpy() * harness.f64(sk)[..., None]
     amax = np.max(np.abs(odk), axis=-1, keepdims=True)
     assert np.all(np.abs(got - odk) <= 2.0 ** -3 * np.abs(odk) + 2.0 ** -9 * amax / 448 + 1e-6)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("De,L_phi", [(64, 33), (8192, 9)])
+def test_match_tma_variant_matches_oracle(De, L_phi):
+    """The opt-in TMA-ring distance kernel (KVCOMM_MATCH_TMA=1, a measured-slower
+    measurement variant) must still match the oracle: a small D_e (many
+    anchor tiles per stage) and D_e = 8192 (each anchor tile split in two 16 KiB chunks),
+    an odd L_φ (a one-position last block)."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import synth; from tests import harness; "
+            "p = synth.make_problem(11, L=1, H=1, d=16, D_e=%d, L_phi=%d, anchor_lens=[%d, %d, %d], prefix_lens=[2], "
+            "target_start=3, pf_base_start=3); g = harness.run_gpu(p, gamma=0.9); o = harness.run_oracle(p, gamma=0.9); "
+            "harness.compare(g, o, p); print('ok')" % (root, De, L_phi, L_phi, L_phi + 4, L_phi + 1))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, KVCOMM_MATCH_TMA="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
