@@ -38,6 +38,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// As mbar_wait, with a suspend-time hint (ns): a waiting warp is suspended until the phase
+// completes or the hint elapses instead of re-polling, which leaves issue slots to the
+// warps that have work (hint 0 = no hint).
+template <uint32_t kHintNs>
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+  if constexpr (kHintNs == 0) {
+    mbar_wait(bar, parity);
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITH_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITH_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(kHintNs)
+        : "memory");
+  }
+}
+
 // L2 policy: streamed-once data (anchor offsets) should not displace reusable lines.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;

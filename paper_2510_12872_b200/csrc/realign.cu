@@ -210,6 +210,13 @@ constexpr bool kProbeVariants = KVC_PROBE_VARIANTS != 0;
 #define KVC_FP8_UNROLL 2
 #endif
 constexpr int kFp8Unroll = KVC_FP8_UNROLL;  // fp8 anchor tiles per iteration (4 measured no faster than 2, and spills)
+#ifndef KVC_WAIT_HINT
+#define KVC_WAIT_HINT 0
+#endif
+// consumers' waits on full stages: suspend-time hint in ns (0 = plain try_wait polling)
+__device__ __forceinline__ void consumer_wait(uint64_t* b, uint32_t parity) {
+  mbar_wait_hint<KVC_WAIT_HINT>(b, parity);
+}
 __device__ __forceinline__ void stage_release(uint64_t* b) {
 #if KVC_WARP_ARRIVE
   __syncwarp();
@@ -223,6 +230,9 @@ template <int kConsumerWarps, int kD>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     realign_kernel(const uint8_t* __restrict__ tab, int variant) {
   constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);
+  // tables that read an fp8 pool always launch the 16-warp instantiation (launch_realign), so
+  // the 8-warp one carries no e4m3 decode (keeps its registers for the bf16 stream)
+  constexpr bool kFp8Path = kConsumerWarps == 16;
   static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
   const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
@@ -387,10 +397,10 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
 
     for (int c0 = 0; c0 < n_cand; c0 += chunk) {
       const int c1 = min(n_cand, c0 + chunk);
-      mbar_wait(&uw_full[ub], uphase);
+      consumer_wait(&uw_full[ub], uphase);
       const float* wv = suw + ub * (kUnitWBytes / 4);
       int c = c0;
-      if (fp8) {
+      if (kFp8Path && fp8) {
         // kFp8Unroll anchor tiles per iteration, all loaded and released before the decode
         // (amortises the per-tile barrier / stage bookkeeping over more elements)
         for (; c + kFp8Unroll - 1 < c1; c += kFp8Unroll, wv += kFp8Unroll * rw) {
@@ -398,7 +408,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
           uint4 cq[kFp8Unroll][2][kItemsPerThread];
 #pragma unroll
           for (int a = 0; a < kFp8Unroll; ++a) {
-            mbar_wait(&full[stage], phase);
+            consumer_wait(&full[stage], phase);
             const uint8_t* ba = sdata + size_t(stage) * kStageStride;
             fp8_load<kItemsPerThread>(wq[a], cq[a], ba, reinterpret_cast<const uint8_t*>(wv + a * rw), ba + scale_off,
                                       coff, roff);
@@ -412,11 +422,11 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
         }
       }
       for (; c < c1; ++c, wv += rw) {
-        mbar_wait(&full[stage], phase);
+        consumer_wait(&full[stage], phase);
         const uint8_t* buf = sdata + size_t(stage) * kStageStride;
         // operands -> registers, release the stage to the producer, then the math: the
         // stage is held only for the shared-memory loads (more bytes in flight)
-        if (fp8) {
+        if (kFp8Path && fp8) {
           float w[2][kItemsPerThread];
           uint4 code[2][kItemsPerThread];
           fp8_load<kItemsPerThread>(w, code, buf, reinterpret_cast<const uint8_t*>(wv), buf + scale_off, coff, roff);
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       const int r0 = s * rpt;
       if (r0 >= nrows) break;
       const int srows = min(rpt, nrows - r0);
-      mbar_wait(&full[stage], phase);
+      consumer_wait(&full[stage], phase);
       uint8_t* buf = sdata + size_t(stage) * kStageStride;
       if (n_cand > 0 || rotate) {  // COPY segments leave the staged rows untouched (bit-exact)
 #pragma unroll
@@ -589,7 +599,7 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   }
   // 8 consumer warps stream bf16 pools at the HBM roofline; the e4m3 decode of fp8
   // pools issues ~2x the instructions per byte and runs ~4 % faster with 16 (profiles/)
-  const int cw = cw_env == 8 || cw_env == 16 ? cw_env : (hdr.any_fp8 ? 16 : 8);
+  const int cw = hdr.any_fp8 ? 16 : (cw_env == 16 ? 16 : 8);  // fp8 decode: 16-warp instantiation only
   if (hdr.n_seg <= 0) return cudaSuccess;
   realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
   if (hdr.total_units <= 0) return cudaGetLastError();
