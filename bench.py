@@ -372,14 +372,18 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- e2e
 
-def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, deliver):
+def run_e2e(args, st, req, kv, stream, world, rank, w, total_tokens, dist, set0, make_set):
     """The same step through the public API with HOST buffers: every step copies the
-    request's inputs (query embeddings of the 5 samples + their base caches; the
-    prefix / p_(m,0) caches are per-template and stay resident) from pinned host
-    memory and reads the 5 realigned prompt caches back into pinned host memory.
-    N = 1: double-buffered over two plans and three streams (H2D of step t+1 and
-    D2H of step t-1 overlap the compute of step t).  N > 1: sequential per step."""
-    from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
+    request's inputs (query embeddings of the 5 samples + this rank's block of their base
+    caches; the prefix / p_(m,0) caches are per-template and stay resident) from pinned
+    host memory and reads the realigned prompt caches back into pinned host memory (N > 1:
+    each consumer rank reads the full caches of the agents it hosts).  Double-buffered
+    over two plans and three streams: the H2D of step t+1 and the D2H of step t-1 overlap
+    the compute (+ delivery to the consumer GPUs) of step t.
+
+    set0 / make_set(1): dict(req, agents, queries, bases, outs, deliver) — outs are the
+    device caches this rank copies back (its agents' destinations at N = 1, the full
+    caches it hosts at N > 1)."""
     pinned_q = {n: q.cpu().pin_memory() for n, q in st.queries.items()}
     bases = {}
     for a in st.agents:
@@ -387,82 +391,13 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
             if sg.kind == kv.PLACEHOLDER and sg.pool not in bases:
                 bases[sg.pool] = (sg.base_k.cpu().pin_memory(), sg.base_v.cpu().pin_memory())
     h2d = sum(q.numel() * 2 for q in pinned_q.values()) + sum(b[0].numel() * 4 for b in bases.values())
-
-    if world > 1:
-        host_out = [(torch.empty(f[0].shape, dtype=torch.bfloat16, pin_memory=True),
-                     torch.empty(f[1].shape, dtype=torch.bfloat16, pin_memory=True)) if f[0] is not None else None
-                    for f in full]
-        d2h = sum(f[0].numel() * 4 for f in full if f[0] is not None)
-        dev_bases = {}
-        for a in st.agents:
-            for sg in a.segments:
-                if sg.kind == kv.PLACEHOLDER:
-                    dev_bases[sg.pool] = (sg.base_k, sg.base_v)
-        qlist = [st.queries[n] for n in req.names]
-
-        def e2e_step():
-            for n, q in pinned_q.items():
-                st.queries[n].copy_(q, non_blocking=True)
-            for n, (hk, hv) in bases.items():
-                dev_bases[n][0].copy_(hk, non_blocking=True)
-                dev_bases[n][1].copy_(hv, non_blocking=True)
-            req.launch(qlist, stream=stream)
-            deliver()
-            for f, ho in zip(full, host_out):
-                if ho is not None:
-                    ho[0].copy_(f[0], non_blocking=True)
-                    ho[1].copy_(f[1], non_blocking=True)
-
-        for _ in range(2):
-            e2e_step()
-        torch.cuda.synchronize()
-        dist.barrier()
-        k2 = max(3, args.steps // 3)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(k2):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        el2 = e0.elapsed_time(e1)
-        t = torch.tensor([el2], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el2 = float(t.item())
-        return {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": False}
-
-    # two buffer sets: set 0 = the bench state, set 1 = clones of the per-request inputs/outputs
-    sets = []
-    for b in range(2):
-        if b == 0:
-            agents, queries = st.agents, st.queries
-        else:
-            queries = {n: torch.empty_like(q) for n, q in st.queries.items()}
-            dev_b = {}
-            for a in st.agents:
-                for sg in a.segments:
-                    if sg.kind == kv.PLACEHOLDER and sg.pool not in dev_b:
-                        dev_b[sg.pool] = (torch.empty_like(sg.base_k), torch.empty_like(sg.base_v))
-            agents = []
-            for a in st.agents:
-                segs = [SegmentLayout(sg.kind, sg.pool, sg.consumer,
-                                      dev_b[sg.pool][0] if sg.kind == kv.PLACEHOLDER else sg.base_k,
-                                      dev_b[sg.pool][1] if sg.kind == kv.PLACEHOLDER else sg.base_v,
-                                      sg.base_start, sg.target_start) for sg in a.segments]
-                agents.append(AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, segs, torch.empty_like(a.dst_k),
-                                          torch.empty_like(a.dst_v)))
-        r = req if b == 0 else ReuseRequest(st.pools, agents, gamma=req.gamma, top_k=req.top_k)
-        dev_bases = {}
-        for a in agents:
-            for sg in a.segments:
-                if sg.kind == kv.PLACEHOLDER:
-                    dev_bases[sg.pool] = (sg.base_k, sg.base_v)
-        host_out = [(torch.empty(a.dst_k.shape, dtype=torch.bfloat16, pin_memory=True),
-                     torch.empty(a.dst_v.shape, dtype=torch.bfloat16, pin_memory=True)) for a in agents]
-        sets.append(dict(req=r, agents=agents, queries=queries, bases=dev_bases, host_out=host_out,
-                         qlist=[queries[n] for n in r.names],
-                         ev_in=torch.cuda.Event(), ev_comp=torch.cuda.Event(), ev_out=torch.cuda.Event()))
-    d2h = sum(a.dst_k.numel() * 4 for a in st.agents)
+    sets = [set0, make_set(1)]
+    for S in sets:
+        S["host_out"] = [(torch.empty(o[0].shape, dtype=torch.bfloat16, pin_memory=True),
+                          torch.empty(o[1].shape, dtype=torch.bfloat16, pin_memory=True)) for o in S["outs"]]
+        S["qlist"] = [S["queries"][n] for n in S["req"].names]
+        S["ev_in"], S["ev_comp"], S["ev_out"] = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
+    d2h = sum(o[0].numel() * 4 for o in set0["outs"])
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     for S in sets:                      # events start "complete"
         for e in (S["ev_comp"], S["ev_out"]):
@@ -480,18 +415,21 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
             S["ev_in"].record(s_in)
         stream.wait_event(S["ev_in"])
         stream.wait_event(S["ev_out"])                # step t-2's results have left this output set
-        S["req"].plan.run(S["qlist"], sync=False, stream=stream)
+        S["req"].launch(S["qlist"], stream=stream)
+        S["deliver"]()                                # N > 1: every rank's rows are in the consumers' caches
         S["ev_comp"].record(stream)
         with torch.cuda.stream(s_out):
             s_out.wait_event(S["ev_comp"])
-            for a, (hk, hv) in zip(S["agents"], S["host_out"]):
-                hk.copy_(a.dst_k, non_blocking=True)
-                hv.copy_(a.dst_v, non_blocking=True)
+            for o, (hk, hv) in zip(S["outs"], S["host_out"]):
+                hk.copy_(o[0], non_blocking=True)
+                hv.copy_(o[1], non_blocking=True)
             S["ev_out"].record(s_out)
 
     for t in range(2):
         e2e_step(t)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     k2 = max(4, args.steps // 3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -507,11 +445,20 @@ def run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist,
         if res.fallback_agents:
             raise SystemExit(f"e2e: agents {res.fallback_agents} fell back")
         # what reached the host is what the device computed last in this buffer set
-        for a, (hk, hv) in zip(S["agents"], S["host_out"]):
-            if not (torch.equal(hk, a.dst_k.cpu()) and torch.equal(hv, a.dst_v.cpu())):
-                raise SystemExit(f"e2e: host copy of agent {a.agent} differs from the device result")
+        for o, (hk, hv) in zip(S["outs"], S["host_out"]):
+            if not (torch.equal(hk, o[0].cpu()) and torch.equal(hv, o[1].cpu())):
+                raise SystemExit("e2e: a host copy differs from the device result")
+    if world > 1:
+        dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+        tm = torch.tensor([el2], device=dev, dtype=torch.float64)
+        tb = torch.tensor([float(d2h)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        el2, d2h = float(tm.item()), float(tb.item())
     return {"value": total_tokens * k2 / (el2 / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": True, "host_result_checked": True}
+            "d2h_bytes_per_step": int(d2h), "steps": k2, "pipelined": True, "host_result_checked": True,
+            **({"bytes_note": "h2d: this rank's (rank 0's) copies; d2h: summed over the consumer ranks"}
+               if world > 1 else {})}
 
 
 # --------------------------------------------------------------------------- ours
@@ -603,12 +550,64 @@ def main():
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
 
-    def deliver():
+    def deliver_for(peer_b, agents_b, full_b):
+        def deliver():
+            if peer_b is not None:
+                peer_b.sync()
+            elif world > 1:
+                shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in agents_b], full_b, w.L, rank,
+                                          world, head_groups=hg)
+        return deliver
+
+    deliver = deliver_for(peer, st.agents, full)
+
+    def set_bases(agents_b):
+        out = {}
+        for a in agents_b:
+            for sg in a.segments:
+                if sg.kind == kv.PLACEHOLDER:
+                    out[sg.pool] = (sg.base_k, sg.base_v)
+        return out
+
+    def outs_of(agents_b, full_b):
+        if world == 1:
+            return [(a.dst_k, a.dst_v) for a in agents_b]
+        return [f for f in full_b if f[0] is not None]
+
+    set0 = dict(req=req, agents=req.agents, queries=st.queries, bases=set_bases(req.agents),
+                outs=outs_of(req.agents, full), deliver=deliver)
+
+    def make_set(b):
+        """A second buffer set for the pipelined e2e run: its own plan, input buffers and
+        output caches (N > 1: its own consumer caches, IPC-mapped for the fused gather)."""
+        from paper_2510_12872_b200.request import AgentLayout, ReuseRequest, SegmentLayout
+        queries = {n: torch.empty_like(q) for n, q in st.queries.items()}
+        dev_b = {}
+        for a in st.agents:
+            for sg in a.segments:
+                if sg.kind == kv.PLACEHOLDER and sg.pool not in dev_b:
+                    dev_b[sg.pool] = (torch.empty_like(sg.base_k), torch.empty_like(sg.base_v))
+        peer_b, full_b = None, []
         if peer is not None:
-            peer.sync()
+            peer_b = shard.PeerCaches([(a.agent, a.N) for a in st.agents], w.L, w.H, w.d, rank, world, local)
+            full_b = [peer_b.full(i) for i in range(len(st.agents))]
         elif world > 1:
-            shard.gather_to_consumers(agents_all, [(a.dst_k, a.dst_v) for a in st.agents], full, w.L, rank, world,
-                                      head_groups=hg)
+            full_b = [(torch.empty_like(f[0]), torch.empty_like(f[1])) if f[0] is not None else (None, None)
+                      for f in full]
+        agents_b = []
+        for i, a in enumerate(st.agents):
+            segs = [SegmentLayout(sg.kind, sg.pool, sg.consumer,
+                                  dev_b[sg.pool][0] if sg.kind == kv.PLACEHOLDER else sg.base_k,
+                                  dev_b[sg.pool][1] if sg.kind == kv.PLACEHOLDER else sg.base_v,
+                                  sg.base_start, sg.target_start) for sg in a.segments]
+            dst = peer_b.destinations(i, lr, hr) if peer_b is not None else (torch.empty_like(a.dst_k),
+                                                                              torch.empty_like(a.dst_v))
+            agents_b.append(AgentLayout(a.agent, a.N, a.p0_k, a.p0_v, segs, *dst))
+        req_b = ReuseRequest(st.pools, agents_b, gamma=req.gamma, top_k=req.top_k)
+        if getattr(req, "_mshard", None) is not None:
+            req_b.shard_matching(rank, world, local)
+        return dict(req=req_b, agents=agents_b, queries=queries, bases=set_bases(agents_b),
+                    outs=outs_of(agents_b, full_b), deliver=deliver_for(peer_b, agents_b, full_b))
 
     # With sharded matching and the fused gather, the cross-rank barrier inside step t+1
     # (after every rank's distance kernel, hence after its realign of step t) already
@@ -702,7 +701,7 @@ def main():
     # ------------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, st, req, kv, stream, world, rank, full, w, total_tokens, dist, deliver)
+        e2e = run_e2e(args, st, req, kv, stream, world, rank, w, total_tokens, dist, set0, make_set)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -729,6 +728,8 @@ def main():
                                         "(K+V of this rank's layers and heads)",
                          **({"peer_bytes_per_launch": peer_bytes, "peer_ref_gbs": 770.0,
                              "peer_bound_ms": peer_bytes / 770e9 * 1e3,
+                             "peer_store": "tma-bulk" if os.environ.get("KVCOMM_PEER_STORE") == "bulk"
+                             else "per-thread 16 B",
                              "peer_note": "fused gather: rows this rank stores into consumer GPUs over NVLink; "
                                           "ref = measured peer copy per direction (B200_PROFILING.md)"}
                             if peer is not None else {})},

@@ -1349,8 +1349,12 @@ static kvcomm_status validate_segment(const kvcomm_realign_desc& g, int idx) {
 }
 
 // Destinations on another GPU (a consumer's cache mapped by CUDA IPC: the fused gather,
-// SURVEY §8(e)) are written with per-thread stores; KVCOMM_STORE_STG=1 forces that path
-// everywhere (tests compare it with the TMA bulk-store path bit for bit).
+// SURVEY §8(e)) are written with per-thread stores (mode 1) by default, or — measurement
+// knob KVCOMM_PEER_STORE=bulk, for the first multi-GPU run — with the same TMA bulk store
+// as local rows, issued to the peer address (mode 2; one 16 KiB transfer per tile instead
+// of 1,024 16-byte stores).  Either way the kernel ends with a system-scope fence.
+// KVCOMM_STORE_STG=1 forces per-thread stores everywhere (tests compare that path with
+// the TMA bulk-store path bit for bit).
 static int32_t dst_store_mode(const void* dst, int device) {
   const char* e = getenv("KVCOMM_STORE_STG");
   if (e && atoi(e) == 1) return 1;
@@ -1359,7 +1363,12 @@ static int32_t dst_store_mode(const void* dst, int device) {
     cudaGetLastError();
     return 0;
   }
-  return (at.type == cudaMemoryTypeDevice && at.device != device) ? 1 : 0;
+  if (!(at.type == cudaMemoryTypeDevice && at.device != device)) return 0;
+  static const bool bulk = [] {
+    const char* v = getenv("KVCOMM_PEER_STORE");
+    return v && std::strcmp(v, "bulk") == 0;
+  }();
+  return bulk ? 2 : 1;
 }
 
 static HostSeg host_segment(const kvcomm_realign_desc& g, int32_t dst_stg = -1) {

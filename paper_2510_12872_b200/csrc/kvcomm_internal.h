@@ -61,7 +61,8 @@ struct SegDev {
                         //   members so the shared base tile is read from HBM once and hit in L2 after)
   int32_t fp8;          // offsets stored as blocked e4m3 codes + row scales
   int64_t wt_off;       // float offset of this segment's weight blocks in Table::wt
-  int32_t dst_stg;      // 1: write rows with per-thread stores (destination on a peer GPU, mapped by
+  int32_t dst_stg;      // 0: local rows, TMA bulk store; 2: peer rows, TMA bulk store to the peer address;
+                        // 1: write rows with per-thread stores (destination on a peer GPU, mapped by
                         //   CUDA IPC: the fused gather of SURVEY §8(e)), 0: TMA bulk store
   int32_t rope_il;      // K's RoPE pairs: 0 (f, f + d/2) rotate_half, 1 (2f, 2f + 1) interleaved
   int32_t dst_heads;    // heads per layer of the destination layout (>= Hs): a head shard writes its
@@ -79,7 +80,7 @@ struct MatchResultDev {
 struct TableHdr {
   int32_t n_seg, d, Ls, Hs;
   int32_t rows_per_tile, any_fp8;  // any_fp8: some segment reads an fp8 pool
-  int32_t any_stg, _pad1;          // any_stg: some segment writes with per-thread (peer) stores
+  int32_t any_stg, _pad1;          // any_stg: some segment writes peer rows (system-scope fence at the end)
   int64_t total_units;
   // byte offsets from the table base
   int64_t seg_off, cand_off, cs_off, wt_off;

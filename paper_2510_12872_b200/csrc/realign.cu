@@ -385,7 +385,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     const bool rope_il = g.rope_il;
     const float2* csg = cs + g.cs_off;
     bf16* const dst = g.dst[un.p] + ((int64_t(un.l) * g.dst_heads + un.h) * g.dst_ld + g.target_start + i0) * d;
-    const bool tstore = tma_store && !g.dst_stg;  // peer destinations: per-thread stores
+    const bool tstore = tma_store && g.dst_stg != 1;  // dst_stg 1: peer rows with per-thread stores
     float* const dbg = g.dbg[un.p] != nullptr ? g.dbg[un.p] + (lh * g.L_seg + i0) * d : nullptr;
     float acc[2][kItemsPerThread][16];  // [64-row tile of the unit][item][element]
 #pragma unroll
