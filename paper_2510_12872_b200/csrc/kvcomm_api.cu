@@ -138,7 +138,10 @@ struct kvcomm_pool_s {
   int64_t pf_plane_stride(int c) const { return int64_t(Ls) * Hs * pf_ld(c) * d; }
 };
 
-static constexpr int kMatchP = 2;  // positions per match work item
+#ifndef KVC_MATCH_P
+#define KVC_MATCH_P 2
+#endif
+static constexpr int kMatchP = KVC_MATCH_P;  // positions per match work item
 
 int64_t kvcomm_pool_s::emb_row_count(int64_t L) const {
   if (emb_world <= 1) return L;
@@ -1105,13 +1108,14 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   RealignLayout L;
   const int n_seg = int(hs.size());
   const int rpt = rows_per_tile(d);
-  size_t n_ints = 0, n_wt = 0;
+  size_t n_ints = 0, n_wt = 0, n_units = 0;
   for (const HostSeg& g : hs) {
     n_ints += g.x.n_cand + g.gates.size();
     if (g.x.fp8) L.hdr.any_fp8 = 1;
     if (g.x.dst_stg) L.hdr.any_stg = 1;
     const int rpu = unit_rows(d, g.x.fp8);
     n_wt += size_t((g.x.L_seg + rpu - 1) / rpu) * g.x.n_cand * weight_row_stride(rpu);
+    n_units += size_t(Ls) * Hs * 2 * size_t((g.x.L_seg + rpu - 1) / rpu);
   }
   TableHdr& hdr = L.hdr;
   hdr.n_seg = n_seg;
@@ -1128,6 +1132,8 @@ RealignLayout layout_realign(int d, int Ls, int Hs, const std::vector<HostSeg>& 
   off = align_up(off + sizeof(float2) * (d / 2) * n_seg, 64);
   hdr.wt_off = int64_t(off);
   off = align_up(off + sizeof(float) * n_wt, 64);
+  hdr.unit_off = int64_t(off);
+  off = align_up(off + sizeof(UnitDev) * std::max<size_t>(n_units, 1), 64);
   L.bytes = off;
   return L;
 }
@@ -1175,6 +1181,7 @@ void write_realign(uint8_t* h, uint8_t* dev, RealignLayout& L, const std::vector
       x.tiles = tiles;
       x.unit_begin = units;
       x.group_size = G;
+      x.group_member = t - t0;
       x.wt = dwt + tpos;
       x.wt_off = tpos;
       tpos += int64_t(tiles) * x.n_cand * weight_row_stride(rpu);

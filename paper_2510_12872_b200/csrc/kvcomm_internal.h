@@ -67,7 +67,15 @@ struct SegDev {
   int32_t rope_il;      // K's RoPE pairs: 0 (f, f + d/2) rotate_half, 1 (2f, 2f + 1) interleaved
   int32_t dst_heads;    // heads per layer of the destination layout (>= Hs): a head shard writes its
                         //   [Ls][Hs] block into a consumer's full [L][H][N][d] cache (70B grid, §9)
-  int32_t _pad_dst;
+  int32_t group_member;  // index of this segment within its group (0 .. group_size-1)
+};
+
+// One realign work unit as the prep kernel lays it out (UnitDev[total_units] at
+// TableHdr::unit_off): the persistent kernel reads one 16-byte descriptor per unit
+// instead of decoding the unit index (binary search over segments + 64-bit divisions,
+// once per warp per unit).  s = -1: the segment's gate is closed (Alg. 1 branch).
+struct UnitDev {
+  int32_t s, l, h, tp;  // segment, layer, head, (tile << 1) | plane
 };
 
 struct MatchResultDev {
@@ -83,7 +91,7 @@ struct TableHdr {
   int32_t any_stg, _pad1;          // any_stg: some segment writes peer rows (system-scope fence at the end)
   int64_t total_units;
   // byte offsets from the table base
-  int64_t seg_off, cand_off, cs_off, wt_off;
+  int64_t seg_off, cand_off, cs_off, wt_off, unit_off;
   const MatchResultDev* gate_results;  // verdicts the segments' gates index (device), or null
 };
 

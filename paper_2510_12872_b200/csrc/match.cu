@@ -35,7 +35,10 @@ constexpr double kTieRel = 1e-6;
 #ifndef KVC_MATCH_UNROLL
 #define KVC_MATCH_UNROLL 8
 #endif
-constexpr int kMatchUnroll = KVC_MATCH_UNROLL;  // 16-byte anchor loads in flight per lane (8 vs 4: match 2-5 % faster)
+constexpr int kMatchUnroll = KVC_MATCH_UNROLL;
+#ifndef KVC_MATCH_MINB
+#define KVC_MATCH_MINB 1
+#endif  // 16-byte anchor loads in flight per lane (8 vs 4: match 2-5 % faster)
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -296,7 +299,7 @@ __device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, in
 // per-job tie counters, zeroed by the host upload), so the last wave has no tail of
 // idle SMs.  Sharded matching: the items are this rank's position blocks only.  The processing order does not affect any result: every item writes its
 // own W columns and partial sums.
-__global__ void __launch_bounds__(kMatchThreads) match_dist_kernel(const uint8_t* __restrict__ tab) {
+__global__ void __launch_bounds__(kMatchThreads, KVC_MATCH_MINB) match_dist_kernel(const uint8_t* __restrict__ tab) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
   int32_t* counter = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off) + hdr->n_jobs;
   __shared__ int s_item;

@@ -54,42 +54,9 @@ constexpr size_t realign_smem_bytes() {
 }
 static_assert(realign_smem_bytes() <= 227 * 1024, "realign shared memory");
 
-__device__ __forceinline__ int find_segment(const SegDev* segs, int n_seg, int64_t u) {
-  int lo = 0, hi = n_seg - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].unit_begin <= u) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
 struct Unit {
   int s, l, h, p, t;
 };
-
-// unit -> (segment, layer, head, plane, tile), tile fastest so that neighbouring CTAs
-// stream neighbouring tiles of the same anchor at the same time.  Segments that share
-// one base cache (one sample realigned for several consumers) form a group whose
-// members are interleaved just outside the tile index: all members' units of one
-// (layer, head, plane) fall in the same round of CTAs, so the shared base tile is
-// fetched from HBM once and hit in L2 by the other members.
-__device__ __forceinline__ Unit decode_unit(const SegDev* segs, int n_seg, int Hs, int64_t u) {
-  Unit r;
-  const int last = find_segment(segs, n_seg, u);   // last member of the unit's group
-  int64_t rem = u - segs[last].unit_begin;
-  const int G = segs[last].group_size;
-  const int tiles = segs[last].tiles;              // equal for every member
-  r.t = int(rem % tiles);
-  rem /= tiles;
-  const int member = int(rem % G);
-  rem /= G;
-  r.s = last - (G - 1) + member;
-  r.p = int(rem & 1);
-  rem >>= 1;
-  r.h = int(rem % Hs);
-  r.l = int(rem / Hs);
-  return r;
-}
 
 // Device-side branch of Algorithm 1: a segment of an agent is realigned only
 // if every placeholder pool the agent depends on was matched Shareable.
@@ -99,8 +66,26 @@ __device__ __forceinline__ bool seg_open(const TableHdr& hdr, const int32_t* int
   return true;
 }
 
-// Per-segment preparation (grid n_seg x kPrepY): cos/sin of δ·inv_freq (fp64 angle,
-// reading A13) and the weight blocks wt[tile][j][row] = weight of candidate j at the
+// The prep kernel's unit list (UnitDev at unit_off): tile fastest so that neighbouring
+// CTAs stream neighbouring tiles of the same anchor at the same time.  Segments that
+// share one base cache (one sample realigned for several consumers) form a group whose
+// members are interleaved just outside the tile index: all members' units of one
+// (layer, head, plane) fall in the same round of CTAs, so the shared base tile is
+// fetched from HBM once and hit in L2 by the other members.
+//   u = unit_begin + (((l * Hs + h) * 2 + p) * group_size + member) * tiles + t
+__device__ __forceinline__ Unit load_unit(const UnitDev* units, int64_t u) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(units + u));
+  Unit r;
+  r.s = v.x;
+  r.l = v.y;
+  r.h = v.z;
+  r.p = v.w & 1;
+  r.t = v.w >> 1;
+  return r;
+}
+
+// Per-segment preparation (grid n_seg x kPrepY): the segment's entries of the unit list,
+// cos/sin of δ·inv_freq (fp64 angle, reading A13) and the weight blocks wt[tile][j][row] = weight of candidate j at the
 // tile's token row (0 past L_seg), from W[slot] (PLACEHOLDER) or w̄[slot] (PREFIX),
 // so the main kernel fetches a unit's weights as contiguous chunks.
 constexpr int kPrepY = 8;
@@ -117,6 +102,25 @@ __global__ void realign_prep_kernel(uint8_t* tab) {
       double sn, cn;
       sincos(double(g.delta) * g.inv_freq[f], &sn, &cn);
       cs[g.cs_off + f] = make_float2(float(cn), float(sn));
+    }
+  }
+  {  // this segment's entries of the unit list (s = -1: gate closed, every unit skipped)
+    UnitDev* units = reinterpret_cast<UnitDev*>(tab + hdr->unit_off);
+    const int32_t* ints = cand;
+    const bool open = seg_open(*hdr, ints, g);
+    const uint32_t tiles = uint32_t(g.tiles), G = uint32_t(g.group_size);
+    const uint32_t nu = uint32_t(hdr->Ls) * uint32_t(hdr->Hs) * 2u * tiles;  // < 2^31: host-validated sizes
+    for (uint32_t x = blockIdx.y * blockDim.x + threadIdx.x; x < nu; x += gridDim.y * blockDim.x) {
+      const uint32_t lhp = x / tiles;
+      const uint32_t t = x - lhp * tiles;
+      const uint32_t lh = lhp >> 1;
+      const uint32_t l = lh / uint32_t(hdr->Hs);
+      UnitDev v;
+      v.s = open ? int32_t(blockIdx.x) : -1;
+      v.l = int32_t(l);
+      v.h = int32_t(lh - l * uint32_t(hdr->Hs));
+      v.tp = int32_t((t << 1) | (lhp & 1u));
+      units[g.unit_begin + (int64_t(lhp) * G + uint32_t(g.group_member)) * tiles + t] = v;
     }
   }
   if (g.n_cand == 0) return;
@@ -227,8 +231,7 @@ __device__ __forceinline__ void stage_release(uint64_t* b) {
 }
 
 template <int kConsumerWarps, int kD>
-__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
-    realign_kernel(const uint8_t* __restrict__ tab, int variant) {
+__device__ __forceinline__ void realign_body(const uint8_t* __restrict__ tab, int variant) {
   constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);
   // tables that read an fp8 pool always launch the 16-warp instantiation (launch_realign), so
   // the 8-warp one carries no e4m3 decode (keeps its registers for the bf16 stream)
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
   const int32_t* cand = reinterpret_cast<const int32_t*>(tab + hdr.cand_off);
   const float2* cs = reinterpret_cast<const float2*>(tab + hdr.cs_off);
+  const UnitDev* units = reinterpret_cast<const UnitDev*>(tab + hdr.unit_off);
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sdata = smem;                                                       // [kNStage][kStageStride]
@@ -284,9 +288,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
       int stage = 0, ub = 0;
       uint32_t phase = 0, uphase = 0;
       for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
-        const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
+        const Unit un = load_unit(units, u);
+        if (un.s < 0) continue;  // gate closed
         const SegDev& g = segs[un.s];
-        if (!seg_open(hdr, cand, g)) continue;
         // segment fields -> registers (the barrier asm's memory clobbers would reload them)
         const bool fp8 = g.fp8;
         const int n_cand = g.n_cand;
@@ -369,9 +373,9 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   int stage = 0, ub = 0;
   uint32_t phase = 0, uphase = 0;
   for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
-    const Unit un = decode_unit(segs, hdr.n_seg, Hs, u);
+    const Unit un = load_unit(units, u);
+    if (un.s < 0) continue;  // gate closed
     const SegDev& g = segs[un.s];
-    if (!seg_open(hdr, cand, g)) continue;
     // segment fields -> registers (the barrier asm's memory clobbers would reload them)
     const bool fp8 = g.fp8;
     const int n_cand = g.n_cand;
@@ -560,6 +564,15 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
   }
   if (tma_store && threadIdx.x == 0) bulk_wait_all();  // global writes complete before exit
   if (hdr.any_stg) __threadfence_system();  // peer-GPU rows: visible system-wide before the kernel ends
+}
+
+// The four instantiations (one CTA per SM: 8 + 1 warps for bf16 tables, 16 + 1 for
+// tables that read an fp8 pool; 17 warps leave 96 registers per thread, as ptxas allocates
+// for 20 warps).
+template <int kConsumerWarps, int kD>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
+    realign_kernel(const uint8_t* __restrict__ tab, int variant) {
+  realign_body<kConsumerWarps, kD>(tab, variant);
 }
 
 int realign_grid_size(int device) {
