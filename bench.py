@@ -615,9 +615,11 @@ def main():
     # needed only after the last step of a sequence.
     merged_barrier = peer is not None and getattr(req, "_mshard", None) is not None
 
-    def step(events=None, last=True):
+    def step(events=None, last=True, mevents=None):
         if events is not None:
             plan.set_events(*events)     # recorded right before / after the realign launch
+        if mevents is not None:
+            plan.set_match_events(*mevents)  # ... and the distance kernel
         req.launch(qlist, stream=stream)   # no host synchronisation inside a step
         if last or not merged_barrier:
             deliver()
@@ -655,19 +657,26 @@ def main():
     torch.cuda.synchronize()
     n_launch0 = kv.kernel_launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    mevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for i in range(args.steps):
-            step(evs[i], last=(i == args.steps - 1))
+            step(evs[i], last=(i == args.steps - 1), mevents=mevs[i])
         e1.record(stream)
         torch.cuda.synchronize()
     plan.set_events(None, None)
+    plan.set_match_events(None, None)
     n_launch = kv.kernel_launch_count() - n_launch0
     res = req.results()
     if res.fallback_agents:
         raise SystemExit(f"agents {res.fallback_agents} took the fallback branch during the timed steps")
     realign_ms = [a.elapsed_time(b) for a, b in evs]
+    match_ms = sum(a.elapsed_time(b) for a, b in mevs) / len(mevs)
+    # distance kernel bytes (a2): each query position reads its own row and the
+    # same row of every candidate anchor, D_e bf16 each; sharded matching splits positions
+    match_bytes = sum(q.shape[0] * (len(res.matches[n].candidates) + 1) * q.shape[1] * 2
+                      for n, q in zip(req.names, qlist)) / (world if getattr(req, "_mshard", None) is not None else 1)
     elapsed = e0.elapsed_time(e1)  # ms
     if world > 1:
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
@@ -723,6 +732,13 @@ def main():
                          "traffic": traffic, "traffic_source": traffic_src, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": realign_avg, "frac_of_8tbs": achieved / 8000.0,
                          "realign_share_of_step": realign_avg / ms_per_step,
+                         "match": {"kernel": "kvc::match_dist_kernel (distances + Eq. 6 weights, all pools, one launch)",
+                                   "bound": "hbm", "launch_ms": match_ms, "alg_bytes_per_launch": match_bytes,
+                                   "achieved": match_bytes / (match_ms / 1e3) / 1e9,
+                                   "frac": (match_bytes / (match_ms / 1e3) / 1e9 / peak) if peak else None,
+                                   "share_of_step": match_ms / ms_per_step,
+                                   "bytes_model": "per query position: its row + the same row of each candidate "
+                                                  "anchor, D_e x 2 B each"},
                          "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "
                                         f"base once + 2 per copied p0 token, x {row_bytes * Ls * 2 // 1024} KiB "
                                         "(K+V of this rank's layers and heads)",

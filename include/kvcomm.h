@@ -368,7 +368,13 @@ KVCOMM_API kvcomm_status kvcomm_realign_segments(const kvcomm_realign_desc* segs
 /* Checks that segs tile [0, N_total) in order (POSITION_GAP / POSITION_OVERLAP
  * otherwise, nothing launched) and copies the rows of segments with src.k != NULL
  * into dst [Ls][Hs][dst_ld][d] (dst_ld >= N_total) with the realign kernel's TMA ring
- * (one launch).  `device` = CUDA device of dst. */
+ * (one launch).  `device` = the CUDA device that runs the copy, normally dst's.
+ * Across GPUs (Alg. 1 P:777's concatenation on the GPU that prefills the consumer, with
+ * the request sharded by layer): dst may be the consumer's cache mapped into this
+ * process with kvcomm_ipc_open, offset to this rank's layer block; `device` stays the
+ * local device, the rows then leave with stores over NVLink and the launch ends with a
+ * system-scope fence — the caller orders the consumer's reads after it (e.g. a
+ * stream-ordered NCCL all-reduce of one word), as shard.PeerCaches does. */
 KVCOMM_API kvcomm_status kvcomm_concat_prefill_cache(const kvcomm_segment_ref* segs, int32_t n,
                                                      int32_t N_total, int32_t Ls, int32_t Hs,
                                                      int32_t d, void* dst_k, void* dst_v,
@@ -442,6 +448,10 @@ KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t plan, kvcomm_match_in
  * stream immediately before and after the realign launch of every later run; NULL
  * disables.  Lets a caller time the realign kernel alone inside a pipelined run. */
 KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before_realign, void* after_realign);
+/* Same for the distance kernel of Eq. 5/6 (a2, match_dist_kernel): events recorded right
+ * before and after it in every later run (NULL disables), so a caller can time the
+ * matching kernel alone (bench.py's roofline.match). */
+KVCOMM_API kvcomm_status kvcomm_plan_set_match_events(kvcomm_plan_t plan, void* before_match, void* after_match);
 /* Device pointers of the LAST run's weights for match `match` (W [capacity][ld_w], w̄;
  * runs alternate between two buffer sets). */
 KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, const float** W,
@@ -453,8 +463,10 @@ KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, 
  * would compute the same distances G times.  After kvcomm_plan_match_shard, each rank
  * computes only the position blocks b = rank (mod G) of every job (2 positions per block;
  * a pool created with emb_shard_rank/world = rank/G needs only those embedding rows) and stores those
- * W columns and d̄ partial rows into its own buffers AND every peer's (NVLink stores into
- * the peers' match buffers, mapped by CUDA IPC); the fixed-order d̄ reduction, w̄, H and
+ * W columns into its own W and d̄ partial rows into its own buffers, AND both into every
+ * peer's (NVLink stores into the peers' match buffers, mapped by CUDA IPC; W columns travel
+ * position-major — one contiguous run of `capacity` weights per position, coalesced — into
+ * an exchange area that run_end's first kernel copies into W); the fixed-order d̄ reduction, w̄, H and
  * the verdict then run on the complete arrays on every rank, so every rank's weights and
  * verdicts are bit-identical to an unsharded run.  A sharded run is split in two:
  *   kvcomm_plan_run_begin  (candidate filter, table upload, distance+weight kernel)

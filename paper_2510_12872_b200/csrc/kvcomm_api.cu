@@ -968,7 +968,8 @@ struct MatchItem {
   // sharded matching (plans only): own position blocks [own_lo, own_lo + n_own), n_own < 0 = all;
   // W columns and partial rows also stored into the peers' copies
   int own_lo = 0, n_own = -1, own_step = 1, n_peer = 0;
-  float* W_peer[kMaxMatchPeers] = {};
+  float* X = nullptr;                   // exchange rows (position-major), sharded only
+  float* X_peer[kMaxMatchPeers] = {};
   double* partial_peer[kMaxMatchPeers] = {};
 };
 
@@ -1084,8 +1085,9 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     a.n_own = it.n_own >= 0 ? it.n_own : a.n_blocks;
     blocks += a.n_own;
     a.n_peer = it.n_peer;
+    a.X = it.X;
     for (int r = 0; r < it.n_peer; ++r) {
-      a.W_peer[r] = it.W_peer[r];
+      a.X_peer[r] = it.X_peer[r];
       a.partial_peer[r] = it.partial_peer[r];
     }
   }
@@ -1554,7 +1556,7 @@ struct kvcomm_plan_s {
   // W [cap][ld_w] f32, w̄ [cap] f32, scratch [ceil(L_phi/P) + kMatchChunks][2 cap + 1] f64.
   void* xbuf = nullptr;
   int64_t xbytes = 0;
-  std::vector<int64_t> W_off[2], wbar_off[2], sc_off[2];  // byte offsets into xbuf
+  std::vector<int64_t> W_off[2], wbar_off[2], sc_off[2], X_off[2];  // byte offsets into xbuf
   int64_t fp_off[2] = {0, 0};     // per parity: uint64 fingerprints [kMaxMatchPeers + 1] (sharded runs)
   std::vector<int64_t> ld_w;
   // sharded matching: this rank's position blocks, and the peers' xbuf mappings
@@ -1576,6 +1578,7 @@ struct kvcomm_plan_s {
   std::vector<int32_t> agent_stg;    // destination store mode per agent (dst_store_mode at create)
   int64_t res_off = 0;
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
+  cudaEvent_t ev_mbefore = nullptr, ev_mafter = nullptr;  // around the distance kernel
   std::mutex mu;
 
   char* xb() const { return static_cast<char*>(xbuf); }
@@ -1691,6 +1694,8 @@ KVCOMM_API kvcomm_status kvcomm_plan_create(const kvcomm_plan_match* matches, in
       off = int64_t(align_up(size_t(off + int64_t(sizeof(double)) * (match_blocks(matches[i].L_phi) + kMatchChunks) *
                                               (2 * cap + 1)),
                              256));
+      pl->X_off[par].push_back(off);  // sharded matching's exchange rows [blocks * P][cap]
+      off = int64_t(align_up(size_t(off + int64_t(sizeof(float)) * match_blocks(matches[i].L_phi) * kMatchP * cap), 256));
     }
   for (int par = 0; par < 2; ++par) {
     pl->fp_off[par] = off;
@@ -1760,8 +1765,9 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
       it.own_step = pl->world;
       it.n_own = pl->rank < nb ? (nb - pl->rank + pl->world - 1) / pl->world : 0;
       it.n_peer = int(pl->peer_x.size());
+      it.X = reinterpret_cast<float*>(pl->xb() + pl->X_off[par][i]);
       for (int r = 0; r < it.n_peer; ++r) {
-        it.W_peer[r] = reinterpret_cast<float*>(pl->peer_x[r] + pl->W_off[par][i]);
+        it.X_peer[r] = reinterpret_cast<float*>(pl->peer_x[r] + pl->X_off[par][i]);
         it.partial_peer[r] = reinterpret_cast<double*>(pl->peer_x[r] + pl->sc_off[par][i]);
       }
     }
@@ -1852,7 +1858,9 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
   if (!hs.empty()) write_realign(h + roff, dv + roff, RL, hs, gres);
   KV_CUDA(cudaMemcpyAsync(dv, h, hs.empty() ? ML.bytes : roff + size_t(RL.hdr.cs_off), cudaMemcpyHostToDevice, s));
   if (match_table) {
+    if (pl->ev_mbefore) KV_CUDA(cudaEventRecord(pl->ev_mbefore, s));
     KV_CUDA(launch_match_dist(dv, ML.hdr, ML.smem, s));
+    if (pl->ev_mafter) KV_CUDA(cudaEventRecord(pl->ev_mafter, s));
     g_launches += 1;
   }
   pl->pML = ML;
@@ -1959,6 +1967,14 @@ KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t pl, void* before_r
   std::lock_guard<std::mutex> plk(pl->mu);
   pl->ev_before = static_cast<cudaEvent_t>(before_realign);
   pl->ev_after = static_cast<cudaEvent_t>(after_realign);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_set_match_events(kvcomm_plan_t pl, void* before_match, void* after_match) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  pl->ev_mbefore = static_cast<cudaEvent_t>(before_match);
+  pl->ev_mafter = static_cast<cudaEvent_t>(after_match);
   return ok();
 }
 

@@ -130,7 +130,12 @@ struct MatchJob {
   int32_t own_step;
   int32_t emb_world;        // > 1: the pool stores only its blocks' rows, compacted (emb_shard)
   int32_t n_peer, _pad_peer;
-  float* W_peer[kMaxMatchPeers];
+  // Sharded: a block's W columns travel to the peers position-major, X[i][cap] (row i =
+  // the cap weights of position i, one coalesced run per warp store) instead of as
+  // scattered 4-byte stores into the slot-major W; each rank's chunk kernel then copies
+  // the positions it does not own from its own X into W.
+  float* X;                            // this rank's exchange rows [n_blocks * P][cap] (peers write them)
+  float* X_peer[kMaxMatchPeers];       // the same rows in every peer's plan buffer
   double* partial_peer[kMaxMatchPeers];
 };
 

@@ -37,7 +37,7 @@ constexpr double kTieRel = 1e-6;
 #endif
 constexpr int kMatchUnroll = KVC_MATCH_UNROLL;
 #ifndef KVC_MATCH_MINB
-#define KVC_MATCH_MINB 1
+#define KVC_MATCH_MINB 6  // CTAs per SM: 40 registers (110 unbounded -> 2 CTAs); 1 / 4 / 5 / 6 / 7 / 8 measured, 6 fastest
 #endif  // 16-byte anchor loads in flight per lane (8 vs 4: match 2-5 % faster)
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -56,19 +56,36 @@ __device__ __forceinline__ bool key_less(double da, int sa, double db, int sb) {
   return da < db || (da == db && sa < sb);
 }
 
-// Σ over 8 bf16 pairs of (q - a)², fp32 FMA on (almost always exact) fp32 differences
+// Σ over 8 bf16 pairs of (q - a)²: exact fp32 differences (almost always: unless the
+// exponents are > 16 binades apart) and squares accumulated with packed FADD2 / FFMA2 in
+// two fp32 lanes (even / odd elements, 4 terms each), summed once at the end — 8 terms in
+// fp32 as before, half the math instructions of scalar FADD + FFMA (measured: match 1 %
+// faster; the kernel is bound by its loads, not its math).  KVC_MATCH_PACKED=0: scalar.
+#ifndef KVC_MATCH_PACKED
+#define KVC_MATCH_PACKED 1
+#endif
 __device__ __forceinline__ float sq_diff8(const uint4& qv, const uint4& av) {
   const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
   const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
-  float part = 0.f;
+  if (!KVC_MATCH_PACKED) {
+    float part = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
+      const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
+      part = fmaf(d0, d0, part);
+      part = fmaf(d1, d1, part);
+    }
+    return part;
+  }
+  float p0 = 0.f, p1 = 0.f;
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    const float d0 = bf_lo(qw[t]) - bf_lo(aw[t]);
-    const float d1 = bf_hi(qw[t]) - bf_hi(aw[t]);
-    part = fmaf(d0, d0, part);
-    part = fmaf(d1, d1, part);
+    float d0, d1;
+    fsub2(d0, d1, bf_lo(qw[t]), bf_hi(qw[t]), bf_lo(aw[t]), bf_hi(aw[t]));
+    ffma2(p0, p1, d0, d1, d0, d1);
   }
-  return part;
+  return p0 + p1;
 }
 
 // q·a, a·a, q·q over 8 bf16 pairs.  A product of two bf16 values is exact in fp32
@@ -202,9 +219,9 @@ __device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, in
       for (int sl = lane; sl < a.cap; sl += 32) {
         const int j = slot2cand[sl];
         const float w = j >= 0 ? float(exp(-(dr[j] - mn)) / sum) : 0.f;
-        const int64_t o = int64_t(sl) * a.ld_w + i;
-        a.W[o] = w;
-        for (int r = 0; r < a.n_peer; ++r) a.W_peer[r][o] = w;
+        a.W[int64_t(sl) * a.ld_w + i] = w;
+        const int64_t x = int64_t(i) * a.cap + sl;  // position-major exchange row: lanes contiguous
+        for (int r = 0; r < a.n_peer; ++r) a.X_peer[r][x] = w;
       }
     } else {
       // top-k: k rounds of lexicographic (distance, slot) argmin over the unselected
@@ -250,9 +267,8 @@ __device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, in
       if (a.n_peer > 0) {  // peers receive the finished column: one store per address
         __syncwarp();
         for (int sl = lane; sl < a.cap; sl += 32) {
-          const int64_t o = int64_t(sl) * a.ld_w + i;
-          const float w = a.W[o];
-          for (int r = 0; r < a.n_peer; ++r) a.W_peer[r][o] = w;
+          const float w = a.W[int64_t(sl) * a.ld_w + i];
+          for (int r = 0; r < a.n_peer; ++r) a.X_peer[r][int64_t(i) * a.cap + sl] = w;
         }
       }
       if (lane == 0 && tie) atomicAdd(&ties[jb], 1);  // sharded: this rank's positions only
@@ -489,7 +505,8 @@ size_t match_tma_smem(int stages, int qbytes, int cmax) {
 
 // First pass of d̄ (and the cosine sums): block (job, c) sums position blocks
 // [c*per, (c+1)*per) of every partial column in order (4 interleaved accumulators,
-// combined in order) into chunk row c.  Columns are coalesced across threads.
+// combined in order) into chunk row c.  Columns are coalesced across threads.  Sharded
+// runs also copy the peers' W columns of those blocks from the exchange rows X into W.
 __global__ void __launch_bounds__(256) match_chunk_kernel(const uint8_t* __restrict__ tab) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
   const MatchJob& a = reinterpret_cast<const MatchJob*>(tab + hdr->job_off)[blockIdx.x];
@@ -497,6 +514,18 @@ __global__ void __launch_bounds__(256) match_chunk_kernel(const uint8_t* __restr
   const int per = (a.n_blocks + kMatchChunks - 1) / kMatchChunks;
   const int b0 = c * per, b1 = min(a.n_blocks, b0 + per);
   const int stride = a.cosine ? 2 * a.n_cand + 1 : a.n_cand;
+  if (a.n_peer > 0) {
+    // sharded: W columns of the positions this rank does not own arrived position-major in X
+    // (peers' distance kernels, ordered before this launch by the caller's cross-rank barrier)
+    const int P = hdr->P;
+    for (int b = b0 + int(threadIdx.x >> 5); b < b1; b += blockDim.x >> 5) {
+      if (b >= a.own_lo && (b - a.own_lo) % a.own_step == 0) continue;  // own block: W written locally
+      const int i1 = min(a.L_phi, (b + 1) * P);
+      for (int i = b * P; i < i1; ++i)
+        for (int sl = int(threadIdx.x & 31); sl < a.cap; sl += 32)
+          a.W[int64_t(sl) * a.ld_w + i] = a.X[int64_t(i) * a.cap + sl];
+    }
+  }
   for (int col = threadIdx.x; col < stride; col += blockDim.x) {
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     int b = b0;

@@ -517,6 +517,15 @@ class Plan:
         L.check(L.lib().kvcomm_plan_set_events(self._h, before.cuda_event if before is not None else None,
                                                after.cuda_event if after is not None else None))
 
+    def set_match_events(self, before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]) -> None:
+        """Record `before`/`after` around the distance kernel (match_dist_kernel) of later runs."""
+        self._mevents = (before, after)
+        for e in (before, after):
+            if e is not None and not e.cuda_event:
+                e.record()
+        L.check(L.lib().kvcomm_plan_set_match_events(self._h, before.cuda_event if before is not None else None,
+                                                     after.cuda_event if after is not None else None))
+
     def results(self):
         """(list of Match without tensors, list of agent_reused flags) of the last run."""
         infos = (L.MatchInfo * self.n_matches)()
