@@ -102,6 +102,8 @@ struct kvcomm_pool_s {
   // emb_rank only, block b stored at b / emb_world; emb_rows = stored rows per slot
   int emb_rank = 0, emb_world = 1;
   int64_t emb_rows = 0;
+  int64_t emb_pad_rows = 0;  // rows of padding between embedding slots (KVCOMM_EMB_SLOT_PAD_ROWS)
+  int64_t emb_slot() const { return (emb_rows + emb_pad_rows) * De; }  // elements between slots
   // device slabs
   bf16* emb = nullptr;                 // [cap][emb_rows][De]
   bool fp8 = false;                    // offset_format == KVCOMM_OFFSET_FP8_E4M3
@@ -297,8 +299,10 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_create(const kvcomm_pool_config* c, 
   {
     const int64_t cyc = int64_t(kMatchP) * p->emb_world;
     p->emb_rows = p->emb_world > 1 ? (p->maxlen + cyc - 1) / cyc * kMatchP : p->maxlen;
+    const char* e = getenv("KVCOMM_EMB_SLOT_PAD_ROWS");
+    p->emb_pad_rows = e ? atoi(e) : 0;
   }
-  ALLOC(p->emb, int64_t(p->cap) * p->emb_rows * p->De, "embedding slab");
+  ALLOC(p->emb, int64_t(p->cap) * p->emb_slot(), "embedding slab");
   if (!p->fp8) {
     ALLOC_OFF(p->ph, int64_t(p->C) * p->cap * p->ph_slot_stride(), "placeholder offset slab");
     p->pf.assign(p->C, nullptr);
@@ -518,7 +522,7 @@ KVCOMM_API kvcomm_status kvcomm_anchor_pool_insert(kvcomm_pool_t p, int32_t L_ps
     p->slots[evicted] = SlotMeta();
     slot = evicted;
   }
-  bf16* edst = p->emb + int64_t(slot) * p->emb_rows * p->De;
+  bf16* edst = p->emb + int64_t(slot) * p->emb_slot();
   if (p->emb_world <= 1) {
     KV_CUDA(launch_copy_flat(static_cast<const bf16*>(emb), edst, int64_t(L_psi) * p->De, s));
     g_launches += 1;
@@ -680,7 +684,7 @@ kvcomm_status slots_io(kvcomm_pool_s* p, bool save, FILE* f) {
     const SlotMeta& m = p->slots[s];
     if (!m.occupied) continue;
     const size_t ew = size_t(p->emb_row_count(m.length)) * p->De * sizeof(bf16);  // rows as stored
-    const Region er{p->emb + int64_t(s) * p->emb_rows * p->De, ew, ew, 1};
+    const Region er{p->emb + int64_t(s) * p->emb_slot(), ew, ew, 1};
     KV_TRY(region_io(er, buf, save, f));
     for (int c = 0; c < p->C; ++c) {
       if (m.ph_mask >> c & 1) KV_TRY(region_io(offset_region(p, c, s, false, m.length), buf, save, f));
@@ -992,6 +996,7 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
     n_ints += it.info->n_candidates + it.p->cap;
     blocks += it.n_own >= 0 ? it.n_own : match_blocks(it.L_phi);
     if (it.n_peer > 0) L.hdr.any_peer = 1;
+    L.hdr.max_de = std::max(L.hdr.max_de, int32_t(it.p->De));
     L.smem = std::max(L.smem, align_up(size_t(kMatchP) * it.p->De * 2, 16) +
                                   size_t(kMatchP) * (3 * it.info->n_candidates + 1) * sizeof(double));
   }
@@ -1049,7 +1054,7 @@ void write_match(uint8_t* h, const MatchLayout& L, const std::vector<MatchItem>&
     MatchJob& a = jobs[t];
     a.query = static_cast<const bf16*>(it.query);
     a.emb = p->emb;
-    a.slot_stride = p->emb_rows * p->De;
+    a.slot_stride = p->emb_slot();
     a.emb_world = p->emb_world;
     a.W = it.W;
     a.ld_w = it.ld_w;

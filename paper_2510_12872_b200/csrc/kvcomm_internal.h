@@ -153,6 +153,7 @@ struct MatchHdr {
   // stages of kMatchStageBytes, query double buffer of tma_qbytes each, partial table for
   // tma_cmax candidates; tma = 0 selects the register-streaming kernel
   int32_t tma, tma_stages, tma_qbytes, tma_cmax;
+  int32_t max_de, _pad_de;                // largest D_e of the launch's jobs (selects the kernel)
   uint64_t* fp_dst[kMaxMatchPeers + 1];   // [r]: this rank's slot in rank r's array
   const uint64_t* fp_mine;                // this rank's array [shard_world]
 };

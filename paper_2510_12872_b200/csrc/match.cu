@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 #include <cfloat>
 #include <algorithm>
 #include "kvcomm_internal.h"
@@ -36,8 +37,14 @@ constexpr double kTieRel = 1e-6;
 #define KVC_MATCH_UNROLL 8
 #endif
 constexpr int kMatchUnroll = KVC_MATCH_UNROLL;
+// Two instantiations of the distance kernel by D_e (measured, profiles/r02g_match_ctas.txt):
+// rows of D_e <= kMatchWideDe (8 KiB at 4096) run 6 CTAs per SM at 40 registers (config 2:
+// 120 -> 104 us); longer rows keep the unbounded 110-register build at 2 CTAs per SM,
+// whose warps hold more loads in flight (config 4: 2.02 ms vs 2.23-3.45 ms at 2-6 CTAs of
+// the 40-register build).
+constexpr int kMatchWideDe = 4096;
 #ifndef KVC_MATCH_MINB
-#define KVC_MATCH_MINB 6  // CTAs per SM: 40 registers (110 unbounded -> 2 CTAs); 1 / 4 / 5 / 6 / 7 / 8 measured, 6 fastest
+#define KVC_MATCH_MINB 6
 #endif  // 16-byte anchor loads in flight per lane (8 vs 4: match 2-5 % faster)
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -315,7 +322,8 @@ __device__ __forceinline__ void match_tail(const MatchJob& a, int jb, int lb, in
 // per-job tie counters, zeroed by the host upload), so the last wave has no tail of
 // idle SMs.  Sharded matching: the items are this rank's position blocks only.  The processing order does not affect any result: every item writes its
 // own W columns and partial sums.
-__global__ void __launch_bounds__(kMatchThreads, KVC_MATCH_MINB) match_dist_kernel(const uint8_t* __restrict__ tab) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kMatchThreads, kMinBlocks) match_dist_kernel(const uint8_t* __restrict__ tab) {
   const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
   int32_t* counter = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off) + hdr->n_jobs;
   __shared__ int s_item;
@@ -637,18 +645,23 @@ cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t
     match_dist_tma_kernel<<<grid, kMatchThreads + 32, sm, s>>>(reinterpret_cast<const uint8_t*>(table_dev));
     return cudaGetLastError();
   }
+  const auto kern = hdr.max_de <= kMatchWideDe ? match_dist_kernel<KVC_MATCH_MINB> : match_dist_kernel<1>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(match_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
   }
   uint8_t* t = reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev));
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_dist_kernel, kMatchThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMatchThreads, smem);
+  static const int ctas_env = [] {  // measurement knob: CTAs per SM (<= occupancy)
+    const char* e = getenv("KVCOMM_MATCH_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (ctas_env > 0) per_sm = std::min(per_sm, ctas_env);
   const int grid = std::max(1, std::min(hdr.total_blocks, sms * std::max(per_sm, 1)));  // >= 1
-  match_dist_kernel<<<grid, kMatchThreads, smem, s>>>(t);
+  kern<<<grid, kMatchThreads, smem, s>>>(t);
   return cudaGetLastError();
 }
 
