@@ -42,17 +42,26 @@
 
 namespace kvc {
 
-#ifndef KVC_NSTAGE
-#define KVC_NSTAGE 9
+// Ring depth per instantiation (stages of kStageStride): fewer bytes in flight means less
+// DRAM contention, as long as the ring still covers the latency.  Measured at config 2
+// (profiles/r02g_ring_depth.jsonl): the bf16 stream (8 consumer warps) is fastest with 7
+// stages (9: 2 % slower, 11: 5 %), the fp8 decode (16 warps, slower consumers) with 9-10.
+#ifndef KVC_NSTAGE_BF16
+#define KVC_NSTAGE_BF16 7
 #endif
-constexpr int kNStage = KVC_NSTAGE;
+#ifndef KVC_NSTAGE_FP8
+#define KVC_NSTAGE_FP8 9
+#endif
+template <int kConsumerWarps>
+constexpr int ring_stages() { return kConsumerWarps == 16 ? KVC_NSTAGE_FP8 : KVC_NSTAGE_BF16; }
 constexpr int kItems = kStageBytes / 32;  // 512 items of 32 B per 16 KiB bf16 tile
 constexpr int kConsumerBar = 1;           // named barrier id (consumers only)
 
-constexpr size_t realign_smem_bytes() {
-  return size_t(kNStage) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * kNStage + 4) * sizeof(uint64_t);
+constexpr size_t realign_smem_bytes(int stages) {
+  return size_t(stages) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * size_t(stages) + 4) * sizeof(uint64_t);
 }
-static_assert(realign_smem_bytes() <= 227 * 1024, "realign shared memory");
+static_assert(realign_smem_bytes(ring_stages<8>()) <= 227 * 1024, "realign shared memory");
+static_assert(realign_smem_bytes(ring_stages<16>()) <= 227 * 1024, "realign shared memory");
 
 struct Unit {
   int s, l, h, p, t;
@@ -236,6 +245,7 @@ __device__ __forceinline__ void realign_body(const uint8_t* __restrict__ tab, in
   // tables that read an fp8 pool always launch the 16-warp instantiation (launch_realign), so
   // the 8-warp one carries no e4m3 decode (keeps its registers for the bf16 stream)
   constexpr bool kFp8Path = kConsumerWarps == 16;
+  constexpr int kNStage = ring_stages<kConsumerWarps>();
   static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
   const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
@@ -590,14 +600,14 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    const int smem = int(realign_smem_bytes());
-    cudaError_t e = cudaFuncSetAttribute(realign_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem8 = int(realign_smem_bytes(ring_stages<8>())), smem16 = int(realign_smem_bytes(ring_stages<16>()));
+    cudaError_t e = cudaFuncSetAttribute(realign_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(realign_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(realign_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(realign_kernel<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(realign_kernel<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(realign_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      e = cudaFuncSetAttribute(realign_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
@@ -618,7 +628,7 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   if (hdr.total_units <= 0) return cudaGetLastError();
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
   const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);
-  const size_t smem = realign_smem_bytes();
+  const size_t smem = realign_smem_bytes(cw == 8 ? ring_stages<8>() : ring_stages<16>());
   const bool d128 = hdr.d == 128 && !(variant & 256);  // bit8: generic-d kernel (probe)
   if (cw == 8 && d128)
     realign_kernel<8, 128><<<int(g), 9 * 32, smem, s>>>(t, variant);
