@@ -13,7 +13,7 @@
 //     weights [n_cand][rows] in chunks of up to 16 KiB (one copy each, double
 //     buffered), then the anchor tiles (one contiguous copy per anchor: bf16 rows, or
 //     an fp8 block of e4m3 codes followed by their row scales) and finally the base
-//     tile(s) into a 9-deep shared-memory ring (9 measured 3 % faster than 11: fewer
+//     tile(s) into a shared-memory ring of 7 (bf16) / 9 (fp8) stages (ring_stages: fewer
 //     bytes in flight, less DRAM contention) with cp.async.bulk (UBLKCP) + mbarrier
 //     complete_tx, L2 evict-first for anchor tiles, evict-last for the weight blocks
 //     (re-read by every (layer, head, plane) unit of a tile) and for shared bases; the
