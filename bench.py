@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--gamma", type=float, default=0.3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="N = 1: run each request's realign on the run stream (no overlap with the next match)")
     ap.add_argument("--offsets", default="bf16", choices=["bf16", "fp8"],
                     help="anchor offset storage; the headline line is bf16 (fp8 = SURVEY f3, lossy)")
     ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
@@ -549,6 +551,13 @@ def main():
             args.match = "replicated (ipc unavailable)"
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
+    # Request pipelining (N = 1): each run's realign kernel goes to its own stream, so the
+    # next request's table upload, matching, reduction and prep (on `stream`) overlap this
+    # request's realign (kvcomm_plan_set_realign_stream).  At N > 1 the
+    # sharded-matching barrier and the fused gather's ordering assume one stream per run.
+    rstream = torch.cuda.Stream() if world == 1 and not args.no_pipeline else None
+    if rstream is not None:
+        plan.set_realign_stream(rstream)
 
     def deliver_for(peer_b, agents_b, full_b):
         def deliver():
@@ -624,14 +633,20 @@ def main():
         if last or not merged_barrier:
             deliver()
 
+    def join():  # the last realign (on its own stream) is part of the timed work
+        if rstream is not None:
+            stream.wait_stream(rstream)
+
     for _ in range(args.warmup):
         step()
+    join()
     torch.cuda.synchronize()
     res = req.results()
     if args.profile:
         torch.cuda.profiler.start()
         for _ in range(args.steps):
             step()
+        join()
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         print(json.dumps({"profile_steps": args.steps, "rows": res.blended_rows}))
@@ -662,12 +677,23 @@ def main():
     with ClockSampler(local) as clk:
         e0.record(stream)
         for i in range(args.steps):
-            step(evs[i], last=(i == args.steps - 1), mevents=mevs[i])
+            # pipelined: the match kernel of request t+1 shares the SMs with request t's
+            # realign, so its events would time the overlap, not the kernel (timed below)
+            step(evs[i], last=(i == args.steps - 1), mevents=None if rstream is not None else mevs[i])
+        join()
         e1.record(stream)
         torch.cuda.synchronize()
     plan.set_events(None, None)
     plan.set_match_events(None, None)
     n_launch = kv.kernel_launch_count() - n_launch0
+    if rstream is not None:
+        plan.set_realign_stream(None)   # the e2e loop below orders its copies on one compute stream
+        # the match kernel's own time: a few unpipelined steps after the timed region
+        for i in range(min(args.steps, max(3, args.warmup))):
+            step(mevents=mevs[i])
+        torch.cuda.synchronize()
+        plan.set_match_events(None, None)
+        mevs = mevs[:min(args.steps, max(3, args.warmup))]
     res = req.results()
     if res.fallback_agents:
         raise SystemExit(f"agents {res.fallback_agents} took the fallback branch during the timed steps")
@@ -738,7 +764,10 @@ def main():
                                    "frac": (match_bytes / (match_ms / 1e3) / 1e9 / peak) if peak else None,
                                    "share_of_step": match_ms / ms_per_step,
                                    "bytes_model": "per query position: its row + the same row of each candidate "
-                                                  "anchor, D_e x 2 B each"},
+                                                  "anchor, D_e x 2 B each",
+                                   "timed": (f"{len(mevs)} unpipelined steps after the timed region (pipelined, "
+                                             "it runs beside the previous request's realign)"
+                                             if rstream is not None else "every timed step")},
                          "bytes_model": "(k offset rows + 1 output row) per realigned token + each distinct "
                                         f"base once + 2 per copied p0 token, x {row_bytes * Ls * 2 // 1024} KiB "
                                         "(K+V of this rank's layers and heads)",
@@ -749,6 +778,9 @@ def main():
                              "peer_note": "fused gather: rows this rank stores into consumer GPUs over NVLink; "
                                           "ref = measured peer copy per direction (B200_PROFILING.md)"}
                             if peer is not None else {})},
+            "schedule": ("requests pipelined: request t+1's table upload, matching and prep (run stream) overlap "
+                         "request t's realign (realign stream); every step still runs the whole hot path"
+                         if rstream is not None else "one stream per request"),
             "verdicts": verdict_summary(res, args),
             "clocks": clk.summary(),
             "e2e": e2e,

@@ -452,6 +452,17 @@ KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before
  * before and after it in every later run (NULL disables), so a caller can time the
  * matching kernel alone (bench.py's roofline.match). */
 KVCOMM_API kvcomm_status kvcomm_plan_set_match_events(kvcomm_plan_t plan, void* before_match, void* after_match);
+/* Request pipelining: with enable != 0, every later run launches its realign kernel on
+ * `stream` (a cudaStream_t; NULL = the legacy default stream) instead of the run's own
+ * stream.  The run's own stream keeps the table upload, matching, reduction, results copy
+ * and the prep kernel, then records an event the realign stream waits on; the run's
+ * completion (kvcomm_plan_results, the next-but-one run's buffer reuse) is ordered after
+ * the realign.  A caller that issues run t+1 on the run stream while run t's realign
+ * occupies the realign stream overlaps t+1's matching with t's realign — every kernel of
+ * a run still sees exactly the same inputs (runs alternate between two table and weight
+ * buffer sets; the run after next waits on the host for this run's completion).  enable = 0
+ * restores single-stream runs.  INVALID_ARGUMENT between run_begin and run_end. */
+KVCOMM_API kvcomm_status kvcomm_plan_set_realign_stream(kvcomm_plan_t plan, void* stream, int32_t enable);
 /* Device pointers of the LAST run's weights for match `match` (W [capacity][ld_w], w̄;
  * runs alternate between two buffer sets). */
 KVCOMM_API kvcomm_status kvcomm_plan_weights(kvcomm_plan_t plan, int32_t match, const float** W,

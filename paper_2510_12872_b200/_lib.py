@@ -139,6 +139,7 @@ _SIGS = {
     "kvcomm_plan_results": (C.c_int, [C.c_void_p, C.POINTER(MatchInfo), C.POINTER(C.c_int32)]),
     "kvcomm_plan_set_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvcomm_plan_set_match_events": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvcomm_plan_set_realign_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "kvcomm_plan_weights": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
                                       C.POINTER(C.c_void_p)]),
     "kvcomm_plan_match_handle": (C.c_int, [C.c_void_p, C.POINTER(IpcHandle), C.POINTER(C.c_int64)]),

@@ -1584,6 +1584,11 @@ struct kvcomm_plan_s {
   int64_t res_off = 0;
   cudaEvent_t ev_before = nullptr, ev_after = nullptr;
   cudaEvent_t ev_mbefore = nullptr, ev_mafter = nullptr;  // around the distance kernel
+  // kvcomm_plan_set_realign_stream: the realign kernel of every run goes to rstream (after
+  // the run's prep, by ev_prep[parity]) so that the next run's matching can overlap it
+  cudaStream_t rstream = nullptr;
+  bool rstream_set = false;
+  cudaEvent_t ev_prep[2] = {nullptr, nullptr};
   std::mutex mu;
 
   char* xb() const { return static_cast<char*>(xbuf); }
@@ -1603,6 +1608,8 @@ static void plan_free(kvcomm_plan_s* pl) {
   if (!pl) return;
   DeviceGuard g(pl->dev);
   for (auto& e : pl->tab) entry_free(e);
+  for (cudaEvent_t& e : pl->ev_prep)
+    if (e) cudaEventDestroy(e);
   plan_close_peers(pl);
   cudaFree(pl->xbuf);
   delete pl;
@@ -1888,20 +1895,35 @@ static kvcomm_status plan_end(kvcomm_plan_s* pl, int32_t sync, cudaStream_t s) {
   const MatchLayout& ML = pl->pML;
   const RealignLayout& RL = pl->pRL;
   const size_t roff = pl->proff;
+  // the realign kernel's stream: the run's own, or the plan's realign stream (pipelined
+  // runs: this run's matching, reduction and prep on s overlap the previous run's realign
+  // on rs; the realign waits for this run's prep through ev_prep)
+  const bool split = pl->rstream_set;
+  cudaStream_t rs = split ? pl->rstream : s;
+  const int par = pl->next;
   if (pl->n_items) {
     KV_CUDA(launch_match_reduce(dv, ML.hdr, s));
     g_launches += 2;
-  }
-  if (pl->ev_before) KV_CUDA(cudaEventRecord(pl->ev_before, s));
-  if (pl->n_hs) {
-    KV_CUDA(launch_realign(dv + roff, RL.hdr, grid_for_device(pl->dev), s));
-    g_launches += RL.hdr.total_units > 0 ? 2 : 1;
-  }
-  if (pl->ev_after) KV_CUDA(cudaEventRecord(pl->ev_after, s));
-  if (pl->n_items)
     KV_CUDA(cudaMemcpyAsync(h + ML.hdr.res_off, dv + ML.hdr.res_off, ML.bytes - size_t(ML.hdr.res_off),
                             cudaMemcpyDeviceToHost, s));
-  KV_CUDA(cudaEventRecord(E.done, s));
+  }
+  const bool realign = pl->n_hs && RL.hdr.n_seg > 0;
+  if (realign) {
+    KV_CUDA(launch_realign_prep(dv + roff, RL.hdr, s));
+    g_launches += 1;
+  }
+  if (split) {
+    if (!pl->ev_prep[par]) KV_CUDA(cudaEventCreateWithFlags(&pl->ev_prep[par], cudaEventDisableTiming));
+    KV_CUDA(cudaEventRecord(pl->ev_prep[par], s));
+    KV_CUDA(cudaStreamWaitEvent(rs, pl->ev_prep[par], 0));
+  }
+  if (pl->ev_before) KV_CUDA(cudaEventRecord(pl->ev_before, rs));  // brackets the realign kernel alone
+  if (realign && RL.hdr.total_units > 0) {
+    KV_CUDA(launch_realign_main(dv + roff, RL.hdr, grid_for_device(pl->dev), rs));
+    g_launches += 1;
+  }
+  if (pl->ev_after) KV_CUDA(cudaEventRecord(pl->ev_after, rs));
+  KV_CUDA(cudaEventRecord(E.done, rs));
   E.used = true;
   pl->res_off = pl->n_items ? ML.hdr.res_off : -1;
   pl->last = pl->next;
@@ -1972,6 +1994,15 @@ KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t pl, void* before_r
   std::lock_guard<std::mutex> plk(pl->mu);
   pl->ev_before = static_cast<cudaEvent_t>(before_realign);
   pl->ev_after = static_cast<cudaEvent_t>(after_realign);
+  return ok();
+}
+
+KVCOMM_API kvcomm_status kvcomm_plan_set_realign_stream(kvcomm_plan_t pl, void* stream, int32_t enable) {
+  if (!pl) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "null plan");
+  std::lock_guard<std::mutex> plk(pl->mu);
+  if (pl->pending) return fail(KVCOMM_ERR_INVALID_ARGUMENT, "a run is in progress (between run_begin and run_end)");
+  pl->rstream = static_cast<cudaStream_t>(stream);
+  pl->rstream_set = enable != 0;
   return ok();
 }
 

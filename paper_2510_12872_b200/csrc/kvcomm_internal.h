@@ -97,6 +97,10 @@ struct TableHdr {
 
 // Launchers (stream-ordered).  Return cudaGetLastError().
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s);
+// the two halves of launch_realign: the prep kernel (unit list, cos/sin, weight blocks), then
+// the persistent realign kernel (callers may put them on different streams, ordered by an event)
+cudaError_t launch_realign_prep(const void* table_dev, const TableHdr& hdr, cudaStream_t s);
+cudaError_t launch_realign_main(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s);
 int realign_grid_size(int device);
 
 constexpr int kMaxMatchPeers = 7;   // one box: 8 GPUs

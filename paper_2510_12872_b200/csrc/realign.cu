@@ -97,7 +97,10 @@ __device__ __forceinline__ Unit load_unit(const UnitDev* units, int64_t u) {
 // cos/sin of δ·inv_freq (fp64 angle, reading A13) and the weight blocks wt[tile][j][row] = weight of candidate j at the
 // tile's token row (0 past L_seg), from W[slot] (PLACEHOLDER) or w̄[slot] (PREFIX),
 // so the main kernel fetches a unit's weights as contiguous chunks.
-constexpr int kPrepY = 8;
+#ifndef KVC_PREP_Y
+#define KVC_PREP_Y 8
+#endif
+constexpr int kPrepY = KVC_PREP_Y;  // block rows per segment
 __global__ void realign_prep_kernel(uint8_t* tab) {
   const TableHdr* hdr = reinterpret_cast<const TableHdr*>(tab);
   SegDev* segs = reinterpret_cast<SegDev*>(tab + hdr->seg_off);
@@ -595,6 +598,17 @@ int realign_grid_size(int device) {
 }
 
 cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
+  cudaError_t e = launch_realign_prep(table_dev, hdr, s);
+  return e != cudaSuccess ? e : launch_realign_main(table_dev, hdr, grid, s);
+}
+
+cudaError_t launch_realign_prep(const void* table_dev, const TableHdr& hdr, cudaStream_t s) {
+  if (hdr.n_seg <= 0) return cudaSuccess;
+  realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_realign_main(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
   static int variant = -1, cw_env = 0;
   int dev = 0;
@@ -608,6 +622,13 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
       e = cudaFuncSetAttribute(realign_kernel<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(realign_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
+    // all of the SM's 228 KiB as shared memory: the realign CTA takes ~153 KiB (bf16 ring), and
+    // the rest must stay free for the CTAs of the next request's match / prep kernels that run
+    // beside it when requests are pipelined (kvcomm_plan_set_realign_stream); at the default
+    // carveout the SM is configured just large enough for the realign CTA alone
+    for (const void* k : {(const void*)realign_kernel<8, 0>, (const void*)realign_kernel<16, 0>,
+                          (const void*)realign_kernel<8, 128>, (const void*)realign_kernel<16, 128>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
@@ -623,9 +644,7 @@ cudaError_t launch_realign(const void* table_dev, const TableHdr& hdr, int grid,
   // 8 consumer warps stream bf16 pools at the HBM roofline; the e4m3 decode of fp8
   // pools issues ~2x the instructions per byte and runs ~4 % faster with 16 (profiles/)
   const int cw = hdr.any_fp8 ? 16 : (cw_env == 16 ? 16 : 8);  // fp8 decode: 16-warp instantiation only
-  if (hdr.n_seg <= 0) return cudaSuccess;
-  realign_prep_kernel<<<dim3(hdr.n_seg, kPrepY), 256, 0, s>>>(reinterpret_cast<uint8_t*>(const_cast<void*>(table_dev)));
-  if (hdr.total_units <= 0) return cudaGetLastError();
+  if (hdr.n_seg <= 0 || hdr.total_units <= 0) return cudaSuccess;
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
   const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);
   const size_t smem = realign_smem_bytes(cw == 8 ? ring_stages<8>() : ring_stages<16>());

@@ -517,6 +517,14 @@ class Plan:
         L.check(L.lib().kvcomm_plan_set_events(self._h, before.cuda_event if before is not None else None,
                                                after.cuda_event if after is not None else None))
 
+    def set_realign_stream(self, stream) -> None:
+        """Pipelined runs: later runs put their realign kernel on `stream` (a
+        torch.cuda.Stream; None restores single-stream runs), so the next run's matching,
+        issued on the run stream, overlaps this run's realign (kvcomm_plan_set_realign_stream)."""
+        self._rstream = stream
+        L.check(L.lib().kvcomm_plan_set_realign_stream(self._h, _stream_handle(stream) if stream is not None else None,
+                                                       1 if stream is not None else 0))
+
     def set_match_events(self, before: Optional[torch.cuda.Event], after: Optional[torch.cuda.Event]) -> None:
         """Record `before`/`after` around the distance kernel (match_dist_kernel) of later runs."""
         self._mevents = (before, after)

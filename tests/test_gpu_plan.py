@@ -53,6 +53,48 @@ def test_plan_pipelined_runs_match_single_run():
         assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
 
 
+def test_realign_stream_pipelining_matches_sequential_runs():
+    """kvcomm_plan_set_realign_stream (the bench's N = 1 schedule): runs alternate between
+    two query sets — B sends agent_2_current's pool NewAnchor, so its agents keep A's rows —
+    with every realign on a second stream and no host sync; the caches and verdicts must be
+    those of the same runs issued one at a time."""
+    st = _small_state(seed=7)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    qa = dict(st.queries)
+    qb = dict(st.queries)
+    qb["agent_2_current"] = (torch.randn(qb["agent_2_current"].shape, generator=g, device="cuda") * 0.125
+                             ).to(torch.bfloat16)
+    for a in st.agents:
+        a.dst_k.fill_(1.0)
+        a.dst_v.fill_(1.0)
+    st.request.run(qa)
+    st.request.run(qb)
+    ref = _snap(st)
+    res_ref = st.request.results()
+    for a in st.agents:
+        a.dst_k.fill_(1.0)
+        a.dst_v.fill_(1.0)
+    torch.cuda.synchronize()
+    plan = st.request.plan
+    rs = torch.cuda.Stream()
+    plan.set_realign_stream(rs)
+    try:
+        for _ in range(3):
+            st.request.launch([qa[n] for n in st.request.names])
+            st.request.launch([qb[n] for n in st.request.names])
+        torch.cuda.current_stream().wait_stream(rs)
+        res = st.request.results()
+    finally:
+        plan.set_realign_stream(None)
+    torch.cuda.synchronize()
+    assert res.fallback_agents == res_ref.fallback_agents == [3, 4, 5]
+    for n in st.request.names:
+        assert res.matches[n].verdict == res_ref.matches[n].verdict
+        assert res.matches[n].entropy == res_ref.matches[n].entropy
+    for (k, v), a in zip(ref, st.agents):
+        assert torch.equal(k, a.dst_k) and torch.equal(v, a.dst_v)
+
+
 def test_device_side_branch_skips_agents_of_a_new_anchor_pool():
     st = _small_state(seed=5)
     g = torch.Generator(device="cuda").manual_seed(1)
