@@ -1003,9 +1003,10 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
   L.hdr.total_blocks = blocks;
   {  // the TMA-streamed distance kernel takes l2 jobs up to 256 candidates and D_e 8192
     static const int tma_env = [] {
-      // measurement knob, off by default: 1 = the TMA-ring distance kernel, measured SLOWER than the
-      // register-streaming kernel (config 4: 3.13 vs 1.99 ms; one config-2 pool: 86 vs 60 us;
-      // profiles/r02_match_tma.json) — DESIGN §7
+      // measurement knob, off by default: 1 = the TMA tile-ring distance kernel, 2 = the TMA
+      // row-ring kernel; both measured SLOWER than the register-streaming kernel (1: config 4
+      // 3.13 vs 1.99 ms, one config-2 pool 86 vs 60 us, profiles/r02_match_tma.json; 2: config 2
+      // 121 vs 103 us, config 4 2.30 vs 2.00 ms, profiles/r02h_match_ring.txt) — DESIGN §7
       const char* e = getenv("KVCOMM_MATCH_TMA");
       return e ? atoi(e) : 0;
     }();
@@ -1017,7 +1018,20 @@ MatchLayout layout_match(const std::vector<MatchItem>& items) {
       de = std::max(de, it.p->De);
       cm = std::max(cm, it.info->n_candidates);
     }
-    if (ok) {
+    if (ok && tma_env == 2) {  // row-ring kernel: one ring stage per anchor row
+      const int rb = int(align_up(size_t(de) * 2, 128));
+      const int qb = int(align_up(size_t(kMatchP) * de * 2, 128));
+      const size_t fixed = match_ring_smem(0, rb, qb, cm, kMatchP);
+      int stages = fixed < 227 * 1024 ? int(std::min<size_t>(16, (227 * 1024 - fixed) / (size_t(rb) + 16))) : 0;
+      stages -= stages % kMatchRingWarps;  // parity safety: a stage's consecutive uses belong to one warp
+      if (stages >= kMatchRingWarps) {
+        L.hdr.tma = 2;
+        L.hdr.tma_stages = stages;
+        L.hdr.tma_qbytes = qb;
+        L.hdr.tma_cmax = cm;
+        L.hdr.ring_row_bytes = rb;
+      }
+    } else if (ok) {
       const int qb = int(align_up(size_t(kMatchP) * de * 2, 16));
       const size_t fixed = match_tma_smem(0, qb, cm);
       const int stages = int(std::min<size_t>(8, (227 * 1024 - fixed) / (kMatchStageBytes + 16)));

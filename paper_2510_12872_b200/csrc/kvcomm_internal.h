@@ -22,6 +22,7 @@ constexpr int kMatchChunks = 32;    // position-block chunks of the two-pass d̄
 constexpr int kMatchStageBytes = 16384;  // TMA distance kernel: bytes per ring stage
 constexpr int kMatchTmaMaxCand = 256;    // TMA distance kernel: candidates per job
 constexpr int kMatchTmaMaxDe = 8192;     // TMA distance kernel: embedding width
+constexpr int kMatchRingWarps = 8;       // row-ring distance kernel: consumer warps (ring depth: a multiple)
 
 // rows per realign tile (16 KiB of bf16 rows) for head_dim d
 __host__ __device__ constexpr int rows_per_tile(int d) { return kStageBytes / (2 * d); }
@@ -157,7 +158,8 @@ struct MatchHdr {
   // stages of kMatchStageBytes, query double buffer of tma_qbytes each, partial table for
   // tma_cmax candidates; tma = 0 selects the register-streaming kernel
   int32_t tma, tma_stages, tma_qbytes, tma_cmax;
-  int32_t max_de, _pad_de;                // largest D_e of the launch's jobs (selects the kernel)
+  int32_t max_de;                         // largest D_e of the launch's jobs (selects the kernel)
+  int32_t ring_row_bytes;                 // tma = 2 (row-ring kernel): bytes per ring stage (max D_e x 2)
   uint64_t* fp_dst[kMaxMatchPeers + 1];   // [r]: this rank's slot in rank r's array
   const uint64_t* fp_mine;                // this rank's array [shard_world]
 };
@@ -169,6 +171,8 @@ cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t
 cudaError_t launch_match_reduce(const void* table_dev, const MatchHdr& hdr, cudaStream_t s);
 // dynamic shared memory of the TMA distance kernel (ring stages, query buffers, partials)
 size_t match_tma_smem(int stages, int qbytes, int cmax);
+// dynamic shared memory of the row-ring distance kernel (stages of one anchor row each)
+size_t match_ring_smem(int stages, int row_bytes, int qbytes, int cmax, int P);
 
 // Strided row-block copy: for l<Ls, h<Hs, i<rows: dst[(l*Hs+h)*dst_ld + i] = src[(l*Hs+h)*src_ld + i]
 cudaError_t launch_copy_rows(const bf16* src, int64_t src_ld, bf16* dst, int64_t dst_ld, int Ls, int Hs,

@@ -506,6 +506,143 @@ __global__ void __launch_bounds__(kMatchThreads + 32, 1) match_dist_tma_kernel(c
   if (hdr->any_peer) __threadfence_system();
 }
 
+// ---- row-ring distance kernel (l2 jobs; round 2) ----------------------------------
+// The register kernel's task model (one warp reduces one whole anchor row of one position)
+// fed by TMA instead of per-lane loads, so the bytes in flight are bounded by a shared-memory
+// ring, not by registers or the LSU's outstanding misses.  One persistent CTA per SM of 8
+// consumer warps + 1 producer warp walks the work items (P positions of one job)
+// round-robin.  The producer's elected lane copies the item's query rows into a double
+// buffer and then, for every task (candidate j, position p) of the item in order, the
+// anchor's row into the next ring stage (one cp.async.bulk of D_e x 2 bytes, L2
+// evict-first).  Tasks are numbered across items; consumer warp w takes the tasks
+// g = w (mod 8), so its ring stage advances by 8 per task.  Per task the warp computes the
+// distance exactly as the register kernel does (lane-strided 16-byte vectors, groups of 8
+// in fp32 with packed FADD2 / FFMA2, fp64 accumulation in the same order, the same
+// butterfly), so both kernels give bit-identical distances; lane 0 releases the stage.
+// The item's distances go to one of two sd buffers; after a consumer-only barrier the 8
+// warps run the same tail (per-position weights, partial sums) as the register kernel
+// while the producer streams the next item.
+// Consumer warps of the row-ring kernel.  The ring depth must be a multiple of it (host,
+// layout_match): task g + NS reuses task g's stage, and the parity wait is only safe if the
+// same warp, in order, consumes both (another warp could otherwise see task g's completed
+// phase as its own).  16 warps measured 117 us at config 2 (8: 121 us; register kernel 103).
+constexpr int kRingWarps = kMatchRingWarps;
+__global__ void __launch_bounds__(kRingWarps * 32 + 32, 1) match_dist_ring_kernel(const uint8_t* __restrict__ tab) {
+  const MatchHdr* hdr = reinterpret_cast<const MatchHdr*>(tab);
+  const MatchJob* jobs = reinterpret_cast<const MatchJob*>(tab + hdr->job_off);
+  const int32_t* ints = reinterpret_cast<const int32_t*>(tab + hdr->int_off);
+  int32_t* ties = reinterpret_cast<int32_t*>(const_cast<uint8_t*>(tab) + hdr->tie_off);
+  const int NS = hdr->tma_stages, QB = hdr->tma_qbytes, CM = hdr->tma_cmax, RB = hdr->ring_row_bytes;
+  const int P = hdr->P;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;                                                  // [NS][RB]
+  uint8_t* qbuf = ring + size_t(NS) * RB;                                // [2][QB]
+  double* sdb = reinterpret_cast<double*>(qbuf + 2 * size_t(QB));        // [2][P * CM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sdb + 2 * size_t(P) * CM);
+  uint64_t* empty = full + NS;
+  uint64_t* qfull = empty + NS;
+  uint64_t* qempty = qfull + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);           // lane 0 of the consuming warp, after __syncwarp
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (hdr->shard_world > 1 && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int r = 0; r < hdr->shard_world; ++r) *hdr->fp_dst[r] = hdr->fingerprint;
+  __syncthreads();
+  const int total = hdr->total_blocks;
+
+  if (warp == kRingWarps) {
+    // ---------------- TMA producer (one lane) ----------------
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      int stage = 0, qb = 0;
+      uint32_t phase = 0, qphase = 0;
+      for (int item = blockIdx.x; item < total; item += gridDim.x) {
+        int jb, lb, i0, np;
+        match_tma_geom(hdr, jobs, item, jb, lb, i0, np);
+        const MatchJob& a = jobs[jb];
+        const uint32_t row = uint32_t(a.De) * 2u;
+        mbar_wait(&qempty[qb], qphase ^ 1u);
+        mbar_arrive_expect_tx(&qfull[qb], uint32_t(np) * row);
+        bulk_g2s(qbuf + size_t(qb) * QB, a.query + int64_t(i0) * a.De, uint32_t(np) * row, &qfull[qb], pol_stream);
+        if (++qb == 2) { qb = 0; qphase ^= 1u; }
+        const int32_t* cand = ints + a.cand_off;
+        const int64_t erow = a.emb_world > 1 ? int64_t(lb / a.emb_world) * P : int64_t(i0);
+        for (int j = 0; j < a.n_cand; ++j) {
+          const bf16* src = a.emb + int64_t(cand[j]) * a.slot_stride + erow * a.De;
+          for (int p = 0; p < np; ++p) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx(&full[stage], row);
+            bulk_g2s(ring + size_t(stage) * RB, src + int64_t(p) * a.De, row, &full[stage], pol_stream);
+            if (++stage == NS) { stage = 0; phase ^= 1u; }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers (threads 0 .. kRingWarps * 32 - 1) ----------------
+  const int tid = threadIdx.x;
+  int64_t gbase = 0;               // tasks of all earlier items of this CTA
+  int stage = warp % NS;           // stage and phase of this warp's next task g = warp + kRingWarps k
+  uint32_t phase = uint32_t((warp / NS) & 1);
+  int64_t gnext = warp;
+  int qb = 0, sb = 0;
+  uint32_t qphase = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    int jb, lb, i0, np;
+    match_tma_geom(hdr, jobs, item, jb, lb, i0, np);
+    const MatchJob& a = jobs[jb];
+    const int De = a.De;
+    const int n_cand = a.n_cand;
+    const int ntask = n_cand * np;
+    double* sd = sdb + size_t(sb) * P * CM;
+    mbar_wait(&qfull[qb], qphase);
+    const bf16* qsm = reinterpret_cast<const bf16*>(qbuf + size_t(qb) * QB);
+    for (; gnext < gbase + ntask; gnext += kRingWarps) {
+      const int t = int(gnext - gbase);
+      const int j = t / np, p = t - j * np;
+      mbar_wait(&full[stage], phase);
+      const bf16* arow = reinterpret_cast<const bf16*>(ring + size_t(stage) * RB);
+      const bf16* qrow = qsm + size_t(p) * De;
+      double sacc = 0.0;
+      for (int e = lane * 8; e < De; e += 256) sacc += double(sq_diff8(lds128(qrow + e), lds128(arow + e)));
+      sacc = warp_sum_d(sacc);
+      __syncwarp();
+      if (lane == 0) {
+        sd[p * n_cand + j] = sqrt(sacc);
+        mbar_arrive(&empty[stage]);    // the whole warp's reads of the stage are done (__syncwarp)
+      }
+      stage += kRingWarps;
+      while (stage >= NS) { stage -= NS; phase ^= 1u; }
+    }
+    gbase += ntask;
+    named_bar_sync(1, kRingWarps * 32);                 // the item's distances are in sd
+    if (tid == 0) mbar_arrive(&qempty[qb]);              // the producer may refill this query buffer
+    if (++qb == 2) { qb = 0; qphase ^= 1u; }
+    if (warp < kMatchWarps)                              // the tail is written for 8 warps
+      match_tail(a, jb, lb, i0, np, sd, nullptr, nullptr, nullptr, ints + a.cand_off, ints + a.s2c_off, ties, warp,
+                 lane, tid);
+    sb ^= 1;  // the next item writes the other sd buffer; the barrier of the item after it
+              // orders every warp's tail of this item before this buffer is written again
+  }
+  if (hdr->any_peer) __threadfence_system();
+}
+
+size_t match_ring_smem(int stages, int row_bytes, int qbytes, int cmax, int P) {
+  return size_t(stages) * row_bytes + 2 * size_t(qbytes) + 2 * size_t(P) * cmax * sizeof(double) +
+         (2 * size_t(stages) + 4) * sizeof(uint64_t);
+}
+
 size_t match_tma_smem(int stages, int qbytes, int cmax) {
   return size_t(stages) * kMatchStageBytes + 2 * size_t(qbytes) + size_t(cmax) * kMatchWarps * 2 * sizeof(double) +
          2 * size_t(cmax) * sizeof(double) + (2 * size_t(stages) + 4) * sizeof(uint64_t);
@@ -629,6 +766,22 @@ __global__ void __launch_bounds__(1024) match_finalize_kernel(uint8_t* tab) {
 
 cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t smem, cudaStream_t s) {
   // (a rank that owns no position block still launches one block: it publishes its fingerprint)
+  if (hdr.tma == 2) {
+    const size_t sm = match_ring_smem(hdr.tma_stages, hdr.ring_row_bytes, hdr.tma_qbytes, hdr.tma_cmax, hdr.P);
+    static bool attr2[64] = {false};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    if (!attr2[dev & 63]) {
+      cudaError_t e = cudaFuncSetAttribute(match_dist_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(227 * 1024));
+      if (e != cudaSuccess) return e;
+      attr2[dev & 63] = true;
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(hdr.total_blocks, sms));
+    match_dist_ring_kernel<<<grid, kRingWarps * 32 + 32, sm, s>>>(reinterpret_cast<const uint8_t*>(table_dev));
+    return cudaGetLastError();
+  }
   if (hdr.tma) {
     const size_t sm = match_tma_smem(hdr.tma_stages, hdr.tma_qbytes, hdr.tma_cmax);
     static bool attr[64] = {false};

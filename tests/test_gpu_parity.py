@@ -549,12 +549,13 @@ def test_fp8_measure_interleaved_close_to_oracle():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["1", "2"])
 @pytest.mark.parametrize("De,L_phi", [(64, 33), (8192, 9)])
-def test_match_tma_variant_matches_oracle(De, L_phi):
-    """The opt-in TMA-ring distance kernel (KVCOMM_MATCH_TMA=1, a measured-slower
-    measurement variant) must still match the oracle: a small D_e (many
-    anchor tiles per stage) and D_e = 8192 (each anchor tile split in two 16 KiB chunks),
-    an odd L_φ (a one-position last block)."""
+def test_match_tma_variant_matches_oracle(De, L_phi, variant):
+    """The TMA-fed distance kernels (KVCOMM_MATCH_TMA=1: 16 KiB tiles shared by all warps,
+    a measured-slower measurement variant; =2: one ring stage per anchor row)
+    must match the oracle: a small D_e (many anchor tiles per stage) and D_e = 8192 (each
+    anchor tile split in two 16 KiB chunks), an odd L_φ (a one-position last block)."""
     import subprocess
     import sys
     import os
@@ -563,6 +564,34 @@ def test_match_tma_variant_matches_oracle(De, L_phi):
             "p = synth.make_problem(11, L=1, H=1, d=16, D_e=%d, L_phi=%d, anchor_lens=[%d, %d, %d], prefix_lens=[2], "
             "target_start=3, pf_base_start=3); g = harness.run_gpu(p, gamma=0.9); o = harness.run_oracle(p, gamma=0.9); "
             "harness.compare(g, o, p); print('ok')" % (root, De, L_phi, L_phi, L_phi + 4, L_phi + 1))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, KVCOMM_MATCH_TMA="1"),
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, KVCOMM_MATCH_TMA=variant),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("top_k", [0, 3])
+def test_match_ring_kernel_bitwise_equals_register_kernel(top_k, tmp_path):
+    """The row-ring distance kernel reduces every anchor row in the register kernel's order
+    (same lanes, groups of 8, fp64 accumulation, butterfly), so W, w̄, the distances and the
+    entropy are bit-identical: D_e 4096 (config 2's width), 20 anchors of mixed lengths
+    (truncation), an odd L_φ, dense and top-k weights."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, torch; sys.path.insert(0, %r); import synth; from tests import harness; "
+            "p = synth.make_problem(21, L=1, H=1, d=16, D_e=4096, L_phi=37, anchor_lens=[37 + (j %% 5) for j in range(20)], "
+            "prefix_lens=[2], target_start=3, pf_base_start=3); g = harness.run_gpu(p, gamma=0.9, top_k=%d); m = g['match']; "
+            "torch.save({'W': m.W.cpu(), 'wbar': m.wbar.cpu(), 'dist': m.dist.cpu(), 'H': m.entropy}, sys.argv[1]); print('ok')"
+            % (root, top_k))
+    outs = {}
+    for v in ("0", "2"):
+        f = str(tmp_path / f"m{v}.pt")
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=dict(os.environ, KVCOMM_MATCH_TMA=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+        outs[v] = torch.load(f)
+    a, b = outs["0"], outs["2"]
+    assert torch.equal(a["W"], b["W"]) and torch.equal(a["wbar"], b["wbar"]) and torch.equal(a["dist"], b["dist"])
+    assert a["H"] == b["H"]
