@@ -12,8 +12,10 @@ T4='python -m pytest -q -x -m gpu tests/test_gpu_checkpoint.py tests/test_gpu_pl
 # round 2: the bench's grouped/gated plan launch at small sizes, and the opt-in TMA match kernel
 T5='python -m pytest -q -x -m gpu tests/test_gpu_request_parity.py -p no:cacheprovider'
 T6='env KVCOMM_MATCH_TMA=1 python -c "import __graft_entry__ as g; g.smoke()"'
+# round 2 (later): the row-ring match kernel; the plan tests include pipelined runs (realign stream)
+T7='env KVCOMM_MATCH_TMA=2 python -c "import __graft_entry__ as g; g.smoke()"'
 for tool in memcheck racecheck synccheck initcheck; do
-  for t in "$T1" "$T2" "$T3" "$T4" "$T5" "$T6"; do
+  for t in "$T1" "$T2" "$T3" "$T4" "$T5" "$T6" "$T7"; do
     out=$(eval compute-sanitizer --tool $tool --error-exitcode 9 $t 2>&1)
     rc=$?
     echo "== $tool rc=$rc :: ${t:0:60} :: $(echo "$out" | grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|passed|failed' | tr '\n' ' ')"
