@@ -559,13 +559,6 @@ def main():
             args.match = "replicated (ipc unavailable)"
     qlist = [st.queries[n] for n in req.names]
     agents_all = [a.agent for a in st.agents]
-    # Request pipelining (N = 1): each run's realign kernel goes to its own stream, so the
-    # next request's table upload, matching, reduction and prep (on `stream`) overlap this
-    # request's realign (kvcomm_plan_set_realign_stream).  At N > 1 the
-    # sharded-matching barrier and the fused gather's ordering assume one stream per run.
-    rstream = torch.cuda.Stream() if world == 1 and not args.no_pipeline else None
-    if rstream is not None:
-        plan.set_realign_stream(rstream)
 
     def deliver_for(peer_b, agents_b, full_b):
         def deliver():
@@ -632,6 +625,21 @@ def main():
     # needed only after the last step of a sequence.
     merged_barrier = peer is not None and getattr(req, "_mshard", None) is not None
 
+    # Request pipelining: each run's realign kernel goes to its own stream, so the next
+    # request's table upload, matching, reduction and prep (on `stream`) overlap this
+    # request's realign (kvcomm_plan_set_realign_stream).  N > 1: only with the
+    # fused gather and sharded matching (the merged barrier) — every reader of the matching
+    # exchange buffers runs on the run stream before the next run's barrier, nothing reads
+    # the consumers' caches inside the loop, and the final delivery waits for the realign
+    # stream; the NCCL gather reads the shard outputs every step, so it keeps one stream.
+    rstream = (torch.cuda.Stream() if not args.no_pipeline and (world == 1 or merged_barrier) else None)
+    if rstream is not None:
+        plan.set_realign_stream(rstream)
+
+    def join():  # the realigns on their own stream are part of the timed work
+        if rstream is not None:
+            stream.wait_stream(rstream)
+
     def step(events=None, last=True, mevents=None):
         if events is not None:
             plan.set_events(*events)     # recorded right before / after the realign launch
@@ -639,11 +647,8 @@ def main():
             plan.set_match_events(*mevents)  # ... and the distance kernel
         req.launch(qlist, stream=stream)   # no host synchronisation inside a step
         if last or not merged_barrier:
+            join()
             deliver()
-
-    def join():  # the last realign (on its own stream) is part of the timed work
-        if rstream is not None:
-            stream.wait_stream(rstream)
 
     for _ in range(args.warmup):
         step()

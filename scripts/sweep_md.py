@@ -15,7 +15,7 @@ print("| anchors m | tokens T | ms | tokens/s | GB/s | PAPER Table A.5 H100 'sof
 print("|---:|---:|---:|---:|---:|---:|---:|")
 for r in rows:
     if r.get("status") == "OOM":
-        print(f"| {r['anchors']} | {r['tokens']} | OOM ({r['need_GiB']:.0f} GiB of offsets) | | | | |")
+        print(f"| {r['anchors']} | {r['tokens']} | OOM ({r.get('need_GiB', r.get('need_GiB_per_gpu', 0)):.0f} GiB of offsets{' per GPU' if 'need_GiB_per_gpu' in r else ''}) | | | | |")
         continue
     p = r.get("paper_h100_softmax_ms")
     sp = r.get("speedup_vs_paper")

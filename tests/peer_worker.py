@@ -29,6 +29,9 @@ def main():
     top_k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     sim = sys.argv[4] if len(sys.argv) > 4 else "l2"
     scal = sys.argv[5] if len(sys.argv) > 5 else "frobenius"
+    # "pipe": the bench's N > 1 schedule — every realign on a second stream
+    # (kvcomm_plan_set_realign_stream), runs issued back to back, one delivery sync at the end
+    pipe = len(sys.argv) > 6 and sys.argv[6] == "pipe"
     pk = dict(offset_format=fmt, similarity=sim, scalar_distance=scal)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
@@ -101,13 +104,22 @@ def main():
         return
     if shard_match:  # each rank computes half the match positions, stored into both ranks' buffers
         req.shard_matching(rank, world, 0)
+    rs = torch.cuda.Stream() if pipe else None
+    if pipe:
+        req.plan.set_realign_stream(rs)
     for _ in range(3):  # the later runs overwrite the same rows (and alternate the match buffers)
         if shard_match:
-            req._mshard.run([st.queries[n] for n in req.names], sync=True)
+            req._mshard.run([st.queries[n] for n in req.names], sync=not pipe)
         else:
-            req.plan.run([st.queries[n] for n in req.names], sync=True)
+            req.plan.run([st.queries[n] for n in req.names], sync=not pipe)
+        if not pipe:
+            peer.sync()
+    if pipe:
+        torch.cuda.current_stream().wait_stream(rs)
         peer.sync()
     ms, reused = req.plan.results()
+    if pipe:
+        req.plan.set_realign_stream(None)
     assert all(reused), reused
     for a, b in zip(ms, ref_ms):   # weights and verdicts bit-identical to the unsharded run
         assert a.candidates == b.candidates and a.verdict == b.verdict

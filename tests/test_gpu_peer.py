@@ -20,22 +20,24 @@ def _free_port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fmt,match,top_k,world,sim,scal", [
-    ("bf16", "replicated", 0, 2, "l2", "frobenius"), ("fp8", "replicated", 0, 2, "l2", "frobenius"),
-    ("bf16", "shard-match", 0, 2, "l2", "frobenius"), ("fp8", "shard-match", 0, 2, "l2", "frobenius"),
-    ("bf16", "shard-match", 2, 2, "l2", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "frobenius"),
-    ("bf16", "shard-match", 0, 2, "cosine", "frobenius"), ("bf16", "shard-match", 0, 3, "l2", "mean_l2"),
-    ("bf16", "shard-match-emb", 0, 2, "l2", "frobenius"), ("fp8", "shard-match-emb", 2, 3, "cosine", "frobenius"),
-    ("bf16", "shard-match-emb", 1, 4, "l2", "mean_l2")])
-def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal):
+@pytest.mark.parametrize("fmt,match,top_k,world,sim,scal,pipe", [
+    ("bf16", "replicated", 0, 2, "l2", "frobenius", "no"), ("fp8", "replicated", 0, 2, "l2", "frobenius", "no"),
+    ("bf16", "shard-match", 0, 2, "l2", "frobenius", "no"), ("fp8", "shard-match", 0, 2, "l2", "frobenius", "no"),
+    ("bf16", "shard-match", 2, 2, "l2", "frobenius", "no"), ("bf16", "shard-match", 0, 3, "l2", "frobenius", "no"),
+    ("bf16", "shard-match", 0, 2, "cosine", "frobenius", "no"), ("bf16", "shard-match", 0, 3, "l2", "mean_l2", "no"),
+    ("bf16", "shard-match-emb", 0, 2, "l2", "frobenius", "no"), ("fp8", "shard-match-emb", 2, 3, "cosine", "frobenius", "no"),
+    ("bf16", "shard-match-emb", 1, 4, "l2", "mean_l2", "no"),
+    ("bf16", "shard-match", 0, 2, "l2", "frobenius", "pipe"), ("fp8", "shard-match-emb", 2, 3, "l2", "frobenius", "pipe")])
+def test_fused_gather_multi_rank_bit_exact(fmt, match, top_k, world, sim, scal, pipe):
     """Also: sharded matching (kvcomm_plan_match_shard) gives weights, verdicts and
     caches bit-identical to the unsharded run (dense and top-k weights; 3 ranks split
     the 48 and 20 position blocks of the two sample lengths unevenly; the cosine
     variant's three partial sums and the mean-l2 scalar distance; pools that hold only
-    their rank's embedding rows, shard-match-emb)."""
+    their rank's embedding rows, shard-match-emb; "pipe": the bench's N > 1 schedule, every
+    realign on a second stream and the runs issued back to back)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "peer_worker.py"),
-           fmt, match, str(top_k), sim, scal]
+           fmt, match, str(top_k), sim, scal, pipe]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     hosted = [sum(1 for m in range(1, 6) if (m - 1) % world == rank) for rank in range(world)]
