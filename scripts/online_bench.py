@@ -34,10 +34,14 @@ def main():
     ap.add_argument("--p-swap", type=float, default=0.15)
     ap.add_argument("--clusters", type=int, default=4)
     ap.add_argument("--gamma", type=float, default=0.3)
-    ap.add_argument("--warm", type=int, default=20,
+    ap.add_argument("--capacity", type=int, default=CAP, help="pool capacity V (Table 6 P:507-515 sweeps 5-25)")
+    ap.add_argument("--warm", type=int, default=None,
                     help="samples of the stream's clusters inserted (measured offsets) before the stream "
-                         "(an empty pool accepts every sample once it holds one anchor: |A| = 1 -> H = 0, A19)")
+                         "(an empty pool accepts every sample once it holds one anchor: |A| = 1 -> H = 0, A19); "
+                         "default: the capacity")
     args = ap.parse_args()
+    if args.warm is None:
+        args.warm = args.capacity
     import paper_2510_12872_b200 as kv
     from paper_2510_12872_b200.online import ConsumerSlot, OnlinePool
     dev = "cuda"
@@ -45,7 +49,7 @@ def main():
     vocab = (torch.randn(V, DE, generator=g, device=dev) / math.sqrt(DE)).to(torch.bfloat16)
     r = lambda n: torch.randn(L, H, n, D, generator=g, device=dev).to(torch.bfloat16)
     inv = synth.llama3_inv_freq(D)
-    pool = kv.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=CAP, max_anchor_len=T,
+    pool = kv.AnchorPool(num_layers=L, num_kv_heads=H, head_dim=D, emb_dim=DE, capacity=args.capacity, max_anchor_len=T,
                          prefix_len=[P] * C, inv_freq=inv)
     p0 = [480 - 32 * c for c in range(C)]
     cons = [ConsumerSlot(p0[c], r(P), r(P), 480, torch.empty(L, H, p0[c] + T + P, D, dtype=torch.bfloat16, device=dev),
@@ -83,7 +87,8 @@ def main():
         "realigned_tokens_per_reuse_step": C * (T + P),
         "entropy_reason_ncand_first10": entropies[:10],
         "reuse_tokens_per_s": C * (T + P) / (reuse_ms / 1e3) if reuse_ms else None,
-        "shape": f"8B shape, {T}-token samples, {C} consumers x {P}-token prefixes, capacity {CAP}, gamma {args.gamma}, "
+        "gamma": args.gamma, "capacity": args.capacity,
+        "shape": f"8B shape, {T}-token samples, {C} consumers x {P}-token prefixes, capacity {args.capacity}, gamma {args.gamma}, "
                  f"{args.clusters} clusters, p_swap {args.p_swap}, {args.warm} warm anchors"}))
     pool.destroy()
 
