@@ -43,6 +43,9 @@ constexpr int kMatchUnroll = KVC_MATCH_UNROLL;
 // whose warps hold more loads in flight (config 4: 2.02 ms vs 2.23-3.45 ms at 2-6 CTAs of
 // the 40-register build).
 constexpr int kMatchWideDe = 4096;
+#ifndef KVC_MATCH_PROBE_NOTAIL
+#define KVC_MATCH_PROBE_NOTAIL 0
+#endif
 #ifndef KVC_MATCH_MINB
 #define KVC_MATCH_MINB 6
 #endif  // 16-byte anchor loads in flight per lane (8 vs 4: match 2-5 % faster)
@@ -199,6 +202,9 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
     }
   }
   __syncthreads();
+#if KVC_MATCH_PROBE_NOTAIL  // bandwidth probe only (wrong results): the loads and distances without the tail
+  if (np < 0)
+#endif
   match_tail(a, jb, lb, i0, np, sd, s_qa, s_aa, s_qq, cand, slot2cand, ties, warp, lane, threadIdx.x);
 }
 
