@@ -646,8 +646,8 @@ def main():
         if mevents is not None:
             plan.set_match_events(*mevents)  # ... and the distance kernel
         req.launch(qlist, stream=stream)   # no host synchronisation inside a step
-        if last or not merged_barrier:
-            join()
+        if world > 1 and (last or not merged_barrier):
+            join()       # the delivery sync orders the consumers after this rank's realign
             deliver()
 
     for _ in range(args.warmup):
