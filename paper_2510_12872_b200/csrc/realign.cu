@@ -44,24 +44,25 @@ namespace kvc {
 
 // Ring depth per instantiation (stages of kStageStride): fewer bytes in flight means less
 // DRAM contention, as long as the ring still covers the latency.  Measured at config 2
-// (profiles/r02g_ring_depth.jsonl): the bf16 stream (8 consumer warps) is fastest with 7
-// stages (9: 2 % slower, 11: 5 %), the fp8 decode (16 warps, slower consumers) with 9-10.
+// (profiles/r02g_ring_depth.jsonl, r02h_fp8_warps.txt): the bf16 stream is fastest with 7
+// stages (9: 2 % slower, 11: 5 %), the fp8 decode (slower consumers) with 10 (7: 1.5 %, 8:
+// 0.8 % slower; 11 would leave no room for a match CTA beside it when pipelined).
 #ifndef KVC_NSTAGE_BF16
 #define KVC_NSTAGE_BF16 7
 #endif
 #ifndef KVC_NSTAGE_FP8
-#define KVC_NSTAGE_FP8 9
+#define KVC_NSTAGE_FP8 10
 #endif
-template <int kConsumerWarps>
-constexpr int ring_stages() { return kConsumerWarps == 16 ? KVC_NSTAGE_FP8 : KVC_NSTAGE_BF16; }
+template <bool kFp8>
+constexpr int ring_stages() { return kFp8 ? KVC_NSTAGE_FP8 : KVC_NSTAGE_BF16; }
 constexpr int kItems = kStageBytes / 32;  // 512 items of 32 B per 16 KiB bf16 tile
 constexpr int kConsumerBar = 1;           // named barrier id (consumers only)
 
 constexpr size_t realign_smem_bytes(int stages) {
   return size_t(stages) * kStageStride + 2 * size_t(kUnitWBytes) + (2 * size_t(stages) + 4) * sizeof(uint64_t);
 }
-static_assert(realign_smem_bytes(ring_stages<8>()) <= 227 * 1024, "realign shared memory");
-static_assert(realign_smem_bytes(ring_stages<16>()) <= 227 * 1024, "realign shared memory");
+static_assert(realign_smem_bytes(ring_stages<false>()) <= 227 * 1024, "realign shared memory");
+static_assert(realign_smem_bytes(ring_stages<true>()) <= 227 * 1024, "realign shared memory");
 
 struct Unit {
   int s, l, h, p, t;
@@ -242,13 +243,13 @@ __device__ __forceinline__ void stage_release(uint64_t* b) {
 #endif
 }
 
-template <int kConsumerWarps, int kD>
+template <int kConsumerWarps, int kD, bool kFp8>
 __device__ __forceinline__ void realign_body(const uint8_t* __restrict__ tab, int variant) {
   constexpr int kItemsPerThread = kItems / (kConsumerWarps * 32);
   // tables that read an fp8 pool always launch the 16-warp instantiation (launch_realign), so
   // the 8-warp one carries no e4m3 decode (keeps its registers for the bf16 stream)
-  constexpr bool kFp8Path = kConsumerWarps == 16;
-  constexpr int kNStage = ring_stages<kConsumerWarps>();
+  constexpr bool kFp8Path = kFp8;
+  constexpr int kNStage = ring_stages<kFp8>();
   static_assert(kItemsPerThread * kConsumerWarps * 32 == kItems, "item split");
   const TableHdr hdr = *reinterpret_cast<const TableHdr*>(tab);
   const SegDev* segs = reinterpret_cast<const SegDev*>(tab + hdr.seg_off);
@@ -579,13 +580,27 @@ __device__ __forceinline__ void realign_body(const uint8_t* __restrict__ tab, in
   if (hdr.any_stg) __threadfence_system();  // peer-GPU rows: visible system-wide before the kernel ends
 }
 
-// The four instantiations (one CTA per SM: 8 + 1 warps for bf16 tables, 16 + 1 for
-// tables that read an fp8 pool; 17 warps leave 96 registers per thread, as ptxas allocates
-// for 20 warps).
+// The instantiations (one CTA per SM): 8 + 1 warps for bf16 tables; 16 + 1 for tables that
+// read an fp8 pool at a generic head_dim (17 warps leave 96 registers per thread, as ptxas
+// allocates for 20 warps); realign_kernel_fp8w8 below for fp8 at head_dim 128.
 template <int kConsumerWarps, int kD>
 __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, 1)
     realign_kernel(const uint8_t* __restrict__ tab, int variant) {
-  realign_body<kConsumerWarps, kD>(tab, variant);
+  realign_body<kConsumerWarps, kD, kConsumerWarps == 16>(tab, variant);
+}
+
+// fp8 tables (head_dim 128, the default): 8 consumer warps with two items per thread under
+// a 144-register cap.  ptxas rounds a CTA to 12 warps, so 12 x 32 x 144 = 55,296 registers
+// leave 10,240 for one CTA of the next request's match kernel beside the realign when
+// requests are pipelined.  Measured at config 2 (profiles/r02h_fp8_warps.txt): step 2.90 ->
+// 2.82 ms against the 16-warp kernel; at 152 registers (no cap needed, 149 used) the
+// realign alone is 1 % faster but the match no longer fits beside it, at 128 it spills.
+// KVCOMM_REALIGN_FP8_WARPS=16 selects the 16-warp kernel.
+#ifndef KVC_FP8W8_REGS
+#define KVC_FP8W8_REGS 144
+#endif
+__global__ void __maxnreg__(KVC_FP8W8_REGS) realign_kernel_fp8w8(const uint8_t* __restrict__ tab, int variant) {
+  realign_body<8, 128, true>(tab, variant);
 }
 
 int realign_grid_size(int device) {
@@ -610,11 +625,11 @@ cudaError_t launch_realign_prep(const void* table_dev, const TableHdr& hdr, cuda
 
 cudaError_t launch_realign_main(const void* table_dev, const TableHdr& hdr, int grid, cudaStream_t s) {
   static bool attr_set[64] = {false};
-  static int variant = -1, cw_env = 0;
+  static int variant = -1, cw_env = 0, fp8w_env = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    const int smem8 = int(realign_smem_bytes(ring_stages<8>())), smem16 = int(realign_smem_bytes(ring_stages<16>()));
+    const int smem8 = int(realign_smem_bytes(ring_stages<false>())), smem16 = int(realign_smem_bytes(ring_stages<true>()));
     cudaError_t e = cudaFuncSetAttribute(realign_kernel<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(realign_kernel<16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
@@ -622,12 +637,15 @@ cudaError_t launch_realign_main(const void* table_dev, const TableHdr& hdr, int 
       e = cudaFuncSetAttribute(realign_kernel<8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem8);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(realign_kernel<16, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(realign_kernel_fp8w8, cudaFuncAttributeMaxDynamicSharedMemorySize, smem16);
     // all of the SM's 228 KiB as shared memory: the realign CTA takes ~153 KiB (bf16 ring), and
     // the rest must stay free for the CTAs of the next request's match / prep kernels that run
     // beside it when requests are pipelined (kvcomm_plan_set_realign_stream); at the default
     // carveout the SM is configured just large enough for the realign CTA alone
     for (const void* k : {(const void*)realign_kernel<8, 0>, (const void*)realign_kernel<16, 0>,
-                          (const void*)realign_kernel<8, 128>, (const void*)realign_kernel<16, 128>})
+                          (const void*)realign_kernel<8, 128>, (const void*)realign_kernel<16, 128>,
+                          (const void*)realign_kernel_fp8w8})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
@@ -640,16 +658,20 @@ cudaError_t launch_realign_main(const void* table_dev, const TableHdr& hdr, int 
                       "builds; ignored\n");
     const char* c = getenv("KVCOMM_REALIGN_CONSUMER_WARPS");
     if (c) cw_env = atoi(c);
+    const char* f = getenv("KVCOMM_REALIGN_FP8_WARPS");
+    if (f) fp8w_env = atoi(f);
   }
-  // 8 consumer warps stream bf16 pools at the HBM roofline; the e4m3 decode of fp8
-  // pools issues ~2x the instructions per byte and runs ~4 % faster with 16 (profiles/)
-  const int cw = hdr.any_fp8 ? 16 : (cw_env == 16 ? 16 : 8);  // fp8 decode: 16-warp instantiation only
+  // 8 consumer warps stream bf16 pools at the HBM roofline; fp8 pools at head_dim 128 take
+  // realign_kernel_fp8w8 (8 warps, two items per thread), other head_dims the 16-warp kernel
+  const int cw = hdr.any_fp8 ? 16 : (cw_env == 16 ? 16 : 8);
   if (hdr.n_seg <= 0 || hdr.total_units <= 0) return cudaSuccess;
   const int64_t g = hdr.total_units < grid ? hdr.total_units : grid;
   const uint8_t* t = reinterpret_cast<const uint8_t*>(table_dev);
-  const size_t smem = realign_smem_bytes(cw == 8 ? ring_stages<8>() : ring_stages<16>());
+  const size_t smem = realign_smem_bytes(hdr.any_fp8 ? ring_stages<true>() : ring_stages<false>());
   const bool d128 = hdr.d == 128 && !(variant & 256);  // bit8: generic-d kernel (probe)
-  if (cw == 8 && d128)
+  if (hdr.any_fp8 && d128 && fp8w_env != 16)
+    realign_kernel_fp8w8<<<int(g), 9 * 32, smem, s>>>(t, variant);
+  else if (cw == 8 && d128)
     realign_kernel<8, 128><<<int(g), 9 * 32, smem, s>>>(t, variant);
   else if (cw == 8)
     realign_kernel<8, 0><<<int(g), 9 * 32, smem, s>>>(t, variant);
