@@ -43,6 +43,9 @@ constexpr int kMatchUnroll = KVC_MATCH_UNROLL;
 // whose warps hold more loads in flight (config 4: 2.02 ms vs 2.23-3.45 ms at 2-6 CTAs of
 // the 40-register build).
 constexpr int kMatchWideDe = 4096;
+#ifndef KVC_MATCH_L2PF
+#define KVC_MATCH_L2PF 0  // TMA L2 prefetch of each warp's next anchor row (measurement knob)
+#endif
 #ifndef KVC_MATCH_PROBE_NOTAIL
 #define KVC_MATCH_PROBE_NOTAIL 0
 #endif
@@ -164,12 +167,22 @@ __device__ __forceinline__ void match_item(const uint8_t* __restrict__ tab, cons
 
   // distances: one warp per (position, candidate) task
   const int ntask = np * n_cand;
+  // anchor row of task t: row i0 + p of candidate j; a pool holding only this rank's blocks
+  // stores block lb at lb / G
+  auto task_row = [&](int t) {
+    const int p = t / n_cand;
+    const int j = t - p * n_cand;
+    const int64_t erow = a.emb_world > 1 ? int64_t(lb / a.emb_world) * P + p : int64_t(i0 + p);
+    return a.emb + int64_t(cand[j]) * a.slot_stride + erow * De;
+  };
+  if (KVC_MATCH_L2PF && lane == 0 && warp < ntask) bulk_prefetch_l2(task_row(warp), uint32_t(De) * 2u);
   for (int task = warp; task < ntask; task += kMatchWarps) {
     const int p = task / n_cand;
     const int j = task - p * n_cand;
-    // anchor row i0 + p; a pool holding only this rank's blocks stores block lb at lb / G
-    const int64_t erow = a.emb_world > 1 ? int64_t(lb / a.emb_world) * P + p : int64_t(i0 + p);
-    const bf16* arow = a.emb + int64_t(cand[j]) * a.slot_stride + erow * De;
+    const bf16* arow = task_row(task);
+    // this warp's next row streams into L2 by TMA while the warp reduces this one
+    if (KVC_MATCH_L2PF && lane == 0 && task + kMatchWarps < ntask)
+      bulk_prefetch_l2(task_row(task + kMatchWarps), uint32_t(De) * 2u);
     const bf16* qrow = q + size_t(p) * De;
     if (!a.cosine) {
       double s = 0.0;

@@ -109,6 +109,11 @@ __device__ __forceinline__ void e4m3x4_to_float(uint32_t u, float* f) {
   f[0] = fa.x; f[1] = fa.y; f[2] = fb.x; f[3] = fb.y;
 }
 
+// TMA prefetch of [src, src + bytes) into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // (d0, d1) += (a0, a1) * (b0, b1) as one packed FFMA2 (sm_100), each lane an IEEE fma.rn
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
   asm("{\n .reg .b64 ra, rb, rc;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%0, %1};\n"
