@@ -1,6 +1,7 @@
 """Full-size parity (BASELINE.json configs[1]) in the launch configuration bench.py
 times: the 8B-shape 5-agent request through ReuseRequest (5 matches, ONE batched
-realign launch over all 30 segments, p_(m,0) copies + ledger).
+realign launch over all 30 segments, p_(m,0) copies + ledger), with the bench's
+pipelined schedule (realign stream, runs back to back).
 
 Matching outputs (all weights / verdicts of every pool) and every realigned or
 copied K/V element of every agent are compared with the oracle (tests/state_oracle.py).  Oracle inputs are regenerated from their keyed seeds (synth.state), never read
@@ -28,7 +29,16 @@ def state(request):
     st = build_five_agent_state(seed=0, gamma=0.3, anchor_extra=16, offset_format=request.param)
     st.offset_format = request.param
     st.oracle_matches = {}
-    res = st.request.run(st.queries)
+    # the bench's schedule: requests pipelined (each realign on its own stream, the next
+    # request's matching beside it), three runs back to back without a host sync
+    plan = st.request.plan
+    rs = torch.cuda.Stream()
+    plan.set_realign_stream(rs)
+    for _ in range(3):
+        st.request.launch([st.queries[n] for n in st.request.names])
+    torch.cuda.current_stream().wait_stream(rs)
+    res = st.request.results()
+    plan.set_realign_stream(None)
     torch.cuda.synchronize()
     yield st, res
     for p in st.pools.values():
