@@ -444,15 +444,17 @@ KVCOMM_API kvcomm_status kvcomm_plan_run(kvcomm_plan_t plan, const void* const* 
  * (1 = realigned, 0 = fallback).  Either may be NULL. */
 KVCOMM_API kvcomm_status kvcomm_plan_results(kvcomm_plan_t plan, kvcomm_match_info* infos,
                                              int32_t* agent_reused);
-/* Optional CUDA events (cudaEvent_t, created by the caller) recorded on the run's
- * stream immediately before and after the realign launch of every later run; NULL
- * disables.  Lets a caller time the realign kernel alone inside a pipelined run. */
+/* Optional CUDA events (cudaEvent_t, created by the caller) recorded immediately before
+ * and after the realign kernel (a4-a6; the prep kernel excluded) of every later run, on
+ * the stream that runs it (the run's own, or the realign stream below); NULL disables.
+ * Lets a caller time the realign kernel alone inside a pipelined run. */
 KVCOMM_API kvcomm_status kvcomm_plan_set_events(kvcomm_plan_t plan, void* before_realign, void* after_realign);
 /* Same for the distance kernel of Eq. 5/6 (a2, match_dist_kernel): events recorded right
  * before and after it in every later run (NULL disables), so a caller can time the
  * matching kernel alone (bench.py's roofline.match). */
 KVCOMM_API kvcomm_status kvcomm_plan_set_match_events(kvcomm_plan_t plan, void* before_match, void* after_match);
-/* Request pipelining: with enable != 0, every later run launches its realign kernel on
+/* Request pipelining (Algorithm 1's reuse branch, for consecutive requests;
+ * "pipelining ... orthogonal"): with enable != 0, every later run launches its realign kernel on
  * `stream` (a cudaStream_t; NULL = the legacy default stream) instead of the run's own
  * stream.  The run's own stream keeps the table upload, matching, reduction, results copy
  * and the prep kernel, then records an event the realign stream waits on; the run's
