@@ -184,3 +184,32 @@ def test_split_run_and_shard_argument_contracts():
         plan.match_shard(0, 2, [b"\0" * 64])     # one handle per rank
     plan.match_shard(0, 1)                         # back to unsharded: runs still work
     plan.run(q, sync=True)
+
+def test_every_pool_new_anchor_launches_nothing_into_the_caches():
+    """All five samples far from their pools: every verdict NewAnchor, every segment's
+    gate closed in the prep kernel's unit list (segment -1), so the one realign launch
+    writes nothing — the caches keep their contents, single-stream and pipelined."""
+    st = _small_state(seed=9)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q = {n: (torch.randn(x.shape, generator=g, device="cuda") * 0.125).to(torch.bfloat16)
+         for n, x in st.queries.items()}
+    for pipelined in (False, True):
+        for a in st.agents:
+            a.dst_k.fill_(3.0)
+            a.dst_v.fill_(3.0)
+        rs = torch.cuda.Stream() if pipelined else None
+        if rs is not None:
+            st.request.plan.set_realign_stream(rs)
+        try:
+            for _ in range(2):
+                st.request.launch([q[n] for n in st.request.names])
+            if rs is not None:
+                torch.cuda.current_stream().wait_stream(rs)
+            res = st.request.results()
+        finally:
+            st.request.plan.set_realign_stream(None)
+        torch.cuda.synchronize()
+        assert res.reused_agents == [] and res.fallback_agents == [1, 2, 3, 4, 5]
+        assert all(not m.shareable for m in res.matches.values())
+        for a in st.agents:
+            assert torch.all(a.dst_k == 3.0) and torch.all(a.dst_v == 3.0)
