@@ -17,6 +17,19 @@
 
 namespace kvc {
 
+// x-blocks of a batched insert launch (blockIdx.z = job): about kInsertItems work items per
+// thread, so a (layer, head) block of a 1,024-row placeholder spreads over several CTAs and
+// the last wave is short (one CTA per block left ~2 waves of 256 KiB CTAs behind a mix of
+// tiny prefix-job CTAs).  KVC_INSERT_ITEMS=0: the former jobs-share-the-machine heuristic.
+#ifndef KVC_INSERT_ITEMS
+#define KVC_INSERT_ITEMS 8
+#endif
+static unsigned batch_gx(int64_t per_block, unsigned gx_old, int n_jobs) {
+  if (KVC_INSERT_ITEMS <= 0) return max(1u, gx_old / unsigned(n_jobs) + 1u);
+  const int64_t per_cta = int64_t(256) * KVC_INSERT_ITEMS;
+  return unsigned(per_block <= per_cta ? 1 : (per_block + per_cta - 1) / per_cta);
+}
+
 static dim3 grid2d(int64_t per_block, int threads, int n_lh) {
   int64_t gx = (per_block + threads - 1) / threads;
   const int64_t cap = (148 * 16 + n_lh - 1) / n_lh;  // ~16 CTAs per SM overall
@@ -76,7 +89,7 @@ cudaError_t launch_copy_rows_batch(const CopyJobs& jobs, int n, int Ls, int Hs, 
   for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
   const int n_lh = Ls * Hs;
   dim3 g = grid2d(int64_t(rows) * (d / 8), 256, n_lh);
-  g.x = max(1u, g.x / unsigned(n) + 1u);  // the jobs share the machine
+  g.x = batch_gx(int64_t(rows) * (d / 8), g.x, n);
   g.z = unsigned(n);
   copy_rows_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d);
   return cudaGetLastError();
@@ -175,7 +188,7 @@ cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs,
   for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
   const int n_lh = Ls * Hs;
   dim3 g = grid2d(int64_t(rows) * (d / 16), 256, n_lh);
-  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.x = batch_gx(int64_t(rows) * (d / 16), g.x, n);
   g.z = unsigned(n);
   measure_batch_kernel<<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
   return cudaGetLastError();
@@ -447,7 +460,7 @@ cudaError_t launch_quantize_rows_batch(const CopyJobs& jobs, int n, int Ls, int 
   for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
   const int n_lh = Ls * Hs;
   dim3 g = grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh);
-  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.x = batch_gx(int64_t(rows) * row_group(d / 16), g.x, n);
   g.z = unsigned(n);
   if (d == 128) quantize_rows_batch_kernel<128><<<g, 256, 0, s>>>(jobs, n_lh, d);
   else quantize_rows_batch_kernel<0><<<g, 256, 0, s>>>(jobs, n_lh, d);
@@ -461,7 +474,7 @@ cudaError_t launch_measure_fp8_batch(const MeasureJobs& jobs, int n, int Ls, int
   for (int i = 0; i < n; ++i) rows = max(rows, jobs.j[i].rows);
   const int n_lh = Ls * Hs;
   dim3 g = grid2d(int64_t(rows) * row_group(d / 16), 256, n_lh);
-  g.x = max(1u, g.x / unsigned(n) + 1u);
+  g.x = batch_gx(int64_t(rows) * row_group(d / 16), g.x, n);
   g.z = unsigned(n);
   if (d == 128) measure_fp8_batch_kernel<128><<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
   else measure_fp8_batch_kernel<0><<<g, 256, 0, s>>>(jobs, n_lh, d, interleaved, inv_freq);
