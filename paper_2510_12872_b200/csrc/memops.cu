@@ -210,6 +210,9 @@ cudaError_t launch_measure_batch(const MeasureJobs& jobs, int n, int Ls, int Hs,
 namespace kvc {
 
 constexpr float kE4M3Max = 448.f;
+#ifndef KVC_QUANT_U
+#define KVC_QUANT_U 2
+#endif
 
 // A row's vph items sit in a group of G consecutive lanes (G = vph rounded up to a
 // power of two, <= 16: groups never straddle a warp); lanes past vph hold 0.
@@ -313,7 +316,7 @@ __device__ __forceinline__ Fp8Row fp8_row(uint8_t* base, int64_t lh, int i, int 
 template <int kD>  // head_dim fixed at compile time (128), or 0 = runtime d
 __device__ __forceinline__ void quantize_rows(const bf16* __restrict__ src, int64_t src_ld, uint8_t* __restrict__ dst,
                                               int64_t lh_bytes, int n_lh, int rows, int d_arg) {
-  constexpr int U = 2;  // items per thread per iteration: both loads in flight before any math
+  constexpr int U = KVC_QUANT_U;  // items per thread per iteration: all loads in flight before any math
   const int d = kD ? kD : d_arg;
   const int vph = d / 16;
   const int G = row_group(vph);
