@@ -1873,6 +1873,19 @@ static kvcomm_status plan_begin(kvcomm_plan_s* pl, const void* const* query_embs
     ML.hdr.fp_mine = reinterpret_cast<const uint64_t*>(pl->xb() + pl->fp_off[par]);
     ML.hdr.any_peer = 1;  // system-scope fence after the (peer) fingerprint stores
   }
+  // Pipelined runs: the next run's match runs beside the realign only in the 40-register
+  // build, at one or two CTAs per SM — worth it while the match is small next to the
+  // realign (config 2: 0.53 vs 30.5 GB; a sharded 70B match: 1.6 vs 33 GB); a large one
+  // (config 4's replicated 12.9 GB) would outlast the realign there, so it keeps the
+  // faster build and follows the realign (measured: profiles/r02h_config4.json)
+  if (pl->rstream_set && match_table) {
+    double mb = 0.0, rb = 0.0;
+    for (const MatchItem& it : items)
+      mb += double(it.n_own >= 0 ? int64_t(it.n_own) * kMatchP : it.L_phi) * (it.info->n_candidates + 1) *
+            it.p->De * 2.0;
+    for (const HostSeg& g : hs) rb += double(g.x.L_seg) * (g.x.n_cand + 2) * 2.0 * pl->Ls * pl->Hs * pl->d * 2.0;
+    ML.hdr.beside_realign = mb * 8.0 <= rb ? 1 : 0;
+  }
   RealignLayout RL = layout_realign(pl->d, pl->Ls, pl->Hs, hs);
   const size_t roff = align_up(ML.bytes, 256);
   KV_TRY(entry_reserve(E, roff + RL.bytes));

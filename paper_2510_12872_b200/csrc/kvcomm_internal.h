@@ -160,6 +160,8 @@ struct MatchHdr {
   int32_t tma, tma_stages, tma_qbytes, tma_cmax;
   int32_t max_de;                         // largest D_e of the launch's jobs (selects the kernel)
   int32_t ring_row_bytes;                 // tma = 2 (row-ring kernel): bytes per ring stage (max D_e x 2)
+  int32_t beside_realign;                 // pipelined plan run: the match shares the SMs with a realign
+  int32_t _pad_br;
   uint64_t* fp_dst[kMaxMatchPeers + 1];   // [r]: this rank's slot in rank r's array
   const uint64_t* fp_mine;                // this rank's array [shard_world]
 };

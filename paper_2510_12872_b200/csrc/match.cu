@@ -817,7 +817,10 @@ cudaError_t launch_match_dist(const void* table_dev, const MatchHdr& hdr, size_t
     match_dist_tma_kernel<<<grid, kMatchThreads + 32, sm, s>>>(reinterpret_cast<const uint8_t*>(table_dev));
     return cudaGetLastError();
   }
-  const auto kern = hdr.max_de <= kMatchWideDe ? match_dist_kernel<KVC_MATCH_MINB> : match_dist_kernel<1>;
+  // beside a realign (pipelined plan runs) only the 40-register build fits next to the
+  // realign CTA on an SM, whatever the row length: slower alone at D_e 8192, but hidden
+  const auto kern = (hdr.max_de <= kMatchWideDe || hdr.beside_realign) ? match_dist_kernel<KVC_MATCH_MINB>
+                                                                         : match_dist_kernel<1>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

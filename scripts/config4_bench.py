@@ -81,6 +81,32 @@ def main():
         steps.append(e0.elapsed_time(e1) / 4)
         realign.extend(ks)
     step_ms = sorted(steps)[len(steps) // 2]
+    plan.set_events(None, None)
+
+    # Requests pipelined (the bench's schedule, kvcomm_plan_set_realign_stream): the next
+    # request's matching (replicated here: all 3,072 positions x 256 anchors, 12.9 GB) runs
+    # beside this request's realign; both streams share HBM
+    rs = torch.cuda.Stream()
+    plan.set_realign_stream(rs)
+    for _ in range(3):
+        plan.run([query], stream=stream)
+    stream.wait_stream(rs)
+    torch.cuda.synchronize()
+    piped = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(8):
+            plan.run([query], stream=stream)
+        stream.wait_stream(rs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        piped.append(e0.elapsed_time(e1) / 8)
+    plan.set_realign_stream(None)
+    _, reused = plan.results()
+    if not all(reused):
+        raise SystemExit("pipelined request fell back")
+    step_ms_piped = sorted(piped)[len(piped) // 2]
 
     # Sharded matching: with G ranks each computes T/G positions of the match.
     # One rank's share is timed here as a match-only plan over the first T/G positions of
@@ -128,6 +154,9 @@ def main():
         "workload": "BASELINE configs[3] shard: llama3-70b-shape layers [0,20) x kv heads [0,4), 3072-token "
                     "segment + 32-token prefix + 200-token p0, 256-anchor pool, k=256",
         "realigned_tokens": T + P, "step_ms": step_ms, "realign_ms": rl_ms,
+        "step_ms_pipelined": step_ms_piped,
+        "pipelined_note": "requests back to back, realign on its own stream, the next request's replicated "
+                          "match beside it (40-register match build)",
         "shard_tokens_per_s": (T + P) / (step_ms / 1e3),
         "realign_alg_bytes": alg, "realign_GBps": alg / (rl_ms / 1e3) / 1e9,
         "frac_of_measured_peak": (alg / (rl_ms / 1e3) / 1e9 / peak) if peak else None,
