@@ -11,3 +11,4 @@ python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$
 python bench.py --offsets fp8 > gpurun_out/bench_fp8.json 2> gpurun_out/bench_fp8.err; echo bench8 rc=$?
 python bench.py --steps 300 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/bench_sustained.json 2>&1; echo sustained rc=$?
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/reference.json 2>&1; echo ref rc=$?
+python scripts/config4_bench.py > gpurun_out/config4.json 2>&1; echo c4 rc=$?
